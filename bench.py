@@ -1,0 +1,438 @@
+#!/usr/bin/env python
+"""Benchmark of the Gaussian map-optimisation iteration on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+Default workload (N=1): `S2r-1M-1280x720-32line` -- 1,048,576 Gaussians seeded on the surfaces
+of a ray-cast room (SLAM-like, SURVEY.md 8d S2 recipe with this repo's own room generator),
+1280x720 keyframes with 32-line LiDAR depth supervision, 4 keyframes cycled.  One step = one
+map-optimisation iteration of R/mapper.py:249-256 (forward -> mapping_loss -> backward ->
+sparse Adam) with reference semantics (Adam after every keyframe).
+
+N > 1 (torchrun, one rank per GPU, NCCL): a 32-keyframe batch per step split 32/N per GPU over
+a replicated map; per-view gradients are accumulated, allreduced with NCCL (touched mask fused
+into the same buffer) and one sparse Adam step is applied on every rank.
+
+`--impl reference` times the reference's own CPU algorithm (the float64 C restatement in
+oracle/, all host cores) on the same workload and prints the same JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "map-opt iters/sec (fwd+bwd+Adam) @1M Gaussians 1280x720; render FPS; % HBM roofline"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+CONFIGS = {
+    # name: (scene kind, n, width, height, lidar, keyframes, mode)
+    "S2r-1M-1280x720-32line": ("room", 1 << 20, 1280, 720, 32, 4, "train"),
+    "S2r-500k-1280x720-32line": ("room", 1 << 19, 1280, 720, 32, 4, "train"),
+    "S1-1M-1280x720": ("s1", 1 << 20, 1280, 720, 30000, 1, "train"),
+    "S1-10k-320x240": ("s1", 10000, 320, 240, 5000, 1, "train"),
+    "S2r-2M-1920x1080-render": ("room", 1 << 21, 1920, 1080, 32, 4, "render"),
+}
+DEFAULT = "S2r-1M-1280x720-32line"
+
+
+def peaks() -> tuple[dict, str]:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return dict(PEAKS_FALLBACK), "fallback"
+
+
+def make_scene(name: str, rank: int = 0, world: int = 1, views_override=None):
+    from paper_2507_04004_b200 import scenes
+    kind, n, w, h, lidar, nkf, mode = CONFIGS[name]
+    if kind == "s1":
+        return scenes.scene_s1(n, w, h, k_lidar=lidar)
+    views = views_override if views_override is not None else tuple(range(0, 32, 32 // nkf))[:nkf]
+    return scenes.scene_room(n, w, h, lidar=lidar, render_views=views)
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes
+
+
+def algorithmic_bytes(eng, scene_cam) -> dict:
+    """Compulsory HBM bytes per launch of each phase, from the iteration's own statistics."""
+    import torch
+    ws = eng.ws
+    n = len(eng.g)
+    cnt = ws.counters[:8].cpu().numpy()
+    n_t = int(cnt[2])
+    E = int(cnt[1])
+    P = eng.W * eng.H
+    nc = ws.n_contrib
+    tx, ty = ws.tiles_x, ws.tiles_y
+    pad = torch.zeros((ty * 16, tx * 16), dtype=torch.int32, device=nc.device)
+    pad[:eng.H, :eng.W] = nc
+    tile_max = pad.view(ty, 16, tx, 16).amax(dim=(1, 3))
+    proc = int(tile_max.sum().item())  # entries the blend must read (per tile, up to max n_contrib)
+    near = int((ws.splat2d[:, 6] > 0.01).sum().item())
+    valid = int(ws.valid.sum().item())
+    K = int(eng.views[0].lidar_z.numel()) if eng.views[0].sparse is not None else 0
+    return {
+        "preprocess": 16 * n + 240 * near + 106 * n,
+        "render_fwd": 52 * proc + 28 * P + 8 * tx * ty,
+        "render_bwd": 28 * P + (52 + 40) * proc + 48 * n_t + 8 * tx * ty,
+        "chain_adam": n_t * (256 + 48 + 512 + 768 + 8 + 4),
+        "loss": 36 * P + 8 * P,
+        "bin": 24 * E * 2 + 12 * E + 8 * E + 4 * E + 16 * valid * 4,
+        "_stats": {"n": n, "n_valid": valid, "n_touched": n_t, "entries": E, "blend_entries": proc, "pixels": P},
+    }
+
+
+def run_ours(args) -> dict:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import GaussianMap
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    name = args.config
+    kind, n_g, W, H, lidar, nkf, mode = CONFIGS[name]
+    if world > 1:
+        return run_ours_dp(args, rank, world, local)
+    sc = make_scene(name)
+    g = GaussianMap.from_rows(sc.rows)
+    kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
+    pk, pk_kind = peaks()
+    if mode == "render":
+        return run_render(args, g, kfs, pk, pk_kind, name)
+    lrs = R.default_lrs(3.0)
+    eng = M.MapOptimizer(g, kfs, lrs)
+    eng.capture()
+    nv = len(kfs)
+    for i in range(args.warmup):
+        eng.step(i % nv)
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        start.record()
+        for i in range(args.steps):
+            eng.step(i % nv)
+        end.record()
+        end.synchronize()
+    ms = start.elapsed_time(end) / args.steps
+    value = 1000.0 / ms
+    loss = eng.loss_sum() / (args.steps + args.warmup)
+    # e2e: host keyframes through the public streaming API (H2D inside the timed region)
+    eng.attach_host_keyframes(kfs)
+    for i in range(args.warmup):
+        eng.step_host(i % nv, i)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for i in range(args.steps):
+        eng.step_host(i % nv, i)
+    e2.record()
+    e2.synchronize()
+    e2e_ms = s2.elapsed_time(e2) / args.steps
+    wall_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    # per-phase profile (eager, events between the C-ABI calls) for the roofline
+    prof = {p: [] for p in M.MapOptimizer.PHASES}
+    for i in range(max(10, min(args.steps, 30))):
+        for p, v in eng.profile_step(i % nv).items():
+            prof[p].append(v)
+    phase_ms = {p: float(np.median(v)) for p, v in prof.items()}
+    bytes_ = algorithmic_bytes(eng, kfs[0].cam)
+    dom = max((p for p in phase_ms if p != "bin"), key=lambda p: phase_ms[p]) if phase_ms else None
+    dom_all = max(phase_ms, key=lambda p: phase_ms[p])
+    hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    achieved = bytes_[dom] / (phase_ms[dom] * 1e-3) / 1e9
+    phases = {p: {"ms": round(phase_ms[p], 4), "share": round(phase_ms[p] / sum(phase_ms.values()), 4),
+                  "alg_bytes": int(bytes_[p]), "gbs": round(bytes_[p] / (phase_ms[p] * 1e-3) / 1e9, 1)}
+              for p in phase_ms}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(dom)
+    out = {
+        "metric": METRIC, "value": round(value, 2), "unit": "it/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: S2r room scene (seed 7), Gaussians seeded on ray-cast surfaces from 32 views, "
+                "targets and LiDAR ray-traced; random-free deterministic generator",
+        "config": {"workload": name, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
+                   "keyframes": nv, "semantics": "per-keyframe sparse Adam (R/mapper.py:246-257)",
+                   "l2": "inputs larger than L2 (params + Adam moments = 768 MB per step)",
+                   "cuda_graph": True, "mean_loss": round(loss, 6)},
+        "e2e": {"value": round(1000.0 / e2e_ms, 2), "unit": "it/s", "h2d_bytes_per_step": int(eng.h2d_bytes),
+                "d2h_bytes_per_step": int(eng.d2h_bytes), "wall_ms_per_step": round(wall_ms, 4),
+                "path": "MapOptimizer.step_host: pinned host keyframe -> H2D -> LiDAR K-list -> iteration -> D2H loss"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": traffic,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
+                     "dominant_phase_overall": dom_all},
+        "phases": phases,
+        "stats": bytes_["_stats"],
+        "gpu_launches": int(eng.kernels_per_step() * args.steps),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(sc, args.cpu_budget)
+    return out
+
+
+def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
+    """Forward-only novel-view rendering (BASELINE config 4, render FPS)."""
+    import torch
+
+    from paper_2507_04004_b200 import _lib
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import stream_ptr
+    views = [R.DeviceView(kf.cam) for kf in kfs]
+    ws, _ = R._bin_frame(g, views[0], True)
+    emax = 0
+    for v in views:
+        _, cnt = R._bin_frame(g, v, True)
+        emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
+    ws = R.Workspace(len(g), kfs[0].cam.width, kfs[0].cam.height, int(emax * 1.3) + 4096, g.device)
+    cur = torch.empty_like(views[0].buf)
+
+    def launch():
+        _lib.call("gs_preprocess", ws.fptr, g.data.data_ptr(), cur.data_ptr(), stream_ptr())
+        _lib.call("gs_bin", ws.fptr, 1, stream_ptr())
+        _lib.call("gs_render_fwd", ws.fptr, 1, stream_ptr())
+
+    cur.copy_(views[0].buf)
+    launch()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        launch()
+    for i in range(args.warmup):
+        cur.copy_(views[i % len(views)].buf)
+        graph.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        s.record()
+        for i in range(args.steps):
+            cur.copy_(views[i % len(views)].buf)
+            graph.replay()
+        e.record()
+        e.synchronize()
+    ms = s.elapsed_time(e) / args.steps
+    return {"metric": METRIC, "value": round(1000.0 / ms, 2), "unit": "FPS", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene",
+            "config": {"workload": name, "gaussians": len(g), "mode": "forward-only render"},
+            "clocks": clk.summary()}
+
+
+def run_ours_dp(args, rank, world, local) -> dict:
+    """Keyframe-batch data parallelism: 32 views per step, 32/N per rank."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import parallel as PAR
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    batch = 32
+    mine = tuple(range(rank, batch, world))
+    sc = make_scene(args.config, views_override=mine)
+    g = GaussianMap.from_rows(sc.rows)
+    kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
+    eng = PAR.BatchMapOptimizer(g, kfs, R.default_lrs(3.0))
+    for _ in range(args.warmup):
+        eng.step(list(range(len(kfs))))
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        s.record()
+        for _ in range(args.steps):
+            eng.step(list(range(len(kfs))))
+        e.record()
+        e.synchronize()
+    ms = torch.tensor([s.elapsed_time(e) / args.steps], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    value = batch * 1000.0 / ms
+    out = {"metric": METRIC, "value": round(value, 2), "unit": "it/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene (seed 7)",
+           "config": {"workload": args.config, "gaussians": len(g), "batch_keyframes": batch,
+                      "semantics": "batch-32 gradient sum + touched union + one sparse Adam per batch",
+                      "parallelism": f"dp{world} (NCCL allreduce of parameter-row gradients)"},
+           "gpu_launches": int(eng.kernels_per_step() * args.steps), "clocks": clk.summary()}
+    dist.barrier()
+    return out
+
+
+def cpu_baseline(sc, budget_s: float) -> dict:
+    """The oracle (float64 C restatement of the reference, all host cores) on a bounded sample:
+    as many full iterations of the same workload as fit the budget (>= 1 after a warm-up)."""
+    import oracle as O
+    O.build()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    rows = sc.rows.astype(np.float32).astype(np.float64)
+    st = O.AdamState()
+    lrs = O.default_lrs(3.0)
+    c = sc.cams[0]
+    cam = O.Camera(c["width"], c["height"], c["fx"], c["fy"], c["cx"], c["cy"], c["rot_cw"], c["trans_cw"])
+    O.map_iteration_rows(rows, cam, sc.targets[0], sc.sparse_depths[0], st, lrs)  # warm-up
+    times = []
+    t_all = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        O.map_iteration_rows(rows, cam, sc.targets[0], sc.sparse_depths[0], st, lrs)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_all + times[-1] > budget_s or len(times) >= 10:
+            break
+    med = float(np.median(times))
+    return {"value": round(1.0 / med, 4), "unit": "it/s", "cores": threads, "kind": "port",
+            "sample": f"{len(times)} full iterations (after 1 warm-up) of the same workload, median "
+                      f"{med:.3f} s/iter, oracle/gs_oracle.c float64 with {threads} OpenMP threads"}
+
+
+def run_reference(args) -> dict | None:
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if rank != 0:
+        return None
+    sc = make_scene(args.config)
+    import oracle as O
+    O.build()
+    threads = os.cpu_count() or 1
+    O.set_threads(threads)
+    rows = sc.rows.astype(np.float32).astype(np.float64)
+    st = O.AdamState()
+    lrs = O.default_lrs(3.0)
+    cams = [O.Camera(c["width"], c["height"], c["fx"], c["fy"], c["cx"], c["cy"], c["rot_cw"], c["trans_cw"])
+            for c in sc.cams]
+    nv = len(cams)
+    budget = float(args.ref_budget)
+    t_start = time.perf_counter()
+    warm = 0
+    for i in range(args.warmup):
+        O.map_iteration_rows(rows, cams[i % nv], sc.targets[i % nv], sc.sparse_depths[i % nv], st, lrs)
+        warm += 1
+        if time.perf_counter() - t_start > budget / 3:
+            break
+    times = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        O.map_iteration_rows(rows, cams[i % nv], sc.targets[i % nv], sc.sparse_depths[i % nv], st, lrs)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start > budget:
+            break
+    ms = 1e3 * float(np.mean(times))
+    value = 1000.0 / ms
+    kind, n_g, W, H, lidar, nkf, mode = CONFIGS[args.config]
+    return {"metric": METRIC, "value": round(value, 4), "unit": "it/s", "n_gpus": world, "steps": len(times),
+            "warmup": warm, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "impl": "reference",
+            "data": "synthetic S2r room scene (seed 7), same generator as the GPU arm",
+            "config": {"workload": args.config, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
+                       "keyframes": nkf, "semantics": "per-keyframe sparse Adam (R/mapper.py:246-257)"},
+            "cpu_baseline": {"value": round(value, 4), "unit": "it/s", "cores": threads, "kind": "port",
+                             "sample": f"{len(times)} full iterations (steps capped by a {budget:.0f} s budget) of "
+                                       f"the workload; oracle/gs_oracle.c float64, {threads} OpenMP threads"},
+            "e2e": {"value": round(value, 4), "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=25.0)
+    ap.add_argument("--ref-budget", type=float, default=150.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        out = run_reference(args)
+    else:
+        out = run_ours(args)
+    if out is not None and int(os.environ.get("RANK", 0)) == 0:
+        print(json.dumps(out), flush=True)
+    if int(os.environ.get("WORLD_SIZE", 1)) > 1 and args.impl == "ours":
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

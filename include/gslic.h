@@ -1,0 +1,190 @@
+/*
+ * gslic.h -- C ABI of the B200-native (sm_100a) Gaussian map-optimisation hot path.
+ *
+ * Drop-in boundary for the reference's Python entry points (R/ = splatslam package of
+ * /root/reference/pkg/src).  Each entry point cites the reference function it replaces:
+ *
+ *   gs_preprocess   R/gaussians.py:180-215 project + R/rasterizer.py:445-452 (sigmoid, view
+ *                   dirs, eval_sh R/gaussians.py:102-111) + influence_radius :91-102
+ *   gs_bin          R/rasterizer.py:169-219 cull_tiles (+ touched of _reduce_entries :424)
+ *   gs_render_fwd   R/rasterizer.py:226-293 _forward_kernel
+ *   gs_loss         R/losses.py:157-161 mapping_loss (photometric :122-130 with
+ *                   dssim_and_grad :89-119, depth_ratio_loss :133-154 on a LiDAR K-list)
+ *   gs_render_bwd   R/rasterizer.py:296-435 _backward_kernel + _reduce_entries
+ *   gs_chain_adam   R/rasterizer.py:559-644 _chain_to_attributes fused with
+ *                   R/rasterizer.py:707-725 sparse_adam_step
+ *   gs_chain        _chain_to_attributes only, accumulating parameter-row gradients
+ *                   (multi-view / multi-GPU batches; followed by an allreduce + gs_adam)
+ *   gs_adam         sparse_adam_step on parameter-row gradients + a touched mask
+ *
+ * Conventions
+ *   - Every pointer is a DEVICE pointer unless named host_*; the caller owns all memory.
+ *   - The library never allocates and keeps no global state: transient per-view state lives
+ *     in a caller-provided workspace carved by gs_frame_layout().  Calls are re-entrant;
+ *     each runs on the caller's stream (cudaStream_t passed as void*).
+ *   - Parameter rows: float32, GS_ROW floats per Gaussian, columns in the order of
+ *     GaussianMap.parameters() (R/gaussians.py:150-153) = the Gaussian PLY field order
+ *     (R/gaussians.py:255-256): pos 0-2, log_scale 3-5, quat(wxyz) 6-9, opacity_logit 10,
+ *     sh_low 11-13, sh_high 14-58; 59-63 padding.
+ *   - Return value: GS_OK or an error code; gs_last_error() gives a thread-local message.
+ *     Codes map onto the reference taxonomy (R/errors.py): GS_ERR_ARG/DIMS -> DomainError,
+ *     GS_ERR_WORKSPACE/CAPACITY -> DataError, GS_ERR_CUDA -> NumericalError-class runtime error.
+ */
+#ifndef GSLIC_H
+#define GSLIC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GS_ROW 64       /* floats per parameter row (59 used) */
+#define GS_NPARAM 59
+#define GS_TILE 16
+#define GS_G2D 12       /* floats per screen-space gradient row: mean2d 2, conic 3, opacity 1, color 3, depth 1, pad 2 */
+
+enum {
+    GS_OK = 0,
+    GS_ERR_ARG = 1,
+    GS_ERR_DIMS = 2,
+    GS_ERR_WORKSPACE = 3,
+    GS_ERR_CAPACITY = 4,
+    GS_ERR_CUDA = 5
+};
+
+/* counters[] slots (int32, device) written by the pipeline */
+enum {
+    GS_CNT_ACTIVE = 0,   /* splats with >= 1 candidate tile */
+    GS_CNT_ENTRIES = 1,  /* E = kept (splat, tile) pairs */
+    GS_CNT_TOUCHED = 2,  /* splats with >= 1 kept pair */
+    GS_CNT_OVERFLOW = 3, /* nonzero when E exceeded entry_capacity (downstream kernels no-op) */
+    GS_CNT_ENTRIES_EFF = 4, /* E, or 0 after an overflow (what the downstream kernels use) */
+    GS_CNT_SLOTS = 16
+};
+
+/* Pinhole camera, world->camera (R/rasterizer.py:47-67).  Pixel centres are integers. */
+typedef struct gs_camera {
+    int32_t width, height;
+    float fx, fy, cx, cy;
+    float rot_cw[9]; /* row-major */
+    float trans_cw[3];
+    float center[3]; /* -rot_cw^T trans_cw (filled by gs_camera_init) */
+} gs_camera;
+
+/* One training view: camera + its supervision (resident in device memory). */
+typedef struct gs_view {
+    gs_camera cam;
+    const float *target;      /* (H, W, 3) image */
+    const int32_t *lidar_idx; /* (K,) pixel index y*W+x of LiDAR returns (sparse_depth > 0) */
+    const float *lidar_z;     /* (K,) LiDAR depth */
+    int32_t lidar_k;
+    int32_t pad_;
+} gs_view;
+
+/* Transient per-view state, carved from one workspace by gs_frame_layout(). */
+typedef struct gs_frame {
+    int64_t n;               /* Gaussians */
+    int64_t entry_capacity;  /* max kept (splat, tile) pairs */
+    int32_t width, height, tiles_x, tiles_y;
+    /* per Gaussian */
+    float *splat2d;          /* n x 12: mx my ca cb | cc opacity depth qcut | r g b pad */
+    float *cov2d;            /* n x 4: c00 c01 c11 radius */
+    int32_t *rect;           /* n x 4: tx0 tx1 ty0 ty1 (empty: tx1 < tx0) */
+    uint8_t *valid;          /* n: near-plane & det test (R/gaussians.py:190-208) */
+    uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
+    int32_t *touched_list;   /* n: compacted touched ids (unordered) */
+    float *g2d;              /* n x GS_G2D screen-space gradients (touched rows valid) */
+    uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles */
+    int32_t *counts;         /* n + 1: kept pairs per active Gaussian (depth order) -> offsets */
+    /* sort buffers */
+    uint64_t *keys_a, *keys_b; /* max(n, entry_capacity) */
+    uint32_t *sort_hist;       /* 8 passes x 256 */
+    uint32_t *sort_status;     /* lookback status words */
+    int32_t *scan_status;      /* scan lookback words */
+    int64_t status_words;      /* length of sort_status */
+    int64_t scan_words;
+    /* per entry / tile */
+    int32_t *entry_splat;    /* entry_capacity */
+    int32_t *tile_offsets;   /* tiles + 1 */
+    int32_t *counters;       /* GS_CNT_SLOTS */
+    /* per pixel */
+    float *color;            /* H x W x 3  (un-normalised, background 0) */
+    float *depth;            /* H x W      (sum z w) */
+    float *opacity;          /* H x W      (1 - T) */
+    float *trans;            /* H x W      (T) */
+    int32_t *n_contrib;      /* H x W */
+    float *g_color;          /* H x W x 3  dL/dcolor */
+    float *g_depth;          /* H x W      xi dLd/ddepth */
+    float *g_opac;           /* H x W      xi dLd/dopacity */
+    double *loss_parts;      /* per-block partial sums */
+    double *loss;            /* 4: total, photometric, depth, dssim */
+    int64_t loss_blocks;
+} gs_frame;
+
+/* ---- setup ---------------------------------------------------------------- */
+size_t gs_workspace_size(int64_t n, int32_t width, int32_t height, int64_t entry_capacity);
+int gs_frame_layout(int64_t n, int32_t width, int32_t height, int64_t entry_capacity, void *ws,
+                    size_t ws_bytes, gs_frame *out);
+/* fills cam->center from rot_cw / trans_cw (host struct) */
+void gs_camera_init(gs_camera *host_cam);
+const char *gs_last_error(void);
+int gs_version(void);
+
+/* ---- the iteration ------------------------------------------------------------------ */
+/* R/gaussians.py:180-215 + R/rasterizer.py:445-452: projection, EWA covariance, SH colour,
+ * opacity sigmoid, influence radius, tile rectangle and cut; also resets touched[]. */
+int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream);
+
+/* R/rasterizer.py:169-219: depth sort of active Gaussians, exact per-tile cull, (tile|depth)
+ * ordered entries, tile ranges, touched mask + list; zeroes touched g2d rows.
+ * cull=0 reproduces the reference's cull=False (every valid Gaussian in every tile). */
+int gs_bin(const gs_frame *f, int32_t cull, void *stream);
+
+/* R/rasterizer.py:226-293 */
+int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream);
+
+/* R/losses.py:157-161 with the depth term on the view's LiDAR K-list; writes g_color,
+ * g_depth, g_opac and loss[0..3]. */
+int gs_loss(const gs_frame *f, const gs_view *view, float lam, float xi, void *stream);
+
+/* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
+int gs_render_bwd(const gs_frame *f, void *stream);
+
+/* R/rasterizer.py:559-644 + :707-725 fused.  lr_cols: device (GS_ROW) per-column rates.
+ * adam_t: per-Gaussian step counter (int32). */
+int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
+                  const gs_view *view, const float *lr_cols, void *stream);
+
+/* R/rasterizer.py:559-644 only: grads[row] += d loss / d params (rows of GS_ROW floats);
+ * touched_accum[i] |= touched[i]. */
+int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum, const gs_view *view,
+             void *stream);
+
+/* R/rasterizer.py:707-725 over a dense touched mask (n entries) and gradient rows. */
+int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,
+            const uint8_t *touched, int64_t n, const float *lr_cols, void *stream);
+
+/* ---- helpers for the reference-shaped Python API ------------------------------------- */
+/* dense sparse_depth (H,W) -> K-list (idx, z); count written to *k_out (device int32). */
+int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_t height, int32_t *idx, float *z,
+                     int32_t *k_out, void *stream);
+/* R/gaussians.py:180-215 full records: mu_cam (n,3) mean2d (n,2) cov2d (n,4) conic (n,3) depth (n)
+ * valid (n) jproj (n,6) m (n,6) cov3d (n,9); any output pointer may be NULL. */
+int gs_project(const float *params, int64_t n, const gs_camera *cam, float *mu_cam, float *mean2d,
+               float *cov2d, float *conic, float *depth, uint8_t *valid, float *jproj, float *mmat,
+               float *cov3d, void *stream);
+/* R/gaussians.py:102-111 */
+int gs_eval_sh(const float *sh_low, const float *sh_high, const float *dirs, int64_t n, float *colors,
+               float *preclamp, void *stream);
+/* Pack externally supplied 2D splats (mean2d, conic, cov2d(3), opacity, depth, valid) into
+ * the frame so gs_bin can run stand-alone (R/rasterizer.py:169 cull_tiles signature). */
+int gs_pack_splats(const gs_frame *f, const float *mean2d, const float *conic, const float *cov2d3,
+                   const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
+                   void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSLIC_H */

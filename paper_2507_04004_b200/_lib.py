@@ -1,0 +1,110 @@
+"""ctypes binding of the C ABI in include/gslic.h (libgslic.so, sm_100a).
+
+The product path has no CPU fallback: if the in-tree library is missing (or there is no CUDA
+device) every entry point raises.  Structures mirror the header field by field.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DataError, DomainError, NumericalError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libgslic.so")
+
+GS_ROW = 64
+GS_NPARAM = 59
+GS_TILE = 16
+GS_G2D = 12
+CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3, 4
+GS_CNT_SLOTS = 16
+
+P = ctypes.c_void_p
+i32 = ctypes.c_int32
+i64 = ctypes.c_int64
+f32 = ctypes.c_float
+
+
+class GsCamera(ctypes.Structure):
+    _fields_ = [("width", i32), ("height", i32), ("fx", f32), ("fy", f32), ("cx", f32), ("cy", f32),
+                ("rot_cw", f32 * 9), ("trans_cw", f32 * 3), ("center", f32 * 3)]
+
+
+class GsView(ctypes.Structure):
+    _fields_ = [("cam", GsCamera), ("target", P), ("lidar_idx", P), ("lidar_z", P), ("lidar_k", i32),
+                ("pad_", i32)]
+
+
+class GsFrame(ctypes.Structure):
+    _fields_ = [("n", i64), ("entry_capacity", i64), ("width", i32), ("height", i32), ("tiles_x", i32),
+                ("tiles_y", i32),
+                ("splat2d", P), ("cov2d", P), ("rect", P), ("valid", P), ("touched", P), ("touched_list", P),
+                ("g2d", P), ("keep_bits", P), ("counts", P),
+                ("keys_a", P), ("keys_b", P), ("sort_hist", P), ("sort_status", P), ("scan_status", P),
+                ("status_words", i64), ("scan_words", i64),
+                ("entry_splat", P), ("tile_offsets", P), ("counters", P),
+                ("color", P), ("depth", P), ("opacity", P), ("trans", P), ("n_contrib", P),
+                ("g_color", P), ("g_depth", P), ("g_opac", P), ("loss_parts", P), ("loss", P),
+                ("loss_blocks", i64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libgslic.so; raise loudly if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2507_04004_b200.build` "
+                           "(the sm_100a kernels are the only implementation; there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    sigs = {
+        "gs_workspace_size": (ctypes.c_size_t, [i64, i32, i32, i64]),
+        "gs_frame_layout": (ctypes.c_int, [i64, i32, i32, i64, P, ctypes.c_size_t, ctypes.POINTER(GsFrame)]),
+        "gs_camera_init": (None, [ctypes.POINTER(GsCamera)]),
+        "gs_last_error": (ctypes.c_char_p, []),
+        "gs_version": (ctypes.c_int, []),
+        "gs_preprocess": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P]),
+        "gs_bin": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
+        "gs_render_fwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
+        "gs_loss": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, P]),
+        "gs_render_bwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), P]),
+        "gs_chain_adam": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P]),
+        "gs_chain": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P]),
+        "gs_adam": (ctypes.c_int, [P, P, P, P, P, P, i64, P, P]),
+        "gs_lidar_compact": (ctypes.c_int, [P, i32, i32, P, P, P, P]),
+        "gs_project": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, P, P]),
+        "gs_eval_sh": (ctypes.c_int, [P, P, P, i64, P, P, P]),
+        "gs_pack_splats": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P, P]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
+            "gs_preprocess", "gs_bin", "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_chain_adam",
+            "gs_chain", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats"]
+
+
+def check(rc: int, what: str) -> None:
+    """Map C-ABI status codes onto the reference's error taxonomy (R/errors.py)."""
+    if rc == 0:
+        return
+    msg = f"{what}: {lib().gs_last_error().decode(errors='replace')}"
+    if rc in (1, 2):
+        raise DomainError(msg)
+    if rc in (3, 4):
+        raise DataError(msg)
+    raise NumericalError(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args), name)

@@ -1,0 +1,319 @@
+// adam.cu -- chain rule to Gaussian attributes fused with the sparse Adam step (sm_100a).
+//
+// R/rasterizer.py:559-644 (_chain_to_attributes, attribute part) and R/rasterizer.py:707-725
+// (sparse_adam_step: per-Gaussian step counter, eps 1e-15, untouched rows untouched).
+// Work runs over the compacted touched list.  Each warp owns 32 touched Gaussians: their
+// 256-B parameter rows are staged in shared memory with coalesced float4 loads, every lane
+// computes its Gaussian's 59 gradients into shared memory, then the warp streams the Adam
+// update over the 32 rows (params, m, v) with coalesced float4 traffic.  Nothing but the
+// updated rows is written: the parameter-gradient rows never reach HBM on the 1-GPU path.
+#include "common.cuh"
+
+namespace gs {
+
+constexpr int CA_WARPS = 4;
+constexpr int CA_THREADS = CA_WARPS * 32;
+constexpr int RP = 65;  // padded smem row
+
+// dR/dq of the normalised quaternion (R/rasterizer.py:490-499), contracted with gR
+__device__ __forceinline__ void quat_grad(const float q0[4], const float gR[9], float out[4]) {
+    float nrm = sqrtf(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
+    float w = q0[0] / nrm, x = q0[1] / nrm, y = q0[2] / nrm, z = q0[3] / nrm;
+    const float dw[9] = {0.f, -z, y, z, 0.f, -x, -y, x, 0.f};
+    const float dx[9] = {0.f, y, z, y, -2.f * x, -w, z, w, -2.f * x};
+    const float dy[9] = {-2.f * y, x, w, x, 0.f, z, -w, z, -2.f * y};
+    const float dz[9] = {-2.f * z, -w, x, w, -2.f * z, y, x, y, 0.f};
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; k++) {
+        a0 += gR[k] * dw[k];
+        a1 += gR[k] * dx[k];
+        a2 += gR[k] * dy[k];
+        a3 += gR[k] * dz[k];
+    }
+    const float gq[4] = {2.f * a0, 2.f * a1, 2.f * a2, 2.f * a3};
+    const float qh[4] = {w, x, y, z};
+    const float dot = gq[0] * qh[0] + gq[1] * qh[1] + gq[2] * qh[2] + gq[3] * qh[3];
+#pragma unroll
+    for (int k = 0; k < 4; k++) out[k] = (gq[k] - qh[k] * dot) / nrm;
+}
+
+// gradient of the scalar loss w.r.t. one parameter row (59 columns written to G)
+__device__ __forceinline__ void chain_row(const float *p, const float *g, const gs_camera &cam, float *G) {
+    const float *Rc = cam.rot_cw;
+    const float fx = cam.fx, fy = cam.fy;
+    Projected pr;
+    project_full(p, cam, pr);
+    const float z = pr.mu[2];
+    // conic -> 2x2 covariance gradient (R/rasterizer.py:583-592)
+    const float ca = pr.ca, cb = pr.cb, cc = pr.cc;
+    const float ga = g[2], gb = 0.5f * g[3], gc = g[4];
+    const float t00 = ca * ga + cb * gb, t01 = ca * gb + cb * gc, t10 = cb * ga + cc * gb, t11 = cb * gb + cc * gc;
+    const float gv00 = -(t00 * ca + t01 * cb), gv01 = -(t00 * cb + t01 * cc);
+    const float gv10 = -(t10 * ca + t11 * cb), gv11 = -(t10 * cb + t11 * cc);
+    // cov2d = M S M^T (R/rasterizer.py:595-597)
+    float tmp[6];
+#pragma unroll
+    for (int b = 0; b < 3; b++) {
+        tmp[b] = gv00 * pr.M[b] + gv01 * pr.M[3 + b];
+        tmp[3 + b] = gv10 * pr.M[b] + gv11 * pr.M[3 + b];
+    }
+    float gS[9], gM[6], gJ[6];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) gS[3 * a + b] = pr.M[a] * tmp[b] + pr.M[3 + a] * tmp[3 + b];
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            gM[3 * a + b] = 2.0f * (tmp[3 * a] * pr.S[b] + tmp[3 * a + 1] * pr.S[3 + b] + tmp[3 * a + 2] * pr.S[6 + b]);
+#pragma unroll
+    for (int a = 0; a < 2; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            gJ[3 * a + b] = gM[3 * a] * Rc[3 * b] + gM[3 * a + 1] * Rc[3 * b + 1] + gM[3 * a + 2] * Rc[3 * b + 2];
+    // J and mean2d depend on the camera-frame mean (R/rasterizer.py:600-611)
+    const float iz = 1.0f / z, iz2 = iz * iz, iz3 = iz2 * iz;
+    float gx = gJ[2] * (-fx * iz2);
+    float gy = gJ[5] * (-fy * iz2);
+    float gz = gJ[0] * (-fx * iz2) + gJ[4] * (-fy * iz2) + gJ[2] * (2.0f * fx * pr.mu[0] * iz3) +
+               gJ[5] * (2.0f * fy * pr.mu[1] * iz3);
+    gx += g[0] * fx * iz;
+    gy += g[1] * fy * iz;
+    gz += -g[0] * fx * pr.mu[0] * iz2 - g[1] * fy * pr.mu[1] * iz2;
+    gz += g[9];
+    float gpos[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) gpos[c] = gx * Rc[c] + gy * Rc[3 + c] + gz * Rc[6 + c];
+    // Sigma = (R S)(R S)^T (R/rasterizer.py:613-626)
+    float gN[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++)
+            gN[3 * a + b] = 2.0f * (gS[3 * a] * pr.R[b] + gS[3 * a + 1] * pr.R[3 + b] + gS[3 * a + 2] * pr.R[6 + b]) * pr.s[b];
+#pragma unroll
+    for (int j = 0; j < 3; j++) G[3 + j] = (pr.R[j] * gN[j] + pr.R[3 + j] * gN[3 + j] + pr.R[6 + j] * gN[6 + j]) * pr.s[j];
+    float gR[9];
+#pragma unroll
+    for (int a = 0; a < 3; a++)
+#pragma unroll
+        for (int b = 0; b < 3; b++) gR[3 * a + b] = gN[3 * a + b] * pr.s[b];
+    float gq[4];
+    quat_grad(p + 6, gR, gq);
+#pragma unroll
+    for (int k = 0; k < 4; k++) G[6 + k] = gq[k];
+    // opacity logit (R/rasterizer.py:629-630)
+    const float o = 1.0f / (1.0f + expf(-p[10]));
+    G[10] = g[5] * o * (1.0f - o);
+    // SH colour incl. the view-direction dependence (R/rasterizer.py:633-644)
+    const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
+    float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
+    if (un < 1e-12f) un = 1.0f;
+    const float d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
+    float bs[16];
+    sh_basis(d0, d1, d2, bs);
+    float gcol[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        float acc = 0.0f;
+#pragma unroll
+        for (int k = 0; k < 15; k++) acc += bs[k + 1] * p[14 + 3 * k + c];
+        const float pre = bs[0] * p[11 + c] + acc + 0.5f;
+        gcol[c] = pre > 0.0f ? g[6 + c] : 0.0f;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) G[11 + c] = bs[0] * gcol[c];
+    float sk[16];
+    sk[0] = p[11] * gcol[0] + p[12] * gcol[1] + p[13] * gcol[2];
+#pragma unroll
+    for (int k = 0; k < 15; k++) {
+#pragma unroll
+        for (int c = 0; c < 3; c++) G[14 + 3 * k + c] = bs[k + 1] * gcol[c];
+        sk[k + 1] = p[14 + 3 * k] * gcol[0] + p[15 + 3 * k] * gcol[1] + p[16 + 3 * k] * gcol[2];
+    }
+    float gd[3];
+    sh_basis_vjp(d0, d1, d2, sk, gd);
+    const float dot = gd[0] * d0 + gd[1] * d1 + gd[2] * d2;
+    G[0] = gpos[0] + (gd[0] - d0 * dot) / un;
+    G[1] = gpos[1] + (gd[1] - d1 * dot) / un;
+    G[2] = gpos[2] + (gd[2] - d2 * dot) / un;
+}
+
+__device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float bc1, float bc2) {
+    m = 0.9f * m + 0.1f * g;
+    v = 0.999f * v + 0.001f * g * g;
+    const float mh = m / bc1, vh = v / bc2;
+    return p - lr * mh / (sqrtf(vh) + 1e-15f);
+}
+
+// mode 0: fused Adam on params/m/v/t.  mode 1: grads[row] += G, touched_accum[row] = 1.
+__global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__restrict__ params,
+                                                           float *__restrict__ am, float *__restrict__ av,
+                                                           int32_t *__restrict__ at, const gs_view *__restrict__ view,
+                                                           const float *__restrict__ lr_cols, int mode,
+                                                           float *__restrict__ grads, uint8_t *__restrict__ touched_accum) {
+    extern __shared__ __align__(16) float ca_smem[];
+    float(*srow)[32][RP] = reinterpret_cast<float(*)[32][RP]>(ca_smem);
+    float(*sgr)[32][RP] = reinterpret_cast<float(*)[32][RP]>(ca_smem + CA_WARPS * 32 * RP);
+    float(*sbc)[32][2] = reinterpret_cast<float(*)[32][2]>(ca_smem + 2 * CA_WARPS * 32 * RP);
+    __shared__ gs_camera scam;
+    if (threadIdx.x == 0) scam = view->cam;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
+    const int64_t k0 = ((int64_t)blockIdx.x * CA_WARPS + warp) * 32;
+    if (k0 >= nt) return;
+    const int64_t k = k0 + lane;
+    const int g = k < nt ? f.touched_list[k] : -1;
+    // stage the 32 parameter rows (coalesced: 16 lanes x float4 = one row)
+#pragma unroll 4
+    for (int j = 0; j < 16; j++) {
+        const int kk = lane + 32 * j, r = kk >> 4, c4 = kk & 15;
+        const int gg = __shfl_sync(0xffffffffu, g, r);
+        if (gg >= 0) {
+            const float4 val = *reinterpret_cast<const float4 *>(params + (int64_t)gg * GS_ROW + 4 * c4);
+            srow[warp][r][4 * c4] = val.x;
+            srow[warp][r][4 * c4 + 1] = val.y;
+            srow[warp][r][4 * c4 + 2] = val.z;
+            srow[warp][r][4 * c4 + 3] = val.w;
+        }
+    }
+    __syncwarp();
+    if (g >= 0) {
+        const float4 *g2 = reinterpret_cast<const float4 *>(f.g2d) + (int64_t)g * (GS_G2D / 4);
+        const float4 a = g2[0], b = g2[1], c = g2[2];
+        const float gv[10] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y};
+        chain_row(srow[warp][lane], gv, scam, sgr[warp][lane]);
+        for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
+        if (mode == 0) {
+            const int tn = at[g] + 1;
+            at[g] = tn;
+            sbc[warp][lane][0] = (float)(1.0 - pow(0.9, (double)tn));
+            sbc[warp][lane][1] = (float)(1.0 - pow(0.999, (double)tn));
+        } else {
+            touched_accum[g] = 1;
+        }
+    }
+    __syncwarp();
+#pragma unroll 2
+    for (int j = 0; j < 16; j++) {
+        const int kk = lane + 32 * j, r = kk >> 4, c4 = kk & 15;
+        const int gg = __shfl_sync(0xffffffffu, g, r);
+        if (gg < 0) continue;
+        const int64_t off = (int64_t)gg * GS_ROW + 4 * c4;
+        const float *G = &sgr[warp][r][4 * c4];
+        if (mode == 0) {
+            const float *P = &srow[warp][r][4 * c4];
+            const float bc1 = sbc[warp][r][0], bc2 = sbc[warp][r][1];
+            float4 m4 = *reinterpret_cast<const float4 *>(am + off);
+            float4 v4 = *reinterpret_cast<const float4 *>(av + off);
+            const float4 lr = *reinterpret_cast<const float4 *>(lr_cols + 4 * c4);
+            float4 p4;
+            p4.x = adam_one(P[0], m4.x, v4.x, G[0], lr.x, bc1, bc2);
+            p4.y = adam_one(P[1], m4.y, v4.y, G[1], lr.y, bc1, bc2);
+            p4.z = adam_one(P[2], m4.z, v4.z, G[2], lr.z, bc1, bc2);
+            p4.w = adam_one(P[3], m4.w, v4.w, G[3], lr.w, bc1, bc2);
+            if (c4 == 14) p4.w = P[3];  // column 59 is padding
+            if (c4 == 15) p4 = make_float4(P[0], P[1], P[2], P[3]);
+            *reinterpret_cast<float4 *>(am + off) = m4;
+            *reinterpret_cast<float4 *>(av + off) = v4;
+            *reinterpret_cast<float4 *>(params + off) = p4;
+        } else {
+            float4 acc = *reinterpret_cast<const float4 *>(grads + off);
+            acc.x += G[0];
+            acc.y += G[1];
+            acc.z += G[2];
+            acc.w += G[3];
+            *reinterpret_cast<float4 *>(grads + off) = acc;
+        }
+    }
+}
+
+// dense sparse-Adam over a touched mask (multi-view / multi-GPU batches)
+__global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, float *__restrict__ av,
+                            int32_t *__restrict__ at, const float *__restrict__ grads,
+                            const uint8_t *__restrict__ touched, int64_t n, const float *__restrict__ lr_cols) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= n * 16) return;
+    const int64_t row = idx >> 4;
+    const int c4 = (int)(idx & 15);
+    if (!touched[row]) return;
+    const int tn = at[row] + 1;
+    const float bc1 = (float)(1.0 - pow(0.9, (double)tn)), bc2 = (float)(1.0 - pow(0.999, (double)tn));
+    const int64_t off = row * GS_ROW + 4 * c4;
+    float4 p4 = *reinterpret_cast<const float4 *>(params + off);
+    float4 m4 = *reinterpret_cast<const float4 *>(am + off);
+    float4 v4 = *reinterpret_cast<const float4 *>(av + off);
+    const float4 g4 = *reinterpret_cast<const float4 *>(grads + off);
+    const float4 lr = *reinterpret_cast<const float4 *>(lr_cols + 4 * c4);
+    const float4 old = p4;
+    p4.x = adam_one(p4.x, m4.x, v4.x, g4.x, lr.x, bc1, bc2);
+    p4.y = adam_one(p4.y, m4.y, v4.y, g4.y, lr.y, bc1, bc2);
+    p4.z = adam_one(p4.z, m4.z, v4.z, g4.z, lr.z, bc1, bc2);
+    p4.w = adam_one(p4.w, m4.w, v4.w, g4.w, lr.w, bc1, bc2);
+    if (c4 == 14) p4.w = old.w;
+    if (c4 == 15) p4 = old;
+    *reinterpret_cast<float4 *>(am + off) = m4;
+    *reinterpret_cast<float4 *>(av + off) = v4;
+    *reinterpret_cast<float4 *>(params + off) = p4;
+}
+
+// step counters advance after the update kernel has read them (no intra-kernel race)
+__global__ void adam_step_kernel(int32_t *__restrict__ at, const uint8_t *__restrict__ touched, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n && touched[i]) at[i] += 1;
+}
+
+}  // namespace gs
+
+using namespace gs;
+
+static int launch_chain(const gs_frame *f, float *params, float *m, float *v, int32_t *t, const gs_view *view,
+                        const float *lr, int mode, float *grads, uint8_t *acc, void *stream) {
+    if (f->n == 0) return GS_OK;
+    const int64_t warps = (f->n + 31) / 32;
+    const unsigned blocks = (unsigned)((warps + CA_WARPS - 1) / CA_WARPS);
+    const size_t smem = sizeof(float) * (2 * CA_WARPS * 32 * RP + CA_WARPS * 32 * 2);
+    chain_kernel<<<blocks, CA_THREADS, smem, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads, acc);
+    return check_launch("chain_kernel");
+}
+
+extern "C" int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
+                             const gs_view *view, const float *lr_cols, void *stream) {
+    if (!params || !adam_m || !adam_v || !adam_t || !view || !lr_cols) {
+        set_error("gs_chain_adam: null argument");
+        return GS_ERR_ARG;
+    }
+    return launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 0, nullptr, nullptr, stream);
+}
+
+extern "C" int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum,
+                        const gs_view *view, void *stream) {
+    if (!params || !grads || !touched_accum || !view) {
+        set_error("gs_chain: null argument");
+        return GS_ERR_ARG;
+    }
+    return launch_chain(f, const_cast<float *>(params), nullptr, nullptr, nullptr, view, nullptr, 1, grads,
+                        touched_accum, stream);
+}
+
+extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,
+                       const uint8_t *touched, int64_t n, const float *lr_cols, void *stream) {
+    if (n == 0) return GS_OK;
+    const int64_t work = n * 16;
+    adam_kernel<<<(unsigned)((work + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, adam_m, adam_v, adam_t, grads,
+                                                                                   touched, n, lr_cols);
+    int rc = check_launch("adam_kernel");
+    if (rc) return rc;
+    adam_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(adam_t, touched, n);
+    return check_launch("adam_step_kernel");
+}
+
+namespace gs {
+void init_chain_attrs() {
+    const size_t smem = sizeof(float) * (2 * CA_WARPS * 32 * RP + CA_WARPS * 32 * 2);
+    cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+}  // namespace gs

@@ -1,0 +1,454 @@
+// binning.cu -- tile binning: depth sort, exact per-tile cull, (tile|depth) entries, ranges.
+//
+// Replaces R/rasterizer.py:169-219 (cull_tiles) and the `touched` bookkeeping of
+// _reduce_entries (:424).  The reference enumerates (splat, tile) pairs in splat order, culls
+// them exactly and lexsorts by (tile, depth, splat).  Here:
+//   1. the active Gaussians (>= 1 candidate tile) are sorted by fp32 depth with a stable
+//      onesweep LSD radix sort over 64-bit words (depth_bits << 32 | id): stability gives the
+//      id tie-break;
+//   2. kept pairs are counted (exact cull, strict fp32) and emitted in depth order as 64-bit
+//      words (tile << 32 | id) at scanned offsets;
+//   3. a second stable onesweep sort on the tile bits only yields lexsort((id, depth, tile));
+//   4. tile ranges come from adjacent-key compares.
+// Every kernel reads its element count from device memory, so the sequence is graph-capturable.
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace gs {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_ITEMS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ITEMS;  // 4096 keys per onesweep tile
+constexpr uint32_t FLAG_AGG = 1u << 30, FLAG_INC = 2u << 30, VAL_MASK = (1u << 30) - 1u;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) { return *(volatile const uint32_t *)p; }
+__device__ __forceinline__ void st_atomic(uint32_t *p, uint32_t v) { atomicExch(p, v); }
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// digit histograms of all requested passes in one read (filter: drop inactive words)
+__global__ void __launch_bounds__(256) radix_hist_kernel(const uint64_t *__restrict__ keys, int64_t n_host,
+                                                         const int32_t *__restrict__ n_dev, int shift0, int npasses,
+                                                         uint32_t *__restrict__ hist, int filter,
+                                                         int32_t *__restrict__ active_out) {
+    __shared__ uint32_t sh[4][256];
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&sh[0][0])[k] = 0;
+    __syncthreads();
+    const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+    uint32_t local_active = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t k = keys[i];
+        if (filter && (k >> 32) == 0xffffffffull) continue;
+        local_active++;
+        for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < npasses * 256; k += blockDim.x) {
+        uint32_t v = (&sh[0][0])[k];
+        if (v) atomicAdd(&hist[k], v);
+    }
+    if (filter && active_out) {
+        for (int o = 16; o > 0; o >>= 1) local_active += __shfl_xor_sync(0xffffffffu, local_active, o);
+        if ((threadIdx.x & 31) == 0 && local_active) atomicAdd(active_out, (int32_t)local_active);
+    }
+}
+
+// exclusive scan of each pass's 256 bins (one block per pass)
+__global__ void radix_bins_kernel(uint32_t *hist) {
+    __shared__ uint32_t s[256];
+    uint32_t *h = hist + blockIdx.x * 256;
+    uint32_t v = h[threadIdx.x];
+    s[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {
+        uint32_t t = threadIdx.x >= o ? s[threadIdx.x - o] : 0u;
+        __syncthreads();
+        s[threadIdx.x] += t;
+        __syncthreads();
+    }
+    h[threadIdx.x] = s[threadIdx.x] - v;
+}
+
+// ---------------------------------------------------------------------------
+// one onesweep pass: stable counting-sort of a 4096-key tile by one 8-bit digit, decoupled
+// look-back across tiles for the per-digit global offsets, scatter through shared memory.
+__global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__restrict__ in, uint64_t *__restrict__ out,
+                                                              int64_t n_host, const int32_t *__restrict__ n_dev,
+                                                              int shift, const uint32_t *__restrict__ bins,
+                                                              uint32_t *status, int32_t *ticket, int filter) {
+    constexpr int WARPS = RS_THREADS / 32;
+    __shared__ uint32_t s_warp[WARPS][256];
+    __shared__ uint32_t s_start[256];
+    __shared__ uint32_t s_base[256];
+    __shared__ uint32_t s_scan[WARPS];
+    __shared__ uint64_t s_keys[RS_TILE];
+    __shared__ int s_tile;
+    __shared__ uint32_t s_total;
+
+    const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    for (int k = threadIdx.x; k < WARPS * 256; k += RS_THREADS) (&s_warp[0][0])[k] = 0u;
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t tbase = (int64_t)tile * RS_TILE;
+    if (tbase >= n) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t wbase = tbase + (int64_t)warp * 32 * RS_ITEMS;
+    const unsigned ltmask = lanemask_lt();
+
+    uint64_t key[RS_ITEMS];
+    uint32_t rank[RS_ITEMS];
+    bool ok[RS_ITEMS];
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        int64_t idx = wbase + i * 32 + lane;
+        ok[i] = idx < n;
+        key[i] = ok[i] ? in[idx] : 0ull;
+        if (filter && ok[i] && (key[i] >> 32) == 0xffffffffull) ok[i] = false;
+    }
+    // warp-level stable ranking: items in order, lanes in order
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        const unsigned active = __ballot_sync(0xffffffffu, ok[i]);
+        if (ok[i]) {
+            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
+            const unsigned peers = __match_any_sync(active, d);
+            const uint32_t before = s_warp[warp][d];
+            rank[i] = before + __popc(peers & ltmask);
+            __syncwarp(active);
+            if (lane == 31 - __clz(peers)) s_warp[warp][d] = before + __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // per-digit warp offsets and tile totals; thread t owns digit t
+    const int t = threadIdx.x;
+    uint32_t run = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; w++) {
+        uint32_t c = s_warp[w][t];
+        s_warp[w][t] = run;
+        run += c;
+    }
+    uint32_t *st = status + (int64_t)tile * 256;
+    if (tile == 0) st_atomic(&st[t], FLAG_INC | run);
+    else st_atomic(&st[t], FLAG_AGG | run);
+    // block exclusive scan of `run` over digits -> s_start
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_scan[warp] = x;
+    __syncthreads();
+    uint32_t wpre = 0;
+#pragma unroll
+    for (int w = 0; w < WARPS; w++)
+        if (w < warp) wpre += s_scan[w];
+    const uint32_t excl = wpre + x - run;
+    s_start[t] = excl;
+    if (t == 255) s_total = excl + run;
+    // decoupled look-back over preceding tiles
+    uint32_t prefix = 0;
+    if (tile > 0) {
+        int j = tile - 1;
+        while (j >= 0) {
+            uint32_t s = ld_volatile(&status[(int64_t)j * 256 + t]);
+            uint32_t flag = s & ~VAL_MASK;
+            if (flag == 0u) continue;
+            prefix += s & VAL_MASK;
+            if (flag == FLAG_INC) break;
+            j--;
+        }
+        st_atomic(&st[t], FLAG_INC | (prefix + run));
+    }
+    s_base[t] = bins[t] + prefix - excl;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < RS_ITEMS; i++) {
+        if (ok[i]) {
+            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
+            s_keys[s_start[d] + s_warp[warp][d] + rank[i]] = key[i];
+        }
+    }
+    __syncthreads();
+    const uint32_t total = s_total;
+    for (uint32_t j = threadIdx.x; j < total; j += RS_THREADS) {
+        uint64_t k = s_keys[j];
+        const uint32_t d = (uint32_t)(k >> shift) & 255u;
+        out[s_base[d] + j] = k;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// single-pass exclusive scan (decoupled look-back) of int32 counts; total -> *total_out
+constexpr int SC_ITEMS = 16;
+constexpr int SC_TILE = RS_THREADS * SC_ITEMS;
+
+__global__ void __launch_bounds__(RS_THREADS) scan_kernel(int32_t *data, int64_t n_host, const int32_t *n_dev,
+                                                          uint32_t *status, int32_t *ticket, int32_t *total_out,
+                                                          int64_t capacity, int32_t *overflow, int32_t *eff_out) {
+    __shared__ int s_tile;
+    __shared__ uint32_t s_warp[RS_THREADS / 32];
+    __shared__ uint32_t s_prefix;
+    const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
+    if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
+    __syncthreads();
+    const int tile = s_tile;
+    const int64_t tbase = (int64_t)tile * SC_TILE;
+    if (tbase >= n && !(tile == 0 && n == 0)) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint32_t v[SC_ITEMS];
+    uint32_t sum = 0;
+    const int64_t mybase = tbase + (int64_t)threadIdx.x * SC_ITEMS;
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; i++) {
+        v[i] = (mybase + i < n) ? (uint32_t)data[mybase + i] : 0u;
+        sum += v[i];
+    }
+    uint32_t x = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    uint32_t wpre = 0, agg = 0;
+    for (int w = 0; w < RS_THREADS / 32; w++) {
+        if (w < warp) wpre += s_warp[w];
+        agg += s_warp[w];
+    }
+    if (threadIdx.x == 0) {
+        uint32_t prefix = 0;
+        if (tile == 0) {
+            st_atomic(&status[0], FLAG_INC | agg);
+        } else {
+            st_atomic(&status[tile], FLAG_AGG | agg);
+            int j = tile - 1;
+            while (j >= 0) {
+                uint32_t s = ld_volatile(&status[j]);
+                uint32_t flag = s & ~VAL_MASK;
+                if (flag == 0u) continue;
+                prefix += s & VAL_MASK;
+                if (flag == FLAG_INC) break;
+                j--;
+            }
+            st_atomic(&status[tile], FLAG_INC | (prefix + agg));
+        }
+        s_prefix = prefix;
+        if (tbase + SC_TILE >= n) {  // last tile
+            const int64_t tot = (int64_t)(prefix + agg);
+            *total_out = (int32_t)tot;
+            if (tot > capacity) *overflow = 1;
+            *eff_out = tot > capacity ? 0 : (int32_t)tot;
+        }
+    }
+    __syncthreads();
+    uint32_t run = s_prefix + wpre + x - sum;
+#pragma unroll
+    for (int i = 0; i < SC_ITEMS; i++) {
+        if (mybase + i < n) data[mybase + i] = (int32_t)run;
+        run += v[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// count (and cache the first 64 cull bits) of kept tiles per active Gaussian, depth order.
+// One warp per Gaussian; lanes stride over its candidate tiles.
+__global__ void __launch_bounds__(256) count_kernel(gs_frame f, const uint64_t *__restrict__ sorted, int cull) {
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t n_active = f.counters[GS_CNT_ACTIVE];
+    if (k >= n_active) return;
+    const uint32_t g = (uint32_t)sorted[k];
+    const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+    const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+    int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+    if (!cull) r = make_int4(0, f.tiles_x - 1, 0, f.tiles_y - 1);
+    const int nx = r.y - r.x + 1, ny = r.w - r.z + 1;
+    const int ncand = nx * ny;
+    uint32_t count = 0;
+    uint64_t bits = 0;
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+        const int c = c0 + lane;
+        bool keep = false;
+        if (c < ncand) {
+            if (!cull) keep = true;
+            else {
+                const int tx = r.x + c % nx, ty = r.z + c / nx;
+                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        count += __popc(b);
+        if (c0 == 0) bits |= (uint64_t)b;
+        else if (c0 == 32) bits |= (uint64_t)b << 32;
+    }
+    if (lane == 0) {
+        f.counts[k] = (int32_t)count;
+        f.keep_bits[k] = bits;
+        if (count) {
+            f.touched[g] = 1;
+            const int32_t slot = atomicAdd(&f.counters[GS_CNT_TOUCHED], 1);
+            f.touched_list[slot] = (int32_t)g;
+        }
+    }
+}
+
+// emit kept pairs as (tile << 32 | id) at the scanned offsets (depth order)
+__global__ void __launch_bounds__(256) emit_kernel(gs_frame f, const uint64_t *__restrict__ sorted,
+                                                   uint64_t *__restrict__ out, int cull) {
+    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t n_active = f.counters[GS_CNT_ACTIVE];
+    if (k >= n_active || f.counters[GS_CNT_OVERFLOW]) return;
+    const uint32_t g = (uint32_t)sorted[k];
+    int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+    if (!cull) r = make_int4(0, f.tiles_x - 1, 0, f.tiles_y - 1);
+    const int nx = r.y - r.x + 1, ny = r.w - r.z + 1;
+    const int ncand = nx * ny;
+    const uint64_t bits = f.keep_bits[k];
+    int64_t off = f.counts[k];
+    float4 s0, s1;
+    if (ncand > 64) {
+        s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+        s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+    }
+    for (int c0 = 0; c0 < ncand; c0 += 32) {
+        const int c = c0 + lane;
+        bool keep = false;
+        const int tx = r.x + c % nx, ty = r.z + c / nx;
+        if (c < ncand) {
+            if (!cull || c < 64) keep = !cull ? true : ((bits >> c) & 1ull);
+            else {
+                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+            }
+        }
+        const unsigned b = __ballot_sync(0xffffffffu, keep);
+        if (keep) {
+            const int64_t pos = off + __popc(b & lanemask_lt());
+            out[pos] = ((uint64_t)(uint32_t)(ty * f.tiles_x + tx) << 32) | (uint64_t)g;
+        }
+        off += __popc(b);
+    }
+}
+
+// tile_offsets[t] = first entry with tile >= t; entry_splat[e] = low word
+__global__ void ranges_kernel(gs_frame f, const uint64_t *__restrict__ sorted) {
+    const int64_t E = f.counters[GS_CNT_ENTRIES_EFF];
+    const int32_t T = f.tiles_x * f.tiles_y;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (E == 0) {
+        for (int64_t t = e; t <= T; t += (int64_t)gridDim.x * blockDim.x) f.tile_offsets[t] = 0;
+        return;
+    }
+    for (int64_t i = e; i < E; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t w = sorted[i];
+        const int32_t tile = (int32_t)(w >> 32);
+        f.entry_splat[i] = (int32_t)(uint32_t)w;
+        const int32_t prev = i == 0 ? -1 : (int32_t)(sorted[i - 1] >> 32);
+        for (int32_t t = prev + 1; t <= tile; t++) f.tile_offsets[t] = (int32_t)i;
+        if (i == E - 1)
+            for (int32_t t = tile + 1; t <= T; t++) f.tile_offsets[t] = (int32_t)E;
+    }
+}
+
+// cull=False keys: every valid Gaussian is active (R/rasterizer.py:195-199)
+__global__ void keys_nocull_kernel(gs_frame f) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= f.n) return;
+    const float d = f.splat2d[12 * i + 6];
+    f.keys_a[i] = f.valid[i] ? (((uint64_t)__float_as_uint(d) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
+}
+
+static int sort_pass(const gs_frame *f, const uint64_t *in, uint64_t *out, int64_t n_host, const int32_t *n_dev,
+                     int shift, const uint32_t *bins, int pass_slot, int filter, cudaStream_t st) {
+    const int64_t tiles = (n_host + RS_TILE - 1) / RS_TILE;
+    if (tiles == 0) return GS_OK;
+    uint32_t *status = f->sort_status + (int64_t)pass_slot * (f->status_words / 8);
+    onesweep_kernel<<<(unsigned)tiles, RS_THREADS, 0, st>>>(in, out, n_host, n_dev, shift, bins, status,
+                                                             f->counters + GS_CNT_TICKET0 + pass_slot, filter);
+    return check_launch("onesweep_kernel");
+}
+
+}  // namespace gs
+
+using namespace gs;
+
+extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t n = f->n;
+    const int32_t T = f->tiles_x * f->tiles_y;
+    int rc;
+    // reset counters, histograms and look-back state
+    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, st);
+    cudaMemsetAsync(f->sort_hist, 0, sizeof(uint32_t) * 8 * 256, st);
+    cudaMemsetAsync(f->sort_status, 0, sizeof(uint32_t) * f->status_words, st);
+    cudaMemsetAsync(f->scan_status, 0, sizeof(uint32_t) * f->scan_words, st);
+    if (n == 0) {
+        ranges_kernel<<<1, 256, 0, st>>>(*f, f->keys_b);
+        return check_launch("ranges_kernel");
+    }
+    if (!cull) {
+        keys_nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
+        if ((rc = check_launch("keys_nocull_kernel"))) return rc;
+    }
+    const int hist_blocks = 4 * 148;
+    // 1) depth sort of the active Gaussians (4 passes over the 32 depth bits, filtered first pass)
+    radix_hist_kernel<<<hist_blocks, 256, 0, st>>>(f->keys_a, n, nullptr, 32, 4, f->sort_hist, 1,
+                                                   f->counters + GS_CNT_ACTIVE);
+    if ((rc = check_launch("radix_hist_kernel"))) return rc;
+    // tile-sort histograms are computed after emit; bins for passes 0-3 now
+    radix_bins_kernel<<<4, 256, 0, st>>>(f->sort_hist);
+    const int32_t *n_act = f->counters + GS_CNT_ACTIVE;
+    if ((rc = sort_pass(f, f->keys_a, f->keys_b, n, nullptr, 32, f->sort_hist + 0 * 256, 0, 1, st))) return rc;
+    if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 40, f->sort_hist + 1 * 256, 1, 0, st))) return rc;
+    if ((rc = sort_pass(f, f->keys_a, f->keys_b, n, n_act, 48, f->sort_hist + 2 * 256, 2, 0, st))) return rc;
+    if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 56, f->sort_hist + 3 * 256, 3, 0, st))) return rc;
+    // 2) exact cull counts in depth order, scan, emit
+    const unsigned warp_blocks = (unsigned)((n * 32 + 255) / 256);
+    count_kernel<<<warp_blocks, 256, 0, st>>>(*f, f->keys_a, cull);
+    if ((rc = check_launch("count_kernel"))) return rc;
+    {
+        const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
+        scan_kernel<<<(unsigned)(tiles > 0 ? tiles : 1), RS_THREADS, 0, st>>>(
+            f->counts, n, n_act, (uint32_t *)f->scan_status, f->counters + GS_CNT_TICKET0 + 7,
+            f->counters + GS_CNT_ENTRIES, f->entry_capacity, f->counters + GS_CNT_OVERFLOW,
+            f->counters + GS_CNT_ENTRIES_EFF);
+        if ((rc = check_launch("scan_kernel"))) return rc;
+    }
+    emit_kernel<<<warp_blocks, 256, 0, st>>>(*f, f->keys_a, f->keys_b, cull);
+    if ((rc = check_launch("emit_kernel"))) return rc;
+    // 3) stable sort of the entries by tile id (bits 32.. of the word)
+    int tile_bits = 0;
+    while ((1 << tile_bits) < T) tile_bits++;
+    const int tpasses = tile_bits <= 8 ? 1 : (tile_bits <= 16 ? 2 : 3);
+    const int32_t *n_ent = f->counters + GS_CNT_ENTRIES_EFF;
+    const int64_t cap = f->entry_capacity;
+    radix_hist_kernel<<<hist_blocks, 256, 0, st>>>(f->keys_b, cap, n_ent, 32, tpasses, f->sort_hist + 4 * 256, 0,
+                                                   nullptr);
+    if ((rc = check_launch("radix_hist_kernel"))) return rc;
+    radix_bins_kernel<<<tpasses, 256, 0, st>>>(f->sort_hist + 4 * 256);
+    uint64_t *src = f->keys_b, *dst = f->keys_a;
+    for (int p = 0; p < tpasses; p++) {
+        if ((rc = sort_pass(f, src, dst, cap, n_ent, 32 + 8 * p, f->sort_hist + (4 + p) * 256, 4 + p, 0, st))) return rc;
+        uint64_t *tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    // 4) ranges + entry ids
+    ranges_kernel<<<4 * 148, 256, 0, st>>>(*f, src);
+    return check_launch("ranges_kernel");
+}

@@ -1,0 +1,276 @@
+// common.cuh -- shared device helpers for the sm_100a map-optimisation kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gslic.h"
+
+#define GS_WARP 32
+#define GS_NEAR_CLIP 0.01f     // R/gaussians.py:34
+#define GS_DILATION 0.3f       // R/gaussians.py:33
+#define GS_ALPHA_CLAMP 0.99f   // R/gaussians.py:35
+#define GS_EARLY_STOP_T 1e-4f  // R/rasterizer.py:43
+#define GS_LOG2E 1.4426950408889634f
+
+// counters beyond the public GS_CNT_* slots: per-pass tile tickets for the lookback kernels
+#define GS_CNT_TICKET0 8
+
+namespace gs {
+
+// ---------------------------------------------------------------------------
+// error plumbing (thread-local, no global mutable state shared across threads)
+void set_error(const char *fmt, ...);
+int check_launch(const char *what);
+
+// ---------------------------------------------------------------------------
+// SH constants, R/gaussians.py:24-30
+__device__ __constant__ static const float SH_C0 = 0.28209479177387814f;
+__device__ __constant__ static const float SH_C1 = 0.4886025119029199f;
+
+struct Sh {
+    static constexpr float C2_0 = 1.0925484305920792f, C2_1 = -1.0925484305920792f, C2_2 = 0.31539156525252005f,
+                           C2_3 = -1.0925484305920792f, C2_4 = 0.5462742152960396f;
+    static constexpr float C3_0 = -0.5900435899266435f, C3_1 = 2.890611442640554f, C3_2 = -0.4570457994644658f,
+                           C3_3 = 0.3731763325901154f, C3_4 = -0.4570457994644658f, C3_5 = 1.445305721320277f,
+                           C3_6 = -0.5900435899266435f;
+};
+
+// real SH basis, degrees 0..3 (R/gaussians.py:51-74)
+__device__ __forceinline__ void sh_basis(float x, float y, float z, float b[16]) {
+    float xx = x * x, yy = y * y, zz = z * z, xy = x * y, yz = y * z, xz = x * z;
+    b[0] = 0.28209479177387814f;
+    b[1] = -0.4886025119029199f * y;
+    b[2] = 0.4886025119029199f * z;
+    b[3] = -0.4886025119029199f * x;
+    b[4] = Sh::C2_0 * xy;
+    b[5] = Sh::C2_1 * yz;
+    b[6] = Sh::C2_2 * (2.0f * zz - xx - yy);
+    b[7] = Sh::C2_3 * xz;
+    b[8] = Sh::C2_4 * (xx - yy);
+    b[9] = Sh::C3_0 * y * (3.0f * xx - yy);
+    b[10] = Sh::C3_1 * xy * z;
+    b[11] = Sh::C3_2 * y * (4.0f * zz - xx - yy);
+    b[12] = Sh::C3_3 * z * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+    b[13] = Sh::C3_4 * x * (4.0f * zz - xx - yy);
+    b[14] = Sh::C3_5 * z * (xx - yy);
+    b[15] = Sh::C3_6 * x * (xx - 3.0f * yy);
+}
+
+// d basis / d dir  (R/gaussians.py:77-99), returns gdir = sum_k dB_k/dd * s_k
+__device__ __forceinline__ void sh_basis_vjp(float x, float y, float z, const float s[16], float g[3]) {
+    float gx = -0.4886025119029199f * s[3], gy = -0.4886025119029199f * s[1], gz = 0.4886025119029199f * s[2];
+    gx += Sh::C2_0 * y * s[4];
+    gy += Sh::C2_0 * x * s[4];
+    gy += Sh::C2_1 * z * s[5];
+    gz += Sh::C2_1 * y * s[5];
+    gx += Sh::C2_2 * (-2.0f * x) * s[6];
+    gy += Sh::C2_2 * (-2.0f * y) * s[6];
+    gz += Sh::C2_2 * (4.0f * z) * s[6];
+    gx += Sh::C2_3 * z * s[7];
+    gz += Sh::C2_3 * x * s[7];
+    gx += Sh::C2_4 * (2.0f * x) * s[8];
+    gy += Sh::C2_4 * (-2.0f * y) * s[8];
+    gx += Sh::C3_0 * (6.0f * x * y) * s[9];
+    gy += Sh::C3_0 * (3.0f * x * x - 3.0f * y * y) * s[9];
+    gx += Sh::C3_1 * (y * z) * s[10];
+    gy += Sh::C3_1 * (x * z) * s[10];
+    gz += Sh::C3_1 * (x * y) * s[10];
+    gx += Sh::C3_2 * (-2.0f * x * y) * s[11];
+    gy += Sh::C3_2 * (4.0f * z * z - x * x - 3.0f * y * y) * s[11];
+    gz += Sh::C3_2 * (8.0f * y * z) * s[11];
+    gx += Sh::C3_3 * (-6.0f * x * z) * s[12];
+    gy += Sh::C3_3 * (-6.0f * y * z) * s[12];
+    gz += Sh::C3_3 * (6.0f * z * z - 3.0f * x * x - 3.0f * y * y) * s[12];
+    gx += Sh::C3_4 * (4.0f * z * z - 3.0f * x * x - y * y) * s[13];
+    gy += Sh::C3_4 * (-2.0f * x * y) * s[13];
+    gz += Sh::C3_4 * (8.0f * x * z) * s[13];
+    gx += Sh::C3_5 * (2.0f * x * z) * s[14];
+    gy += Sh::C3_5 * (-2.0f * y * z) * s[14];
+    gz += Sh::C3_5 * (x * x - y * y) * s[14];
+    gx += Sh::C3_6 * (3.0f * x * x - 3.0f * y * y) * s[15];
+    gy += Sh::C3_6 * (-6.0f * x * y) * s[15];
+    g[0] = gx;
+    g[1] = gy;
+    g[2] = gz;
+}
+
+// ---------------------------------------------------------------------------
+// projection (R/gaussians.py:156-215)
+
+struct Projected {
+    float mu[3];
+    float J[6];   // 2x3
+    float M[6];   // J R_cw
+    float R[9];   // rotation of the Gaussian (normalised quaternion)
+    float s[3];   // exp(log_scale)
+    float S[9];   // world covariance
+    float c00, c01, c11;  // dilated 2x2 covariance
+    float det;
+    float mx, my;
+    float ca, cb, cc;  // conic
+    bool valid;
+};
+
+__device__ __forceinline__ void quat_rot(const float q0[4], float R[9]) {
+    float nrm = sqrtf(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
+    float w = q0[0] / nrm, x = q0[1] / nrm, y = q0[2] / nrm, z = q0[3] / nrm;
+    R[0] = 1.0f - 2.0f * (y * y + z * z); R[1] = 2.0f * (x * y - w * z); R[2] = 2.0f * (x * z + w * y);
+    R[3] = 2.0f * (x * y + w * z); R[4] = 1.0f - 2.0f * (x * x + z * z); R[5] = 2.0f * (y * z - w * x);
+    R[6] = 2.0f * (x * z - w * y); R[7] = 2.0f * (y * z + w * x); R[8] = 1.0f - 2.0f * (x * x + y * y);
+}
+
+// p: pos[3], log_scale[3], quat[4] (the first 10 columns of a parameter row)
+__device__ __forceinline__ void project_full(const float *p, const gs_camera &cam, Projected &o) {
+    const float *Rc = cam.rot_cw;
+    for (int r = 0; r < 3; r++) o.mu[r] = (p[0] * Rc[3 * r] + p[1] * Rc[3 * r + 1] + p[2] * Rc[3 * r + 2]) + cam.trans_cw[r];
+    float z = o.mu[2];
+    bool v = z > GS_NEAR_CLIP;
+    float zs = v ? z : 1.0f;
+    float iz = 1.0f / zs;
+    o.mx = cam.fx * o.mu[0] * iz + cam.cx;
+    o.my = cam.fy * o.mu[1] * iz + cam.cy;
+    o.J[0] = cam.fx * iz; o.J[1] = 0.0f; o.J[2] = -cam.fx * o.mu[0] * iz * iz;
+    o.J[3] = 0.0f; o.J[4] = cam.fy * iz; o.J[5] = -cam.fy * o.mu[1] * iz * iz;
+    for (int r = 0; r < 2; r++)
+        for (int c = 0; c < 3; c++)
+            o.M[3 * r + c] = o.J[3 * r] * Rc[c] + o.J[3 * r + 1] * Rc[3 + c] + o.J[3 * r + 2] * Rc[6 + c];
+    quat_rot(p + 6, o.R);
+    o.s[0] = expf(p[3]); o.s[1] = expf(p[4]); o.s[2] = expf(p[5]);
+    float s2[3] = {o.s[0] * o.s[0], o.s[1] * o.s[1], o.s[2] * o.s[2]};
+    for (int a = 0; a < 3; a++)
+        for (int b = a; b < 3; b++) {
+            float val = o.R[3 * a] * s2[0] * o.R[3 * b] + o.R[3 * a + 1] * s2[1] * o.R[3 * b + 1] +
+                        o.R[3 * a + 2] * s2[2] * o.R[3 * b + 2];
+            o.S[3 * a + b] = val;
+            o.S[3 * b + a] = val;
+        }
+    float MS[6];
+    for (int r = 0; r < 2; r++)
+        for (int c = 0; c < 3; c++) MS[3 * r + c] = o.M[3 * r] * o.S[c] + o.M[3 * r + 1] * o.S[3 + c] + o.M[3 * r + 2] * o.S[6 + c];
+    o.c00 = MS[0] * o.M[0] + MS[1] * o.M[1] + MS[2] * o.M[2] + GS_DILATION;
+    o.c01 = MS[0] * o.M[3] + MS[1] * o.M[4] + MS[2] * o.M[5];
+    o.c11 = MS[3] * o.M[3] + MS[4] * o.M[4] + MS[5] * o.M[5] + GS_DILATION;
+    o.det = o.c00 * o.c11 - o.c01 * o.c01;
+    v = v && (o.det > 1e-12f) && isfinite(o.det);
+    o.valid = v;
+    float dets = v ? o.det : 1.0f;
+    o.ca = o.c11 / dets;
+    o.cb = -o.c01 / dets;
+    o.cc = o.c00 / dets;
+}
+
+// ---------------------------------------------------------------------------
+// binning decision path: strict IEEE fp32 (no contraction) so that the CPU fp32 restatement
+// (oracle/gs_oracle.c f32_rect / f32_tile_min_q) reproduces every decision bit for bit.
+
+__device__ __forceinline__ float det_logf(float x) {  // x >= 1, see DESIGN.md
+    uint32_t u = __float_as_uint(x);
+    int e = (int)((u >> 23) & 0xffu) - 127;
+    float m = __uint_as_float((u & 0x7fffffu) | 0x3f800000u);
+    if (m > 1.41421353816986083984375f) {
+        m = __fmul_rn(m, 0.5f);
+        e += 1;
+    }
+    float s = __fdiv_rn(__fsub_rn(m, 1.0f), __fadd_rn(m, 1.0f));
+    float s2 = __fmul_rn(s, s);
+    float p = __fmaf_rn(s2, 0.111111111938953399658203125f, 0.14285714924335479736328125f);
+    p = __fmaf_rn(p, s2, 0.20000000298023223876953125f);
+    p = __fmaf_rn(p, s2, 0.3333333432674407958984375f);
+    p = __fmaf_rn(p, s2, 1.0f);
+    float lm = __fmul_rn(__fmul_rn(2.0f, s), p);
+    return __fmaf_rn((float)e, 0.693147182464599609375f, lm);
+}
+
+// influence radius + tile rectangle (R/rasterizer.py:84-102, 183-194).  Returns false when the
+// Gaussian has no candidate tile.
+__device__ __forceinline__ bool tile_rect(float c00, float c01, float c11, float o, float mx, float my, int width,
+                                          int height, int tiles_x, int tiles_y, int4 &rect, float &qcut,
+                                          float &radius) {
+    float half_tr = __fmul_rn(0.5f, __fadd_rn(c00, c11));
+    float df = __fsub_rn(c00, c11);
+    float dd = __fadd_rn(__fmul_rn(0.25f, __fmul_rn(df, df)), __fmul_rn(c01, c01));
+    float lam = __fadd_rn(half_tr, __fsqrt_rn(dd > 0.0f ? dd : 0.0f));
+    if (!(o > (float)(1.0 / 255.0))) return false;
+    float L = det_logf(__fmul_rn(255.0f, o));
+    float r = __fadd_rn(__fsqrt_rn(__fmul_rn(__fmul_rn(2.0f, L), lam)), 1e-6f);
+    radius = r;
+    if (!(r > 0.0f)) return false;
+    if ((__fadd_rn(mx, r) < 0.0f) || (__fsub_rn(mx, r) > (float)(width - 1)) || (__fadd_rn(my, r) < 0.0f) ||
+        (__fsub_rn(my, r) > (float)(height - 1)))
+        return false;
+    float f;
+    f = floorf(__fmul_rn(__fsub_rn(mx, r), 0.0625f));
+    rect.x = f < 0.0f ? 0 : (f > (float)(tiles_x - 1) ? tiles_x - 1 : (int)f);
+    f = floorf(__fmul_rn(__fadd_rn(mx, r), 0.0625f));
+    rect.y = f < 0.0f ? 0 : (f > (float)(tiles_x - 1) ? tiles_x - 1 : (int)f);
+    f = floorf(__fmul_rn(__fsub_rn(my, r), 0.0625f));
+    rect.z = f < 0.0f ? 0 : (f > (float)(tiles_y - 1) ? tiles_y - 1 : (int)f);
+    f = floorf(__fmul_rn(__fadd_rn(my, r), 0.0625f));
+    rect.w = f < 0.0f ? 0 : (f > (float)(tiles_y - 1) ? tiles_y - 1 : (int)f);
+    qcut = __fmul_rn(2.0f, L);
+    return true;
+}
+
+// q at integer pixel column xc on row offset dy (R/rasterizer.py:143-144, strict order)
+__device__ __forceinline__ float quad_q(float ca, float cb, float cc, float dx, float dy) {
+    return __fadd_rn(__fadd_rn(__fmul_rn(__fmul_rn(ca, dx), dx), __fmul_rn(__fmul_rn(__fmul_rn(2.0f, cb), dx), dy)),
+                     __fmul_rn(__fmul_rn(cc, dy), dy));
+}
+
+// Exact cull of one (Gaussian, tile) pair (R/rasterizer.py:125-166): keep iff the minimum of
+// the quadratic over the tile's integer pixel grid is <= qcut (= 2 ln(255 o), the q-domain
+// form of o e^{-q/2} >= 1/255).  "min <= qcut" == "some evaluated q <= qcut", so rows are
+// scanned outward from the mean row and the scan stops at the first hit.  A conservative
+// continuous lower bound rejects clearly-outside tiles without the scan.
+__device__ __forceinline__ bool tile_keep(float mx, float my, float ca, float cb, float cc, float qcut, int x0,
+                                          int x1, int y0, int y1) {
+    // continuous minimum over [x0,x1]x[y0,y1] (real-valued), only as a safe early reject
+    float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
+    if (!(ax0 <= 0.0f && ax1 >= 0.0f && ay0 <= 0.0f && ay1 >= 0.0f)) {
+        float qc = 3.0e38f;
+        float ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            float y = ys[k];
+            float dx = fminf(fmaxf(-cb * y / ca, ax0), ax1);
+            qc = fminf(qc, ca * dx * dx + 2.0f * cb * dx * y + cc * y * y);
+            float x = xs[k];
+            float dy = fminf(fmaxf(-cb * x / cc, ay0), ay1);
+            qc = fminf(qc, ca * x * x + 2.0f * cb * x * dy + cc * dy * dy);
+        }
+        float scale = ca * fmaxf(ax0 * ax0, ax1 * ax1) + cc * fmaxf(ay0 * ay0, ay1 * ay1);
+        if (qc - 1e-4f * scale - 1e-4f > qcut) return false;
+    }
+    int r0 = (int)floorf(my + 0.5f);
+    r0 = r0 < y0 ? y0 : (r0 > y1 ? y1 : r0);
+    int nrows = y1 - y0 + 1;
+    float lo = (float)(x0 - 1), hi = (float)(x1 + 1);
+    for (int k = 0, up = r0, dn = r0 - 1; k < nrows; k++) {
+        int py;
+        // alternate r0, r0-1, r0+1, r0-2, ... staying inside [y0, y1]
+        if ((k & 1) == 0) {
+            if (up <= y1) py = up++;
+            else py = dn--;
+        } else {
+            if (dn >= y0) py = dn--;
+            else py = up++;
+        }
+        float dy = __fsub_rn((float)py, my);
+        float xsr = __fsub_rn(mx, __fdiv_rn(__fmul_rn(cb, dy), ca));
+        if (!(xsr >= lo)) xsr = lo;
+        if (xsr > hi) xsr = hi;
+        int xf = (int)floorf(xsr);
+#pragma unroll
+        for (int j = 0; j < 2; j++) {
+            int xc = xf + j;
+            xc = xc < x0 ? x0 : (xc > x1 ? x1 : xc);
+            float dx = __fsub_rn((float)xc, mx);
+            if (quad_q(ca, cb, cc, dx, dy) <= qcut) return true;
+        }
+    }
+    return false;
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+}  // namespace gs

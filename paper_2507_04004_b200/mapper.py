@@ -1,0 +1,367 @@
+"""Mapping driver: mirror of R/mapper.py's optimisation loop over a device-resident engine.
+
+`MapOptimizer` keeps every keyframe (target image + LiDAR K-list + camera) resident in HBM
+and runs one map-optimisation iteration (R/mapper.py:246-263: forward -> mapping_loss ->
+backward -> sparse_adam_step) as six C-ABI launches with no host synchronisation; the launch
+sequence can be captured once into a CUDA graph and replayed per keyframe.  `optimize_map`
+keeps the reference's signature and sampling (R/mapper.py:233-264).
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import call
+from .errors import DataError
+from .gaussians import GaussianMap, as_device_map, init_from_points, stream_ptr
+from .rasterizer import (AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from, default_lrs, forward,
+                         lr_columns)
+
+NEAR_CLIP = 0.01
+
+
+@dataclass
+class MappingConfig:
+    """R/mapper.py:28-50 (the hot-path knobs: lam, xi, k_keyframes)."""
+    lam: float = 0.2
+    xi: float = 0.005
+    k_keyframes: int = 100
+    tau: float = 0.99
+    n_p: int = 10
+    eps1: float = 0.1
+    eps2: float = 50.0
+    keyframe_stride: int = 5
+    grad_thresh: float = 1.0
+    patch: int = 30
+    refine_rounds: int = 0
+
+    def __post_init__(self):
+        if not 0.0 < self.tau < 1.0:
+            raise ValueError("tau must lie in (0, 1)")
+        if self.xi < 0:
+            raise ValueError("xi must be non-negative")
+        for name in ("lam", "k_keyframes", "n_p", "eps1", "eps2", "keyframe_stride", "grad_thresh", "patch"):
+            if getattr(self, name) <= 0:
+                raise ValueError(f"{name} must be positive")
+
+
+@dataclass
+class Keyframe:
+    """R/mapper.py:53-66: a posed image plus its sparse LiDAR depth (and seed points)."""
+    cam: Camera
+    image: np.ndarray
+    sparse_depth: np.ndarray
+    points: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    colors: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    stamp: float = 0.0
+
+
+class MapOptimizer:
+    """Device-resident map-optimisation iterations over a fixed keyframe set."""
+
+    def __init__(self, gmap: GaussianMap, keyframes, lrs: dict, lam: float = 0.2, xi: float = 0.005,
+                 adam: AdamState | None = None, headroom: float = 1.3, views=None):
+        self.g = as_device_map(gmap)
+        if len(self.g) == 0:
+            raise DataError("map not initialized")
+        self.dev = self.g.device
+        self.lam, self.xi = float(lam), float(xi)
+        self.views = views if views is not None else [
+            DeviceView(camera_from(kf.cam), kf.image, kf.sparse_depth, self.dev) for kf in keyframes]
+        cams = [v.cam for v in self.views]
+        self.W, self.H = int(cams[0].width), int(cams[0].height)
+        if any((int(c.width), int(c.height)) != (self.W, self.H) for c in cams):
+            raise DataError("all keyframes of one optimiser must share the image size")
+        self.adam = adam if adam is not None else AdamState()
+        self.adam.ensure(self.g)
+        self.lr = lr_columns(lrs, self.dev)
+        self.cur = torch.empty_like(self.views[0].buf)
+        # entry capacity from a dry binning pass over every keyframe
+        emax = 1
+        for v in self.views:
+            _, cnt = _bin_frame(self.g, v, True)
+            emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
+        self.headroom = headroom
+        self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.graph = None
+        self._ring = [torch.zeros(8, dtype=torch.int32).pin_memory() for _ in range(4)]
+        self._events = [None] * 4
+        self._steps = 0
+        self._grow = False
+
+    # -- one iteration: R/mapper.py:249-256 --------------------------------------------
+    def _launch(self) -> None:
+        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        call("gs_bin", f, 1, s)
+        call("gs_render_fwd", f, 1, s)
+        call("gs_loss", f, cur, self.lam, self.xi, s)
+        call("gs_render_bwd", f, s)
+        call("gs_chain_adam", f, self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
+             self.adam.t.data_ptr(), cur, self.lr.data_ptr(), s)
+        self.loss_acc += self.ws.loss[0:1]
+
+    def capture(self) -> None:
+        """Capture the launch sequence into a CUDA graph (replayed by step())."""
+        torch.cuda.current_stream().synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):  # capture records the launches; it executes nothing
+            self._launch()
+        self.graph = g
+
+    def step(self, k: int) -> None:
+        self._check()
+        self.cur.copy_(self.views[k].buf)
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+        slot = self._steps % 4
+        self._ring[slot].copy_(self.ws.counters[:8], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[slot] = ev
+        self._steps += 1
+
+    def _check(self) -> None:
+        """Look at the counters of the step before last (already finished in practice)."""
+        if self._steps < 2:
+            return
+        slot = (self._steps - 2) % 4
+        self._events[slot].synchronize()
+        cnt = self._ring[slot]
+        if int(cnt[_lib.CNT_OVERFLOW]):
+            raise DataError(f"entry capacity {self.ws.capacity} overflowed (E={int(cnt[_lib.CNT_ENTRIES])}); "
+                            "raise MapOptimizer headroom")
+        if int(cnt[_lib.CNT_ENTRIES]) > 0.9 * self.ws.capacity:
+            torch.cuda.current_stream().synchronize()
+            self.ws = Workspace(len(self.g), self.W, self.H, int(int(cnt[_lib.CNT_ENTRIES]) * self.headroom), self.dev)
+            if self.graph is not None:
+                self.capture()
+
+    PHASES = ("preprocess", "bin", "render_fwd", "loss", "render_bwd", "chain_adam")
+
+    def kernels_per_step(self) -> int:
+        """Kernels of ours launched by one iteration."""
+        tiles = self.ws.tiles_x * self.ws.tiles_y
+        tile_bits = max(1, (tiles - 1).bit_length())
+        tpasses = 1 if tile_bits <= 8 else (2 if tile_bits <= 16 else 3)
+        return 1 + (2 + 4 + 3 + 2 + tpasses + 1) + 1 + 4 + 2 + 1
+
+    def profile_step(self, k: int) -> dict:
+        """Eager iteration with CUDA events between the six C-ABI calls; returns ms per phase."""
+        self.cur.copy_(self.views[k].buf)
+        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(self.PHASES) + 1)]
+        ev[0].record()
+        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        ev[1].record()
+        call("gs_bin", f, 1, s)
+        ev[2].record()
+        call("gs_render_fwd", f, 1, s)
+        ev[3].record()
+        call("gs_loss", f, cur, self.lam, self.xi, s)
+        ev[4].record()
+        call("gs_render_bwd", f, s)
+        ev[5].record()
+        call("gs_chain_adam", f, self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
+             self.adam.t.data_ptr(), cur, self.lr.data_ptr(), s)
+        ev[6].record()
+        ev[6].synchronize()
+        return {p: ev[i].elapsed_time(ev[i + 1]) for i, p in enumerate(self.PHASES)}
+
+    # -- streaming keyframes from host memory (the e2e path) ---------------------------------
+    def attach_host_keyframes(self, keyframes) -> None:
+        """Keep keyframes in pinned host memory; step_host(k) uploads one per iteration."""
+        h, w = self.H, self.W
+        self._h_img = [torch.as_tensor(np.asarray(kf.image, dtype=np.float32)).reshape(h, w, 3).pin_memory()
+                       for kf in keyframes]
+        self._h_sd = [torch.as_tensor(np.asarray(kf.sparse_depth, dtype=np.float32)).reshape(h, w).pin_memory()
+                      for kf in keyframes]
+        self._d_img = torch.empty((h, w, 3), device=self.dev)
+        self._d_sd = torch.empty((h, w), device=self.dev)
+        self._d_idx = torch.empty(h * w, dtype=torch.int32, device=self.dev)
+        self._d_z = torch.empty(h * w, device=self.dev)
+        self._h_view = []
+        for kf in keyframes:
+            s = _lib.GsView()
+            s.cam = camera_from(kf.cam).struct()
+            s.target, s.lidar_idx, s.lidar_z = self._d_img.data_ptr(), self._d_idx.data_ptr(), self._d_z.data_ptr()
+            raw = bytes(memoryview(s).cast("B"))
+            self._h_view.append(torch.frombuffer(bytearray(raw), dtype=torch.uint8).pin_memory())
+        self._h_loss = torch.zeros(1024, dtype=torch.float64).pin_memory()
+        self.h2d_bytes = self._h_img[0].numel() * 4 + self._h_sd[0].numel() * 4 + self._h_view[0].numel()
+        self.d2h_bytes = 8
+
+    def step_host(self, k: int, slot: int) -> None:
+        """One iteration on host keyframe k: H2D image + sparse depth + view, device K-list
+        compaction, the iteration, and a D2H copy of the loss into pinned slot `slot`."""
+        self._check()
+        self._d_img.copy_(self._h_img[k], non_blocking=True)
+        self._d_sd.copy_(self._h_sd[k], non_blocking=True)
+        self.cur.copy_(self._h_view[k], non_blocking=True)
+        k_ptr = self.cur.data_ptr() + _lib.GsView.lidar_k.offset
+        call("gs_lidar_compact", self._d_sd.data_ptr(), self.W, self.H, self._d_idx.data_ptr(), self._d_z.data_ptr(),
+             k_ptr, stream_ptr())
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._launch()
+        self._h_loss[slot % 1024].copy_(self.ws.loss[0], non_blocking=True)
+        s = self._steps % 4
+        self._ring[s].copy_(self.ws.counters[:8], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[s] = ev
+        self._steps += 1
+
+    def loss_sum(self, reset: bool = True) -> float:
+        v = float(self.loss_acc.item())
+        if reset:
+            self.loss_acc.zero_()
+        return v
+
+    def counters(self) -> dict:
+        c = self.ws.counters[:8].cpu()
+        return {"active": int(c[0]), "entries": int(c[1]), "touched": int(c[2]), "overflow": int(c[3])}
+
+
+_ENGINES: dict = {}
+_ENGINES_LOCK = threading.Lock()
+
+
+def _engine_for(gmap, keyframes, adam, lrs, cfg) -> MapOptimizer:
+    key = (id(gmap), id(keyframes), len(keyframes), len(gmap), id(adam))
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(key)
+    if eng is None or eng.g is not gmap:
+        eng = MapOptimizer(gmap, keyframes, lrs, cfg.lam, cfg.xi, adam)
+        with _ENGINES_LOCK:
+            _ENGINES.clear()
+            _ENGINES[key] = eng
+    eng.lr = lr_columns(lrs, eng.dev)
+    eng.lam, eng.xi = float(cfg.lam), float(cfg.xi)
+    return eng
+
+
+def optimize_map(gmap, keyframes, cfg: MappingConfig, rng, adam: AdamState, lrs: dict,
+                 timing: dict | None = None) -> float:
+    """R/mapper.py:233-264: sample min(K, #kf) keyframes without replacement, shuffle, and run
+    one descent step (fwd -> loss -> bwd -> sparse Adam) on each; returns the mean loss."""
+    if len(gmap) == 0:
+        raise DataError("map not initialized")
+    m = min(cfg.k_keyframes, len(keyframes))
+    order = rng.choice(len(keyframes), size=m, replace=False)
+    rng.shuffle(order)
+    eng = _engine_for(gmap, keyframes, adam, lrs, cfg)
+    eng.loss_sum(reset=True)
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record()
+    for i in order:
+        eng.step(int(i))
+    end.record()
+    total = eng.loss_sum()
+    if timing is not None:
+        end.synchronize()
+        timing["iter"] = timing.get("iter", 0.0) + start.elapsed_time(end) / 1e3
+        timing["steps"] = timing.get("steps", 0) + m
+    return total / max(m, 1)
+
+
+# ---------------------------------------------------------------------------
+# map growth (R/mapper.py:69-107, 209-230) -- device versions of the keyframe helpers
+
+
+def project_points(points_w, cam: Camera):
+    """R/mapper.py:69-81 (torch): pixel coords, depths and an inside-image mask."""
+    cam = camera_from(cam)
+    dev = points_w.device
+    R = torch.as_tensor(np.asarray(cam.rot_cw), dtype=torch.float32, device=dev)
+    t = torch.as_tensor(np.asarray(cam.trans_cw), dtype=torch.float32, device=dev)
+    p = points_w @ R.T + t
+    z = p[:, 2]
+    front = z > NEAR_CLIP
+    zs = torch.where(front, z, torch.ones_like(z))
+    u = cam.fx * p[:, 0] / zs + cam.cx
+    v = cam.fy * p[:, 1] / zs + cam.cy
+    ui, vi = torch.round(u).long(), torch.round(v).long()
+    inside = front & (ui >= 0) & (ui < cam.width) & (vi >= 0) & (vi < cam.height)
+    return u, v, ui, vi, z, inside
+
+
+def init_map(gmap: GaussianMap, kf: Keyframe) -> int:
+    """R/mapper.py:209-215."""
+    if len(gmap):
+        raise DataError("map already initialized")
+    pts = torch.as_tensor(np.asarray(kf.points, dtype=np.float32), device=gmap.device)
+    cam = camera_from(kf.cam)
+    R = torch.as_tensor(np.asarray(cam.rot_cw), dtype=torch.float32, device=gmap.device)
+    depths = pts @ R[2] + float(np.asarray(cam.trans_cw)[2])
+    gmap.append(init_from_points(pts, kf.colors, depths, cam.fx, device=gmap.device))
+    return len(pts)
+
+
+def expand_map(gmap: GaussianMap, kf: Keyframe, tau: float) -> int:
+    """R/mapper.py:218-230: add Gaussians only where the rendered opacity is below tau."""
+    if len(gmap) == 0:
+        raise DataError("map not initialized")
+    opac = forward(gmap, kf.cam).opacity
+    pts = torch.as_tensor(np.asarray(kf.points, dtype=np.float32), device=gmap.device)
+    _, _, ui, vi, z, inside = project_points(pts, kf.cam)
+    fresh = inside.clone()
+    fresh[inside] = opac[vi[inside], ui[inside]] < tau
+    if not bool(fresh.any()):
+        return 0
+    cols = torch.as_tensor(np.asarray(kf.colors, dtype=np.float32), device=gmap.device)
+    gmap.append(init_from_points(pts[fresh], cols[fresh], z[fresh], camera_from(kf.cam).fx, device=gmap.device))
+    return int(fresh.sum())
+
+
+class Mapper:
+    """R/mapper.py:267-316: keyframe-driven map owner with copy-on-publish snapshots."""
+
+    def __init__(self, cfg: MappingConfig | None = None, seed: int = 0, device=None):
+        self.cfg = cfg or MappingConfig()
+        self.seed = seed
+        self.gmap = GaussianMap(device=device)
+        self.keyframes: list = []
+        self.adam = AdamState()
+        self.lrs = None
+        self.losses: list = []
+        self.timing: dict = {}
+        self._lock = threading.Lock()
+        self._published = self.gmap.snapshot()
+
+    def submit(self, kf: Keyframe) -> int:
+        if len(self.gmap) == 0:
+            added = init_map(self.gmap, kf)
+            pts = np.asarray(kf.points, dtype=np.float64)
+            extent = float(np.linalg.norm(pts - pts.mean(axis=0), axis=1).max()) if len(pts) else 1.0
+            self.lrs = default_lrs(max(extent, 1e-6))
+        else:
+            added = expand_map(self.gmap, kf, self.cfg.tau)
+        self.keyframes.append(kf)
+        rng = np.random.default_rng([self.seed, len(self.keyframes)])
+        self.losses.append(optimize_map(self.gmap, self.keyframes, self.cfg, rng, self.adam, self.lrs, self.timing))
+        with self._lock:
+            self._published = self.gmap.snapshot()
+        return added
+
+    def refine(self, rounds: int) -> None:
+        for k in range(rounds):
+            rng = np.random.default_rng([self.seed, 1 << 20, k])
+            self.losses.append(optimize_map(self.gmap, self.keyframes, self.cfg, rng, self.adam, self.lrs,
+                                            self.timing))
+        with self._lock:
+            self._published = self.gmap.snapshot()
+
+    def snapshot(self) -> GaussianMap:
+        with self._lock:
+            return self._published

@@ -1,0 +1,93 @@
+"""Keyframe-batch data parallelism over NCCL.
+
+Every rank holds a replica of the map and its Adam state.  Per step, a batch of keyframes is
+split across the ranks; each rank runs forward -> loss -> backward -> chain rule for its
+views, accumulating parameter-row gradients and a touched mask.  One NCCL allreduce sums the
+gradient rows; the touched mask rides in the rows' padding column 63 of the same buffer, so
+the union of touched sets costs no second collective (a touched Gaussian with zero gradient
+still steps: its moments decay, R/rasterizer.py:714-725).  Every rank then applies the same
+sparse Adam step, so the replicas stay bitwise identical.
+
+This is a deliberate, documented deviation from the reference's per-keyframe Adam
+(R/mapper.py:246-257): the batch oracle is sum of per-view gradients, union of touched,
+one sparse_adam_step.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from ._lib import GS_ROW, call
+from .errors import DataError
+from .gaussians import as_device_map, stream_ptr
+from .rasterizer import AdamState, DeviceView, Workspace, _bin_frame, camera_from, lr_columns
+
+TOUCH_COL = GS_ROW - 1  # padding column carrying the touched flag through the allreduce
+
+
+def allreduce_grads(rows: torch.Tensor, touched: torch.Tensor, group=None) -> None:
+    """Sum gradient rows across ranks and OR the touched masks, with one collective."""
+    if TOUCH_COL < _lib.GS_NPARAM:
+        raise DataError("no padding column for the touched flag")
+    rows[:, TOUCH_COL] = touched.to(rows.dtype)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(rows, op=dist.ReduceOp.SUM, group=group)
+    touched.copy_((rows[:, TOUCH_COL] > 0).to(touched.dtype))
+    rows[:, TOUCH_COL] = 0.0
+
+
+class BatchMapOptimizer:
+    """Batched (optionally data-parallel) map optimisation over this rank's keyframes."""
+
+    def __init__(self, gmap, keyframes, lrs: dict, lam: float = 0.2, xi: float = 0.005, group=None,
+                 adam: AdamState | None = None, headroom: float = 1.3):
+        self.g = as_device_map(gmap)
+        if len(self.g) == 0:
+            raise DataError("map not initialized")
+        self.dev = self.g.device
+        self.lam, self.xi, self.group = float(lam), float(xi), group
+        self.views = [DeviceView(camera_from(kf.cam), kf.image, kf.sparse_depth, self.dev) for kf in keyframes]
+        self.W, self.H = int(self.views[0].cam.width), int(self.views[0].cam.height)
+        self.adam = adam if adam is not None else AdamState()
+        self.adam.ensure(self.g)
+        self.lr = lr_columns(lrs, self.dev)
+        emax = 1
+        for v in self.views:
+            _, cnt = _bin_frame(self.g, v, True)
+            emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
+        self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
+        n = len(self.g)
+        self.grads = torch.zeros((n, GS_ROW), dtype=torch.float32, device=self.dev)
+        self.touched = torch.zeros(n, dtype=torch.uint8, device=self.dev)
+        self.cur = torch.empty_like(self.views[0].buf)
+        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+
+    def kernels_per_step(self, views: int | None = None) -> int:
+        tiles = self.ws.tiles_x * self.ws.tiles_y
+        tpasses = 1 if tiles <= 256 else (2 if tiles <= 65536 else 3)
+        per_view = 1 + (2 + 4 + 3 + 2 + tpasses + 1) + 1 + 4 + 2 + 1
+        return per_view * (views if views is not None else len(self.views)) + 2
+
+    def accumulate(self, k: int) -> None:
+        """forward -> loss -> backward -> chain rule of view k into (grads, touched)."""
+        self.cur.copy_(self.views[k].buf)
+        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        call("gs_bin", f, 1, s)
+        call("gs_render_fwd", f, 1, s)
+        call("gs_loss", f, cur, self.lam, self.xi, s)
+        call("gs_render_bwd", f, s)
+        call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
+        self.loss_acc += self.ws.loss[0:1]
+
+    def step(self, view_ids) -> None:
+        self.grads.zero_()
+        self.touched.zero_()
+        for k in view_ids:
+            self.accumulate(int(k))
+        allreduce_grads(self.grads, self.touched, self.group)
+        call("gs_adam", self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
+             self.adam.t.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), len(self.g),
+             self.lr.data_ptr(), stream_ptr())

@@ -1,0 +1,389 @@
+"""Drop-in mirror of R/rasterizer.py over the sm_100a kernels.
+
+Same entry points and argument meaning as the reference (`forward`, `backward`, `backward_2d`,
+`cull_tiles`, `sparse_adam_step`, `AdamState`, `default_lrs`, `Camera`, `RenderOutput`); arrays
+are torch CUDA tensors (numpy inputs are accepted and uploaded).  Each call runs on the
+current torch stream through the C ABI of include/gslic.h; per-view transient state lives in
+a `Workspace` owned by the returned RenderOutput, so concurrent renders (tracker thread vs
+mapper thread, R/cli.py:298-344) never share scratch memory.
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import GS_G2D, GS_ROW, call
+from .errors import DataError
+from .gaussians import (GaussianMap, NAMES, SLICES, as_device_map, camera_struct, default_device,
+                        stream_ptr, struct_to_device)
+
+TILE = 16
+CULL_ALPHA = 1.0 / 255.0
+EARLY_STOP_T = 1e-4
+BUCKET = 32  # the reference's checkpoint bucket; the B200 backward needs no checkpoints
+
+ADAM_BETA1 = 0.9
+ADAM_BETA2 = 0.999
+ADAM_EPS = 1e-15
+
+
+@dataclass
+class Camera:
+    """R/rasterizer.py:47-67 (world->camera pose, pixel centres at integers)."""
+    width: int
+    height: int
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    rot_cw: np.ndarray
+    trans_cw: np.ndarray
+
+    @property
+    def intrinsics(self):
+        return (self.fx, self.fy, self.cx, self.cy)
+
+    def center(self) -> np.ndarray:
+        return -np.asarray(self.rot_cw).T @ np.asarray(self.trans_cw)
+
+    def with_pose(self, rot_cw, trans_cw) -> "Camera":
+        return Camera(self.width, self.height, self.fx, self.fy, self.cx, self.cy,
+                      np.asarray(rot_cw, float), np.asarray(trans_cw, float))
+
+    def struct(self) -> _lib.GsCamera:
+        return camera_struct(self.rot_cw, self.trans_cw, self.intrinsics, self.width, self.height)
+
+
+def camera_from(c) -> Camera:
+    if isinstance(c, Camera):
+        return c
+    if isinstance(c, dict):
+        return Camera(c["width"], c["height"], c["fx"], c["fy"], c["cx"], c["cy"], c["rot_cw"], c["trans_cw"])
+    return Camera(c.width, c.height, c.fx, c.fy, c.cx, c.cy, np.asarray(c.rot_cw), np.asarray(c.trans_cw))
+
+
+@dataclass
+class RenderOutput:
+    """R/rasterizer.py:70-77."""
+    color: torch.Tensor
+    depth: torch.Tensor
+    opacity: torch.Tensor
+    transmittance: torch.Tensor
+    n_contrib: torch.Tensor
+    ctx: dict
+
+
+# ---------------------------------------------------------------------------
+# device-side view (camera + supervision) and workspace
+
+
+class DeviceView:
+    """A gs_view struct in device memory, plus the tensors it points at."""
+
+    def __init__(self, cam, target=None, sparse_depth=None, device=None):
+        cam = camera_from(cam)
+        self.cam = cam
+        self.device = torch.device(device) if device is not None else default_device()
+        s = _lib.GsView()
+        s.cam = cam.struct()
+        h, w = int(cam.height), int(cam.width)
+        self.target = None
+        if target is not None:
+            self.target = _f32(target, self.device).reshape(h, w, 3).contiguous()
+            s.target = self.target.data_ptr()
+        self.sparse = None
+        if sparse_depth is not None:
+            self.sparse = _f32(sparse_depth, self.device).reshape(h, w).contiguous()
+            self.lidar_idx = torch.empty(h * w, dtype=torch.int32, device=self.device)
+            self.lidar_z = torch.empty(h * w, dtype=torch.float32, device=self.device)
+            s.lidar_idx = self.lidar_idx.data_ptr()
+            s.lidar_z = self.lidar_z.data_ptr()
+        s.lidar_k = 0
+        self.buf = struct_to_device(s, self.device)
+        if self.sparse is not None:
+            k_ptr = self.buf.data_ptr() + _lib.GsView.lidar_k.offset
+            call("gs_lidar_compact", self.sparse.data_ptr(), w, h, self.lidar_idx.data_ptr(),
+                 self.lidar_z.data_ptr(), k_ptr, stream_ptr())
+
+    @property
+    def ptr(self) -> int:
+        return self.buf.data_ptr()
+
+
+def _f32(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        return x.to(device=device, dtype=torch.float32)
+    return torch.as_tensor(np.asarray(x, dtype=np.float32), device=device)
+
+
+_DT = {"f32": (torch.float32, 4), "i32": (torch.int32, 4), "u8": (torch.uint8, 1), "f64": (torch.float64, 8),
+       "u64": (torch.int64, 8)}
+
+
+class Workspace:
+    """One view's transient device state (gs_frame), carved from a single torch buffer."""
+
+    def __init__(self, n: int, width: int, height: int, capacity: int, device=None):
+        self.device = torch.device(device) if device is not None else default_device()
+        L = _lib.lib()
+        self.n, self.width, self.height, self.capacity = int(n), int(width), int(height), int(capacity)
+        size = int(L.gs_workspace_size(self.n, self.width, self.height, self.capacity))
+        self.buf = torch.empty(size + 256, dtype=torch.uint8, device=self.device)
+        base = self.buf.data_ptr()
+        self.base = (base + 255) & ~255
+        self.frame = _lib.GsFrame()
+        call("gs_frame_layout", self.n, self.width, self.height, self.capacity, self.base, size, self.frame)
+        self.fptr = _lib.ctypes.byref(self.frame)
+        self.tiles_x, self.tiles_y = self.frame.tiles_x, self.frame.tiles_y
+        h, w, n = self.height, self.width, max(self.n, 0)
+        self.color = self.view("color", "f32", (h, w, 3))
+        self.depth = self.view("depth", "f32", (h, w))
+        self.opacity = self.view("opacity", "f32", (h, w))
+        self.trans = self.view("trans", "f32", (h, w))
+        self.n_contrib = self.view("n_contrib", "i32", (h, w))
+        self.g_color = self.view("g_color", "f32", (h, w, 3))
+        self.g_depth = self.view("g_depth", "f32", (h, w))
+        self.g_opac = self.view("g_opac", "f32", (h, w))
+        self.splat2d = self.view("splat2d", "f32", (n, 12))
+        self.cov2d = self.view("cov2d", "f32", (n, 4))
+        self.valid = self.view("valid", "u8", (n,))
+        self.touched = self.view("touched", "u8", (n,))
+        self.g2d = self.view("g2d", "f32", (n, GS_G2D))
+        self.counters = self.view("counters", "i32", (2 * _lib.GS_CNT_SLOTS,))
+        self.entry_splat = self.view("entry_splat", "i32", (max(self.capacity, 1),))
+        self.tile_offsets = self.view("tile_offsets", "i32", (self.tiles_x * self.tiles_y + 1,))
+        self.loss = self.view("loss", "f64", (4,))
+
+    def view(self, field: str, kind: str, shape) -> torch.Tensor:
+        dtype, item = _DT[kind]
+        off = getattr(self.frame, field) - self.base + (self.base - self.buf.data_ptr())
+        nbytes = int(np.prod(shape)) * item
+        return self.buf[off:off + nbytes].view(dtype).view(*shape)
+
+
+_CAP_HINT: dict = {}
+_CAP_LOCK = threading.Lock()
+
+
+def _capacity_hint(n: int, w: int, h: int, cull: bool) -> int:
+    with _CAP_LOCK:
+        hint = _CAP_HINT.get((n, w, h, cull))
+    if hint:
+        return hint
+    if not cull:
+        return max(n * ((w + 15) // 16) * ((h + 15) // 16), 1024)
+    return max(8 * n, 1 << 16)
+
+
+def _remember_capacity(n, w, h, cull, entries):
+    with _CAP_LOCK:
+        _CAP_HINT[(n, w, h, cull)] = max(int(entries * 1.25) + 1024, 1 << 16)
+
+
+def _bin_frame(g: GaussianMap, view: DeviceView, cull: bool, ws: Workspace | None = None):
+    """preprocess + bin with an exact-capacity retry (one host sync: E is data dependent)."""
+    cam = view.cam
+    n, w, h = len(g), int(cam.width), int(cam.height)
+    cap = _capacity_hint(n, w, h, cull)
+    for _ in range(4):
+        if ws is None or ws.capacity < cap:
+            ws = Workspace(n, w, h, cap, g.device)
+        call("gs_preprocess", ws.fptr, g.data.data_ptr(), view.ptr, stream_ptr())
+        call("gs_bin", ws.fptr, int(bool(cull)), stream_ptr())
+        cnt = ws.counters[:8].cpu()
+        entries = int(cnt[_lib.CNT_ENTRIES])
+        if not int(cnt[_lib.CNT_OVERFLOW]):
+            _remember_capacity(n, w, h, cull, entries)
+            return ws, cnt
+        cap = int(entries * 1.25) + 1024
+    raise DataError("tile binning kept overflowing its entry capacity")
+
+
+def forward(gmap, cam, cull: bool = True, early_stop: bool = True) -> RenderOutput:
+    """R/rasterizer.py:442-484: render colour, depth (sum z w), opacity, transmittance, n_contrib."""
+    g = as_device_map(gmap)
+    cam = camera_from(cam)
+    view = DeviceView(cam, device=g.device)
+    ws, cnt = _bin_frame(g, view, cull)
+    call("gs_render_fwd", ws.fptr, int(bool(early_stop)), stream_ptr())
+    E = int(cnt[_lib.CNT_ENTRIES])
+    n = len(g)
+    s2 = ws.splat2d
+    proj = {"mean2d": s2[:, 0:2], "conic": s2[:, 2:5], "depth": s2[:, 6], "valid": ws.valid.bool(),
+            "cov2d": ws.cov2d[:, 0:3], "radius": ws.cov2d[:, 3]}
+    ctx = {"proj": proj, "opac": s2[:, 5], "colors": s2[:, 8:11], "entry_splat": ws.entry_splat[:E],
+           "tile_offsets": ws.tile_offsets, "tiles_x": ws.tiles_x, "tiles_y": ws.tiles_y, "cam": cam,
+           "workspace": ws, "view": view, "gmap": g, "n": n, "counters": cnt}
+    return RenderOutput(ws.color, ws.depth, ws.opacity, ws.trans, ws.n_contrib, ctx)
+
+
+def _load_image_grads(ws: Workspace, g_color_img, g_depth_img, g_opac_img):
+    dev = ws.device
+    for dst, src in ((ws.g_color, g_color_img), (ws.g_depth, g_depth_img), (ws.g_opac, g_opac_img)):
+        if src is None:
+            dst.zero_()
+        elif isinstance(src, torch.Tensor) and src.data_ptr() == dst.data_ptr():
+            continue
+        else:
+            dst.copy_(_f32(src, dev).reshape(dst.shape))
+
+
+def backward_2d(out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=None):
+    """R/rasterizer.py:502-540: (g_mean2d, g_conic, g_opacity, g_color, g_depth, touched)."""
+    ws: Workspace = out.ctx["workspace"]
+    _load_image_grads(ws, g_color_img, g_depth_img, g_opac_img)
+    call("gs_render_bwd", ws.fptr, stream_ptr())
+    touched = ws.touched.bool()
+    g2d = torch.where(touched[:, None], ws.g2d, torch.zeros((), device=ws.device))
+    return g2d[:, 0:2], g2d[:, 2:5], g2d[:, 5], g2d[:, 6:9], g2d[:, 9], touched
+
+
+def rows_to_grads(rows: torch.Tensor) -> dict:
+    n = rows.shape[0]
+    out = {}
+    for name in NAMES:
+        a, b = SLICES[name]
+        v = rows[:, a:b]
+        out[name] = v[:, 0] if name == "opacity_logit" else (v.reshape(n, 15, 3) if name == "sh_high" else v)
+    out["_rows"] = rows
+    return out
+
+
+def grads_to_rows(grads: dict, n: int, device) -> torch.Tensor:
+    if "_rows" in grads:
+        return grads["_rows"]
+    rows = torch.zeros((n, GS_ROW), dtype=torch.float32, device=device)
+    for name in NAMES:
+        a, b = SLICES[name]
+        rows[:, a:b] = _f32(grads[name], device).reshape(n, b - a)
+    return rows
+
+
+def backward(gmap, out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=None, with_pose: bool = False):
+    """R/rasterizer.py:543-556 -> (grads dict mirroring parameters(), touched, pose_grad)."""
+    if with_pose:
+        raise NotImplementedError("pose gradients (R/rasterizer.py:646-657) are a later row (SURVEY.md 8f)")
+    g = as_device_map(gmap)
+    ws: Workspace = out.ctx["workspace"]
+    view: DeviceView = out.ctx["view"]
+    _load_image_grads(ws, g_color_img, g_depth_img, g_opac_img)
+    call("gs_render_bwd", ws.fptr, stream_ptr())
+    n = len(g)
+    rows = torch.zeros((n, GS_ROW), dtype=torch.float32, device=g.device)
+    acc = torch.zeros(n, dtype=torch.uint8, device=g.device)
+    call("gs_chain", ws.fptr, g.data.data_ptr(), rows.data_ptr(), acc.data_ptr(), view.ptr, stream_ptr())
+    return rows_to_grads(rows), acc.bool(), None
+
+
+def pose_backward(gmap, out, g_color_img, g_depth_img=None, g_opac_img=None):
+    return backward(gmap, out, g_color_img, g_depth_img, g_opac_img, with_pose=True)[2]
+
+
+def cull_tiles(mean2d, conic, cov2d, opacity, depth, valid, width, height, cull=True):
+    """R/rasterizer.py:169-219 on externally supplied 2D splats.
+
+    cov2d may be (n, 2, 2), (n, 4) or (n, 3) = (c00, c01, c11).  Returns
+    (entry_splat, tile_offsets, tiles_x, tiles_y) as device tensors."""
+    dev = default_device()
+    m = _f32(mean2d, dev).reshape(-1, 2).contiguous()
+    n = len(m)
+    cv = _f32(cov2d, dev).reshape(n, -1)
+    if cv.shape[1] == 4:
+        cv = cv[:, [0, 1, 3]]
+    cv = cv.contiguous()
+    cn = _f32(conic, dev).reshape(n, 3).contiguous()
+    op = _f32(opacity, dev).reshape(n).contiguous()
+    dp = _f32(depth, dev).reshape(n).contiguous()
+    vd = torch.as_tensor(np.asarray(valid.cpu() if isinstance(valid, torch.Tensor) else valid, dtype=np.uint8),
+                         device=dev).contiguous()
+    cap = _capacity_hint(n, width, height, cull)
+    for _ in range(4):
+        ws = Workspace(n, width, height, cap, dev)
+        call("gs_pack_splats", ws.fptr, m.data_ptr(), cn.data_ptr(), cv.data_ptr(), op.data_ptr(), dp.data_ptr(),
+             vd.data_ptr(), None, stream_ptr())
+        call("gs_bin", ws.fptr, int(bool(cull)), stream_ptr())
+        cnt = ws.counters[:8].cpu()
+        E = int(cnt[_lib.CNT_ENTRIES])
+        if not int(cnt[_lib.CNT_OVERFLOW]):
+            _remember_capacity(n, width, height, cull, E)
+            return ws.entry_splat[:E].clone(), ws.tile_offsets.clone(), ws.tiles_x, ws.tiles_y
+        cap = int(E * 1.25) + 1024
+    raise DataError("tile binning kept overflowing its entry capacity")
+
+
+# ---------------------------------------------------------------------------
+# sparse Adam (R/rasterizer.py:674-725)
+
+
+def default_lrs(scene_extent: float) -> dict:
+    """R/rasterizer.py:679-681."""
+    return {"pos": 1.6e-4 * scene_extent, "sh_low": 2.5e-3, "sh_high": 1.25e-4,
+            "opacity_logit": 0.05, "log_scale": 5e-3, "quat": 1e-3}
+
+
+def lr_columns(lrs: dict, device) -> torch.Tensor:
+    col = torch.zeros(GS_ROW, dtype=torch.float32)
+    for name, (a, b) in SLICES.items():
+        col[a:b] = float(lrs[name])
+    return col.to(device)
+
+
+class AdamState:
+    """First/second moments (parameter rows) plus a per-splat int32 step counter."""
+
+    def __init__(self, device=None) -> None:
+        self.device = torch.device(device) if device is not None else None
+        self.m_rows = None
+        self.v_rows = None
+        self.t = None
+
+    def ensure(self, gmap) -> None:
+        g = as_device_map(gmap)
+        dev = g.device
+        n = len(g)
+        if self.t is None:
+            self.m_rows = torch.zeros((0, GS_ROW), device=dev)
+            self.v_rows = torch.zeros((0, GS_ROW), device=dev)
+            self.t = torch.zeros(0, dtype=torch.int32, device=dev)
+        if self.t.numel() < n:
+            grow = n - self.t.numel()
+            cap = max(n, 2 * self.t.numel())
+            for name in ("m_rows", "v_rows"):
+                old = getattr(self, name)
+                new = torch.zeros((cap, GS_ROW), device=dev)
+                new[:old.shape[0]] = old
+                setattr(self, name, new)
+            t = torch.zeros(cap, dtype=torch.int32, device=dev)
+            t[:self.t.numel()] = self.t
+            self.t = t[:n] if grow else t
+            self._cap_t = t
+        if self.t.numel() > n:
+            self.t = self.t[:n]
+
+    @property
+    def m(self) -> dict:
+        return rows_to_grads(self.m_rows[:self.t.numel()])
+
+    @property
+    def v(self) -> dict:
+        return rows_to_grads(self.v_rows[:self.t.numel()])
+
+
+def sparse_adam_step(gmap, grads: dict, touched, state: AdamState, lrs: dict) -> None:
+    """R/rasterizer.py:707-725: Adam restricted to touched splats, per-splat bias correction."""
+    g = as_device_map(gmap)
+    state.ensure(g)
+    n = len(g)
+    if n == 0:
+        return
+    rows = grads_to_rows(grads, n, g.device).contiguous()
+    tm = touched if isinstance(touched, torch.Tensor) else torch.as_tensor(np.asarray(touched))
+    tm = tm.to(device=g.device, dtype=torch.uint8).contiguous()
+    lr = lr_columns(lrs, g.device)
+    call("gs_adam", g.data.data_ptr(), state.m_rows.data_ptr(), state.v_rows.data_ptr(), state.t.data_ptr(),
+         rows.data_ptr(), tm.data_ptr(), n, lr.data_ptr(), stream_ptr())
