@@ -43,7 +43,8 @@ extern "C" {
 #define GS_ROW 64       /* floats per parameter row (59 used) */
 #define GS_NPARAM 59
 #define GS_TILE 16
-#define GS_G2D 12       /* floats per screen-space gradient row: mean2d 2, conic 3, opacity 1, color 3, depth 1, pad 2 */
+#define GS_SMALL_CAND 16 /* candidate tiles culled per thread; larger footprints go warp-wide */
+#define GS_G2D 12      /* floats per screen-space gradient row: mean2d 2, conic 3, opacity 1, color 3, depth 1, pad 2 */
 
 enum {
     GS_OK = 0,
@@ -61,6 +62,9 @@ enum {
     GS_CNT_TOUCHED = 2,  /* splats with >= 1 kept pair */
     GS_CNT_OVERFLOW = 3, /* nonzero when E exceeded entry_capacity (downstream kernels no-op) */
     GS_CNT_ENTRIES_EFF = 4, /* E, or 0 after an overflow (what the downstream kernels use) */
+    GS_CNT_BIG = 5,      /* Gaussians culled warp-cooperatively (many candidate tiles) */
+    GS_CNT_BIG_EMIT = 6, /* ... and emitted warp-cooperatively */
+    GS_CNT_BIG_BITS = 7, /* words of big_bits in use */
     GS_CNT_SLOTS = 16
 };
 
@@ -96,8 +100,13 @@ typedef struct gs_frame {
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
     float *g2d;              /* n x GS_G2D screen-space gradients (touched rows valid) */
-    uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles */
-    int32_t *counts;         /* n + 1: kept pairs per active Gaussian (depth order) -> offsets */
+    uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
+    int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
+    int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */
+    int32_t *big_list;       /* n: Gaussians with > GS_SMALL_CAND candidate tiles (warp-culled) */
+    int32_t *big_emit;       /* n: depth ranks of those Gaussians (warp-emitted) */
+    uint32_t *big_bits;      /* cull bitmaps of the large-footprint Gaussians (base in keep_bits) */
+    int64_t big_bits_words;  /* capacity of big_bits; overflowing Gaussians are re-culled at emit */
     /* sort buffers */
     uint64_t *keys_a, *keys_b; /* max(n, entry_capacity) */
     uint32_t *sort_hist;       /* 8 passes x 256 */
@@ -167,7 +176,8 @@ int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const 
             const uint8_t *touched, int64_t n, const float *lr_cols, void *stream);
 
 /* ---- helpers for the reference-shaped Python API ------------------------------------- */
-/* dense sparse_depth (H,W) -> K-list (idx, z); count written to *k_out (device int32). */
+/* dense sparse_depth (H,W) -> K-list (idx, z) in pixel order; count written to *k_out (device
+ * int32).  idx must hold H*W + ceil(H*W/1024) ints (the tail is scratch), z H*W floats. */
 int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_t height, int32_t *idx, float *z,
                      int32_t *k_out, void *stream);
 /* R/gaussians.py:180-215 full records: mu_cam (n,3) mean2d (n,2) cov2d (n,4) conic (n,3) depth (n)

@@ -38,7 +38,8 @@ __device__ __forceinline__ void quat_grad(const float q0[4], const float gR[9], 
     for (int k = 0; k < 4; k++) out[k] = (gq[k] - qh[k] * dot) / nrm;
 }
 
-// gradient of the scalar loss w.r.t. one parameter row (59 columns written to G)
+// gradient of the scalar loss w.r.t. one parameter row (59 columns written to G; every write
+// happens after the last read of p, so G may alias p)
 __device__ __forceinline__ void chain_row(const float *p, const float *g, const gs_camera &cam, float *G) {
     const float *Rc = cam.rot_cw;
     const float fx = cam.fx, fy = cam.fy;
@@ -93,8 +94,9 @@ __device__ __forceinline__ void chain_row(const float *p, const float *g, const 
 #pragma unroll
         for (int b = 0; b < 3; b++)
             gN[3 * a + b] = 2.0f * (gS[3 * a] * pr.R[b] + gS[3 * a + 1] * pr.R[3 + b] + gS[3 * a + 2] * pr.R[6 + b]) * pr.s[b];
+    float gls[3];
 #pragma unroll
-    for (int j = 0; j < 3; j++) G[3 + j] = (pr.R[j] * gN[j] + pr.R[3 + j] * gN[3 + j] + pr.R[6 + j] * gN[6 + j]) * pr.s[j];
+    for (int j = 0; j < 3; j++) gls[j] = (pr.R[j] * gN[j] + pr.R[3 + j] * gN[3 + j] + pr.R[6 + j] * gN[6 + j]) * pr.s[j];
     float gR[9];
 #pragma unroll
     for (int a = 0; a < 3; a++)
@@ -102,11 +104,9 @@ __device__ __forceinline__ void chain_row(const float *p, const float *g, const 
         for (int b = 0; b < 3; b++) gR[3 * a + b] = gN[3 * a + b] * pr.s[b];
     float gq[4];
     quat_grad(p + 6, gR, gq);
-#pragma unroll
-    for (int k = 0; k < 4; k++) G[6 + k] = gq[k];
     // opacity logit (R/rasterizer.py:629-630)
     const float o = 1.0f / (1.0f + expf(-p[10]));
-    G[10] = g[5] * o * (1.0f - o);
+    const float g_opl = g[5] * o * (1.0f - o);
     // SH colour incl. the view-direction dependence (R/rasterizer.py:633-644)
     const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
     float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
@@ -123,22 +123,28 @@ __device__ __forceinline__ void chain_row(const float *p, const float *g, const 
         const float pre = bs[0] * p[11 + c] + acc + 0.5f;
         gcol[c] = pre > 0.0f ? g[6 + c] : 0.0f;
     }
-#pragma unroll
-    for (int c = 0; c < 3; c++) G[11 + c] = bs[0] * gcol[c];
     float sk[16];
     sk[0] = p[11] * gcol[0] + p[12] * gcol[1] + p[13] * gcol[2];
 #pragma unroll
-    for (int k = 0; k < 15; k++) {
-#pragma unroll
-        for (int c = 0; c < 3; c++) G[14 + 3 * k + c] = bs[k + 1] * gcol[c];
-        sk[k + 1] = p[14 + 3 * k] * gcol[0] + p[15 + 3 * k] * gcol[1] + p[16 + 3 * k] * gcol[2];
-    }
+    for (int k = 0; k < 15; k++) sk[k + 1] = p[14 + 3 * k] * gcol[0] + p[15 + 3 * k] * gcol[1] + p[16 + 3 * k] * gcol[2];
     float gd[3];
     sh_basis_vjp(d0, d1, d2, sk, gd);
     const float dot = gd[0] * d0 + gd[1] * d1 + gd[2] * d2;
+    // every read of p is done: G may alias p from here on
+#pragma unroll
+    for (int c = 0; c < 3; c++) G[11 + c] = bs[0] * gcol[c];
+#pragma unroll
+    for (int k = 0; k < 15; k++)
+#pragma unroll
+        for (int c = 0; c < 3; c++) G[14 + 3 * k + c] = bs[k + 1] * gcol[c];
     G[0] = gpos[0] + (gd[0] - d0 * dot) / un;
     G[1] = gpos[1] + (gd[1] - d1 * dot) / un;
     G[2] = gpos[2] + (gd[2] - d2 * dot) / un;
+#pragma unroll
+    for (int j = 0; j < 3; j++) G[3 + j] = gls[j];
+#pragma unroll
+    for (int k = 0; k < 4; k++) G[6 + k] = gq[k];
+    G[10] = g_opl;
 }
 
 __device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float bc1, float bc2) {
@@ -154,10 +160,10 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
                                                            int32_t *__restrict__ at, const gs_view *__restrict__ view,
                                                            const float *__restrict__ lr_cols, int mode,
                                                            float *__restrict__ grads, uint8_t *__restrict__ touched_accum) {
-    extern __shared__ __align__(16) float ca_smem[];
-    float(*srow)[32][RP] = reinterpret_cast<float(*)[32][RP]>(ca_smem);
-    float(*sgr)[32][RP] = reinterpret_cast<float(*)[32][RP]>(ca_smem + CA_WARPS * 32 * RP);
-    float(*sbc)[32][2] = reinterpret_cast<float(*)[32][2]>(ca_smem + 2 * CA_WARPS * 32 * RP);
+    // one 32 x 65 staging tile per warp: parameter rows in, gradient rows out (in place)
+    __shared__ float srow[CA_WARPS][32][RP];
+    __shared__ float sbc[CA_WARPS][32][2];
+    float(*sgr)[32][RP] = srow;
     __shared__ gs_camera scam;
     if (threadIdx.x == 0) scam = view->cam;
     __syncthreads();
@@ -205,18 +211,19 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         const int64_t off = (int64_t)gg * GS_ROW + 4 * c4;
         const float *G = &sgr[warp][r][4 * c4];
         if (mode == 0) {
-            const float *P = &srow[warp][r][4 * c4];
+            // parameters re-read from global (just staged: an L2 hit); the smem tile holds G
+            const float4 P = *reinterpret_cast<const float4 *>(params + off);
             const float bc1 = sbc[warp][r][0], bc2 = sbc[warp][r][1];
             float4 m4 = *reinterpret_cast<const float4 *>(am + off);
             float4 v4 = *reinterpret_cast<const float4 *>(av + off);
             const float4 lr = *reinterpret_cast<const float4 *>(lr_cols + 4 * c4);
             float4 p4;
-            p4.x = adam_one(P[0], m4.x, v4.x, G[0], lr.x, bc1, bc2);
-            p4.y = adam_one(P[1], m4.y, v4.y, G[1], lr.y, bc1, bc2);
-            p4.z = adam_one(P[2], m4.z, v4.z, G[2], lr.z, bc1, bc2);
-            p4.w = adam_one(P[3], m4.w, v4.w, G[3], lr.w, bc1, bc2);
-            if (c4 == 14) p4.w = P[3];  // column 59 is padding
-            if (c4 == 15) p4 = make_float4(P[0], P[1], P[2], P[3]);
+            p4.x = adam_one(P.x, m4.x, v4.x, G[0], lr.x, bc1, bc2);
+            p4.y = adam_one(P.y, m4.y, v4.y, G[1], lr.y, bc1, bc2);
+            p4.z = adam_one(P.z, m4.z, v4.z, G[2], lr.z, bc1, bc2);
+            p4.w = adam_one(P.w, m4.w, v4.w, G[3], lr.w, bc1, bc2);
+            if (c4 == 14) p4.w = P.w;  // column 59 is padding
+            if (c4 == 15) p4 = P;
             *reinterpret_cast<float4 *>(am + off) = m4;
             *reinterpret_cast<float4 *>(av + off) = v4;
             *reinterpret_cast<float4 *>(params + off) = p4;
@@ -275,8 +282,7 @@ static int launch_chain(const gs_frame *f, float *params, float *m, float *v, in
     if (f->n == 0) return GS_OK;
     const int64_t warps = (f->n + 31) / 32;
     const unsigned blocks = (unsigned)((warps + CA_WARPS - 1) / CA_WARPS);
-    const size_t smem = sizeof(float) * (2 * CA_WARPS * 32 * RP + CA_WARPS * 32 * 2);
-    chain_kernel<<<blocks, CA_THREADS, smem, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads, acc);
+    chain_kernel<<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads, acc);
     return check_launch("chain_kernel");
 }
 
@@ -313,7 +319,7 @@ extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *ada
 
 namespace gs {
 void init_chain_attrs() {
-    const size_t smem = sizeof(float) * (2 * CA_WARPS * 32 * RP + CA_WARPS * 32 * 2);
-    cudaFuncSetAttribute(chain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // static shared memory only (33 KB per 4-warp CTA); nothing to opt in
+    cudaFuncSetAttribute(chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 }  // namespace gs

@@ -30,6 +30,7 @@ int check_launch(const char *what) {
 int64_t loss_parts_needed(int32_t width, int32_t height);  // loss.cu
 void init_loss_attrs();                                     // loss.cu
 void init_chain_attrs();                                    // adam.cu
+void init_binning_attrs();                                  // binning.cu
 
 // kernel attributes (dynamic shared-memory opt-in) are set once per process, outside any
 // stream capture, the first time a workspace is laid out
@@ -38,6 +39,7 @@ static void init_attrs_once() {
     std::call_once(flag, [] {
         init_loss_attrs();
         init_chain_attrs();
+        init_binning_attrs();
     });
 }
 
@@ -73,7 +75,12 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.touched_list = c.take<int32_t>(nn);
     f.g2d = c.take<float>(GS_G2D * nn);
     f.keep_bits = c.take<uint64_t>(nn);
+    f.kept = c.take<int32_t>(nn);
     f.counts = c.take<int32_t>(nn + 1);
+    f.big_list = c.take<int32_t>(nn);
+    f.big_emit = c.take<int32_t>(nn);
+    f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
+    f.big_bits = c.take<uint32_t>(f.big_bits_words);
     f.keys_a = c.take<uint64_t>(keys);
     f.keys_b = c.take<uint64_t>(keys);
     f.sort_hist = c.take<uint32_t>(8 * 256);

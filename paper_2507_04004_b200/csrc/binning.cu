@@ -33,24 +33,35 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 
 // ---------------------------------------------------------------------------
 // digit histograms of all requested passes in one read (filter: drop inactive words)
-__global__ void __launch_bounds__(256) radix_hist_kernel(const uint64_t *__restrict__ keys, int64_t n_host,
+template <typename K>
+__device__ __forceinline__ bool inactive_key(K k, int filter) {
+    return filter && (uint64_t)k >> 32 == 0xffffffffull;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) radix_hist_kernel(const K *__restrict__ keys, int64_t n_host,
                                                          const int32_t *__restrict__ n_dev, int shift0, int npasses,
                                                          uint32_t *__restrict__ hist, int filter,
                                                          int32_t *__restrict__ active_out) {
-    __shared__ uint32_t sh[4][256];
-    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x) (&sh[0][0])[k] = 0;
+    // per-warp privatised sub-histograms cut shared-atomic contention on skewed digits
+    __shared__ uint32_t sh[4][4][256];
+    for (int k = threadIdx.x; k < 16 * 256; k += blockDim.x) (&sh[0][0][0])[k] = 0;
     __syncthreads();
+    const int sub = (threadIdx.x >> 5) & 3;
     const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
     uint32_t local_active = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        uint64_t k = keys[i];
-        if (filter && (k >> 32) == 0xffffffffull) continue;
+        const K k = keys[i];
+        if (inactive_key(k, filter)) continue;
         local_active++;
-        for (int p = 0; p < npasses; p++) atomicAdd(&sh[p][(k >> (shift0 + 8 * p)) & 255u], 1u);
+        for (int p = 0; p < npasses; p++) atomicAdd(&sh[sub][p][(uint32_t)(k >> (shift0 + 8 * p)) & 255u], 1u);
     }
     __syncthreads();
+    for (int k = threadIdx.x; k < 4 * 256; k += blockDim.x)
+        (&sh[0][0][0])[k] += (&sh[1][0][0])[k] + (&sh[2][0][0])[k] + (&sh[3][0][0])[k];
+    __syncthreads();
     for (int k = threadIdx.x; k < npasses * 256; k += blockDim.x) {
-        uint32_t v = (&sh[0][0])[k];
+        uint32_t v = (&sh[0][0][0])[k];
         if (v) atomicAdd(&hist[k], v);
     }
     if (filter && active_out) {
@@ -78,7 +89,8 @@ __global__ void radix_bins_kernel(uint32_t *hist) {
 // ---------------------------------------------------------------------------
 // one onesweep pass: stable counting-sort of a 4096-key tile by one 8-bit digit, decoupled
 // look-back across tiles for the per-digit global offsets, scatter through shared memory.
-__global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__restrict__ in, uint64_t *__restrict__ out,
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const K *__restrict__ in, K *__restrict__ out,
                                                               int64_t n_host, const int32_t *__restrict__ n_dev,
                                                               int shift, const uint32_t *__restrict__ bins,
                                                               uint32_t *status, int32_t *ticket, int filter) {
@@ -87,7 +99,7 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__
     __shared__ uint32_t s_start[256];
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_scan[WARPS];
-    __shared__ uint64_t s_keys[RS_TILE];
+    __shared__ K s_keys[RS_TILE];
     __shared__ int s_tile;
     __shared__ uint32_t s_total;
 
@@ -102,15 +114,15 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__
     const int64_t wbase = tbase + (int64_t)warp * 32 * RS_ITEMS;
     const unsigned ltmask = lanemask_lt();
 
-    uint64_t key[RS_ITEMS];
+    K key[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
     bool ok[RS_ITEMS];
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
         int64_t idx = wbase + i * 32 + lane;
         ok[i] = idx < n;
-        key[i] = ok[i] ? in[idx] : 0ull;
-        if (filter && ok[i] && (key[i] >> 32) == 0xffffffffull) ok[i] = false;
+        key[i] = ok[i] ? in[idx] : (K)0;
+        if (ok[i] && inactive_key(key[i], filter)) ok[i] = false;
     }
     // warp-level stable ranking: items in order, lanes in order
 #pragma unroll
@@ -181,7 +193,7 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__
     __syncthreads();
     const uint32_t total = s_total;
     for (uint32_t j = threadIdx.x; j < total; j += RS_THREADS) {
-        uint64_t k = s_keys[j];
+        const K k = s_keys[j];
         const uint32_t d = (uint32_t)(k >> shift) & 255u;
         out[s_base[d] + j] = k;
     }
@@ -192,7 +204,9 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const uint64_t *__
 constexpr int SC_ITEMS = 16;
 constexpr int SC_TILE = RS_THREADS * SC_ITEMS;
 
-__global__ void __launch_bounds__(RS_THREADS) scan_kernel(int32_t *data, int64_t n_host, const int32_t *n_dev,
+__global__ void __launch_bounds__(RS_THREADS) scan_kernel(const int32_t *__restrict__ vals,
+                                                          const uint64_t *__restrict__ perm, int32_t *data,
+                                                          int64_t n_host, const int32_t *n_dev,
                                                           uint32_t *status, int32_t *ticket, int32_t *total_out,
                                                           int64_t capacity, int32_t *overflow, int32_t *eff_out) {
     __shared__ int s_tile;
@@ -210,7 +224,8 @@ __global__ void __launch_bounds__(RS_THREADS) scan_kernel(int32_t *data, int64_t
     const int64_t mybase = tbase + (int64_t)threadIdx.x * SC_ITEMS;
 #pragma unroll
     for (int i = 0; i < SC_ITEMS; i++) {
-        v[i] = (mybase + i < n) ? (uint32_t)data[mybase + i] : 0u;
+        // value of rank mybase+i: kept count of the Gaussian at that depth rank
+        v[i] = (mybase + i < n) ? (uint32_t)vals[(uint32_t)perm[mybase + i]] : 0u;
         sum += v[i];
     }
     uint32_t x = sum;
@@ -261,126 +276,160 @@ __global__ void __launch_bounds__(RS_THREADS) scan_kernel(int32_t *data, int64_t
 }
 
 // ---------------------------------------------------------------------------
-// count (and cache the first 64 cull bits) of kept tiles per active Gaussian, depth order.
-// One warp per Gaussian; lanes stride over its candidate tiles.
-__global__ void __launch_bounds__(256) count_kernel(gs_frame f, const uint64_t *__restrict__ sorted, int cull) {
-    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t n_active = f.counters[GS_CNT_ACTIVE];
-    if (k >= n_active) return;
-    const uint32_t g = (uint32_t)sorted[k];
-    const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-    const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
-    int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
-    if (!cull) r = make_int4(0, f.tiles_x - 1, 0, f.tiles_y - 1);
-    const int nx = r.y - r.x + 1, ny = r.w - r.z + 1;
-    const int ncand = nx * ny;
-    uint32_t count = 0;
-    uint64_t bits = 0;
-    for (int c0 = 0; c0 < ncand; c0 += 32) {
-        const int c = c0 + lane;
-        bool keep = false;
-        if (c < ncand) {
-            if (!cull) keep = true;
-            else {
-                const int tx = r.x + c % nx, ty = r.z + c / nx;
-                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
-            }
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        count += __popc(b);
-        if (c0 == 0) bits |= (uint64_t)b;
-        else if (c0 == 32) bits |= (uint64_t)b << 32;
-    }
-    if (lane == 0) {
-        f.counts[k] = (int32_t)count;
-        f.keep_bits[k] = bits;
-        if (count) {
-            f.touched[g] = 1;
-            const int32_t slot = atomicAdd(&f.counters[GS_CNT_TOUCHED], 1);
-            f.touched_list[slot] = (int32_t)g;
-        }
-    }
+// emit kept pairs as (tile << 32 | id) at the scanned offsets, one thread per touched
+// Gaussian in depth order.  The cull bits of the first 64 candidates come from preprocess;
+// candidates beyond 64 are re-culled here (same strict decision function).
+// entry word: 64-bit (tile << 32 | id), or 32-bit (tile << rank_bits | depth rank) when both fit
+__device__ __forceinline__ void put_entry(void *out, int64_t pos, int rank_bits, int tile, uint32_t g, int64_t k) {
+    if (rank_bits) reinterpret_cast<uint32_t *>(out)[pos] = ((uint32_t)tile << rank_bits) | (uint32_t)k;
+    else reinterpret_cast<uint64_t *>(out)[pos] = ((uint64_t)(uint32_t)tile << 32) | (uint64_t)g;
 }
 
-// emit kept pairs as (tile << 32 | id) at the scanned offsets (depth order)
-__global__ void __launch_bounds__(256) emit_kernel(gs_frame f, const uint64_t *__restrict__ sorted,
-                                                   uint64_t *__restrict__ out, int cull) {
-    const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t n_active = f.counters[GS_CNT_ACTIVE];
-    if (k >= n_active || f.counters[GS_CNT_OVERFLOW]) return;
+__global__ void __launch_bounds__(256) emit_kernel(gs_frame f, const uint64_t *__restrict__ sorted, void *out,
+                                                   int cull, int rank_bits) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_sorted = f.counters[GS_CNT_ACTIVE];
+    if (k >= n_sorted || f.counters[GS_CNT_OVERFLOW]) return;
     const uint32_t g = (uint32_t)sorted[k];
     int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
     if (!cull) r = make_int4(0, f.tiles_x - 1, 0, f.tiles_y - 1);
-    const int nx = r.y - r.x + 1, ny = r.w - r.z + 1;
-    const int ncand = nx * ny;
-    const uint64_t bits = f.keep_bits[k];
+    const int nx = r.y - r.x + 1;
+    const int ncand = nx * (r.w - r.z + 1);
+    if (cull && ncand > GS_SMALL_CAND) {  // large footprint: emitted warp-wide by emit_big_kernel
+        f.big_emit[atomicAdd(&f.counters[GS_CNT_BIG_EMIT], 1)] = (int32_t)k;
+        return;
+    }
+    const uint64_t bits = f.keep_bits[g];
     int64_t off = f.counts[k];
-    float4 s0, s1;
-    if (ncand > 64) {
-        s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-        s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
-    }
-    for (int c0 = 0; c0 < ncand; c0 += 32) {
-        const int c = c0 + lane;
-        bool keep = false;
+    for (int c = 0; c < ncand; c++) {
         const int tx = r.x + c % nx, ty = r.z + c / nx;
-        if (c < ncand) {
-            if (!cull || c < 64) keep = !cull ? true : ((bits >> c) & 1ull);
-            else {
-                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
-            }
-        }
-        const unsigned b = __ballot_sync(0xffffffffu, keep);
-        if (keep) {
-            const int64_t pos = off + __popc(b & lanemask_lt());
-            out[pos] = ((uint64_t)(uint32_t)(ty * f.tiles_x + tx) << 32) | (uint64_t)g;
-        }
-        off += __popc(b);
+        if (!cull || ((bits >> c) & 1ull)) put_entry(out, off++, rank_bits, ty * f.tiles_x + tx, g, k);
     }
 }
 
-// tile_offsets[t] = first entry with tile >= t; entry_splat[e] = low word
-__global__ void ranges_kernel(gs_frame f, const uint64_t *__restrict__ sorted) {
+// warp per large-footprint Gaussian: lanes stride over candidates; ballot prefix gives the
+// in-order slot (candidates in ty-major order, as the thread path writes them)
+__global__ void __launch_bounds__(256) emit_big_kernel(gs_frame f, const uint64_t *__restrict__ sorted, void *out,
+                                                       int rank_bits) {
+    // one CTA per large-footprint Gaussian; 256 candidates per round, block-wide ordered slots
+    __shared__ int s_warp[8];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (f.counters[GS_CNT_OVERFLOW]) return;
+    const int64_t nb = f.counters[GS_CNT_BIG_EMIT];
+    const unsigned ltmask = lanemask_lt();
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t k = f.big_emit[b];
+        const uint32_t g = (uint32_t)sorted[k];
+        const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+        const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+        const int64_t base = (int64_t)f.keep_bits[g];  // cull bitmap from cull_big_kernel (-1: none)
+        int64_t off = f.counts[k];
+        for (int c0 = 0; c0 < ncand; c0 += 256) {
+            const int c = c0 + threadIdx.x;
+            const int tx = r.x + c % nx, ty = r.z + c / nx;
+            bool keep = false;
+            if (c < ncand) {
+                if (base >= 0) keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
+                else {
+                    const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                    const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                    keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                }
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0) s_warp[warp] = __popc(bal);
+            __syncthreads();
+            int before = 0, total = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                const int v = s_warp[w];
+                before += w < warp ? v : 0;
+                total += v;
+            }
+            if (keep) put_entry(out, off + before + __popc(bal & ltmask), rank_bits, ty * f.tiles_x + tx, g, k);
+            off += total;
+            __syncthreads();
+        }
+    }
+}
+
+// tile_offsets[t] = first entry with tile >= t; entry_splat[e] = the entry's Gaussian id
+// (64-bit words carry it; 32-bit words carry the depth rank, mapped through depth_sorted)
+template <typename K>
+__global__ void ranges_kernel(gs_frame f, const K *__restrict__ sorted, int rank_bits,
+                              const uint64_t *__restrict__ depth_sorted) {
     const int64_t E = f.counters[GS_CNT_ENTRIES_EFF];
     const int32_t T = f.tiles_x * f.tiles_y;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int tshift = rank_bits ? rank_bits : 32;
     if (E == 0) {
         for (int64_t t = e; t <= T; t += (int64_t)gridDim.x * blockDim.x) f.tile_offsets[t] = 0;
         return;
     }
     for (int64_t i = e; i < E; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t w = sorted[i];
-        const int32_t tile = (int32_t)(w >> 32);
-        f.entry_splat[i] = (int32_t)(uint32_t)w;
-        const int32_t prev = i == 0 ? -1 : (int32_t)(sorted[i - 1] >> 32);
+        const K w = sorted[i];
+        const int32_t tile = (int32_t)((uint64_t)w >> tshift);
+        f.entry_splat[i] = rank_bits ? (int32_t)(uint32_t)depth_sorted[(uint32_t)w & ((1u << rank_bits) - 1u)]
+                                     : (int32_t)(uint32_t)w;
+        const int32_t prev = i == 0 ? -1 : (int32_t)((uint64_t)sorted[i - 1] >> tshift);
         for (int32_t t = prev + 1; t <= tile; t++) f.tile_offsets[t] = (int32_t)i;
         if (i == E - 1)
             for (int32_t t = tile + 1; t <= T; t++) f.tile_offsets[t] = (int32_t)E;
     }
 }
 
-// cull=False keys: every valid Gaussian is active (R/rasterizer.py:195-199)
-__global__ void keys_nocull_kernel(gs_frame f) {
+// cull=False: every valid Gaussian lands in every tile (R/rasterizer.py:195-199)
+__global__ void nocull_kernel(gs_frame f) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= f.n) return;
-    const float d = f.splat2d[12 * i + 6];
-    f.keys_a[i] = f.valid[i] ? (((uint64_t)__float_as_uint(d) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
+    bool v = false;
+    if (i < f.n) {
+        v = f.valid[i] != 0;
+        const float d = f.splat2d[12 * i + 6];
+        f.keys_a[i] = v ? (((uint64_t)__float_as_uint(d) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
+        f.kept[i] = v ? f.tiles_x * f.tiles_y : 0;
+        f.touched[i] = v;
+    }
+    warp_append(v, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
 }
 
-static int sort_pass(const gs_frame *f, const uint64_t *in, uint64_t *out, int64_t n_host, const int32_t *n_dev,
-                     int shift, const uint32_t *bins, int pass_slot, int filter, cudaStream_t st) {
+template <typename K>
+static int sort_pass(const gs_frame *f, const K *in, K *out, int64_t n_host, const int32_t *n_dev, int shift,
+                     const uint32_t *bins, int pass_slot, int filter, cudaStream_t st) {
     const int64_t tiles = (n_host + RS_TILE - 1) / RS_TILE;
     if (tiles == 0) return GS_OK;
     uint32_t *status = f->sort_status + (int64_t)pass_slot * (f->status_words / 8);
-    onesweep_kernel<<<(unsigned)tiles, RS_THREADS, 0, st>>>(in, out, n_host, n_dev, shift, bins, status,
-                                                             f->counters + GS_CNT_TICKET0 + pass_slot, filter);
+    onesweep_kernel<K><<<(unsigned)tiles, RS_THREADS, 0, st>>>(in, out, n_host, n_dev, shift, bins, status,
+                                                                f->counters + GS_CNT_TICKET0 + pass_slot, filter);
     return check_launch("onesweep_kernel");
+}
+
+// stable LSD sort of the entry words on the tile field; returns the buffer holding the result
+template <typename K>
+static int tile_sort(const gs_frame *f, K *a, K *b, int shift0, int tpasses, cudaStream_t st, K **result) {
+    const int32_t *n_ent = f->counters + GS_CNT_ENTRIES_EFF;
+    const int64_t cap = f->entry_capacity;
+    radix_hist_kernel<K><<<4 * 148, 256, 0, st>>>(a, cap, n_ent, shift0, tpasses, f->sort_hist + 4 * 256, 0, nullptr);
+    int rc = check_launch("radix_hist_kernel");
+    if (rc) return rc;
+    radix_bins_kernel<<<tpasses, 256, 0, st>>>(f->sort_hist + 4 * 256);
+    K *src = a, *dst = b;
+    for (int p = 0; p < tpasses; p++) {
+        if ((rc = sort_pass<K>(f, src, dst, cap, n_ent, shift0 + 8 * p, f->sort_hist + (4 + p) * 256, 4 + p, 0, st)))
+            return rc;
+        K *tmp = src;
+        src = dst;
+        dst = tmp;
+    }
+    *result = src;
+    return GS_OK;
+}
+
+void init_binning_attrs() {
+    // the onesweep tiles want the full shared-memory carveout (occupancy is smem-limited)
+    cudaFuncSetAttribute(onesweep_kernel<uint64_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(onesweep_kernel<uint32_t>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 }  // namespace gs
@@ -392,63 +441,65 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     const int64_t n = f->n;
     const int32_t T = f->tiles_x * f->tiles_y;
     int rc;
-    // reset counters, histograms and look-back state
-    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, st);
+    // reset the binning counters (the touched count/list belong to preprocess), histograms and
+    // look-back state
+    cudaMemsetAsync(f->counters + GS_CNT_ACTIVE, 0, sizeof(int32_t) * 2, st);
+    cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * (2 * GS_CNT_SLOTS - GS_CNT_OVERFLOW), st);
     cudaMemsetAsync(f->sort_hist, 0, sizeof(uint32_t) * 8 * 256, st);
     cudaMemsetAsync(f->sort_status, 0, sizeof(uint32_t) * f->status_words, st);
     cudaMemsetAsync(f->scan_status, 0, sizeof(uint32_t) * f->scan_words, st);
     if (n == 0) {
-        ranges_kernel<<<1, 256, 0, st>>>(*f, f->keys_b);
+        ranges_kernel<uint64_t><<<1, 256, 0, st>>>(*f, f->keys_b, 0, nullptr);
         return check_launch("ranges_kernel");
     }
     if (!cull) {
-        keys_nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
-        if ((rc = check_launch("keys_nocull_kernel"))) return rc;
+        cudaMemsetAsync(f->counters + GS_CNT_TOUCHED, 0, sizeof(int32_t), st);
+        nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
+        if ((rc = check_launch("nocull_kernel"))) return rc;
     }
     const int hist_blocks = 4 * 148;
-    // 1) depth sort of the active Gaussians (4 passes over the 32 depth bits, filtered first pass)
-    radix_hist_kernel<<<hist_blocks, 256, 0, st>>>(f->keys_a, n, nullptr, 32, 4, f->sort_hist, 1,
+    // 1) depth sort of the touched Gaussians (4 passes over the 32 depth bits, the first pass
+    //    drops untouched ones)
+    radix_hist_kernel<uint64_t><<<hist_blocks, 256, 0, st>>>(f->keys_a, n, nullptr, 32, 4, f->sort_hist, 1,
                                                    f->counters + GS_CNT_ACTIVE);
     if ((rc = check_launch("radix_hist_kernel"))) return rc;
-    // tile-sort histograms are computed after emit; bins for passes 0-3 now
     radix_bins_kernel<<<4, 256, 0, st>>>(f->sort_hist);
     const int32_t *n_act = f->counters + GS_CNT_ACTIVE;
     if ((rc = sort_pass(f, f->keys_a, f->keys_b, n, nullptr, 32, f->sort_hist + 0 * 256, 0, 1, st))) return rc;
     if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 40, f->sort_hist + 1 * 256, 1, 0, st))) return rc;
     if ((rc = sort_pass(f, f->keys_a, f->keys_b, n, n_act, 48, f->sort_hist + 2 * 256, 2, 0, st))) return rc;
     if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 56, f->sort_hist + 3 * 256, 3, 0, st))) return rc;
-    // 2) exact cull counts in depth order, scan, emit
-    const unsigned warp_blocks = (unsigned)((n * 32 + 255) / 256);
-    count_kernel<<<warp_blocks, 256, 0, st>>>(*f, f->keys_a, cull);
-    if ((rc = check_launch("count_kernel"))) return rc;
+    // 2) entry offsets: exclusive scan of the kept counts in depth order, then emit
     {
         const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
         scan_kernel<<<(unsigned)(tiles > 0 ? tiles : 1), RS_THREADS, 0, st>>>(
-            f->counts, n, n_act, (uint32_t *)f->scan_status, f->counters + GS_CNT_TICKET0 + 7,
+            f->kept, f->keys_a, f->counts, n, n_act, (uint32_t *)f->scan_status, f->counters + GS_CNT_TICKET0 + 7,
             f->counters + GS_CNT_ENTRIES, f->entry_capacity, f->counters + GS_CNT_OVERFLOW,
             f->counters + GS_CNT_ENTRIES_EFF);
         if ((rc = check_launch("scan_kernel"))) return rc;
     }
-    emit_kernel<<<warp_blocks, 256, 0, st>>>(*f, f->keys_a, f->keys_b, cull);
-    if ((rc = check_launch("emit_kernel"))) return rc;
-    // 3) stable sort of the entries by tile id (bits 32.. of the word)
-    int tile_bits = 0;
+    // entry words: 32-bit (tile << rank_bits | depth rank) when tile and rank bits fit, so the
+    // tile sort moves half the bytes; 64-bit (tile << 32 | id) otherwise
+    int tile_bits = 0, rank_bits = 0;
     while ((1 << tile_bits) < T) tile_bits++;
+    while ((int64_t(1) << rank_bits) < n) rank_bits++;
+    if (rank_bits == 0) rank_bits = 1;
+    const bool compact = tile_bits + rank_bits <= 32;
     const int tpasses = tile_bits <= 8 ? 1 : (tile_bits <= 16 ? 2 : 3);
-    const int32_t *n_ent = f->counters + GS_CNT_ENTRIES_EFF;
-    const int64_t cap = f->entry_capacity;
-    radix_hist_kernel<<<hist_blocks, 256, 0, st>>>(f->keys_b, cap, n_ent, 32, tpasses, f->sort_hist + 4 * 256, 0,
-                                                   nullptr);
-    if ((rc = check_launch("radix_hist_kernel"))) return rc;
-    radix_bins_kernel<<<tpasses, 256, 0, st>>>(f->sort_hist + 4 * 256);
-    uint64_t *src = f->keys_b, *dst = f->keys_a;
-    for (int p = 0; p < tpasses; p++) {
-        if ((rc = sort_pass(f, src, dst, cap, n_ent, 32 + 8 * p, f->sort_hist + (4 + p) * 256, 4 + p, 0, st))) return rc;
-        uint64_t *tmp = src;
-        src = dst;
-        dst = tmp;
+    const int rb = compact ? rank_bits : 0;
+    emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f, f->keys_a, f->keys_b, cull, rb);
+    if ((rc = check_launch("emit_kernel"))) return rc;
+    emit_big_kernel<<<8 * 148, 256, 0, st>>>(*f, f->keys_a, f->keys_b, rb);
+    if ((rc = check_launch("emit_big_kernel"))) return rc;
+    // 3) stable sort of the entries on the tile field, 4) ranges + entry ids
+    if (compact) {
+        uint32_t *a = reinterpret_cast<uint32_t *>(f->keys_b), *b = a + f->entry_capacity, *res = nullptr;
+        if ((rc = tile_sort<uint32_t>(f, a, b, rank_bits, tpasses, st, &res))) return rc;
+        ranges_kernel<uint32_t><<<4 * 148, 256, 0, st>>>(*f, res, rank_bits, f->keys_a);
+    } else {
+        uint64_t *res = nullptr;
+        if ((rc = tile_sort<uint64_t>(f, f->keys_b, f->keys_a, 32, tpasses, st, &res))) return rc;
+        ranges_kernel<uint64_t><<<4 * 148, 256, 0, st>>>(*f, res, 0, nullptr);
     }
-    // 4) ranges + entry ids
-    ranges_kernel<<<4 * 148, 256, 0, st>>>(*f, src);
     return check_launch("ranges_kernel");
 }

@@ -222,55 +222,93 @@ __device__ __forceinline__ float quad_q(float ca, float cb, float cc, float dx, 
 // form of o e^{-q/2} >= 1/255).  "min <= qcut" == "some evaluated q <= qcut", so rows are
 // scanned outward from the mean row and the scan stops at the first hit.  A conservative
 // continuous lower bound rejects clearly-outside tiles without the scan.
+// the two per-row candidates of R/rasterizer.py:134-146 for one pixel row; true if either
+// evaluates to q <= qcut
+__device__ __forceinline__ bool row_hits(float mx, float my, float ca, float cb, float cc, float qcut, int x0, int x1,
+                                         int py) {
+    const float dy = __fsub_rn((float)py, my);
+    float xsr = __fsub_rn(mx, __fdiv_rn(__fmul_rn(cb, dy), ca));
+    const float lo = (float)(x0 - 1), hi = (float)(x1 + 1);
+    if (!(xsr >= lo)) xsr = lo;
+    if (xsr > hi) xsr = hi;
+    const int xf = (int)floorf(xsr);
+#pragma unroll
+    for (int j = 0; j < 2; j++) {
+        int xc = xf + j;
+        xc = xc < x0 ? x0 : (xc > x1 ? x1 : xc);
+        const float dx = __fsub_rn((float)xc, mx);
+        if (quad_q(ca, cb, cc, dx, dy) <= qcut) return true;
+    }
+    return false;
+}
+
 __device__ __forceinline__ bool tile_keep(float mx, float my, float ca, float cb, float cc, float qcut, int x0,
                                           int x1, int y0, int y1) {
-    // continuous minimum over [x0,x1]x[y0,y1] (real-valued), only as a safe early reject
-    float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
-    if (!(ax0 <= 0.0f && ax1 >= 0.0f && ay0 <= 0.0f && ay1 >= 0.0f)) {
-        float qc = 3.0e38f;
-        float ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
-#pragma unroll
-        for (int k = 0; k < 2; k++) {
-            float y = ys[k];
-            float dx = fminf(fmaxf(-cb * y / ca, ax0), ax1);
-            qc = fminf(qc, ca * dx * dx + 2.0f * cb * dx * y + cc * y * y);
-            float x = xs[k];
-            float dy = fminf(fmaxf(-cb * x / cc, ay0), ay1);
-            qc = fminf(qc, ca * x * x + 2.0f * cb * x * dy + cc * dy * dy);
-        }
-        float scale = ca * fmaxf(ax0 * ax0, ax1 * ax1) + cc * fmaxf(ay0 * ay0, ay1 * ay1);
-        if (qc - 1e-4f * scale - 1e-4f > qcut) return false;
-    }
+    // 1) the row nearest the mean first: most kept tiles are decided by its two candidates
     int r0 = (int)floorf(my + 0.5f);
     r0 = r0 < y0 ? y0 : (r0 > y1 ? y1 : r0);
-    int nrows = y1 - y0 + 1;
-    float lo = (float)(x0 - 1), hi = (float)(x1 + 1);
-    for (int k = 0, up = r0, dn = r0 - 1; k < nrows; k++) {
-        int py;
-        // alternate r0, r0-1, r0+1, r0-2, ... staying inside [y0, y1]
-        if ((k & 1) == 0) {
-            if (up <= y1) py = up++;
-            else py = dn--;
-        } else {
-            if (dn >= y0) py = dn--;
-            else py = up++;
-        }
-        float dy = __fsub_rn((float)py, my);
-        float xsr = __fsub_rn(mx, __fdiv_rn(__fmul_rn(cb, dy), ca));
-        if (!(xsr >= lo)) xsr = lo;
-        if (xsr > hi) xsr = hi;
-        int xf = (int)floorf(xsr);
+    if (row_hits(mx, my, ca, cb, cc, qcut, x0, x1, r0)) return true;
+    // 2) conservative continuous lower bound over [x0,x1]x[y0,y1] rejects clearly-outside
+    //    tiles (margin >> the fp32 evaluation error of q, so no kept tile is ever rejected)
+    const float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
+    if (!(ax0 <= 0.0f && ax1 >= 0.0f && ay0 <= 0.0f && ay1 >= 0.0f)) {
+        float qc = 3.0e38f;
+        const float ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
 #pragma unroll
-        for (int j = 0; j < 2; j++) {
-            int xc = xf + j;
-            xc = xc < x0 ? x0 : (xc > x1 ? x1 : xc);
-            float dx = __fsub_rn((float)xc, mx);
-            if (quad_q(ca, cb, cc, dx, dy) <= qcut) return true;
+        for (int k = 0; k < 2; k++) {
+            const float y = ys[k];
+            const float dx = fminf(fmaxf(-cb * y / ca, ax0), ax1);
+            qc = fminf(qc, ca * dx * dx + 2.0f * cb * dx * y + cc * y * y);
+            const float x = xs[k];
+            const float dy = fminf(fmaxf(-cb * x / cc, ay0), ay1);
+            qc = fminf(qc, ca * x * x + 2.0f * cb * x * dy + cc * dy * dy);
         }
+        const float scale = ca * fmaxf(ax0 * ax0, ax1 * ax1) + cc * fmaxf(ay0 * ay0, ay1 * ay1);
+        if (qc - 1e-5f * scale - 1e-6f > qcut) return false;
+    }
+    // 3) the remaining rows, outward from r0 (r0-1, r0+1, r0-2, ...)
+    for (int k = 1, up = r0 + 1, dn = r0 - 1; k < y1 - y0 + 1; k++) {
+        int py;
+        if ((k & 1) == 1) py = (dn >= y0) ? dn-- : up++;
+        else py = (up <= y1) ? up++ : dn--;
+        if (row_hits(mx, my, ca, cb, cc, qcut, x0, x1, py)) return true;
     }
     return false;
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// Exact cull of every candidate tile of a Gaussian's rectangle (ty-major, then tx, as
+// R/rasterizer.py:113-122 enumerates them).  Returns the kept count; bit c of `bits` is the
+// result for candidate c < 64 (the emit pass recomputes candidates >= 64).
+__device__ __forceinline__ int cull_rect(float mx, float my, float ca, float cb, float cc, float qcut, int4 r,
+                                         int width, int height, uint64_t &bits) {
+    const int nx = r.y - r.x + 1;
+    const int ncand = nx > 0 ? nx * (r.w - r.z + 1) : 0;
+    int count = 0;
+    bits = 0ull;
+    for (int c = 0; c < ncand; c++) {
+        const int tx = r.x + c % nx, ty = r.z + c / nx;
+        const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+        const int x1 = min(x0 + GS_TILE - 1, width - 1), y1 = min(y0 + GS_TILE - 1, height - 1);
+        if (tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1)) {
+            count++;
+            if (c < 64) bits |= 1ull << c;
+        }
+    }
+    return count;
+}
+
+// Append flagged ids to a list with one atomic per warp (all 32 lanes must call).
+__device__ __forceinline__ void warp_append(bool flag, int32_t id, int32_t *counter, int32_t *list) {
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if (!m) return;
+    const unsigned lane = threadIdx.x & 31u;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if ((int)lane == leader) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (flag) list[base + __popc(m & ((1u << lane) - 1u))] = id;
+}
 
 }  // namespace gs

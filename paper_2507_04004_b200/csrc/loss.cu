@@ -39,6 +39,9 @@ __device__ __forceinline__ int reflect_idx(int j, int n) {  // R/losses.py:31-42
 // Tables per axis, 22 floats per position: F[q][d+5] (blur) then A[p][d+5] = F[p+d][5-d]
 // (adjoint, zero where p+d leaves the axis).  Layout: x axis (w positions) then y axis.
 __global__ void loss_tables_kernel(float *tab_x, int w, float *tab_y, int h) {
+    // the tables depend only on (w, h): loss_finalize_kernel stamps them valid after first use
+    const int *stamp = reinterpret_cast<const int *>(tab_y + 22 * h);
+    if (stamp[0] == (w << 16) + h && stamp[1] == ~((w << 16) + h)) return;
     double K[11], s = 0.0;
     for (int i = 0; i < 11; i++) {
         double x = i - 5;
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
 }
 
 __global__ void loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
-                                     float xi) {
+                                     float xi, float *tab_stamp) {
     __shared__ double r[3][256];
     double a = 0.0, b = 0.0, c = 0.0;
     for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
@@ -299,6 +302,9 @@ __global__ void loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ vie
         f.loss[1] = lc;
         f.loss[2] = ld;
         f.loss[3] = dssim;
+        int *stamp = reinterpret_cast<int *>(tab_stamp);
+        stamp[0] = (f.width << 16) + f.height;
+        stamp[1] = ~((f.width << 16) + f.height);
     }
 }
 
@@ -334,7 +340,7 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     depth_loss_kernel<<<DEPTH_BLOCKS, 256, 0, st>>>(*f, view, xi, ssim_blocks);
     if ((rc = check_launch("depth_loss_kernel"))) return rc;
-    loss_finalize_kernel<<<1, 256, 0, st>>>(*f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi);
+    loss_finalize_kernel<<<1, 256, 0, st>>>(*f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
     return check_launch("loss_finalize_kernel");
 }
 

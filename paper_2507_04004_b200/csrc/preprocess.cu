@@ -51,54 +51,126 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
         }
     }
     __syncwarp();
-    if (i >= n) return;
-    const float *p = srow[warp][lane];
-    f.touched[i] = 0;
-    float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-    float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
-    int4 *rc = reinterpret_cast<int4 *>(f.rect) + i;
-    const uint64_t inactive_key = (0xffffffffull << 32) | (uint64_t)i;
-    if (!near_ok) {
-        float z = (p[0] * cam.rot_cw[6] + p[1] * cam.rot_cw[7] + p[2] * cam.rot_cw[8]) + cam.trans_cw[2];
-        s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-        s2[1] = make_float4(0.f, 0.f, z, 0.f);
-        s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-        *cv = make_float4(0.f, 0.f, 0.f, -1.f);
-        *rc = make_int4(0, -1, 0, -1);
-        f.valid[i] = 0;
-        f.keys_a[i] = inactive_key;
-        return;
-    }
-    Projected pr;
-    project_full(p, cam, pr);
-    float op = 1.0f / (1.0f + expf(-p[10]));
-    // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
-    float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
-    float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
-    if (un < 1e-12f) un = 1.0f;
-    float b[16];
-    sh_basis(u0 / un, u1 / un, u2 / un, b);
-    float col[3];
+    bool touched = false, big = false;
+    if (i < n) {
+        const float *p = srow[warp][lane];
+        float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+        float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
+        int4 *rc = reinterpret_cast<int4 *>(f.rect) + i;
+        if (!near_ok) {
+            float z = (p[0] * cam.rot_cw[6] + p[1] * cam.rot_cw[7] + p[2] * cam.rot_cw[8]) + cam.trans_cw[2];
+            s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+            s2[1] = make_float4(0.f, 0.f, z, 0.f);
+            s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+            *cv = make_float4(0.f, 0.f, 0.f, -1.f);
+            *rc = make_int4(0, -1, 0, -1);
+            f.valid[i] = 0;
+            f.kept[i] = 0;
+            f.keys_a[i] = (0xffffffffull << 32) | (uint64_t)i;
+        } else {
+            Projected pr;
+            project_full(p, cam, pr);
+            const float op = 1.0f / (1.0f + expf(-p[10]));
+            // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
+            const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
+            float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
+            if (un < 1e-12f) un = 1.0f;
+            float b[16];
+            sh_basis(u0 / un, u1 / un, u2 / un, b);
+            float col[3];
 #pragma unroll
-    for (int c = 0; c < 3; c++) {
-        float acc = 0.0f;
+            for (int c = 0; c < 3; c++) {
+                float acc = 0.0f;
 #pragma unroll
-        for (int k = 0; k < 15; k++) acc += b[k + 1] * p[14 + 3 * k + c];
-        float pre = b[0] * p[11 + c] + acc + 0.5f;
-        col[c] = pre > 0.0f ? pre : 0.0f;
+                for (int k = 0; k < 15; k++) acc += b[k + 1] * p[14 + 3 * k + c];
+                const float pre = b[0] * p[11 + c] + acc + 0.5f;
+                col[c] = pre > 0.0f ? pre : 0.0f;
+            }
+            int4 rect = make_int4(0, -1, 0, -1);
+            float qcut = 0.0f, radius = -1.0f;
+            const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width, f.height,
+                                                      f.tiles_x, f.tiles_y, rect, qcut, radius);
+            if (!active) rect = make_int4(0, -1, 0, -1);
+            // exact per-tile cull of the rectangle (R/rasterizer.py:150-166), fused here for small
+            // footprints; large ones are culled warp-cooperatively by cull_big_kernel
+            const int ncand = (rect.y - rect.x + 1) * (rect.w - rect.z + 1);
+            big = active && ncand > GS_SMALL_CAND;
+            uint64_t bits = 0ull;
+            const int kept = (active && !big)
+                                 ? cull_rect(pr.mx, pr.my, pr.ca, pr.cb, pr.cc, qcut, rect, f.width, f.height, bits)
+                                 : 0;
+            touched = kept > 0;
+            s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
+            s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
+            s2[2] = make_float4(col[0], col[1], col[2], 0.0f);
+            *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
+            *rc = rect;
+            f.valid[i] = pr.valid ? 1 : 0;
+            f.kept[i] = kept;
+            f.keep_bits[i] = bits;
+            f.keys_a[i] = touched ? (((uint64_t)__float_as_uint(pr.mu[2]) << 32) | (uint64_t)i)
+                                  : ((0xffffffffull << 32) | (uint64_t)i);
+        }
+        f.touched[i] = touched ? 1 : 0;
     }
-    int4 rect = make_int4(0, -1, 0, -1);
-    float qcut = 0.0f, radius = -1.0f;
-    bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width, f.height, f.tiles_x,
-                                         f.tiles_y, rect, qcut, radius);
-    if (!active) rect = make_int4(0, -1, 0, -1);
-    s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
-    s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-    s2[2] = make_float4(col[0], col[1], col[2], 0.0f);
-    *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
-    *rc = rect;
-    f.valid[i] = pr.valid ? 1 : 0;
-    f.keys_a[i] = active ? (((uint64_t)__float_as_uint(pr.mu[2]) << 32) | (uint64_t)i) : inactive_key;
+    warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+    warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
+}
+
+// Warp-cooperative exact cull of the large-footprint Gaussians (lanes stride over candidate
+// tiles; same decision function as cull_rect).  Completes kept/keep_bits/touched/key.
+constexpr int BIG_THREADS = 256;
+
+__global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f) {
+    // one CTA per large-footprint Gaussian: threads stride over its candidate tiles
+    __shared__ int s_cnt;
+    __shared__ int64_t s_base;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t nb = f.counters[GS_CNT_BIG];
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int g = f.big_list[b];
+        const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+        const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+        const int words = (ncand + 31) >> 5;
+        if (threadIdx.x == 0) {
+            s_cnt = 0;
+            // reserve the Gaussian's cull bitmap; on overflow the emit pass re-culls instead
+            const int64_t base = atomicAdd(&f.counters[GS_CNT_BIG_BITS], words);
+            s_base = base + words <= f.big_bits_words ? base : -1;
+        }
+        __syncthreads();
+        const int64_t base = s_base;
+        int count = 0;
+        for (int c0 = 0; c0 < ncand; c0 += BIG_THREADS) {  // uniform trip count: ballots are warp-wide
+            const int c = c0 + threadIdx.x;
+            bool keep = false;
+            if (c < ncand) {
+                const int tx = r.x + c % nx, ty = r.z + c / nx;
+                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+            }
+            count += keep;
+            const unsigned bal = __ballot_sync(0xffffffffu, keep);
+            if (lane == 0 && base >= 0 && (c0 >> 5) + warp < words) f.big_bits[base + (c0 >> 5) + warp] = bal;
+        }
+        for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
+        if (lane == 0 && count) atomicAdd(&s_cnt, count);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const int kept = s_cnt;
+            f.kept[g] = kept;
+            f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+            f.touched[g] = kept > 0;
+            if (kept > 0) {
+                f.keys_a[g] = ((uint64_t)__float_as_uint(s1.z) << 32) | (uint64_t)g;
+                f.touched_list[atomicAdd(&f.counters[GS_CNT_TOUCHED], 1)] = g;
+            }
+        }
+        __syncthreads();
+    }
 }
 
 // gs_project: full projection records for the project() API (R/gaussians.py:180-215)
@@ -170,47 +242,79 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     bool v = valid[i] != 0;
     bool active = v && tile_rect(c00, c01, c11, o, mx, my, f.width, f.height, f.tiles_x, f.tiles_y, rect, qcut, radius);
     if (!active) rect = make_int4(0, -1, 0, -1);
+    const float ca = conic[3 * i], cb = conic[3 * i + 1], cc = conic[3 * i + 2];
+    uint64_t bits = 0ull;
+    const bool big = active && (rect.y - rect.x + 1) * (rect.w - rect.z + 1) > GS_SMALL_CAND;
+    const int kept = (active && !big) ? cull_rect(mx, my, ca, cb, cc, qcut, rect, f.width, f.height, bits)
+                                      : (big ? -1 : 0);
     float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-    s2[0] = make_float4(mx, my, conic[3 * i], conic[3 * i + 1]);
-    s2[1] = make_float4(conic[3 * i + 2], o, depth[i], qcut);
+    s2[0] = make_float4(mx, my, ca, cb);
+    s2[1] = make_float4(cc, o, depth[i], qcut);
     s2[2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(c00, c01, c11, radius);
     reinterpret_cast<int4 *>(f.rect)[i] = rect;
     f.valid[i] = v;
-    f.touched[i] = 0;
-    f.keys_a[i] = active ? (((uint64_t)__float_as_uint(depth[i]) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
+    f.kept[i] = kept;
+    f.keep_bits[i] = bits;
+    f.touched[i] = kept > 0;
+    f.keys_a[i] = kept > 0 ? (((uint64_t)__float_as_uint(depth[i]) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
 }
 
-__global__ void lidar_compact_kernel(const float *__restrict__ sparse, int64_t npx, int32_t *idx, float *z,
-                                     int32_t *k_out) {
-    // ordered compaction (single block, so the K-list keeps pixel order like np.flatnonzero)
-    __shared__ int32_t s_base;
-    __shared__ int32_t s_warp[32];
+// the touched and large-footprint lists of the pack path (unordered; consumers are order
+// independent)
+__global__ void touched_list_kernel(gs_frame f) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = i < f.n ? f.kept[i] : 0;
+    if (k < 0) f.kept[i] = 0;
+    warp_append(k > 0, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+    warp_append(k < 0, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
+}
+
+// Ordered compaction of sparse_depth > 0 into the K-list (np.flatnonzero order), two passes:
+// per-chunk counts, then each chunk sums its predecessors' counts and writes in order.
+constexpr int LC_CHUNK = 1024;
+
+__global__ void lidar_count_kernel(const float *__restrict__ sparse, int64_t npx, int32_t *chunk_cnt) {
+    __shared__ int s;
+    if (threadIdx.x == 0) s = 0;
+    __syncthreads();
+    const int64_t p = (int64_t)blockIdx.x * LC_CHUNK + threadIdx.x;
+    const bool hit = p < npx && sparse[p] > 0.0f;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&s, __popc(m));
+    __syncthreads();
+    if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = s;
+}
+
+__global__ void lidar_write_kernel(const float *__restrict__ sparse, int64_t npx, const int32_t *__restrict__ chunk_cnt,
+                                   int32_t *idx, float *z, int32_t *k_out) {
+    __shared__ int s_warp[LC_CHUNK / 32];
+    __shared__ int s_base;
     if (threadIdx.x == 0) s_base = 0;
     __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    for (int64_t off = 0; off < npx; off += blockDim.x) {
-        int64_t p = off + threadIdx.x;
-        float v = p < npx ? sparse[p] : 0.0f;
-        bool hit = v > 0.0f;
-        unsigned m = __ballot_sync(0xffffffffu, hit);
-        if (lane == 0) s_warp[warp] = __popc(m);
-        __syncthreads();
-        int before = 0, total = 0;
-        for (int w = 0; w < nwarps; w++) {
-            if (w < warp) before += s_warp[w];
-            total += s_warp[w];
-        }
-        int pos = s_base + before + __popc(m & ((1u << lane) - 1u));
-        if (hit) {
-            idx[pos] = (int32_t)p;
-            z[pos] = v;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_base += total;
-        __syncthreads();
+    int acc = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += LC_CHUNK) acc += chunk_cnt[c];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_base, acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t p = (int64_t)blockIdx.x * LC_CHUNK + threadIdx.x;
+    const float v = p < npx ? sparse[p] : 0.0f;
+    const bool hit = v > 0.0f;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int before = s_base;
+    for (int w = 0; w < warp; w++) before += s_warp[w];
+    if (hit) {
+        const int pos = before + __popc(m & ((1u << lane) - 1u));
+        idx[pos] = (int32_t)p;
+        z[pos] = v;
     }
-    if (threadIdx.x == 0) *k_out = s_base;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        int tot = s_base;
+        for (int w = 0; w < LC_CHUNK / 32; w++) tot += s_warp[w];
+        *k_out = tot;
+    }
 }
 
 }  // namespace gs
@@ -222,11 +326,15 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
         set_error("gs_preprocess: null argument");
         return GS_ERR_ARG;
     }
+    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     int64_t warps = (f->n + 31) / 32;
     int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
     preprocess_kernel<<<blocks, PP_THREADS, 0, (cudaStream_t)stream>>>(*f, params, view);
-    return check_launch("preprocess_kernel");
+    int rc = check_launch("preprocess_kernel");
+    if (rc) return rc;
+    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    return check_launch("cull_big_kernel");
 }
 
 extern "C" int gs_project(const float *params, int64_t n, const gs_camera *cam, float *mu_cam, float *mean2d,
@@ -249,14 +357,28 @@ extern "C" int gs_eval_sh(const float *sh_low, const float *sh_high, const float
 extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const float *conic, const float *cov2d3,
                               const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                               void *stream) {
+    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);
-    return check_launch("pack_kernel");
+    int rc = check_launch("pack_kernel");
+    if (rc) return rc;
+    touched_list_kernel<<<(unsigned)((f->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
+    if ((rc = check_launch("touched_list_kernel"))) return rc;
+    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    return check_launch("cull_big_kernel");
 }
 
 extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_t height, int32_t *idx, float *z,
                                 int32_t *k_out, void *stream) {
-    lidar_compact_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(sparse_depth, (int64_t)width * height, idx, z, k_out);
-    return check_launch("lidar_compact_kernel");
+    // idx has room for npx + ceil(npx / 1024) ints; the tail holds the per-chunk counts
+    const int64_t npx = (int64_t)width * height;
+    const unsigned chunks = (unsigned)((npx + LC_CHUNK - 1) / LC_CHUNK);
+    if (chunks == 0) return GS_OK;
+    int32_t *scratch = idx + npx;
+    lidar_count_kernel<<<chunks, LC_CHUNK, 0, (cudaStream_t)stream>>>(sparse_depth, npx, scratch);
+    int rc = check_launch("lidar_count_kernel");
+    if (rc) return rc;
+    lidar_write_kernel<<<chunks, LC_CHUNK, 0, (cudaStream_t)stream>>>(sparse_depth, npx, scratch, idx, z, k_out);
+    return check_launch("lidar_write_kernel");
 }

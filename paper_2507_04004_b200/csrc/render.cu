@@ -33,7 +33,9 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
     const bool inside = px < f.width && py < f.height;
     const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
     const float fx = (float)px, fy = (float)py;
-    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, dsum = 0.0f;
+    // opacity is accumulated as sum(w) (== 1 - T exactly in real arithmetic): 1 - T in fp32
+    // cancels for nearly transparent pixels, and the depth loss divides by it
+    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, dsum = 0.0f, osum = 0.0f;
     int cnt = 0;
     bool done = !inside;
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
@@ -60,6 +62,7 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
                 c1 += C.y * w;
                 c2 += C.z * w;
                 dsum += B.z * w;
+                osum += w;
                 T *= 1.0f - alpha;
                 if (early_stop && T < GS_EARLY_STOP_T) {
                     done = true;
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
         f.color[3 * p + 1] = c1;
         f.color[3 * p + 2] = c2;
         f.depth[p] = dsum;
-        f.opacity[p] = 1.0f - T;
+        f.opacity[p] = osum;
         f.trans[p] = T;
         f.n_contrib[p] = cnt;
     }

@@ -25,6 +25,16 @@ from .rasterizer import (AdamState, Camera, DeviceView, Workspace, _bin_frame, c
 NEAR_CLIP = 0.01
 
 
+def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
+    """Our kernels per map-optimisation iteration:
+    preprocess 2 (projection+cull, large-footprint cull), bin 11 + tile-sort passes
+    (2 histograms, 2 bin scans, 4 depth passes, scan, 2 emits, ranges), forward 1,
+    loss 4, backward 2 (zero + tiles), chain(+Adam) 1."""
+    tile_bits = max(1, (tiles - 1).bit_length())
+    tpasses = 1 if tile_bits <= 8 else (2 if tile_bits <= 16 else 3)
+    return 2 + 11 + tpasses + 1 + 4 + 2 + 1
+
+
 @dataclass
 class MappingConfig:
     """R/mapper.py:28-50 (the hot-path knobs: lam, xi, k_keyframes)."""
@@ -149,10 +159,7 @@ class MapOptimizer:
 
     def kernels_per_step(self) -> int:
         """Kernels of ours launched by one iteration."""
-        tiles = self.ws.tiles_x * self.ws.tiles_y
-        tile_bits = max(1, (tiles - 1).bit_length())
-        tpasses = 1 if tile_bits <= 8 else (2 if tile_bits <= 16 else 3)
-        return 1 + (2 + 4 + 3 + 2 + tpasses + 1) + 1 + 4 + 2 + 1
+        return kernels_per_iteration(self.ws.tiles_x * self.ws.tiles_y)
 
     def profile_step(self, k: int) -> dict:
         """Eager iteration with CUDA events between the six C-ABI calls; returns ms per phase."""
@@ -186,7 +193,7 @@ class MapOptimizer:
                       for kf in keyframes]
         self._d_img = torch.empty((h, w, 3), device=self.dev)
         self._d_sd = torch.empty((h, w), device=self.dev)
-        self._d_idx = torch.empty(h * w, dtype=torch.int32, device=self.dev)
+        self._d_idx = torch.empty(h * w + (h * w + 1023) // 1024, dtype=torch.int32, device=self.dev)
         self._d_z = torch.empty(h * w, device=self.dev)
         self._h_view = []
         for kf in keyframes:

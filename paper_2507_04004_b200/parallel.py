@@ -65,10 +65,9 @@ class BatchMapOptimizer:
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
 
     def kernels_per_step(self, views: int | None = None) -> int:
-        tiles = self.ws.tiles_x * self.ws.tiles_y
-        tpasses = 1 if tiles <= 256 else (2 if tiles <= 65536 else 3)
-        per_view = 1 + (2 + 4 + 3 + 2 + tpasses + 1) + 1 + 4 + 2 + 1
-        return per_view * (views if views is not None else len(self.views)) + 2
+        from .mapper import kernels_per_iteration
+        per_view = kernels_per_iteration(self.ws.tiles_x * self.ws.tiles_y)
+        return per_view * (views if views is not None else len(self.views)) + 2  # + adam, step counters
 
     def accumulate(self, k: int) -> None:
         """forward -> loss -> backward -> chain rule of view k into (grads, touched)."""

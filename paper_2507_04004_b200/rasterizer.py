@@ -99,7 +99,7 @@ class DeviceView:
         self.sparse = None
         if sparse_depth is not None:
             self.sparse = _f32(sparse_depth, self.device).reshape(h, w).contiguous()
-            self.lidar_idx = torch.empty(h * w, dtype=torch.int32, device=self.device)
+            self.lidar_idx = torch.empty(h * w + (h * w + 1023) // 1024, dtype=torch.int32, device=self.device)
             self.lidar_z = torch.empty(h * w, dtype=torch.float32, device=self.device)
             s.lidar_idx = self.lidar_idx.data_ptr()
             s.lidar_z = self.lidar_z.data_ptr()
