@@ -93,13 +93,13 @@ typedef struct gs_frame {
     int64_t entry_capacity;  /* max kept (splat, tile) pairs */
     int32_t width, height, tiles_x, tiles_y;
     /* per Gaussian */
-    float *splat2d;          /* n x 12: mx my ca cb | cc opacity depth qcut | r g b pad */
+    float *splat2d;          /* n x 12: mx my ca cb | cc opacity depth qcut | r g b 1-opacity */
     float *cov2d;            /* n x 4: c00 c01 c11 radius */
     int32_t *rect;           /* n x 4: tx0 tx1 ty0 ty1 (empty: tx1 < tx0) */
     uint8_t *valid;          /* n: near-plane & det test (R/gaussians.py:190-208) */
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
-    float *g2d;              /* n x GS_G2D screen-space gradients (touched rows valid) */
+    double *g2d;             /* n x GS_G2D screen-space gradients, FP64 accumulators (touched rows) */
     uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
     int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
     int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */

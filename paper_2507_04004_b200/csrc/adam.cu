@@ -16,14 +16,17 @@ constexpr int CA_THREADS = CA_WARPS * 32;
 constexpr int RP = 65;  // padded smem row
 
 // dR/dq of the normalised quaternion (R/rasterizer.py:490-499), contracted with gR
-__device__ __forceinline__ void quat_grad(const float q0[4], const float gR[9], float out[4]) {
-    float nrm = sqrtf(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
-    float w = q0[0] / nrm, x = q0[1] / nrm, y = q0[2] / nrm, z = q0[3] / nrm;
-    const float dw[9] = {0.f, -z, y, z, 0.f, -x, -y, x, 0.f};
-    const float dx[9] = {0.f, y, z, y, -2.f * x, -w, z, w, -2.f * x};
-    const float dy[9] = {-2.f * y, x, w, x, 0.f, z, -w, z, -2.f * y};
-    const float dz[9] = {-2.f * z, -w, x, w, -2.f * z, y, x, y, 0.f};
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+template <typename T>
+__device__ __forceinline__ void quat_grad(const float q0[4], const T gR[9], float out[4]) {
+    const T a = q0[0], b = q0[1], c = q0[2], d = q0[3];
+    const T nrm = gs_sqrt(a * a + b * b + c * c + d * d);
+    const T w = a / nrm, x = b / nrm, y = c / nrm, z = d / nrm;
+    const T zero = 0, two = 2;
+    const T dw[9] = {zero, -z, y, z, zero, -x, -y, x, zero};
+    const T dx[9] = {zero, y, z, y, -two * x, -w, z, w, -two * x};
+    const T dy[9] = {-two * y, x, w, x, zero, z, -w, z, -two * y};
+    const T dz[9] = {-two * z, -w, x, w, -two * z, y, x, y, zero};
+    T a0 = 0, a1 = 0, a2 = 0, a3 = 0;
 #pragma unroll
     for (int k = 0; k < 9; k++) {
         a0 += gR[k] * dw[k];
@@ -31,35 +34,41 @@ __device__ __forceinline__ void quat_grad(const float q0[4], const float gR[9], 
         a2 += gR[k] * dy[k];
         a3 += gR[k] * dz[k];
     }
-    const float gq[4] = {2.f * a0, 2.f * a1, 2.f * a2, 2.f * a3};
-    const float qh[4] = {w, x, y, z};
-    const float dot = gq[0] * qh[0] + gq[1] * qh[1] + gq[2] * qh[2] + gq[3] * qh[3];
+    const T gq[4] = {two * a0, two * a1, two * a2, two * a3};
+    const T qh[4] = {w, x, y, z};
+    const T dot = gq[0] * qh[0] + gq[1] * qh[1] + gq[2] * qh[2] + gq[3] * qh[3];
 #pragma unroll
-    for (int k = 0; k < 4; k++) out[k] = (gq[k] - qh[k] * dot) / nrm;
+    for (int k = 0; k < 4; k++) out[k] = (float)((gq[k] - qh[k] * dot) / nrm);
 }
 
 // gradient of the scalar loss w.r.t. one parameter row (59 columns written to G; every write
 // happens after the last read of p, so G may alias p)
-__device__ __forceinline__ void chain_row(const float *p, const float *g, const gs_camera &cam, float *G) {
-    const float *Rc = cam.rot_cw;
-    const float fx = cam.fx, fy = cam.fy;
-    Projected pr;
-    project_full(p, cam, pr);
-    const float z = pr.mu[2];
+__device__ __forceinline__ void chain_row(const float *p, const double *g, const gs_camera &cam, float *G) {
+    // geometric chain in FP64: for Gaussians just past the 0.01 m near plane, J ~ fx/z ~ 1e5 and
+    // the products below lose several fp32 digits; B200's FP64 pipe makes this nearly free here
+    using D = double;
+    const float *Rcf = cam.rot_cw;
+    D Rc[9];
+#pragma unroll
+    for (int k = 0; k < 9; k++) Rc[k] = Rcf[k];
+    const D fx = cam.fx, fy = cam.fy;
+    ProjectedT<D> pr;
+    project_full<D>(p, cam, pr);
+    const D z = pr.mu[2];
     // conic -> 2x2 covariance gradient (R/rasterizer.py:583-592)
-    const float ca = pr.ca, cb = pr.cb, cc = pr.cc;
-    const float ga = g[2], gb = 0.5f * g[3], gc = g[4];
-    const float t00 = ca * ga + cb * gb, t01 = ca * gb + cb * gc, t10 = cb * ga + cc * gb, t11 = cb * gb + cc * gc;
-    const float gv00 = -(t00 * ca + t01 * cb), gv01 = -(t00 * cb + t01 * cc);
-    const float gv10 = -(t10 * ca + t11 * cb), gv11 = -(t10 * cb + t11 * cc);
+    const D ca = pr.ca, cb = pr.cb, cc = pr.cc;
+    const D ga = g[2], gb = 0.5 * (D)g[3], gc = g[4];
+    const D t00 = ca * ga + cb * gb, t01 = ca * gb + cb * gc, t10 = cb * ga + cc * gb, t11 = cb * gb + cc * gc;
+    const D gv00 = -(t00 * ca + t01 * cb), gv01 = -(t00 * cb + t01 * cc);
+    const D gv10 = -(t10 * ca + t11 * cb), gv11 = -(t10 * cb + t11 * cc);
     // cov2d = M S M^T (R/rasterizer.py:595-597)
-    float tmp[6];
+    D tmp[6];
 #pragma unroll
     for (int b = 0; b < 3; b++) {
         tmp[b] = gv00 * pr.M[b] + gv01 * pr.M[3 + b];
         tmp[3 + b] = gv10 * pr.M[b] + gv11 * pr.M[3 + b];
     }
-    float gS[9], gM[6], gJ[6];
+    D gS[9], gM[6], gJ[6];
 #pragma unroll
     for (int a = 0; a < 3; a++)
 #pragma unroll
@@ -68,45 +77,46 @@ __device__ __forceinline__ void chain_row(const float *p, const float *g, const 
     for (int a = 0; a < 2; a++)
 #pragma unroll
         for (int b = 0; b < 3; b++)
-            gM[3 * a + b] = 2.0f * (tmp[3 * a] * pr.S[b] + tmp[3 * a + 1] * pr.S[3 + b] + tmp[3 * a + 2] * pr.S[6 + b]);
+            gM[3 * a + b] = 2.0 * (tmp[3 * a] * pr.S[b] + tmp[3 * a + 1] * pr.S[3 + b] + tmp[3 * a + 2] * pr.S[6 + b]);
 #pragma unroll
     for (int a = 0; a < 2; a++)
 #pragma unroll
         for (int b = 0; b < 3; b++)
             gJ[3 * a + b] = gM[3 * a] * Rc[3 * b] + gM[3 * a + 1] * Rc[3 * b + 1] + gM[3 * a + 2] * Rc[3 * b + 2];
     // J and mean2d depend on the camera-frame mean (R/rasterizer.py:600-611)
-    const float iz = 1.0f / z, iz2 = iz * iz, iz3 = iz2 * iz;
-    float gx = gJ[2] * (-fx * iz2);
-    float gy = gJ[5] * (-fy * iz2);
-    float gz = gJ[0] * (-fx * iz2) + gJ[4] * (-fy * iz2) + gJ[2] * (2.0f * fx * pr.mu[0] * iz3) +
-               gJ[5] * (2.0f * fy * pr.mu[1] * iz3);
-    gx += g[0] * fx * iz;
-    gy += g[1] * fy * iz;
-    gz += -g[0] * fx * pr.mu[0] * iz2 - g[1] * fy * pr.mu[1] * iz2;
-    gz += g[9];
+    const D iz = 1.0 / z, iz2 = iz * iz, iz3 = iz2 * iz;
+    D gx = gJ[2] * (-fx * iz2);
+    D gy = gJ[5] * (-fy * iz2);
+    D gz = gJ[0] * (-fx * iz2) + gJ[4] * (-fy * iz2) + gJ[2] * (2.0 * fx * pr.mu[0] * iz3) +
+           gJ[5] * (2.0 * fy * pr.mu[1] * iz3);
+    gx += (D)g[0] * fx * iz;
+    gy += (D)g[1] * fy * iz;
+    gz += -(D)g[0] * fx * pr.mu[0] * iz2 - (D)g[1] * fy * pr.mu[1] * iz2;
+    gz += (D)g[9];
     float gpos[3];
 #pragma unroll
-    for (int c = 0; c < 3; c++) gpos[c] = gx * Rc[c] + gy * Rc[3 + c] + gz * Rc[6 + c];
+    for (int c = 0; c < 3; c++) gpos[c] = (float)(gx * Rc[c] + gy * Rc[3 + c] + gz * Rc[6 + c]);
     // Sigma = (R S)(R S)^T (R/rasterizer.py:613-626)
-    float gN[9];
+    D gN[9];
 #pragma unroll
     for (int a = 0; a < 3; a++)
 #pragma unroll
         for (int b = 0; b < 3; b++)
-            gN[3 * a + b] = 2.0f * (gS[3 * a] * pr.R[b] + gS[3 * a + 1] * pr.R[3 + b] + gS[3 * a + 2] * pr.R[6 + b]) * pr.s[b];
+            gN[3 * a + b] = 2.0 * (gS[3 * a] * pr.R[b] + gS[3 * a + 1] * pr.R[3 + b] + gS[3 * a + 2] * pr.R[6 + b]) * pr.s[b];
     float gls[3];
 #pragma unroll
-    for (int j = 0; j < 3; j++) gls[j] = (pr.R[j] * gN[j] + pr.R[3 + j] * gN[3 + j] + pr.R[6 + j] * gN[6 + j]) * pr.s[j];
-    float gR[9];
+    for (int j = 0; j < 3; j++)
+        gls[j] = (float)((pr.R[j] * gN[j] + pr.R[3 + j] * gN[3 + j] + pr.R[6 + j] * gN[6 + j]) * pr.s[j]);
+    D gR[9];
 #pragma unroll
     for (int a = 0; a < 3; a++)
 #pragma unroll
         for (int b = 0; b < 3; b++) gR[3 * a + b] = gN[3 * a + b] * pr.s[b];
     float gq[4];
-    quat_grad(p + 6, gR, gq);
+    quat_grad<D>(p + 6, gR, gq);
     // opacity logit (R/rasterizer.py:629-630)
     const float o = 1.0f / (1.0f + expf(-p[10]));
-    const float g_opl = g[5] * o * (1.0f - o);
+    const float g_opl = (float)g[5] * o * (1.0f - o);
     // SH colour incl. the view-direction dependence (R/rasterizer.py:633-644)
     const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
     float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
@@ -121,7 +131,7 @@ __device__ __forceinline__ void chain_row(const float *p, const float *g, const 
 #pragma unroll
         for (int k = 0; k < 15; k++) acc += bs[k + 1] * p[14 + 3 * k + c];
         const float pre = bs[0] * p[11 + c] + acc + 0.5f;
-        gcol[c] = pre > 0.0f ? g[6 + c] : 0.0f;
+        gcol[c] = pre > 0.0f ? (float)g[6 + c] : 0.0f;
     }
     float sk[16];
     sk[0] = p[11] * gcol[0] + p[12] * gcol[1] + p[13] * gcol[2];
@@ -188,9 +198,9 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
     }
     __syncwarp();
     if (g >= 0) {
-        const float4 *g2 = reinterpret_cast<const float4 *>(f.g2d) + (int64_t)g * (GS_G2D / 4);
-        const float4 a = g2[0], b = g2[1], c = g2[2];
-        const float gv[10] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y};
+        const double2 *g2 = reinterpret_cast<const double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
+        const double2 a = g2[0], b = g2[1], c = g2[2], d = g2[3], e = g2[4];
+        const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
         chain_row(srow[warp][lane], gv, scam, sgr[warp][lane]);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0) {

@@ -97,63 +97,78 @@ __device__ __forceinline__ void sh_basis_vjp(float x, float y, float z, const fl
 // ---------------------------------------------------------------------------
 // projection (R/gaussians.py:156-215)
 
-struct Projected {
-    float mu[3];
-    float J[6];   // 2x3
-    float M[6];   // J R_cw
-    float R[9];   // rotation of the Gaussian (normalised quaternion)
-    float s[3];   // exp(log_scale)
-    float S[9];   // world covariance
-    float c00, c01, c11;  // dilated 2x2 covariance
-    float det;
-    float mx, my;
-    float ca, cb, cc;  // conic
+// T = float on the forward path; T = double in the chain rule, whose Jacobian products are
+// ill-conditioned for Gaussians just beyond the 0.01 m near plane (fx/z ~ 1e5)
+template <typename T>
+struct ProjectedT {
+    T mu[3];
+    T J[6];   // 2x3
+    T M[6];   // J R_cw
+    T R[9];   // rotation of the Gaussian (normalised quaternion)
+    T s[3];   // exp(log_scale)
+    T S[9];   // world covariance
+    T c00, c01, c11;  // dilated 2x2 covariance
+    T det;
+    T mx, my;
+    T ca, cb, cc;  // conic
     bool valid;
 };
+using Projected = ProjectedT<float>;
 
-__device__ __forceinline__ void quat_rot(const float q0[4], float R[9]) {
-    float nrm = sqrtf(q0[0] * q0[0] + q0[1] * q0[1] + q0[2] * q0[2] + q0[3] * q0[3]);
-    float w = q0[0] / nrm, x = q0[1] / nrm, y = q0[2] / nrm, z = q0[3] / nrm;
-    R[0] = 1.0f - 2.0f * (y * y + z * z); R[1] = 2.0f * (x * y - w * z); R[2] = 2.0f * (x * z + w * y);
-    R[3] = 2.0f * (x * y + w * z); R[4] = 1.0f - 2.0f * (x * x + z * z); R[5] = 2.0f * (y * z - w * x);
-    R[6] = 2.0f * (x * z - w * y); R[7] = 2.0f * (y * z + w * x); R[8] = 1.0f - 2.0f * (x * x + y * y);
+__device__ __forceinline__ float gs_sqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double gs_sqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float gs_exp(float x) { return expf(x); }
+__device__ __forceinline__ double gs_exp(double x) { return exp(x); }
+
+template <typename T>
+__device__ __forceinline__ void quat_rot(const float q[4], T R[9]) {
+    const T q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
+    const T nrm = gs_sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+    const T w = q0 / nrm, x = q1 / nrm, y = q2 / nrm, z = q3 / nrm;
+    const T one = 1, two = 2;
+    R[0] = one - two * (y * y + z * z); R[1] = two * (x * y - w * z); R[2] = two * (x * z + w * y);
+    R[3] = two * (x * y + w * z); R[4] = one - two * (x * x + z * z); R[5] = two * (y * z - w * x);
+    R[6] = two * (x * z - w * y); R[7] = two * (y * z + w * x); R[8] = one - two * (x * x + y * y);
 }
 
 // p: pos[3], log_scale[3], quat[4] (the first 10 columns of a parameter row)
-__device__ __forceinline__ void project_full(const float *p, const gs_camera &cam, Projected &o) {
+template <typename T>
+__device__ __forceinline__ void project_full(const float *p, const gs_camera &cam, ProjectedT<T> &o) {
     const float *Rc = cam.rot_cw;
-    for (int r = 0; r < 3; r++) o.mu[r] = (p[0] * Rc[3 * r] + p[1] * Rc[3 * r + 1] + p[2] * Rc[3 * r + 2]) + cam.trans_cw[r];
-    float z = o.mu[2];
-    bool v = z > GS_NEAR_CLIP;
-    float zs = v ? z : 1.0f;
-    float iz = 1.0f / zs;
-    o.mx = cam.fx * o.mu[0] * iz + cam.cx;
-    o.my = cam.fy * o.mu[1] * iz + cam.cy;
-    o.J[0] = cam.fx * iz; o.J[1] = 0.0f; o.J[2] = -cam.fx * o.mu[0] * iz * iz;
-    o.J[3] = 0.0f; o.J[4] = cam.fy * iz; o.J[5] = -cam.fy * o.mu[1] * iz * iz;
+    for (int r = 0; r < 3; r++)
+        o.mu[r] = ((T)p[0] * (T)Rc[3 * r] + (T)p[1] * (T)Rc[3 * r + 1] + (T)p[2] * (T)Rc[3 * r + 2]) + (T)cam.trans_cw[r];
+    const T z = o.mu[2];
+    bool v = z > (T)GS_NEAR_CLIP;
+    const T zs = v ? z : (T)1;
+    const T iz = (T)1 / zs;
+    const T fx = cam.fx, fy = cam.fy;
+    o.mx = fx * o.mu[0] * iz + (T)cam.cx;
+    o.my = fy * o.mu[1] * iz + (T)cam.cy;
+    o.J[0] = fx * iz; o.J[1] = 0; o.J[2] = -fx * o.mu[0] * iz * iz;
+    o.J[3] = 0; o.J[4] = fy * iz; o.J[5] = -fy * o.mu[1] * iz * iz;
     for (int r = 0; r < 2; r++)
         for (int c = 0; c < 3; c++)
-            o.M[3 * r + c] = o.J[3 * r] * Rc[c] + o.J[3 * r + 1] * Rc[3 + c] + o.J[3 * r + 2] * Rc[6 + c];
-    quat_rot(p + 6, o.R);
-    o.s[0] = expf(p[3]); o.s[1] = expf(p[4]); o.s[2] = expf(p[5]);
-    float s2[3] = {o.s[0] * o.s[0], o.s[1] * o.s[1], o.s[2] * o.s[2]};
+            o.M[3 * r + c] = o.J[3 * r] * (T)Rc[c] + o.J[3 * r + 1] * (T)Rc[3 + c] + o.J[3 * r + 2] * (T)Rc[6 + c];
+    quat_rot<T>(p + 6, o.R);
+    o.s[0] = gs_exp((T)p[3]); o.s[1] = gs_exp((T)p[4]); o.s[2] = gs_exp((T)p[5]);
+    const T s2[3] = {o.s[0] * o.s[0], o.s[1] * o.s[1], o.s[2] * o.s[2]};
     for (int a = 0; a < 3; a++)
         for (int b = a; b < 3; b++) {
-            float val = o.R[3 * a] * s2[0] * o.R[3 * b] + o.R[3 * a + 1] * s2[1] * o.R[3 * b + 1] +
-                        o.R[3 * a + 2] * s2[2] * o.R[3 * b + 2];
+            const T val = o.R[3 * a] * s2[0] * o.R[3 * b] + o.R[3 * a + 1] * s2[1] * o.R[3 * b + 1] +
+                          o.R[3 * a + 2] * s2[2] * o.R[3 * b + 2];
             o.S[3 * a + b] = val;
             o.S[3 * b + a] = val;
         }
-    float MS[6];
+    T MS[6];
     for (int r = 0; r < 2; r++)
         for (int c = 0; c < 3; c++) MS[3 * r + c] = o.M[3 * r] * o.S[c] + o.M[3 * r + 1] * o.S[3 + c] + o.M[3 * r + 2] * o.S[6 + c];
-    o.c00 = MS[0] * o.M[0] + MS[1] * o.M[1] + MS[2] * o.M[2] + GS_DILATION;
+    o.c00 = MS[0] * o.M[0] + MS[1] * o.M[1] + MS[2] * o.M[2] + (T)GS_DILATION;
     o.c01 = MS[0] * o.M[3] + MS[1] * o.M[4] + MS[2] * o.M[5];
-    o.c11 = MS[3] * o.M[3] + MS[4] * o.M[4] + MS[5] * o.M[5] + GS_DILATION;
+    o.c11 = MS[3] * o.M[3] + MS[4] * o.M[4] + MS[5] * o.M[5] + (T)GS_DILATION;
     o.det = o.c00 * o.c11 - o.c01 * o.c01;
-    v = v && (o.det > 1e-12f) && isfinite(o.det);
+    v = v && (o.det > (T)1e-12f) && isfinite(o.det);
     o.valid = v;
-    float dets = v ? o.det : 1.0f;
+    const T dets = v ? o.det : (T)1;
     o.ca = o.c11 / dets;
     o.cb = -o.c01 / dets;
     o.cc = o.c00 / dets;

@@ -20,13 +20,6 @@ constexpr int BW = LW + 10, BH = LH + 10;    // blurred-moment region (halo 5)
 constexpr int L_THREADS = 256;
 constexpr float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
 
-struct LossSmem {
-    float in_a[IH][IW], in_b[IH][IW];
-    float hx[5][IH][BW];   // horizontally blurred a, b, aa, bb, ab
-    float g[3][BH][BW];    // partials g_ua, g_uaa, g_uab (zero outside the image)
-    float ry[3][LH][BW];   // vertical adjoint
-    float red[2][L_THREADS / 32];
-};
 
 __device__ __forceinline__ int reflect_idx(int j, int n) {  // R/losses.py:31-42
     if (n == 1) return 0;
@@ -72,18 +65,44 @@ __global__ void loss_tables_kernel(float *tab_x, int w, float *tab_y, int h) {
     }
 }
 
-__global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
-                                                            const float *__restrict__ tab_x,
-                                                            const float *__restrict__ tab_y, float lam) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    LossSmem &sm = *reinterpret_cast<LossSmem *>(smem_raw);
+// normalised 11-tap Gaussian (sigma 1.5), R/losses.py:22-25, as fp32 immediates
+__device__ __forceinline__ float kw(int d) {
+    constexpr float K[11] = {0.001028380123898387f, 0.0075987582094967365f, 0.036000773310661316f,
+                             0.10936068743467331f, 0.21300554275512695f, 0.26601171493530273f,
+                             0.21300554275512695f, 0.10936068743467331f, 0.036000773310661316f,
+                             0.0075987582094967365f, 0.001028380123898387f};
+    return K[d];
+}
+
+// INTERIOR: the CTA's whole halo lies >= 10 px inside the image, so every blur / adjoint
+// weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
+struct SsimSmem {
+    // region A: inputs (2 x IH x IW), later the SSIM partials (3 x BH x BW)
+    // region B: horizontal moments (5 x IH x BW), later the vertical adjoint (3 x LH x BW)
+    float A[2 * IH * IW];
+    float B[5 * IH * BW];
+    float red[2][L_THREADS / 32];
+};
+
+template <bool INTERIOR>
+__device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
+                                          const float *__restrict__ tab_x, const float *__restrict__ tab_y,
+                                          float lam) {
+    float *smA = sm.A, *smB = sm.B;
+    float(*red)[L_THREADS / 32] = sm.red;
+    float(*in_a)[IW] = reinterpret_cast<float(*)[IW]>(smA);
+    float(*in_b)[IW] = reinterpret_cast<float(*)[IW]>(smA + IH * IW);
+    float(*g)[BH][BW] = reinterpret_cast<float(*)[BH][BW]>(smA);
+    float(*hx)[IH][BW] = reinterpret_cast<float(*)[IH][BW]>(smB);
+    float(*ry)[LH][BW] = reinterpret_cast<float(*)[LH][BW]>(smB);
+    static_assert(3 * BH * BW <= 2 * IH * IW && 3 * LH * BW <= 5 * IH * BW, "smem aliasing");
+
     const float *__restrict__ target = view->target;
     const int W = f.width, H = f.height;
     const int x0 = blockIdx.x * LW, y0 = blockIdx.y * LH;
     const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
     const int tid = threadIdx.x;
     float l1_acc = 0.0f, s_acc = 0.0f;
-    // each thread owns output pixels (tid % 32, tid / 32) and (.., +8)
     float grad_out[2][3];
     for (int c = 0; c < 3; c++) {
         __syncthreads();
@@ -92,38 +111,46 @@ __global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs
             const int iy = k / IW, ix = k % IW;
             const int y = y0 - 10 + iy, x = x0 - 10 + ix;
             float a = 0.0f, b = 0.0f;
-            if (x >= 0 && x < W && y >= 0 && y < H) {
+            if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
                 const int64_t p = (int64_t)y * W + x;
                 a = f.color[3 * p + c];
                 b = target[3 * p + c];
             }
-            sm.in_a[iy][ix] = a;
-            sm.in_b[iy][ix] = b;
+            in_a[iy][ix] = a;
+            in_b[iy][ix] = b;
         }
         __syncthreads();
+        // the two output pixels' own (a, b) are kept in registers: region A is reused below
+        float av[2], bv[2];
+#pragma unroll
+        for (int h = 0; h < 2; h++) {
+            av[h] = in_a[(tid >> 5) + 8 * h + 10][(tid & 31) + 10];
+            bv[h] = in_b[(tid >> 5) + 8 * h + 10][(tid & 31) + 10];
+        }
         // 2) horizontal blur of the 5 moments at columns [x0-5, x0+LW+5)
         for (int k = tid; k < IH * BW; k += L_THREADS) {
             const int iy = k / BW, bx = k % BW;
             const int x = x0 - 5 + bx;
             float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-            if (x >= 0 && x < W) {
+            if (INTERIOR || (x >= 0 && x < W)) {
                 const float *F = tab_x + 22 * x;
 #pragma unroll
                 for (int d = 0; d < 11; d++) {
-                    const float wgt = F[d];
-                    const float a = sm.in_a[iy][bx + d], b = sm.in_b[iy][bx + d];
-                    m0 += wgt * a;
-                    m1 += wgt * b;
-                    m2 += wgt * a * a;
-                    m3 += wgt * b * b;
-                    m4 += wgt * a * b;
+                    const float wgt = INTERIOR ? kw(d) : F[d];
+                    const float a = in_a[iy][bx + d], b = in_b[iy][bx + d];
+                    const float wa = wgt * a, wb = wgt * b;
+                    m0 += wa;
+                    m1 += wb;
+                    m2 += wa * a;
+                    m3 += wb * b;
+                    m4 += wa * b;
                 }
             }
-            sm.hx[0][iy][bx] = m0;
-            sm.hx[1][iy][bx] = m1;
-            sm.hx[2][iy][bx] = m2;
-            sm.hx[3][iy][bx] = m3;
-            sm.hx[4][iy][bx] = m4;
+            hx[0][iy][bx] = m0;
+            hx[1][iy][bx] = m1;
+            hx[2][iy][bx] = m2;
+            hx[3][iy][bx] = m3;
+            hx[4][iy][bx] = m4;
         }
         __syncthreads();
         // 3) vertical blur -> SSIM map and its partials at [y0-5, y0+LH+5) x [x0-5, x0+LW+5)
@@ -131,32 +158,32 @@ __global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs
             const int by = k / BW, bx = k % BW;
             const int y = y0 - 5 + by, x = x0 - 5 + bx;
             float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-            if (x >= 0 && x < W && y >= 0 && y < H) {
+            if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
                 const float *F = tab_y + 22 * y;
                 float ua = 0.f, ub = 0.f, uaa = 0.f, ubb = 0.f, uab = 0.f;
 #pragma unroll
                 for (int d = 0; d < 11; d++) {
-                    const float wgt = F[d];
-                    ua += wgt * sm.hx[0][by + d][bx];
-                    ub += wgt * sm.hx[1][by + d][bx];
-                    uaa += wgt * sm.hx[2][by + d][bx];
-                    ubb += wgt * sm.hx[3][by + d][bx];
-                    uab += wgt * sm.hx[4][by + d][bx];
+                    const float wgt = INTERIOR ? kw(d) : F[d];
+                    ua += wgt * hx[0][by + d][bx];
+                    ub += wgt * hx[1][by + d][bx];
+                    uaa += wgt * hx[2][by + d][bx];
+                    ubb += wgt * hx[3][by + d][bx];
+                    uab += wgt * hx[4][by + d][bx];
                 }
                 // R/losses.py:96-113
                 const float va = uaa - ua * ua, vb = ubb - ub * ub, vab = uab - ua * ub;
                 const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
                 const float b1 = ua * ua + ub * ub + C1, b2 = va + vb + C2;
-                const float den = b1 * b2;
-                const float S = (a1 * a2) / den;
-                g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) / den - S * (2.0f * ua / b1) + S * (2.0f * ua / b2)) * inv_n;
+                const float rden = 1.0f / (b1 * b2);
+                const float S = (a1 * a2) * rden;
+                g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua / b1) + S * (2.0f * ua / b2)) * inv_n;
                 g1 = (-S / b2) * inv_n;
-                g2 = (2.0f * a1 / den) * inv_n;
+                g2 = (2.0f * a1 * rden) * inv_n;
                 if (by >= 5 && by < 5 + LH && bx >= 5 && bx < 5 + LW) s_acc += S;
             }
-            sm.g[0][by][bx] = g0;
-            sm.g[1][by][bx] = g1;
-            sm.g[2][by][bx] = g2;
+            g[0][by][bx] = g0;
+            g[1][by][bx] = g1;
+            g[2][by][bx] = g2;
         }
         __syncthreads();
         // 4) vertical adjoint at rows [y0, y0+LH): sum_d F[p+d][-d] g(p+d)
@@ -164,19 +191,19 @@ __global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs
             const int oy = k / BW, bx = k % BW;
             const int y = y0 + oy;
             float r0 = 0.f, r1 = 0.f, r2 = 0.f;
-            if (y < H) {
+            if (INTERIOR || y < H) {
                 const float *A = tab_y + 22 * y + 11;  // zero weights where y+d leaves the image
 #pragma unroll
                 for (int d = 0; d < 11; d++) {
-                    const float wgt = A[d];
-                    r0 += wgt * sm.g[0][oy + d][bx];
-                    r1 += wgt * sm.g[1][oy + d][bx];
-                    r2 += wgt * sm.g[2][oy + d][bx];
+                    const float wgt = INTERIOR ? kw(d) : A[d];
+                    r0 += wgt * g[0][oy + d][bx];
+                    r1 += wgt * g[1][oy + d][bx];
+                    r2 += wgt * g[2][oy + d][bx];
                 }
             }
-            sm.ry[0][oy][bx] = r0;
-            sm.ry[1][oy][bx] = r1;
-            sm.ry[2][oy][bx] = r2;
+            ry[0][oy][bx] = r0;
+            ry[1][oy][bx] = r1;
+            ry[2][oy][bx] = r2;
         }
         __syncthreads();
         // 5) horizontal adjoint + gradient assembly for this channel
@@ -185,17 +212,17 @@ __global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs
             const int ox = tid & 31, oy = (tid >> 5) + 8 * h;
             const int x = x0 + ox, y = y0 + oy;
             float gsum = 0.0f;
-            if (x < W && y < H) {
+            if (INTERIOR || (x < W && y < H)) {
                 float A0 = 0.f, A1 = 0.f, A2 = 0.f;
                 const float *Aw = tab_x + 22 * x + 11;
 #pragma unroll
                 for (int d = 0; d < 11; d++) {
-                    const float wgt = Aw[d];
-                    A0 += wgt * sm.ry[0][oy][ox + d];
-                    A1 += wgt * sm.ry[1][oy][ox + d];
-                    A2 += wgt * sm.ry[2][oy][ox + d];
+                    const float wgt = INTERIOR ? kw(d) : Aw[d];
+                    A0 += wgt * ry[0][oy][ox + d];
+                    A1 += wgt * ry[1][oy][ox + d];
+                    A2 += wgt * ry[2][oy][ox + d];
                 }
-                const float a = sm.in_a[oy + 10][ox + 10], b = sm.in_b[oy + 10][ox + 10];
+                const float a = av[h], b = bv[h];
                 const float diff = a - b;
                 l1_acc += fabsf(diff);
                 const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
@@ -224,21 +251,34 @@ __global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs
         s_acc += __shfl_xor_sync(0xffffffffu, s_acc, o);
     }
     if ((tid & 31) == 0) {
-        sm.red[0][tid >> 5] = l1_acc;
-        sm.red[1][tid >> 5] = s_acc;
+        red[0][tid >> 5] = l1_acc;
+        red[1][tid >> 5] = s_acc;
     }
     __syncthreads();
     if (tid == 0) {
         double l1 = 0.0, ss = 0.0;
         for (int w = 0; w < L_THREADS / 32; w++) {
-            l1 += sm.red[0][w];
-            ss += sm.red[1][w];
+            l1 += red[0][w];
+            ss += red[1][w];
         }
         const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
         f.loss_parts[3 * blk] = l1;
         f.loss_parts[3 * blk + 1] = ss;
         f.loss_parts[3 * blk + 2] = 0.0;
     }
+}
+
+// one launch for every tile: interior tiles (halo >= 10 px inside the image) take the
+// compile-time-weight path, border tiles the reflection-table path
+__global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
+                                                            const float *__restrict__ tab_x,
+                                                            const float *__restrict__ tab_y, float lam) {
+    __shared__ SsimSmem sm;
+    const int x0 = blockIdx.x * LW, y0 = blockIdx.y * LH;
+    if (x0 >= 10 && x0 + LW + 10 <= f.width && y0 >= 10 && y0 + LH + 10 <= f.height)
+        ssim_tile<true>(sm, f, view, tab_x, tab_y, lam);
+    else
+        ssim_tile<false>(sm, f, view, tab_x, tab_y, lam);
 }
 
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
@@ -334,9 +374,8 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     loss_tables_kernel<<<(f->width + f->height + 127) / 128, 128, 0, st>>>(tab_x, f->width, tab_y, f->height);
     int rc = check_launch("loss_tables_kernel");
     if (rc) return rc;
-    static_assert(sizeof(LossSmem) < 200 * 1024, "loss smem");
     dim3 grid((f->width + LW - 1) / LW, (f->height + LH - 1) / LH);
-    ssim_l1_kernel<<<grid, L_THREADS, sizeof(LossSmem), st>>>(*f, view, tab_x, tab_y, lam);
+    ssim_l1_kernel<<<grid, L_THREADS, 0, st>>>(*f, view, tab_x, tab_y, lam);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     depth_loss_kernel<<<DEPTH_BLOCKS, 256, 0, st>>>(*f, view, xi, ssim_blocks);
     if ((rc = check_launch("depth_loss_kernel"))) return rc;
@@ -346,6 +385,6 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
 
 namespace gs {
 void init_loss_attrs() {
-    cudaFuncSetAttribute(ssim_l1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LossSmem));
+    cudaFuncSetAttribute(ssim_l1_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 }  // namespace gs

@@ -68,8 +68,21 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             f.kept[i] = 0;
             f.keys_a[i] = (0xffffffffull << 32) | (uint64_t)i;
         } else {
+            // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians near
+            // the 0.01 m clip plane, and fp32 would shift their whole footprint
+            ProjectedT<double> pd;
+            project_full<double>(p, cam, pd);
             Projected pr;
-            project_full(p, cam, pr);
+            pr.mu[2] = (float)pd.mu[2];
+            pr.mx = (float)pd.mx;
+            pr.my = (float)pd.my;
+            pr.c00 = (float)pd.c00;
+            pr.c01 = (float)pd.c01;
+            pr.c11 = (float)pd.c11;
+            pr.ca = (float)pd.ca;
+            pr.cb = (float)pd.cb;
+            pr.cc = (float)pd.cc;
+            pr.valid = pd.valid;
             const float op = 1.0f / (1.0f + expf(-p[10]));
             // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
             const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
@@ -102,7 +115,8 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             touched = kept > 0;
             s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
             s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-            s2[2] = make_float4(col[0], col[1], col[2], 0.0f);
+            // 1 - opacity = sigmoid(-logit), kept exact for the blend's 1 - alpha
+            s2[2] = make_float4(col[0], col[1], col[2], 1.0f / (1.0f + expf(p[10])));
             *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
             *rc = rect;
             f.valid[i] = pr.valid ? 1 : 0;
@@ -250,7 +264,8 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
     s2[0] = make_float4(mx, my, ca, cb);
     s2[1] = make_float4(cc, o, depth[i], qcut);
-    s2[2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 0.f) : make_float4(0.f, 0.f, 0.f, 0.f);
+    s2[2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 1.0f - o)
+                   : make_float4(0.f, 0.f, 0.f, 1.0f - o);
     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(c00, c01, c11, radius);
     reinterpret_cast<int4 *>(f.rect)[i] = rect;
     f.valid[i] = v;

@@ -23,6 +23,23 @@ __device__ __forceinline__ float quad(float ca, float cb, float cc, float dx, fl
     return ca * dx * dx + 2.0f * cb * dx * dy + cc * dy * dy;
 }
 
+// alpha = min(o e^{-q/2}, 0.99) (R/rasterizer.py:270-272) and 1 - alpha.  1 - alpha is formed
+// with one rounding (FMA) and is exactly 0.01 on the clamp, so the transmittance product does
+// not pick up the cancellation of 1 - 0.99f.  (omo = 1 - o is carried in the splat record for
+// the higher-accuracy variant 1 - o e = (1 - e) + (1 - o) e.)
+__device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &araw, float &alpha, float &oma) {
+    (void)omo;
+    const float e = exp2f(-0.5f * GS_LOG2E * q);
+    araw = op * e;
+    if (araw > GS_ALPHA_CLAMP) {
+        alpha = GS_ALPHA_CLAMP;
+        oma = 0.01f;
+    } else {
+        alpha = araw;
+        oma = fmaf(-op, e, 1.0f);
+    }
+}
+
 __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_stop) {
     __shared__ float4 s_a[RT];  // mx my ca cb
     __shared__ float4 s_b[RT];  // cc opacity depth -
@@ -52,18 +69,17 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
         if (!done) {
             const int nb = min(RT, stop - b);
             for (int j = 0; j < nb; j++) {
-                const float4 A = s_a[j], B = s_b[j];
+                const float4 A = s_a[j], B = s_b[j], C = s_c[j];
                 const float dx = fx - A.x, dy = fy - A.y;
-                const float q = quad(A.z, A.w, B.x, dx, dy);
-                const float alpha = fminf(B.y * exp2f(NEG_HALF_LOG2E * q), GS_ALPHA_CLAMP);
+                float araw, alpha, oma;
+                alpha_oma(B.y, C.w, quad(A.z, A.w, B.x, dx, dy), araw, alpha, oma);
                 const float w = alpha * T;
-                const float4 C = s_c[j];
                 c0 += C.x * w;
                 c1 += C.y * w;
                 c2 += C.z * w;
                 dsum += B.z * w;
                 osum += w;
-                T *= 1.0f - alpha;
+                T *= oma;
                 if (early_stop && T < GS_EARLY_STOP_T) {
                     done = true;
                     cnt = b - start + j + 1;
@@ -177,10 +193,8 @@ __global__ void __launch_bounds__(RT) render_bwd_kernel(gs_frame f) {
                 const float4 A = s_a[j], B = s_b[j], C = s_c[j];
                 const float dx = fx - A.x, dy = fy - A.y;
                 const float ca = A.z, cb = A.w, cc = B.x, op = B.y, dep = B.z;
-                const float q = quad(ca, cb, cc, dx, dy);
-                const float araw = op * exp2f(NEG_HALF_LOG2E * q);
-                const float alpha = fminf(araw, GS_ALPHA_CLAMP);
-                const float om = 1.0f - alpha;
+                float araw, alpha, om;
+                alpha_oma(op, C.w, quad(ca, cb, cc, dx, dy), araw, alpha, om);
                 const float Tb = T / om;
                 const float w = alpha * Tb;
                 v[6] = w * gc0;
@@ -211,25 +225,24 @@ __global__ void __launch_bounds__(RT) render_bwd_kernel(gs_frame f) {
         }
         __syncthreads();
         if ((int)threadIdx.x < nb) {
+            // cross-tile accumulation in FP64: a large Gaussian collects thousands of per-tile
+            // partial sums of mixed sign (near-plane splats cover every tile of the image)
             const float *a = s_acc[threadIdx.x];
-            float4 *dst = reinterpret_cast<float4 *>(f.g2d) + (int64_t)s_g[threadIdx.x] * (GS_G2D / 4);
-            const float4 v0 = make_float4(a[0], a[1], a[2], a[3]);
-            const float4 v1 = make_float4(a[4], a[5], a[6], a[7]);
-            const float4 v2 = make_float4(a[8], a[9], 0.0f, 0.0f);
-            if (v0.x != 0.f || v0.y != 0.f || v0.z != 0.f || v0.w != 0.f) atomicAdd(dst, v0);
-            if (v1.x != 0.f || v1.y != 0.f || v1.z != 0.f || v1.w != 0.f) atomicAdd(dst + 1, v1);
-            if (v2.x != 0.f || v2.y != 0.f) atomicAdd(dst + 2, v2);
+            double *dst = f.g2d + (int64_t)s_g[threadIdx.x] * GS_G2D;
+#pragma unroll
+            for (int k = 0; k < 10; k++)
+                if (a[k] != 0.0f) atomicAdd(dst + k, (double)a[k]);
         }
     }
 }
 
-// zero the g2d rows of the touched Gaussians (3 float4 per row, touched list order)
+// zero the g2d rows of the touched Gaussians (12 doubles = 6 double2 per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
-    if (i >= 3 * nt) return;
-    const int64_t g = f.touched_list[i / 3];
-    reinterpret_cast<float4 *>(f.g2d)[g * (GS_G2D / 4) + i % 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i >= 6 * nt) return;
+    const int64_t g = f.touched_list[i / 6];
+    reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + i % 6] = make_double2(0.0, 0.0);
 }
 
 }  // namespace gs
@@ -247,7 +260,7 @@ extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
     if (f->n > 0) {  // each backward starts from zero gradients (backward_2d is a pure function)
-        zero_g2d_kernel<<<(unsigned)((f->n * 3 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
+        zero_g2d_kernel<<<(unsigned)((f->n * 6 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
         int rc = check_launch("zero_g2d_kernel");
         if (rc) return rc;
     }

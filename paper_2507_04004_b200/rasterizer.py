@@ -153,7 +153,7 @@ class Workspace:
         self.cov2d = self.view("cov2d", "f32", (n, 4))
         self.valid = self.view("valid", "u8", (n,))
         self.touched = self.view("touched", "u8", (n,))
-        self.g2d = self.view("g2d", "f32", (n, GS_G2D))
+        self.g2d = self.view("g2d", "f64", (n, GS_G2D))
         self.counters = self.view("counters", "i32", (2 * _lib.GS_CNT_SLOTS,))
         self.entry_splat = self.view("entry_splat", "i32", (max(self.capacity, 1),))
         self.tile_offsets = self.view("tile_offsets", "i32", (self.tiles_x * self.tiles_y + 1,))
