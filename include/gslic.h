@@ -100,6 +100,8 @@ typedef struct gs_frame {
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
     double *g2d;             /* n x GS_G2D screen-space gradients, FP64 accumulators (touched rows) */
+    float *grad_rows;        /* n x GS_ROW parameter gradients in touched-list order */
+    float *bias_corr;        /* n x 2 Adam bias corrections (1-b1^t, 1-b2^t) in touched-list order */
     uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
     int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
     int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */

@@ -203,16 +203,28 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
         chain_row(srow[warp][lane], gv, scam, sgr[warp][lane]);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
-        if (mode == 0) {
+        if (mode == 0 || mode == 2) {
             const int tn = at[g] + 1;
             at[g] = tn;
-            sbc[warp][lane][0] = (float)(1.0 - pow(0.9, (double)tn));
-            sbc[warp][lane][1] = (float)(1.0 - pow(0.999, (double)tn));
+            const float bc1 = (float)(1.0 - pow(0.9, (double)tn)), bc2 = (float)(1.0 - pow(0.999, (double)tn));
+            sbc[warp][lane][0] = bc1;
+            sbc[warp][lane][1] = bc2;
+            if (mode == 2) reinterpret_cast<float2 *>(f.bias_corr)[k] = make_float2(bc1, bc2);
         } else {
             touched_accum[g] = 1;
         }
     }
     __syncwarp();
+    if (mode == 2) {  // gradient rows in touched-list order, streamed by adam_list_kernel
+#pragma unroll 4
+        for (int j = 0; j < 16; j++) {
+            const int kk = lane + 32 * j, r = kk >> 4, c4 = kk & 15;
+            if (k0 + r >= nt) continue;
+            const float *G = &sgr[warp][r][4 * c4];
+            reinterpret_cast<float4 *>(f.grad_rows)[(k0 + r) * (GS_ROW / 4) + c4] = make_float4(G[0], G[1], G[2], G[3]);
+        }
+        return;
+    }
 #pragma unroll 2
     for (int j = 0; j < 16; j++) {
         const int kk = lane + 32 * j, r = kk >> 4, c4 = kk & 15;
@@ -245,6 +257,36 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
             acc.w += G[3];
             *reinterpret_cast<float4 *>(grads + off) = acc;
         }
+    }
+}
+
+// sparse Adam streamed over the touched list: 16 threads per 256-B row, gradient rows and
+// bias corrections produced by chain_kernel (mode 2) in the same order
+__global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__restrict__ params,
+                                                        float *__restrict__ am, float *__restrict__ av,
+                                                        const float *__restrict__ lr_cols) {
+    const int64_t nt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nt * 16;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = idx >> 4;
+        const int c4 = (int)(idx & 15);
+        if (c4 == 15) continue;  // columns 60-63: padding
+        const int64_t g = f.touched_list[k];
+        const float2 bc = reinterpret_cast<const float2 *>(f.bias_corr)[k];
+        const float4 G = reinterpret_cast<const float4 *>(f.grad_rows)[k * (GS_ROW / 4) + c4];
+        const int64_t off = g * GS_ROW + 4 * c4;
+        const float4 P = *reinterpret_cast<const float4 *>(params + off);
+        float4 m4 = *reinterpret_cast<const float4 *>(am + off);
+        float4 v4 = *reinterpret_cast<const float4 *>(av + off);
+        const float4 lr = __ldg(reinterpret_cast<const float4 *>(lr_cols) + c4);
+        float4 p4;
+        p4.x = adam_one(P.x, m4.x, v4.x, G.x, lr.x, bc.x, bc.y);
+        p4.y = adam_one(P.y, m4.y, v4.y, G.y, lr.y, bc.x, bc.y);
+        p4.z = adam_one(P.z, m4.z, v4.z, G.z, lr.z, bc.x, bc.y);
+        p4.w = c4 == 14 ? P.w : adam_one(P.w, m4.w, v4.w, G.w, lr.w, bc.x, bc.y);  // column 59: padding
+        *reinterpret_cast<float4 *>(am + off) = m4;
+        *reinterpret_cast<float4 *>(av + off) = v4;
+        *reinterpret_cast<float4 *>(params + off) = p4;
     }
 }
 
@@ -302,7 +344,13 @@ extern "C" int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, fl
         set_error("gs_chain_adam: null argument");
         return GS_ERR_ARG;
     }
-    return launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 0, nullptr, nullptr, stream);
+    // chain rule (FP64 geometry, low occupancy) writes compact gradient rows; a separate
+    // bandwidth-bound kernel streams the Adam update over the touched rows
+    int rc = launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 2, nullptr, nullptr, stream);
+    if (rc) return rc;
+    if (f->n == 0) return GS_OK;
+    adam_list_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols);
+    return check_launch("adam_list_kernel");
 }
 
 extern "C" int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum,

@@ -74,6 +74,8 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.touched = c.take<uint8_t>(nn);
     f.touched_list = c.take<int32_t>(nn);
     f.g2d = c.take<double>(GS_G2D * nn);
+    f.grad_rows = c.take<float>((int64_t)GS_ROW * nn);
+    f.bias_corr = c.take<float>(2 * nn);
     f.keep_bits = c.take<uint64_t>(nn);
     f.kept = c.take<int32_t>(nn);
     f.counts = c.take<int32_t>(nn + 1);

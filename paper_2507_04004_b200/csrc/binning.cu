@@ -90,12 +90,13 @@ __global__ void radix_bins_kernel(uint32_t *hist) {
 // one onesweep pass: stable counting-sort of a 4096-key tile by one 8-bit digit, decoupled
 // look-back across tiles for the per-digit global offsets, scatter through shared memory.
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const K *__restrict__ in, K *__restrict__ out,
+__global__ void __launch_bounds__(RS_THREADS, sizeof(K) == 4 ? 4 : 3) onesweep_kernel(const K *__restrict__ in, K *__restrict__ out,
                                                               int64_t n_host, const int32_t *__restrict__ n_dev,
                                                               int shift, const uint32_t *__restrict__ bins,
                                                               uint32_t *status, int32_t *ticket, int filter) {
     constexpr int WARPS = RS_THREADS / 32;
-    __shared__ uint32_t s_warp[WARPS][256];
+    // digit 256 is a dummy bucket for out-of-range and filtered items (never scattered)
+    __shared__ uint32_t s_warp[WARPS][257];
     __shared__ uint32_t s_start[256];
     __shared__ uint32_t s_base[256];
     __shared__ uint32_t s_scan[WARPS];
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const K *__restric
 
     const int64_t n = n_dev ? (int64_t)*n_dev : n_host;
     if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1);
-    for (int k = threadIdx.x; k < WARPS * 256; k += RS_THREADS) (&s_warp[0][0])[k] = 0u;
+    for (int k = threadIdx.x; k < WARPS * 257; k += RS_THREADS) (&s_warp[0][0])[k] = 0u;
     __syncthreads();
     const int tile = s_tile;
     const int64_t tbase = (int64_t)tile * RS_TILE;
@@ -115,28 +116,24 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const K *__restric
     const unsigned ltmask = lanemask_lt();
 
     K key[RS_ITEMS];
+    uint32_t dig[RS_ITEMS];
     uint32_t rank[RS_ITEMS];
-    bool ok[RS_ITEMS];
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
-        int64_t idx = wbase + i * 32 + lane;
-        ok[i] = idx < n;
-        key[i] = ok[i] ? in[idx] : (K)0;
-        if (ok[i] && inactive_key(key[i], filter)) ok[i] = false;
+        const int64_t idx = wbase + i * 32 + lane;
+        key[i] = idx < n ? in[idx] : (K)0;
+        dig[i] = (idx < n && !inactive_key(key[i], filter)) ? ((uint32_t)(key[i] >> shift) & 255u) : 256u;
     }
-    // warp-level stable ranking: items in order, lanes in order
+    // warp-level stable ranking (items in order, lanes in order): the highest lane of each
+    // peer group bumps the warp's digit counter and broadcasts the old value
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
-        const unsigned active = __ballot_sync(0xffffffffu, ok[i]);
-        if (ok[i]) {
-            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
-            const unsigned peers = __match_any_sync(active, d);
-            const uint32_t before = s_warp[warp][d];
-            rank[i] = before + __popc(peers & ltmask);
-            __syncwarp(active);
-            if (lane == 31 - __clz(peers)) s_warp[warp][d] = before + __popc(peers);
-        }
-        __syncwarp();
+        const unsigned peers = __match_any_sync(0xffffffffu, dig[i]);
+        const int leader = 31 - __clz(peers);
+        uint32_t before = 0;
+        if (lane == leader) before = atomicAdd(&s_warp[warp][dig[i]], (uint32_t)__popc(peers));
+        before = __shfl_sync(0xffffffffu, before, leader);
+        rank[i] = before + __popc(peers & ltmask);
     }
     __syncthreads();
     // per-digit warp offsets and tile totals; thread t owns digit t
@@ -185,10 +182,8 @@ __global__ void __launch_bounds__(RS_THREADS) onesweep_kernel(const K *__restric
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < RS_ITEMS; i++) {
-        if (ok[i]) {
-            const uint32_t d = (uint32_t)(key[i] >> shift) & 255u;
-            s_keys[s_start[d] + s_warp[warp][d] + rank[i]] = key[i];
-        }
+        const uint32_t d = dig[i];
+        if (d < 256u) s_keys[s_start[d] + s_warp[warp][d] + rank[i]] = key[i];
     }
     __syncthreads();
     const uint32_t total = s_total;
