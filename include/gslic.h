@@ -65,8 +65,16 @@ enum {
     GS_CNT_BIG = 5,      /* Gaussians culled warp-cooperatively (many candidate tiles) */
     GS_CNT_BIG_EMIT = 6, /* ... and emitted warp-cooperatively */
     GS_CNT_BIG_BITS = 7, /* words of big_bits in use */
-    GS_CNT_SLOTS = 16
+    GS_CNT_SLOTS = 16,
+    /* slots 8-15: look-back tickets; second half of the counters array: */
+    GS_CNT_HUGE = 16,    /* screen-covering Gaussians binned per tile by bitmap (not sorted) */
+    GS_CNT_HUGE_E = 17,  /* their kept pairs */
+    GS_CNT_SMALL_E = 18, /* entries emitted into the tile sort (0 after an overflow) */
+    GS_CNT_HUGE_N = 19   /* huge Gaussians with >= 1 kept tile (records in depth order) */
 };
+
+#define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */
+#define GS_HUGE_CAP 4096 /* at most this many such Gaussians per view (the rest take the sort) */
 
 /* Pinhole camera, world->camera (R/rasterizer.py:47-67).  Pixel centres are integers. */
 typedef struct gs_camera {
@@ -107,6 +115,10 @@ typedef struct gs_frame {
     int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */
     int32_t *big_list;       /* n: Gaussians with > GS_SMALL_CAND candidate tiles (warp-culled) */
     int32_t *big_emit;       /* n: depth ranks of those Gaussians (warp-emitted) */
+    int32_t *huge;           /* GS_HUGE_CAP x 8: screen-covering Gaussians in depth order (id,
+                                rank, rect, bitmap base) + compaction scratch */
+    uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: which huge Gaussians keep each tile */
+    int32_t *tile_scratch;   /* 2 x (tiles + 1): per-tile sorted-entry offsets, huge counts */
     uint32_t *big_bits;      /* cull bitmaps of the large-footprint Gaussians (base in keep_bits) */
     int64_t big_bits_words;  /* capacity of big_bits; overflowing Gaussians are re-culled at emit */
     /* sort buffers */

@@ -81,6 +81,9 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.counts = c.take<int32_t>(nn + 1);
     f.big_list = c.take<int32_t>(nn);
     f.big_emit = c.take<int32_t>(nn);
+    f.huge = c.take<int32_t>(8 * GS_HUGE_CAP + (nn + 1023) / 1024 + 1);
+    f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
+    f.tile_scratch = c.take<int32_t>(2 * ((int64_t)tx * ty + 1));
     f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
     f.big_bits = c.take<uint32_t>(f.big_bits_words);
     f.keys_a = c.take<uint64_t>(keys);

@@ -219,8 +219,9 @@ __global__ void __launch_bounds__(RS_THREADS) scan_kernel(const int32_t *__restr
     const int64_t mybase = tbase + (int64_t)threadIdx.x * SC_ITEMS;
 #pragma unroll
     for (int i = 0; i < SC_ITEMS; i++) {
-        // value of rank mybase+i: kept count of the Gaussian at that depth rank
-        v[i] = (mybase + i < n) ? (uint32_t)vals[(uint32_t)perm[mybase + i]] : 0u;
+        // value of rank mybase+i: kept count of the Gaussian at that depth rank (huge
+        // Gaussians, encoded negative, emit nothing into the sort)
+        v[i] = (mybase + i < n) ? (uint32_t)max(vals[(uint32_t)perm[mybase + i]], 0) : 0u;
         sum += v[i];
     }
     uint32_t x = sum;
@@ -286,6 +287,8 @@ __global__ void __launch_bounds__(256) emit_kernel(gs_frame f, const uint64_t *_
     const int64_t n_sorted = f.counters[GS_CNT_ACTIVE];
     if (k >= n_sorted || f.counters[GS_CNT_OVERFLOW]) return;
     const uint32_t g = (uint32_t)sorted[k];
+    const int kept = f.kept[g];
+    if (kept < 0) return;  // screen-covering: binned per tile by huge_count/merge
     int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
     if (!cull) r = make_int4(0, f.tiles_x - 1, 0, f.tiles_y - 1);
     const int nx = r.y - r.x + 1;
@@ -350,28 +353,231 @@ __global__ void __launch_bounds__(256) emit_big_kernel(gs_frame f, const uint64_
     }
 }
 
-// tile_offsets[t] = first entry with tile >= t; entry_splat[e] = the entry's Gaussian id
-// (64-bit words carry it; 32-bit words carry the depth rank, mapped through depth_sorted)
+// per-tile ranges of the tile-sorted (non-huge) entry words: small_off[t] = first word with
+// tile >= t (adjacent-word compares)
 template <typename K>
-__global__ void ranges_kernel(gs_frame f, const K *__restrict__ sorted, int rank_bits,
-                              const uint64_t *__restrict__ depth_sorted) {
-    const int64_t E = f.counters[GS_CNT_ENTRIES_EFF];
+__global__ void ranges_kernel(gs_frame f, const K *__restrict__ sorted, int rank_bits) {
+    const int64_t E = f.counters[GS_CNT_SMALL_E];
     const int32_t T = f.tiles_x * f.tiles_y;
+    int32_t *small_off = f.tile_scratch;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int tshift = rank_bits ? rank_bits : 32;
     if (E == 0) {
-        for (int64_t t = e; t <= T; t += (int64_t)gridDim.x * blockDim.x) f.tile_offsets[t] = 0;
+        for (int64_t t = e; t <= T; t += (int64_t)gridDim.x * blockDim.x) small_off[t] = 0;
         return;
     }
     for (int64_t i = e; i < E; i += (int64_t)gridDim.x * blockDim.x) {
-        const K w = sorted[i];
-        const int32_t tile = (int32_t)((uint64_t)w >> tshift);
-        f.entry_splat[i] = rank_bits ? (int32_t)(uint32_t)depth_sorted[(uint32_t)w & ((1u << rank_bits) - 1u)]
-                                     : (int32_t)(uint32_t)w;
+        const int32_t tile = (int32_t)((uint64_t)sorted[i] >> tshift);
         const int32_t prev = i == 0 ? -1 : (int32_t)((uint64_t)sorted[i - 1] >> tshift);
-        for (int32_t t = prev + 1; t <= tile; t++) f.tile_offsets[t] = (int32_t)i;
+        for (int32_t t = prev + 1; t <= tile; t++) small_off[t] = (int32_t)i;
         if (i == E - 1)
-            for (int32_t t = tile + 1; t <= T; t++) f.tile_offsets[t] = (int32_t)E;
+            for (int32_t t = tile + 1; t <= T; t++) small_off[t] = (int32_t)E;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// screen-covering ("huge") Gaussians: binned per tile from their cull bitmaps in depth order,
+// then merged with the tile's sorted entries.  They never enter the emit + sort.
+
+// Huge records (depth order), 8 ints each: id, rank, rect (tx0 tx1 ty0 ty1), bitmap base (lo, hi)
+constexpr int HREC = 8;
+constexpr int HCHUNK = 1024;
+
+// ordered compaction of the huge Gaussians from the depth-sorted list, pass 1: counts per chunk
+__global__ void __launch_bounds__(HCHUNK) huge_flag_count_kernel(gs_frame f, const uint64_t *__restrict__ sorted) {
+    __shared__ int s;
+    if (f.counters[GS_CNT_HUGE] == 0) return;
+    if (threadIdx.x == 0) s = 0;
+    __syncthreads();
+    const int64_t k = (int64_t)blockIdx.x * HCHUNK + threadIdx.x;
+    const bool h = k < f.counters[GS_CNT_ACTIVE] && f.kept[(uint32_t)sorted[k]] < 0;
+    const unsigned m = __ballot_sync(0xffffffffu, h);
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&s, __popc(m));
+    __syncthreads();
+    if (threadIdx.x == 0) f.huge[HREC * GS_HUGE_CAP + blockIdx.x] = s;
+}
+
+// pass 2: each chunk sums its predecessors and writes its huge records in order
+__global__ void __launch_bounds__(HCHUNK) huge_write_kernel(gs_frame f, const uint64_t *__restrict__ sorted) {
+    __shared__ int s_warp[HCHUNK / 32];
+    __shared__ int s_base;
+    if (f.counters[GS_CNT_HUGE] == 0) return;
+    const int32_t *chunk_cnt = f.huge + HREC * GS_HUGE_CAP;
+    if (threadIdx.x == 0) s_base = 0;
+    __syncthreads();
+    int acc = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += HCHUNK) acc += chunk_cnt[c];
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(&s_base, acc);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t k = (int64_t)blockIdx.x * HCHUNK + threadIdx.x;
+    uint32_t g = 0;
+    bool h = false;
+    if (k < f.counters[GS_CNT_ACTIVE]) {
+        g = (uint32_t)sorted[k];
+        h = f.kept[g] < 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) s_warp[warp] = __popc(m);
+    __syncthreads();
+    int pos = s_base;
+    for (int w = 0; w < warp; w++) pos += s_warp[w];
+    pos += __popc(m & ((1u << lane) - 1u));
+    if (h && pos < GS_HUGE_CAP) {
+        int4 *rec = reinterpret_cast<int4 *>(f.huge + HREC * pos);
+        rec[0] = make_int4((int)g, (int)k, -f.kept[g] - 1, 0);  // id, depth rank, huge slot
+    }
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < HCHUNK / 32; w++) tot += s_warp[w];
+        if (tot) atomicAdd(&f.counters[GS_CNT_HUGE_N], tot);
+    }
+}
+
+// warp per tile: huge Gaussians keeping the tile = popcount of its slot mask (set by
+// cull_big_kernel)
+__global__ void __launch_bounds__(256) huge_count_kernel(gs_frame f) {
+    const int T = f.tiles_x * f.tiles_y;
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= T) return;
+    const int nslots = min(f.counters[GS_CNT_HUGE], GS_HUGE_CAP);
+    const uint32_t *mask = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
+    int cnt = 0;
+    for (int w = lane; w < (nslots + 31) >> 5; w += 32) cnt += __popc(mask[w]);
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) f.tile_scratch[T + 1 + t] = cnt;
+}
+
+// one CTA: tile_offsets = exclusive scan of (sorted entries + huge entries) per tile; E total
+__global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f) {
+    __shared__ int32_t s_warp[32];
+    __shared__ int32_t s_carry;
+    const int T = f.tiles_x * f.tiles_y;
+    const int32_t *small_off = f.tile_scratch, *hcount = f.tile_scratch + T + 1;
+    const bool use_huge = min(f.counters[GS_CNT_HUGE], GS_HUGE_CAP) > 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int t0 = 0; t0 < T; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        const int v = t < T ? (small_off[t + 1] - small_off[t]) + (use_huge ? hcount[t] : 0) : 0;
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        int before = s_carry, total = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+            before += w < warp ? s_warp[w] : 0;
+            total += s_warp[w];
+        }
+        if (t < T) f.tile_offsets[t] = before + x - v;
+        __syncthreads();
+        if (threadIdx.x == 0) s_carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const int64_t E = s_carry;
+        f.tile_offsets[T] = (int32_t)E;
+        f.counters[GS_CNT_ENTRIES] = (int32_t)E;
+        const bool over = f.counters[GS_CNT_OVERFLOW] || E > f.entry_capacity;
+        if (over) f.counters[GS_CNT_OVERFLOW] = 1;
+        f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
+    }
+}
+
+// CTA per tile: merge the tile's huge Gaussians (depth order, from the bitmaps) with its
+// tile-sorted entries (depth order) by depth rank; write entry_splat.  Ranks are unique
+// within a tile, so each element's output slot is its index plus a lower bound in the other
+// list.  On an overflow every tile range is emptied instead.
+constexpr int MERGE_B = 2048;
+
+template <typename K>
+__global__ void __launch_bounds__(256) merge_kernel(gs_frame f, const K *__restrict__ sorted, int rank_bits,
+                                                    const uint64_t *__restrict__ depth_sorted) {
+    __shared__ int32_t s_arank[GS_HUGE_CAP], s_aid[GS_HUGE_CAP];
+    __shared__ int32_t s_brank[MERGE_B];
+    __shared__ int s_warp[8];
+    __shared__ int s_na;
+    const int T = f.tiles_x * f.tiles_y;
+    const int t = blockIdx.x;
+    if (f.counters[GS_CNT_OVERFLOW]) {
+        if (threadIdx.x == 0) f.tile_offsets[t] = 0;
+        if (t == 0 && threadIdx.x == 1) f.tile_offsets[T] = 0;
+        return;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nh = min(f.counters[GS_CNT_HUGE], GS_HUGE_CAP);
+    const int off = f.tile_offsets[t];
+    const int sb = f.tile_scratch[t], nb = f.tile_scratch[t + 1] - sb;
+    const uint32_t rmask = rank_bits ? (1u << rank_bits) - 1u : 0u;
+    // A: this tile's huge Gaussians in depth order: walk the depth-ordered records and test
+    // each one's slot bit in the tile's mask (staged in smem)
+    __shared__ uint32_t s_mask[GS_HUGE_CAP / 32];
+    if (threadIdx.x == 0) s_na = 0;
+    const uint32_t *mask = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
+    for (int w = threadIdx.x; w < (nh + 31) >> 5; w += 256) s_mask[w] = mask[w];
+    __syncthreads();
+    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
+    for (int c0 = 0; c0 < nrec; c0 += 256) {
+        const int i = c0 + threadIdx.x;
+        int4 rec = make_int4(0, 0, 0, 0);
+        bool m = false;
+        if (i < nrec) {
+            rec = reinterpret_cast<const int4 *>(f.huge + HREC * i)[0];
+            m = (s_mask[rec.z >> 5] >> (rec.z & 31)) & 1u;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, m);
+        if (lane == 0) s_warp[warp] = __popc(bal);
+        __syncthreads();
+        int before = s_na, total = 0;
+        for (int ww = 0; ww < 8; ww++) {
+            before += ww < warp ? s_warp[ww] : 0;
+            total += s_warp[ww];
+        }
+        if (m) {
+            const int p = before + __popc(bal & ((1u << lane) - 1u));
+            s_arank[p] = rec.y;
+            s_aid[p] = rec.x;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) s_na += total;
+        __syncthreads();
+    }
+    const int na = s_na;
+    // B ranks staged in smem when they fit (only the rank field is compared)
+    const bool b_in_smem = nb <= MERGE_B;
+    if (na > 0 && b_in_smem)
+        for (int j = threadIdx.x; j < nb; j += 256) s_brank[j] = (int)((uint32_t)sorted[sb + j] & rmask);
+    __syncthreads();
+    for (int i = threadIdx.x; i < na; i += 256) {
+        const int r = s_arank[i];
+        int lo = 0, hi = nb;  // first B with rank > r (ranks unique)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            const int br = b_in_smem ? s_brank[mid] : (int)((uint32_t)sorted[sb + mid] & rmask);
+            if (br < r) lo = mid + 1;
+            else hi = mid;
+        }
+        f.entry_splat[off + i + lo] = s_aid[i];
+    }
+    for (int j = threadIdx.x; j < nb; j += 256) {
+        const K w = sorted[sb + j];
+        int lo = 0;
+        if (na > 0) {
+            const int r = (int)((uint32_t)w & rmask);
+            int hi = na;
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (s_arank[mid] < r) lo = mid + 1;
+                else hi = mid;
+            }
+        }
+        f.entry_splat[off + j + lo] = rank_bits ? (int32_t)(uint32_t)depth_sorted[(uint32_t)w & rmask]
+                                                : (int32_t)(uint32_t)w;
     }
 }
 
@@ -403,7 +609,7 @@ static int sort_pass(const gs_frame *f, const K *in, K *out, int64_t n_host, con
 // stable LSD sort of the entry words on the tile field; returns the buffer holding the result
 template <typename K>
 static int tile_sort(const gs_frame *f, K *a, K *b, int shift0, int tpasses, cudaStream_t st, K **result) {
-    const int32_t *n_ent = f->counters + GS_CNT_ENTRIES_EFF;
+    const int32_t *n_ent = f->counters + GS_CNT_SMALL_E;
     const int64_t cap = f->entry_capacity;
     radix_hist_kernel<K><<<4 * 148, 256, 0, st>>>(a, cap, n_ent, shift0, tpasses, f->sort_hist + 4 * 256, 0, nullptr);
     int rc = check_launch("radix_hist_kernel");
@@ -436,19 +642,21 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     const int64_t n = f->n;
     const int32_t T = f->tiles_x * f->tiles_y;
     int rc;
-    // reset the binning counters (the touched count/list belong to preprocess), histograms and
+    // reset the binning counters (touched and huge belong to preprocess), histograms and
     // look-back state
     cudaMemsetAsync(f->counters + GS_CNT_ACTIVE, 0, sizeof(int32_t) * 2, st);
-    cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * (2 * GS_CNT_SLOTS - GS_CNT_OVERFLOW), st);
+    cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * (GS_CNT_SLOTS - GS_CNT_OVERFLOW), st);
+    cudaMemsetAsync(f->counters + GS_CNT_SMALL_E, 0, sizeof(int32_t) * 2, st);  // SMALL_E, HUGE_N
     cudaMemsetAsync(f->sort_hist, 0, sizeof(uint32_t) * 8 * 256, st);
     cudaMemsetAsync(f->sort_status, 0, sizeof(uint32_t) * f->status_words, st);
     cudaMemsetAsync(f->scan_status, 0, sizeof(uint32_t) * f->scan_words, st);
     if (n == 0) {
-        ranges_kernel<uint64_t><<<1, 256, 0, st>>>(*f, f->keys_b, 0, nullptr);
-        return check_launch("ranges_kernel");
+        cudaMemsetAsync(f->tile_offsets, 0, sizeof(int32_t) * (T + 1), st);
+        return check_launch("gs_bin");
     }
-    if (!cull) {
+    if (!cull) {  // every valid Gaussian in every tile: no huge binning, all through the sort
         cudaMemsetAsync(f->counters + GS_CNT_TOUCHED, 0, sizeof(int32_t), st);
+        cudaMemsetAsync(f->counters + GS_CNT_HUGE, 0, sizeof(int32_t) * 2, st);
         nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
         if ((rc = check_launch("nocull_kernel"))) return rc;
     }
@@ -456,7 +664,7 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     // 1) depth sort of the touched Gaussians (4 passes over the 32 depth bits, the first pass
     //    drops untouched ones)
     radix_hist_kernel<uint64_t><<<hist_blocks, 256, 0, st>>>(f->keys_a, n, nullptr, 32, 4, f->sort_hist, 1,
-                                                   f->counters + GS_CNT_ACTIVE);
+                                                             f->counters + GS_CNT_ACTIVE);
     if ((rc = check_launch("radix_hist_kernel"))) return rc;
     radix_bins_kernel<<<4, 256, 0, st>>>(f->sort_hist);
     const int32_t *n_act = f->counters + GS_CNT_ACTIVE;
@@ -464,37 +672,50 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 40, f->sort_hist + 1 * 256, 1, 0, st))) return rc;
     if ((rc = sort_pass(f, f->keys_a, f->keys_b, n, n_act, 48, f->sort_hist + 2 * 256, 2, 0, st))) return rc;
     if ((rc = sort_pass(f, f->keys_b, f->keys_a, n, n_act, 56, f->sort_hist + 3 * 256, 3, 0, st))) return rc;
-    // 2) entry offsets: exclusive scan of the kept counts in depth order, then emit
+    // 2) offsets of the sorted (non-huge) entries: exclusive scan of kept counts in depth order
     {
         const int64_t tiles = (n + SC_TILE - 1) / SC_TILE;
         scan_kernel<<<(unsigned)(tiles > 0 ? tiles : 1), RS_THREADS, 0, st>>>(
             f->kept, f->keys_a, f->counts, n, n_act, (uint32_t *)f->scan_status, f->counters + GS_CNT_TICKET0 + 7,
             f->counters + GS_CNT_ENTRIES, f->entry_capacity, f->counters + GS_CNT_OVERFLOW,
-            f->counters + GS_CNT_ENTRIES_EFF);
+            f->counters + GS_CNT_SMALL_E);
         if ((rc = check_launch("scan_kernel"))) return rc;
     }
     // entry words: 32-bit (tile << rank_bits | depth rank) when tile and rank bits fit, so the
     // tile sort moves half the bytes; 64-bit (tile << 32 | id) otherwise
     int tile_bits = 0, rank_bits = 0;
-    while ((1 << tile_bits) < T) tile_bits++;
-    while ((int64_t(1) << rank_bits) < n) rank_bits++;
-    if (rank_bits == 0) rank_bits = 1;
-    const bool compact = tile_bits + rank_bits <= 32;
+    const bool compact = compact_words(n, T, &tile_bits, &rank_bits);
     const int tpasses = tile_bits <= 8 ? 1 : (tile_bits <= 16 ? 2 : 3);
     const int rb = compact ? rank_bits : 0;
     emit_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f, f->keys_a, f->keys_b, cull, rb);
     if ((rc = check_launch("emit_kernel"))) return rc;
     emit_big_kernel<<<8 * 148, 256, 0, st>>>(*f, f->keys_a, f->keys_b, rb);
     if ((rc = check_launch("emit_big_kernel"))) return rc;
-    // 3) stable sort of the entries on the tile field, 4) ranges + entry ids
-    if (compact) {
-        uint32_t *a = reinterpret_cast<uint32_t *>(f->keys_b), *b = a + f->entry_capacity, *res = nullptr;
-        if ((rc = tile_sort<uint32_t>(f, a, b, rank_bits, tpasses, st, &res))) return rc;
-        ranges_kernel<uint32_t><<<4 * 148, 256, 0, st>>>(*f, res, rank_bits, f->keys_a);
-    } else {
-        uint64_t *res = nullptr;
-        if ((rc = tile_sort<uint64_t>(f, f->keys_b, f->keys_a, 32, tpasses, st, &res))) return rc;
-        ranges_kernel<uint64_t><<<4 * 148, 256, 0, st>>>(*f, res, 0, nullptr);
+    {
+        const unsigned chunks = (unsigned)((n + HCHUNK - 1) / HCHUNK);
+        huge_flag_count_kernel<<<chunks, HCHUNK, 0, st>>>(*f, f->keys_a);
+        if ((rc = check_launch("huge_flag_count_kernel"))) return rc;
+        huge_write_kernel<<<chunks, HCHUNK, 0, st>>>(*f, f->keys_a);
+        if ((rc = check_launch("huge_write_kernel"))) return rc;
     }
-    return check_launch("ranges_kernel");
+    // 3) stable sort of the emitted entries on the tile field, their per-tile ranges
+    uint32_t *res32 = nullptr;
+    uint64_t *res64 = nullptr;
+    if (compact) {
+        uint32_t *a = reinterpret_cast<uint32_t *>(f->keys_b), *b = a + f->entry_capacity;
+        if ((rc = tile_sort<uint32_t>(f, a, b, rank_bits, tpasses, st, &res32))) return rc;
+        ranges_kernel<uint32_t><<<4 * 148, 256, 0, st>>>(*f, res32, rank_bits);
+    } else {
+        if ((rc = tile_sort<uint64_t>(f, f->keys_b, f->keys_a, 32, tpasses, st, &res64))) return rc;
+        ranges_kernel<uint64_t><<<4 * 148, 256, 0, st>>>(*f, res64, 0);
+    }
+    if ((rc = check_launch("ranges_kernel"))) return rc;
+    // 4) huge Gaussians per tile, tile offsets, merged entry lists
+    huge_count_kernel<<<(unsigned)((T * 32 + 255) / 256), 256, 0, st>>>(*f);
+    if ((rc = check_launch("huge_count_kernel"))) return rc;
+    tile_scan_kernel<<<1, 1024, 0, st>>>(*f);
+    if ((rc = check_launch("tile_scan_kernel"))) return rc;
+    if (compact) merge_kernel<uint32_t><<<T, 256, 0, st>>>(*f, res32, rank_bits, f->keys_a);
+    else merge_kernel<uint64_t><<<T, 256, 0, st>>>(*f, res64, 0, f->keys_a);
+    return check_launch("merge_kernel");
 }

@@ -135,9 +135,9 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
 // tiles; same decision function as cull_rect).  Completes kept/keep_bits/touched/key.
 constexpr int BIG_THREADS = 256;
 
-__global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f) {
+__global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f, int allow_huge) {
     // one CTA per large-footprint Gaussian: threads stride over its candidate tiles
-    __shared__ int s_cnt;
+    __shared__ int s_cnt, s_slot;
     __shared__ int64_t s_base;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t nb = f.counters[GS_CNT_BIG];
@@ -150,25 +150,46 @@ __global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f) {
         const int words = (ncand + 31) >> 5;
         if (threadIdx.x == 0) {
             s_cnt = 0;
-            // reserve the Gaussian's cull bitmap; on overflow the emit pass re-culls instead
-            const int64_t base = atomicAdd(&f.counters[GS_CNT_BIG_BITS], words);
-            s_base = base + words <= f.big_bits_words ? base : -1;
+            // screen-covering Gaussians take a huge slot: their kept tiles are recorded in the
+            // per-tile masks (huge_mask[tile] bit slot) and they skip the emit + sort
+            int slot = -1;
+            if (allow_huge && ncand > GS_HUGE_CAND) {
+                slot = atomicAdd(&f.counters[GS_CNT_HUGE], 1);
+                if (slot >= GS_HUGE_CAP) slot = -1;
+            }
+            s_slot = slot;
+            // the others keep a cull bitmap for the emit (on overflow the emit re-culls)
+            int64_t base = -1;
+            if (slot < 0) {
+                base = atomicAdd(&f.counters[GS_CNT_BIG_BITS], words);
+                if (base + words > f.big_bits_words) base = -1;
+            }
+            s_base = base;
         }
         __syncthreads();
         const int64_t base = s_base;
+        const int slot = s_slot;
         int count = 0;
         for (int c0 = 0; c0 < ncand; c0 += BIG_THREADS) {  // uniform trip count: ballots are warp-wide
             const int c = c0 + threadIdx.x;
             bool keep = false;
+            int tx = 0, ty = 0;
             if (c < ncand) {
-                const int tx = r.x + c % nx, ty = r.z + c / nx;
+                tx = r.x + c % nx;
+                ty = r.z + c / nx;
                 const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
                 const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
                 keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
             }
             count += keep;
-            const unsigned bal = __ballot_sync(0xffffffffu, keep);
-            if (lane == 0 && base >= 0 && (c0 >> 5) + warp < words) f.big_bits[base + (c0 >> 5) + warp] = bal;
+            if (slot >= 0) {
+                if (keep)
+                    atomicOr(&f.huge_mask[(int64_t)(ty * f.tiles_x + tx) * (GS_HUGE_CAP / 32) + (slot >> 5)],
+                             1u << (slot & 31));
+            } else {
+                const unsigned bal = __ballot_sync(0xffffffffu, keep);
+                if (lane == 0 && base >= 0 && (c0 >> 5) + warp < words) f.big_bits[base + (c0 >> 5) + warp] = bal;
+            }
         }
         for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
         if (lane == 0 && count) atomicAdd(&s_cnt, count);
@@ -177,6 +198,10 @@ __global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f) {
             const int kept = s_cnt;
             f.kept[g] = kept;
             f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+            if (slot >= 0 && kept > 0) {  // kept < 0 encodes the huge slot
+                f.kept[g] = -(1 + slot);
+                atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
+            }
             f.touched[g] = kept > 0;
             if (kept > 0) {
                 f.keys_a[g] = ((uint64_t)__float_as_uint(s1.z) << 32) | (uint64_t)g;
@@ -342,13 +367,17 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
         return GS_ERR_ARG;
     }
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
+    cudaMemsetAsync(f->huge_mask, 0, sizeof(uint32_t) * (size_t)f->tiles_x * f->tiles_y * (GS_HUGE_CAP / 32),
+                    (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     int64_t warps = (f->n + 31) / 32;
     int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
     preprocess_kernel<<<blocks, PP_THREADS, 0, (cudaStream_t)stream>>>(*f, params, view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
-    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    int tb = 0, rb = 0;
+    const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
+    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, allow_huge);
     return check_launch("cull_big_kernel");
 }
 
@@ -373,6 +402,8 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
                               const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                               void *stream) {
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
+    cudaMemsetAsync(f->huge_mask, 0, sizeof(uint32_t) * (size_t)f->tiles_x * f->tiles_y * (GS_HUGE_CAP / 32),
+                    (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);
@@ -380,7 +411,9 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
     if (rc) return rc;
     touched_list_kernel<<<(unsigned)((f->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
     if ((rc = check_launch("touched_list_kernel"))) return rc;
-    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    int tb = 0, rb = 0;
+    const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
+    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, allow_huge);
     return check_launch("cull_big_kernel");
 }
 

@@ -27,12 +27,13 @@ NEAR_CLIP = 0.01
 
 def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     """Our kernels per map-optimisation iteration:
-    preprocess 2 (projection+cull, large-footprint cull), bin 11 + tile-sort passes
-    (2 histograms, 2 bin scans, 4 depth passes, scan, 2 emits, ranges), forward 1,
-    loss 4 (tables, SSIM+L1, depth, finalize), backward 2 (zero + tiles), chain + Adam 2."""
+    preprocess 2 (projection+cull, large-footprint cull), bin 17 + tile-sort passes
+    (2 histograms, 2 bin scans, 4 depth passes, scan, 2 emits, 2 huge compaction, ranges,
+    huge count, tile scan, merge), forward 1, loss 4 (tables, SSIM+L1, depth, finalize),
+    backward 2 (zero + tiles), chain + Adam 2."""
     tile_bits = max(1, (tiles - 1).bit_length())
     tpasses = 1 if tile_bits <= 8 else (2 if tile_bits <= 16 else 3)
-    return 2 + 11 + tpasses + 1 + 4 + 2 + (1 if chain_only else 2)
+    return 2 + 17 + tpasses + 1 + 4 + 2 + (1 if chain_only else 2)
 
 
 @dataclass
