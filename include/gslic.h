@@ -75,6 +75,7 @@ enum {
 
 #define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */
 #define GS_HUGE_CAP 4096 /* at most this many such Gaussians per view (the rest take the sort) */
+#define GS_MAX_TILES 65536 /* tiles per view (4096 x 4096 px): bounds the per-CTA cull bitmaps */
 
 /* Pinhole camera, world->camera (R/rasterizer.py:47-67).  Pixel centres are integers. */
 typedef struct gs_camera {
@@ -109,7 +110,7 @@ typedef struct gs_frame {
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
     double *g2d;             /* n x GS_G2D screen-space gradients, FP64 accumulators (touched rows) */
     float *grad_rows;        /* n x GS_ROW parameter gradients in touched-list order */
-    float *bias_corr;        /* n x 2 Adam bias corrections (1-b1^t, 1-b2^t) in touched-list order */
+    float *bias_corr;        /* n x 2 reciprocal Adam bias corrections 1/(1-b1^t), 1/(1-b2^t) (touched-list order) */
     uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
     int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
     int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */
@@ -117,7 +118,10 @@ typedef struct gs_frame {
     int32_t *big_emit;       /* n: depth ranks of those Gaussians (warp-emitted) */
     int32_t *huge;           /* GS_HUGE_CAP x 8: screen-covering Gaussians in depth order (id,
                                 rank, rect, bitmap base) + compaction scratch */
-    uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: which huge Gaussians keep each tile */
+    uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: bit j of word w <-> the (32w+j)-th huge
+                                Gaussian in depth order keeps the tile */
+    uint32_t *huge_mask_t;   /* GS_HUGE_CAP x ceil(tiles/32): per huge slot, its kept tiles */
+    int32_t *huge_before;    /* n: per depth rank, the huge Gaussians ahead of it (merge key) */
     int32_t *tile_scratch;   /* 2 x (tiles + 1): per-tile sorted-entry offsets, huge counts */
     uint32_t *big_bits;      /* cull bitmaps of the large-footprint Gaussians (base in keep_bits) */
     int64_t big_bits_words;  /* capacity of big_bits; overflowing Gaussians are re-culled at emit */

@@ -157,11 +157,15 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
     G[10] = g_opl;
 }
 
-__device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float bc1, float bc2) {
+// One Adam element (R/rasterizer.py:715-725): m, v moments, bias-corrected step
+// lr * (m / bc1) / (sqrt(v / bc2) + 1e-15).  rbc1 = 1/bc1, rbc2 = 1/bc2 are per-row constants;
+// the final quotient uses the MUFU reciprocal (<= 2 ulp): the update is bandwidth-bound only
+// if it is not issue-bound on IEEE divides.
+__device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float rbc1, float rbc2) {
     m = 0.9f * m + 0.1f * g;
     v = 0.999f * v + 0.001f * g * g;
-    const float mh = m / bc1, vh = v / bc2;
-    return p - lr * mh / (sqrtf(vh) + 1e-15f);
+    const float den = sqrtf(v * rbc2) + 1e-15f;
+    return p - (lr * (m * rbc1)) * __frcp_rn(den);
 }
 
 // mode 0: fused Adam on params/m/v/t.  mode 1: grads[row] += G, touched_accum[row] = 1.
@@ -206,7 +210,9 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         if (mode == 0 || mode == 2) {
             const int tn = at[g] + 1;
             at[g] = tn;
-            const float bc1 = (float)(1.0 - pow(0.9, (double)tn)), bc2 = (float)(1.0 - pow(0.999, (double)tn));
+            // reciprocal bias corrections 1/(1-b1^t), 1/(1-b2^t) (per-Gaussian t, R/rasterizer.py:714-722)
+            const float bc1 = (float)(1.0 / (1.0 - pow(0.9, (double)tn))),
+                        bc2 = (float)(1.0 / (1.0 - pow(0.999, (double)tn)));
             sbc[warp][lane][0] = bc1;
             sbc[warp][lane][1] = bc2;
             if (mode == 2) reinterpret_cast<float2 *>(f.bias_corr)[k] = make_float2(bc1, bc2);
@@ -300,7 +306,7 @@ __global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, 
     const int c4 = (int)(idx & 15);
     if (!touched[row]) return;
     const int tn = at[row] + 1;
-    const float bc1 = (float)(1.0 - pow(0.9, (double)tn)), bc2 = (float)(1.0 - pow(0.999, (double)tn));
+    const float bc1 = (float)(1.0 / (1.0 - pow(0.9, (double)tn))), bc2 = (float)(1.0 / (1.0 - pow(0.999, (double)tn)));
     const int64_t off = row * GS_ROW + 4 * c4;
     float4 p4 = *reinterpret_cast<const float4 *>(params + off);
     float4 m4 = *reinterpret_cast<const float4 *>(am + off);

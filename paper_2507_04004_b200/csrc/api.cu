@@ -81,8 +81,11 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.counts = c.take<int32_t>(nn + 1);
     f.big_list = c.take<int32_t>(nn);
     f.big_emit = c.take<int32_t>(nn);
-    f.huge = c.take<int32_t>(8 * GS_HUGE_CAP + (nn + 1023) / 1024 + 1);
+    // huge records (8 ints each), their ids in depth order, per-chunk compaction counts
+    f.huge = c.take<int32_t>(9 * GS_HUGE_CAP + (nn + 1023) / 1024 + 1);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
+    f.huge_mask_t = c.take<uint32_t>((int64_t)GS_HUGE_CAP * (((int64_t)tx * ty + 31) / 32));
+    f.huge_before = c.take<int32_t>(nn);
     f.tile_scratch = c.take<int32_t>(2 * ((int64_t)tx * ty + 1));
     f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
     f.big_bits = c.take<uint32_t>(f.big_bits_words);
@@ -130,6 +133,10 @@ extern "C" int gs_frame_layout(int64_t n, int32_t width, int32_t height, int64_t
     }
     if (n >= (1ll << 31) || entry_capacity >= (1ll << 30)) {
         set_error("gs_frame_layout: n or entry_capacity exceeds the 32-bit index range");
+        return GS_ERR_DIMS;
+    }
+    if ((int64_t)((width + GS_TILE - 1) / GS_TILE) * ((height + GS_TILE - 1) / GS_TILE) > GS_MAX_TILES) {
+        set_error("gs_frame_layout: %dx%d exceeds GS_MAX_TILES (%d) tiles", width, height, GS_MAX_TILES);
         return GS_ERR_DIMS;
     }
     const size_t need = gs_workspace_size(n, width, height, entry_capacity);

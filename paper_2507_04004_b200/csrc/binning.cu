@@ -379,8 +379,11 @@ __global__ void ranges_kernel(gs_frame f, const K *__restrict__ sorted, int rank
 // screen-covering ("huge") Gaussians: binned per tile from their cull bitmaps in depth order,
 // then merged with the tile's sorted entries.  They never enter the emit + sort.
 
-// Huge records (depth order), 8 ints each: id, rank, rect (tx0 tx1 ty0 ty1), bitmap base (lo, hi)
+// Huge records (depth order), 8 ints each: id, depth rank, slot; then their ids alone (depth
+// order), then the per-chunk counts of the ordered compaction
 constexpr int HREC = 8;
+constexpr int HIDS = HREC * GS_HUGE_CAP;
+constexpr int HCNT0 = HIDS + GS_HUGE_CAP;
 constexpr int HCHUNK = 1024;
 
 // ordered compaction of the huge Gaussians from the depth-sorted list, pass 1: counts per chunk
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(HCHUNK) huge_flag_count_kernel(gs_frame f, con
     const unsigned m = __ballot_sync(0xffffffffu, h);
     if ((threadIdx.x & 31) == 0 && m) atomicAdd(&s, __popc(m));
     __syncthreads();
-    if (threadIdx.x == 0) f.huge[HREC * GS_HUGE_CAP + blockIdx.x] = s;
+    if (threadIdx.x == 0) f.huge[HCNT0 + blockIdx.x] = s;
 }
 
 // pass 2: each chunk sums its predecessors and writes its huge records in order
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(HCHUNK) huge_write_kernel(gs_frame f, const ui
     __shared__ int s_warp[HCHUNK / 32];
     __shared__ int s_base;
     if (f.counters[GS_CNT_HUGE] == 0) return;
-    const int32_t *chunk_cnt = f.huge + HREC * GS_HUGE_CAP;
+    const int32_t *chunk_cnt = f.huge + HCNT0;
     if (threadIdx.x == 0) s_base = 0;
     __syncthreads();
     int acc = 0;
@@ -423,9 +426,12 @@ __global__ void __launch_bounds__(HCHUNK) huge_write_kernel(gs_frame f, const ui
     int pos = s_base;
     for (int w = 0; w < warp; w++) pos += s_warp[w];
     pos += __popc(m & ((1u << lane) - 1u));
+    // merge key of every depth rank: the huge Gaussians ahead of it
+    if (k < f.counters[GS_CNT_ACTIVE]) f.huge_before[k] = pos;
     if (h && pos < GS_HUGE_CAP) {
         int4 *rec = reinterpret_cast<int4 *>(f.huge + HREC * pos);
         rec[0] = make_int4((int)g, (int)k, -f.kept[g] - 1, 0);  // id, depth rank, huge slot
+        f.huge[HIDS + pos] = (int)g;
     }
     if (threadIdx.x == 0) {
         int tot = 0;
@@ -434,19 +440,30 @@ __global__ void __launch_bounds__(HCHUNK) huge_write_kernel(gs_frame f, const ui
     }
 }
 
-// warp per tile: huge Gaussians keeping the tile = popcount of its slot mask (set by
-// cull_big_kernel)
-__global__ void __launch_bounds__(256) huge_count_kernel(gs_frame f) {
-    const int T = f.tiles_x * f.tiles_y;
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// Per-tile masks in depth order: bit j of huge_mask[t][w] <-> huge record 32w + j keeps tile t
+// (a 32 x 32 bit transpose per warp of huge_mask_t rows, which cull_big_kernel wrote by slot),
+// plus the per-tile huge counts.
+__global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
+    const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
+    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
     const int lane = threadIdx.x & 31;
-    if (t >= T) return;
-    const int nslots = min(f.counters[GS_CNT_HUGE], GS_HUGE_CAP);
-    const uint32_t *mask = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
-    int cnt = 0;
-    for (int w = lane; w < (nslots + 31) >> 5; w += 32) cnt += __popc(mask[w]);
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) f.tile_scratch[T + 1 + t] = cnt;
+    const int w = blockIdx.y * 8 + (threadIdx.x >> 5);  // 32 records in depth order
+    if (32 * w >= nrec) return;
+    const int u = blockIdx.x;  // 32 tiles
+    const int i = 32 * w + lane;
+    uint32_t v = 0u;
+    if (i < nrec) v = f.huge_mask_t[(int64_t)f.huge[HREC * i + 2] * tw + u];
+    uint32_t mine = 0u;
+#pragma unroll
+    for (int j = 0; j < 32; j++) {
+        const uint32_t b = __ballot_sync(0xffffffffu, (v >> j) & 1u);
+        if (lane == j) mine = b;
+    }
+    const int t = 32 * u + lane;
+    if (t < T) {
+        f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + w] = mine;
+        if (mine) atomicAdd(&f.tile_scratch[T + 1 + t], __popc(mine));
+    }
 }
 
 // one CTA: tile_offsets = exclusive scan of (sorted entries + huge entries) per tile; E total
@@ -489,95 +506,133 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f) {
     }
 }
 
-// CTA per tile: merge the tile's huge Gaussians (depth order, from the bitmaps) with its
-// tile-sorted entries (depth order) by depth rank; write entry_splat.  Ranks are unique
-// within a tile, so each element's output slot is its index plus a lower bound in the other
-// list.  On an overflow every tile range is emptied instead.
+// CTA per tile: merge the tile's huge Gaussians (depth order: the set bits of its mask words)
+// with its tile-sorted entries (depth order) and write entry_splat.  Keys: a huge record's
+// index i, a sorted entry's huge_before h (huge records ahead of its depth rank), so record i
+// precedes the entry iff i < h.  On an overflow every range is emptied.
 constexpr int MERGE_B = 2048;
 
 template <typename K>
 __global__ void __launch_bounds__(256) merge_kernel(gs_frame f, const K *__restrict__ sorted, int rank_bits,
                                                     const uint64_t *__restrict__ depth_sorted) {
-    __shared__ int32_t s_arank[GS_HUGE_CAP], s_aid[GS_HUGE_CAP];
-    __shared__ int32_t s_brank[MERGE_B];
+    __shared__ int32_t s_a[GS_HUGE_CAP];
+    __shared__ uint32_t s_isb[(GS_HUGE_CAP + MERGE_B) / 32];
+    __shared__ int32_t s_wpre[(GS_HUGE_CAP + MERGE_B) / 32];
     __shared__ int s_warp[8];
-    __shared__ int s_na;
     const int T = f.tiles_x * f.tiles_y;
     const int t = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (f.counters[GS_CNT_OVERFLOW]) {
-        if (threadIdx.x == 0) f.tile_offsets[t] = 0;
-        if (t == 0 && threadIdx.x == 1) f.tile_offsets[T] = 0;
+        if (tid == 0) f.tile_offsets[t] = 0;
+        if (t == 0 && tid == 1) f.tile_offsets[T] = 0;
         return;
     }
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int nh = min(f.counters[GS_CNT_HUGE], GS_HUGE_CAP);
+    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
     const int off = f.tile_offsets[t];
     const int sb = f.tile_scratch[t], nb = f.tile_scratch[t + 1] - sb;
     const uint32_t rmask = rank_bits ? (1u << rank_bits) - 1u : 0u;
-    // A: this tile's huge Gaussians in depth order: walk the depth-ordered records and test
-    // each one's slot bit in the tile's mask (staged in smem)
-    __shared__ uint32_t s_mask[GS_HUGE_CAP / 32];
-    if (threadIdx.x == 0) s_na = 0;
-    const uint32_t *mask = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
-    for (int w = threadIdx.x; w < (nh + 31) >> 5; w += 256) s_mask[w] = mask[w];
-    __syncthreads();
-    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
-    for (int c0 = 0; c0 < nrec; c0 += 256) {
-        const int i = c0 + threadIdx.x;
-        int4 rec = make_int4(0, 0, 0, 0);
-        bool m = false;
-        if (i < nrec) {
-            rec = reinterpret_cast<const int4 *>(f.huge + HREC * i)[0];
-            m = (s_mask[rec.z >> 5] >> (rec.z & 31)) & 1u;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, m);
-        if (lane == 0) s_warp[warp] = __popc(bal);
-        __syncthreads();
-        int before = s_na, total = 0;
-        for (int ww = 0; ww < 8; ww++) {
-            before += ww < warp ? s_warp[ww] : 0;
-            total += s_warp[ww];
-        }
-        if (m) {
-            const int p = before + __popc(bal & ((1u << lane) - 1u));
-            s_arank[p] = rec.y;
-            s_aid[p] = rec.x;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) s_na += total;
-        __syncthreads();
-    }
-    const int na = s_na;
-    // B ranks staged in smem when they fit (only the rank field is compared)
-    const bool b_in_smem = nb <= MERGE_B;
-    if (na > 0 && b_in_smem)
-        for (int j = threadIdx.x; j < nb; j += 256) s_brank[j] = (int)((uint32_t)sorted[sb + j] & rmask);
-    __syncthreads();
-    for (int i = threadIdx.x; i < na; i += 256) {
-        const int r = s_arank[i];
-        int lo = 0, hi = nb;  // first B with rank > r (ranks unique)
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            const int br = b_in_smem ? s_brank[mid] : (int)((uint32_t)sorted[sb + mid] & rmask);
-            if (br < r) lo = mid + 1;
-            else hi = mid;
-        }
-        f.entry_splat[off + i + lo] = s_aid[i];
-    }
-    for (int j = threadIdx.x; j < nb; j += 256) {
+    int32_t *out = f.entry_splat + off;
+    auto b_id = [&](int j) -> int {
         const K w = sorted[sb + j];
-        int lo = 0;
-        if (na > 0) {
-            const int r = (int)((uint32_t)w & rmask);
-            int hi = na;
+        return rank_bits ? (int)(uint32_t)depth_sorted[(uint32_t)w & rmask] : (int)(uint32_t)w;
+    };
+    // A: expand the depth-ordered mask words (thread per word)
+    const int nw = (nrec + 31) >> 5;
+    uint32_t v = tid < nw ? f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + tid] : 0u;
+    const int c = __popc(v);
+    int x = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_warp[warp] = x;
+    __syncthreads();
+    int na = 0, pos = x - c;
+#pragma unroll
+    for (int w = 0; w < 8; w++) {
+        const int sw = s_warp[w];
+        pos += w < warp ? sw : 0;
+        na += sw;
+    }
+    if (tid < nw) s_wpre[tid] = pos;
+    __syncthreads();
+    // expand: a warp per word, lane j <-> bit j (coalesced shared stores)
+    for (int w = warp; w < nw; w += 8) {
+        const uint32_t word = f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + w];
+        if ((word >> lane) & 1u) s_a[s_wpre[w] + __popc(word & ((1u << lane) - 1u))] = 32 * w + lane;
+    }
+    if (na == 0) {  // no huge Gaussian in this tile: the sorted entries as they are
+        for (int j = tid; j < nb; j += 256) out[j] = b_id(j);
+        return;
+    }
+    const int total = na + nb;
+    const int32_t *hid = f.huge + HIDS;
+    if (nb <= MERGE_B) {
+        // B element j lands at j + #{A preceding it} (binary search in A); its slot is marked in
+        // a bitmap.  Every other output d is A element d - #{B slots before d}.  Both write
+        // passes are coalesced.
+        const int tw = (total + 31) >> 5;
+        for (int w = tid; w < tw; w += 256) s_isb[w] = 0u;
+        __syncthreads();
+        for (int j = tid; j < nb; j += 256) {
+            const int h = f.huge_before[(uint32_t)sorted[sb + j] & rmask];
+            int lo = 0, hi = na;
             while (lo < hi) {
                 const int mid = (lo + hi) >> 1;
-                if (s_arank[mid] < r) lo = mid + 1;
+                if (s_a[mid] < h) lo = mid + 1;
                 else hi = mid;
             }
+            const int d = j + lo;
+            out[d] = b_id(j);
+            atomicOr(&s_isb[d >> 5], 1u << (d & 31));
         }
-        f.entry_splat[off + j + lo] = rank_bits ? (int32_t)(uint32_t)depth_sorted[(uint32_t)w & rmask]
-                                                : (int32_t)(uint32_t)w;
+        __syncthreads();
+        // exclusive prefix of the B-slot popcounts per word (tw <= 192 words)
+        const int cnt = tid < tw ? __popc(s_isb[tid]) : 0;
+        int xx = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, xx, o);
+            if (lane >= o) xx += y;
+        }
+        if (lane == 31) s_warp[warp] = xx;
+        __syncthreads();
+        int pre = xx - cnt;
+        for (int w = 0; w < warp; w++) pre += s_warp[w];
+        if (tid < tw) s_wpre[tid] = pre;
+        __syncthreads();
+        for (int d = tid; d < total; d += 256) {
+            const uint32_t word = s_isb[d >> 5];
+            if ((word >> (d & 31)) & 1u) continue;
+            const int a = d - (s_wpre[d >> 5] + __popc(word & ((1u << (d & 31)) - 1u)));
+            out[d] = hid[s_a[a]];
+        }
+        return;
+    }
+    // many sorted entries: merge path, each thread merges a run of ceil(total / 256) outputs
+    __syncthreads();
+    auto bh = [&](int j) -> int { return f.huge_before[(uint32_t)sorted[sb + j] & rmask]; };
+    const int L = (total + 255) / 256;
+    const int d0 = min(tid * L, total), d1 = min(d0 + L, total);
+    if (d0 >= d1) return;
+    int lo = max(0, d0 - nb), hi = min(d0, na);
+    while (lo < hi) {  // a = number of A among the first d0 outputs
+        const int mid = (lo + hi) >> 1;
+        if (s_a[mid] < bh(d0 - 1 - mid)) lo = mid + 1;
+        else hi = mid;
+    }
+    int aa = lo, bb = d0 - lo;
+    int hb = bb < nb ? bh(bb) : 0;
+    for (int d = d0; d < d1; d++) {
+        if (bb >= nb || (aa < na && s_a[aa] < hb)) {
+            out[d] = hid[s_a[aa]];
+            aa++;
+        } else {
+            out[d] = b_id(bb);
+            bb++;
+            if (bb < nb) hb = bh(bb);
+        }
     }
 }
 
@@ -650,6 +705,7 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     cudaMemsetAsync(f->sort_hist, 0, sizeof(uint32_t) * 8 * 256, st);
     cudaMemsetAsync(f->sort_status, 0, sizeof(uint32_t) * f->status_words, st);
     cudaMemsetAsync(f->scan_status, 0, sizeof(uint32_t) * f->scan_words, st);
+    cudaMemsetAsync(f->tile_scratch + T + 1, 0, sizeof(int32_t) * T, st);  // per-tile huge counts
     if (n == 0) {
         cudaMemsetAsync(f->tile_offsets, 0, sizeof(int32_t) * (T + 1), st);
         return check_launch("gs_bin");
@@ -697,6 +753,8 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         if ((rc = check_launch("huge_flag_count_kernel"))) return rc;
         huge_write_kernel<<<chunks, HCHUNK, 0, st>>>(*f, f->keys_a);
         if ((rc = check_launch("huge_write_kernel"))) return rc;
+        huge_transpose_kernel<<<dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st>>>(*f);
+        if ((rc = check_launch("huge_transpose_kernel"))) return rc;
     }
     // 3) stable sort of the emitted entries on the tile field, their per-tile ranges
     uint32_t *res32 = nullptr;
@@ -711,8 +769,6 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     }
     if ((rc = check_launch("ranges_kernel"))) return rc;
     // 4) huge Gaussians per tile, tile offsets, merged entry lists
-    huge_count_kernel<<<(unsigned)((T * 32 + 255) / 256), 256, 0, st>>>(*f);
-    if ((rc = check_launch("huge_count_kernel"))) return rc;
     tile_scan_kernel<<<1, 1024, 0, st>>>(*f);
     if ((rc = check_launch("tile_scan_kernel"))) return rc;
     if (compact) merge_kernel<uint32_t><<<T, 256, 0, st>>>(*f, res32, rank_bits, f->keys_a);

@@ -5,19 +5,32 @@
 // dependent 11-tap correlations: blur(x)(q) = sum_d F[q][d] x(q+d) with
 // F[q][d] = sum_t K(t) [refl(q+t) == q+d], and adjoint(g)(p) = sum_d F[p+d][-d] g(p+d); the
 // per-axis tables absorb every reflection, so interior and border pixels share one code path.
-// One CTA computes a 32x16 output tile for all three channels: halo-10 inputs -> 5 blurred
-// moments (halo 5) -> SSIM map + partials -> two adjoint passes -> gradient, all in shared
-// memory (one HBM read of rendered+target, one write of the gradient).
+// One CTA computes a 32x16 output tile of one channel: halo-10 inputs -> 5 blurred moments
+// (halo 5) -> SSIM map + partials -> two adjoint passes -> gradient, all in shared memory (one
+// HBM read of rendered+target, one write of the gradient).
 //
 // Depth term (R/losses.py:133-154) is evaluated only at the view's LiDAR pixels (K-list).
 #include "common.cuh"
 
 namespace gs {
 
-constexpr int LW = 32, LH = 16;              // output tile
-constexpr int IW = LW + 20, IH = LH + 20;    // input region (halo 10)
-constexpr int BW = LW + 10, BH = LH + 10;    // blurred-moment region (halo 5)
+// One CTA per (32 x 16 output tile, colour channel).  Every pass is register-blocked along its
+// blur axis (a thread produces a strip of outputs from one sliding window of shared-memory
+// reads); row strides are odd so that a warp reading one column per lane (or one row per lane)
+// hits 32 distinct banks.  46 KB of shared memory and <= 64 registers give 4 CTAs (32 warps)
+// per SM: the passes are separated by barriers, so it is the other CTAs that keep the SM busy.
+constexpr int TW = 32, TH = 16;
+constexpr int NIR = TH + 20;          // input rows (halo 10)
+constexpr int HXC = TW + 10;          // horizontal-moment columns (strips of 6 / 3)
+constexpr int HXS = HXC + 1;          // their row stride (odd)
+constexpr int NIC = HXC + 11;         // input row stride (odd, >= HXC + 10); columns >= TW + 20 are 0
+constexpr int GR = TH + 10;           // SSIM-map rows (halo 5)
+constexpr int GW = TW + 10;           // SSIM-map columns
+constexpr int GC = GW + 1;            // SSIM-map / vertical-adjoint row stride (odd)
+constexpr int HS = 2;                 // horizontal adjoint: strips of 2 columns, one per thread
 constexpr int L_THREADS = 256;
+static_assert(TH * (TW / HS) == L_THREADS, "one horizontal-adjoint strip per thread");
+static_assert(HXC % 6 == 0 && HXC % 3 == 0, "horizontal strips");
 constexpr float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
 
 
@@ -77,172 +90,212 @@ __device__ __forceinline__ float kw(int d) {
 // INTERIOR: the CTA's whole halo lies >= 10 px inside the image, so every blur / adjoint
 // weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
 struct SsimSmem {
-    // region A: inputs (2 x IH x IW), later the SSIM partials (3 x BH x BW)
-    // region B: horizontal moments (5 x IH x BW), later the vertical adjoint (3 x LH x BW)
-    float A[2 * IH * IW];
-    float B[5 * IH * BW];
+    float in[2][NIR][NIC];  // rendered / target channel; later the SSIM partials g[3][GR][GC]
+    float hx[5][NIR][HXS];  // horizontal moments; later the vertical adjoint ry[3][TH][GC]
     float red[2][L_THREADS / 32];
 };
+static_assert(3 * GR * GC <= 2 * NIR * NIC && 3 * TH * GC <= 5 * NIR * HXS, "smem aliasing");
+
+template <bool INTERIOR>
+__device__ __forceinline__ float wtab(const float *__restrict__ tab, int pos, int d) {
+    return INTERIOR ? kw(d) : __ldg(tab + 22 * pos + d);
+}
 
 template <bool INTERIOR>
 __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
                                           const float *__restrict__ tab_x, const float *__restrict__ tab_y,
                                           float lam) {
-    float *smA = sm.A, *smB = sm.B;
-    float(*red)[L_THREADS / 32] = sm.red;
-    float(*in_a)[IW] = reinterpret_cast<float(*)[IW]>(smA);
-    float(*in_b)[IW] = reinterpret_cast<float(*)[IW]>(smA + IH * IW);
-    float(*g)[BH][BW] = reinterpret_cast<float(*)[BH][BW]>(smA);
-    float(*hx)[IH][BW] = reinterpret_cast<float(*)[IH][BW]>(smB);
-    float(*ry)[LH][BW] = reinterpret_cast<float(*)[LH][BW]>(smB);
-    static_assert(3 * BH * BW <= 2 * IH * IW && 3 * LH * BW <= 5 * IH * BW, "smem aliasing");
-
+    float(*g)[GR][GC] = reinterpret_cast<float(*)[GR][GC]>(&sm.in[0][0][0]);
+    float(*ry)[TH][GC] = reinterpret_cast<float(*)[TH][GC]>(&sm.hx[0][0][0]);
     const float *__restrict__ target = view->target;
+    const float *__restrict__ color = f.color;
     const int W = f.width, H = f.height;
-    const int x0 = blockIdx.x * LW, y0 = blockIdx.y * LH;
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, c = blockIdx.z;
     const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
     const int tid = threadIdx.x;
-    float l1_acc = 0.0f, s_acc = 0.0f;
-    float grad_out[2][3];
-    for (int c = 0; c < 3; c++) {
-        __syncthreads();
-        // 1) inputs on [y0-10, y0+LH+10) x [x0-10, x0+LW+10), zero outside the image
-        for (int k = tid; k < IH * IW; k += L_THREADS) {
-            const int iy = k / IW, ix = k % IW;
+    // strip lengths: border tiles (per-position table weights) use shorter strips so that the
+    // table loads do not push the register budget
+    constexpr int HB = INTERIOR ? 6 : 3;
+    constexpr int VS = 5, NVS = (GR + VS - 1) / VS;
+    constexpr int AS = 4, NAS = TH / AS;
+    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, zero outside the image
+    {
+        constexpr int NEL = NIR * NIC, PER = (NEL + L_THREADS - 1) / L_THREADS;
+        float va[PER], vb[PER];
+#pragma unroll
+        for (int q = 0; q < PER; q++) {  // all loads in flight before the stores
+            const int k = tid + q * L_THREADS;
+            const int iy = k / NIC, ix = k % NIC;
             const int y = y0 - 10 + iy, x = x0 - 10 + ix;
-            float a = 0.0f, b = 0.0f;
-            if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
+            va[q] = vb[q] = 0.0f;
+            if (k < NEL && ix < TW + 20 && (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H))) {
                 const int64_t p = (int64_t)y * W + x;
-                a = f.color[3 * p + c];
-                b = target[3 * p + c];
+                va[q] = __ldg(color + 3 * p + c);
+                vb[q] = __ldg(target + 3 * p + c);
             }
-            in_a[iy][ix] = a;
-            in_b[iy][ix] = b;
         }
-        __syncthreads();
-        // the two output pixels' own (a, b) are kept in registers: region A is reused below
-        float av[2], bv[2];
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            av[h] = in_a[(tid >> 5) + 8 * h + 10][(tid & 31) + 10];
-            bv[h] = in_b[(tid >> 5) + 8 * h + 10][(tid & 31) + 10];
+        for (int q = 0; q < PER; q++) {
+            const int k = tid + q * L_THREADS;
+            if (k < NEL) {
+                (&sm.in[0][0][0])[k] = va[q];
+                (&sm.in[1][0][0])[k] = vb[q];
+            }
         }
-        // 2) horizontal blur of the 5 moments at columns [x0-5, x0+LW+5)
-        for (int k = tid; k < IH * BW; k += L_THREADS) {
-            const int iy = k / BW, bx = k % BW;
-            const int x = x0 - 5 + bx;
-            float m0 = 0.f, m1 = 0.f, m2 = 0.f, m3 = 0.f, m4 = 0.f;
-            if (INTERIOR || (x >= 0 && x < W)) {
-                const float *F = tab_x + 22 * x;
+    }
+    __syncthreads();
+    // 2) horizontal blur of the 5 moments (a, b, aa, bb, ab); hx column j <-> x = x0-5+j
+    for (int it = tid; it < NIR * (HXC / HB); it += L_THREADS) {
+        const int iy = it % NIR, c0 = HB * (it / NIR);  // a warp: consecutive rows, one strip
+        float m[5][HB];
 #pragma unroll
-                for (int d = 0; d < 11; d++) {
-                    const float wgt = INTERIOR ? kw(d) : F[d];
-                    const float a = in_a[iy][bx + d], b = in_b[iy][bx + d];
-                    const float wa = wgt * a, wb = wgt * b;
-                    m0 += wa;
-                    m1 += wb;
-                    m2 += wa * a;
-                    m3 += wb * b;
-                    m4 += wa * b;
+        for (int k = 0; k < HB; k++) m[0][k] = m[1][k] = m[2][k] = m[3][k] = m[4][k] = 0.0f;
+#pragma unroll
+        for (int t = 0; t < HB + 10; t++) {
+            const float at = sm.in[0][iy][c0 + t], bt = sm.in[1][iy][c0 + t];
+            const float aa = at * at, bb = bt * bt, ab = at * bt;
+#pragma unroll
+            for (int k = 0; k < HB; k++) {
+                const int d = t - k;
+                if (d >= 0 && d < 11) {
+                    const int xp = min(max(x0 - 5 + c0 + k, 0), W - 1);
+                    const float w = wtab<INTERIOR>(tab_x, xp, d);
+                    m[0][k] += w * at;
+                    m[1][k] += w * bt;
+                    m[2][k] += w * aa;
+                    m[3][k] += w * bb;
+                    m[4][k] += w * ab;
                 }
             }
-            hx[0][iy][bx] = m0;
-            hx[1][iy][bx] = m1;
-            hx[2][iy][bx] = m2;
-            hx[3][iy][bx] = m3;
-            hx[4][iy][bx] = m4;
         }
-        __syncthreads();
-        // 3) vertical blur -> SSIM map and its partials at [y0-5, y0+LH+5) x [x0-5, x0+LW+5)
-        for (int k = tid; k < BH * BW; k += L_THREADS) {
-            const int by = k / BW, bx = k % BW;
-            const int y = y0 - 5 + by, x = x0 - 5 + bx;
-            float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-            if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
-                const float *F = tab_y + 22 * y;
-                float ua = 0.f, ub = 0.f, uaa = 0.f, ubb = 0.f, uab = 0.f;
 #pragma unroll
-                for (int d = 0; d < 11; d++) {
-                    const float wgt = INTERIOR ? kw(d) : F[d];
-                    ua += wgt * hx[0][by + d][bx];
-                    ub += wgt * hx[1][by + d][bx];
-                    uaa += wgt * hx[2][by + d][bx];
-                    ubb += wgt * hx[3][by + d][bx];
-                    uab += wgt * hx[4][by + d][bx];
-                }
-                // R/losses.py:96-113
-                const float va = uaa - ua * ua, vb = ubb - ub * ub, vab = uab - ua * ub;
-                const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
-                const float b1 = ua * ua + ub * ub + C1, b2 = va + vb + C2;
-                const float rden = 1.0f / (b1 * b2);
-                const float S = (a1 * a2) * rden;
-                g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua / b1) + S * (2.0f * ua / b2)) * inv_n;
-                g1 = (-S / b2) * inv_n;
-                g2 = (2.0f * a1 * rden) * inv_n;
-                if (by >= 5 && by < 5 + LH && bx >= 5 && bx < 5 + LW) s_acc += S;
-            }
-            g[0][by][bx] = g0;
-            g[1][by][bx] = g1;
-            g[2][by][bx] = g2;
-        }
-        __syncthreads();
-        // 4) vertical adjoint at rows [y0, y0+LH): sum_d F[p+d][-d] g(p+d)
-        for (int k = tid; k < LH * BW; k += L_THREADS) {
-            const int oy = k / BW, bx = k % BW;
-            const int y = y0 + oy;
-            float r0 = 0.f, r1 = 0.f, r2 = 0.f;
-            if (INTERIOR || y < H) {
-                const float *A = tab_y + 22 * y + 11;  // zero weights where y+d leaves the image
+        for (int q = 0; q < 5; q++)
 #pragma unroll
-                for (int d = 0; d < 11; d++) {
-                    const float wgt = INTERIOR ? kw(d) : A[d];
-                    r0 += wgt * g[0][oy + d][bx];
-                    r1 += wgt * g[1][oy + d][bx];
-                    r2 += wgt * g[2][oy + d][bx];
+            for (int k = 0; k < HB; k++) sm.hx[q][iy][c0 + k] = m[q][k];
+    }
+    __syncthreads();
+    // 3) vertical blur -> SSIM map and its partials (R/losses.py:96-113); g row gy <-> y0-5+gy
+    float s_acc = 0.0f;
+    for (int it = tid; it < GW * NVS; it += L_THREADS) {
+        const int gx = it % GW, gy0 = VS * (it / GW);
+        const int x = x0 - 5 + gx;
+        float u[5][VS];
+#pragma unroll
+        for (int k = 0; k < VS; k++) u[0][k] = u[1][k] = u[2][k] = u[3][k] = u[4][k] = 0.0f;
+#pragma unroll
+        for (int r = 0; r < VS + 10; r++) {
+            if (gy0 + r < NIR) {
+                float h[5];
+#pragma unroll
+                for (int q = 0; q < 5; q++) h[q] = sm.hx[q][gy0 + r][gx];
+#pragma unroll
+                for (int k = 0; k < VS; k++) {
+                    const int d = r - k;
+                    if (d >= 0 && d < 11) {
+                        const int yp = min(max(y0 - 5 + gy0 + k, 0), H - 1);
+                        const float w = wtab<INTERIOR>(tab_y, yp, d);
+#pragma unroll
+                        for (int q = 0; q < 5; q++) u[q][k] += w * h[q];
+                    }
                 }
             }
-            ry[0][oy][bx] = r0;
-            ry[1][oy][bx] = r1;
-            ry[2][oy][bx] = r2;
         }
-        __syncthreads();
-        // 5) horizontal adjoint + gradient assembly for this channel
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int ox = tid & 31, oy = (tid >> 5) + 8 * h;
-            const int x = x0 + ox, y = y0 + oy;
-            float gsum = 0.0f;
+        for (int k = 0; k < VS; k++) {
+            const int gy = gy0 + k, y = y0 - 5 + gy;
+            if (gy < GR) {
+                float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+                if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
+                    const float ua = u[0][k], ub = u[1][k];
+                    const float va = u[2][k] - ua * ua, vb = u[3][k] - ub * ub, vab = u[4][k] - ua * ub;
+                    const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
+                    const float b1 = ua * ua + ub * ub + C1, b2 = va + vb + C2;
+                    const float rden = 1.0f / (b1 * b2);
+                    const float S = (a1 * a2) * rden;
+                    g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua / b1) + S * (2.0f * ua / b2)) *
+                         inv_n;
+                    g1 = (-S / b2) * inv_n;
+                    g2 = (2.0f * a1 * rden) * inv_n;
+                    if (gy >= 5 && gy < 5 + TH && gx >= 5 && gx < 5 + TW) s_acc += S;
+                }
+                g[0][gy][gx] = g0;
+                g[1][gy][gx] = g1;
+                g[2][gy][gx] = g2;
+            }
+        }
+    }
+    __syncthreads();
+    // 4) vertical adjoint at rows [y0, y0+TH): r(p) = sum_d A[p][d] g(p+d) (zero weights where
+    //    p+d leaves the image)
+    for (int it = tid; it < GW * NAS; it += L_THREADS) {
+        const int gx = it % GW, oy0 = AS * (it / GW);
+        float r3[3][AS];
+#pragma unroll
+        for (int k = 0; k < AS; k++) r3[0][k] = r3[1][k] = r3[2][k] = 0.0f;
+#pragma unroll
+        for (int r = 0; r < AS + 10; r++) {
+            const float h0 = g[0][oy0 + r][gx], h1 = g[1][oy0 + r][gx], h2 = g[2][oy0 + r][gx];
+#pragma unroll
+            for (int k = 0; k < AS; k++) {
+                const int d = r - k;
+                if (d >= 0 && d < 11) {
+                    const int yp = min(y0 + oy0 + k, H - 1);
+                    const float w = wtab<INTERIOR>(tab_y + 11, yp, d);
+                    r3[0][k] += w * h0;
+                    r3[1][k] += w * h1;
+                    r3[2][k] += w * h2;
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < AS; k++) {
+            const bool ok = INTERIOR || y0 + oy0 + k < H;
+            ry[0][oy0 + k][gx] = ok ? r3[0][k] : 0.0f;
+            ry[1][oy0 + k][gx] = ok ? r3[1][k] : 0.0f;
+            ry[2][oy0 + k][gx] = ok ? r3[2][k] : 0.0f;
+        }
+    }
+    __syncthreads();
+    // 5) horizontal adjoint + gradient assembly (R/losses.py:115-117 and :126-130); a warp
+    //    covers 16 rows x 2 strips
+    float l1_acc = 0.0f;
+    {
+        const int oy = tid & 15, ox0 = HS * (tid >> 4);
+        float A[3][HS];
+#pragma unroll
+        for (int k = 0; k < HS; k++) A[0][k] = A[1][k] = A[2][k] = 0.0f;
+#pragma unroll
+        for (int q = 0; q < 3; q++)
+#pragma unroll
+            for (int t = 0; t < HS + 10; t++) {
+                const float v = ry[q][oy][ox0 + t];
+#pragma unroll
+                for (int k = 0; k < HS; k++) {
+                    const int d = t - k;
+                    if (d >= 0 && d < 11) {
+                        const int xp = min(x0 + ox0 + k, W - 1);
+                        A[q][k] += wtab<INTERIOR>(tab_x + 11, xp, d) * v;
+                    }
+                }
+            }
+        const int y = y0 + oy;
+#pragma unroll
+        for (int k = 0; k < HS; k++) {
+            const int x = x0 + ox0 + k;
             if (INTERIOR || (x < W && y < H)) {
-                float A0 = 0.f, A1 = 0.f, A2 = 0.f;
-                const float *Aw = tab_x + 22 * x + 11;
-#pragma unroll
-                for (int d = 0; d < 11; d++) {
-                    const float wgt = INTERIOR ? kw(d) : Aw[d];
-                    A0 += wgt * ry[0][oy][ox + d];
-                    A1 += wgt * ry[1][oy][ox + d];
-                    A2 += wgt * ry[2][oy][ox + d];
-                }
-                const float a = av[h], b = bv[h];
+                const int64_t p = (int64_t)y * W + x;
+                const float a = __ldg(color + 3 * p + c), b = __ldg(target + 3 * p + c);
                 const float diff = a - b;
                 l1_acc += fabsf(diff);
                 const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
-                // R/losses.py:115-117 and :126-130
-                gsum = (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A0 + 2.0f * a * A1 + b * A2));
+                f.g_color[3 * p + c] =
+                    (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A[0][k] + 2.0f * a * A[1][k] + b * A[2][k]));
+                // the depth/opacity gradient images start at zero (the LiDAR kernel follows)
+                if (c == 0) {
+                    f.g_depth[p] = 0.0f;
+                    f.g_opac[p] = 0.0f;
+                }
             }
-            grad_out[h][c] = gsum;
-        }
-    }
-    // write gradients (and zero the depth/opacity gradient images: the LiDAR kernel follows)
-#pragma unroll
-    for (int h = 0; h < 2; h++) {
-        const int x = x0 + (tid & 31), y = y0 + (tid >> 5) + 8 * h;
-        if (x < W && y < H) {
-            const int64_t p = (int64_t)y * W + x;
-            f.g_color[3 * p] = grad_out[h][0];
-            f.g_color[3 * p + 1] = grad_out[h][1];
-            f.g_color[3 * p + 2] = grad_out[h][2];
-            f.g_depth[p] = 0.0f;
-            f.g_opac[p] = 0.0f;
         }
     }
     // block partial sums (deterministic order: warp butterfly, then fixed warp order)
@@ -251,31 +304,31 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
         s_acc += __shfl_xor_sync(0xffffffffu, s_acc, o);
     }
     if ((tid & 31) == 0) {
-        red[0][tid >> 5] = l1_acc;
-        red[1][tid >> 5] = s_acc;
+        sm.red[0][tid >> 5] = l1_acc;
+        sm.red[1][tid >> 5] = s_acc;
     }
     __syncthreads();
     if (tid == 0) {
         double l1 = 0.0, ss = 0.0;
         for (int w = 0; w < L_THREADS / 32; w++) {
-            l1 += red[0][w];
-            ss += red[1][w];
+            l1 += sm.red[0][w];
+            ss += sm.red[1][w];
         }
-        const int64_t blk = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        const int64_t blk = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
         f.loss_parts[3 * blk] = l1;
         f.loss_parts[3 * blk + 1] = ss;
         f.loss_parts[3 * blk + 2] = 0.0;
     }
 }
 
-// one launch for every tile: interior tiles (halo >= 10 px inside the image) take the
-// compile-time-weight path, border tiles the reflection-table path
-__global__ void __launch_bounds__(L_THREADS) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
-                                                            const float *__restrict__ tab_x,
-                                                            const float *__restrict__ tab_y, float lam) {
+// one launch for every (tile, channel): interior tiles (halo >= 10 px inside the image) take
+// the compile-time-weight path, border tiles the reflection-table path
+__global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
+                                                               const float *__restrict__ tab_x,
+                                                               const float *__restrict__ tab_y, float lam) {
     __shared__ SsimSmem sm;
-    const int x0 = blockIdx.x * LW, y0 = blockIdx.y * LH;
-    if (x0 >= 10 && x0 + LW + 10 <= f.width && y0 >= 10 && y0 + LH + 10 <= f.height)
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+    if (x0 >= 10 && x0 + TW + 10 <= f.width && y0 >= 10 && y0 + TH + 10 <= f.height)
         ssim_tile<true>(sm, f, view, tab_x, tab_y, lam);
     else
         ssim_tile<false>(sm, f, view, tab_x, tab_y, lam);
@@ -352,7 +405,7 @@ constexpr int DEPTH_BLOCKS = 64;
 
 // loss_parts holds ssim blocks followed by DEPTH_BLOCKS depth partials; the F tables follow.
 int64_t loss_parts_needed(int32_t width, int32_t height) {
-    return (int64_t)((width + LW - 1) / LW) * ((height + LH - 1) / LH) + DEPTH_BLOCKS;
+    return 3 * (int64_t)((width + TW - 1) / TW) * ((height + TH - 1) / TH) + DEPTH_BLOCKS;
 }
 
 }  // namespace gs
@@ -364,7 +417,7 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
         set_error("gs_loss: empty image");
         return GS_ERR_DIMS;
     }
-    const int64_t ssim_blocks = (int64_t)((f->width + LW - 1) / LW) * ((f->height + LH - 1) / LH);
+    const int64_t ssim_blocks = 3 * (int64_t)((f->width + TW - 1) / TW) * ((f->height + TH - 1) / TH);
     if (ssim_blocks + DEPTH_BLOCKS > f->loss_blocks) {
         set_error("gs_loss: workspace laid out for a different image size");
         return GS_ERR_WORKSPACE;
@@ -374,7 +427,7 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     loss_tables_kernel<<<(f->width + f->height + 127) / 128, 128, 0, st>>>(tab_x, f->width, tab_y, f->height);
     int rc = check_launch("loss_tables_kernel");
     if (rc) return rc;
-    dim3 grid((f->width + LW - 1) / LW, (f->height + LH - 1) / LH);
+    dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
     ssim_l1_kernel<<<grid, L_THREADS, 0, st>>>(*f, view, tab_x, tab_y, lam);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     depth_loss_kernel<<<DEPTH_BLOCKS, 256, 0, st>>>(*f, view, xi, ssim_blocks);

@@ -131,27 +131,73 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
     warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
 }
 
-// Warp-cooperative exact cull of the large-footprint Gaussians (lanes stride over candidate
-// tiles; same decision function as cull_rect).  Completes kept/keep_bits/touched/key.
+// Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), one CTA per
+// Gaussian, same decision as cull_rect:
+//   A) every candidate tile is classified by continuous bounds of q over its pixel rectangle
+//      (q is convex: its maximum is at a corner; the lower bound is the one of tile_keep) with
+//      a margin far above the fp32 evaluation error, so "surely kept" / "surely culled" agree
+//      with the exact integer-grid test.  Only tiles straddling the qcut boundary are queued;
+//   B) the queued tiles get the exact per-row test, 16 lanes per tile (one pixel row each).
+// Results go to a shared-memory bitmap: by candidate index (big_bits, for the emit) or, for
+// screen-covering Gaussians with a huge slot, by tile index (huge_mask_t row of the slot,
+// transposed into depth order by huge_transpose_kernel).
 constexpr int BIG_THREADS = 256;
+constexpr int CB_WORDS = GS_MAX_TILES / 32;
+constexpr int CB_QCAP = 2048;
+
+// 1: every pixel of the tile has q <= qcut; 0: none has; -1: decide exactly
+__device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb, float cc, float qcut, float kx,
+                                          float ky, int x0, int x1, int y0, int y1) {
+    const float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
+    const float scale = ca * fmaxf(ax0 * ax0, ax1 * ax1) + cc * fmaxf(ay0 * ay0, ay1 * ay1);
+    const float margin = 1e-5f * scale + 1e-6f;
+    const float tb = 2.0f * cb;
+    const float xx0 = ca * ax0 * ax0, xx1 = ca * ax1 * ax1, yy0 = cc * ay0 * ay0, yy1 = cc * ay1 * ay1;
+    float qmax = xx0 + tb * ax0 * ay0 + yy0;
+    qmax = fmaxf(qmax, xx1 + tb * ax1 * ay0 + yy0);
+    qmax = fmaxf(qmax, xx0 + tb * ax0 * ay1 + yy1);
+    qmax = fmaxf(qmax, xx1 + tb * ax1 * ay1 + yy1);
+    if (qmax + margin < qcut) return 1;
+    if (!(ax0 <= 0.0f && ax1 >= 0.0f && ay0 <= 0.0f && ay1 >= 0.0f)) {
+        float qc = 3.0e38f;
+        const float ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
+#pragma unroll
+        for (int k = 0; k < 2; k++) {
+            const float y = ys[k];
+            const float dx = fminf(fmaxf(kx * y, ax0), ax1);  // kx = -cb/ca
+            qc = fminf(qc, ca * dx * dx + tb * dx * y + cc * y * y);
+            const float x = xs[k];
+            const float dy = fminf(fmaxf(ky * x, ay0), ay1);  // ky = -cb/cc
+            qc = fminf(qc, ca * x * x + tb * x * dy + cc * dy * dy);
+        }
+        if (qc - margin > qcut) return 0;
+    }
+    return -1;
+}
 
 __global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f, int allow_huge) {
-    // one CTA per large-footprint Gaussian: threads stride over its candidate tiles
-    __shared__ int s_cnt, s_slot;
+    __shared__ uint32_t s_bits[CB_WORDS];
+    __shared__ int32_t s_queue[CB_QCAP];
+    __shared__ int s_nq, s_slot, s_cnt;
     __shared__ int64_t s_base;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
     const int64_t nb = f.counters[GS_CNT_BIG];
     for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
         const int g = f.big_list[b];
         const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
         const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+        const float mx = s0.x, my = s0.y, ca = s0.z, cb = s0.w, cc = s1.x, qcut = s1.w;
         const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
         const int words = (ncand + 31) >> 5;
-        if (threadIdx.x == 0) {
+        // the bounds are conservative (margin), so their minimisers need not be exact
+        const float kx = __fdividef(-cb, ca), ky = __fdividef(-cb, cc);
+        if (tid == 0) {
             s_cnt = 0;
-            // screen-covering Gaussians take a huge slot: their kept tiles are recorded in the
-            // per-tile masks (huge_mask[tile] bit slot) and they skip the emit + sort
+            s_nq = 0;
+            // screen-covering Gaussians take a huge slot: their kept tiles are recorded per
+            // tile and they skip the emit + sort
             int slot = -1;
             if (allow_huge && ncand > GS_HUGE_CAND) {
                 slot = atomicAdd(&f.counters[GS_CNT_HUGE], 1);
@@ -167,34 +213,79 @@ __global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f, int a
             s_base = base;
         }
         __syncthreads();
-        const int64_t base = s_base;
         const int slot = s_slot;
-        int count = 0;
-        for (int c0 = 0; c0 < ncand; c0 += BIG_THREADS) {  // uniform trip count: ballots are warp-wide
-            const int c = c0 + threadIdx.x;
-            bool keep = false;
-            int tx = 0, ty = 0;
-            if (c < ncand) {
-                tx = r.x + c % nx;
-                ty = r.z + c / nx;
+        const int64_t base = s_base;
+        const bool by_tile = slot >= 0;
+        const int nwords = by_tile ? tw : words;
+        for (int w = tid; w < nwords; w += BIG_THREADS) s_bits[w] = 0u;
+        __syncthreads();
+        // A) classification; (tx, ty) of candidate c advance incrementally (no divides)
+        {
+            const int sy = BIG_THREADS / nx, sx = BIG_THREADS % nx;
+            int ty = r.z + tid / nx, tx = r.x + tid % nx;
+            for (int c = tid; c < ncand; c += BIG_THREADS) {
                 const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
                 const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                int cls = tile_class(mx, my, ca, cb, cc, qcut, kx, ky, x0, x1, y0, y1);
+                if (cls < 0) {
+                    const unsigned amb = __activemask();
+                    const unsigned lt = amb & ((1u << lane) - 1u);
+                    int q0 = 0;
+                    if (lt == 0u) q0 = atomicAdd(&s_nq, __popc(amb));
+                    const int q = __shfl_sync(amb, q0, __ffs(amb) - 1) + __popc(lt);
+                    if (q < CB_QCAP) s_queue[q] = c;
+                    else cls = tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1) ? 1 : 0;
+                }
+                // one shared atomic per distinct bitmap word of the warp
+                const int bit = by_tile ? ty * f.tiles_x + tx : c;
+                const unsigned act = __activemask();
+                const unsigned peers = __match_any_sync(act, bit >> 5);
+                const unsigned word = __reduce_or_sync(peers, cls > 0 ? 1u << (bit & 31) : 0u);
+                if (lane == __ffs(peers) - 1 && word) atomicOr(&s_bits[bit >> 5], word);
+                tx += sx;
+                ty += sy;
+                if (tx > r.y) {
+                    tx -= nx;
+                    ty++;
+                }
             }
-            count += keep;
-            if (slot >= 0) {
-                if (keep)
-                    atomicOr(&f.huge_mask[(int64_t)(ty * f.tiles_x + tx) * (GS_HUGE_CAP / 32) + (slot >> 5)],
-                             1u << (slot & 31));
-            } else {
-                const unsigned bal = __ballot_sync(0xffffffffu, keep);
-                if (lane == 0 && base >= 0 && (c0 >> 5) + warp < words) f.big_bits[base + (c0 >> 5) + warp] = bal;
+        }
+        __syncthreads();
+        // B) exact test of the queued tiles: 16 lanes per tile, one pixel row per lane
+        {
+            const int nq = min(s_nq, CB_QCAP);
+            const int grp = tid >> 4, row = tid & 15;
+            for (int q0 = 0; q0 < nq; q0 += BIG_THREADS / 16) {  // uniform trip count: ballots are warp-wide
+                const int qi = q0 + grp;
+                bool hit = false;
+                int c = 0, tx = 0, ty = 0;
+                if (qi < nq) {
+                    c = s_queue[qi];
+                    ty = r.z + c / nx;
+                    tx = r.x + c % nx;
+                    const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                    const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                    if (y0 + row <= y1) hit = row_hits(mx, my, ca, cb, cc, qcut, x0, x1, y0 + row);
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, hit);
+                if (row == 0 && ((bal >> (lane & 16)) & 0xffffu)) {
+                    const int bit = by_tile ? ty * f.tiles_x + tx : c;
+                    atomicOr(&s_bits[bit >> 5], 1u << (bit & 31));
+                }
             }
+        }
+        __syncthreads();
+        int count = 0;
+        for (int w = tid; w < nwords; w += BIG_THREADS) {
+            const uint32_t v = s_bits[w];
+            count += __popc(v);
+            if (by_tile) f.huge_mask_t[(int64_t)slot * tw + w] = v;
+            else if (base >= 0) f.big_bits[base + w] = v;
         }
         for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
         if (lane == 0 && count) atomicAdd(&s_cnt, count);
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (tid == 0) {
             const int kept = s_cnt;
             f.kept[g] = kept;
             f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
@@ -367,8 +458,6 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
         return GS_ERR_ARG;
     }
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
-    cudaMemsetAsync(f->huge_mask, 0, sizeof(uint32_t) * (size_t)f->tiles_x * f->tiles_y * (GS_HUGE_CAP / 32),
-                    (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     int64_t warps = (f->n + 31) / 32;
     int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
@@ -402,8 +491,6 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
                               const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                               void *stream) {
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
-    cudaMemsetAsync(f->huge_mask, 0, sizeof(uint32_t) * (size_t)f->tiles_x * f->tiles_y * (GS_HUGE_CAP / 32),
-                    (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);

@@ -28,3 +28,5 @@ tx0 = np.maximum(tx0, rect[:, 0]); tx1 = np.minimum(tx1, rect[:, 1]); ty0 = np.m
 nc2 = np.where(act & (tx1 >= tx0) & (ty1 >= ty0), (tx1 - tx0 + 1) * (ty1 - ty0 + 1), 0)
 print("ellipse-bbox cand", nc2.sum(), "big", (nc2 > 16).sum(), "cand of big", nc2[nc2 > 16].sum())
 print("touched", (kept > 0).sum(), "E", int(out.ctx["counters"][1]))
+c = out.ctx["counters"].cpu().numpy() if hasattr(out.ctx["counters"], "cpu") else out.ctx["counters"]
+print("counters", list(c[:20]))
