@@ -70,7 +70,8 @@ enum {
     GS_CNT_HUGE = 16,    /* screen-covering Gaussians binned per tile by bitmap (not sorted) */
     GS_CNT_HUGE_E = 17,  /* their kept pairs */
     GS_CNT_SMALL_E = 18, /* entries emitted into the tile sort (0 after an overflow) */
-    GS_CNT_HUGE_N = 19   /* huge Gaussians with >= 1 kept tile (records in depth order) */
+    GS_CNT_HUGE_N = 19,  /* huge Gaussians with >= 1 kept tile (records in depth order) */
+    GS_CNT_CULLQ1 = 20   /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
 };
 
 #define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */
@@ -116,6 +117,9 @@ typedef struct gs_frame {
     int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */
     int32_t *big_list;       /* n: Gaussians with > GS_SMALL_CAND candidate tiles (warp-culled) */
     int32_t *big_emit;       /* n: depth ranks of those Gaussians (warp-emitted) */
+    int32_t *big_slot;       /* n: huge slot (or -1) per big_list entry */
+    int32_t *cull_queue;     /* cull_queue_cap x 2: (big index, tx << 16 | ty) left open by the band bounds */
+    int64_t cull_queue_cap;
     int32_t *huge;           /* GS_HUGE_CAP x 8: screen-covering Gaussians in depth order (id,
                                 rank, rect, bitmap base) + compaction scratch */
     uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: bit j of word w <-> the (32w+j)-th huge

@@ -42,6 +42,7 @@ class GsFrame(ctypes.Structure):
                 ("tiles_y", i32),
                 ("splat2d", P), ("cov2d", P), ("rect", P), ("valid", P), ("touched", P), ("touched_list", P),
                 ("g2d", P), ("grad_rows", P), ("bias_corr", P), ("keep_bits", P), ("kept", P), ("counts", P), ("big_list", P), ("big_emit", P),
+                ("big_slot", P), ("cull_queue", P), ("cull_queue_cap", i64),
                 ("huge", P), ("huge_mask", P), ("huge_mask_t", P), ("huge_before", P),
                 ("tile_scratch", P), ("big_bits", P), ("big_bits_words", i64),
                 ("keys_a", P), ("keys_b", P), ("sort_hist", P), ("sort_status", P), ("scan_status", P),

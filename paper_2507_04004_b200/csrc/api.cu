@@ -81,6 +81,9 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.counts = c.take<int32_t>(nn + 1);
     f.big_list = c.take<int32_t>(nn);
     f.big_emit = c.take<int32_t>(nn);
+    f.big_slot = c.take<int32_t>(nn);
+    f.cull_queue_cap = nn > (1 << 20) ? nn : (1 << 20);
+    f.cull_queue = c.take<int32_t>(2 * f.cull_queue_cap);
     // huge records (8 ints each), their ids in depth order, per-chunk compaction counts
     f.huge = c.take<int32_t>(9 * GS_HUGE_CAP + (nn + 1023) / 1024 + 1);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));

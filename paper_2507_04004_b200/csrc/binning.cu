@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) emit_big_kernel(gs_frame f, const uint64_
         const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
         const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
-        const int64_t base = (int64_t)f.keep_bits[g];  // cull bitmap from cull_big_kernel (-1: none)
+        const int64_t base = (int64_t)f.keep_bits[g];  // cull bitmap from big_bands_kernel (-1: none)
         int64_t off = f.counts[k];
         for (int c0 = 0; c0 < ncand; c0 += 256) {
             const int c = c0 + threadIdx.x;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(HCHUNK) huge_write_kernel(gs_frame f, const ui
 }
 
 // Per-tile masks in depth order: bit j of huge_mask[t][w] <-> huge record 32w + j keeps tile t
-// (a 32 x 32 bit transpose per warp of huge_mask_t rows, which cull_big_kernel wrote by slot),
+// (a 32 x 32 bit transpose per warp of huge_mask_t rows, which the big_* cull kernels wrote by slot),
 // plus the per-tile huge counts.
 __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
     const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
                                                       f.tiles_x, f.tiles_y, rect, qcut, radius);
             if (!active) rect = make_int4(0, -1, 0, -1);
             // exact per-tile cull of the rectangle (R/rasterizer.py:150-166), fused here for small
-            // footprints; large ones are culled warp-cooperatively by cull_big_kernel
+            // footprints; large ones by the big_* kernels (band bounds, tile bounds, exact rows)
             const int ncand = (rect.y - rect.x + 1) * (rect.w - rect.z + 1);
             big = active && ncand > GS_SMALL_CAND;
             uint64_t bits = 0ull;
@@ -131,21 +131,24 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
     warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
 }
 
-// Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), one CTA per
-// Gaussian, same decision as cull_rect:
-//   A) every candidate tile is classified by continuous bounds of q over its pixel rectangle
-//      (q is convex: its maximum is at a corner; the lower bound is the one of tile_keep) with
-//      a margin far above the fp32 evaluation error, so "surely kept" / "surely culled" agree
-//      with the exact integer-grid test.  Only tiles straddling the qcut boundary are queued;
-//   B) the queued tiles get the exact per-row test, 16 lanes per tile (one pixel row each).
-// Results go to a shared-memory bitmap: by candidate index (big_bits, for the emit) or, for
-// screen-covering Gaussians with a huge slot, by tile index (huge_mask_t row of the slot,
-// transposed into depth order by huge_transpose_kernel).
-constexpr int BIG_THREADS = 256;
-constexpr int CB_WORDS = GS_MAX_TILES / 32;
-constexpr int CB_QCAP = 2048;
+// Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), same decision
+// as cull_rect, spread over the whole GPU in four launches (a few screen-covering Gaussians
+// carry thousands of candidate tiles, so per-Gaussian work units would serialise on them):
+//   K0 big_setup_kernel  huge slot / bitmap base per Gaussian;
+//   K1 big_bands_kernel  warp per Gaussian, lane per tile row ("band"): bounds of the footprint
+//                        ellipse give a run of surely-kept tiles (set as bit ranges) between
+//                        runs of surely-culled ones; the tiles in between are queued;
+//   K2 big_tiles_kernel  thread per queued tile: per-tile corner / lower bounds; the tiles the
+//                        boundary actually crosses get the exact test, 16 lanes per tile and
+//                        one pixel row each (row_hits);
+//   K3 big_finish_kernel touched / key / huge encoding / touched list.
+// Output bitmaps: big_bits by candidate index (for the emit) or, for screen-covering Gaussians
+// with a huge slot, by tile index (huge_mask_t row of the slot, transposed into depth order by
+// huge_transpose_kernel).
 
-// 1: every pixel of the tile has q <= qcut; 0: none has; -1: decide exactly
+// Per-tile bounds: 1 if every pixel of the tile has q <= qcut (its four corners, q convex),
+// 0 if none has (continuous lower bound over the rectangle, as tile_keep), -1: decide exactly.
+// kx = -cb/ca, ky = -cb/cc: the bounds carry a margin, so their minimisers need not be exact.
 __device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb, float cc, float qcut, float kx,
                                           float ky, int x0, int x1, int y0, int y1) {
     const float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
@@ -164,10 +167,10 @@ __device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb
 #pragma unroll
         for (int k = 0; k < 2; k++) {
             const float y = ys[k];
-            const float dx = fminf(fmaxf(kx * y, ax0), ax1);  // kx = -cb/ca
+            const float dx = fminf(fmaxf(kx * y, ax0), ax1);
             qc = fminf(qc, ca * dx * dx + tb * dx * y + cc * y * y);
             const float x = xs[k];
-            const float dy = fminf(fmaxf(ky * x, ay0), ay1);  // ky = -cb/cc
+            const float dy = fminf(fmaxf(ky * x, ay0), ay1);
             qc = fminf(qc, ca * x * x + tb * x * dy + cc * dy * dy);
         }
         if (qc - margin > qcut) return 0;
@@ -175,15 +178,164 @@ __device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb
     return -1;
 }
 
-__global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f, int allow_huge) {
-    __shared__ uint32_t s_bits[CB_WORDS];
-    __shared__ int32_t s_queue[CB_QCAP];
-    __shared__ int s_nq, s_slot, s_cnt;
-    __shared__ int64_t s_base;
-    const int tid = threadIdx.x, lane = tid & 31;
+// Per-Gaussian constants of the band bounds.  E(k) = {q <= k} is an ellipse: its x-extent over
+// a band's rows bounds the possibly-kept tiles (k = qp = qcut + margin), and a tile whose four
+// corner pixels lie in E(qm), qm = qcut - margin, has every pixel inside (q is convex).  The
+// discriminants are formed in FP64 (no cancellation), the square roots in fp32: their 1e-7
+// relative error is far below the margin's 5e-6 relative widening of the ellipse.
+struct BandConst {
+    double mx, my, a, b, det, inv_a, qm, qp, dymax, dyr, eps;
+    bool ok;
+};
+
+__device__ __forceinline__ BandConst band_const(float mx, float my, float ca, float cb, float cc, float qcut, int4 r) {
+    BandConst k;
+    k.mx = mx;
+    k.my = my;
+    k.a = ca;
+    k.b = cb;
+    const double c = cc;
+    k.det = k.a * c - k.b * k.b;
+    const double ax = fmax(fabs((double)(r.x * GS_TILE) - k.mx), fabs((double)(r.y * GS_TILE + GS_TILE) - k.mx));
+    const double ay = fmax(fabs((double)(r.z * GS_TILE) - k.my), fabs((double)(r.w * GS_TILE + GS_TILE) - k.my));
+    const double margin = 1e-5 * (k.a * ax * ax + c * ay * ay) + 1e-6;
+    k.qm = (double)qcut - margin;
+    k.qp = (double)qcut + margin;
+    k.ok = k.a > 0.0 && c > 0.0 && k.det > 0.0 && k.qp > 0.0 && isfinite(k.det) && isfinite(margin);
+    k.inv_a = k.ok ? 1.0 / k.a : 0.0;
+    k.dymax = k.ok ? (double)sqrtf((float)(k.a * k.qp / k.det)) * (1.0 + 1e-6) : 0.0;
+    k.dyr = k.ok ? -k.b / c * (double)sqrtf((float)(k.qp * c / k.det)) : 0.0;  // dy of the rightmost point
+    const double hw = k.ok ? (double)sqrtf((float)(k.qp * c / k.det)) : 0.0;
+    k.eps = 1e-3 + 1e-6 * (fabs(k.mx) + hw);
+    return k;
+}
+
+// (pl, kl, kr, pr): tiles outside [pl, pr] surely culled, [kl, kr] surely kept (empty if
+// kl > kr), the rest ambiguous
+__device__ __forceinline__ int4 band_ranges(const BandConst &k, int ty, int4 r, int width, int height, int tiles_x) {
+    const int y0 = ty * GS_TILE, y1 = min(y0 + GS_TILE - 1, height - 1);
+    if (!k.ok) return make_int4(r.x, r.y + 1, r.y, r.y);
+    const double D0 = (double)y0 - k.my, D1 = (double)y1 - k.my;
+    const double lo = fmax(D0, -k.dymax), hi = fmin(D1, k.dymax);
+    if (lo > hi) return make_int4(r.x, r.y + 1, r.y, r.x - 1);  // the band misses E(qp)
+    const double dyr = fmin(fmax(k.dyr, lo), hi), dyl = fmin(fmax(-k.dyr, lo), hi);
+    const double sr = sqrtf((float)fmax(0.0, k.a * k.qp - k.det * dyr * dyr));
+    const double sl = sqrtf((float)fmax(0.0, k.a * k.qp - k.det * dyl * dyl));
+    const double xr = k.mx + (-k.b * dyr + sr) * k.inv_a + k.eps;
+    const double xl = k.mx + (-k.b * dyl - sl) * k.inv_a - k.eps;
+    // tile t spans pixels [16t, min(16t+15, W-1)]: possible iff 16t+15 >= xl and 16t <= xr
+    const int pl = (int)fmax((double)r.x, fmin((double)r.y + 1.0, ceil((xl - 15.0) * 0.0625)));
+    const int pr = (int)fmin((double)r.y, fmax((double)r.x - 1.0, floor(xr * 0.0625)));
+    if (pl > pr) return make_int4(r.x, r.y + 1, r.y, r.x - 1);
+    int4 out = make_int4(pl, pr + 1, pr, pr);
+    if (k.qm > 0.0) {
+        const double d0 = k.a * k.qm - k.det * D0 * D0, d1 = k.a * k.qm - k.det * D1 * D1;
+        if (d0 > 0.0 && d1 > 0.0) {
+            const double s0 = sqrtf((float)d0), s1 = sqrtf((float)d1);
+            const double il = k.mx + fmax(-k.b * D0 - s0, -k.b * D1 - s1) * k.inv_a + k.eps;
+            const double ir = k.mx + fmin(-k.b * D0 + s0, -k.b * D1 + s1) * k.inv_a - k.eps;
+            if (il <= ir) {
+                int kl = (int)fmax(-1.0, fmin(1e9, ceil(il * 0.0625)));
+                int kr = ((double)(width - 1) <= ir) ? tiles_x - 1
+                                                     : (int)fmax(-2.0, fmin(1e9, floor((ir - 15.0) * 0.0625)));
+                kl = max(kl, pl);
+                kr = min(kr, pr);
+                if (kl <= kr) out = make_int4(pl, kl, kr, pr);
+            }
+        }
+    }
+    return out;
+}
+
+// K1: warp per large-footprint Gaussian: zeroes the output bitmap row, sets the surely-kept run
+// of every band and queues the band's ambiguous tiles (overflowing the queue: exact test in
+// place).  kept[g] starts at the surely-kept count.
+__device__ __forceinline__ void set_bit_range(uint32_t *bits, int b0, int b1) {
+    for (int w = b0 >> 5; w <= (b1 >> 5); w++) {
+        const int lo_b = max(b0, w << 5) - (w << 5), hi_b = min(b1, (w << 5) + 31) - (w << 5);
+        const uint32_t m = (hi_b - lo_b == 31) ? 0xffffffffu : (((1u << (hi_b - lo_b + 1)) - 1u) << lo_b);
+        atomicOr(&bits[w], m);
+    }
+}
+
+struct BigCtx {
+    int g, slot;
+    int64_t base;
+    float4 s0, s1;
+    int4 r;
+    uint32_t *bits;  // output bitmap row (nullptr: big_bits overflow, the emit re-culls)
+};
+
+__device__ __forceinline__ BigCtx big_ctx(const gs_frame &f, int64_t b) {
+    BigCtx c;
+    c.g = f.big_list[b];
+    c.s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * c.g];
+    c.s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * c.g + 1];
+    c.r = reinterpret_cast<const int4 *>(f.rect)[c.g];
+    c.slot = f.big_slot[b];
+    c.base = (int64_t)f.keep_bits[c.g];
+    const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
+    c.bits = c.slot >= 0 ? f.huge_mask_t + (int64_t)c.slot * tw : (c.base >= 0 ? f.big_bits + c.base : nullptr);
+    return c;
+}
+
+__device__ __forceinline__ int big_bit(const BigCtx &c, int tiles_x, int tx, int ty) {
+    return c.slot >= 0 ? ty * tiles_x + tx : (ty - c.r.z) * (c.r.y - c.r.x + 1) + (tx - c.r.x);
+}
+
+constexpr int CB_WARPS = 8;
+
+// K0: thread per large-footprint Gaussian: huge slot or bitmap base (warp-aggregated
+// reservations: one atomic per warp and counter)
+__global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_huge) {
+    const int64_t nb = f.counters[GS_CNT_BIG];
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = b0 + threadIdx.x;  // uniform trip count: the reservations are warp-wide
+        int g = 0, words = 0;
+        bool huge = false;
+        if (b < nb) {
+            g = f.big_list[b];
+            const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+            const int ncand = (r.y - r.x + 1) * (r.w - r.z + 1);
+            words = (ncand + 31) >> 5;
+            huge = allow_huge && ncand > GS_HUGE_CAND;
+        }
+        // screen-covering Gaussians take a huge slot: their kept tiles are recorded per tile
+        // and they skip the emit + sort; the others keep a cull bitmap for the emit
+        const unsigned hm = __ballot_sync(0xffffffffu, huge);
+        int s0 = 0;
+        if (lane == 0 && hm) s0 = atomicAdd(&f.counters[GS_CNT_HUGE], __popc(hm));
+        const int sbase = __shfl_sync(0xffffffffu, s0, 0);  // all lanes: full-mask shuffle
+        int slot = huge ? sbase + __popc(hm & ((1u << lane) - 1u)) : -1;
+        if (slot >= GS_HUGE_CAP) slot = -1;
+        const int w = (b < nb && slot < 0) ? words : 0;
+        int x = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const int tot = __shfl_sync(0xffffffffu, x, 31);
+        long long bb = 0;
+        if (lane == 0 && tot) bb = atomicAdd(&f.counters[GS_CNT_BIG_BITS], tot);
+        long long base = __shfl_sync(0xffffffffu, bb, 0) + (x - w);
+        if (b < nb) {
+            if (slot >= 0 || base + w > f.big_bits_words) base = -1;  // overflow: the emit re-culls
+            f.big_slot[b] = slot;
+            f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+        }
+    }
+}
+
+__global__ void __launch_bounds__(CB_WARPS * 32) big_bands_kernel(gs_frame f) {
+    const int lane = threadIdx.x & 31;
     const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
     const int64_t nb = f.counters[GS_CNT_BIG];
-    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    const int64_t cap = f.cull_queue_cap;
+    int2 *q1 = reinterpret_cast<int2 *>(f.cull_queue);
+    for (int64_t b = (int64_t)blockIdx.x * CB_WARPS + (threadIdx.x >> 5); b < nb;
+         b += (int64_t)gridDim.x * CB_WARPS) {
         const int g = f.big_list[b];
         const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
         const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
@@ -191,115 +343,137 @@ __global__ void __launch_bounds__(BIG_THREADS) cull_big_kernel(gs_frame f, int a
         const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
         const int words = (ncand + 31) >> 5;
-        // the bounds are conservative (margin), so their minimisers need not be exact
-        const float kx = __fdividef(-cb, ca), ky = __fdividef(-cb, cc);
-        if (tid == 0) {
-            s_cnt = 0;
-            s_nq = 0;
-            // screen-covering Gaussians take a huge slot: their kept tiles are recorded per
-            // tile and they skip the emit + sort
-            int slot = -1;
-            if (allow_huge && ncand > GS_HUGE_CAND) {
-                slot = atomicAdd(&f.counters[GS_CNT_HUGE], 1);
-                if (slot >= GS_HUGE_CAP) slot = -1;
+        const int slot = f.big_slot[b];
+        const int64_t base = (int64_t)f.keep_bits[g];
+        uint32_t *bits = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : (base >= 0 ? f.big_bits + base : nullptr);
+        const int nwords = slot >= 0 ? tw : words;
+        if (bits)
+            for (int w = lane; w < nwords; w += 32) bits[w] = 0u;
+        __syncwarp();
+        const BandConst K = band_const(mx, my, ca, cb, cc, qcut, r);
+        int kept = 0;
+        const int nbands = r.w - r.z + 1;
+        for (int b0 = 0; b0 < nbands; b0 += 32) {  // uniform trip count: the queue slots are reserved warp-wide
+            const int bi = b0 + lane;
+            const int ty = r.z + bi;
+            int4 br = make_int4(0, 1, 0, -1);  // nothing
+            if (bi < nbands) br = band_ranges(K, ty, r, f.width, f.height, f.tiles_x);
+            const int base_bit = slot >= 0 ? ty * f.tiles_x : bi * nx - r.x;  // bit of tile tx: base_bit + tx
+            const bool has_keep = br.y <= br.z;
+            if (has_keep) {
+                kept += br.z - br.y + 1;
+                if (bits) set_bit_range(bits, base_bit + br.y, base_bit + br.z);
             }
-            s_slot = slot;
-            // the others keep a cull bitmap for the emit (on overflow the emit re-culls)
-            int64_t base = -1;
-            if (slot < 0) {
-                base = atomicAdd(&f.counters[GS_CNT_BIG_BITS], words);
-                if (base + words > f.big_bits_words) base = -1;
+            // ambiguous: [pl, kl) and (kr, pr] (all of [pl, pr] when nothing is surely kept)
+            const int namb = has_keep ? (br.y - br.x) + (br.w - br.z) : max(0, br.w - br.x + 1);
+            int x = namb;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
-            s_base = base;
-        }
-        __syncthreads();
-        const int slot = s_slot;
-        const int64_t base = s_base;
-        const bool by_tile = slot >= 0;
-        const int nwords = by_tile ? tw : words;
-        for (int w = tid; w < nwords; w += BIG_THREADS) s_bits[w] = 0u;
-        __syncthreads();
-        // A) classification; (tx, ty) of candidate c advance incrementally (no divides)
-        {
-            const int sy = BIG_THREADS / nx, sx = BIG_THREADS % nx;
-            int ty = r.z + tid / nx, tx = r.x + tid % nx;
-            for (int c = tid; c < ncand; c += BIG_THREADS) {
-                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                int cls = tile_class(mx, my, ca, cb, cc, qcut, kx, ky, x0, x1, y0, y1);
-                if (cls < 0) {
-                    const unsigned amb = __activemask();
-                    const unsigned lt = amb & ((1u << lane) - 1u);
-                    int q0 = 0;
-                    if (lt == 0u) q0 = atomicAdd(&s_nq, __popc(amb));
-                    const int q = __shfl_sync(amb, q0, __ffs(amb) - 1) + __popc(lt);
-                    if (q < CB_QCAP) s_queue[q] = c;
-                    else cls = tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1) ? 1 : 0;
-                }
-                // one shared atomic per distinct bitmap word of the warp
-                const int bit = by_tile ? ty * f.tiles_x + tx : c;
-                const unsigned act = __activemask();
-                const unsigned peers = __match_any_sync(act, bit >> 5);
-                const unsigned word = __reduce_or_sync(peers, cls > 0 ? 1u << (bit & 31) : 0u);
-                if (lane == __ffs(peers) - 1 && word) atomicOr(&s_bits[bit >> 5], word);
-                tx += sx;
-                ty += sy;
-                if (tx > r.y) {
-                    tx -= nx;
-                    ty++;
-                }
-            }
-        }
-        __syncthreads();
-        // B) exact test of the queued tiles: 16 lanes per tile, one pixel row per lane
-        {
-            const int nq = min(s_nq, CB_QCAP);
-            const int grp = tid >> 4, row = tid & 15;
-            for (int q0 = 0; q0 < nq; q0 += BIG_THREADS / 16) {  // uniform trip count: ballots are warp-wide
-                const int qi = q0 + grp;
-                bool hit = false;
-                int c = 0, tx = 0, ty = 0;
-                if (qi < nq) {
-                    c = s_queue[qi];
-                    ty = r.z + c / nx;
-                    tx = r.x + c % nx;
+            const int tot = __shfl_sync(0xffffffffu, x, 31);
+            if (tot == 0) continue;
+            long long qb = 0;
+            if (lane == 0) qb = atomicAdd(&f.counters[GS_CNT_CULLQ1], tot);
+            int64_t q = (int64_t)__shfl_sync(0xffffffffu, qb, 0) + (x - namb);
+            if (namb == 0) continue;
+            for (int tx = br.x; tx <= br.w; tx++, q++) {
+                if (has_keep && tx == br.y) tx = br.z + 1;
+                if (tx > br.w) break;
+                if (q < cap) {
+                    q1[q] = make_int2((int)b, (int)(((uint32_t)tx << 16) | (uint32_t)ty));
+                } else {
                     const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
                     const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                    if (y0 + row <= y1) hit = row_hits(mx, my, ca, cb, cc, qcut, x0, x1, y0 + row);
-                }
-                const unsigned bal = __ballot_sync(0xffffffffu, hit);
-                if (row == 0 && ((bal >> (lane & 16)) & 0xffffu)) {
-                    const int bit = by_tile ? ty * f.tiles_x + tx : c;
-                    atomicOr(&s_bits[bit >> 5], 1u << (bit & 31));
+                    if (tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1)) {
+                        kept++;
+                        if (bits) atomicOr(&bits[(base_bit + tx) >> 5], 1u << ((base_bit + tx) & 31));
+                    }
                 }
             }
         }
-        __syncthreads();
-        int count = 0;
-        for (int w = tid; w < nwords; w += BIG_THREADS) {
-            const uint32_t v = s_bits[w];
-            count += __popc(v);
-            if (by_tile) f.huge_mask_t[(int64_t)slot * tw + w] = v;
-            else if (base >= 0) f.big_bits[base + w] = v;
+        for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+        if (lane == 0) f.kept[g] = kept;
+    }
+}
+
+// K2: thread per band-ambiguous tile: per-tile bounds; the tiles the qcut boundary actually
+// crosses get the exact per-row test cooperatively, 16 lanes per tile (one pixel row each)
+__global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
+    const int64_t cap = f.cull_queue_cap;
+    const int64_t n1 = min((int64_t)f.counters[GS_CNT_CULLQ1], cap);
+    const int2 *q1 = reinterpret_cast<const int2 *>(f.cull_queue);
+    const int lane = threadIdx.x & 31, row = lane & 15;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n1; i0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;  // uniform trip count: the exact test is warp-wide
+        int cls = 0, g = 0, bit = 0;
+        uint32_t *bits = nullptr;
+        float mx = 0.f, my = 0.f, ca = 1.f, cb = 0.f, cc = 1.f, qcut = 0.f;
+        int x0 = 0, x1 = 0, y0 = 0, y1 = -1;
+        if (i < n1) {
+            const int2 e = q1[i];
+            const BigCtx c = big_ctx(f, e.x);
+            g = c.g;
+            bits = c.bits;
+            const int tx = (int)((uint32_t)e.y >> 16), ty = e.y & 0xffff;
+            bit = big_bit(c, f.tiles_x, tx, ty);
+            x0 = tx * GS_TILE;
+            y0 = ty * GS_TILE;
+            x1 = min(x0 + GS_TILE - 1, f.width - 1);
+            y1 = min(y0 + GS_TILE - 1, f.height - 1);
+            mx = c.s0.x;
+            my = c.s0.y;
+            ca = c.s0.z;
+            cb = c.s0.w;
+            cc = c.s1.x;
+            qcut = c.s1.w;
+            cls = tile_class(mx, my, ca, cb, cc, qcut, __fdividef(-cb, ca), __fdividef(-cb, cc), x0, x1, y0, y1);
         }
-        for (int o = 16; o > 0; o >>= 1) count += __shfl_xor_sync(0xffffffffu, count, o);
-        if (lane == 0 && count) atomicAdd(&s_cnt, count);
-        __syncthreads();
-        if (tid == 0) {
-            const int kept = s_cnt;
-            f.kept[g] = kept;
-            f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
-            if (slot >= 0 && kept > 0) {  // kept < 0 encodes the huge slot
+        unsigned amb = __ballot_sync(0xffffffffu, cls < 0);
+        while (amb) {  // two open tiles per round: lanes 0-15 test the first, 16-31 the second
+            const int l0 = __ffs(amb) - 1;
+            amb &= amb - 1u;
+            const int l1 = amb ? __ffs(amb) - 1 : -1;
+            if (l1 >= 0) amb &= amb - 1u;
+            const int src = lane < 16 ? l0 : (l1 >= 0 ? l1 : l0);
+            const float smx = __shfl_sync(0xffffffffu, mx, src), smy = __shfl_sync(0xffffffffu, my, src);
+            const float sca = __shfl_sync(0xffffffffu, ca, src), scb = __shfl_sync(0xffffffffu, cb, src);
+            const float scc = __shfl_sync(0xffffffffu, cc, src), sq = __shfl_sync(0xffffffffu, qcut, src);
+            const int sx0 = __shfl_sync(0xffffffffu, x0, src), sx1 = __shfl_sync(0xffffffffu, x1, src);
+            const int sy0 = __shfl_sync(0xffffffffu, y0, src), sy1 = __shfl_sync(0xffffffffu, y1, src);
+            const bool act = lane < 16 || l1 >= 0;
+            const bool hit = act && sy0 + row <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, sy0 + row);
+            const unsigned bal = __ballot_sync(0xffffffffu, hit);
+            if (lane == l0) cls = (bal & 0xffffu) ? 1 : 0;
+            if (lane == l1) cls = (bal >> 16) ? 1 : 0;
+        }
+        if (cls > 0) {
+            atomicAdd(&f.kept[g], 1);
+            if (bits) atomicOr(&bits[bit >> 5], 1u << (bit & 31));
+        }
+    }
+}
+
+// K3: per large-footprint Gaussian: touched, depth key, huge encoding, touched list
+__global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
+    const int64_t nb = f.counters[GS_CNT_BIG];
+    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = b0 + threadIdx.x;  // uniform trip count: warp_append is warp-wide
+        int g = -1;
+        bool t = false;
+        if (b < nb) {
+            g = f.big_list[b];
+            const int kept = f.kept[g], slot = f.big_slot[b];
+            t = kept > 0;
+            if (slot >= 0 && t) {  // kept < 0 encodes the huge slot
                 f.kept[g] = -(1 + slot);
                 atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
             }
-            f.touched[g] = kept > 0;
-            if (kept > 0) {
-                f.keys_a[g] = ((uint64_t)__float_as_uint(s1.z) << 32) | (uint64_t)g;
-                f.touched_list[atomicAdd(&f.counters[GS_CNT_TOUCHED], 1)] = g;
-            }
+            f.touched[g] = t;
+            if (t) f.keys_a[g] = ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint64_t)g;
         }
-        __syncthreads();
+        warp_append(t, g, &f.counters[GS_CNT_TOUCHED], f.touched_list);
     }
 }
 
@@ -452,6 +626,19 @@ __global__ void lidar_write_kernel(const float *__restrict__ sparse, int64_t npx
 
 using namespace gs;
 
+static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
+    big_setup_kernel<<<148, 256, 0, st>>>(*f, allow_huge);
+    int rc = check_launch("big_setup_kernel");
+    if (rc) return rc;
+    big_bands_kernel<<<4 * 148, CB_WARPS * 32, 0, st>>>(*f);
+    if ((rc = check_launch("big_bands_kernel"))) return rc;
+    if (rc) return rc;
+    big_tiles_kernel<<<8 * 148, 256, 0, st>>>(*f);
+    if ((rc = check_launch("big_tiles_kernel"))) return rc;
+    big_finish_kernel<<<148, 256, 0, st>>>(*f);
+    return check_launch("big_finish_kernel");
+}
+
 extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream) {
     if (!f || !params || !view) {
         set_error("gs_preprocess: null argument");
@@ -466,8 +653,7 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
     if (rc) return rc;
     int tb = 0, rb = 0;
     const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
-    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, allow_huge);
-    return check_launch("cull_big_kernel");
+    return launch_big_cull(f, allow_huge, (cudaStream_t)stream);
 }
 
 extern "C" int gs_project(const float *params, int64_t n, const gs_camera *cam, float *mu_cam, float *mean2d,
@@ -500,8 +686,7 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
     if ((rc = check_launch("touched_list_kernel"))) return rc;
     int tb = 0, rb = 0;
     const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
-    cull_big_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, allow_huge);
-    return check_launch("cull_big_kernel");
+    return launch_big_cull(f, allow_huge, (cudaStream_t)stream);
 }
 
 extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_t height, int32_t *idx, float *z,

@@ -29,4 +29,6 @@ nc2 = np.where(act & (tx1 >= tx0) & (ty1 >= ty0), (tx1 - tx0 + 1) * (ty1 - ty0 +
 print("ellipse-bbox cand", nc2.sum(), "big", (nc2 > 16).sum(), "cand of big", nc2[nc2 > 16].sum())
 print("touched", (kept > 0).sum(), "E", int(out.ctx["counters"][1]))
 c = out.ctx["counters"].cpu().numpy() if hasattr(out.ctx["counters"], "cpu") else out.ctx["counters"]
-print("counters", list(c[:20]))
+print("counters", [int(x) for x in c[:32]])
+torch.cuda.synchronize()
+print("all counters", [int(x) for x in ws.counters.cpu().numpy()])

@@ -11,7 +11,11 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"reg
                       "--launch-count", "1"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
-data = [dict(zip(h, r)) for r in rows[2:] if len(r) == len(h) and r[0].startswith("0x")]
+data, seen = [], set()
+for r in rows[2:]:
+    if len(r) == len(h) and r[0].startswith("0x") and r[0] not in seen:
+        seen.add(r[0])
+        data.append(dict(zip(h, r)))
 tot_i = sum(int(d["Instructions Executed"] or 0) for d in data)
 tot_s = sum(int(d["Warp Stall Sampling (All Samples)"] or 0) for d in data)
 ops = collections.Counter()
