@@ -134,13 +134,13 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
 // Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), same decision
 // as cull_rect, spread over the whole GPU in four launches (a few screen-covering Gaussians
 // carry thousands of candidate tiles, so per-Gaussian work units would serialise on them):
-//   K0 big_setup_kernel  huge slot / bitmap base per Gaussian;
-//   K1 big_bands_kernel  warp per Gaussian, lane per tile row ("band"): bounds of the footprint
+//   K0 big_setup_kernel  huge slot / bitmap base per Gaussian, zeroed output rows;
+//   K1 big_bands_kernel  thread per (Gaussian, tile row = "band"): bounds of the footprint
 //                        ellipse give a run of surely-kept tiles (set as bit ranges) between
 //                        runs of surely-culled ones; the tiles in between are queued;
 //   K2 big_tiles_kernel  thread per queued tile: per-tile corner / lower bounds; the tiles the
-//                        boundary actually crosses get the exact test, 16 lanes per tile and
-//                        one pixel row each (row_hits);
+//                        boundary actually crosses get the exact test, 8 lanes per tile and
+//                        two pixel rows each (row_hits);
 //   K3 big_finish_kernel touched / key / huge encoding / touched list.
 // Output bitmaps: big_bits by candidate index (for the emit) or, for screen-covering Gaussians
 // with a huge slot, by tile index (huge_mask_t row of the slot, transposed into depth order by
@@ -247,9 +247,9 @@ __device__ __forceinline__ int4 band_ranges(const BandConst &k, int ty, int4 r, 
     return out;
 }
 
-// K1: warp per large-footprint Gaussian: zeroes the output bitmap row, sets the surely-kept run
-// of every band and queues the band's ambiguous tiles (overflowing the queue: exact test in
-// place).  kept[g] starts at the surely-kept count.
+// K1: thread per (large-footprint Gaussian, band): sets the surely-kept run of the band and
+// queues its ambiguous tiles (overflowing the queue: exact test in place); kept[g] accumulates
+// the surely-kept counts.
 __device__ __forceinline__ void set_bit_range(uint32_t *bits, int b0, int b1) {
     for (int w = b0 >> 5; w <= (b1 >> 5); w++) {
         const int lo_b = max(b0, w << 5) - (w << 5), hi_b = min(b1, (w << 5) + 31) - (w << 5);
@@ -283,7 +283,7 @@ __device__ __forceinline__ int big_bit(const BigCtx &c, int tiles_x, int tx, int
     return c.slot >= 0 ? ty * tiles_x + tx : (ty - c.r.z) * (c.r.y - c.r.x + 1) + (tx - c.r.x);
 }
 
-constexpr int CB_WARPS = 8;
+constexpr int CB_BSTRIDE = 64;  // threads per Gaussian in big_bands_kernel (bands beyond: strided)
 
 // K0: thread per large-footprint Gaussian: huge slot or bitmap base (warp-aggregated
 // reservations: one atomic per warp and counter)
@@ -324,48 +324,68 @@ __global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_hu
             if (slot >= 0 || base + w > f.big_bits_words) base = -1;  // overflow: the emit re-culls
             f.big_slot[b] = slot;
             f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+            f.kept[g] = 0;
+        }
+        // zero the output bitmap rows (the band / tile kernels OR into them), one row at a time
+        // with the whole warp (coalesced)
+        const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
+        uint32_t *bits = (b < nb) ? (slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : (base >= 0 ? f.big_bits + base : nullptr))
+                                  : nullptr;
+        const int nwords = slot >= 0 ? tw : words;
+        for (int k = 0; k < 32; k++) {
+            uint32_t *row = reinterpret_cast<uint32_t *>(__shfl_sync(0xffffffffu, (unsigned long long)bits, k));
+            const int nw = __shfl_sync(0xffffffffu, nwords, k);
+            if (row)
+                for (int w = lane; w < nw; w += 32) row[w] = 0u;
         }
     }
 }
 
-__global__ void __launch_bounds__(CB_WARPS * 32) big_bands_kernel(gs_frame f) {
+__global__ void __launch_bounds__(256, 3) big_bands_kernel(gs_frame f) {
     const int lane = threadIdx.x & 31;
-    const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
     const int64_t nb = f.counters[GS_CNT_BIG];
     const int64_t cap = f.cull_queue_cap;
     int2 *q1 = reinterpret_cast<int2 *>(f.cull_queue);
-    for (int64_t b = (int64_t)blockIdx.x * CB_WARPS + (threadIdx.x >> 5); b < nb;
-         b += (int64_t)gridDim.x * CB_WARPS) {
-        const int g = f.big_list[b];
-        const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-        const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
-        const float mx = s0.x, my = s0.y, ca = s0.z, cb = s0.w, cc = s1.x, qcut = s1.w;
-        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
-        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
-        const int words = (ncand + 31) >> 5;
-        const int slot = f.big_slot[b];
-        const int64_t base = (int64_t)f.keep_bits[g];
-        uint32_t *bits = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : (base >= 0 ? f.big_bits + base : nullptr);
-        const int nwords = slot >= 0 ? tw : words;
-        if (bits)
-            for (int w = lane; w < nwords; w += 32) bits[w] = 0u;
-        __syncwarp();
+    // thread per (Gaussian, band): CB_BSTRIDE threads per Gaussian, striding its bands
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nb * CB_BSTRIDE; t0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = t0 + threadIdx.x;  // uniform trip count: the queue slots are reserved warp-wide
+        const int64_t b = t / CB_BSTRIDE;
+        const int j = (int)(t % CB_BSTRIDE);
+        int nbands = 0, g = 0, nx = 1, slot = -1;
+        int4 r = make_int4(0, -1, 0, -1);
+        float mx = 0.f, my = 0.f, ca = 1.f, cb = 0.f, cc = 1.f, qcut = 0.f;
+        uint32_t *bits = nullptr;
+        if (b < nb) {
+            const BigCtx c = big_ctx(f, b);
+            g = c.g;
+            r = c.r;
+            nx = r.y - r.x + 1;
+            nbands = r.w - r.z + 1;
+            slot = c.slot;
+            bits = c.bits;
+            mx = c.s0.x;
+            my = c.s0.y;
+            ca = c.s0.z;
+            cb = c.s0.w;
+            cc = c.s1.x;
+            qcut = c.s1.w;
+        }
         const BandConst K = band_const(mx, my, ca, cb, cc, qcut, r);
-        int kept = 0;
-        const int nbands = r.w - r.z + 1;
-        for (int b0 = 0; b0 < nbands; b0 += 32) {  // uniform trip count: the queue slots are reserved warp-wide
-            const int bi = b0 + lane;
+        for (int bi0 = 0; bi0 < ((nbands + CB_BSTRIDE - 1) / CB_BSTRIDE) * CB_BSTRIDE || bi0 == 0; bi0 += CB_BSTRIDE) {
+            const int bi = bi0 + j;
             const int ty = r.z + bi;
             int4 br = make_int4(0, 1, 0, -1);  // nothing
             if (bi < nbands) br = band_ranges(K, ty, r, f.width, f.height, f.tiles_x);
             const int base_bit = slot >= 0 ? ty * f.tiles_x : bi * nx - r.x;  // bit of tile tx: base_bit + tx
             const bool has_keep = br.y <= br.z;
+            int kept = 0;
             if (has_keep) {
-                kept += br.z - br.y + 1;
+                kept = br.z - br.y + 1;
                 if (bits) set_bit_range(bits, base_bit + br.y, base_bit + br.z);
             }
             // ambiguous: [pl, kl) and (kr, pr] (all of [pl, pr] when nothing is surely kept)
             const int namb = has_keep ? (br.y - br.x) + (br.w - br.z) : max(0, br.w - br.x + 1);
+            // warp-wide reservation (every lane gets here: the band loop is warp-uniform)
             int x = namb;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -373,12 +393,10 @@ __global__ void __launch_bounds__(CB_WARPS * 32) big_bands_kernel(gs_frame f) {
                 if (lane >= o) x += y;
             }
             const int tot = __shfl_sync(0xffffffffu, x, 31);
-            if (tot == 0) continue;
             long long qb = 0;
-            if (lane == 0) qb = atomicAdd(&f.counters[GS_CNT_CULLQ1], tot);
+            if (lane == 0 && tot) qb = atomicAdd(&f.counters[GS_CNT_CULLQ1], tot);
             int64_t q = (int64_t)__shfl_sync(0xffffffffu, qb, 0) + (x - namb);
-            if (namb == 0) continue;
-            for (int tx = br.x; tx <= br.w; tx++, q++) {
+            for (int tx = br.x; tx <= br.w && namb > 0; tx++, q++) {
                 if (has_keep && tx == br.y) tx = br.z + 1;
                 if (tx > br.w) break;
                 if (q < cap) {
@@ -392,14 +410,13 @@ __global__ void __launch_bounds__(CB_WARPS * 32) big_bands_kernel(gs_frame f) {
                     }
                 }
             }
+            if (kept) atomicAdd(&f.kept[g], kept);
         }
-        for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
-        if (lane == 0) f.kept[g] = kept;
     }
 }
 
 // K2: thread per band-ambiguous tile: per-tile bounds; the tiles the qcut boundary actually
-// crosses get the exact per-row test cooperatively, 16 lanes per tile (one pixel row each)
+// crosses get the exact per-row test cooperatively, 8 lanes per tile (two pixel rows each)
 __global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
     const int64_t cap = f.cull_queue_cap;
     const int64_t n1 = min((int64_t)f.counters[GS_CNT_CULLQ1], cap);
@@ -431,22 +448,34 @@ __global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
             cls = tile_class(mx, my, ca, cb, cc, qcut, __fdividef(-cb, ca), __fdividef(-cb, cc), x0, x1, y0, y1);
         }
         unsigned amb = __ballot_sync(0xffffffffu, cls < 0);
-        while (amb) {  // two open tiles per round: lanes 0-15 test the first, 16-31 the second
-            const int l0 = __ffs(amb) - 1;
-            amb &= amb - 1u;
-            const int l1 = amb ? __ffs(amb) - 1 : -1;
-            if (l1 >= 0) amb &= amb - 1u;
-            const int src = lane < 16 ? l0 : (l1 >= 0 ? l1 : l0);
+        const int grp = lane >> 3, sub = lane & 7;
+        while (amb) {  // four open tiles per round: 8 lanes per tile, two pixel rows per lane
+            int mine = -1;  // the open tile of this lane's group
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int l = amb ? __ffs(amb) - 1 : -1;
+                if (l >= 0) amb &= amb - 1u;
+                if (k == grp) mine = l;
+            }
+            const int src = mine >= 0 ? mine : 0;
             const float smx = __shfl_sync(0xffffffffu, mx, src), smy = __shfl_sync(0xffffffffu, my, src);
             const float sca = __shfl_sync(0xffffffffu, ca, src), scb = __shfl_sync(0xffffffffu, cb, src);
             const float scc = __shfl_sync(0xffffffffu, cc, src), sq = __shfl_sync(0xffffffffu, qcut, src);
             const int sx0 = __shfl_sync(0xffffffffu, x0, src), sx1 = __shfl_sync(0xffffffffu, x1, src);
             const int sy0 = __shfl_sync(0xffffffffu, y0, src), sy1 = __shfl_sync(0xffffffffu, y1, src);
-            const bool act = lane < 16 || l1 >= 0;
-            const bool hit = act && sy0 + row <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, sy0 + row);
+            bool hit = false;
+            if (mine >= 0) {
+                const int ya = sy0 + sub, yb = sy0 + sub + 8;
+                hit = (ya <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, ya)) ||
+                      (yb <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, yb));
+            }
             const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            if (lane == l0) cls = (bal & 0xffffu) ? 1 : 0;
-            if (lane == l1) cls = (bal >> 16) ? 1 : 0;
+            // hand each group's verdict to the tile's owner lane
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int owner = __shfl_sync(0xffffffffu, mine, 8 * k);
+                if (lane == owner && owner >= 0) cls = ((bal >> (8 * k)) & 0xffu) ? 1 : 0;
+            }
         }
         if (cls > 0) {
             atomicAdd(&f.kept[g], 1);
@@ -630,7 +659,7 @@ static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
     big_setup_kernel<<<148, 256, 0, st>>>(*f, allow_huge);
     int rc = check_launch("big_setup_kernel");
     if (rc) return rc;
-    big_bands_kernel<<<4 * 148, CB_WARPS * 32, 0, st>>>(*f);
+    big_bands_kernel<<<8 * 148, 256, 0, st>>>(*f);
     if ((rc = check_launch("big_bands_kernel"))) return rc;
     if (rc) return rc;
     big_tiles_kernel<<<8 * 148, 256, 0, st>>>(*f);

@@ -52,3 +52,12 @@ for gid in hk:
 print("huge rows wrong", bad, "of", len(hk))
 slots = -kept[hk] - 1
 print("unique slots", len(np.unique(slots)), len(slots))
+# per-Gaussian tile sets of the mismatching ones
+tiles_of = {}
+for gid in diff[:18]:
+    tg = np.flatnonzero([gid in set(ge[go[t]:go[t+1]].tolist()) for t in range(T)]) if False else None
+og_t = np.repeat(np.arange(T), np.diff(offs)); gg_t = np.repeat(np.arange(T), np.diff(go))
+sel = diff[:18]
+mo = np.isin(ent, sel); mg = np.isin(ge, sel)
+np.savez("gpurun_out/diffdump.npz", ids=sel, s2=_np(ws.splat2d)[sel], rect=rect[sel],
+         o_ent=ent[mo], o_tile=og_t[mo], g_ent=ge[mg], g_tile=gg_t[mg])
