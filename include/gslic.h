@@ -57,19 +57,19 @@ enum {
 
 /* counters[] slots (int32, device) written by the pipeline */
 enum {
-    GS_CNT_ACTIVE = 0,   /* splats with >= 1 candidate tile */
+    GS_CNT_ACTIVE = 0,   /* reserved (0) */
     GS_CNT_ENTRIES = 1,  /* E = kept (splat, tile) pairs */
     GS_CNT_TOUCHED = 2,  /* splats with >= 1 kept pair */
     GS_CNT_OVERFLOW = 3, /* nonzero when E exceeded entry_capacity (downstream kernels no-op) */
     GS_CNT_ENTRIES_EFF = 4, /* E, or 0 after an overflow (what the downstream kernels use) */
     GS_CNT_BIG = 5,      /* Gaussians culled warp-cooperatively (many candidate tiles) */
-    GS_CNT_BIG_EMIT = 6, /* ... and emitted warp-cooperatively */
+    GS_CNT_RESERVED6 = 6,
     GS_CNT_BIG_BITS = 7, /* words of big_bits in use */
     GS_CNT_SLOTS = 16,
     /* slots 8-15: look-back tickets; second half of the counters array: */
     GS_CNT_HUGE = 16,    /* screen-covering Gaussians binned per tile by bitmap (not sorted) */
     GS_CNT_HUGE_E = 17,  /* their kept pairs */
-    GS_CNT_SMALL_E = 18, /* entries emitted into the tile sort (0 after an overflow) */
+    GS_CNT_SMALL_E = 18, /* entries binned through the per-tile buckets */
     GS_CNT_HUGE_N = 19,  /* huge Gaussians with >= 1 kept tile (records in depth order) */
     GS_CNT_CULLQ1 = 20   /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
 };
@@ -114,28 +114,20 @@ typedef struct gs_frame {
     float *bias_corr;        /* n x 2 reciprocal Adam bias corrections 1/(1-b1^t), 1/(1-b2^t) (touched-list order) */
     uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
     int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
-    int32_t *counts;         /* n + 1: entry offsets per touched Gaussian in depth order */
     int32_t *big_list;       /* n: Gaussians with > GS_SMALL_CAND candidate tiles (warp-culled) */
-    int32_t *big_emit;       /* n: depth ranks of those Gaussians (warp-emitted) */
     int32_t *big_slot;       /* n: huge slot (or -1) per big_list entry */
     int32_t *cull_queue;     /* cull_queue_cap x 2: (big index, tx << 16 | ty) left open by the band bounds */
     int64_t cull_queue_cap;
-    int32_t *huge;           /* GS_HUGE_CAP x 8: screen-covering Gaussians in depth order (id,
-                                rank, rect, bitmap base) + compaction scratch */
+    int32_t *huge;           /* screen-covering Gaussians in depth order: GS_HUGE_CAP records of 8
+                                ints (id, depth bits, slot), their ids, their 64-bit keys */
     uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: bit j of word w <-> the (32w+j)-th huge
                                 Gaussian in depth order keeps the tile */
     uint32_t *huge_mask_t;   /* GS_HUGE_CAP x ceil(tiles/32): per huge slot, its kept tiles */
-    int32_t *huge_before;    /* n: per depth rank, the huge Gaussians ahead of it (merge key) */
-    int32_t *tile_scratch;   /* 2 x (tiles + 1): per-tile sorted-entry offsets, huge counts */
+    int32_t *tile_scratch;   /* 3 x (tiles + 1): bucket counts / fill cursors, huge counts, bucket offsets */
     uint32_t *big_bits;      /* cull bitmaps of the large-footprint Gaussians (base in keep_bits) */
     int64_t big_bits_words;  /* capacity of big_bits; overflowing Gaussians are re-culled at emit */
     /* sort buffers */
-    uint64_t *keys_a, *keys_b; /* max(n, entry_capacity) */
-    uint32_t *sort_hist;       /* 8 passes x 256 */
-    uint32_t *sort_status;     /* lookback status words */
-    int32_t *scan_status;      /* scan lookback words */
-    int64_t status_words;      /* length of sort_status */
-    int64_t scan_words;
+    uint64_t *keys_a, *keys_b; /* entry_capacity: per-tile buckets of (depth << 32 | id) keys, merge scratch */
     /* per entry / tile */
     int32_t *entry_splat;    /* entry_capacity */
     int32_t *tile_offsets;   /* tiles + 1 */
@@ -155,6 +147,8 @@ typedef struct gs_frame {
 } gs_frame;
 
 /* ---- setup ---------------------------------------------------------------- */
+/* The workspace (>= gs_workspace_size bytes, 256-B aligned) must be zero-filled once before its
+ * first use; afterwards frames reuse it without clearing. */
 size_t gs_workspace_size(int64_t n, int32_t width, int32_t height, int64_t entry_capacity);
 int gs_frame_layout(int64_t n, int32_t width, int32_t height, int64_t entry_capacity, void *ws,
                     size_t ws_bytes, gs_frame *out);

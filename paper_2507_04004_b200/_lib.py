@@ -41,12 +41,11 @@ class GsFrame(ctypes.Structure):
     _fields_ = [("n", i64), ("entry_capacity", i64), ("width", i32), ("height", i32), ("tiles_x", i32),
                 ("tiles_y", i32),
                 ("splat2d", P), ("cov2d", P), ("rect", P), ("valid", P), ("touched", P), ("touched_list", P),
-                ("g2d", P), ("grad_rows", P), ("bias_corr", P), ("keep_bits", P), ("kept", P), ("counts", P), ("big_list", P), ("big_emit", P),
+                ("g2d", P), ("grad_rows", P), ("bias_corr", P), ("keep_bits", P), ("kept", P), ("big_list", P),
                 ("big_slot", P), ("cull_queue", P), ("cull_queue_cap", i64),
-                ("huge", P), ("huge_mask", P), ("huge_mask_t", P), ("huge_before", P),
+                ("huge", P), ("huge_mask", P), ("huge_mask_t", P),
                 ("tile_scratch", P), ("big_bits", P), ("big_bits_words", i64),
-                ("keys_a", P), ("keys_b", P), ("sort_hist", P), ("sort_status", P), ("scan_status", P),
-                ("status_words", i64), ("scan_words", i64),
+                ("keys_a", P), ("keys_b", P),
                 ("entry_splat", P), ("tile_offsets", P), ("counters", P),
                 ("color", P), ("depth", P), ("opacity", P), ("trans", P), ("n_contrib", P),
                 ("g_color", P), ("g_depth", P), ("g_opac", P), ("loss_parts", P), ("loss", P),

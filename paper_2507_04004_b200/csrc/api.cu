@@ -1,3 +1,4 @@
+#include <algorithm>
 // api.cu -- workspace layout, camera setup and error reporting of the C ABI (include/gslic.h).
 #include <cmath>
 #include <cstdarg>
@@ -59,8 +60,6 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     const int64_t nn = n > 0 ? n : 1;
     const int32_t tx = (w + GS_TILE - 1) / GS_TILE, ty = (h + GS_TILE - 1) / GS_TILE;
     const int64_t P = (int64_t)w * h;
-    const int64_t keys = nn > cap ? nn : cap;
-    const int64_t sort_tiles = (keys + 4095) / 4096;
     f.n = n;
     f.entry_capacity = cap;
     f.width = w;
@@ -78,27 +77,19 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.bias_corr = c.take<float>(2 * nn);
     f.keep_bits = c.take<uint64_t>(nn);
     f.kept = c.take<int32_t>(nn);
-    f.counts = c.take<int32_t>(nn + 1);
     f.big_list = c.take<int32_t>(nn);
-    f.big_emit = c.take<int32_t>(nn);
     f.big_slot = c.take<int32_t>(nn);
     f.cull_queue_cap = nn > (1 << 20) ? nn : (1 << 20);
     f.cull_queue = c.take<int32_t>(2 * f.cull_queue_cap);
-    // huge records (8 ints each), their ids in depth order, per-chunk compaction counts
-    f.huge = c.take<int32_t>(9 * GS_HUGE_CAP + (nn + 1023) / 1024 + 1);
+    // huge records (8 ints each), their ids and 64-bit keys, in depth order
+    f.huge = c.take<int32_t>(11 * GS_HUGE_CAP);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
     f.huge_mask_t = c.take<uint32_t>((int64_t)GS_HUGE_CAP * (((int64_t)tx * ty + 31) / 32));
-    f.huge_before = c.take<int32_t>(nn);
-    f.tile_scratch = c.take<int32_t>(2 * ((int64_t)tx * ty + 1));
+    f.tile_scratch = c.take<int32_t>(3 * ((int64_t)tx * ty + 1));
     f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
     f.big_bits = c.take<uint32_t>(f.big_bits_words);
-    f.keys_a = c.take<uint64_t>(keys);
-    f.keys_b = c.take<uint64_t>(keys);
-    f.sort_hist = c.take<uint32_t>(8 * 256);
-    f.status_words = 8 * sort_tiles * 256;
-    f.sort_status = c.take<uint32_t>(f.status_words);
-    f.scan_words = (nn + 4095) / 4096 + 1;
-    f.scan_status = c.take<int32_t>(f.scan_words);
+    f.keys_a = c.take<uint64_t>(cap > 0 ? cap : 1);
+    f.keys_b = c.take<uint64_t>(cap > 0 ? cap : 1);
     f.entry_splat = c.take<int32_t>(cap > 0 ? cap : 1);
     f.tile_offsets = c.take<int32_t>((int64_t)tx * ty + 1);
     f.counters = c.take<int32_t>(GS_CNT_SLOTS * 2);

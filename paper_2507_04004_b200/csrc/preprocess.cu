@@ -66,7 +66,6 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             *rc = make_int4(0, -1, 0, -1);
             f.valid[i] = 0;
             f.kept[i] = 0;
-            f.keys_a[i] = (0xffffffffull << 32) | (uint64_t)i;
         } else {
             // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians near
             // the 0.01 m clip plane, and fp32 would shift their whole footprint
@@ -122,8 +121,6 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             f.valid[i] = pr.valid ? 1 : 0;
             f.kept[i] = kept;
             f.keep_bits[i] = bits;
-            f.keys_a[i] = touched ? (((uint64_t)__float_as_uint(pr.mu[2]) << 32) | (uint64_t)i)
-                                  : ((0xffffffffull << 32) | (uint64_t)i);
         }
         f.touched[i] = touched ? 1 : 0;
     }
@@ -500,7 +497,6 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                 atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
             }
             f.touched[g] = t;
-            if (t) f.keys_a[g] = ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint64_t)g;
         }
         warp_append(t, g, &f.counters[GS_CNT_TOUCHED], f.touched_list);
     }
@@ -591,7 +587,6 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     f.kept[i] = kept;
     f.keep_bits[i] = bits;
     f.touched[i] = kept > 0;
-    f.keys_a[i] = kept > 0 ? (((uint64_t)__float_as_uint(depth[i]) << 32) | (uint64_t)i) : ((0xffffffffull << 32) | (uint64_t)i);
 }
 
 // the touched and large-footprint lists of the pack path (unordered; consumers are order

@@ -27,13 +27,12 @@ NEAR_CLIP = 0.01
 
 def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     """Our kernels per map-optimisation iteration:
-    preprocess 2 (projection+cull, large-footprint cull), bin 17 + tile-sort passes
-    (2 histograms, 2 bin scans, 4 depth passes, scan, 2 emits, 2 huge compaction, ranges,
-    huge count, tile scan, merge), forward 1, loss 4 (tables, SSIM+L1, depth, finalize),
-    backward 2 (zero + tiles), chain + Adam 2."""
-    tile_bits = max(1, (tiles - 1).bit_length())
-    tpasses = 1 if tile_bits <= 8 else (2 if tile_bits <= 16 else 3)
-    return 2 + 17 + tpasses + 1 + 4 + 2 + (1 if chain_only else 2)
+    preprocess 5 (projection + small-footprint cull, large-footprint setup / bands / tiles /
+    finish), bin 6 (bucket count, huge sort, huge transpose, tile scan, bucket fill, per-tile
+    sort + merge), forward 1, loss 4 (tables, SSIM+L1, depth, finalize), backward 2 (zero +
+    tiles), chain + Adam 2."""
+    del tiles
+    return 5 + 6 + 1 + 4 + 2 + (1 if chain_only else 2)
 
 
 @dataclass
@@ -236,8 +235,9 @@ class MapOptimizer:
         return v
 
     def counters(self) -> dict:
-        c = self.ws.counters[:8].cpu()
-        return {"active": int(c[0]), "entries": int(c[1]), "touched": int(c[2]), "overflow": int(c[3])}
+        c = self.ws.counters.cpu()
+        return {"entries": int(c[1]), "touched": int(c[2]), "overflow": int(c[3]),
+                "huge": int(c[_lib.GS_CNT_SLOTS + 3]), "bucketed_entries": int(c[_lib.GS_CNT_SLOTS + 2])}
 
 
 _ENGINES: dict = {}

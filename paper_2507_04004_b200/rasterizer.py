@@ -133,7 +133,8 @@ class Workspace:
         L = _lib.lib()
         self.n, self.width, self.height, self.capacity = int(n), int(width), int(height), int(capacity)
         size = int(L.gs_workspace_size(self.n, self.width, self.height, self.capacity))
-        self.buf = torch.empty(size + 256, dtype=torch.uint8, device=self.device)
+        # zero-filled once: the sort look-back words are epoch-tagged and never cleared (gslic.h)
+        self.buf = torch.zeros(size + 256, dtype=torch.uint8, device=self.device)
         base = self.buf.data_ptr()
         self.base = (base + 255) & ~255
         self.frame = _lib.GsFrame()
