@@ -5,7 +5,8 @@
 // them exactly and lexsorts by (tile, depth, splat).  The exact cull itself runs in
 // preprocess.cu (kept counts, cull bitmaps, huge-slot masks); here, with the 64-bit key
 // (depth_f32_bits << 32 | id) -- a total order equal to lexsort((id, depth)) inside a tile:
-//   1. bucket_count: per-tile counts of the kept pairs of the non-screen-covering Gaussians;
+//   1. per-tile counts of the kept pairs of the non-screen-covering Gaussians, taken where the
+//      cull decides them (preprocess_kernel, big_finish_kernel; bucket_count for cull=False);
 //   2. huge_sort: the screen-covering ("huge") Gaussians, already binned per tile by bitmap,
 //      are sorted by key in one CTA (records in depth order);
 //   3. huge_transpose: their per-tile masks in that order, per-tile counts;
@@ -74,21 +75,13 @@ __global__ void nocull_kernel(gs_frame f) {
     warp_append(v, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
 }
 
-// 1) per-tile counts of the bucketed pairs (tile_scratch[0..T))
-__global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f, int cull) {
+// 1) per-tile bucket counts for cull=False (every tile holds every valid Gaussian); with the
+// cull they are counted where the cull decides (preprocess_kernel, big_finish_kernel)
+__global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f) {
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     const int T = f.tiles_x * f.tiles_y;
-    int32_t *cnt = f.tile_scratch;
-    if (!cull) {  // every tile holds every valid Gaussian
-        for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
-            cnt[t] = (int32_t)nt;
-        return;
-    }
-    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += (int64_t)gridDim.x * blockDim.x) {
-        const int g = f.touched_list[k];
-        if (f.kept[g] <= 0) continue;  // huge (kept < 0 encodes the slot): binned by bitmap
-        for_kept_tiles(f, g, [&](int t) { atomicAdd(&cnt[t], 1); });
-    }
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
+        f.tile_scratch[t] = (int32_t)nt;
 }
 
 // 2) the huge Gaussians with >= 1 kept tile, sorted by key in one CTA: records in depth order
@@ -96,19 +89,10 @@ constexpr int HS_THREADS = 1024;
 
 __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
     __shared__ uint64_t s_key[GS_HUGE_CAP];
-    __shared__ int s_n;
-    if (threadIdx.x == 0) s_n = 0;
-    __syncthreads();
-    const int64_t nb = f.counters[GS_CNT_BIG];
-    for (int64_t b = threadIdx.x; b < nb; b += HS_THREADS) {
-        const int g = f.big_list[b];
-        if (f.kept[g] < 0) {
-            const int i = atomicAdd(&s_n, 1);
-            if (i < GS_HUGE_CAP) s_key[i] = depth_key(f, g);
-        }
-    }
-    __syncthreads();
-    const int nh = min(s_n, GS_HUGE_CAP);
+    // the keys were staged (unordered) by big_finish_kernel
+    uint64_t *keys = reinterpret_cast<uint64_t *>(f.huge + HKEYS);
+    const int nh = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
+    for (int i = threadIdx.x; i < nh; i += HS_THREADS) s_key[i] = keys[i];
     int np = 1;
     while (np < nh) np <<= 1;
     for (int i = nh + threadIdx.x; i < np; i += HS_THREADS) s_key[i] = ~0ull;
@@ -127,7 +111,6 @@ __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
             }
             __syncthreads();
         }
-    uint64_t *keys = reinterpret_cast<uint64_t *>(f.huge + HKEYS);
     for (int i = threadIdx.x; i < nh; i += HS_THREADS) {
         const uint64_t key = s_key[i];
         const int g = (int)(uint32_t)key;
@@ -135,7 +118,6 @@ __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
         f.huge[HIDS + i] = g;
         keys[i] = key;
     }
-    if (threadIdx.x == 0) f.counters[GS_CNT_HUGE_N] = nh;
 }
 
 // 3) per-tile masks in depth order: bit j of huge_mask[t][w] <-> huge record 32w + j keeps tile
@@ -241,7 +223,21 @@ __global__ void __launch_bounds__(256) bucket_fill_kernel(gs_frame f, int cull) 
         const int g = f.touched_list[k];
         if (f.kept[g] <= 0) continue;
         const uint64_t key = depth_key(f, g);
-        for_kept_tiles(f, g, [&](int t) { bucket[atomicAdd(&cur[t], 1)] = key; });
+        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+        if (ncand <= GS_SMALL_CAND) {
+            // all slot reservations in flight before the first store
+            const uint64_t bits = f.keep_bits[g];
+            int pos[GS_SMALL_CAND];
+#pragma unroll
+            for (int c = 0; c < GS_SMALL_CAND; c++)
+                if ((bits >> c) & 1ull) pos[c] = atomicAdd(&cur[(r.z + c / nx) * f.tiles_x + r.x + c % nx], 1);
+#pragma unroll
+            for (int c = 0; c < GS_SMALL_CAND; c++)
+                if ((bits >> c) & 1ull) bucket[pos[c]] = key;
+        } else {
+            for_kept_tiles(f, g, [&](int t) { bucket[atomicAdd(&cur[t], 1)] = key; });
+        }
     }
 }
 
@@ -366,6 +362,7 @@ __global__ void __launch_bounds__(SM_THREADS) tile_sort_merge_kernel(gs_frame f)
         for (int j = tid; j < nb; j += SM_THREADS) out[j] = (int32_t)(uint32_t)B[j];
         return;
     }
+    __syncthreads();  // sm.a complete
     const uint64_t *hkeys = reinterpret_cast<const uint64_t *>(f.huge + HKEYS);
     const int32_t *hid = f.huge + HIDS;
     auto huge_before = [&](uint64_t key) -> int {  // records with a smaller key
@@ -378,6 +375,12 @@ __global__ void __launch_bounds__(SM_THREADS) tile_sort_merge_kernel(gs_frame f)
         return lo;
     };
     const int total = na + nb;
+    // the common case: every huge Gaussian of the tile is in front of every bucketed one
+    // (screen-covering Gaussians hug the near plane): the merged list is a concatenation
+    if (nb == 0 || hkeys[sm.a[na - 1]] < B[0]) {
+        for (int d = tid; d < total; d += SM_THREADS) out[d] = d < na ? hid[sm.a[d]] : (int32_t)(uint32_t)B[d - na];
+        return;
+    }
     if (nb <= SM_CAP) {
         // B_j lands at j + #{A preceding it}; its slot is marked in a bitmap.  Every other output
         // d is A element d - #{B slots before d}.  Both write passes are coalesced.
@@ -461,8 +464,7 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     // counts
     cudaMemsetAsync(f->counters + GS_CNT_ENTRIES, 0, sizeof(int32_t), st);
     cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * 2, st);  // OVERFLOW, ENTRIES_EFF
-    cudaMemsetAsync(f->counters + GS_CNT_SMALL_E, 0, sizeof(int32_t) * 2, st);   // SMALL_E, HUGE_N
-    cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)T + 1), st);
+    cudaMemsetAsync(f->counters + GS_CNT_SMALL_E, 0, sizeof(int32_t), st);
     if (n == 0) {
         cudaMemsetAsync(f->tile_offsets, 0, sizeof(int32_t) * (T + 1), st);
         return check_launch("gs_bin");
@@ -470,12 +472,14 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     if (!cull) {  // every valid Gaussian in every tile: no huge binning
         cudaMemsetAsync(f->counters + GS_CNT_TOUCHED, 0, sizeof(int32_t), st);
         cudaMemsetAsync(f->counters + GS_CNT_HUGE, 0, sizeof(int32_t) * 2, st);
+        cudaMemsetAsync(f->counters + GS_CNT_HUGE_N, 0, sizeof(int32_t), st);
+        cudaMemsetAsync(f->tile_scratch + T + 1, 0, sizeof(int32_t) * ((size_t)T + 1), st);  // no huge
         nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
         if ((rc = check_launch("nocull_kernel"))) return rc;
+        bucket_count_kernel<<<4 * 148, 256, 0, st>>>(*f);
+        if ((rc = check_launch("bucket_count_kernel"))) return rc;
     }
-    bucket_count_kernel<<<4 * 148, 256, 0, st>>>(*f, cull);
-    if ((rc = check_launch("bucket_count_kernel"))) return rc;
-    if (cull) {
+    if (cull) {  // the bucket counts come from the cull (preprocess, big_finish)
         huge_sort_kernel<<<1, HS_THREADS, 0, st>>>(*f);
         if ((rc = check_launch("huge_sort_kernel"))) return rc;
         huge_transpose_kernel<<<dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st>>>(*f);

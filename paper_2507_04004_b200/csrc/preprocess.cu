@@ -121,6 +121,7 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             f.valid[i] = pr.valid ? 1 : 0;
             f.kept[i] = kept;
             f.keep_bits[i] = bits;
+            if (kept > 0) count_kept_tiles(f.tile_scratch, rect, bits, f.tiles_x);  // binning buckets
         }
         f.touched[i] = touched ? 1 : 0;
     }
@@ -495,6 +496,29 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
             if (slot >= 0 && t) {  // kept < 0 encodes the huge slot
                 f.kept[g] = -(1 + slot);
                 atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
+                // stage the depth key for the binning's huge sort (binning.cu, HKEYS)
+                const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
+                if (h < GS_HUGE_CAP)
+                    reinterpret_cast<uint64_t *>(f.huge + 9 * GS_HUGE_CAP)[h] =
+                        ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
+            } else if (t) {  // per-tile bucket counts of the binning (bitmap or exact re-test)
+                const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+                const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+                const int64_t base = (int64_t)f.keep_bits[g];
+                const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+                const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+                for (int c = 0; c < ncand; c++) {
+                    const int tx = r.x + c % nx, ty = r.z + c / nx;
+                    bool keep;
+                    if (base >= 0) {
+                        keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
+                    } else {
+                        const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                        const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                        keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                    }
+                    if (keep) atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
+                }
             }
             f.touched[g] = t;
         }
@@ -576,6 +600,7 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     const bool big = active && (rect.y - rect.x + 1) * (rect.w - rect.z + 1) > GS_SMALL_CAND;
     const int kept = (active && !big) ? cull_rect(mx, my, ca, cb, cc, qcut, rect, f.width, f.height, bits)
                                       : (big ? -1 : 0);
+    if (kept > 0) count_kept_tiles(f.tile_scratch, rect, bits, f.tiles_x);  // binning buckets
     float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
     s2[0] = make_float4(mx, my, ca, cb);
     s2[1] = make_float4(cc, o, depth[i], qcut);
@@ -669,6 +694,8 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
         return GS_ERR_ARG;
     }
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
+    // per-tile bucket counts and huge counts of the binning (gs_bin reads them)
+    cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     int64_t warps = (f->n + 31) / 32;
     int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
@@ -701,6 +728,7 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
                               const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                               void *stream) {
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
+    cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);
