@@ -71,7 +71,9 @@ enum {
     GS_CNT_HUGE_E = 17,  /* their kept pairs */
     GS_CNT_SMALL_E = 18, /* entries binned through the per-tile buckets */
     GS_CNT_HUGE_N = 19,  /* huge Gaussians with >= 1 kept tile (records in depth order) */
-    GS_CNT_CULLQ1 = 20   /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
+    GS_CNT_CULLQ1 = 20,  /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
+    GS_CNT_LAZY = 21,    /* 1: gs_bin(GS_BIN_LAZY) left the tile lists unmaterialised */
+    GS_CNT_ANYFLAG = 22  /* lazy lists: some tile needs its bucket (blend continuation) */
 };
 
 #define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */
@@ -123,7 +125,9 @@ typedef struct gs_frame {
     uint32_t *huge_mask;     /* tiles x GS_HUGE_CAP/32: bit j of word w <-> the (32w+j)-th huge
                                 Gaussian in depth order keeps the tile */
     uint32_t *huge_mask_t;   /* GS_HUGE_CAP x ceil(tiles/32): per huge slot, its kept tiles */
-    int32_t *tile_scratch;   /* 3 x (tiles + 1): bucket counts / fill cursors, huge counts, bucket offsets */
+    int32_t *tile_scratch;   /* 5 x (tiles + 1): bucket counts / fill cursors, huge counts, bucket
+                                offsets, list mode per tile, last huge record per tile */
+    uint64_t *tile_minkey;   /* tiles: smallest bucketed (depth << 32 | id) key per tile */
     uint32_t *big_bits;      /* cull bitmaps of the large-footprint Gaussians (base in keep_bits) */
     int64_t big_bits_words;  /* capacity of big_bits; overflowing Gaussians are re-culled at emit */
     /* sort buffers */
@@ -166,6 +170,12 @@ int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, v
  * ordered entries, tile ranges, touched mask + list; zeroes touched g2d rows.
  * cull=0 reproduces the reference's cull=False (every valid Gaussian in every tile). */
 int gs_bin(const gs_frame *f, int32_t cull, void *stream);
+/* cull = GS_BIN_LAZY (the iteration engine): cull as cull=1, but the tile lists are not
+ * materialised.  A tile's list is its screen-covering Gaussians (depth-ordered masks) followed by
+ * its depth-sorted bucket; gs_render_fwd sorts and merges buckets only for the tiles whose blend
+ * gets that far (or whose bucket interleaves with the screen-covering ones).  entry_splat is then
+ * valid only for those tiles; tile_offsets, touched and the rendered images are always complete. */
+#define GS_BIN_LAZY 2
 
 /* R/rasterizer.py:226-293 */
 int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream);

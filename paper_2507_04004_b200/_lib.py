@@ -20,6 +20,7 @@ GS_TILE = 16
 GS_G2D = 12
 CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3, 4
 GS_CNT_SLOTS = 16
+GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists materialised on demand)
 
 P = ctypes.c_void_p
 i32 = ctypes.c_int32
@@ -44,7 +45,7 @@ class GsFrame(ctypes.Structure):
                 ("g2d", P), ("grad_rows", P), ("bias_corr", P), ("keep_bits", P), ("kept", P), ("big_list", P),
                 ("big_slot", P), ("cull_queue", P), ("cull_queue_cap", i64),
                 ("huge", P), ("huge_mask", P), ("huge_mask_t", P),
-                ("tile_scratch", P), ("big_bits", P), ("big_bits_words", i64),
+                ("tile_scratch", P), ("tile_minkey", P), ("big_bits", P), ("big_bits_words", i64),
                 ("keys_a", P), ("keys_b", P),
                 ("entry_splat", P), ("tile_offsets", P), ("counters", P),
                 ("color", P), ("depth", P), ("opacity", P), ("trans", P), ("n_contrib", P),

@@ -32,6 +32,7 @@ int64_t loss_parts_needed(int32_t width, int32_t height);  // loss.cu
 void init_loss_attrs();                                     // loss.cu
 void init_chain_attrs();                                    // adam.cu
 void init_binning_attrs();                                  // binning.cu
+void init_render_attrs();                                   // render.cu
 
 // kernel attributes (dynamic shared-memory opt-in) are set once per process, outside any
 // stream capture, the first time a workspace is laid out
@@ -41,6 +42,7 @@ static void init_attrs_once() {
         init_loss_attrs();
         init_chain_attrs();
         init_binning_attrs();
+        init_render_attrs();
     });
 }
 
@@ -85,7 +87,8 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.huge = c.take<int32_t>(11 * GS_HUGE_CAP);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
     f.huge_mask_t = c.take<uint32_t>((int64_t)GS_HUGE_CAP * (((int64_t)tx * ty + 31) / 32));
-    f.tile_scratch = c.take<int32_t>(3 * ((int64_t)tx * ty + 1));
+    f.tile_scratch = c.take<int32_t>(5 * ((int64_t)tx * ty + 1));
+    f.tile_minkey = c.take<uint64_t>((int64_t)tx * ty + 1);
     f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
     f.big_bits = c.take<uint32_t>(f.big_bits_words);
     f.keys_a = c.take<uint64_t>(cap > 0 ? cap : 1);

@@ -18,19 +18,9 @@
 // Every kernel reads its element counts from device memory, so the sequence is graph-capturable.
 #include <cstdio>
 
-#include "common.cuh"
+#include "tilelist.cuh"
 
 namespace gs {
-
-// Huge records (depth order), 8 ints each: id, depth bits, slot; then their ids alone, then
-// their 64-bit keys
-constexpr int HREC = 8;
-constexpr int HIDS = HREC * GS_HUGE_CAP;
-constexpr int HKEYS = HIDS + GS_HUGE_CAP;  // int offset of the uint64 key array (8-B aligned)
-
-__device__ __forceinline__ uint64_t depth_key(const gs_frame &f, int g) {
-    return ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
-}
 
 // Calls fn(tile) for every kept tile of a non-huge touched Gaussian, in candidate order
 // (ty-major, then tx, R/rasterizer.py:113-122).
@@ -142,20 +132,25 @@ __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
     const int t = 32 * u + lane;
     if (t < T) {
         f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + w] = mine;
-        if (mine) atomicAdd(&f.tile_scratch[T + 1 + t], __popc(mine));
+        if (mine) {
+            atomicAdd(&ts_huge(f)[t], __popc(mine));
+            atomicMax(&ts_last(f)[t], 32 * w + 31 - __clz(mine));  // last record of the tile
+        }
     }
 }
 
 // 4) one CTA: tile_offsets = exclusive scan of (bucket + huge) counts; bucket offsets (both
 // as the fill cursors, tile_scratch[0..T], and kept, tile_scratch[2T+2 ..]); E
-__global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f) {
+__global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f, int lazy) {
     __shared__ int32_t s_warp[2][32];
     __shared__ int32_t s_carry[2];
+    __shared__ int s_any;
     const int T = f.tiles_x * f.tiles_y;
     int32_t *cur = f.tile_scratch, *hcount = f.tile_scratch + T + 1, *boff = f.tile_scratch + 2 * (T + 1);
     const bool use_huge = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) > 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
     for (int t0 = 0; t0 < T; t0 += blockDim.x) {
         const int t = t0 + threadIdx.x;
@@ -185,6 +180,12 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f) {
             f.tile_offsets[t] = before + x - v;
             cur[t] = bb + xb - vb;
             boff[t] = bb + xb - vb;
+            // lazy lists: a tile whose bucket interleaves with its screen-covering Gaussians
+            // needs the merged list; the others are A then B
+            int flag = TL_CONCAT;
+            if (use_huge && vb > 0 && v > vb && huge_keys(f)[ts_last(f)[t]] > f.tile_minkey[t]) flag = TL_MERGED;
+            ts_flag(f)[t] = flag;
+            if (flag) s_any = 1;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -202,6 +203,8 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f) {
         const bool over = E > f.entry_capacity;
         if (over) f.counters[GS_CNT_OVERFLOW] = 1;
         f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
+        f.counters[GS_CNT_LAZY] = lazy;
+        f.counters[GS_CNT_ANYFLAG] = lazy && s_any;
     }
 }
 
@@ -241,209 +244,37 @@ __global__ void __launch_bounds__(256) bucket_fill_kernel(gs_frame f, int cull) 
     }
 }
 
-// 6) CTA per tile: sort the bucket, merge it with the tile's huge list, write entry_splat.
-// A = the tile's huge records (record indices, ascending = depth order), B = the sorted bucket;
-// B_j is preceded by exactly the records with key < key_j, hb_j of them in total, so record i
-// precedes B_j iff i < hb_j.
+// 6) CTA per tile (materialised lists): sort the bucket, merge it with the tile's huge list,
+// write entry_splat
 constexpr int SM_THREADS = 256;
-constexpr int SM_CAP = 4096;  // bucket keys sorted in shared memory at once
 
 struct SortMergeSmem {
     uint64_t key[SM_CAP];
     int32_t a[GS_HUGE_CAP];
+    uint32_t words[GS_HUGE_CAP / 32];
+    int32_t wpre_a[GS_HUGE_CAP / 32];
     uint32_t isb[(GS_HUGE_CAP + SM_CAP) / 32];
     int32_t wpre[(GS_HUGE_CAP + SM_CAP) / 32];
-    int warp[SM_THREADS / 32];
+    int32_t tmp[SM_THREADS / 32];
 };
-
-__device__ __forceinline__ void bitonic_smem(uint64_t *k, int np) {
-    for (int s = 2; s <= np; s <<= 1)
-        for (int j = s >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < np; i += SM_THREADS) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const uint64_t a = k[i], c = k[l];
-                    if ((a > c) == ((i & s) == 0)) {
-                        k[i] = c;
-                        k[l] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-}
-
-// sorted B in shared memory (nb <= SM_CAP), or in global memory (returned) otherwise
-__device__ const uint64_t *sort_bucket(SortMergeSmem &sm, uint64_t *src, uint64_t *tmp, int nb) {
-    if (nb <= SM_CAP) {
-        int np = 1;
-        while (np < nb) np <<= 1;
-        for (int i = threadIdx.x; i < np; i += SM_THREADS) sm.key[i] = i < nb ? src[i] : ~0ull;
-        __syncthreads();
-        bitonic_smem(sm.key, np);
-        return sm.key;
-    }
-    // oversized bucket: sorted runs of SM_CAP in shared memory, then pairwise merges in global
-    // memory (each element's output slot = its rank in its run + its rank in the other run)
-    for (int c0 = 0; c0 < nb; c0 += SM_CAP) {
-        const int m = min(SM_CAP, nb - c0);
-        int np = 1;
-        while (np < m) np <<= 1;
-        for (int i = threadIdx.x; i < np; i += SM_THREADS) sm.key[i] = i < m ? src[c0 + i] : ~0ull;
-        __syncthreads();
-        bitonic_smem(sm.key, np);
-        for (int i = threadIdx.x; i < m; i += SM_THREADS) src[c0 + i] = sm.key[i];
-        __syncthreads();
-    }
-    for (int w = SM_CAP; w < nb; w <<= 1) {
-        for (int i = threadIdx.x; i < nb; i += SM_THREADS) {
-            const int lo = (i / (2 * w)) * (2 * w), mid = min(lo + w, nb), hi = min(lo + 2 * w, nb);
-            const uint64_t v = src[i];
-            const bool in_a = i < mid;
-            int a = in_a ? mid : lo, b = in_a ? hi : mid;  // rank in the other run
-            while (a < b) {
-                const int m = (a + b) >> 1;
-                if (src[m] < v) a = m + 1;
-                else b = m;
-            }
-            tmp[lo + (i - (in_a ? lo : mid)) + (a - (in_a ? mid : lo))] = v;
-        }
-        __syncthreads();
-        uint64_t *t = src;
-        src = tmp;
-        tmp = t;
-    }
-    return src;
-}
 
 __global__ void __launch_bounds__(SM_THREADS) tile_sort_merge_kernel(gs_frame f) {
     extern __shared__ uint64_t sm_raw[];
     SortMergeSmem &sm = *reinterpret_cast<SortMergeSmem *>(sm_raw);
     const int T = f.tiles_x * f.tiles_y;
     const int t = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (f.counters[GS_CNT_OVERFLOW]) {
-        if (tid == 0) f.tile_offsets[t] = 0;
-        if (t == 0 && tid == 1) f.tile_offsets[T] = 0;
+        if (threadIdx.x == 0) f.tile_offsets[t] = 0;
+        if (t == 0 && threadIdx.x == 1) f.tile_offsets[T] = 0;
         return;
     }
-    const int32_t *boff = f.tile_scratch + 2 * (T + 1);
-    const int sb = boff[t], nb = boff[t + 1] - sb;
-    int32_t *out = f.entry_splat + f.tile_offsets[t];
-    const uint64_t *B = sort_bucket(sm, f.keys_b + sb, f.keys_a + sb, nb);
-    // A: expand the depth-ordered mask words (prefix of the per-word popcounts, then a warp per
-    // word, lane j <-> bit j)
-    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
-    const int nw = (nrec + 31) >> 5;
-    const uint32_t *mask = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
-    const int c = tid < nw ? __popc(mask[tid]) : 0;
-    int x = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) sm.warp[warp] = x;
-    __syncthreads();
-    int na = 0, pos = x - c;
-#pragma unroll
-    for (int w = 0; w < SM_THREADS / 32; w++) {
-        const int sw = sm.warp[w];
-        pos += w < warp ? sw : 0;
-        na += sw;
-    }
-    if (tid < nw) sm.wpre[tid] = pos;
-    __syncthreads();
-    for (int w = warp; w < nw; w += SM_THREADS / 32) {
-        const uint32_t word = mask[w];
-        if ((word >> lane) & 1u) sm.a[sm.wpre[w] + __popc(word & ((1u << lane) - 1u))] = 32 * w + lane;
-    }
-    if (na == 0) {  // no huge Gaussian in this tile: the sorted bucket as it is
-        for (int j = tid; j < nb; j += SM_THREADS) out[j] = (int32_t)(uint32_t)B[j];
-        return;
-    }
-    __syncthreads();  // sm.a complete
-    const uint64_t *hkeys = reinterpret_cast<const uint64_t *>(f.huge + HKEYS);
-    const int32_t *hid = f.huge + HIDS;
-    auto huge_before = [&](uint64_t key) -> int {  // records with a smaller key
-        int lo = 0, hi = nrec;
-        while (lo < hi) {
-            const int m = (lo + hi) >> 1;
-            if (hkeys[m] < key) lo = m + 1;
-            else hi = m;
-        }
-        return lo;
-    };
-    const int total = na + nb;
-    // the common case: every huge Gaussian of the tile is in front of every bucketed one
-    // (screen-covering Gaussians hug the near plane): the merged list is a concatenation
-    if (nb == 0 || hkeys[sm.a[na - 1]] < B[0]) {
-        for (int d = tid; d < total; d += SM_THREADS) out[d] = d < na ? hid[sm.a[d]] : (int32_t)(uint32_t)B[d - na];
-        return;
-    }
-    if (nb <= SM_CAP) {
-        // B_j lands at j + #{A preceding it}; its slot is marked in a bitmap.  Every other output
-        // d is A element d - #{B slots before d}.  Both write passes are coalesced.
-        const int tw = (total + 31) >> 5;
-        for (int w = tid; w < tw; w += SM_THREADS) sm.isb[w] = 0u;
-        __syncthreads();
-        for (int j = tid; j < nb; j += SM_THREADS) {
-            const int h = huge_before(B[j]);
-            int lo = 0, hi = na;
-            while (lo < hi) {
-                const int m = (lo + hi) >> 1;
-                if (sm.a[m] < h) lo = m + 1;
-                else hi = m;
-            }
-            const int d = j + lo;
-            out[d] = (int32_t)(uint32_t)B[j];
-            atomicOr(&sm.isb[d >> 5], 1u << (d & 31));
-        }
-        __syncthreads();
-        const int cnt = tid < tw ? __popc(sm.isb[tid]) : 0;
-        int xx = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, xx, o);
-            if (lane >= o) xx += y;
-        }
-        if (lane == 31) sm.warp[warp] = xx;
-        __syncthreads();
-        int pre = xx - cnt;
-        for (int w = 0; w < warp; w++) pre += sm.warp[w];
-        if (tid < tw) sm.wpre[tid] = pre;
-        __syncthreads();
-        for (int d = tid; d < total; d += SM_THREADS) {
-            const uint32_t word = sm.isb[d >> 5];
-            if ((word >> (d & 31)) & 1u) continue;
-            const int a = d - (sm.wpre[d >> 5] + __popc(word & ((1u << (d & 31)) - 1u)));
-            out[d] = hid[sm.a[a]];
-        }
-        return;
-    }
-    // oversized bucket: merge path, each thread merges a run of ceil(total / 256) outputs
-    __syncthreads();
-    const int L = (total + SM_THREADS - 1) / SM_THREADS;
-    const int d0 = min(tid * L, total), d1 = min(d0 + L, total);
-    if (d0 >= d1) return;
-    int lo = max(0, d0 - nb), hi = min(d0, na);
-    while (lo < hi) {  // a = number of A among the first d0 outputs
-        const int m = (lo + hi) >> 1;
-        if (sm.a[m] < huge_before(B[d0 - 1 - m])) lo = m + 1;
-        else hi = m;
-    }
-    int aa = lo, bb = d0 - lo;
-    int hb = bb < nb ? huge_before(B[bb]) : 0;
-    for (int d = d0; d < d1; d++) {
-        if (bb >= nb || (aa < na && sm.a[aa] < hb)) {
-            out[d] = hid[sm.a[aa]];
-            aa++;
-        } else {
-            out[d] = (int32_t)(uint32_t)B[bb];
-            bb++;
-            if (bb < nb) hb = huge_before(B[bb]);
-        }
-    }
+    const int sb = ts_boff(f)[t], nb = ts_boff(f)[t + 1] - sb;
+    const uint64_t *B = sort_bucket<SM_THREADS>(sm.key, f.keys_b + sb, f.keys_a + sb, nb, false);
+    const int na = tile_huge_setup(f, t, sm.words, sm.wpre_a, sm.tmp);
+    const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+    tile_huge_expand(sm.words, sm.wpre_a, nw, sm.a);
+    merge_tile_list<SM_THREADS>(f, f.entry_splat + f.tile_offsets[t], sm.a, na, B, nb, sm.isb, sm.wpre, sm.tmp,
+                                GS_HUGE_CAP + SM_CAP);
 }
 
 void init_binning_attrs() {
@@ -459,7 +290,14 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t n = f->n;
     const int32_t T = f->tiles_x * f->tiles_y;
+    const bool lazy = cull == GS_BIN_LAZY;
     int rc;
+    if (cull < 0 || cull > GS_BIN_LAZY) {
+        set_error("gs_bin: cull must be 0, 1 or GS_BIN_LAZY");
+        return GS_ERR_ARG;
+    }
+    // last huge record per tile: -1
+    cudaMemsetAsync(f->tile_scratch + 4 * ((size_t)T + 1), 0xff, sizeof(int32_t) * ((size_t)T + 1), st);
     // reset the binning counters (touched, big and huge belong to preprocess) and the per-tile
     // counts
     cudaMemsetAsync(f->counters + GS_CNT_ENTRIES, 0, sizeof(int32_t), st);
@@ -485,8 +323,9 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         huge_transpose_kernel<<<dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st>>>(*f);
         if ((rc = check_launch("huge_transpose_kernel"))) return rc;
     }
-    tile_scan_kernel<<<1, 1024, 0, st>>>(*f);
+    tile_scan_kernel<<<1, 1024, 0, st>>>(*f, lazy ? 1 : 0);
     if ((rc = check_launch("tile_scan_kernel"))) return rc;
+    if (lazy) return GS_OK;  // buckets filled, sorted and merged on demand by gs_render_fwd
     bucket_fill_kernel<<<4 * 148, 256, 0, st>>>(*f, cull);
     if ((rc = check_launch("bucket_fill_kernel"))) return rc;
     tile_sort_merge_kernel<<<T, SM_THREADS, sizeof(SortMergeSmem), st>>>(*f);

@@ -326,14 +326,17 @@ __device__ __forceinline__ int cull_rect(float mx, float my, float ca, float cb,
     return count;
 }
 
-// Per-tile bucket counts (tile_scratch[0..T)) of one Gaussian's kept candidates (cull bits of
-// cull_rect, ncand <= GS_SMALL_CAND); fire-and-forget reductions.
-__device__ __forceinline__ void count_kept_tiles(int32_t *cnt, int4 r, uint64_t bits, int tiles_x) {
+// Per-tile bucket counts (tile_scratch[0..T)) and smallest keys of one Gaussian's kept
+// candidates (cull bits of cull_rect, ncand <= GS_SMALL_CAND); fire-and-forget reductions.
+__device__ __forceinline__ void count_kept_tiles(int32_t *cnt, unsigned long long *minkey, unsigned long long key, int4 r,
+                                                 uint64_t bits, int tiles_x) {
     const int nx = r.y - r.x + 1;
     while (bits) {
         const int c = __ffsll((long long)bits) - 1;
         bits &= bits - 1ull;
-        atomicAdd(&cnt[(r.z + c / nx) * tiles_x + r.x + c % nx], 1);
+        const int t = (r.z + c / nx) * tiles_x + r.x + c % nx;
+        atomicAdd(&cnt[t], 1);
+        atomicMin(&minkey[t], key);  // smallest bucketed key of the tile (lazy lists)
     }
 }
 

@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             f.valid[i] = pr.valid ? 1 : 0;
             f.kept[i] = kept;
             f.keep_bits[i] = bits;
-            if (kept > 0) count_kept_tiles(f.tile_scratch, rect, bits, f.tiles_x);  // binning buckets
+            if (kept > 0)  // binning buckets
+                count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
+                                 ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
+                                 f.tiles_x);
         }
         f.touched[i] = touched ? 1 : 0;
     }
@@ -517,7 +520,11 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                         const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
                         keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
                     }
-                    if (keep) atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
+                    if (keep) {
+                        atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
+                        atomicMin(reinterpret_cast<unsigned long long *>(f.tile_minkey) + ty * f.tiles_x + tx,
+                                  ((unsigned long long)__float_as_uint(s1.z) << 32) | (uint32_t)g);
+                    }
                 }
             }
             f.touched[g] = t;
@@ -600,7 +607,9 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     const bool big = active && (rect.y - rect.x + 1) * (rect.w - rect.z + 1) > GS_SMALL_CAND;
     const int kept = (active && !big) ? cull_rect(mx, my, ca, cb, cc, qcut, rect, f.width, f.height, bits)
                                       : (big ? -1 : 0);
-    if (kept > 0) count_kept_tiles(f.tile_scratch, rect, bits, f.tiles_x);  // binning buckets
+    if (kept > 0)  // binning buckets
+        count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
+                         ((unsigned long long)__float_as_uint(depth[i]) << 32) | (uint32_t)i, rect, bits, f.tiles_x);
     float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
     s2[0] = make_float4(mx, my, ca, cb);
     s2[1] = make_float4(cc, o, depth[i], qcut);
@@ -696,6 +705,7 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
     // per-tile bucket counts and huge counts of the binning (gs_bin reads them)
     cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
+    cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     int64_t warps = (f->n + 31) / 32;
     int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
@@ -729,6 +739,7 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
                               void *stream) {
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
     cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
+    cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);

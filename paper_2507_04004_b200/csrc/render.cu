@@ -12,7 +12,7 @@
 // contributions are summed in registers, reduced across the warp with a transposed butterfly
 // (10 fields in 12 shuffles), merged across the 4 warps with shared-memory atomics, and added
 // to the per-Gaussian FP64 gradient rows once per tile.
-#include "common.cuh"
+#include "tilelist.cuh"
 
 namespace gs {
 
@@ -40,65 +40,208 @@ __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &a
     }
 }
 
-__global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_stop) {
-    __shared__ float4 s_a[RT];  // mx my ca cb
-    __shared__ float4 s_b[RT];  // cc opacity depth -
-    __shared__ float4 s_c[RT];  // r g b -
-    const int tile = blockIdx.x;
+// One pixel's blend state (R/rasterizer.py:256-291).  Opacity is accumulated as sum(w) (== 1 - T
+// exactly in real arithmetic): 1 - T in fp32 cancels for nearly transparent pixels, and the
+// depth loss divides by it.
+struct FwdPixel {
+    float fx, fy, T, c0, c1, c2, dsum, osum;
+    int cnt;
+    bool inside, done;
+};
+
+struct FwdStage {
+    float4 a[RT];  // mx my ca cb
+    float4 b[RT];  // cc opacity depth 1-opacity
+    float4 c[RT];  // r g b -
+};
+
+__device__ __forceinline__ FwdPixel fwd_pixel_init(const gs_frame &f, int tile) {
+    FwdPixel p;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int px = tx * GS_TILE + (threadIdx.x & 15), py = ty * GS_TILE + (threadIdx.x >> 4);
-    const bool inside = px < f.width && py < f.height;
-    const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
-    const float fx = (float)px, fy = (float)py;
-    // opacity is accumulated as sum(w) (== 1 - T exactly in real arithmetic): 1 - T in fp32
-    // cancels for nearly transparent pixels, and the depth loss divides by it
-    float T = 1.0f, c0 = 0.0f, c1 = 0.0f, c2 = 0.0f, dsum = 0.0f, osum = 0.0f;
-    int cnt = 0;
-    bool done = !inside;
+    p.inside = px < f.width && py < f.height;
+    p.fx = (float)px;
+    p.fy = (float)py;
+    p.T = 1.0f;
+    p.c0 = p.c1 = p.c2 = p.dsum = p.osum = 0.0f;
+    p.cnt = 0;
+    p.done = !p.inside;
+    return p;
+}
+
+__device__ __forceinline__ int64_t fwd_pixel_index(const gs_frame &f, int tile) {
+    const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
+    return (int64_t)(ty * GS_TILE + (threadIdx.x >> 4)) * f.width + tx * GS_TILE + (threadIdx.x & 15);
+}
+
+__device__ __forceinline__ void fwd_pixel_store(const gs_frame &f, int tile, const FwdPixel &p) {
+    if (!p.inside) return;
+    const int64_t q = fwd_pixel_index(f, tile);
+    f.color[3 * q] = p.c0;
+    f.color[3 * q + 1] = p.c1;
+    f.color[3 * q + 2] = p.c2;
+    f.depth[q] = p.dsum;
+    f.opacity[q] = p.osum;
+    f.trans[q] = p.T;
+    f.n_contrib[q] = p.cnt;
+}
+
+// Blends list positions [p0, p1) of the tile front to back; fetch(p) -> Gaussian id.  The
+// tile's entries are staged RT at a time in shared memory; the CTA stops once every pixel is
+// done.  Returns whether every pixel is done.
+template <typename Fetch>
+__device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, FwdStage &st, int p0, int p1,
+                                            int early_stop, Fetch fetch) {
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
-    for (int b = start; b < stop; b += RT) {
-        if (__syncthreads_count(done) == RT) break;
+    for (int b = p0; b < p1; b += RT) {
+        if (__syncthreads_count(px.done) == RT) return true;
         const int e = b + threadIdx.x;
-        if (e < stop) {
-            const int g = f.entry_splat[e];
-            s_a[threadIdx.x] = __ldg(sp + 3 * g);
-            s_b[threadIdx.x] = __ldg(sp + 3 * g + 1);
-            s_c[threadIdx.x] = __ldg(sp + 3 * g + 2);
+        if (e < p1) {
+            const int g = fetch(e);
+            st.a[threadIdx.x] = __ldg(sp + 3 * g);
+            st.b[threadIdx.x] = __ldg(sp + 3 * g + 1);
+            st.c[threadIdx.x] = __ldg(sp + 3 * g + 2);
         }
         __syncthreads();
-        if (!done) {
-            const int nb = min(RT, stop - b);
+        if (!px.done) {
+            const int nb = min(RT, p1 - b);
             for (int j = 0; j < nb; j++) {
-                const float4 A = s_a[j], B = s_b[j], C = s_c[j];
-                const float dx = fx - A.x, dy = fy - A.y;
+                const float4 A = st.a[j], B = st.b[j], C = st.c[j];
+                const float dx = px.fx - A.x, dy = px.fy - A.y;
                 float araw, alpha, oma;
                 alpha_oma(B.y, C.w, quad(A.z, A.w, B.x, dx, dy), araw, alpha, oma);
-                const float w = alpha * T;
-                c0 += C.x * w;
-                c1 += C.y * w;
-                c2 += C.z * w;
-                dsum += B.z * w;
-                osum += w;
-                T *= oma;
-                if (early_stop && T < GS_EARLY_STOP_T) {
-                    done = true;
-                    cnt = b - start + j + 1;
+                const float w = alpha * px.T;
+                px.c0 += C.x * w;
+                px.c1 += C.y * w;
+                px.c2 += C.z * w;
+                px.dsum += B.z * w;
+                px.osum += w;
+                px.T *= oma;
+                if (early_stop && px.T < GS_EARLY_STOP_T) {
+                    px.done = true;
+                    px.cnt = b + j + 1;
                     break;
                 }
             }
-            if (!done) cnt = b - start + nb;
+            if (!px.done) px.cnt = b + nb;
         }
     }
-    if (inside) {
-        const int64_t p = (int64_t)py * f.width + px;
-        f.color[3 * p] = c0;
-        f.color[3 * p + 1] = c1;
-        f.color[3 * p + 2] = c2;
-        f.depth[p] = dsum;
-        f.opacity[p] = osum;
-        f.trans[p] = T;
-        f.n_contrib[p] = cnt;
+    return __syncthreads_count(px.done) == RT;
+}
+
+__global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_stop) {
+    __shared__ FwdStage st;
+    __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
+    __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
+    __shared__ int32_t s_tmp[RT / 32];
+    const int tile = blockIdx.x;
+    FwdPixel px = fwd_pixel_init(f, tile);
+    if (f.counters[GS_CNT_LAZY]) {
+        // lazy lists: the screen-covering Gaussians first; the bucket only if the blend gets
+        // past them (tile_finish_kernel continues from the stored state)
+        if (ts_flag(f)[tile] == TL_MERGED) return;  // interleaved lists: tile_finish_kernel
+        const int na = tile_huge_setup(f, tile, s_words, s_wpre, s_tmp);
+        const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+        const int32_t *hid = f.huge + HIDS;
+        const bool all = blend_range(f, px, st, 0, na, early_stop,
+                                     [&](int p) { return hid[tile_huge_select(p, s_words, s_wpre, nw)]; });
+        const int nb = ts_boff(f)[tile + 1] - ts_boff(f)[tile];
+        if (!all && nb > 0 && threadIdx.x == 0) {
+            ts_flag(f)[tile] = TL_NEEDS_B;
+            f.counters[GS_CNT_ANYFLAG] = 1;
+        }
+    } else {
+        const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
+        const int32_t *list = f.entry_splat + start;
+        blend_range(f, px, st, 0, stop - start, early_stop, [&](int p) { return list[p]; });
     }
+    fwd_pixel_store(f, tile, px);
+}
+
+// Lazy lists, continuation 1: the bucket keys of the tiles that need them (ts_flag != 0)
+__global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
+    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
+    const int64_t nt = f.counters[GS_CNT_TOUCHED];
+    int32_t *cur = ts_cursor(f);
+    const int32_t *flag = ts_flag(f);
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += (int64_t)gridDim.x * blockDim.x) {
+        const int g = f.touched_list[k];
+        if (f.kept[g] <= 0) continue;
+        const uint64_t key = depth_key(f, g);
+        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+        const int64_t base = (int64_t)f.keep_bits[g];
+        const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
+        const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+        for (int c = 0; c < ncand; c++) {
+            const int tx = r.x + c % nx, ty = r.z + c / nx, t = ty * f.tiles_x + tx;
+            bool keep;
+            if (ncand <= GS_SMALL_CAND) {
+                keep = (f.keep_bits[g] >> c) & 1ull;
+            } else if (base >= 0) {
+                keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
+            } else {
+                const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+            }
+            if (keep && flag[t]) f.keys_b[atomicAdd(&cur[t], 1)] = key;
+        }
+    }
+}
+
+// Lazy lists, continuation 2: CTA per flagged tile.  Sorts the bucket (written back sorted, the
+// backward reads it); interleaved tiles get their merged list in entry_splat and are blended
+// from the start; the others continue the blend past their screen-covering Gaussians from the
+// state the forward stored.
+constexpr int TF_THREADS = RT;
+
+struct FinishSmem {
+    uint64_t key[SM_CAP];
+    int32_t a[GS_HUGE_CAP];
+    uint32_t words[GS_HUGE_CAP / 32];
+    int32_t wpre_a[GS_HUGE_CAP / 32];
+    uint32_t isb[(GS_HUGE_CAP + SM_CAP) / 32];
+    int32_t wpre[(GS_HUGE_CAP + SM_CAP) / 32];
+    int32_t tmp[TF_THREADS / 32];
+    FwdStage st;
+};
+
+__global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int early_stop) {
+    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
+    const int tile = blockIdx.x;
+    const int flag = ts_flag(f)[tile];
+    if (flag == TL_CONCAT) return;
+    extern __shared__ uint64_t fin_raw[];
+    FinishSmem &sm = *reinterpret_cast<FinishSmem *>(fin_raw);
+    const int sb = ts_boff(f)[tile], nb = ts_boff(f)[tile + 1] - sb;
+    uint64_t *bucket = f.keys_b + sb;
+    const uint64_t *B = sort_bucket<TF_THREADS>(sm.key, bucket, f.keys_a + sb, nb, true);
+    const int na = tile_huge_setup(f, tile, sm.words, sm.wpre_a, sm.tmp);
+    FwdPixel px = fwd_pixel_init(f, tile);
+    if (flag == TL_MERGED) {
+        const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+        tile_huge_expand(sm.words, sm.wpre_a, nw, sm.a);
+        int32_t *list = f.entry_splat + f.tile_offsets[tile];
+        merge_tile_list<TF_THREADS>(f, list, sm.a, na, B, nb, sm.isb, sm.wpre, sm.tmp, GS_HUGE_CAP + SM_CAP);
+        __syncthreads();
+        blend_range(f, px, sm.st, 0, na + nb, early_stop, [&](int p) { return list[p]; });
+    } else {  // TL_NEEDS_B: resume after the screen-covering Gaussians
+        __syncthreads();
+        if (px.inside) {
+            const int64_t q = fwd_pixel_index(f, tile);
+            px.c0 = f.color[3 * q];
+            px.c1 = f.color[3 * q + 1];
+            px.c2 = f.color[3 * q + 2];
+            px.dsum = f.depth[q];
+            px.osum = f.opacity[q];
+            px.T = f.trans[q];
+            px.cnt = f.n_contrib[q];
+            px.done = early_stop && px.T < GS_EARLY_STOP_T;
+        }
+        blend_range(f, px, sm.st, na, na + nb, early_stop, [&](int p) { return (int)(uint32_t)bucket[p - na]; });
+    }
+    fwd_pixel_store(f, tile, px);
 }
 
 // Transposed butterfly over 10 fields in 12 shuffles: on return, an even lane L holds the warp
@@ -202,6 +345,23 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
     if (stop == start) return;
     const unsigned lane = threadIdx.x & 31u;
     const int fld = reduce10_field(lane);
+    // entry source: materialised list, or (lazy lists) the screen-covering Gaussians then the
+    // sorted bucket
+    __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
+    __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
+    __shared__ int32_t s_tmp[BT / 32];
+    const bool lazy = f.counters[GS_CNT_LAZY] && ts_flag(f)[tile] != TL_MERGED;
+    int na = 0, nw = 0;
+    if (lazy) {
+        na = tile_huge_setup(f, tile, s_words, s_wpre, s_tmp);
+        nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+    }
+    const int32_t *hid = f.huge + HIDS;
+    const uint64_t *bucket = f.keys_b + ts_boff(f)[tile];
+    auto fetch = [&](int p) -> int {  // list position -> Gaussian id
+        if (!lazy) return f.entry_splat[start + p];
+        return p < na ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : (int)(uint32_t)bucket[p - na];
+    };
     BwdPixel px[2];
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
@@ -235,7 +395,7 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
         const int nb = b_end - b0;
         __syncthreads();
         for (int i = threadIdx.x; i < nb; i += BT) {
-            const int g = f.entry_splat[b0 + i];
+            const int g = fetch(b0 - start + i);
             s_g[i] = g;
             s_a[i] = __ldg(sp + 3 * g);
             s_b[i] = __ldg(sp + 3 * g + 1);
@@ -287,7 +447,13 @@ extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
     render_fwd_kernel<<<T, RT, 0, (cudaStream_t)stream>>>(*f, early_stop);
-    return check_launch("render_fwd_kernel");
+    int rc = check_launch("render_fwd_kernel");
+    if (rc) return rc;
+    // lazy lists: bucket fill + sorted continuation of the tiles that need them (no-ops otherwise)
+    lazy_fill_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    if ((rc = check_launch("lazy_fill_kernel"))) return rc;
+    tile_finish_kernel<<<T, TF_THREADS, sizeof(FinishSmem), (cudaStream_t)stream>>>(*f, early_stop);
+    return check_launch("tile_finish_kernel");
 }
 
 extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
@@ -301,3 +467,9 @@ extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
     render_bwd_kernel<<<T, BT, 0, (cudaStream_t)stream>>>(*f);
     return check_launch("render_bwd_kernel");
 }
+
+namespace gs {
+void init_render_attrs() {
+    cudaFuncSetAttribute(tile_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FinishSmem));
+}
+}  // namespace gs

@@ -28,11 +28,11 @@ NEAR_CLIP = 0.01
 def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     """Our kernels per map-optimisation iteration:
     preprocess 5 (projection + small-footprint cull, large-footprint setup / bands / tiles /
-    finish), bin 6 (bucket count, huge sort, huge transpose, tile scan, bucket fill, per-tile
-    sort + merge), forward 1, loss 4 (tables, SSIM+L1, depth, finalize), backward 2 (zero +
-    tiles), chain + Adam 2."""
+    finish), bin 3 (lazy lists: huge sort, huge transpose, tile scan), forward 3 (blend, bucket
+    fill + sorted continuation for the tiles that need them), loss 4 (tables, SSIM+L1, depth,
+    finalize), backward 2 (zero + tiles), chain + Adam 2."""
     del tiles
-    return 5 + 6 + 1 + 4 + 2 + (1 if chain_only else 2)
+    return 5 + 3 + 3 + 4 + 2 + (1 if chain_only else 2)
 
 
 @dataclass
@@ -109,7 +109,7 @@ class MapOptimizer:
     def _launch(self) -> None:
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
         call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
-        call("gs_bin", f, 1, s)
+        call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss", f, cur, self.lam, self.xi, s)
         call("gs_render_bwd", f, s)
@@ -169,7 +169,7 @@ class MapOptimizer:
         ev[0].record()
         call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
         ev[1].record()
-        call("gs_bin", f, 1, s)
+        call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         ev[2].record()
         call("gs_render_fwd", f, 1, s)
         ev[3].record()

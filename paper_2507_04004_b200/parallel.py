@@ -74,7 +74,7 @@ class BatchMapOptimizer:
         self.cur.copy_(self.views[k].buf)
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
         call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
-        call("gs_bin", f, 1, s)
+        call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss", f, cur, self.lam, self.xi, s)
         call("gs_render_bwd", f, s)
