@@ -132,10 +132,7 @@ __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
     const int t = 32 * u + lane;
     if (t < T) {
         f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + w] = mine;
-        if (mine) {
-            atomicAdd(&ts_huge(f)[t], __popc(mine));
-            atomicMax(&ts_last(f)[t], 32 * w + 31 - __clz(mine));  // last record of the tile
-        }
+        if (mine) atomicAdd(&ts_huge(f)[t], __popc(mine));
     }
 }
 
@@ -144,13 +141,11 @@ __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
 __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f, int lazy) {
     __shared__ int32_t s_warp[2][32];
     __shared__ int32_t s_carry[2];
-    __shared__ int s_any;
     const int T = f.tiles_x * f.tiles_y;
     int32_t *cur = f.tile_scratch, *hcount = f.tile_scratch + T + 1, *boff = f.tile_scratch + 2 * (T + 1);
     const bool use_huge = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) > 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_any = 0;
     __syncthreads();
     for (int t0 = 0; t0 < T; t0 += blockDim.x) {
         const int t = t0 + threadIdx.x;
@@ -180,12 +175,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f, int lazy) {
             f.tile_offsets[t] = before + x - v;
             cur[t] = bb + xb - vb;
             boff[t] = bb + xb - vb;
-            // lazy lists: a tile whose bucket interleaves with its screen-covering Gaussians
-            // needs the merged list; the others are A then B
-            int flag = TL_CONCAT;
-            if (use_huge && vb > 0 && v > vb && huge_keys(f)[ts_last(f)[t]] > f.tile_minkey[t]) flag = TL_MERGED;
-            ts_flag(f)[t] = flag;
-            if (flag) s_any = 1;
+            ts_flag(f)[t] = TL_LAZY_A;  // lazy lists: the forward flags the tiles it cannot finish
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -204,7 +194,7 @@ __global__ void __launch_bounds__(1024) tile_scan_kernel(gs_frame f, int lazy) {
         if (over) f.counters[GS_CNT_OVERFLOW] = 1;
         f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
         f.counters[GS_CNT_LAZY] = lazy;
-        f.counters[GS_CNT_ANYFLAG] = lazy && s_any;
+        f.counters[GS_CNT_ANYFLAG] = 0;
     }
 }
 
@@ -296,8 +286,6 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         set_error("gs_bin: cull must be 0, 1 or GS_BIN_LAZY");
         return GS_ERR_ARG;
     }
-    // last huge record per tile: -1
-    cudaMemsetAsync(f->tile_scratch + 4 * ((size_t)T + 1), 0xff, sizeof(int32_t) * ((size_t)T + 1), st);
     // reset the binning counters (touched, big and huge belong to preprocess) and the per-tile
     // counts
     cudaMemsetAsync(f->counters + GS_CNT_ENTRIES, 0, sizeof(int32_t), st);

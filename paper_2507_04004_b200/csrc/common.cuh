@@ -310,17 +310,16 @@ inline bool compact_words(int64_t n, int32_t tiles, int *tile_bits, int *rank_bi
 // result for candidate c < 64 (the emit pass recomputes candidates >= 64).
 __device__ __forceinline__ int cull_rect(float mx, float my, float ca, float cb, float cc, float qcut, int4 r,
                                          int width, int height, uint64_t &bits) {
-    const int nx = r.y - r.x + 1;
-    const int ncand = nx > 0 ? nx * (r.w - r.z + 1) : 0;
-    int count = 0;
+    int count = 0, c = 0;
     bits = 0ull;
-    for (int c = 0; c < ncand; c++) {
-        const int tx = r.x + c % nx, ty = r.z + c / nx;
-        const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-        const int x1 = min(x0 + GS_TILE - 1, width - 1), y1 = min(y0 + GS_TILE - 1, height - 1);
-        if (tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1)) {
-            count++;
-            if (c < 64) bits |= 1ull << c;
+    for (int ty = r.z; ty <= r.w; ty++) {
+        const int y0 = ty * GS_TILE, y1 = min(y0 + GS_TILE - 1, height - 1);
+        for (int tx = r.x; tx <= r.y; tx++, c++) {
+            const int x0 = tx * GS_TILE, x1 = min(x0 + GS_TILE - 1, width - 1);
+            if (tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1)) {
+                count++;
+                if (c < 64) bits |= 1ull << c;
+            }
         }
     }
     return count;

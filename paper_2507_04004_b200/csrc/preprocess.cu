@@ -37,12 +37,13 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
         srow[warp][lane][3] = p0.w;
     }
     const unsigned need = __ballot_sync(0xffffffffu, near_ok);
-    // 2) cooperative, coalesced load of the remaining 15 float4 of every needed row
+    // 2) cooperative, coalesced load of float4 columns 1..14 of every needed row (half a warp per
+    //    row: 2 rows per instruction; column 15 is row padding)
+    const int c4 = lane & 15;
 #pragma unroll
-    for (int j = 0; j < 15; j++) {
-        int k = lane + 32 * j;       // 0..479
-        int r = k / 15, c4 = 1 + k % 15;
-        if ((need >> r) & 1u) {
+    for (int j = 0; j < 16; j++) {
+        const int r = 2 * j + (lane >> 4);
+        if (c4 >= 1 && c4 <= 14 && ((need >> r) & 1u)) {
             float4 v = __ldg(reinterpret_cast<const float4 *>(params + (base + r) * GS_ROW + 4 * c4));
             srow[warp][r][4 * c4 + 0] = v.x;
             srow[warp][r][4 * c4 + 1] = v.y;

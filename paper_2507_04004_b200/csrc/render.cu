@@ -137,17 +137,25 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
     const int tile = blockIdx.x;
     FwdPixel px = fwd_pixel_init(f, tile);
     if (f.counters[GS_CNT_LAZY]) {
-        // lazy lists: the screen-covering Gaussians first; the bucket only if the blend gets
-        // past them (tile_finish_kernel continues from the stored state)
-        if (ts_flag(f)[tile] == TL_MERGED) return;  // interleaved lists: tile_finish_kernel
+        // lazy lists: the leading screen-covering Gaussians (every one whose key is below the
+        // tile's smallest bucketed key precedes the whole bucket); tiles whose blend outlives them
+        // are finished by tile_finish_kernel from the stored state
+        __shared__ int s_lead;
         const int na = tile_huge_setup(f, tile, s_words, s_wpre, s_tmp);
         const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+        if (threadIdx.x == 0) {
+            const uint64_t mk = f.tile_minkey[tile];
+            s_lead = mk == ~0ull ? na : tile_huge_rank(huge_before_key(f, mk), s_words, s_wpre, nw, na);
+        }
+        __syncthreads();
+        const int lead = s_lead;
         const int32_t *hid = f.huge + HIDS;
-        const bool all = blend_range(f, px, st, 0, na, early_stop,
+        const bool all = blend_range(f, px, st, 0, lead, early_stop,
                                      [&](int p) { return hid[tile_huge_select(p, s_words, s_wpre, nw)]; });
-        const int nb = ts_boff(f)[tile + 1] - ts_boff(f)[tile];
-        if (!all && nb > 0 && threadIdx.x == 0) {
-            ts_flag(f)[tile] = TL_NEEDS_B;
+        const int total = f.tile_offsets[tile + 1] - f.tile_offsets[tile];
+        if (!all && total > lead && threadIdx.x == 0) {
+            ts_flag(f)[tile] = TL_LIST;
+            ts_resume(f)[tile] = lead;
             f.counters[GS_CNT_ANYFLAG] = 1;
         }
     } else {
@@ -190,10 +198,9 @@ __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
     }
 }
 
-// Lazy lists, continuation 2: CTA per flagged tile.  Sorts the bucket (written back sorted, the
-// backward reads it); interleaved tiles get their merged list in entry_splat and are blended
-// from the start; the others continue the blend past their screen-covering Gaussians from the
-// state the forward stored.
+// Lazy lists, continuation 2: CTA per flagged tile.  Sorts the bucket, writes the tile's merged
+// list to entry_splat (the backward reads it there) and resumes the blend where the forward
+// stopped (state from the stored images).
 constexpr int TF_THREADS = RT;
 
 struct FinishSmem {
@@ -210,37 +217,30 @@ struct FinishSmem {
 __global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int early_stop) {
     if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
     const int tile = blockIdx.x;
-    const int flag = ts_flag(f)[tile];
-    if (flag == TL_CONCAT) return;
+    if (ts_flag(f)[tile] != TL_LIST) return;
     extern __shared__ uint64_t fin_raw[];
     FinishSmem &sm = *reinterpret_cast<FinishSmem *>(fin_raw);
     const int sb = ts_boff(f)[tile], nb = ts_boff(f)[tile + 1] - sb;
-    uint64_t *bucket = f.keys_b + sb;
-    const uint64_t *B = sort_bucket<TF_THREADS>(sm.key, bucket, f.keys_a + sb, nb, true);
+    const uint64_t *B = sort_bucket<TF_THREADS>(sm.key, f.keys_b + sb, f.keys_a + sb, nb, false);
     const int na = tile_huge_setup(f, tile, sm.words, sm.wpre_a, sm.tmp);
+    const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
+    tile_huge_expand(sm.words, sm.wpre_a, nw, sm.a);
+    int32_t *list = f.entry_splat + f.tile_offsets[tile];
+    merge_tile_list<TF_THREADS>(f, list, sm.a, na, B, nb, sm.isb, sm.wpre, sm.tmp, GS_HUGE_CAP + SM_CAP);
+    __syncthreads();
     FwdPixel px = fwd_pixel_init(f, tile);
-    if (flag == TL_MERGED) {
-        const int nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
-        tile_huge_expand(sm.words, sm.wpre_a, nw, sm.a);
-        int32_t *list = f.entry_splat + f.tile_offsets[tile];
-        merge_tile_list<TF_THREADS>(f, list, sm.a, na, B, nb, sm.isb, sm.wpre, sm.tmp, GS_HUGE_CAP + SM_CAP);
-        __syncthreads();
-        blend_range(f, px, sm.st, 0, na + nb, early_stop, [&](int p) { return list[p]; });
-    } else {  // TL_NEEDS_B: resume after the screen-covering Gaussians
-        __syncthreads();
-        if (px.inside) {
-            const int64_t q = fwd_pixel_index(f, tile);
-            px.c0 = f.color[3 * q];
-            px.c1 = f.color[3 * q + 1];
-            px.c2 = f.color[3 * q + 2];
-            px.dsum = f.depth[q];
-            px.osum = f.opacity[q];
-            px.T = f.trans[q];
-            px.cnt = f.n_contrib[q];
-            px.done = early_stop && px.T < GS_EARLY_STOP_T;
-        }
-        blend_range(f, px, sm.st, na, na + nb, early_stop, [&](int p) { return (int)(uint32_t)bucket[p - na]; });
+    if (px.inside) {
+        const int64_t q = fwd_pixel_index(f, tile);
+        px.c0 = f.color[3 * q];
+        px.c1 = f.color[3 * q + 1];
+        px.c2 = f.color[3 * q + 2];
+        px.dsum = f.depth[q];
+        px.osum = f.opacity[q];
+        px.T = f.trans[q];
+        px.cnt = f.n_contrib[q];
+        px.done = early_stop && px.T < GS_EARLY_STOP_T;
     }
+    blend_range(f, px, sm.st, ts_resume(f)[tile], na + nb, early_stop, [&](int p) { return list[p]; });
     fwd_pixel_store(f, tile, px);
 }
 
@@ -350,17 +350,16 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
     __shared__ int32_t s_tmp[BT / 32];
-    const bool lazy = f.counters[GS_CNT_LAZY] && ts_flag(f)[tile] != TL_MERGED;
-    int na = 0, nw = 0;
+    const bool lazy = f.counters[GS_CNT_LAZY] && ts_flag(f)[tile] == TL_LAZY_A;
+    int nw = 0;
     if (lazy) {
-        na = tile_huge_setup(f, tile, s_words, s_wpre, s_tmp);
+        tile_huge_setup(f, tile, s_words, s_wpre, s_tmp);
         nw = (min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) + 31) >> 5;
     }
     const int32_t *hid = f.huge + HIDS;
-    const uint64_t *bucket = f.keys_b + ts_boff(f)[tile];
     auto fetch = [&](int p) -> int {  // list position -> Gaussian id
-        if (!lazy) return f.entry_splat[start + p];
-        return p < na ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : (int)(uint32_t)bucket[p - na];
+        // lazy, unflagged: the blend ended within the leading screen-covering Gaussians
+        return lazy ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : f.entry_splat[start + p];
     };
     BwdPixel px[2];
     if (threadIdx.x == 0) s_max = 0;

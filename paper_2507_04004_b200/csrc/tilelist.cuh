@@ -22,10 +22,12 @@ __device__ __forceinline__ int32_t *ts_cursor(const gs_frame &f) { return f.tile
 __device__ __forceinline__ int32_t *ts_huge(const gs_frame &f) { return f.tile_scratch + (f.tiles_x * f.tiles_y + 1); }
 __device__ __forceinline__ int32_t *ts_boff(const gs_frame &f) { return f.tile_scratch + 2 * (f.tiles_x * f.tiles_y + 1); }
 __device__ __forceinline__ int32_t *ts_flag(const gs_frame &f) { return f.tile_scratch + 3 * (f.tiles_x * f.tiles_y + 1); }
-__device__ __forceinline__ int32_t *ts_last(const gs_frame &f) { return f.tile_scratch + 4 * (f.tiles_x * f.tiles_y + 1); }
+__device__ __forceinline__ int32_t *ts_resume(const gs_frame &f) { return f.tile_scratch + 4 * (f.tiles_x * f.tiles_y + 1); }
 
-// per-tile list modes of lazy binning (ts_flag)
-enum { TL_CONCAT = 0, TL_MERGED = 1, TL_NEEDS_B = 2 };
+// per-tile list state of lazy binning (ts_flag): the forward blends the leading run of
+// screen-covering Gaussians (those ahead of every bucketed key); a tile whose blend outlives
+// it gets its full merged list in entry_splat and is resumed at ts_resume by tile_finish_kernel
+enum { TL_LAZY_A = 0, TL_LIST = 1 };
 
 __device__ __forceinline__ const uint64_t *huge_keys(const gs_frame &f) {
     return reinterpret_cast<const uint64_t *>(f.huge + HKEYS);
@@ -36,6 +38,26 @@ __device__ __forceinline__ uint64_t depth_key(const gs_frame &f, int g) {
 }
 
 // ---------------------------------------------------------------------------------------------
+// records with a key below `key` (binary search over the sorted huge keys)
+__device__ __forceinline__ int huge_before_key(const gs_frame &f, uint64_t key) {
+    const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
+    const uint64_t *hkeys = huge_keys(f);
+    int lo = 0, hi = nrec;
+    while (lo < hi) {
+        const int m = (lo + hi) >> 1;
+        if (hkeys[m] < key) lo = m + 1;
+        else hi = m;
+    }
+    return lo;
+}
+
+// A elements of the tile with record index < h (rank in the setup words)
+__device__ __forceinline__ int tile_huge_rank(int h, const uint32_t *s_words, const int32_t *s_wpre, int nw, int na) {
+    const int w = h >> 5;
+    if (w >= nw) return na;
+    return s_wpre[w] + __popc(s_words[w] & ((1u << (h & 31)) - 1u));
+}
+
 // A of a tile: the depth-ordered mask words and their exclusive popcount prefix in shared
 // memory (collective over the CTA; returns |A|).  s_tmp: >= blockDim.x / 32 ints.
 __device__ __forceinline__ int tile_huge_setup(const gs_frame &f, int t, uint32_t *s_words, int32_t *s_wpre,
