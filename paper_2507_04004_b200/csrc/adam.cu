@@ -202,8 +202,10 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
     }
     __syncwarp();
     if (g >= 0) {
-        const double2 *g2 = reinterpret_cast<const double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
+        double2 *g2 = reinterpret_cast<double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
         const double2 a = g2[0], b = g2[1], c = g2[2], d = g2[3], e = g2[4];
+        if (mode == 1 && f.counters[GS_CNT_LAZY])  // batches: keep the row zero for the next view
+            for (int q = 0; q < GS_G2D / 2; q++) g2[q] = make_double2(0.0, 0.0);
         const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
         chain_row(srow[warp][lane], gv, scam, sgr[warp][lane]);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
@@ -278,6 +280,10 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
         const int c4 = (int)(idx & 15);
         if (c4 == 15) continue;  // columns 60-63: padding
         const int64_t g = f.touched_list[k];
+        // the iteration engine keeps the screen-space gradient rows zero between backwards (the
+        // chain has consumed this one)
+        if (c4 < GS_G2D / 2 && f.counters[GS_CNT_LAZY])
+            reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + c4] = make_double2(0.0, 0.0);
         const float2 bc = reinterpret_cast<const float2 *>(f.bias_corr)[k];
         const float4 G = reinterpret_cast<const float4 *>(f.grad_rows)[k * (GS_ROW / 4) + c4];
         const int64_t off = g * GS_ROW + 4 * c4;

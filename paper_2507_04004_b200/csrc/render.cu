@@ -93,10 +93,11 @@ template <typename Fetch>
 __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, FwdStage &st, int p0, int p1,
                                             int early_stop, Fetch fetch) {
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
-    for (int b = p0; b < p1; b += RT) {
+    // the first round stages 64 entries (most blends end within a few dozen), then RT at a time
+    for (int b = p0, step = RT / 4; b < p1; b += step, step = RT) {
         if (__syncthreads_count(px.done) == RT) return true;
         const int e = b + threadIdx.x;
-        if (e < p1) {
+        if ((int)threadIdx.x < step && e < p1) {
             const int g = fetch(e);
             st.a[threadIdx.x] = __ldg(sp + 3 * g);
             st.b[threadIdx.x] = __ldg(sp + 3 * g + 1);
@@ -104,7 +105,7 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
         }
         __syncthreads();
         if (!px.done) {
-            const int nb = min(RT, p1 - b);
+            const int nb = min(step, p1 - b);
             for (int j = 0; j < nb; j++) {
                 const float4 A = st.a[j], B = st.b[j], C = st.c[j];
                 const float dx = px.fx - A.x, dy = px.fy - A.y;
@@ -431,6 +432,9 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
 
 // zero the g2d rows of the touched Gaussians (12 doubles = 6 double2 per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
+    // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
+    // batches, the chain rule) clears every row it consumes, and the workspace starts zero-filled
+    if (f.counters[GS_CNT_LAZY]) return;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     if (i >= 6 * nt) return;
