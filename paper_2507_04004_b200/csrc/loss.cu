@@ -87,6 +87,19 @@ __device__ __forceinline__ float kw(int d) {
     return K[d];
 }
 
+// Item it of `groups` groups of `len` (>= 32) elements, in warp-aligned order: the first 32
+// elements of every group (one warp each), then the remaining len - 32 of every group.
+__device__ __forceinline__ void split32(int it, int groups, int len, int &group, int &elem) {
+    if (it < 32 * groups) {
+        group = it >> 5;
+        elem = it & 31;
+    } else {
+        const int j = it - 32 * groups, rest = len - 32;
+        group = j / rest;
+        elem = 32 + j % rest;
+    }
+}
+
 // INTERIOR: the CTA's whole halo lies >= 10 px inside the image, so every blur / adjoint
 // weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
 struct SsimSmem {
@@ -146,7 +159,11 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     __syncthreads();
     // 2) horizontal blur of the 5 moments (a, b, aa, bb, ab); hx column j <-> x = x0-5+j
     for (int it = tid; it < NIR * (HXC / HB); it += L_THREADS) {
-        const int iy = it % NIR, c0 = HB * (it / NIR);  // a warp: consecutive rows, one strip
+        // warp-aligned items: rows 0..31 of a strip per warp, then the last NIR - 32 rows of every
+        // strip (odd row stride: a warp's 32 rows hit 32 banks)
+        int iy, c0;
+        split32(it, HXC / HB, NIR, c0, iy);
+        c0 *= HB;
         float m[5][HB];
 #pragma unroll
         for (int k = 0; k < HB; k++) m[0][k] = m[1][k] = m[2][k] = m[3][k] = m[4][k] = 0.0f;
@@ -177,7 +194,9 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     // 3) vertical blur -> SSIM map and its partials (R/losses.py:96-113); g row gy <-> y0-5+gy
     float s_acc = 0.0f;
     for (int it = tid; it < GW * NVS; it += L_THREADS) {
-        const int gx = it % GW, gy0 = VS * (it / GW);
+        int gx, gy0;  // warp-aligned items: 32 consecutive columns of one strip per warp
+        split32(it, NVS, GW, gy0, gx);
+        gy0 *= VS;
         const int x = x0 - 5 + gx;
         float u[5][VS];
 #pragma unroll
@@ -228,7 +247,9 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     // 4) vertical adjoint at rows [y0, y0+TH): r(p) = sum_d A[p][d] g(p+d) (zero weights where
     //    p+d leaves the image)
     for (int it = tid; it < GW * NAS; it += L_THREADS) {
-        const int gx = it % GW, oy0 = AS * (it / GW);
+        int gx, oy0;
+        split32(it, NAS, GW, oy0, gx);
+        oy0 *= AS;
         float r3[3][AS];
 #pragma unroll
         for (int k = 0; k < AS; k++) r3[0][k] = r3[1][k] = r3[2][k] = 0.0f;
@@ -260,7 +281,8 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     //    covers 16 rows x 2 strips
     float l1_acc = 0.0f;
     {
-        const int oy = tid & 15, ox0 = HS * (tid >> 4);
+        // lanes 0-15: strip w, lanes 16-31: strip w + 8 (16 banks apart: conflict-free rows)
+        const int oy = tid & 15, ox0 = HS * ((tid >> 5) + 8 * ((tid >> 4) & 1));
         float A[3][HS];
 #pragma unroll
         for (int k = 0; k < HS; k++) A[0][k] = A[1][k] = A[2][k] = 0.0f;
