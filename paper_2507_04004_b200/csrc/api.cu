@@ -33,6 +33,7 @@ void init_loss_attrs();                                     // loss.cu
 void init_chain_attrs();                                    // adam.cu
 void init_binning_attrs();                                  // binning.cu
 void init_render_attrs();                                   // render.cu
+void init_preprocess_attrs();                               // preprocess.cu
 
 // kernel attributes (dynamic shared-memory opt-in) are set once per process, outside any
 // stream capture, the first time a workspace is laid out
@@ -43,6 +44,7 @@ static void init_attrs_once() {
         init_chain_attrs();
         init_binning_attrs();
         init_render_attrs();
+        init_preprocess_attrs();
     });
 }
 

@@ -11,126 +11,156 @@ namespace gs {
 
 constexpr int PP_WARPS = 4;
 constexpr int PP_THREADS = PP_WARPS * 32;
-constexpr int ROWP = 65;  // padded smem row (conflict-free per-lane column reads)
 
+__device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void pp_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void pp_cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// A warp's batch of 32 parameter rows in shared memory: 16-B chunk c of row r sits at chunk
+// c ^ (r & 7), so the 8 lanes of each 128-bit shared wavefront (one row each, same logical
+// chunk) hit distinct banks.
+struct PPBatch {
+    float4 row[32][16];
+};
+
+__device__ __forceinline__ float4 pp_chunk(const PPBatch &bt, int r, int c) { return bt.row[r][c ^ (r & 7)]; }
+
+// Persistent warps over batches of 32 Gaussians, double-buffered: the next batch's rows stream
+// in (cp.async) while the current one is projected, shaded and culled.
 __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, const float *__restrict__ params,
                                                                 const gs_view *__restrict__ view) {
-    __shared__ float srow[PP_WARPS][32][ROWP];
+    extern __shared__ float4 pp_raw[];
+    PPBatch(*bufs)[2] = reinterpret_cast<PPBatch(*)[2]>(pp_raw);
     __shared__ gs_camera scam;
     if (threadIdx.x == 0) scam = view->cam;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t base = ((int64_t)blockIdx.x * PP_WARPS + warp) * 32;
-    const int64_t i = base + lane;
+    PPBatch *buf = bufs[warp];
     const int64_t n = f.n;
+    const int64_t nbatch = (n + 31) / 32;
+    const int64_t stride = (int64_t)gridDim.x * PP_WARPS;
     const gs_camera &cam = scam;
-
-    // 1) own row's first float4 (pos) -> near-plane test (R/gaussians.py:188-191)
-    bool near_ok = false;
-    if (i < n) {
-        float4 p0 = __ldg(reinterpret_cast<const float4 *>(params + i * GS_ROW));
-        float z = (p0.x * cam.rot_cw[6] + p0.y * cam.rot_cw[7] + p0.z * cam.rot_cw[8]) + cam.trans_cw[2];
-        near_ok = z > GS_NEAR_CLIP;
-        srow[warp][lane][0] = p0.x;
-        srow[warp][lane][1] = p0.y;
-        srow[warp][lane][2] = p0.z;
-        srow[warp][lane][3] = p0.w;
-    }
-    const unsigned need = __ballot_sync(0xffffffffu, near_ok);
-    // 2) cooperative, coalesced load of float4 columns 1..14 of every needed row (half a warp per
-    //    row: 2 rows per instruction; column 15 is row padding)
-    const int c4 = lane & 15;
+    auto issue = [&](int64_t batch, PPBatch &bt) {  // 16 chunks per lane, two rows per instruction
+        const int64_t base = batch * 32;
 #pragma unroll
-    for (int j = 0; j < 16; j++) {
-        const int r = 2 * j + (lane >> 4);
-        if (c4 >= 1 && c4 <= 14 && ((need >> r) & 1u)) {
-            float4 v = __ldg(reinterpret_cast<const float4 *>(params + (base + r) * GS_ROW + 4 * c4));
-            srow[warp][r][4 * c4 + 0] = v.x;
-            srow[warp][r][4 * c4 + 1] = v.y;
-            srow[warp][r][4 * c4 + 2] = v.z;
-            srow[warp][r][4 * c4 + 3] = v.w;
+        for (int j = 0; j < 16; j++) {
+            const int r = 2 * j + (lane >> 4), c = lane & 15;
+            if (base + r < n) pp_cp_async16(&bt.row[r][c ^ (r & 7)], params + (base + r) * GS_ROW + 4 * c);
         }
-    }
-    __syncwarp();
-    bool touched = false, big = false;
-    if (i < n) {
-        const float *p = srow[warp][lane];
-        float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-        float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
-        int4 *rc = reinterpret_cast<int4 *>(f.rect) + i;
-        if (!near_ok) {
-            float z = (p[0] * cam.rot_cw[6] + p[1] * cam.rot_cw[7] + p[2] * cam.rot_cw[8]) + cam.trans_cw[2];
-            s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-            s2[1] = make_float4(0.f, 0.f, z, 0.f);
-            s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-            *cv = make_float4(0.f, 0.f, 0.f, -1.f);
-            *rc = make_int4(0, -1, 0, -1);
-            f.valid[i] = 0;
-            f.kept[i] = 0;
-        } else {
-            // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians near
-            // the 0.01 m clip plane, and fp32 would shift their whole footprint
-            ProjectedT<double> pd;
-            project_full<double>(p, cam, pd);
-            Projected pr;
-            pr.mu[2] = (float)pd.mu[2];
-            pr.mx = (float)pd.mx;
-            pr.my = (float)pd.my;
-            pr.c00 = (float)pd.c00;
-            pr.c01 = (float)pd.c01;
-            pr.c11 = (float)pd.c11;
-            pr.ca = (float)pd.ca;
-            pr.cb = (float)pd.cb;
-            pr.cc = (float)pd.cc;
-            pr.valid = pd.valid;
-            const float op = 1.0f / (1.0f + expf(-p[10]));
-            // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
-            const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
-            float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
-            if (un < 1e-12f) un = 1.0f;
-            float b[16];
-            sh_basis(u0 / un, u1 / un, u2 / un, b);
-            float col[3];
+        pp_cp_commit();
+    };
+    int64_t batch = (int64_t)blockIdx.x * PP_WARPS + warp;
+    if (batch < nbatch) issue(batch, buf[0]);
+    for (int cur = 0; batch < nbatch; batch += stride, cur ^= 1) {
+        if (batch + stride < nbatch) issue(batch + stride, buf[cur ^ 1]);
+        else pp_cp_commit();  // empty group: the wait below still means "this batch landed"
+        pp_cp_wait_1();
+        __syncwarp();
+        const PPBatch &bt = buf[cur];
+        const int64_t i = batch * 32 + lane;
+        bool touched = false, big = false;
+        if (i < n) {
+            // floats 0-15: pos 0-2, log_scale 3-5, quat 6-9, opacity logit 10, sh_low 11-13,
+            // sh_high[0] 14-15 (R/gaussians.py:150-153)
+            float pk[16];
 #pragma unroll
-            for (int c = 0; c < 3; c++) {
-                float acc = 0.0f;
-#pragma unroll
-                for (int k = 0; k < 15; k++) acc += b[k + 1] * p[14 + 3 * k + c];
-                const float pre = b[0] * p[11 + c] + acc + 0.5f;
-                col[c] = pre > 0.0f ? pre : 0.0f;
+            for (int c = 0; c < 4; c++) {
+                const float4 v = pp_chunk(bt, lane, c);
+                pk[4 * c] = v.x;
+                pk[4 * c + 1] = v.y;
+                pk[4 * c + 2] = v.z;
+                pk[4 * c + 3] = v.w;
             }
-            int4 rect = make_int4(0, -1, 0, -1);
-            float qcut = 0.0f, radius = -1.0f;
-            const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width, f.height,
-                                                      f.tiles_x, f.tiles_y, rect, qcut, radius);
-            if (!active) rect = make_int4(0, -1, 0, -1);
-            // exact per-tile cull of the rectangle (R/rasterizer.py:150-166), fused here for small
-            // footprints; large ones by the big_* kernels (band bounds, tile bounds, exact rows)
-            const int ncand = (rect.y - rect.x + 1) * (rect.w - rect.z + 1);
-            big = active && ncand > GS_SMALL_CAND;
-            uint64_t bits = 0ull;
-            const int kept = (active && !big)
-                                 ? cull_rect(pr.mx, pr.my, pr.ca, pr.cb, pr.cc, qcut, rect, f.width, f.height, bits)
-                                 : 0;
-            touched = kept > 0;
-            s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
-            s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-            // 1 - opacity = sigmoid(-logit), kept exact for the blend's 1 - alpha
-            s2[2] = make_float4(col[0], col[1], col[2], 1.0f / (1.0f + expf(p[10])));
-            *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
-            *rc = rect;
-            f.valid[i] = pr.valid ? 1 : 0;
-            f.kept[i] = kept;
-            f.keep_bits[i] = bits;
-            if (kept > 0)  // binning buckets
-                count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
-                                 ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
-                                 f.tiles_x);
+            float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+            float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
+            int4 *rc = reinterpret_cast<int4 *>(f.rect) + i;
+            // near-plane test (R/gaussians.py:188-191)
+            const float zf = (pk[0] * cam.rot_cw[6] + pk[1] * cam.rot_cw[7] + pk[2] * cam.rot_cw[8]) + cam.trans_cw[2];
+            if (!(zf > GS_NEAR_CLIP)) {
+                s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                s2[1] = make_float4(0.f, 0.f, zf, 0.f);
+                s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                *cv = make_float4(0.f, 0.f, 0.f, -1.f);
+                *rc = make_int4(0, -1, 0, -1);
+                f.valid[i] = 0;
+                f.kept[i] = 0;
+            } else {
+                // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians
+                // near the 0.01 m clip plane, and fp32 would shift their whole footprint
+                ProjectedT<double> pd;
+                project_full<double>(pk, cam, pd);
+                Projected pr;
+                pr.mu[2] = (float)pd.mu[2];
+                pr.mx = (float)pd.mx;
+                pr.my = (float)pd.my;
+                pr.c00 = (float)pd.c00;
+                pr.c01 = (float)pd.c01;
+                pr.c11 = (float)pd.c11;
+                pr.ca = (float)pd.ca;
+                pr.cb = (float)pd.cb;
+                pr.cc = (float)pd.cc;
+                pr.valid = pd.valid;
+                const float op = 1.0f / (1.0f + expf(-pk[10]));
+                // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
+                const float u0 = pk[0] - cam.center[0], u1 = pk[1] - cam.center[1], u2 = pk[2] - cam.center[2];
+                float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
+                if (un < 1e-12f) un = 1.0f;
+                float b[16];
+                sh_basis(u0 / un, u1 / un, u2 / un, b);
+                float acc[3] = {b[1] * pk[14], b[1] * pk[15], 0.0f};
+#pragma unroll
+                for (int c = 4; c < 15; c++) {  // sh_high floats 16..58 streamed as float4 chunks
+                    const float4 v = pp_chunk(bt, lane, c);
+                    const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const int fi = 4 * c + e - 14;  // sh_high flat index (k * 3 + channel)
+                        if (fi < 45) acc[fi % 3] += b[fi / 3 + 1] * e4[e];
+                    }
+                }
+                float col[3];
+#pragma unroll
+                for (int c = 0; c < 3; c++) {
+                    const float pre = b[0] * pk[11 + c] + acc[c] + 0.5f;
+                    col[c] = pre > 0.0f ? pre : 0.0f;
+                }
+                int4 rect = make_int4(0, -1, 0, -1);
+                float qcut = 0.0f, radius = -1.0f;
+                const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width,
+                                                          f.height, f.tiles_x, f.tiles_y, rect, qcut, radius);
+                if (!active) rect = make_int4(0, -1, 0, -1);
+                // exact per-tile cull of the rectangle (R/rasterizer.py:150-166), fused here for
+                // small footprints; large ones by the big_* kernels (band / tile bounds, exact rows)
+                const int ncand = (rect.y - rect.x + 1) * (rect.w - rect.z + 1);
+                big = active && ncand > GS_SMALL_CAND;
+                uint64_t bits = 0ull;
+                const int kept = (active && !big) ? cull_rect(pr.mx, pr.my, pr.ca, pr.cb, pr.cc, qcut, rect, f.width,
+                                                              f.height, bits)
+                                                  : 0;
+                touched = kept > 0;
+                s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
+                s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
+                // 1 - opacity = sigmoid(-logit), kept exact for the blend's 1 - alpha
+                s2[2] = make_float4(col[0], col[1], col[2], 1.0f / (1.0f + expf(pk[10])));
+                *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
+                *rc = rect;
+                f.valid[i] = pr.valid ? 1 : 0;
+                f.kept[i] = kept;
+                f.keep_bits[i] = bits;
+                if (kept > 0)  // binning buckets
+                    count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
+                                     ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
+                                     f.tiles_x);
+            }
+            f.touched[i] = touched ? 1 : 0;
         }
-        f.touched[i] = touched ? 1 : 0;
+        warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+        warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
+        __syncwarp();  // the buffer is refilled two batches on
     }
-    warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
-    warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
 }
 
 // Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), same decision
@@ -708,9 +738,8 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
     cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
-    int64_t warps = (f->n + 31) / 32;
-    int blocks = (int)((warps + PP_WARPS - 1) / PP_WARPS);
-    preprocess_kernel<<<blocks, PP_THREADS, 0, (cudaStream_t)stream>>>(*f, params, view);
+    preprocess_kernel<<<3 * 148, PP_THREADS, PP_WARPS * 2 * sizeof(PPBatch), (cudaStream_t)stream>>>(*f, params,
+                                                                                                     view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
     int tb = 0, rb = 0;
@@ -766,3 +795,10 @@ extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_
     lidar_write_kernel<<<chunks, LC_CHUNK, 0, (cudaStream_t)stream>>>(sparse_depth, npx, scratch, idx, z, k_out);
     return check_launch("lidar_write_kernel");
 }
+
+namespace gs {
+void init_preprocess_attrs() {
+    cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(PP_WARPS * 2 * sizeof(PPBatch)));
+}
+}  // namespace gs
