@@ -27,9 +27,22 @@ __device__ __forceinline__ float quad(float ca, float cb, float cc, float dx, fl
 // with one rounding (FMA) and is exactly 0.01 on the clamp, so the transmittance product does
 // not pick up the cancellation of 1 - 0.99f.  (omo = 1 - o is carried in the splat record for
 // the higher-accuracy variant 1 - o e = (1 - e) + (1 - o) e.)
+// MUFU ex2 / rcp without the IEEE range and rounding fix-ups (relative error ~2^-22; results
+// below 2^-126 flush to 0, i.e. alpha < 1e-38): the blend and its adjoint use the same alpha.
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &araw, float &alpha, float &oma) {
     (void)omo;
-    const float e = exp2f(-0.5f * GS_LOG2E * q);
+    const float e = fast_ex2(-0.5f * GS_LOG2E * q);
     araw = op * e;
     if (araw > GS_ALPHA_CLAMP) {
         alpha = GS_ALPHA_CLAMP;
@@ -298,12 +311,12 @@ struct BwdPixel {
 __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const float4 &B, const float4 &C, float v[10]) {
     const float dx = p.fx - A.x, dy = p.fy - A.y;
     const float ca = A.z, cb = A.w, cc = B.x, op = B.y, dep = B.z;
-    const float e = exp2f(NEG_HALF_LOG2E * quad(ca, cb, cc, dx, dy));
+    const float e = fast_ex2(NEG_HALF_LOG2E * quad(ca, cb, cc, dx, dy));
     const float araw = op * e;
     const bool clamped = araw > GS_ALPHA_CLAMP;
     const float alpha = clamped ? GS_ALPHA_CLAMP : araw;
     const float om = clamped ? 0.01f : fmaf(-op, e, 1.0f);
-    const float rom = __frcp_rn(om);
+    const float rom = fast_rcp(om);
     const float Tb = p.T * rom;
     const float w = alpha * Tb;
     v[6] += w * p.gc0;
