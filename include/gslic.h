@@ -15,6 +15,7 @@
  *                   R/rasterizer.py:707-725 sparse_adam_step
  *   gs_chain        _chain_to_attributes only, accumulating parameter-row gradients
  *                   (multi-view / multi-GPU batches; followed by an allreduce + gs_adam)
+ *   gs_chain_pose   _chain_to_attributes(with_pose=True) R/rasterizer.py:646-657
  *   gs_adam         sparse_adam_step on parameter-row gradients + a touched mask
  *
  * Conventions
@@ -165,6 +166,11 @@ int gs_version(void);
 /* R/gaussians.py:180-215 + R/rasterizer.py:445-452: projection, EWA covariance, SH colour,
  * opacity sigmoid, influence radius, tile rectangle and cut; also resets touched[]. */
 int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream);
+/* flags = GS_PP_LAZY_SH (the iteration engine): SH colours only for the Gaussians that can be
+ * blended (kept in >= 1 tile, or large footprints still to be culled); the others' colour slots
+ * are left 0 and their SH columns are never read.  gs_preprocess(...) = gs_preprocess_ex(..., 0). */
+#define GS_PP_LAZY_SH 1
+int gs_preprocess_ex(const gs_frame *f, const float *params, const gs_view *view, int32_t flags, void *stream);
 
 /* R/rasterizer.py:169-219: depth sort of active Gaussians, exact per-tile cull, (tile|depth)
  * ordered entries, tile ranges, touched mask + list; zeroes touched g2d rows.
@@ -196,6 +202,13 @@ int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, float *adam_v
  * touched_accum[i] |= touched[i]. */
 int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum, const gs_view *view,
              void *stream);
+
+/* backward(with_pose=True) (R/rasterizer.py:543-556, pose part :646-657): as gs_chain, plus the
+ * 6-dof pose gradient (rho, theta) on the left tangent of T_cw, written to pose[6] (device FP64,
+ * overwritten).  grads and touched_accum both NULL: the pose gradient only (the tracker's
+ * photometric_refine, R/odometry.py:305-336). */
+int gs_chain_pose(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum,
+                  const gs_view *view, double *pose, void *stream);
 
 /* R/rasterizer.py:707-725 over a dense touched mask (n entries) and gradient rows. */
 int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,

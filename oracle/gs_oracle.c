@@ -690,8 +690,16 @@ static void quat_partials(const double q0[4], double dR[4][9]) {
 }
 
 /* grads (n, 59) rows; only touched rows are written, others zeroed. */
+/* pose_parts (nullable, n x 6): per-Gaussian terms of the 6-dof pose gradient (rho, theta) on
+ * the left tangent of T_cw (R/rasterizer.py:646-657); the caller sums them over touched ids. */
+void or_chain_pose(int64_t n, const double *params, const or_camera *cam, const double *g2d,
+                   const uint8_t *touched, double *grads, double *pose_parts);
 void or_chain(int64_t n, const double *params, const or_camera *cam, const double *g2d, const uint8_t *touched,
               double *grads) {
+    or_chain_pose(n, params, cam, g2d, touched, grads, NULL);
+}
+void or_chain_pose(int64_t n, const double *params, const or_camera *cam, const double *g2d,
+                   const uint8_t *touched, double *grads, double *pose_parts) {
     const double *Rc = cam->rot_cw, *tc = cam->trans_cw;
     double fx = cam->fx, fy = cam->fy;
     double Cc[3];
@@ -700,6 +708,7 @@ void or_chain(int64_t n, const double *params, const or_camera *cam, const doubl
     for (int64_t i = 0; i < n; i++) {
         double *G = grads + (size_t)NP * i;
         memset(G, 0, sizeof(double) * NP);
+        if (pose_parts) memset(pose_parts + (size_t)6 * i, 0, sizeof(double) * 6);
         if (!touched[i]) continue;
         const double *p = params + (size_t)NP * i;
         const double *g = g2d + 10 * i;
@@ -814,7 +823,31 @@ void or_chain(int64_t n, const double *params, const or_camera *cam, const doubl
             for (int dd = 0; dd < 3; dd++) gdir[dd] += bg[k][dd] * sc;
         }
         double gd = gdir[0] * d[0] + gdir[1] * d[1] + gdir[2] * d[2];
-        for (int c = 0; c < 3; c++) G[c] += (gdir[c] - d[c] * gd) / un;
+        double gu[3];
+        for (int c = 0; c < 3; c++) {
+            gu[c] = (gdir[c] - d[c] * gd) / un;
+            G[c] += gu[c];
+        }
+        if (pose_parts) {
+            /* :647-657 -- translation: g_mu_cam + R_cw gu (the view-direction path);
+             * rotation: mu_cam x g_mu_cam + the covariance path through M = J R_cw with
+             * X = (J^T gM) R_cw^T, theta += (X21 - X12, X02 - X20, X10 - X01) */
+            double *P6 = pose_parts + (size_t)6 * i;
+            const double gmu[3] = {gx, gy, gz};
+            for (int r = 0; r < 3; r++) P6[r] = gmu[r] + (Rc[3 * r] * gu[0] + Rc[3 * r + 1] * gu[1] + Rc[3 * r + 2] * gu[2]);
+            P6[3] = mu[1] * gz - mu[2] * gy;
+            P6[4] = mu[2] * gx - mu[0] * gz;
+            P6[5] = mu[0] * gy - mu[1] * gx;
+            double grc[9], X[9];
+            for (int a = 0; a < 3; a++)
+                for (int b = 0; b < 3; b++) grc[3 * a + b] = J[a] * gM[b] + J[3 + a] * gM[3 + b];
+            for (int a = 0; a < 3; a++)
+                for (int k = 0; k < 3; k++)
+                    X[3 * a + k] = grc[3 * a] * Rc[3 * k] + grc[3 * a + 1] * Rc[3 * k + 1] + grc[3 * a + 2] * Rc[3 * k + 2];
+            P6[3] += X[7] - X[5];
+            P6[4] += X[2] - X[6];
+            P6[5] += X[3] - X[1];
+        }
     }
 }
 

@@ -21,6 +21,7 @@ GS_G2D = 12
 CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3, 4
 GS_CNT_SLOTS = 16
 GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists materialised on demand)
+GS_PP_LAZY_SH = 1  # gs_preprocess_ex flag of the iteration engine (colours only where blended)
 
 P = ctypes.c_void_p
 i32 = ctypes.c_int32
@@ -72,12 +73,14 @@ def lib():
         "gs_last_error": (ctypes.c_char_p, []),
         "gs_version": (ctypes.c_int, []),
         "gs_preprocess": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P]),
+        "gs_preprocess_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, i32, P]),
         "gs_bin": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_render_fwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_loss": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, P]),
         "gs_render_bwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), P]),
         "gs_chain_adam": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P]),
         "gs_chain": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P]),
+        "gs_chain_pose": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P]),
         "gs_adam": (ctypes.c_int, [P, P, P, P, P, P, i64, P, P]),
         "gs_lidar_compact": (ctypes.c_int, [P, i32, i32, P, P, P, P]),
         "gs_project": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, P, P]),
@@ -93,8 +96,8 @@ def lib():
 
 
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
-            "gs_preprocess", "gs_bin", "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_chain_adam",
-            "gs_chain", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats"]
+            "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_chain_adam",
+            "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats"]
 
 
 def check(rc: int, what: str) -> None:

@@ -42,8 +42,11 @@ __device__ __forceinline__ void quat_grad(const float q0[4], const T gR[9], floa
 }
 
 // gradient of the scalar loss w.r.t. one parameter row (59 columns written to G; every write
-// happens after the last read of p, so G may alias p)
-__device__ __forceinline__ void chain_row(const float *p, const double *g, const gs_camera &cam, float *G) {
+// happens after the last read of p, so G may alias p).  POSE: also this Gaussian's terms of the
+// 6-dof pose gradient (rho, theta) on the left tangent of T_cw (R/rasterizer.py:646-657).
+template <bool POSE>
+__device__ __forceinline__ void chain_row(const float *p, const double *g, const gs_camera &cam, float *G,
+                                          double *pose6) {
     // geometric chain in FP64: for Gaussians just past the 0.01 m near plane, J ~ fx/z ~ 1e5 and
     // the products below lose several fp32 digits; B200's FP64 pipe makes this nearly free here
     using D = double;
@@ -140,6 +143,29 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
     float gd[3];
     sh_basis_vjp(d0, d1, d2, sk, gd);
     const float dot = gd[0] * d0 + gd[1] * d1 + gd[2] * d2;
+    const float gu[3] = {(gd[0] - d0 * dot) / un, (gd[1] - d1 * dot) / un, (gd[2] - d2 * dot) / un};
+    if (POSE) {
+        // translation: g_mu_cam + R_cw gu (the camera centre moves with rho, :656); rotation:
+        // mu_cam x g_mu_cam + the covariance path through M = J R_cw: X = (J^T gM) R_cw^T,
+        // theta += (X21 - X12, X02 - X20, X10 - X01) (:648-655)
+        const D gmu[3] = {gx, gy, gz};
+#pragma unroll
+        for (int r = 0; r < 3; r++) pose6[r] = gmu[r] + (Rc[3 * r] * gu[0] + Rc[3 * r + 1] * gu[1] + Rc[3 * r + 2] * gu[2]);
+        pose6[3] = pr.mu[1] * gz - pr.mu[2] * gy;
+        pose6[4] = pr.mu[2] * gx - pr.mu[0] * gz;
+        pose6[5] = pr.mu[0] * gy - pr.mu[1] * gx;
+        D grc[9];
+#pragma unroll
+        for (int a = 0; a < 3; a++)
+#pragma unroll
+            for (int b = 0; b < 3; b++) grc[3 * a + b] = pr.J[a] * gM[b] + pr.J[3 + a] * gM[3 + b];
+        auto X = [&](int a, int k) {
+            return grc[3 * a] * Rc[3 * k] + grc[3 * a + 1] * Rc[3 * k + 1] + grc[3 * a + 2] * Rc[3 * k + 2];
+        };
+        pose6[3] += X(2, 1) - X(1, 2);
+        pose6[4] += X(0, 2) - X(2, 0);
+        pose6[5] += X(1, 0) - X(0, 1);
+    }
     // every read of p is done: G may alias p from here on
 #pragma unroll
     for (int c = 0; c < 3; c++) G[11 + c] = bs[0] * gcol[c];
@@ -147,9 +173,9 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
     for (int k = 0; k < 15; k++)
 #pragma unroll
         for (int c = 0; c < 3; c++) G[14 + 3 * k + c] = bs[k + 1] * gcol[c];
-    G[0] = gpos[0] + (gd[0] - d0 * dot) / un;
-    G[1] = gpos[1] + (gd[1] - d1 * dot) / un;
-    G[2] = gpos[2] + (gd[2] - d2 * dot) / un;
+    G[0] = gpos[0] + gu[0];
+    G[1] = gpos[1] + gu[1];
+    G[2] = gpos[2] + gu[2];
 #pragma unroll
     for (int j = 0; j < 3; j++) G[3 + j] = gls[j];
 #pragma unroll
@@ -169,11 +195,15 @@ __device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, 
 }
 
 // mode 0: fused Adam on params/m/v/t.  mode 1: grads[row] += G, touched_accum[row] = 1.
+// mode 2: compact gradient rows + bias corrections for adam_list_kernel.  mode 3: nothing but the
+// pose gradient (tracking).  POSE: pose6 (FP64, 6) += the pose gradient of the touched Gaussians.
+template <bool POSE>
 __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__restrict__ params,
                                                            float *__restrict__ am, float *__restrict__ av,
                                                            int32_t *__restrict__ at, const gs_view *__restrict__ view,
                                                            const float *__restrict__ lr_cols, int mode,
-                                                           float *__restrict__ grads, uint8_t *__restrict__ touched_accum) {
+                                                           float *__restrict__ grads, uint8_t *__restrict__ touched_accum,
+                                                           double *__restrict__ pose_out) {
     // one 32 x 65 staging tile per warp: parameter rows in, gradient rows out (in place)
     __shared__ float srow[CA_WARPS][32][RP];
     __shared__ float sbc[CA_WARPS][32][2];
@@ -201,13 +231,14 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         }
     }
     __syncwarp();
+    double pose6[6] = {0, 0, 0, 0, 0, 0};
     if (g >= 0) {
         double2 *g2 = reinterpret_cast<double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
         const double2 a = g2[0], b = g2[1], c = g2[2], d = g2[3], e = g2[4];
-        if (mode == 1 && f.counters[GS_CNT_LAZY])  // batches: keep the row zero for the next view
+        if ((mode == 1 || mode == 3) && f.counters[GS_CNT_LAZY])  // keep the row zero for the next view
             for (int q = 0; q < GS_G2D / 2; q++) g2[q] = make_double2(0.0, 0.0);
         const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
-        chain_row(srow[warp][lane], gv, scam, sgr[warp][lane]);
+        chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {
             const int tn = at[g] + 1;
@@ -218,9 +249,20 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
             sbc[warp][lane][0] = bc1;
             sbc[warp][lane][1] = bc2;
             if (mode == 2) reinterpret_cast<float2 *>(f.bias_corr)[k] = make_float2(bc1, bc2);
-        } else {
+        } else if (mode == 1) {
             touched_accum[g] = 1;
         }
+    }
+    if (POSE) {
+        // warp butterfly, then one FP64 atomic per component per warp
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+            double v = pose6[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) atomicAdd(pose_out + q, v);
+        }
+        if (mode == 3) return;
     }
     __syncwarp();
     if (mode == 2) {  // gradient rows in touched-list order, streamed by adam_list_kernel
@@ -342,11 +384,16 @@ __global__ void adam_step_kernel(int32_t *__restrict__ at, const uint8_t *__rest
 using namespace gs;
 
 static int launch_chain(const gs_frame *f, float *params, float *m, float *v, int32_t *t, const gs_view *view,
-                        const float *lr, int mode, float *grads, uint8_t *acc, void *stream) {
+                        const float *lr, int mode, float *grads, uint8_t *acc, void *stream, double *pose = nullptr) {
     if (f->n == 0) return GS_OK;
     const int64_t warps = (f->n + 31) / 32;
     const unsigned blocks = (unsigned)((warps + CA_WARPS - 1) / CA_WARPS);
-    chain_kernel<<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads, acc);
+    if (pose)
+        chain_kernel<true><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
+                                                                            acc, pose);
+    else
+        chain_kernel<false><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
+                                                                             acc, nullptr);
     return check_launch("chain_kernel");
 }
 
@@ -375,6 +422,21 @@ extern "C" int gs_chain(const gs_frame *f, const float *params, float *grads, ui
                         touched_accum, stream);
 }
 
+extern "C" int gs_chain_pose(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum,
+                             const gs_view *view, double *pose, void *stream) {
+    if (!params || !view || !pose || (!grads) != (!touched_accum)) {
+        set_error("gs_chain_pose: null argument (grads and touched_accum are both set or both NULL)");
+        return GS_ERR_ARG;
+    }
+    cudaError_t e = cudaMemsetAsync(pose, 0, 6 * sizeof(double), (cudaStream_t)stream);
+    if (e != cudaSuccess) {
+        set_error("gs_chain_pose: %s", cudaGetErrorString(e));
+        return GS_ERR_CUDA;
+    }
+    return launch_chain(f, const_cast<float *>(params), nullptr, nullptr, nullptr, view, nullptr, grads ? 1 : 3, grads,
+                        touched_accum, stream, pose);
+}
+
 extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,
                        const uint8_t *touched, int64_t n, const float *lr_cols, void *stream) {
     if (n == 0) return GS_OK;
@@ -390,6 +452,7 @@ extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *ada
 namespace gs {
 void init_chain_attrs() {
     // static shared memory only (33 KB per 4-warp CTA); nothing to opt in
-    cudaFuncSetAttribute(chain_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(chain_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(chain_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 }  // namespace gs

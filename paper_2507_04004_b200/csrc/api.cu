@@ -85,8 +85,9 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.big_slot = c.take<int32_t>(nn);
     f.cull_queue_cap = nn > (1 << 20) ? nn : (1 << 20);
     f.cull_queue = c.take<int32_t>(2 * f.cull_queue_cap);
-    // huge records (8 ints each), their ids and 64-bit keys, in depth order
-    f.huge = c.take<int32_t>(11 * GS_HUGE_CAP);
+    // huge records (8 ints each), their ids and 64-bit keys in depth order, then the unsorted
+    // staged keys
+    f.huge = c.take<int32_t>(13 * GS_HUGE_CAP);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
     f.huge_mask_t = c.take<uint32_t>((int64_t)GS_HUGE_CAP * (((int64_t)tx * ty + 31) / 32));
     f.tile_scratch = c.take<int32_t>(5 * ((int64_t)tx * ty + 1));

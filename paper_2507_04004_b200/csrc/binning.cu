@@ -8,7 +8,7 @@
 //   1. per-tile counts of the kept pairs of the non-screen-covering Gaussians, taken where the
 //      cull decides them (preprocess_kernel, big_finish_kernel; bucket_count for cull=False);
 //   2. huge_sort: the screen-covering ("huge") Gaussians, already binned per tile by bitmap,
-//      are sorted by key in one CTA (records in depth order);
+//      are rank-sorted by key (records in depth order);
 //   3. huge_transpose: their per-tile masks in that order, per-tile counts;
 //   4. tile_scan: tile ranges (bucket + huge counts), bucket offsets, E;
 //   5. bucket_fill: every kept pair's key lands in its tile's bucket (atomic cursors);
@@ -74,39 +74,42 @@ __global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f) {
         f.tile_scratch[t] = (int32_t)nt;
 }
 
-// 2) the huge Gaussians with >= 1 kept tile, sorted by key in one CTA: records in depth order
-constexpr int HS_THREADS = 1024;
+// 2) the huge Gaussians with >= 1 kept tile, in key order: a rank sort spread over the GPU.  Keys
+// are unique (the id is in the low word), so a key's rank -- the number of smaller keys -- is its
+// slot.  CTA c ranks keys [HS_KEYS c, HS_KEYS (c+1)): its HS_GROUPS thread groups each count
+// over one slice of all keys (staged in shared memory), the partial counts are summed in shared
+// memory and every record is written straight to its slot.  No atomics, no global sync.
+constexpr int HS_KEYS = 64;
+constexpr int HS_GROUPS = 16;
+constexpr int HS_THREADS = HS_KEYS * HS_GROUPS;
 
 __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
     __shared__ uint64_t s_key[GS_HUGE_CAP];
-    // the keys were staged (unordered) by big_finish_kernel
-    uint64_t *keys = reinterpret_cast<uint64_t *>(f.huge + HKEYS);
+    __shared__ int s_part[HS_GROUPS][HS_KEYS];
     const int nh = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
-    for (int i = threadIdx.x; i < nh; i += HS_THREADS) s_key[i] = keys[i];
-    int np = 1;
-    while (np < nh) np <<= 1;
-    for (int i = nh + threadIdx.x; i < np; i += HS_THREADS) s_key[i] = ~0ull;
+    const int i0 = blockIdx.x * HS_KEYS;
+    if (i0 >= nh) return;
+    const uint64_t *staged = reinterpret_cast<const uint64_t *>(f.huge + HSTAGE);
+    for (int i = threadIdx.x; i < nh; i += HS_THREADS) s_key[i] = staged[i];
     __syncthreads();
-    for (int k = 2; k <= np; k <<= 1)
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < np; i += HS_THREADS) {
-                const int l = i ^ j;
-                if (l > i) {
-                    const uint64_t a = s_key[i], c = s_key[l];
-                    if ((a > c) == ((i & k) == 0)) {
-                        s_key[i] = c;
-                        s_key[l] = a;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    for (int i = threadIdx.x; i < nh; i += HS_THREADS) {
-        const uint64_t key = s_key[i];
-        const int g = (int)(uint32_t)key;
-        reinterpret_cast<int4 *>(f.huge + HREC * i)[0] = make_int4(g, (int)(key >> 32), -f.kept[g] - 1, 0);
-        f.huge[HIDS + i] = g;
-        keys[i] = key;
+    const int k = threadIdx.x % HS_KEYS, grp = threadIdx.x / HS_KEYS;
+    const int i = i0 + k;
+    const uint64_t mine = i < nh ? s_key[i] : 0ull;
+    const int per = (nh + HS_GROUPS - 1) / HS_GROUPS;
+    const int j0 = grp * per, j1 = min(nh, j0 + per);
+    int cnt = 0;
+#pragma unroll 8
+    for (int j = j0; j < j1; j++) cnt += s_key[j] < mine;  // same j across the warp: broadcast
+    s_part[grp][k] = cnt;
+    __syncthreads();
+    if (grp == 0 && i < nh) {
+        int rank = 0;
+#pragma unroll
+        for (int q = 0; q < HS_GROUPS; q++) rank += s_part[q][k];
+        const int g = (int)(uint32_t)mine;
+        reinterpret_cast<int4 *>(f.huge + HREC * rank)[0] = make_int4(g, (int)(mine >> 32), -f.kept[g] - 1, 0);
+        f.huge[HIDS + rank] = g;
+        reinterpret_cast<uint64_t *>(f.huge + HKEYS)[rank] = mine;
     }
 }
 
@@ -306,7 +309,7 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         if ((rc = check_launch("bucket_count_kernel"))) return rc;
     }
     if (cull) {  // the bucket counts come from the cull (preprocess, big_finish)
-        huge_sort_kernel<<<1, HS_THREADS, 0, st>>>(*f);
+        huge_sort_kernel<<<GS_HUGE_CAP / HS_KEYS, HS_THREADS, 0, st>>>(*f);
         if ((rc = check_launch("huge_sort_kernel"))) return rc;
         huge_transpose_kernel<<<dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st>>>(*f);
         if ((rc = check_launch("huge_transpose_kernel"))) return rc;

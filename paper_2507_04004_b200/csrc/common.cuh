@@ -17,6 +17,12 @@
 
 namespace gs {
 
+// huge records (depth order): 8 ints each (id, depth bits, slot), then their ids, then their keys
+constexpr int HREC = 8;
+constexpr int HIDS = HREC * GS_HUGE_CAP;
+constexpr int HKEYS = HIDS + GS_HUGE_CAP;  // int offset of the uint64 key array (8-B aligned)
+constexpr int HSTAGE = HKEYS + 2 * GS_HUGE_CAP;  // unsorted keys staged by big_finish_kernel
+
 // ---------------------------------------------------------------------------
 // error plumbing (thread-local, no global mutable state shared across threads)
 void set_error(const char *fmt, ...);

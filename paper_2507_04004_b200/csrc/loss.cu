@@ -387,22 +387,41 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
     }
 }
 
-__global__ void loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
+constexpr int LF_THREADS = 1024;
+static_assert(LF_THREADS % 3 == 1, "component bookkeeping of loss_finalize_kernel");
+
+__global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
                                      float xi, float *tab_stamp) {
-    __shared__ double r[3][256];
-    double a = 0.0, b = 0.0, c = 0.0;
-    for (int64_t k = threadIdx.x; k < nparts; k += blockDim.x) {
-        a += f.loss_parts[3 * k];
-        b += f.loss_parts[3 * k + 1];
-        c += f.loss_parts[3 * k + 2];
+    // 1024 threads, coalesced over the flat (nparts x 3) array with 4 loads in flight each, then
+    // a fixed-order shuffle tree: deterministic, and latency-bound only ~2 round trips deep
+    __shared__ double r[3][32];
+    const int64_t total = 3 * nparts;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int64_t stride = LF_THREADS * 3;  // every thread keeps one component
+    const int comp0 = threadIdx.x % 3;
+    // thread t reads elements t, t + 3072, ...: element e is component e % 3, and 3072 % 3 == 0
+#pragma unroll 4
+    for (int64_t e = threadIdx.x; e < total; e += stride) {
+        acc[0] += f.loss_parts[e];
+        if (e + LF_THREADS < total) acc[1] += f.loss_parts[e + LF_THREADS];
+        if (e + 2 * LF_THREADS < total) acc[2] += f.loss_parts[e + 2 * LF_THREADS];
     }
-    r[0][threadIdx.x] = a;
-    r[1][threadIdx.x] = b;
-    r[2][threadIdx.x] = c;
+    // acc[j] holds component (comp0 + j * (LF_THREADS % 3)) % 3 -- LF_THREADS % 3 == 1
+    double comp[3];
+#pragma unroll
+    for (int j = 0; j < 3; j++) comp[(comp0 + j) % 3] = acc[j];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        double v = comp[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) r[q][warp] = v;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         double l1 = 0.0, ss = 0.0, dd = 0.0;
-        for (int k = 0; k < 256; k++) {
+        for (int k = 0; k < LF_THREADS / 32; k++) {
             l1 += r[0][k];
             ss += r[1][k];
             dd += r[2][k];
@@ -454,7 +473,7 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     depth_loss_kernel<<<DEPTH_BLOCKS, 256, 0, st>>>(*f, view, xi, ssim_blocks);
     if ((rc = check_launch("depth_loss_kernel"))) return rc;
-    loss_finalize_kernel<<<1, 256, 0, st>>>(*f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
+    loss_finalize_kernel<<<1, LF_THREADS, 0, st>>>(*f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
     return check_launch("loss_finalize_kernel");
 }
 

@@ -2,9 +2,9 @@
 //
 // R/gaussians.py:180-215 (project), R/rasterizer.py:445-452 (sigmoid, camera->Gaussian view
 // directions, eval_sh R/gaussians.py:102-111), R/rasterizer.py:84-102 + 183-194 (influence
-// radius and tile rectangle).  One thread per Gaussian; each warp stages its 32 parameter
-// rows (256 B each) through shared memory with coalesced float4 loads, skipping the SH
-// columns of Gaussians behind the near plane.
+// radius and tile rectangle).  One thread per Gaussian; each warp stages the geometry of its 32
+// parameter rows through shared memory with coalesced cp.async, and the SH columns only of the
+// Gaussians that need a colour.
 #include "common.cuh"
 
 namespace gs {
@@ -19,60 +19,108 @@ __device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void pp_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void pp_cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// A warp's batch of 32 parameter rows in shared memory: 16-B chunk c of row r sits at chunk
-// c ^ (r & 7), so the 8 lanes of each 128-bit shared wavefront (one row each, same logical
-// chunk) hit distinct banks.
-struct PPBatch {
-    float4 row[32][16];
+// Per warp, batches of 32 Gaussians flow through a three-stage software pipeline:
+//   A  the geometry chunks (floats 0-15 of each row: pos, log_scale, quat, opacity logit,
+//      sh_low, sh_high[0]) of batch b+1 stream in (cp.async) while batch b is projected,
+//      its radius / rectangle computed and its small footprints culled;
+//   SH the remaining 176 B of a row (sh_high[0..14], floats 16-58) are fetched only for the
+//      Gaussians that need a colour, issued once batch b's geometry is known, and consumed one
+//      iteration later (colour of batch b-1), so the fetch latency hides behind batch b+1.
+// Which Gaussians need a colour: every one in front of the camera for the reference-shaped API
+// (ctx["colors"], R/rasterizer.py:452); only those that can be blended -- kept in >= 1 tile, or
+// large footprints still to be culled -- for the iteration engine (GS_PP_LAZY_SH).  The
+// engine's parameter reads fall from 256 B to ~64 B for the Gaussians that are not drawn.
+struct PPGeom {  // chunk c of row r at c ^ ((r >> 1) & 3): 8 consecutive rows hit distinct banks
+    float4 row[32][4];
+};
+struct PPSh {  // 11 chunks per row, 176-B row stride (conflict-free without a swizzle)
+    float4 row[32][11];
+};
+struct PPWarp {
+    PPGeom geom[3];
+    PPSh sh;
 };
 
-__device__ __forceinline__ float4 pp_chunk(const PPBatch &bt, int r, int c) { return bt.row[r][c ^ (r & 7)]; }
+__device__ __forceinline__ float4 pp_geom(const PPGeom &g, int r, int c) { return g.row[r][c ^ ((r >> 1) & 3)]; }
+__device__ __forceinline__ void pp_cp_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-// Persistent warps over batches of 32 Gaussians, double-buffered: the next batch's rows stream
-// in (cp.async) while the current one is projected, shaded and culled.
+// colour of one Gaussian (R/rasterizer.py:447-452, eval_sh R/gaussians.py:102-111) from its
+// geometry chunks and its staged sh_high chunks
+__device__ __forceinline__ float3 pp_colour(const PPGeom &g, const PPSh &sh, int r, const gs_camera &cam) {
+    const float4 c0 = pp_geom(g, r, 0), c2 = pp_geom(g, r, 2), c3 = pp_geom(g, r, 3);
+    const float u0 = c0.x - cam.center[0], u1 = c0.y - cam.center[1], u2 = c0.z - cam.center[2];
+    float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
+    if (un < 1e-12f) un = 1.0f;
+    float b[16];
+    sh_basis(u0 / un, u1 / un, u2 / un, b);
+    // floats 11-15: sh_low 0-2 (c2.w, c3.x, c3.y), sh_high[0] (c3.z, c3.w)
+    float acc[3] = {b[1] * c3.z, b[1] * c3.w, 0.0f};
+#pragma unroll
+    for (int c = 4; c < 15; c++) {  // sh_high floats 16..58
+        const float4 v = sh.row[r][c - 4];
+        const float e4[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; e++) {
+            const int fi = 4 * c + e - 14;  // sh_high flat index (k * 3 + channel)
+            if (fi < 45) acc[fi % 3] += b[fi / 3 + 1] * e4[e];
+        }
+    }
+    const float low[3] = {c2.w, c3.x, c3.y};
+    float col[3];
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const float pre = b[0] * low[c] + acc[c] + 0.5f;
+        col[c] = pre > 0.0f ? pre : 0.0f;
+    }
+    return make_float3(col[0], col[1], col[2]);
+}
+
+// Persistent warps over batches of 32 Gaussians (pipeline above).
+template <bool LAZY_SH>
 __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, const float *__restrict__ params,
                                                                 const gs_view *__restrict__ view) {
     extern __shared__ float4 pp_raw[];
-    PPBatch(*bufs)[2] = reinterpret_cast<PPBatch(*)[2]>(pp_raw);
+    PPWarp *ws_all = reinterpret_cast<PPWarp *>(pp_raw);
     __shared__ gs_camera scam;
     if (threadIdx.x == 0) scam = view->cam;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    PPBatch *buf = bufs[warp];
+    PPWarp &W = ws_all[warp];
     const int64_t n = f.n;
     const int64_t nbatch = (n + 31) / 32;
     const int64_t stride = (int64_t)gridDim.x * PP_WARPS;
     const gs_camera &cam = scam;
-    auto issue = [&](int64_t batch, PPBatch &bt) {  // 16 chunks per lane, two rows per instruction
+    auto issue_geom = [&](int64_t batch, PPGeom &g) {  // 4 chunks per row, 8 rows per instruction
         const int64_t base = batch * 32;
 #pragma unroll
-        for (int j = 0; j < 16; j++) {
-            const int r = 2 * j + (lane >> 4), c = lane & 15;
-            if (base + r < n) pp_cp_async16(&bt.row[r][c ^ (r & 7)], params + (base + r) * GS_ROW + 4 * c);
+        for (int j = 0; j < 4; j++) {
+            const int r = 8 * j + (lane >> 2), c = lane & 3;
+            if (base + r < n) pp_cp_async16(&g.row[r][c ^ ((r >> 1) & 3)], params + (base + r) * GS_ROW + 4 * c);
         }
         pp_cp_commit();
     };
     int64_t batch = (int64_t)blockIdx.x * PP_WARPS + warp;
-    if (batch < nbatch) issue(batch, buf[0]);
-    for (int cur = 0; batch < nbatch; batch += stride, cur ^= 1) {
-        if (batch + stride < nbatch) issue(batch + stride, buf[cur ^ 1]);
-        else pp_cp_commit();  // empty group: the wait below still means "this batch landed"
-        pp_cp_wait_1();
+    if (batch < nbatch) issue_geom(batch, W.geom[0]);
+    pp_cp_commit();  // (empty) SH group of the batch before the first
+    bool prev_need = false;
+    int64_t prev_i = -1;
+    int slot = 0;
+    for (; batch < nbatch; batch += stride, slot = slot == 2 ? 0 : slot + 1) {
+        const int next_slot = slot == 2 ? 0 : slot + 1, prev_slot = slot == 0 ? 2 : slot - 1;
+        if (batch + stride < nbatch) issue_geom(batch + stride, W.geom[next_slot]);
+        else pp_cp_commit();
+        pp_cp_wait_1();  // this batch's geometry and the previous batch's SH chunks have landed
         __syncwarp();
-        const PPBatch &bt = buf[cur];
+        const PPGeom &G = W.geom[slot];
         const int64_t i = batch * 32 + lane;
-        bool touched = false, big = false;
+        bool touched = false, big = false, need = false;
         if (i < n) {
-            // floats 0-15: pos 0-2, log_scale 3-5, quat 6-9, opacity logit 10, sh_low 11-13,
-            // sh_high[0] 14-15 (R/gaussians.py:150-153)
-            float pk[16];
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const float4 v = pp_chunk(bt, lane, c);
-                pk[4 * c] = v.x;
-                pk[4 * c + 1] = v.y;
-                pk[4 * c + 2] = v.z;
-                pk[4 * c + 3] = v.w;
+            float pk[11];
+            {
+                const float4 c0 = pp_geom(G, lane, 0), c1 = pp_geom(G, lane, 1), c2 = pp_geom(G, lane, 2);
+                pk[0] = c0.x; pk[1] = c0.y; pk[2] = c0.z; pk[3] = c0.w;
+                pk[4] = c1.x; pk[5] = c1.y; pk[6] = c1.z; pk[7] = c1.w;
+                pk[8] = c2.x; pk[9] = c2.y; pk[10] = c2.z;
             }
             float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
             float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
@@ -104,29 +152,6 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
                 pr.cc = (float)pd.cc;
                 pr.valid = pd.valid;
                 const float op = 1.0f / (1.0f + expf(-pk[10]));
-                // view direction camera->Gaussian (R/rasterizer.py:447-451) and SH colour
-                const float u0 = pk[0] - cam.center[0], u1 = pk[1] - cam.center[1], u2 = pk[2] - cam.center[2];
-                float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
-                if (un < 1e-12f) un = 1.0f;
-                float b[16];
-                sh_basis(u0 / un, u1 / un, u2 / un, b);
-                float acc[3] = {b[1] * pk[14], b[1] * pk[15], 0.0f};
-#pragma unroll
-                for (int c = 4; c < 15; c++) {  // sh_high floats 16..58 streamed as float4 chunks
-                    const float4 v = pp_chunk(bt, lane, c);
-                    const float e4[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int e = 0; e < 4; e++) {
-                        const int fi = 4 * c + e - 14;  // sh_high flat index (k * 3 + channel)
-                        if (fi < 45) acc[fi % 3] += b[fi / 3 + 1] * e4[e];
-                    }
-                }
-                float col[3];
-#pragma unroll
-                for (int c = 0; c < 3; c++) {
-                    const float pre = b[0] * pk[11 + c] + acc[c] + 0.5f;
-                    col[c] = pre > 0.0f ? pre : 0.0f;
-                }
                 int4 rect = make_int4(0, -1, 0, -1);
                 float qcut = 0.0f, radius = -1.0f;
                 const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width,
@@ -141,10 +166,12 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
                                                               f.height, bits)
                                                   : 0;
                 touched = kept > 0;
+                need = LAZY_SH ? (touched || big) : true;
                 s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
                 s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-                // 1 - opacity = sigmoid(-logit), kept exact for the blend's 1 - alpha
-                s2[2] = make_float4(col[0], col[1], col[2], 1.0f / (1.0f + expf(pk[10])));
+                // the colour (s2[2].xyz) follows one iteration later; 1 - opacity = sigmoid(-logit),
+                // kept exact for the blend's 1 - alpha
+                if (!need) s2[2] = make_float4(0.f, 0.f, 0.f, 1.0f / (1.0f + expf(pk[10])));
                 *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
                 *rc = rect;
                 f.valid[i] = pr.valid ? 1 : 0;
@@ -159,7 +186,29 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
         }
         warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
         warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
-        __syncwarp();  // the buffer is refilled two batches on
+        // colour of the previous batch (its SH chunks landed with this batch's geometry)
+        if (prev_need) {
+            const float3 col = pp_colour(W.geom[prev_slot], W.sh, lane, cam);
+            const float lg = pp_geom(W.geom[prev_slot], lane, 2).z;
+            reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] =
+                make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(lg)));
+        }
+        __syncwarp();  // the SH buffer and the previous geometry slot are free again
+        if (need) {
+            const float *src = params + i * GS_ROW + 16;
+#pragma unroll
+            for (int c = 0; c < 11; c++) pp_cp_async16(&W.sh.row[lane][c], src + 4 * c);
+        }
+        pp_cp_commit();
+        prev_need = need;
+        prev_i = i;
+    }
+    if (prev_need) {  // drain: the last batch's colour
+        pp_cp_wait_0();
+        const int last = slot == 0 ? 2 : slot - 1;
+        const float3 col = pp_colour(W.geom[last], W.sh, lane, cam);
+        const float lg = pp_geom(W.geom[last], lane, 2).z;
+        reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] = make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(lg)));
     }
 }
 
@@ -533,7 +582,7 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                 // stage the depth key for the binning's huge sort (binning.cu, HKEYS)
                 const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
                 if (h < GS_HUGE_CAP)
-                    reinterpret_cast<uint64_t *>(f.huge + 9 * GS_HUGE_CAP)[h] =
+                    reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] =
                         ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
             } else if (t) {  // per-tile bucket counts of the binning (bitmap or exact re-test)
                 const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
@@ -729,8 +778,13 @@ static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
 }
 
 extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream) {
-    if (!f || !params || !view) {
-        set_error("gs_preprocess: null argument");
+    return gs_preprocess_ex(f, params, view, 0, stream);
+}
+
+extern "C" int gs_preprocess_ex(const gs_frame *f, const float *params, const gs_view *view, int32_t flags,
+                                void *stream) {
+    if (!f || !params || !view || (flags & ~GS_PP_LAZY_SH)) {
+        set_error("gs_preprocess: null argument or unknown flags");
         return GS_ERR_ARG;
     }
     cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
@@ -738,8 +792,12 @@ extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_vi
     cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
-    preprocess_kernel<<<3 * 148, PP_THREADS, PP_WARPS * 2 * sizeof(PPBatch), (cudaStream_t)stream>>>(*f, params,
-                                                                                                     view);
+    if (flags & GS_PP_LAZY_SH)
+        preprocess_kernel<true><<<4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream>>>(*f, params,
+                                                                                                         view);
+    else
+        preprocess_kernel<false><<<4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream>>>(*f, params,
+                                                                                                          view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
     int tb = 0, rb = 0;
@@ -798,7 +856,9 @@ extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_
 
 namespace gs {
 void init_preprocess_attrs() {
-    cudaFuncSetAttribute(preprocess_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(PP_WARPS * 2 * sizeof(PPBatch)));
+    cudaFuncSetAttribute(preprocess_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(PP_WARPS * sizeof(PPWarp)));
+    cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(PP_WARPS * sizeof(PPWarp)));
 }
 }  // namespace gs

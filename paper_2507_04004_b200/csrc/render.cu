@@ -448,11 +448,11 @@ __global__ void zero_g2d_kernel(gs_frame f) {
     // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
     // batches, the chain rule) clears every row it consumes, and the workspace starts zero-filled
     if (f.counters[GS_CNT_LAZY]) return;
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
-    if (i >= 6 * nt) return;
-    const int64_t g = f.touched_list[i / 6];
-    reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + i % 6] = make_double2(0.0, 0.0);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * nt; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = f.touched_list[i / 6];
+        reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + i % 6] = make_double2(0.0, 0.0);
+    }
 }
 
 }  // namespace gs
@@ -476,7 +476,8 @@ extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
     if (f->n > 0) {  // each backward starts from zero gradients (backward_2d is a pure function)
-        zero_g2d_kernel<<<(unsigned)((f->n * 6 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
+        // grid-stride over a small fixed grid: in the engine (lazy lists) every CTA exits at once
+        zero_g2d_kernel<<<2 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
         int rc = check_launch("zero_g2d_kernel");
         if (rc) return rc;
     }

@@ -12,10 +12,6 @@
 
 namespace gs {
 
-// huge records (depth order): 8 ints each (id, depth bits, slot), then their ids, then their keys
-constexpr int HREC = 8;
-constexpr int HIDS = HREC * GS_HUGE_CAP;
-constexpr int HKEYS = HIDS + GS_HUGE_CAP;  // int offset of the uint64 key array (8-B aligned)
 
 // tile_scratch segments (each tiles + 1 ints)
 __device__ __forceinline__ int32_t *ts_cursor(const gs_frame &f) { return f.tile_scratch; }

@@ -108,7 +108,7 @@ class MapOptimizer:
     # -- one iteration: R/mapper.py:249-256 --------------------------------------------
     def _launch(self) -> None:
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
-        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss", f, cur, self.lam, self.xi, s)
@@ -167,7 +167,7 @@ class MapOptimizer:
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(self.PHASES) + 1)]
         ev[0].record()
-        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         ev[1].record()
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         ev[2].record()
@@ -227,6 +227,16 @@ class MapOptimizer:
         ev.record()
         self._events[s] = ev
         self._steps += 1
+
+    def save_state(self) -> tuple:
+        """Device copies of the optimised state (parameter rows, Adam m, v, t)."""
+        a = self.adam
+        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t))
+
+    def restore_state(self, state: tuple) -> None:
+        a = self.adam
+        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t), state):
+            dst.copy_(src)
 
     def loss_sum(self, reset: bool = True) -> float:
         v = float(self.loss_acc.item())

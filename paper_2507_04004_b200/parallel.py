@@ -73,7 +73,7 @@ class BatchMapOptimizer:
         """forward -> loss -> backward -> chain rule of view k into (grads, touched)."""
         self.cur.copy_(self.views[k].buf)
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
-        call("gs_preprocess", f, self.g.data.data_ptr(), cur, s)
+        call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss", f, cur, self.lam, self.xi, s)

@@ -266,9 +266,10 @@ def grads_to_rows(grads: dict, n: int, device) -> torch.Tensor:
 
 
 def backward(gmap, out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=None, with_pose: bool = False):
-    """R/rasterizer.py:543-556 -> (grads dict mirroring parameters(), touched, pose_grad)."""
-    if with_pose:
-        raise NotImplementedError("pose gradients (R/rasterizer.py:646-657) are a later row (SURVEY.md 8f)")
+    """R/rasterizer.py:543-556 -> (grads dict mirroring parameters(), touched, pose_grad).
+
+    pose_grad (with_pose=True) is the 6-vector (rho, theta) on the left tangent of T_cw
+    (R/rasterizer.py:646-657) as a float64 device tensor, else None."""
     g = as_device_map(gmap)
     ws: Workspace = out.ctx["workspace"]
     view: DeviceView = out.ctx["view"]
@@ -277,12 +278,26 @@ def backward(gmap, out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=
     n = len(g)
     rows = torch.zeros((n, GS_ROW), dtype=torch.float32, device=g.device)
     acc = torch.zeros(n, dtype=torch.uint8, device=g.device)
+    if with_pose:
+        pose = torch.empty(6, dtype=torch.float64, device=g.device)
+        call("gs_chain_pose", ws.fptr, g.data.data_ptr(), rows.data_ptr(), acc.data_ptr(), view.ptr,
+             pose.data_ptr(), stream_ptr())
+        return rows_to_grads(rows), acc.bool(), pose
     call("gs_chain", ws.fptr, g.data.data_ptr(), rows.data_ptr(), acc.data_ptr(), view.ptr, stream_ptr())
     return rows_to_grads(rows), acc.bool(), None
 
 
 def pose_backward(gmap, out, g_color_img, g_depth_img=None, g_opac_img=None):
-    return backward(gmap, out, g_color_img, g_depth_img, g_opac_img, with_pose=True)[2]
+    """The pose gradient alone (the tracker's need, R/odometry.py:324-328): the attribute
+    gradients are not materialised."""
+    g = as_device_map(gmap)
+    ws: Workspace = out.ctx["workspace"]
+    view: DeviceView = out.ctx["view"]
+    _load_image_grads(ws, g_color_img, g_depth_img, g_opac_img)
+    call("gs_render_bwd", ws.fptr, stream_ptr())
+    pose = torch.empty(6, dtype=torch.float64, device=g.device)
+    call("gs_chain_pose", ws.fptr, g.data.data_ptr(), None, None, view.ptr, pose.data_ptr(), stream_ptr())
+    return pose
 
 
 def cull_tiles(mean2d, conic, cov2d, opacity, depth, valid, width, height, cull=True):

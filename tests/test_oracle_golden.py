@@ -14,7 +14,7 @@ import oracle as O
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SCENES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-                if not p.endswith("losses.npz"))
+                if os.path.basename(p) not in ("losses.npz", "pose.npz"))
 
 
 def rel(a, b, floor=1e-9):
@@ -123,3 +123,52 @@ def test_known_answers():
 def test_det_logf():
     for x in (1.0001, 1.5, 2.0, 3.7, 100.0, 254.9):
         assert abs(O.det_logf(x) - np.log(np.float32(x))) < 2e-7 * max(1.0, np.log(x))
+
+
+def _pose_scene(z, key):
+    c = z[f"{key}_cam"]
+    cam = O.Camera(int(c[0]), int(c[1]), float(c[2]), float(c[3]), float(c[4]), float(c[5]), z[f"{key}_rot"],
+                   z[f"{key}_trans"])
+    return cam, O.GaussianMap.from_rows(z[f"{key}_rows"])
+
+
+@pytest.mark.parametrize("name", SCENES)
+def test_pose_gradient_matches_reference(name):
+    """backward(with_pose=True): R/rasterizer.py:646-657 on the golden scenes' loss gradients."""
+    p = np.load(os.path.join(GOLD, "pose.npz"))
+    z, cam, g = load(name)
+    out = O.forward(g, cam)
+    _, _, pose = O.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"], with_pose=True)
+    ref = p[f"{name}_pose"]
+    assert np.max(np.abs(pose - ref)) < 1e-9 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_pose_gradient_finite_differences(seed):
+    """The reference's own check (T/test_rasterizer.py:261-280): left-perturbed T_cw, central
+    differences of the cull=False, early_stop=False weighted render, plus its golden value."""
+    p = np.load(os.path.join(GOLD, "pose.npz"))
+    key = f"fd{seed}"
+    cam, g = _pose_scene(p, key)
+    wc, wd, wo = p[f"{key}_wc"], p[f"{key}_wd"], p[f"{key}_wo"]
+    out = O.forward(g, cam, cull=False, early_stop=False)
+    grads, _, pose = O.backward(g, out, wc, wd, wo, with_pose=True)
+    assert np.max(np.abs(pose - p[f"{key}_pose"])) < 1e-9 * np.abs(p[f"{key}_pose"]).max()
+    assert np.max(np.abs(O.grads_to_rows(grads) - p[f"{key}_grads"])) < 1e-9 * np.abs(p[f"{key}_grads"]).max()
+    from paper_2507_04004_b200.scenes import exp_so3
+
+    def loss(c):
+        o = O.forward(g, c, cull=False, early_stop=False)
+        return float((o.color * wc).sum() + (o.depth * wd).sum() + (o.opacity * wo).sum())
+
+    step = 1e-6
+    for k in range(6):
+        vals = []
+        for sgn in (1.0, -1.0):
+            eps = np.zeros(6)
+            eps[k] = sgn * step
+            rot = exp_so3(eps[3:]) @ cam.rot_cw
+            trans = exp_so3(eps[3:]) @ cam.trans_cw + eps[:3]
+            vals.append(loss(O.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, rot, trans)))
+        fd = (vals[0] - vals[1]) / (2 * step)
+        assert abs(pose[k] - fd) / max(abs(fd), abs(pose[k]), 1e-4) < 1e-4, (k, pose[k], fd)
