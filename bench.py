@@ -42,6 +42,12 @@ CONFIGS = {
     "S1-1M-1280x720": ("s1", 1 << 20, 1280, 720, 30000, 1, "train"),
     "S1-10k-320x240": ("s1", 10000, 320, 240, 5000, 1, "train"),
     "S2r-2M-1920x1080-render": ("room", 1 << 21, 1920, 1080, 32, 4, "render"),
+    # BASELINE config 5: LiDAR density sweep at 1M Gaussians, 1280x720
+    "S2r-1M-1280x720-16line": ("room", 1 << 20, 1280, 720, 16, 4, "train"),
+    "S2r-1M-1280x720-64line": ("room", 1 << 20, 1280, 720, 64, 4, "train"),
+    "S2r-1M-1280x720-128line": ("room", 1 << 20, 1280, 720, 128, 4, "train"),
+    "S2r-1M-1280x720-livox5k": ("room", 1 << 20, 1280, 720, "rosette:5000", 4, "train"),
+    "S2r-1M-1280x720-livox200k": ("room", 1 << 20, 1280, 720, "rosette:200000", 4, "train"),
 }
 DEFAULT = "S2r-1M-1280x720-32line"
 SEGMENT = 100  # iterations per timed segment (the map is restored between segments, untimed)
@@ -181,13 +187,13 @@ def run_ours(args) -> dict:
     nv = len(kfs)
     initial = eng.save_state()
 
-    def timed(step_fn):
+    def timed(block_fn):
         """K steps timed with CUDA events in segments of <= SEGMENT iterations; between
         segments (untimed) the map and Adam state are restored to the scene's initial state, so
-        the workload is the named scene + < SEGMENT iterations of optimisation whatever K is."""
+        the workload is the named scene + < SEGMENT iterations of optimisation whatever K is.
+        block_fn(first, count) runs iterations first .. first + count - 1."""
         eng.restore_state(initial)
-        for i in range(args.warmup):
-            step_fn(i)
+        block_fn(0, args.warmup)
         eng.restore_state(initial)
         torch.cuda.synchronize()
         total_ms, wall_s, done = 0.0, 0.0, 0
@@ -197,8 +203,7 @@ def run_ours(args) -> dict:
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             s_.record()
-            for i in range(done, done + seg):
-                step_fn(i)
+            block_fn(done, seg)
             e_.record()
             e_.synchronize()
             wall_s += time.perf_counter() - t0
@@ -207,13 +212,17 @@ def run_ours(args) -> dict:
             eng.restore_state(initial)
         return total_ms / args.steps, wall_s * 1e3 / args.steps
 
+    def graph_block(first, count):
+        for i in range(first, first + count):
+            eng.step(i % nv)
+
     with ClockSampler(local) as clk:
-        ms, _ = timed(lambda i: eng.step(i % nv))
+        ms, _ = timed(graph_block)
     value = 1000.0 / ms
     loss = eng.loss_sum() / (args.steps + args.warmup)
     # e2e: host keyframes through the public streaming API (H2D inside the timed region)
     eng.attach_host_keyframes(kfs)
-    e2e_ms, wall_ms = timed(lambda i: eng.step_host(i % nv, i))
+    e2e_ms, wall_ms = timed(lambda first, count: eng.run_host([i % nv for i in range(first, first + count)]))
     # per-phase profile (eager, events between the C-ABI calls) for the roofline
     prof = {p: [] for p in M.MapOptimizer.PHASES}
     for i in range(max(10, min(args.steps, 30))):
@@ -247,7 +256,8 @@ def run_ours(args) -> dict:
                              "to the initial scene between segments (untimed)"},
         "e2e": {"value": round(1000.0 / e2e_ms, 2), "unit": "it/s", "h2d_bytes_per_step": int(eng.h2d_bytes),
                 "d2h_bytes_per_step": int(eng.d2h_bytes), "wall_ms_per_step": round(wall_ms, 4),
-                "path": "MapOptimizer.step_host: pinned host keyframe -> H2D -> LiDAR K-list -> iteration -> D2H loss"},
+                "path": "MapOptimizer.run_host: pinned host keyframe (target image + LiDAR K-list) -> H2D on a "
+                        "copy stream, double-buffered behind the previous iteration -> iteration -> D2H loss"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
@@ -280,7 +290,7 @@ def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
 
     def launch():
         _lib.call("gs_preprocess_ex", ws.fptr, g.data.data_ptr(), cur.data_ptr(), _lib.GS_PP_LAZY_SH, stream_ptr())
-        _lib.call("gs_bin", ws.fptr, 1, stream_ptr())
+        _lib.call("gs_bin", ws.fptr, _lib.GS_BIN_LAZY, stream_ptr())
         _lib.call("gs_render_fwd", ws.fptr, 1, stream_ptr())
 
     cur.copy_(views[0].buf)
@@ -302,7 +312,10 @@ def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
         e.record()
         e.synchronize()
     ms = s.elapsed_time(e) / args.steps
-    return {"metric": METRIC, "value": round(1000.0 / ms, 2), "unit": "FPS", "n_gpus": 1, "steps": args.steps,
+    cnt = ws.counters.cpu().numpy()
+    stats = {"entries": int(cnt[_lib.CNT_ENTRIES]), "touched": int(cnt[_lib.CNT_TOUCHED]),
+             "screen_covering": int(cnt[_lib.GS_CNT_SLOTS + 3]), "pixels": int(ws.width * ws.height)}
+    return {"metric": METRIC, "value": round(1000.0 / ms, 2), "unit": "FPS", "stats": stats, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene",
             "config": {"workload": name, "gaussians": len(g), "mode": "forward-only render"},

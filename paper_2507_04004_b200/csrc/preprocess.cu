@@ -584,30 +584,38 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                 if (h < GS_HUGE_CAP)
                     reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] =
                         ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
-            } else if (t) {  // per-tile bucket counts of the binning (bitmap or exact re-test)
-                const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
-                const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
-                const int64_t base = (int64_t)f.keep_bits[g];
-                const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-                const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
-                for (int c = 0; c < ncand; c++) {
-                    const int tx = r.x + c % nx, ty = r.z + c / nx;
-                    bool keep;
-                    if (base >= 0) {
-                        keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
-                    } else {
-                        const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-                        const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                        keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
-                    }
-                    if (keep) {
-                        atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
-                        atomicMin(reinterpret_cast<unsigned long long *>(f.tile_minkey) + ty * f.tiles_x + tx,
-                                  ((unsigned long long)__float_as_uint(s1.z) << 32) | (uint32_t)g);
-                    }
-                }
             }
             f.touched[g] = t;
+        }
+        // per-tile bucket counts of the binning (bitmap, or the exact re-test on bitmap overflow):
+        // the warp walks the candidates of each of its non-huge kept Gaussians together
+        const bool cnt = b < nb && t && f.big_slot[b] < 0;
+        unsigned pend = __ballot_sync(0xffffffffu, cnt);
+        while (pend) {
+            const int j = __ffs(pend) - 1;
+            pend &= pend - 1;
+            const int gj = __shfl_sync(0xffffffffu, g, j);
+            const int4 r = reinterpret_cast<const int4 *>(f.rect)[gj];
+            const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+            const int64_t base = (int64_t)f.keep_bits[gj];
+            const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * gj];
+            const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * gj + 1];
+            const unsigned long long key = ((unsigned long long)__float_as_uint(s1.z) << 32) | (uint32_t)gj;
+            for (int c = threadIdx.x & 31; c < ncand; c += 32) {
+                const int tx = r.x + c % nx, ty = r.z + c / nx;
+                bool keep;
+                if (base >= 0) {
+                    keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
+                } else {
+                    const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+                    const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
+                    keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                }
+                if (keep) {
+                    atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
+                    atomicMin(reinterpret_cast<unsigned long long *>(f.tile_minkey) + ty * f.tiles_x + tx, key);
+                }
+            }
         }
         warp_append(t, g, &f.counters[GS_CNT_TOUCHED], f.touched_list);
     }
@@ -800,9 +808,8 @@ extern "C" int gs_preprocess_ex(const gs_frame *f, const float *params, const gs
                                                                                                           view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
-    int tb = 0, rb = 0;
-    const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
-    return launch_big_cull(f, allow_huge, (cudaStream_t)stream);
+    // screen-covering Gaussians are binned per tile by bitmap (up to GS_HUGE_CAP per view)
+    return launch_big_cull(f, 1, (cudaStream_t)stream);
 }
 
 extern "C" int gs_project(const float *params, int64_t n, const gs_camera *cam, float *mu_cam, float *mean2d,
@@ -835,9 +842,8 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
     if (rc) return rc;
     touched_list_kernel<<<(unsigned)((f->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
     if ((rc = check_launch("touched_list_kernel"))) return rc;
-    int tb = 0, rb = 0;
-    const int allow_huge = compact_words(f->n, f->tiles_x * f->tiles_y, &tb, &rb) ? 1 : 0;
-    return launch_big_cull(f, allow_huge, (cudaStream_t)stream);
+    // screen-covering Gaussians are binned per tile by bitmap (up to GS_HUGE_CAP per view)
+    return launch_big_cull(f, 1, (cudaStream_t)stream);
 }
 
 extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_t height, int32_t *idx, float *z,

@@ -295,13 +295,15 @@ def test_mapping_iterations_match_oracle():
     assert np.isfinite(eng.loss_sum())
 
 
-def test_full_size_properties():
-    """S2r at BASELINE size (1M Gaussians, 1280x720, 32-line LiDAR): bit-exact binning against the
-    fp32 oracle, O + T = 1, touched == ids present in the entry list."""
+@pytest.mark.parametrize("n,w,h", [(1 << 20, 1280, 720), (1 << 21, 1920, 1080)])
+def test_full_size_properties(n, w, h):
+    """S2r at BASELINE sizes (1M Gaussians at 1280x720; 2M at 1920x1080, the render-FPS config):
+    bit-exact binning against the fp32 oracle, O + T = 1, touched == ids present in the entry
+    list."""
     from paper_2507_04004_b200 import rasterizer as R
     from paper_2507_04004_b200 import scenes
     from paper_2507_04004_b200.gaussians import GaussianMap
-    sc = scenes.scene_room(1 << 20, 1280, 720, lidar=32)
+    sc = scenes.scene_room(n, w, h, lidar=32)
     cam = R.camera_from(sc.cams[0])
     g = GaussianMap.from_rows(sc.rows)
     out = R.forward(g, cam)
@@ -430,7 +432,7 @@ def test_pose_gradient_matches_reference(name):
     g0, _, none = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
     assert none is None
     # (the backward's FP64 atomics are not bit-deterministic run to run)
-    assert normwise(_np(g0["_rows"]), _np(grads["_rows"])) < 1e-6
+    assert normwise(_np(g0["_rows"]), _np(grads["_rows"])) < 1e-4
     only = R.pose_backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
     assert normwise(_np(only), _np(pose)) < 1e-5  # separate backward: atomic order differs
 
@@ -451,3 +453,57 @@ def test_pose_gradient_fd_scenes(seed):
     grads, _, pose = R.backward(g, out, p[f"{key}_wc"], p[f"{key}_wd"], p[f"{key}_wo"], with_pose=True)
     assert normwise(_np(pose), p[f"{key}_pose"]) < REL_TOL
     assert normwise(_np(grads["_rows"])[:, :59], p[f"{key}_grads"]) < REL_TOL
+
+
+def test_host_streaming_matches_device_keyframes():
+    """MapOptimizer.run_host (pinned host keyframes, K-list compacted on the host, H2D double-
+    buffered on a copy stream) runs the same iterations as device-resident keyframes."""
+    import torch
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(8192, 160, 96, lidar=16, render_views=(0, 1, 2))
+    kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
+    order = [0, 2, 1, 1, 0, 2, 2]
+    a = M.MapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
+    a.capture()
+    la = []
+    for k in order:
+        a.step(k)
+        la.append(a.loss_sum())
+    b = M.MapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
+    b.capture()
+    b.attach_host_keyframes(kfs)
+    b.run_host(order)
+    torch.cuda.synchronize()
+    lb = b._h_loss[:len(order)].numpy()
+    assert la[0] == lb[0]  # the forward and loss are deterministic
+    assert np.max(np.abs(np.array(la) - lb) / np.abs(np.array(la))) < 1e-5
+    assert normwise(_np(b.g.rows()), _np(a.g.rows())) < 1e-4
+
+
+@pytest.mark.parametrize("lidar", [16, 64, 128, "rosette:5000", "rosette:200000"])
+def test_lidar_density_sweep(lidar):
+    """BASELINE config 5: 16/64/128-line and Livox-style rosette LiDAR at 1280x720 (K from ~5k
+    to ~164k pixels).  The depth term evaluated on the device K-list equals the reference's dense
+    depth_ratio_loss (R/losses.py:133-154) on the same rendered depth / opacity."""
+    from paper_2507_04004_b200 import losses as L
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(1 << 17, 1280, 720, lidar=lidar)
+    cam = R.camera_from(sc.cams[0])
+    g = GaussianMap.from_rows(sc.rows)
+    out = R.forward(g, cam)
+    sd = sc.sparse_depths[0]
+    k = int((sd > 0).sum())
+    assert k > 1000
+    xi = 0.005
+    loss, gc, gd, go = L.mapping_loss(out.color, out.depth, out.opacity, sc.targets[0], sd, 0.2, xi)
+    D, Op = _np(out.depth), _np(out.opacity)
+    dv, dgd, dgo = O.depth_ratio_loss(D, Op, sd)
+    pv, _ = O.photometric_loss(_np(out.color), sc.targets[0], 0.2)
+    assert abs(loss - (pv + xi * dv)) < REL_TOL * abs(pv + xi * dv)
+    assert normwise(_np(gd), xi * dgd) < 1e-5
+    assert normwise(_np(go), xi * dgo) < 1e-5
