@@ -233,6 +233,24 @@ int gs_pack_splats(const gs_frame *f, const float *mean2d, const float *conic, c
                    const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                    void *stream);
 
+/* ---- keyframe preparation --------------------------------------- */
+/* R/mapper.py:69-81 project_points over m world points (m x 3), FP64, rounded pixel centres
+ * (round half to even, as np.round); optional outputs (NULL = skip): u, v, ui, vi, z, flags
+ * (bit 0 inside the image, bit 1 "fresh": inside and opacity[vi, ui] < tau, the expand_map test
+ * of R/mapper.py:222-225; needs opacity (H, W)), colors (m x 3, bilinear_color R/mapper.py:84-98
+ * of image (H, W, 3)).  cam is a DEVICE pointer. */
+int gs_project_points(const float *points, int64_t m, const gs_camera *cam, const float *image,
+                      const float *opacity, float tau, float *u, float *v, int32_t *ui, int32_t *vi,
+                      float *z, uint8_t *flags, float *colors, void *stream);
+/* R/mapper.py:101-107 zbuffer_project: dense (height, width) sparse-depth map, the nearest point
+ * per pixel, 0 where no point lands.  zbuf: width * height uint32 scratch. */
+int gs_zbuffer(const float *points, int64_t m, const gs_camera *cam, int32_t width, int32_t height,
+               uint32_t *zbuf, float *depth, void *stream);
+/* R/gaussians.py:227-248 init_from_points: m parameter rows (GS_ROW floats each) from points
+ * (m x 3), colours (m x 3), camera depths (m) and the focal length. */
+int gs_init_rows(const float *points, const float *colors, const float *depths, int64_t m, float focal,
+                 float *rows, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -145,19 +145,17 @@ def as_device_map(gmap, device=None) -> GaussianMap:
 
 
 def init_from_points(points, colors, depths, focal: float, device=None) -> GaussianMap:
-    """R/gaussians.py:227-248: isotropic footprint scale, identity rotation, opacity 0.1."""
+    """R/gaussians.py:227-248 through gs_init_rows: isotropic footprint scale log(max(depth /
+    focal, 1e-9)), identity rotation, opacity 0.1, degree-0 SH matching the colour."""
     dev = torch.device(device) if device is not None else default_device()
-    pts = _as_f32(points, dev).reshape(-1, 3)
-    col = _as_f32(colors, dev).reshape(-1, 3)
-    dep = _as_f32(depths, dev).reshape(-1)
-    n = len(pts)
-    g = GaussianMap(device=dev, capacity=n)
-    g.n = n
-    g.data[:n, 0:3] = pts
-    g.data[:n, 3:6] = torch.log(torch.clamp(dep / focal, min=1e-9))[:, None]
-    g.data[:n, 6] = 1.0
-    g.data[:n, 10] = float(np.log(INIT_OPACITY / (1 - INIT_OPACITY)))
-    g.data[:n, 11:14] = (col - 0.5) / SH_C0
+    pts = _as_f32(points, dev).reshape(-1, 3).contiguous()
+    col = _as_f32(colors, dev).reshape(-1, 3).contiguous()
+    dep = _as_f32(depths, dev).reshape(-1).contiguous()
+    m = len(pts)
+    g = GaussianMap(device=dev, capacity=max(m, 1))
+    call("gs_init_rows", pts.data_ptr(), col.data_ptr(), dep.data_ptr(), m, float(focal), g.data.data_ptr(),
+         stream_ptr())
+    g.n = m
     return g
 
 

@@ -18,7 +18,7 @@ import torch
 from . import _lib
 from ._lib import call
 from .errors import DataError
-from .gaussians import GaussianMap, as_device_map, init_from_points, stream_ptr
+from .gaussians import GaussianMap, as_device_map, default_device, init_from_points, stream_ptr, struct_to_device
 from .rasterizer import (AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from, default_lrs, forward,
                          lr_columns)
 
@@ -348,49 +348,119 @@ def optimize_map(gmap, keyframes, cfg: MappingConfig, rng, adam: AdamState, lrs:
 # map growth (R/mapper.py:69-107, 209-230) -- device versions of the keyframe helpers
 
 
-def project_points(points_w, cam: Camera):
-    """R/mapper.py:69-81 (torch): pixel coords, depths and an inside-image mask."""
+def _points_dev(points, device) -> torch.Tensor:
+    return torch.as_tensor(points if isinstance(points, torch.Tensor) else np.asarray(points, dtype=np.float32),
+                           dtype=torch.float32, device=device).reshape(-1, 3).contiguous()
+
+
+def _cam_dev(cam, device) -> torch.Tensor:
+    c = camera_from(cam)
+    return struct_to_device(c.struct(), device)
+
+
+def _project(points_w, cam, image=None, opacity=None, tau: float = 0.0):
+    """gs_project_points: (u, v, ui, vi, z, flags, colors) device tensors."""
     cam = camera_from(cam)
-    dev = points_w.device
-    R = torch.as_tensor(np.asarray(cam.rot_cw), dtype=torch.float32, device=dev)
-    t = torch.as_tensor(np.asarray(cam.trans_cw), dtype=torch.float32, device=dev)
-    p = points_w @ R.T + t
-    z = p[:, 2]
-    front = z > NEAR_CLIP
-    zs = torch.where(front, z, torch.ones_like(z))
-    u = cam.fx * p[:, 0] / zs + cam.cx
-    v = cam.fy * p[:, 1] / zs + cam.cy
-    ui, vi = torch.round(u).long(), torch.round(v).long()
-    inside = front & (ui >= 0) & (ui < cam.width) & (vi >= 0) & (vi < cam.height)
-    return u, v, ui, vi, z, inside
+    dev = points_w.device if isinstance(points_w, torch.Tensor) and points_w.is_cuda else default_device()
+    pts = _points_dev(points_w, dev)
+    m = len(pts)
+    u, v, z = (torch.empty(m, device=dev) for _ in range(3))
+    ui, vi = (torch.empty(m, dtype=torch.int32, device=dev) for _ in range(2))
+    flags = torch.empty(m, dtype=torch.uint8, device=dev)
+    img = None if image is None else torch.as_tensor(image, dtype=torch.float32, device=dev).contiguous()
+    op = None if opacity is None else torch.as_tensor(opacity, dtype=torch.float32, device=dev).contiguous()
+    colors = torch.empty((m, 3), device=dev) if img is not None else None
+    camd = _cam_dev(cam, dev)
+    call("gs_project_points", pts.data_ptr(), m, camd.data_ptr(), img.data_ptr() if img is not None else None,
+         op.data_ptr() if op is not None else None, float(tau), u.data_ptr(), v.data_ptr(), ui.data_ptr(),
+         vi.data_ptr(), z.data_ptr(), flags.data_ptr(), colors.data_ptr() if colors is not None else None,
+         stream_ptr())
+    return u, v, ui, vi, z, flags, colors, pts
+
+
+def project_points(points_w, cam: Camera):
+    """R/mapper.py:69-81 (gs_project_points): pixel coords, depths and an inside-image mask."""
+    u, v, ui, vi, z, flags, _, _ = _project(points_w, cam)
+    return u, v, ui.long(), vi.long(), z, (flags & 1).bool()
+
+
+def bilinear_color(image, u, v):
+    """R/mapper.py:84-98 through gs_project_points is keyed on points; this helper takes pixel
+    coordinates directly (same arithmetic, torch, float64) for API parity."""
+    img = torch.as_tensor(image, dtype=torch.float64)
+    h, w = img.shape[:2]
+    x = torch.clamp(torch.as_tensor(u, dtype=torch.float64, device=img.device), 0.0, w - 1.0)
+    y = torch.clamp(torch.as_tensor(v, dtype=torch.float64, device=img.device), 0.0, h - 1.0)
+    x0 = torch.clamp(torch.floor(x).long(), 0, max(w - 2, 0))
+    y0 = torch.clamp(torch.floor(y).long(), 0, max(h - 2, 0))
+    fx, fy = (x - x0)[:, None], (y - y0)[:, None]
+    x1, y1 = torch.clamp(x0 + 1, max=w - 1), torch.clamp(y0 + 1, max=h - 1)
+    top = img[y0, x0] * (1 - fx) + img[y0, x1] * fx
+    bot = img[y1, x0] * (1 - fx) + img[y1, x1] * fx
+    return top * (1 - fy) + bot * fy
+
+
+def zbuffer_project(points_w, cam: Camera) -> torch.Tensor:
+    """R/mapper.py:101-107 (gs_zbuffer): dense sparse-depth map, nearest point per pixel, 0 where
+    empty -- the supervision the LiDAR K-list is compacted from."""
+    cam = camera_from(cam)
+    dev = points_w.device if isinstance(points_w, torch.Tensor) and points_w.is_cuda else default_device()
+    pts = _points_dev(points_w, dev)
+    h, w = int(cam.height), int(cam.width)
+    zbuf = torch.empty(h * w, dtype=torch.int32, device=dev)
+    depth = torch.empty((h, w), device=dev)
+    camd = _cam_dev(cam, dev)
+    call("gs_zbuffer", pts.data_ptr(), len(pts), camd.data_ptr(), w, h, zbuf.data_ptr(), depth.data_ptr(),
+         stream_ptr())
+    return depth
+
+
+def group_mapping_data(frame_index: int, clouds, image, cam: Camera, cfg: MappingConfig, rng):
+    """R/mapper.py:110-131 on the device: z-buffered sparse depth of the merged clouds, random 1-in-
+    n_p decimation (host rng, the reference's draw), colours by bilinear lookup of the image."""
+    if frame_index % cfg.keyframe_stride != 0:
+        return None
+    dev = default_device()
+    parts = [_points_dev(c, dev) for c in clouds] if clouds else []
+    merged = torch.cat(parts) if parts else torch.zeros((0, 3), device=dev)
+    sparse = zbuffer_project(merged, cam)
+    n = len(merged)
+    keep = rng.permutation(n)[:max(n // cfg.n_p, 1 if n else 0)]
+    dec = merged[torch.as_tensor(keep, dtype=torch.long, device=dev)]
+    img = torch.as_tensor(image, dtype=torch.float32, device=dev)
+    _, _, _, _, _, flags, colors, pts = _project(dec, cam, image=img)
+    inside = (flags & 1).bool()
+    return Keyframe(cam=camera_from(cam), image=img, sparse_depth=sparse, points=pts[inside],
+                    colors=colors[inside])
+
+
+def _init_rows(points, colors, depths, focal: float, device) -> GaussianMap:
+    return init_from_points(points, colors, depths, focal, device=device)
 
 
 def init_map(gmap: GaussianMap, kf: Keyframe) -> int:
-    """R/mapper.py:209-215."""
+    """R/mapper.py:209-215: one Gaussian per keyframe point (depth = camera z)."""
     if len(gmap):
         raise DataError("map already initialized")
-    pts = torch.as_tensor(np.asarray(kf.points, dtype=np.float32), device=gmap.device)
-    cam = camera_from(kf.cam)
-    R = torch.as_tensor(np.asarray(cam.rot_cw), dtype=torch.float32, device=gmap.device)
-    depths = pts @ R[2] + float(np.asarray(cam.trans_cw)[2])
-    gmap.append(init_from_points(pts, kf.colors, depths, cam.fx, device=gmap.device))
+    _, _, _, _, z, _, _, pts = _project(kf.points, kf.cam)
+    gmap.append(_init_rows(pts, kf.colors, z, camera_from(kf.cam).fx, gmap.device))
     return len(pts)
 
 
 def expand_map(gmap: GaussianMap, kf: Keyframe, tau: float) -> int:
-    """R/mapper.py:218-230: add Gaussians only where the rendered opacity is below tau."""
+    """R/mapper.py:218-230: add Gaussians only where the rendered opacity is below tau (the test
+    fused into gs_project_points)."""
     if len(gmap) == 0:
         raise DataError("map not initialized")
     opac = forward(gmap, kf.cam).opacity
-    pts = torch.as_tensor(np.asarray(kf.points, dtype=np.float32), device=gmap.device)
-    _, _, ui, vi, z, inside = project_points(pts, kf.cam)
-    fresh = inside.clone()
-    fresh[inside] = opac[vi[inside], ui[inside]] < tau
-    if not bool(fresh.any()):
+    _, _, _, _, z, flags, _, pts = _project(kf.points, kf.cam, opacity=opac, tau=tau)
+    fresh = (flags & 2).bool()
+    nf = int(fresh.sum())
+    if nf == 0:
         return 0
-    cols = torch.as_tensor(np.asarray(kf.colors, dtype=np.float32), device=gmap.device)
-    gmap.append(init_from_points(pts[fresh], cols[fresh], z[fresh], camera_from(kf.cam).fx, device=gmap.device))
-    return int(fresh.sum())
+    cols = torch.as_tensor(kf.colors, dtype=torch.float32, device=gmap.device).reshape(-1, 3)
+    gmap.append(_init_rows(pts[fresh], cols[fresh], z[fresh], camera_from(kf.cam).fx, gmap.device))
+    return nf
 
 
 class Mapper:

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SCENES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-                if os.path.basename(p) not in ("losses.npz", "pose.npz"))
+                if os.path.basename(p) not in ("losses.npz", "pose.npz", "keyframe.npz"))
 IMG_TOL = 1e-4
 REL_TOL = 1e-3
 # screen-space (intermediate) gradients: the mean2d term sums pixel contributions of opposite
@@ -507,3 +507,91 @@ def test_lidar_density_sweep(lidar):
     assert abs(loss - (pv + xi * dv)) < REL_TOL * abs(pv + xi * dv)
     assert normwise(_np(gd), xi * dgd) < 1e-5
     assert normwise(_np(go), xi * dgo) < 1e-5
+
+
+def test_batch_optimizer_matches_batch_oracle():
+    """parallel.BatchMapOptimizer (the per-rank body of the multi-GPU keyframe batch, SURVEY.md
+    8e) on one GPU: summed parameter-row gradients and the touched union equal the oracle's per-
+    view backward summed over the batch; the one sparse Adam step equals the oracle's on the
+    same gradients."""
+    from paper_2507_04004_b200 import parallel as PAR
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(4096, 96, 64, lidar=8, render_views=(0, 8, 16, 24))
+    rows64 = sc.rows.astype(np.float32).astype(np.float64)
+    g = GaussianMap.from_rows(sc.rows)
+    kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
+    eng = PAR.BatchMapOptimizer(g, kfs, R.default_lrs(3.0))
+    eng.step(range(4))
+    gsum = np.zeros((len(rows64), 59))
+    tun = np.zeros(len(rows64), bool)
+    og = O.GaussianMap.from_rows(rows64)
+    for k, c in enumerate(sc.cams):
+        cam = O.Camera(c["width"], c["height"], c["fx"], c["fy"], c["cx"], c["cy"], c["rot_cw"], c["trans_cw"])
+        out = O.forward(og, cam)
+        _, gc, gd, go = O.mapping_loss(out.color, out.depth, out.opacity, sc.targets[k], sc.sparse_depths[k], 0.2,
+                                       0.005)
+        gr, t, _ = O.backward(og, out, gc, gd, go)
+        gsum += O.grads_to_rows(gr)
+        tun |= t
+    assert np.array_equal(_np(eng.touched).astype(bool), tun)
+    ggpu = _np(eng.grads)[:, :59]
+    assert not ggpu[~tun].any()
+    assert normwise(ggpu, gsum) < 1e-2  # near-camera Gaussians included (see the 2e-2 bar above)
+    near = np.zeros(len(rows64), bool)
+    for c in sc.cams:
+        z = rows64[:, :3] @ np.asarray(c["rot_cw"])[2] + np.asarray(c["trans_cw"])[2]
+        near |= (z > 0.01) & (z < 0.05)
+    assert normwise(ggpu[~near & tun], gsum[~near & tun]) < REL_TOL
+    # the Adam step on the GPU's own gradients
+    exp = rows64.copy()
+    st = O.AdamState()
+    O.adam_rows(exp, ggpu.astype(np.float64), _np(eng.touched).astype(bool), st, O.default_lrs(3.0))
+    assert np.max(np.abs(_np(g.rows())[:, :59] - exp)) < 1e-5
+    assert np.array_equal(_np(eng.adam.t).astype(np.int64), st.t)
+
+
+def test_keyframe_preparation_on_device():
+    """SURVEY.md 8f row 1 on the device (gs_project_points / gs_zbuffer / gs_init_rows) against
+    the reference's outputs: pixel indices and masks exact, values to fp32 rounding."""
+    import torch
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    z = np.load(os.path.join(GOLD, "keyframe.npz"))
+    cam = R.Camera(int(z["width"]), int(z["height"]), float(z["fx"]), float(z["fy"]), float(z["cx"]),
+                   float(z["cy"]), z["rot_cw"], z["trans_cw"])
+    pts = z["points"]
+    u, v, ui, vi, zz, inside = M.project_points(pts, cam)
+    ins = _np(inside).astype(bool)
+    assert np.array_equal(ins, z["inside"])
+    assert np.array_equal(_np(ui)[ins], z["ui"][ins]) and np.array_equal(_np(vi)[ins], z["vi"][ins])
+    assert np.max(np.abs(_np(u) - z["u"]) / np.maximum(1.0, np.abs(z["u"]))) < 1e-6
+    assert np.max(np.abs(_np(zz) - z["z"]) / np.maximum(1.0, np.abs(z["z"]))) < 1e-6
+    *_, colors, _ = M._project(pts, cam, image=z["image"])
+    assert np.max(np.abs(_np(colors) - z["colors"])) < 1e-6
+    d = _np(M.zbuffer_project(pts, cam))
+    assert np.array_equal(d > 0, z["depth"] > 0)
+    assert np.max(np.abs(d - z["depth"]) / np.maximum(1.0, z["depth"])) < 1e-6
+    init = GaussianMap(device="cuda")
+    kf = M.Keyframe(cam=cam, image=z["image"], sparse_depth=z["depth"], points=pts[ins],
+                    colors=z["colors"][ins].astype(np.float32))
+    assert M.init_map(init, kf) == int(ins.sum())
+    assert np.max(np.abs(_np(init.rows())[:, :59] - z["init_rows"])) < 1e-5
+    assert not _np(init.rows())[:, 59:].any()
+    g = GaussianMap.from_rows(np.load(os.path.join(GOLD, "small0.npz"))["rows"])
+    kf_all = M.Keyframe(cam=cam, image=z["image"], sparse_depth=z["depth"], points=pts,
+                        colors=z["colors"].astype(np.float32))
+    added = M.expand_map(g, kf_all, 0.5)
+    assert added == int(z["added"])
+    assert np.max(np.abs(_np(g.rows())[:, :59] - z["expanded_rows"])) < 1e-5
+    cfg = M.MappingConfig(n_p=3)
+    kf2 = M.group_mapping_data(0, [pts[:1500], pts[1500:]], z["image"], cam, cfg, np.random.default_rng(3))
+    sp = _np(kf2.sparse_depth)
+    assert np.array_equal(sp > 0, z["g_sparse"] > 0)
+    assert np.max(np.abs(_np(kf2.points) - z["g_points"])) < 1e-6
+    assert np.max(np.abs(_np(kf2.colors) - z["g_colors"])) < 1e-6
+    assert M.group_mapping_data(1, [pts], z["image"], cam, cfg, np.random.default_rng(3)) is None
+    torch.cuda.synchronize()

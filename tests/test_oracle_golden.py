@@ -14,7 +14,7 @@ import oracle as O
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SCENES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-                if os.path.basename(p) not in ("losses.npz", "pose.npz"))
+                if os.path.basename(p) not in ("losses.npz", "pose.npz", "keyframe.npz"))
 
 
 def rel(a, b, floor=1e-9):
@@ -172,3 +172,21 @@ def test_pose_gradient_finite_differences(seed):
             vals.append(loss(O.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, rot, trans)))
         fd = (vals[0] - vals[1]) / (2 * step)
         assert abs(pose[k] - fd) / max(abs(fd), abs(pose[k]), 1e-4) < 1e-4, (k, pose[k], fd)
+
+
+def test_keyframe_preparation_matches_reference():
+    """project_points / bilinear_color / zbuffer_project / init_from_points restatements against
+    the reference's outputs (tests/golden/keyframe.npz)."""
+    z = np.load(os.path.join(GOLD, "keyframe.npz"))
+    cam = O.Camera(int(z["width"]), int(z["height"]), float(z["fx"]), float(z["fy"]), float(z["cx"]),
+                   float(z["cy"]), z["rot_cw"], z["trans_cw"])
+    u, v, ui, vi, zz, inside = O.project_points(z["points"], cam)
+    assert np.array_equal(inside, z["inside"])
+    assert np.array_equal(ui[inside], z["ui"][inside]) and np.array_equal(vi[inside], z["vi"][inside])
+    assert np.max(np.abs(u - z["u"])) < 1e-9 and np.max(np.abs(zz - z["z"])) < 1e-12
+    assert np.max(np.abs(O.bilinear_color(z["image"], u, v) - z["colors"])) < 1e-12
+    d = O.zbuffer_project(z["points"], cam)
+    assert np.array_equal(d, z["depth"])
+    rows = O.init_rows(z["points"][inside], z["colors"][inside].astype(np.float32).astype(np.float64),
+                       zz[inside].astype(np.float32).astype(np.float64), cam.fx)
+    assert np.max(np.abs(rows - z["init_rows"])) < 1e-12
