@@ -7,6 +7,8 @@
 // computes its Gaussian's 59 gradients into shared memory, then the warp streams the Adam
 // update over the 32 rows (params, m, v) with coalesced float4 traffic.  Nothing but the
 // updated rows is written: the parameter-gradient rows never reach HBM on the 1-GPU path.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace gs {
@@ -14,6 +16,7 @@ namespace gs {
 constexpr int CA_WARPS = 4;
 constexpr int CA_THREADS = CA_WARPS * 32;
 constexpr int RP = 65;  // padded smem row
+constexpr int CA_BATCH = 4;  // float4 per lane and array in flight in the fused Adam stream
 
 // dR/dq of the normalised quaternion (R/rasterizer.py:490-499), contracted with gR
 template <typename T>
@@ -217,6 +220,7 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
     if (k0 >= nt) return;
     const int64_t k = k0 + lane;
     const int g = k < nt ? f.touched_list[k] : -1;
+
     // stage the 32 parameter rows (coalesced: 16 lanes x float4 = one row)
 #pragma unroll 4
     for (int j = 0; j < 16; j++) {
@@ -235,7 +239,7 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
     if (g >= 0) {
         double2 *g2 = reinterpret_cast<double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
         const double2 a = g2[0], b = g2[1], c = g2[2], d = g2[3], e = g2[4];
-        if ((mode == 1 || mode == 3) && f.counters[GS_CNT_LAZY])  // keep the row zero for the next view
+        if (mode != 2 && f.counters[GS_CNT_LAZY])  // keep the row zero for the next view
             for (int q = 0; q < GS_G2D / 2; q++) g2[q] = make_double2(0.0, 0.0);
         const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
@@ -275,6 +279,50 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         }
         return;
     }
+    if (mode == 0) {
+        // the warp's 32 rows streamed in batches of CA_BATCH float4 per lane and array: every load
+        // of a batch is in flight before the first use, so the update keeps HBM busy even at the
+        // chain's low occupancy.  Parameters are re-read from global (staged a
+        // moment ago: L2 hits); the smem tile holds G.
+#pragma unroll 1
+        for (int j0 = 0; j0 < 16; j0 += CA_BATCH) {
+            float4 P[CA_BATCH], M4[CA_BATCH], V4[CA_BATCH];
+            int64_t off[CA_BATCH];
+            int gq[CA_BATCH];
+#pragma unroll
+            for (int q = 0; q < CA_BATCH; q++) {
+                const int kk = lane + 32 * (j0 + q), r = kk >> 4, c4 = kk & 15;
+                gq[q] = __shfl_sync(0xffffffffu, g, r);
+                off[q] = (int64_t)gq[q] * GS_ROW + 4 * c4;
+                if (gq[q] >= 0 && c4 < 15) {  // columns 60-63: padding, untouched
+                    P[q] = *reinterpret_cast<const float4 *>(params + off[q]);
+                    M4[q] = *reinterpret_cast<const float4 *>(am + off[q]);
+                    V4[q] = *reinterpret_cast<const float4 *>(av + off[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < CA_BATCH; q++) {
+                const int kk = lane + 32 * (j0 + q), r = kk >> 4, c4 = kk & 15;
+                if (gq[q] < 0 || c4 == 15) continue;
+                const float *G = &sgr[warp][r][4 * c4];
+                const float bc1 = sbc[warp][r][0], bc2 = sbc[warp][r][1];
+                const float4 lr = __ldg(reinterpret_cast<const float4 *>(lr_cols) + c4);
+                float4 m4 = M4[q], v4 = V4[q], p4;
+                p4.x = adam_one(P[q].x, m4.x, v4.x, G[0], lr.x, bc1, bc2);
+                p4.y = adam_one(P[q].y, m4.y, v4.y, G[1], lr.y, bc1, bc2);
+                p4.z = adam_one(P[q].z, m4.z, v4.z, G[2], lr.z, bc1, bc2);
+                p4.w = c4 == 14 ? P[q].w : adam_one(P[q].w, m4.w, v4.w, G[3], lr.w, bc1, bc2);  // col 59: padding
+                if (c4 == 14) {
+                    m4.w = M4[q].w;
+                    v4.w = V4[q].w;
+                }
+                *reinterpret_cast<float4 *>(am + off[q]) = m4;
+                *reinterpret_cast<float4 *>(av + off[q]) = v4;
+                *reinterpret_cast<float4 *>(params + off[q]) = p4;
+            }
+        }
+        return;
+    }
 #pragma unroll 2
     for (int j = 0; j < 16; j++) {
         const int kk = lane + 32 * j, r = kk >> 4, c4 = kk & 15;
@@ -282,24 +330,7 @@ __global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__
         if (gg < 0) continue;
         const int64_t off = (int64_t)gg * GS_ROW + 4 * c4;
         const float *G = &sgr[warp][r][4 * c4];
-        if (mode == 0) {
-            // parameters re-read from global (just staged: an L2 hit); the smem tile holds G
-            const float4 P = *reinterpret_cast<const float4 *>(params + off);
-            const float bc1 = sbc[warp][r][0], bc2 = sbc[warp][r][1];
-            float4 m4 = *reinterpret_cast<const float4 *>(am + off);
-            float4 v4 = *reinterpret_cast<const float4 *>(av + off);
-            const float4 lr = *reinterpret_cast<const float4 *>(lr_cols + 4 * c4);
-            float4 p4;
-            p4.x = adam_one(P.x, m4.x, v4.x, G[0], lr.x, bc1, bc2);
-            p4.y = adam_one(P.y, m4.y, v4.y, G[1], lr.y, bc1, bc2);
-            p4.z = adam_one(P.z, m4.z, v4.z, G[2], lr.z, bc1, bc2);
-            p4.w = adam_one(P.w, m4.w, v4.w, G[3], lr.w, bc1, bc2);
-            if (c4 == 14) p4.w = P.w;  // column 59 is padding
-            if (c4 == 15) p4 = P;
-            *reinterpret_cast<float4 *>(am + off) = m4;
-            *reinterpret_cast<float4 *>(av + off) = v4;
-            *reinterpret_cast<float4 *>(params + off) = p4;
-        } else {
+        {
             float4 acc = *reinterpret_cast<const float4 *>(grads + off);
             acc.x += G[0];
             acc.y += G[1];
@@ -403,10 +434,15 @@ extern "C" int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, fl
         set_error("gs_chain_adam: null argument");
         return GS_ERR_ARG;
     }
-    // chain rule (FP64 geometry, low occupancy) writes compact gradient rows; a separate
-    // bandwidth-bound kernel streams the Adam update over the touched rows
-    int rc = launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 2, nullptr, nullptr, stream);
-    if (rc) return rc;
+    // fused: the chain rule (FP64 geometry) hands each warp's 32 gradient rows to the Adam update
+    // through shared memory, so gradient rows never reach HBM.  GSLIC_SPLIT_ADAM=1 selects the
+    // split form (compact gradient rows + a streaming adam_list_kernel) for comparison.
+    static const bool split = [] {
+        const char *e = getenv("GSLIC_SPLIT_ADAM");
+        return e && e[0] == '1';
+    }();
+    int rc = launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, split ? 2 : 0, nullptr, nullptr, stream);
+    if (rc || !split) return rc;
     if (f->n == 0) return GS_OK;
     adam_list_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols);
     return check_launch("adam_list_kernel");

@@ -30,9 +30,12 @@ def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     preprocess 5 (projection + small-footprint cull, large-footprint setup / bands / tiles /
     finish), bin 3 (lazy lists: huge sort, huge transpose, tile scan), forward 3 (blend, bucket
     fill + sorted continuation for the tiles that need them), loss 4 (tables, SSIM+L1, depth,
-    finalize), backward 2 (zero + tiles), chain + Adam 2."""
+    finalize), backward 2 (zero + tiles), chain rule fused with Adam 1 (2 with
+    GSLIC_SPLIT_ADAM=1: chain + adam_list)."""
     del tiles
-    return 5 + 3 + 3 + 4 + 2 + (1 if chain_only else 2)
+    import os
+    split = os.environ.get("GSLIC_SPLIT_ADAM", "0") == "1"
+    return 5 + 3 + 3 + 4 + 2 + (1 if chain_only or not split else 2)
 
 
 @dataclass
