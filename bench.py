@@ -150,7 +150,9 @@ def algorithmic_bytes(eng, scene_cam) -> dict:
         "preprocess": 16 * n + 240 * near + 106 * n,
         "render_fwd": 52 * proc + 28 * P + 8 * tx * ty,
         "render_bwd": 28 * P + (52 + 40) * proc + 48 * n_t + 8 * tx * ty,
-        "chain_adam": n_t * (256 + 48 + 512 + 768 + 8 + 4),
+        # fused chain + Adam: params, m, v read and written (240 of 256 B per row), the FP64
+        # screen-space gradients read (80 B) and zeroed (96 B), the step counter
+        "chain_adam": n_t * (3 * 240 + 80 + 4 + 3 * 240 + 96 + 4),
         "loss": 36 * P + 8 * P,
         "bin": 24 * E * 2 + 12 * E + 8 * E + 4 * E + 16 * valid * 4,
         "_stats": {"n": n, "n_valid": valid, "n_touched": n_t, "entries": E, "blend_entries": proc, "pixels": P},

@@ -17,6 +17,9 @@ constexpr int CA_WARPS = 4;
 constexpr int CA_THREADS = CA_WARPS * 32;
 constexpr int RP = 65;  // padded smem row
 constexpr int CA_BATCH = 4;  // float4 per lane and array in flight in the fused Adam stream
+#ifndef CA_MINB
+#define CA_MINB 4  // CTAs per SM the register budget is fitted to (16 warps)
+#endif
 
 // dR/dq of the normalised quaternion (R/rasterizer.py:490-499), contracted with gR
 template <typename T>
@@ -201,7 +204,7 @@ __device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, 
 // mode 2: compact gradient rows + bias corrections for adam_list_kernel.  mode 3: nothing but the
 // pose gradient (tracking).  POSE: pose6 (FP64, 6) += the pose gradient of the touched Gaussians.
 template <bool POSE>
-__global__ void __launch_bounds__(CA_THREADS) chain_kernel(gs_frame f, float *__restrict__ params,
+__global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, float *__restrict__ params,
                                                            float *__restrict__ am, float *__restrict__ av,
                                                            int32_t *__restrict__ at, const gs_view *__restrict__ view,
                                                            const float *__restrict__ lr_cols, int mode,
