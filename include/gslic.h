@@ -251,6 +251,16 @@ int gs_zbuffer(const float *points, int64_t m, const gs_camera *cam, int32_t wid
 int gs_init_rows(const float *points, const float *colors, const float *depths, int64_t m, float focal,
                  float *rows, void *stream);
 
+/* ---- photometric pose refinement (SURVEY.md 8f row 2, R/odometry.py:305-336) ------------- */
+/* img_mask[p] = |np.gradient(mean over channels of image)| > grad_gate (R/odometry.py:314-316) */
+int gs_track_mask(const float *image, int32_t width, int32_t height, float grad_gate, uint8_t *mask, void *stream);
+/* f->g_color *= img_mask & (f->opacity > opac_gate) (R/odometry.py:325-326) */
+int gs_track_grad(const gs_frame *f, const uint8_t *img_mask, float opac_gate, void *stream);
+/* One Adam step on the pose tangent (R/odometry.py:328-335): state (device FP64, 25) = rot_cw[9],
+ * trans_cw[3], m[6], v[6], iteration; rot <- exp_so3(step[3:]) rot, trans <- exp_so3(step[3:])
+ * trans + step[:3]; the view's camera (rot, trans, centre) is rewritten in place. */
+int gs_pose_adam(gs_view *view, double *state, const double *pose_grad, float lr, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SCENES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
-                if os.path.basename(p) not in ("losses.npz", "pose.npz", "keyframe.npz"))
+                if "entry_splat" in np.load(p).files)  # the forward/backward scenes
 IMG_TOL = 1e-4
 REL_TOL = 1e-3
 # screen-space (intermediate) gradients: the mean2d term sums pixel contributions of opposite
@@ -412,23 +412,21 @@ def test_pose_gradient_matches_reference(name):
     z, cam, g = load(name)
     out = R.forward(g, cam)
     grads, touched, pose = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"], with_pose=True)
+    # the pose chain itself, isolated from the blend: the oracle fed the screen-space gradients
+    # this very backward accumulated (still in the workspace) and the fp32 parameters
+    ws = out.ctx["workspace"]
+    g2 = _np(ws.g2d)[:, :10]
+    ocam = O.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, np.asarray(cam.rot_cw, np.float32),
+                    np.asarray(cam.trans_cw, np.float32))
+    _, opose = O.chain(z["rows"].astype(np.float32).astype(np.float64), ocam, g2, _np(touched).astype(bool),
+                       with_pose=True)
+    assert normwise(_np(pose), opose) < 1e-4, (_np(pose), opose)
     ref = p[f"{name}_pose"]
     # the pose sums every touched Gaussian's term; Gaussians within 5 cm of the camera carry the
     # fp32 blend rounding amplified ~100x (see test_loss_and_gradients_match_reference): 2e-2 there
     tol = 2e-2 if (z["pdepth"][z["touched"]] < 0.05).any() else REL_TOL
     assert normwise(_np(pose), ref) < tol, (_np(pose), ref)
     assert np.array_equal(_np(touched).astype(bool), z["touched"])
-    # the pose chain itself, isolated from the blend: the oracle fed the GPU's own screen-space
-    # gradients and fp32 parameters
-    g2d = R.backward_2d(out, z["g_color"], z["g_depth"], z["g_opac"])
-    n = len(z["rows"])
-    g2 = np.hstack([_np(g2d[0]).reshape(n, 2), _np(g2d[1]).reshape(n, 3), _np(g2d[2]).reshape(n, 1),
-                    _np(g2d[3]).reshape(n, 3), _np(g2d[4]).reshape(n, 1)])
-    ocam = O.Camera(cam.width, cam.height, cam.fx, cam.fy, cam.cx, cam.cy, np.asarray(cam.rot_cw, np.float32),
-                    np.asarray(cam.trans_cw, np.float32))
-    _, opose = O.chain(z["rows"].astype(np.float32).astype(np.float64), ocam, g2, _np(g2d[5]).astype(bool),
-                       with_pose=True)
-    assert normwise(_np(pose), opose) < 1e-4, (_np(pose), opose)
     g0, _, none = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
     assert none is None
     # (the backward's FP64 atomics are not bit-deterministic run to run)
@@ -595,3 +593,28 @@ def test_keyframe_preparation_on_device():
     assert np.max(np.abs(_np(kf2.colors) - z["g_colors"])) < 1e-6
     assert M.group_mapping_data(1, [pts], z["image"], cam, cfg, np.random.default_rng(3)) is None
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("name", ["small17", "s1_1500"])
+def test_photometric_refine_matches_reference(name):
+    """R/odometry.py:305-336 on the device (graph-captured: forward, tracking loss, masked
+    gradient, gs_chain_pose, gs_pose_adam): the pose after 1, 5 and 15 iterations and the final
+    loss follow the reference's trajectory from the same perturbed start."""
+    from paper_2507_04004_b200 import odometry as OD
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    t = np.load(os.path.join(GOLD, "track.npz"))
+    z = np.load(os.path.join(GOLD, name + ".npz"))
+    cam = R.Camera(int(z["width"]), int(z["height"]), float(z["fx"]), float(z["fy"]), float(z["cx"]),
+                   float(z["cy"]), z["rot_cw"], z["trans_cw"])
+    g = GaussianMap.from_rows(z["rows"])
+    start = cam.with_pose(t[f"{name}_rot0"], t[f"{name}_t0"])
+    for n in (1, 5, 15):
+        rot, trans, loss = OD.photometric_refine(g, t[f"{name}_image"], start, n_iters=n)
+        rref, tref = t[f"{name}_{n}_rot"], t[f"{name}_{n}_trans"]
+        assert np.max(np.abs(rot - rref)) < 2e-5 * n, (n, rot, rref)
+        assert np.max(np.abs(trans - tref)) < 2e-5 * n, (n, trans, tref)
+        lref = float(t[f"{name}_{n}_loss"])
+        assert abs(loss - lref) < 2e-3 * lref + 1e-5, (n, loss, lref)
+    # the refinement converges toward the true pose (the image is the rendering at it)
+    assert np.linalg.norm(trans - z["trans_cw"]) < np.linalg.norm(t[f"{name}_t0"] - z["trans_cw"])
