@@ -147,6 +147,7 @@ constexpr int TS_THREADS = 1024, TS_PER = 8;  // up to 8192 tiles in one pass (1
 
 __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int lazy) {
     __shared__ int32_t s_warp[2][32];
+    __shared__ int32_t s_pre[2][33];
     __shared__ int32_t s_carry[2];
     const int T = f.tiles_x * f.tiles_y;
     int32_t *cur = f.tile_scratch, *hcount = f.tile_scratch + T + 1, *boff = f.tile_scratch + 2 * (T + 1);
@@ -182,13 +183,26 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
             s_warp[1][warp] = xb;
         }
         __syncthreads();
-        int before = s_carry[0], bb = s_carry[1], total = 0, totb = 0;
-        for (int w = 0; w < TS_THREADS / 32; w++) {
-            before += w < warp ? s_warp[0][w] : 0;
-            bb += w < warp ? s_warp[1][w] : 0;
-            total += s_warp[0][w];
-            totb += s_warp[1][w];
+        if (warp == 0) {  // exclusive scan of the 32 warp totals by one warp
+            const int w0 = s_warp[0][lane], w1 = s_warp[1][lane];
+            int a0 = w0, a1 = w1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y0 = __shfl_up_sync(0xffffffffu, a0, o), y1 = __shfl_up_sync(0xffffffffu, a1, o);
+                if (lane >= o) {
+                    a0 += y0;
+                    a1 += y1;
+                }
+            }
+            s_pre[0][lane] = a0 - w0;
+            s_pre[1][lane] = a1 - w1;
+            if (lane == 31) {
+                s_pre[0][32] = a0;
+                s_pre[1][32] = a1;
+            }
         }
+        __syncthreads();
+        const int before = s_carry[0] + s_pre[0][warp], bb = s_carry[1] + s_pre[1][warp];
+        const int total = s_pre[0][32], totb = s_pre[1][32];
         int run = before + x - sx, runb = bb + xb - sb;  // exclusive prefix of this thread's first tile
 #pragma unroll
         for (int q = 0; q < TS_PER; q++) {

@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
 : > gpurun_out/sweep_$TAG.jsonl
 for C in S2r-500k-1280x720-32line S2r-1M-1280x720-32line S2r-1M-1280x720-16line S2r-1M-1280x720-64line \
-         S2r-1M-1280x720-128line S2r-1M-1280x720-livox5k S2r-1M-1280x720-livox200k S2r-2M-1920x1080-render \
+         S2r-1M-1280x720-128line S2r-1M-1280x720-livox5k S2r-1M-1280x720-livox200k S2r-2M-1920x1080-render S2r-1M-1280x720-track \
          S1-1M-1280x720 S1-10k-320x240; do
   timeout 600 python bench.py --config $C --steps 300 --warmup 5 --no-cpu-baseline >> gpurun_out/sweep_$TAG.jsonl \
       2>> gpurun_out/sweep_$TAG.err
