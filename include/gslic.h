@@ -198,6 +198,13 @@ int gs_render_bwd(const gs_frame *f, void *stream);
 int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
                   const gs_view *view, const float *lr_cols, void *stream);
 
+/* gs_chain_adam split over touched-list chunks so that the chain rule of chunk i+1 (stage 0,
+ * FP64-latency-bound) can run concurrently with the Adam stream of chunk i (stage 1, HBM-bound)
+ * on a second stream: stage 0 of a chunk must precede its stage 1; chunks are disjoint. */
+int gs_chain_adam_part(const gs_frame *f, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
+                       const gs_view *view, const float *lr_cols, int32_t stage, int32_t part, int32_t nparts,
+                       void *stream);
+
 /* R/rasterizer.py:559-644 only: grads[row] += d loss / d params (rows of GS_ROW floats);
  * touched_accum[i] |= touched[i]. */
 int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum, const gs_view *view,

@@ -79,6 +79,7 @@ def lib():
         "gs_loss": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, P]),
         "gs_render_bwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), P]),
         "gs_chain_adam": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P]),
+        "gs_chain_adam_part": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, i32, i32, i32, P]),
         "gs_chain": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P]),
         "gs_chain_pose": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P]),
         "gs_project_points": (ctypes.c_int, [P, i64, P, P, P, f32, P, P, P, P, P, P, P, P]),
@@ -103,7 +104,7 @@ def lib():
 
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
             "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_chain_adam",
-            "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
+            "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
             "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_track_mask", "gs_track_grad", "gs_pose_adam"]
 
 

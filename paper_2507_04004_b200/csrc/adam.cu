@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
                                                            int32_t *__restrict__ at, const gs_view *__restrict__ view,
                                                            const float *__restrict__ lr_cols, int mode,
                                                            float *__restrict__ grads, uint8_t *__restrict__ touched_accum,
-                                                           double *__restrict__ pose_out) {
+                                                           double *__restrict__ pose_out, int part, int nparts) {
     // one 32 x 65 staging tile per warp: parameter rows in, gradient rows out (in place)
     __shared__ float srow[CA_WARPS][32][RP];
     __shared__ float sbc[CA_WARPS][32][2];
@@ -218,8 +218,11 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     if (threadIdx.x == 0) scam = view->cam;
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
-    const int64_t k0 = ((int64_t)blockIdx.x * CA_WARPS + warp) * 32;
+    const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
+    // touched-list chunk `part` of `nparts` (warp-aligned bounds)
+    const int64_t kb = (ntt * part / nparts) & ~(int64_t)31;
+    const int64_t nt = part == nparts - 1 ? ntt : ((ntt * (part + 1) / nparts) & ~(int64_t)31);
+    const int64_t k0 = kb + ((int64_t)blockIdx.x * CA_WARPS + warp) * 32;
     if (k0 >= nt) return;
     const int64_t k = k0 + lane;
     const int g = k < nt ? f.touched_list[k] : -1;
@@ -348,9 +351,11 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
 // bias corrections produced by chain_kernel (mode 2) in the same order
 __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__restrict__ params,
                                                         float *__restrict__ am, float *__restrict__ av,
-                                                        const float *__restrict__ lr_cols) {
-    const int64_t nt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
-    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nt * 16;
+                                                        const float *__restrict__ lr_cols, int part, int nparts) {
+    const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
+    const int64_t kb = (ntt * part / nparts) & ~(int64_t)31;
+    const int64_t nt = part == nparts - 1 ? ntt : ((ntt * (part + 1) / nparts) & ~(int64_t)31);
+    for (int64_t idx = kb * 16 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nt * 16;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int64_t k = idx >> 4;
         const int c4 = (int)(idx & 15);
@@ -418,16 +423,17 @@ __global__ void adam_step_kernel(int32_t *__restrict__ at, const uint8_t *__rest
 using namespace gs;
 
 static int launch_chain(const gs_frame *f, float *params, float *m, float *v, int32_t *t, const gs_view *view,
-                        const float *lr, int mode, float *grads, uint8_t *acc, void *stream, double *pose = nullptr) {
+                        const float *lr, int mode, float *grads, uint8_t *acc, void *stream, double *pose = nullptr,
+                        int part = 0, int nparts = 1) {
     if (f->n == 0) return GS_OK;
-    const int64_t warps = (f->n + 31) / 32;
+    const int64_t warps = (f->n / nparts + 63) / 32;  // a chunk's upper bound (touched <= n)
     const unsigned blocks = (unsigned)((warps + CA_WARPS - 1) / CA_WARPS);
     if (pose)
         chain_kernel<true><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
-                                                                            acc, pose);
+                                                                            acc, pose, part, nparts);
     else
         chain_kernel<false><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
-                                                                             acc, nullptr);
+                                                                             acc, nullptr, part, nparts);
     return check_launch("chain_kernel");
 }
 
@@ -447,7 +453,23 @@ extern "C" int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, fl
     int rc = launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, split ? 2 : 0, nullptr, nullptr, stream);
     if (rc || !split) return rc;
     if (f->n == 0) return GS_OK;
-    adam_list_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols);
+    adam_list_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols, 0, 1);
+    return check_launch("adam_list_kernel");
+}
+
+extern "C" int gs_chain_adam_part(const gs_frame *f, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
+                                  const gs_view *view, const float *lr_cols, int32_t stage, int32_t part,
+                                  int32_t nparts, void *stream) {
+    if (!params || !adam_m || !adam_v || !adam_t || !view || !lr_cols || nparts < 1 || part < 0 || part >= nparts ||
+        (stage != 0 && stage != 1)) {
+        set_error("gs_chain_adam_part: bad arguments");
+        return GS_ERR_ARG;
+    }
+    if (f->n == 0) return GS_OK;
+    if (stage == 0)  // chain rule of the chunk: compact gradient rows + bias corrections, t bumped
+        return launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 2, nullptr, nullptr, stream, nullptr,
+                            part, nparts);
+    adam_list_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols, part, nparts);
     return check_launch("adam_list_kernel");
 }
 

@@ -107,6 +107,9 @@ class MapOptimizer:
         self._events = [None] * 4
         self._steps = 0
         self._grow = False
+        import os
+        self.overlap_parts = int(os.environ.get("GSLIC_OVERLAP_PARTS", "0"))
+        self._side = torch.cuda.Stream(device=self.dev)
 
     # -- one iteration: R/mapper.py:249-256 --------------------------------------------
     def _launch(self) -> None:
@@ -116,9 +119,29 @@ class MapOptimizer:
         call("gs_render_fwd", f, 1, s)
         call("gs_loss", f, cur, self.lam, self.xi, s)
         call("gs_render_bwd", f, s)
-        call("gs_chain_adam", f, self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
-             self.adam.t.data_ptr(), cur, self.lr.data_ptr(), s)
+        self._chain_adam()
         self.loss_acc += self.ws.loss[0:1]
+
+    def _chain_adam(self) -> None:
+        """Chain rule + sparse Adam.  overlap_parts > 1: the touched list is cut into chunks; the
+        FP64 chain of chunk i+1 runs on this stream while the HBM-bound Adam stream of chunk i runs
+        on a side stream (gs_chain_adam_part), so latency-bound math and bandwidth overlap."""
+        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+        args = (self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
+                self.adam.t.data_ptr(), cur, self.lr.data_ptr())
+        P = self.overlap_parts
+        if P <= 1:
+            call("gs_chain_adam", f, *args, s)
+            return
+        main = torch.cuda.current_stream()
+        for i in range(P):
+            call("gs_chain_adam_part", f, *args, 0, i, P, stream_ptr())
+            ev = torch.cuda.Event()
+            ev.record(main)
+            self._side.wait_event(ev)
+            with torch.cuda.stream(self._side):
+                call("gs_chain_adam_part", f, *args, 1, i, P, stream_ptr())
+        main.wait_stream(self._side)
 
     def capture(self) -> None:
         """Capture the launch sequence into a CUDA graph (replayed by step())."""
@@ -180,8 +203,7 @@ class MapOptimizer:
         ev[4].record()
         call("gs_render_bwd", f, s)
         ev[5].record()
-        call("gs_chain_adam", f, self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
-             self.adam.t.data_ptr(), cur, self.lr.data_ptr(), s)
+        self._chain_adam()
         ev[6].record()
         ev[6].synchronize()
         return {p: ev[i].elapsed_time(ev[i + 1]) for i, p in enumerate(self.PHASES)}
