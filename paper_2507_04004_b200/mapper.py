@@ -74,6 +74,81 @@ class Keyframe:
     stamp: float = 0.0
 
 
+class HostKeyframes:
+    """Keyframes in pinned host memory -- the target image and the LiDAR returns as a K-list
+    (pixel index, depth; compacted once here, as the device path caches it) -- streamed into two
+    device slots: the upload of keyframe j+1 (copy stream) overlaps iteration j.  `cur` is the
+    engine's device gs_view that the captured iteration reads."""
+
+    def __init__(self, keyframes, width: int, height: int, cur: torch.Tensor, device):
+        h, w = int(height), int(width)
+        self.cur, self.dev = cur, device
+        self.img, self.idx, self.z = [], [], []
+        for kf in keyframes:
+            self.img.append(torch.as_tensor(np.asarray(kf.image, dtype=np.float32)).reshape(h, w, 3).pin_memory())
+            sd = np.asarray(kf.sparse_depth, dtype=np.float32).reshape(-1) if kf.sparse_depth is not None else \
+                np.zeros(h * w, np.float32)
+            idx = np.flatnonzero(sd > 0).astype(np.int32)  # pixel order, as gs_lidar_compact
+            self.idx.append(torch.as_tensor(idx).pin_memory())
+            self.z.append(torch.as_tensor(sd[idx]).pin_memory())
+        kmax = max(1, max(len(i) for i in self.idx))
+        self.slots = [{"img": torch.empty((h, w, 3), device=device),
+                       "idx": torch.empty(kmax, dtype=torch.int32, device=device),
+                       "z": torch.empty(kmax, device=device), "view": torch.empty_like(cur)} for _ in range(2)]
+        self.views = []  # per keyframe, per slot: the gs_view pointing at that slot's buffers
+        for k, kf in enumerate(keyframes):
+            per = []
+            for sl in self.slots:
+                v = _lib.GsView()
+                v.cam = camera_from(kf.cam).struct()
+                v.target, v.lidar_idx, v.lidar_z = sl["img"].data_ptr(), sl["idx"].data_ptr(), sl["z"].data_ptr()
+                v.lidar_k = len(self.idx[k])
+                per.append(torch.frombuffer(bytearray(bytes(memoryview(v).cast("B"))), dtype=torch.uint8).pin_memory())
+            self.views.append(per)
+        self.copy_stream = torch.cuda.Stream(device=device)
+        self.slot_free = [None, None]
+        nbytes = [self.img[k].numel() * 4 + self.idx[k].numel() * 8 + self.views[k][0].numel()
+                  for k in range(len(keyframes))]
+        self.h2d_bytes = int(round(float(np.mean(nbytes))))
+
+    def upload(self, j: int, k: int) -> torch.cuda.Event:
+        """H2D of keyframe k into slot j % 2 on the copy stream, once the iteration that last read
+        that slot has finished; returns the event marking the slot ready."""
+        s = j % 2
+        sl, cs = self.slots[s], self.copy_stream
+        with torch.cuda.stream(cs):
+            if self.slot_free[s] is not None:
+                cs.wait_event(self.slot_free[s])
+            kk = self.idx[k].numel()
+            sl["img"].copy_(self.img[k], non_blocking=True)
+            if kk:
+                sl["idx"][:kk].copy_(self.idx[k], non_blocking=True)
+                sl["z"][:kk].copy_(self.z[k], non_blocking=True)
+            sl["view"].copy_(self.views[k][s], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        return ev
+
+    def stream(self, order, body) -> None:
+        """For j, k in enumerate(order): keyframe k lands in `cur`'s slot, then body(j, k) runs the
+        iteration on the current stream; keyframe j+1 uploads meanwhile."""
+        main = torch.cuda.current_stream()
+        order = [int(k) for k in order]
+        if not order:
+            return
+        self.copy_stream.wait_stream(main)  # uploads start after the work queued so far
+        ready = self.upload(0, order[0])
+        for j, k in enumerate(order):
+            nxt = self.upload(j + 1, order[j + 1]) if j + 1 < len(order) else None
+            main.wait_event(ready)
+            self.cur.copy_(self.slots[j % 2]["view"])
+            body(j, k)
+            free = torch.cuda.Event()
+            free.record(main)
+            self.slot_free[j % 2] = free
+            ready = nxt
+
+
 class MapOptimizer:
     """Device-resident map-optimisation iterations over a fixed keyframe set."""
 
@@ -210,95 +285,33 @@ class MapOptimizer:
 
     # -- streaming keyframes from host memory (the e2e path) ---------------------------------
     def attach_host_keyframes(self, keyframes) -> None:
-        """Keep keyframes in pinned host memory -- the target image and the LiDAR returns as a
-        K-list (pixel index, depth; compacted once here, as the device path caches it) -- and set
-        up two device slots: run_host() uploads keyframe j+1 into one while iteration j reads the
-        other."""
-        h, w = self.H, self.W
-        self._h_img, self._h_idx, self._h_z = [], [], []
-        for kf in keyframes:
-            self._h_img.append(torch.as_tensor(np.asarray(kf.image, dtype=np.float32)).reshape(h, w, 3).pin_memory())
-            sd = np.asarray(kf.sparse_depth, dtype=np.float32).reshape(-1) if kf.sparse_depth is not None else \
-                np.zeros(h * w, np.float32)
-            idx = np.flatnonzero(sd > 0).astype(np.int32)  # pixel order, as gs_lidar_compact
-            self._h_idx.append(torch.as_tensor(idx).pin_memory())
-            self._h_z.append(torch.as_tensor(sd[idx]).pin_memory())
-        kmax = max(1, max(len(i) for i in self._h_idx))
-        self._slots = []
-        for _ in range(2):
-            self._slots.append({"img": torch.empty((h, w, 3), device=self.dev),
-                                "idx": torch.empty(kmax, dtype=torch.int32, device=self.dev),
-                                "z": torch.empty(kmax, device=self.dev),
-                                "view": torch.empty_like(self.cur)})
-        self._h_view = []  # per keyframe, per slot: the gs_view pointing at that slot's buffers
-        for k, kf in enumerate(keyframes):
-            per = []
-            for sl in self._slots:
-                v = _lib.GsView()
-                v.cam = camera_from(kf.cam).struct()
-                v.target, v.lidar_idx, v.lidar_z = sl["img"].data_ptr(), sl["idx"].data_ptr(), sl["z"].data_ptr()
-                v.lidar_k = len(self._h_idx[k])
-                raw = bytes(memoryview(v).cast("B"))
-                per.append(torch.frombuffer(bytearray(raw), dtype=torch.uint8).pin_memory())
-            self._h_view.append(per)
-        self._copy_stream = torch.cuda.Stream(device=self.dev)
-        self._slot_free = [None, None]
+        """Keep keyframes in pinned host memory (HostKeyframes); run_host() uploads keyframe j+1
+        on a copy stream while iteration j runs."""
+        self.host = HostKeyframes(keyframes, self.W, self.H, self.cur, self.dev)
+        self.h2d_bytes, self.d2h_bytes = self.host.h2d_bytes, 8
         self._h_loss = torch.zeros(1024, dtype=torch.float64).pin_memory()
-        nbytes = [self._h_img[k].numel() * 4 + self._h_idx[k].numel() * 8 + self._h_view[k][0].numel()
-                  for k in range(len(keyframes))]
-        self.h2d_bytes = int(round(float(np.mean(nbytes))))
-        self.d2h_bytes = 8
         self._host_steps = 0
-
-    def _upload(self, j: int, k: int) -> torch.cuda.Event:
-        """H2D of host keyframe k into slot j % 2 on the copy stream, once the iteration that last
-        read that slot has finished; returns the event marking the slot ready."""
-        s = j % 2
-        sl, cs = self._slots[s], self._copy_stream
-        with torch.cuda.stream(cs):
-            if self._slot_free[s] is not None:
-                cs.wait_event(self._slot_free[s])
-            kk = self._h_idx[k].numel()
-            sl["img"].copy_(self._h_img[k], non_blocking=True)
-            if kk:
-                sl["idx"][:kk].copy_(self._h_idx[k], non_blocking=True)
-                sl["z"][:kk].copy_(self._h_z[k], non_blocking=True)
-            sl["view"].copy_(self._h_view[k][s], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(cs)
-        return ev
 
     def run_host(self, order) -> None:
         """Map-optimisation iterations over host keyframes `order` (R/mapper.py:242-256 samples
         the keyframe order up front): keyframe j+1 is uploaded on a copy stream while iteration j
         runs; each iteration's loss is read back into pinned host memory (D2H)."""
-        main = torch.cuda.current_stream()
-        order = [int(k) for k in order]
-        if not order:
-            return
-        self._copy_stream.wait_stream(main)  # uploads start after the work queued so far
-        ready = self._upload(0, order[0])
-        for j, k in enumerate(order):
-            nxt = self._upload(j + 1, order[j + 1]) if j + 1 < len(order) else None
+        def body(j, k):
             self._check()
-            main.wait_event(ready)
-            self.cur.copy_(self._slots[j % 2]["view"])
             if self.graph is not None:
                 self.graph.replay()
             else:
                 self._launch()
             self._h_loss[self._host_steps % 1024].copy_(self.ws.loss[0], non_blocking=True)
             self._host_steps += 1
-            free = torch.cuda.Event()
-            free.record(main)
-            self._slot_free[j % 2] = free
             s = self._steps % 4
             self._ring[s].copy_(self.ws.counters[:8], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record()
             self._events[s] = ev
             self._steps += 1
-            ready = nxt
+
+        self.host.stream(order, body)
 
     def step_host(self, k: int, slot: int = 0) -> None:
         """One iteration on host keyframe k (no prefetch): run_host([k])."""

@@ -72,6 +72,9 @@ class BatchMapOptimizer:
     def accumulate(self, k: int) -> None:
         """forward -> loss -> backward -> chain rule of view k into (grads, touched)."""
         self.cur.copy_(self.views[k].buf)
+        self._accumulate_cur()
+
+    def _accumulate_cur(self) -> None:
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
@@ -81,11 +84,39 @@ class BatchMapOptimizer:
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
         self.loss_acc += self.ws.loss[0:1]
 
+    def attach_host_keyframes(self, keyframes) -> None:
+        """Keyframes in pinned host memory, streamed per view (mapper.HostKeyframes)."""
+        from .mapper import HostKeyframes
+        self.host = HostKeyframes(keyframes, self.W, self.H, self.cur, self.dev)
+        self.h2d_bytes_per_view = self.host.h2d_bytes
+        self._h_loss = torch.zeros(1, dtype=torch.float64).pin_memory()
+
+    def step_host(self, view_ids) -> None:
+        """One batch over host keyframes: each view's image + K-list uploaded while the previous
+        view runs, then the allreduce and the Adam step; the batch loss is read back (D2H)."""
+        self.grads.zero_()
+        self.touched.zero_()
+        self.host.stream(view_ids, lambda j, k: self._accumulate_cur())
+        self._finish()
+        self._h_loss.copy_(self.loss_acc, non_blocking=True)
+
     def step(self, view_ids) -> None:
         self.grads.zero_()
         self.touched.zero_()
         for k in view_ids:
             self.accumulate(int(k))
+        self._finish()
+
+    def save_state(self) -> tuple:
+        a = self.adam
+        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t))
+
+    def restore_state(self, state: tuple) -> None:
+        a = self.adam
+        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t), state):
+            dst.copy_(src)
+
+    def _finish(self) -> None:
         allreduce_grads(self.grads, self.touched, self.group)
         call("gs_adam", self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
              self.adam.t.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), len(self.g),
