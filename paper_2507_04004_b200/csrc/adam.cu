@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
                                                            const float *__restrict__ lr_cols, int mode,
                                                            float *__restrict__ grads, uint8_t *__restrict__ touched_accum,
                                                            double *__restrict__ pose_out, int part, int nparts) {
+    pdl_wait();
     // one 32 x 65 staging tile per warp: parameter rows in, gradient rows out (in place)
     __shared__ float srow[CA_WARPS][32][RP];
     __shared__ float sbc[CA_WARPS][32][2];
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
 __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__restrict__ params,
                                                         float *__restrict__ am, float *__restrict__ av,
                                                         const float *__restrict__ lr_cols, int part, int nparts) {
+    pdl_wait();
     const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
     const int64_t kb = (ntt * part / nparts) & ~(int64_t)31;
     const int64_t nt = part == nparts - 1 ? ntt : ((ntt * (part + 1) / nparts) & ~(int64_t)31);
@@ -387,6 +389,7 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
 __global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, float *__restrict__ av,
                             int32_t *__restrict__ at, const float *__restrict__ grads,
                             const uint8_t *__restrict__ touched, int64_t n, const float *__restrict__ lr_cols) {
+    pdl_wait();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= n * 16) return;
     const int64_t row = idx >> 4;
@@ -414,6 +417,7 @@ __global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, 
 
 // step counters advance after the update kernel has read them (no intra-kernel race)
 __global__ void adam_step_kernel(int32_t *__restrict__ at, const uint8_t *__restrict__ touched, int64_t n) {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n && touched[i]) at[i] += 1;
 }
@@ -429,10 +433,10 @@ static int launch_chain(const gs_frame *f, float *params, float *m, float *v, in
     const int64_t warps = (f->n / nparts + 63) / 32;  // a chunk's upper bound (touched <= n)
     const unsigned blocks = (unsigned)((warps + CA_WARPS - 1) / CA_WARPS);
     if (pose)
-        chain_kernel<true><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
+        launch_pdl(chain_kernel<true>, blocks, CA_THREADS, 0, (cudaStream_t)stream, *f, params, m, v, t, view, lr, mode, grads,
                                                                             acc, pose, part, nparts);
     else
-        chain_kernel<false><<<blocks, CA_THREADS, 0, (cudaStream_t)stream>>>(*f, params, m, v, t, view, lr, mode, grads,
+        launch_pdl(chain_kernel<false>, blocks, CA_THREADS, 0, (cudaStream_t)stream, *f, params, m, v, t, view, lr, mode, grads,
                                                                              acc, nullptr, part, nparts);
     return check_launch("chain_kernel");
 }
@@ -453,7 +457,7 @@ extern "C" int gs_chain_adam(const gs_frame *f, float *params, float *adam_m, fl
     int rc = launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, split ? 2 : 0, nullptr, nullptr, stream);
     if (rc || !split) return rc;
     if (f->n == 0) return GS_OK;
-    adam_list_kernel<<<8 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols, 0, 1);
+    launch_pdl(adam_list_kernel, 8 * 148, 256, 0, (cudaStream_t)stream, *f, params, adam_m, adam_v, lr_cols, 0, 1);
     return check_launch("adam_list_kernel");
 }
 
@@ -469,7 +473,7 @@ extern "C" int gs_chain_adam_part(const gs_frame *f, float *params, float *adam_
     if (stage == 0)  // chain rule of the chunk: compact gradient rows + bias corrections, t bumped
         return launch_chain(f, params, adam_m, adam_v, adam_t, view, lr_cols, 2, nullptr, nullptr, stream, nullptr,
                             part, nparts);
-    adam_list_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(*f, params, adam_m, adam_v, lr_cols, part, nparts);
+    launch_pdl(adam_list_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, *f, params, adam_m, adam_v, lr_cols, part, nparts);
     return check_launch("adam_list_kernel");
 }
 
@@ -502,11 +506,11 @@ extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *ada
                        const uint8_t *touched, int64_t n, const float *lr_cols, void *stream) {
     if (n == 0) return GS_OK;
     const int64_t work = n * 16;
-    adam_kernel<<<(unsigned)((work + 255) / 256), 256, 0, (cudaStream_t)stream>>>(params, adam_m, adam_v, adam_t, grads,
+    launch_pdl(adam_kernel, (unsigned)((work + 255) / 256), 256, 0, (cudaStream_t)stream, params, adam_m, adam_v, adam_t, grads,
                                                                                    touched, n, lr_cols);
     int rc = check_launch("adam_kernel");
     if (rc) return rc;
-    adam_step_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(adam_t, touched, n);
+    launch_pdl(adam_step_kernel, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, adam_t, touched, n);
     return check_launch("adam_step_kernel");
 }
 

@@ -55,6 +55,7 @@ __device__ __forceinline__ void for_kept_tiles(const gs_frame &f, int g, F fn) {
 
 // cull=False: every valid Gaussian lands in every tile (R/rasterizer.py:195-199)
 __global__ void nocull_kernel(gs_frame f) {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     bool v = false;
     if (i < f.n) {
@@ -68,6 +69,7 @@ __global__ void nocull_kernel(gs_frame f) {
 // 1) per-tile bucket counts for cull=False (every tile holds every valid Gaussian); with the
 // cull they are counted where the cull decides (preprocess_kernel, big_finish_kernel)
 __global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f) {
+    pdl_wait();
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     const int T = f.tiles_x * f.tiles_y;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < T; t += (int64_t)gridDim.x * blockDim.x)
@@ -84,6 +86,7 @@ constexpr int HS_GROUPS = 16;
 constexpr int HS_THREADS = HS_KEYS * HS_GROUPS;
 
 __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
+    pdl_wait();
     __shared__ uint64_t s_key[GS_HUGE_CAP];
     __shared__ int s_part[HS_GROUPS][HS_KEYS];
     const int nh = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
@@ -117,6 +120,7 @@ __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
 // t (a 32 x 32 bit transpose per warp of huge_mask_t rows, which the big_* cull kernels wrote
 // by slot), plus the per-tile huge counts (tile_scratch[T+1 ..))
 __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
+    pdl_wait();
     const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
     const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
     const int lane = threadIdx.x & 31;
@@ -146,6 +150,7 @@ __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
 constexpr int TS_THREADS = 1024, TS_PER = 8;  // up to 8192 tiles in one pass (1080p: 8160)
 
 __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int lazy) {
+    pdl_wait();
     __shared__ int32_t s_warp[2][32];
     __shared__ int32_t s_pre[2][33];
     __shared__ int32_t s_carry[2];
@@ -239,6 +244,7 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
 
 // 5) every bucketed pair's key into its tile's bucket (keys_b), unordered
 __global__ void __launch_bounds__(256) bucket_fill_kernel(gs_frame f, int cull) {
+    pdl_wait();
     if (f.counters[GS_CNT_OVERFLOW]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     int32_t *cur = f.tile_scratch;
@@ -288,6 +294,7 @@ struct SortMergeSmem {
 };
 
 __global__ void __launch_bounds__(SM_THREADS) tile_sort_merge_kernel(gs_frame f) {
+    pdl_wait();
     extern __shared__ uint64_t sm_raw[];
     SortMergeSmem &sm = *reinterpret_cast<SortMergeSmem *>(sm_raw);
     const int T = f.tiles_x * f.tiles_y;
@@ -339,22 +346,22 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         cudaMemsetAsync(f->counters + GS_CNT_HUGE, 0, sizeof(int32_t) * 2, st);
         cudaMemsetAsync(f->counters + GS_CNT_HUGE_N, 0, sizeof(int32_t), st);
         cudaMemsetAsync(f->tile_scratch + T + 1, 0, sizeof(int32_t) * ((size_t)T + 1), st);  // no huge
-        nocull_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(*f);
+        launch_pdl(nocull_kernel, (unsigned)((n + 255) / 256), 256, 0, st, *f);
         if ((rc = check_launch("nocull_kernel"))) return rc;
-        bucket_count_kernel<<<4 * 148, 256, 0, st>>>(*f);
+        launch_pdl(bucket_count_kernel, 4 * 148, 256, 0, st, *f);
         if ((rc = check_launch("bucket_count_kernel"))) return rc;
     }
     if (cull) {  // the bucket counts come from the cull (preprocess, big_finish)
-        huge_sort_kernel<<<GS_HUGE_CAP / HS_KEYS, HS_THREADS, 0, st>>>(*f);
+        launch_pdl(huge_sort_kernel, GS_HUGE_CAP / HS_KEYS, HS_THREADS, 0, st, *f);
         if ((rc = check_launch("huge_sort_kernel"))) return rc;
-        huge_transpose_kernel<<<dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st>>>(*f);
+        launch_pdl(huge_transpose_kernel, dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st, *f);
         if ((rc = check_launch("huge_transpose_kernel"))) return rc;
     }
-    tile_scan_kernel<<<1, TS_THREADS, 0, st>>>(*f, lazy ? 1 : 0);
+    launch_pdl(tile_scan_kernel, 1, TS_THREADS, 0, st, *f, lazy ? 1 : 0);
     if ((rc = check_launch("tile_scan_kernel"))) return rc;
     if (lazy) return GS_OK;  // buckets filled, sorted and merged on demand by gs_render_fwd
-    bucket_fill_kernel<<<4 * 148, 256, 0, st>>>(*f, cull);
+    launch_pdl(bucket_fill_kernel, 4 * 148, 256, 0, st, *f, cull);
     if ((rc = check_launch("bucket_fill_kernel"))) return rc;
-    tile_sort_merge_kernel<<<T, SM_THREADS, sizeof(SortMergeSmem), st>>>(*f);
+    launch_pdl(tile_sort_merge_kernel, T, SM_THREADS, sizeof(SortMergeSmem), st, *f);
     return check_launch("tile_sort_merge_kernel");
 }

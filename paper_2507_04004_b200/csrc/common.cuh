@@ -1,5 +1,6 @@
 // common.cuh -- shared device helpers for the sm_100a map-optimisation kernels.
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -27,6 +28,28 @@ constexpr int HSTAGE = HKEYS + 2 * GS_HUGE_CAP;  // unsorted keys staged by big_
 // error plumbing (thread-local, no global mutable state shared across threads)
 void set_error(const char *fmt, ...);
 int check_launch(const char *what);
+
+// Programmatic dependent launch: every kernel of the library is launched with programmatic
+// stream serialisation and waits for its predecessor's completion (and memory flush) as its
+// first action, so its launch and block scheduling overlap the predecessor's tail instead of
+// following it.  Outside a PDL launch griddepcontrol.wait returns at once.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                              Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // SH constants, R/gaussians.py:24-30

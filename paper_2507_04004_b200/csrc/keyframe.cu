@@ -43,6 +43,7 @@ __global__ void project_points_kernel(const float *__restrict__ points, int64_t 
                                       const float *__restrict__ image, const float *__restrict__ opacity, float tau,
                                       float *u, float *v, int32_t *ui, int32_t *vi, float *z, uint8_t *flags,
                                       float *colors) {
+    pdl_wait();
     __shared__ gs_camera cam;
     if (threadIdx.x == 0) cam = *camp;
     __syncthreads();
@@ -78,12 +79,14 @@ __global__ void project_points_kernel(const float *__restrict__ points, int64_t 
 }
 
 __global__ void zbuffer_fill_kernel(uint32_t *zbuf, int64_t npx) {
+    pdl_wait();
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x)
         zbuf[p] = 0xffffffffu;
 }
 
 __global__ void zbuffer_kernel(const float *__restrict__ points, int64_t m, const gs_camera *__restrict__ camp,
                                uint32_t *zbuf) {
+    pdl_wait();
     __shared__ gs_camera cam;
     if (threadIdx.x == 0) cam = *camp;
     __syncthreads();
@@ -95,6 +98,7 @@ __global__ void zbuffer_kernel(const float *__restrict__ points, int64_t m, cons
 }
 
 __global__ void zbuffer_finish_kernel(const uint32_t *__restrict__ zbuf, float *depth, int64_t npx) {
+    pdl_wait();
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t b = zbuf[p];
         depth[p] = b == 0xffffffffu ? 0.0f : __uint_as_float(b);
@@ -105,6 +109,7 @@ __global__ void zbuffer_finish_kernel(const uint32_t *__restrict__ zbuf, float *
 // opacity logit(0.1), sh_low = (colour - 0.5) / C0, sh_high = 0; padding columns 0
 __global__ void init_rows_kernel(const float *__restrict__ points, const float *__restrict__ colors,
                                  const float *__restrict__ depths, int64_t m, float focal, float *rows) {
+    pdl_wait();
     const double C0 = 0.28209479177387814, logit01 = log(0.1 / 0.9);
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < m * 16;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -143,7 +148,7 @@ extern "C" int gs_project_points(const float *points, int64_t m, const gs_camera
         return GS_ERR_ARG;
     }
     if (m == 0) return GS_OK;
-    project_points_kernel<<<grid_for(m), 256, 0, (cudaStream_t)stream>>>(points, m, cam, image, opacity, tau, u, v,
+    launch_pdl(project_points_kernel, grid_for(m), 256, 0, (cudaStream_t)stream, points, m, cam, image, opacity, tau, u, v,
                                                                         ui, vi, z, flags, colors);
     return check_launch("project_points_kernel");
 }
@@ -156,14 +161,14 @@ extern "C" int gs_zbuffer(const float *points, int64_t m, const gs_camera *cam, 
     }
     const int64_t npx = (int64_t)width * height;
     cudaStream_t st = (cudaStream_t)stream;
-    zbuffer_fill_kernel<<<grid_for(npx), 256, 0, st>>>(zbuf, npx);
+    launch_pdl(zbuffer_fill_kernel, grid_for(npx), 256, 0, st, zbuf, npx);
     int rc = check_launch("zbuffer_fill_kernel");
     if (rc) return rc;
     if (m > 0) {
-        zbuffer_kernel<<<grid_for(m), 256, 0, st>>>(points, m, cam, zbuf);
+        launch_pdl(zbuffer_kernel, grid_for(m), 256, 0, st, points, m, cam, zbuf);
         if ((rc = check_launch("zbuffer_kernel"))) return rc;
     }
-    zbuffer_finish_kernel<<<grid_for(npx), 256, 0, st>>>(zbuf, depth, npx);
+    launch_pdl(zbuffer_finish_kernel, grid_for(npx), 256, 0, st, zbuf, depth, npx);
     return check_launch("zbuffer_finish_kernel");
 }
 
@@ -174,6 +179,6 @@ extern "C" int gs_init_rows(const float *points, const float *colors, const floa
         return GS_ERR_ARG;
     }
     if (m == 0) return GS_OK;
-    init_rows_kernel<<<grid_for(m * 16), 256, 0, (cudaStream_t)stream>>>(points, colors, depths, m, focal, rows);
+    launch_pdl(init_rows_kernel, grid_for(m * 16), 256, 0, (cudaStream_t)stream, points, colors, depths, m, focal, rows);
     return check_launch("init_rows_kernel");
 }

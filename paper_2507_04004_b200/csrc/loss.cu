@@ -45,6 +45,7 @@ __device__ __forceinline__ int reflect_idx(int j, int n) {  // R/losses.py:31-42
 // Tables per axis, 22 floats per position: F[q][d+5] (blur) then A[p][d+5] = F[p+d][5-d]
 // (adjoint, zero where p+d leaves the axis).  Layout: x axis (w positions) then y axis.
 __global__ void loss_tables_kernel(float *tab_x, int w, float *tab_y, int h) {
+    pdl_wait();
     // the tables depend only on (w, h): loss_finalize_kernel stamps them valid after first use
     const int *stamp = reinterpret_cast<const int *>(tab_y + 22 * h);
     if (stamp[0] == (w << 16) + h && stamp[1] == ~((w << 16) + h)) return;
@@ -348,6 +349,7 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
 __global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
                                                                const float *__restrict__ tab_x,
                                                                const float *__restrict__ tab_y, float lam) {
+    pdl_wait();
     __shared__ SsimSmem sm;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
     if (x0 >= 10 && x0 + TW + 10 <= f.width && y0 >= 10 && y0 + TH + 10 <= f.height)
@@ -359,6 +361,7 @@ __global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
 __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_view *__restrict__ view, float xi,
                                                          int64_t part0) {
+    pdl_wait();
     __shared__ float red[8];
     const int32_t K = view->lidar_k;
     const int32_t *idx = view->lidar_idx;
@@ -392,6 +395,7 @@ static_assert(LF_THREADS % 3 == 1, "component bookkeeping of loss_finalize_kerne
 
 __global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
                                      float xi, float *tab_stamp) {
+    pdl_wait();
     // 1024 threads, coalesced over the flat (nparts x 3) array with 4 loads in flight each, then
     // a fixed-order shuffle tree: deterministic, and latency-bound only ~2 round trips deep
     __shared__ double r[3][32];
@@ -465,15 +469,15 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     }
     float *tab_x = reinterpret_cast<float *>(f->loss_parts + 3 * f->loss_blocks);
     float *tab_y = tab_x + 22 * f->width;
-    loss_tables_kernel<<<(f->width + f->height + 127) / 128, 128, 0, st>>>(tab_x, f->width, tab_y, f->height);
+    launch_pdl(loss_tables_kernel, (f->width + f->height + 127) / 128, 128, 0, st, tab_x, f->width, tab_y, f->height);
     int rc = check_launch("loss_tables_kernel");
     if (rc) return rc;
     dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
-    ssim_l1_kernel<<<grid, L_THREADS, 0, st>>>(*f, view, tab_x, tab_y, lam);
+    launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
-    depth_loss_kernel<<<DEPTH_BLOCKS, 256, 0, st>>>(*f, view, xi, ssim_blocks);
+    launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, xi, ssim_blocks);
     if ((rc = check_launch("depth_loss_kernel"))) return rc;
-    loss_finalize_kernel<<<1, LF_THREADS, 0, st>>>(*f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
+    launch_pdl(loss_finalize_kernel, 1, LF_THREADS, 0, st, *f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
     return check_launch("loss_finalize_kernel");
 }
 

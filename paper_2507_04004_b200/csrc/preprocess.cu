@@ -79,6 +79,7 @@ __device__ __forceinline__ float3 pp_colour(const PPGeom &g, const PPSh &sh, int
 template <bool LAZY_SH>
 __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, const float *__restrict__ params,
                                                                 const gs_view *__restrict__ view) {
+    pdl_wait();
     extern __shared__ float4 pp_raw[];
     PPWarp *ws_all = reinterpret_cast<PPWarp *>(pp_raw);
     __shared__ gs_camera scam;
@@ -369,6 +370,7 @@ constexpr int CB_BSTRIDE = 64;  // threads per Gaussian in big_bands_kernel (ban
 // K0: thread per large-footprint Gaussian: huge slot or bitmap base (warp-aggregated
 // reservations: one atomic per warp and counter)
 __global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_huge) {
+    pdl_wait();
     const int64_t nb = f.counters[GS_CNT_BIG];
     const int lane = threadIdx.x & 31;
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_hu
 }
 
 __global__ void __launch_bounds__(256, 3) big_bands_kernel(gs_frame f) {
+    pdl_wait();
     const int lane = threadIdx.x & 31;
     const int64_t nb = f.counters[GS_CNT_BIG];
     const int64_t cap = f.cull_queue_cap;
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(256, 3) big_bands_kernel(gs_frame f) {
 // K2: thread per band-ambiguous tile: per-tile bounds; the tiles the qcut boundary actually
 // crosses get the exact per-row test cooperatively, 8 lanes per tile (two pixel rows each)
 __global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
+    pdl_wait();
     const int64_t cap = f.cull_queue_cap;
     const int64_t n1 = min((int64_t)f.counters[GS_CNT_CULLQ1], cap);
     const int2 *q1 = reinterpret_cast<const int2 *>(f.cull_queue);
@@ -567,6 +571,7 @@ __global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
 
 // K3: per large-footprint Gaussian: touched, depth key, huge encoding, touched list
 __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
+    pdl_wait();
     const int64_t nb = f.counters[GS_CNT_BIG];
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = b0 + threadIdx.x;  // uniform trip count: warp_append is warp-wide
@@ -625,6 +630,7 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
 __global__ void project_kernel(const float *__restrict__ params, int64_t n, const gs_camera *__restrict__ camp,
                                float *mu_cam, float *mean2d, float *cov2d, float *conic, float *depth,
                                uint8_t *valid, float *jproj, float *mmat, float *cov3d) {
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     gs_camera cam = *camp;
@@ -662,6 +668,7 @@ __global__ void project_kernel(const float *__restrict__ params, int64_t n, cons
 
 __global__ void eval_sh_kernel(const float *__restrict__ sh_low, const float *__restrict__ sh_high,
                                const float *__restrict__ dirs, int64_t n, float *colors, float *preclamp) {
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float b[16];
@@ -680,6 +687,7 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
                             const float *__restrict__ cov2d3, const float *__restrict__ opac,
                             const float *__restrict__ depth, const uint8_t *__restrict__ valid,
                             const float *__restrict__ colors) {
+    pdl_wait();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= f.n) return;
     float mx = mean2d[2 * i], my = mean2d[2 * i + 1];
@@ -714,6 +722,7 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
 // the touched and large-footprint lists of the pack path (unordered; consumers are order
 // independent)
 __global__ void touched_list_kernel(gs_frame f) {
+    pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int k = i < f.n ? f.kept[i] : 0;
     if (k < 0) f.kept[i] = 0;
@@ -726,6 +735,7 @@ __global__ void touched_list_kernel(gs_frame f) {
 constexpr int LC_CHUNK = 1024;
 
 __global__ void lidar_count_kernel(const float *__restrict__ sparse, int64_t npx, int32_t *chunk_cnt) {
+    pdl_wait();
     __shared__ int s;
     if (threadIdx.x == 0) s = 0;
     __syncthreads();
@@ -739,6 +749,7 @@ __global__ void lidar_count_kernel(const float *__restrict__ sparse, int64_t npx
 
 __global__ void lidar_write_kernel(const float *__restrict__ sparse, int64_t npx, const int32_t *__restrict__ chunk_cnt,
                                    int32_t *idx, float *z, int32_t *k_out) {
+    pdl_wait();
     __shared__ int s_warp[LC_CHUNK / 32];
     __shared__ int s_base;
     if (threadIdx.x == 0) s_base = 0;
@@ -773,15 +784,15 @@ __global__ void lidar_write_kernel(const float *__restrict__ sparse, int64_t npx
 using namespace gs;
 
 static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
-    big_setup_kernel<<<148, 256, 0, st>>>(*f, allow_huge);
+    launch_pdl(big_setup_kernel, 148, 256, 0, st, *f, allow_huge);
     int rc = check_launch("big_setup_kernel");
     if (rc) return rc;
-    big_bands_kernel<<<8 * 148, 256, 0, st>>>(*f);
+    launch_pdl(big_bands_kernel, 8 * 148, 256, 0, st, *f);
     if ((rc = check_launch("big_bands_kernel"))) return rc;
     if (rc) return rc;
-    big_tiles_kernel<<<8 * 148, 256, 0, st>>>(*f);
+    launch_pdl(big_tiles_kernel, 8 * 148, 256, 0, st, *f);
     if ((rc = check_launch("big_tiles_kernel"))) return rc;
-    big_finish_kernel<<<148, 256, 0, st>>>(*f);
+    launch_pdl(big_finish_kernel, 148, 256, 0, st, *f);
     return check_launch("big_finish_kernel");
 }
 
@@ -801,10 +812,10 @@ extern "C" int gs_preprocess_ex(const gs_frame *f, const float *params, const gs
     cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     if (flags & GS_PP_LAZY_SH)
-        preprocess_kernel<true><<<4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream>>>(*f, params,
+        launch_pdl(preprocess_kernel<true>, 4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
                                                                                                          view);
     else
-        preprocess_kernel<false><<<4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream>>>(*f, params,
+        launch_pdl(preprocess_kernel<false>, 4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
                                                                                                           view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
@@ -816,7 +827,7 @@ extern "C" int gs_project(const float *params, int64_t n, const gs_camera *cam, 
                           float *cov2d, float *conic, float *depth, uint8_t *valid, float *jproj, float *mmat,
                           float *cov3d, void *stream) {
     if (n == 0) return GS_OK;
-    project_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+    launch_pdl(project_kernel, (unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream, 
         params, n, cam, mu_cam, mean2d, cov2d, conic, depth, valid, jproj, mmat, cov3d);
     return check_launch("project_kernel");
 }
@@ -824,7 +835,7 @@ extern "C" int gs_project(const float *params, int64_t n, const gs_camera *cam, 
 extern "C" int gs_eval_sh(const float *sh_low, const float *sh_high, const float *dirs, int64_t n, float *colors,
                           float *preclamp, void *stream) {
     if (n == 0) return GS_OK;
-    eval_sh_kernel<<<(unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(sh_low, sh_high, dirs, n, colors,
+    launch_pdl(eval_sh_kernel, (unsigned)((n + 127) / 128), 128, 0, (cudaStream_t)stream, sh_low, sh_high, dirs, n, colors,
                                                                                    preclamp);
     return check_launch("eval_sh_kernel");
 }
@@ -836,11 +847,11 @@ extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const floa
     cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
-    pack_kernel<<<(unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream>>>(*f, mean2d, conic, cov2d3, opacity,
+    launch_pdl(pack_kernel, (unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream, *f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);
     int rc = check_launch("pack_kernel");
     if (rc) return rc;
-    touched_list_kernel<<<(unsigned)((f->n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*f);
+    launch_pdl(touched_list_kernel, (unsigned)((f->n + 255) / 256), 256, 0, (cudaStream_t)stream, *f);
     if ((rc = check_launch("touched_list_kernel"))) return rc;
     // screen-covering Gaussians are binned per tile by bitmap (up to GS_HUGE_CAP per view)
     return launch_big_cull(f, 1, (cudaStream_t)stream);
@@ -853,10 +864,10 @@ extern "C" int gs_lidar_compact(const float *sparse_depth, int32_t width, int32_
     const unsigned chunks = (unsigned)((npx + LC_CHUNK - 1) / LC_CHUNK);
     if (chunks == 0) return GS_OK;
     int32_t *scratch = idx + npx;
-    lidar_count_kernel<<<chunks, LC_CHUNK, 0, (cudaStream_t)stream>>>(sparse_depth, npx, scratch);
+    launch_pdl(lidar_count_kernel, chunks, LC_CHUNK, 0, (cudaStream_t)stream, sparse_depth, npx, scratch);
     int rc = check_launch("lidar_count_kernel");
     if (rc) return rc;
-    lidar_write_kernel<<<chunks, LC_CHUNK, 0, (cudaStream_t)stream>>>(sparse_depth, npx, scratch, idx, z, k_out);
+    launch_pdl(lidar_write_kernel, chunks, LC_CHUNK, 0, (cudaStream_t)stream, sparse_depth, npx, scratch, idx, z, k_out);
     return check_launch("lidar_write_kernel");
 }
 

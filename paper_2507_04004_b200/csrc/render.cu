@@ -144,6 +144,7 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
 }
 
 __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_stop) {
+    pdl_wait();
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
@@ -182,6 +183,7 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
 
 // Lazy lists, continuation 1: the bucket keys of the tiles that need them (ts_flag != 0)
 __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
+    pdl_wait();
     if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     int32_t *cur = ts_cursor(f);
@@ -229,6 +231,7 @@ struct FinishSmem {
 };
 
 __global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int early_stop) {
+    pdl_wait();
     if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
     const int tile = blockIdx.x;
     if (ts_flag(f)[tile] != TL_LIST) return;
@@ -347,6 +350,7 @@ __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const flo
 constexpr int BT = 128;
 
 __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
+    pdl_wait();
     __shared__ float4 s_a[RT];
     __shared__ float4 s_b[RT];
     __shared__ float4 s_c[RT];
@@ -445,6 +449,7 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
 
 // zero the g2d rows of the touched Gaussians (12 doubles = 6 double2 per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
+    pdl_wait();
     // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
     // batches, the chain rule) clears every row it consumes, and the workspace starts zero-filled
     if (f.counters[GS_CNT_LAZY]) return;
@@ -462,13 +467,13 @@ using namespace gs;
 extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream) {
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
-    render_fwd_kernel<<<T, RT, 0, (cudaStream_t)stream>>>(*f, early_stop);
+    launch_pdl(render_fwd_kernel, T, RT, 0, (cudaStream_t)stream, *f, early_stop);
     int rc = check_launch("render_fwd_kernel");
     if (rc) return rc;
     // lazy lists: bucket fill + sorted continuation of the tiles that need them (no-ops otherwise)
-    lazy_fill_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+    launch_pdl(lazy_fill_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, *f);
     if ((rc = check_launch("lazy_fill_kernel"))) return rc;
-    tile_finish_kernel<<<T, TF_THREADS, sizeof(FinishSmem), (cudaStream_t)stream>>>(*f, early_stop);
+    launch_pdl(tile_finish_kernel, T, TF_THREADS, sizeof(FinishSmem), (cudaStream_t)stream, *f, early_stop);
     return check_launch("tile_finish_kernel");
 }
 
@@ -477,11 +482,11 @@ extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
     if (T == 0) return GS_OK;
     if (f->n > 0) {  // each backward starts from zero gradients (backward_2d is a pure function)
         // grid-stride over a small fixed grid: in the engine (lazy lists) every CTA exits at once
-        zero_g2d_kernel<<<2 * 148, 256, 0, (cudaStream_t)stream>>>(*f);
+        launch_pdl(zero_g2d_kernel, 2 * 148, 256, 0, (cudaStream_t)stream, *f);
         int rc = check_launch("zero_g2d_kernel");
         if (rc) return rc;
     }
-    render_bwd_kernel<<<T, BT, 0, (cudaStream_t)stream>>>(*f);
+    launch_pdl(render_bwd_kernel, T, BT, 0, (cudaStream_t)stream, *f);
     return check_launch("render_bwd_kernel");
 }
 

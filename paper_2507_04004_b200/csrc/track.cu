@@ -12,6 +12,7 @@ namespace gs {
 // img_mask = hypot(np.gradient(gray)) > gate, gray = mean over the channels (R/odometry.py:314-316);
 // np.gradient: central differences inside, one-sided at the borders
 __global__ void track_mask_kernel(const float *__restrict__ image, int w, int h, float gate, uint8_t *mask) {
+    pdl_wait();
     const int64_t npx = (int64_t)w * h;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
         const int y = (int)(p / w), x = (int)(p % w);
@@ -36,6 +37,7 @@ __global__ void track_mask_kernel(const float *__restrict__ image, int w, int h,
 
 // g_color *= img_mask & (opacity > gate) (R/odometry.py:325-326)
 __global__ void track_grad_kernel(gs_frame f, const uint8_t *__restrict__ mask, float gate) {
+    pdl_wait();
     const int64_t npx = (int64_t)f.width * f.height;
     for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npx; p += (int64_t)gridDim.x * blockDim.x) {
         if (!(mask[p] && f.opacity[p] > gate)) {
@@ -63,6 +65,7 @@ __device__ void exp_so3(const double phi[3], double R[9]) {
 
 // state (FP64): rot_cw 0-8, trans_cw 9-11, m 12-17, v 18-23, iteration 24
 __global__ void pose_adam_kernel(gs_view *view, double *state, const double *__restrict__ g, float lr) {
+    pdl_wait();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const double it = state[24] + 1.0;
     state[24] = it;
@@ -102,7 +105,7 @@ extern "C" int gs_track_mask(const float *image, int32_t width, int32_t height, 
         set_error("gs_track_mask: bad arguments");
         return GS_ERR_ARG;
     }
-    track_mask_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(image, width, height, grad_gate, mask);
+    launch_pdl(track_mask_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, image, width, height, grad_gate, mask);
     return check_launch("track_mask_kernel");
 }
 
@@ -111,7 +114,7 @@ extern "C" int gs_track_grad(const gs_frame *f, const uint8_t *img_mask, float o
         set_error("gs_track_grad: null argument");
         return GS_ERR_ARG;
     }
-    track_grad_kernel<<<4 * 148, 256, 0, (cudaStream_t)stream>>>(*f, img_mask, opac_gate);
+    launch_pdl(track_grad_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, *f, img_mask, opac_gate);
     return check_launch("track_grad_kernel");
 }
 
@@ -120,6 +123,6 @@ extern "C" int gs_pose_adam(gs_view *view, double *state, const double *pose_gra
         set_error("gs_pose_adam: null argument");
         return GS_ERR_ARG;
     }
-    pose_adam_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(view, state, pose_grad, lr);
+    launch_pdl(pose_adam_kernel, 1, 32, 0, (cudaStream_t)stream, view, state, pose_grad, lr);
     return check_launch("pose_adam_kernel");
 }
