@@ -144,34 +144,39 @@ __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
 }
 
 // 4) one CTA: tile_offsets = exclusive scan of (bucket + huge) counts; bucket offsets (both
-// as the fill cursors, tile_scratch[0..T], and kept, tile_scratch[2T+2 ..]); E.  Each thread owns
-// TS_PER consecutive tiles: all their counts are loaded before any dependent work (one memory
-// round trip), then a single block-wide scan of the per-thread sums.
-constexpr int TS_THREADS = 1024, TS_PER = 8;  // up to 8192 tiles in one pass (1080p: 8160)
+// as the fill cursors, tile_scratch[0..T], and kept, tile_scratch[2T+2 ..]); E.  Passes of
+// TS_THREADS * TS_PER tiles: coalesced loads into shared memory, a sequential scan of TS_PER
+// consecutive tiles per thread, one block scan of the per-thread sums, results back through
+// shared memory and coalesced stores (a thread storing its own consecutive tiles would scatter
+// every warp store over 32 sectors).
+constexpr int TS_THREADS = 1024, TS_PER = 4;
 
 __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int lazy) {
     pdl_wait();
+    __shared__ int32_t s_b[TS_THREADS * TS_PER], s_h[TS_THREADS * TS_PER];
     __shared__ int32_t s_warp[2][32];
     __shared__ int32_t s_pre[2][33];
     __shared__ int32_t s_carry[2];
     const int T = f.tiles_x * f.tiles_y;
     int32_t *cur = f.tile_scratch, *hcount = f.tile_scratch + T + 1, *boff = f.tile_scratch + 2 * (T + 1);
+    int32_t *flag = ts_flag(f);
     const bool use_huge = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP) > 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (threadIdx.x < 2) s_carry[threadIdx.x] = 0;
-    __syncthreads();
-    for (int t0 = 0; t0 < T; t0 += TS_THREADS * TS_PER) {
-        const int tb = t0 + threadIdx.x * TS_PER;
-        int vb[TS_PER], vh[TS_PER];
+    constexpr int PASS = TS_THREADS * TS_PER;
+    for (int t0 = 0; t0 < T; t0 += PASS) {
 #pragma unroll
-        for (int q = 0; q < TS_PER; q++) {
-            const int t = tb + q;
-            vb[q] = t < T ? cur[t] : 0;
-            vh[q] = (t < T && use_huge) ? hcount[t] : 0;
+        for (int q = 0; q < TS_PER; q++) {  // coalesced loads
+            const int i = q * TS_THREADS + threadIdx.x, t = t0 + i;
+            s_b[i] = t < T ? cur[t] : 0;
+            s_h[i] = (t < T && use_huge) ? hcount[t] : 0;
         }
-        int sx = 0, sb = 0;
+        __syncthreads();
+        int vb[TS_PER], vh[TS_PER], sx = 0, sb = 0;
 #pragma unroll
         for (int q = 0; q < TS_PER; q++) {
+            vb[q] = s_b[threadIdx.x * TS_PER + q];
+            vh[q] = s_h[threadIdx.x * TS_PER + q];
             sx += vb[q] + vh[q];
             sb += vb[q];
         }
@@ -206,25 +211,28 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
             }
         }
         __syncthreads();
-        const int before = s_carry[0] + s_pre[0][warp], bb = s_carry[1] + s_pre[1][warp];
-        const int total = s_pre[0][32], totb = s_pre[1][32];
-        int run = before + x - sx, runb = bb + xb - sb;  // exclusive prefix of this thread's first tile
+        int run = s_carry[0] + s_pre[0][warp] + x - sx, runb = s_carry[1] + s_pre[1][warp] + xb - sb;
 #pragma unroll
-        for (int q = 0; q < TS_PER; q++) {
-            const int t = tb + q;
-            if (t < T) {
-                f.tile_offsets[t] = run;
-                cur[t] = runb;
-                boff[t] = runb;
-                ts_flag(f)[t] = TL_LAZY_A;  // lazy lists: the forward flags the tiles it cannot finish
-            }
+        for (int q = 0; q < TS_PER; q++) {  // exclusive prefixes back into shared memory
+            s_b[threadIdx.x * TS_PER + q] = runb;
+            s_h[threadIdx.x * TS_PER + q] = run;
             run += vb[q] + vh[q];
             runb += vb[q];
         }
         __syncthreads();
+#pragma unroll
+        for (int q = 0; q < TS_PER; q++) {  // coalesced stores
+            const int i = q * TS_THREADS + threadIdx.x, t = t0 + i;
+            if (t < T) {
+                f.tile_offsets[t] = s_h[i];
+                cur[t] = s_b[i];
+                boff[t] = s_b[i];
+                flag[t] = TL_LAZY_A;  // lazy lists: the forward flags the tiles it cannot finish
+            }
+        }
         if (threadIdx.x == 0) {
-            s_carry[0] += total;
-            s_carry[1] += totb;
+            s_carry[0] += s_pre[0][32];
+            s_carry[1] += s_pre[1][32];
         }
         __syncthreads();
     }
