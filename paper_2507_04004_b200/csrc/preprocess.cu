@@ -75,6 +75,62 @@ __device__ __forceinline__ float3 pp_colour(const PPGeom &g, const PPSh &sh, int
     return make_float3(col[0], col[1], col[2]);
 }
 
+// Exact cull of the small rectangles (<= GS_SMALL_CAND candidate tiles) of a warp's 32
+// Gaussians, shared by the whole warp: the candidates of all flagged lanes are laid end to end
+// (warp prefix sum) and each round every lane tests one (Gaussian, tile) pair -- the owner and
+// its parameters fetched by shuffles -- so the warp runs at full width whatever the mix of
+// rectangle sizes (a lane-serial loop over each lane's own candidates runs at the width of the
+// largest).  Returns the calling lane's keep bits in candidate order (ty-major, then tx), the
+// same bits and decision arithmetic as cull_rect.
+__device__ __forceinline__ uint32_t warp_cull_small(bool flag, float mx, float my, float ca, float cb, float cc,
+                                                    float qcut, int4 r, int width, int height) {
+    const int lane = threadIdx.x & 31;
+    const int nx = r.y - r.x + 1;
+    const int nc = flag ? nx * (r.w - r.z + 1) : 0;
+    int pre = nc;  // inclusive prefix of the candidate counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, pre, o);
+        if (lane >= o) pre += y;
+    }
+    const int total = __shfl_sync(0xffffffffu, pre, 31);
+    const int start = pre - nc;  // exclusive prefix: this lane's first pair
+    uint32_t bits = 0u;
+    for (int base = 0; base < total; base += 32) {
+        const int idx = base + lane;
+        // owner = the lane whose [start, start + nc) holds idx: the first lane with pre > idx
+        int lo = 0, hi = 31;
+#pragma unroll
+        for (int it = 0; it < 5; it++) {
+            const int mid = (lo + hi) >> 1;
+            if (__shfl_sync(0xffffffffu, pre, mid) > idx) hi = mid;
+            else lo = mid + 1;
+        }
+        const int own = lo;
+        const int c = idx - __shfl_sync(0xffffffffu, start, own);
+        const float omx = __shfl_sync(0xffffffffu, mx, own), omy = __shfl_sync(0xffffffffu, my, own);
+        const float oca = __shfl_sync(0xffffffffu, ca, own), ocb = __shfl_sync(0xffffffffu, cb, own);
+        const float occ = __shfl_sync(0xffffffffu, cc, own), oq = __shfl_sync(0xffffffffu, qcut, own);
+        const int orx = __shfl_sync(0xffffffffu, r.x, own), orz = __shfl_sync(0xffffffffu, r.z, own);
+        const int onx = __shfl_sync(0xffffffffu, nx, own);
+        bool keep = false;
+        if (idx < total) {
+            const int tx = orx + c % onx, ty = orz + c / onx;
+            const int x0 = tx * GS_TILE, x1 = min(x0 + GS_TILE - 1, width - 1);
+            const int y0 = ty * GS_TILE, y1 = min(y0 + GS_TILE - 1, height - 1);
+            keep = tile_keep(omx, omy, oca, ocb, occ, oq, x0, x1, y0, y1);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        // this lane's pairs inside the round [base, base + 32)
+        const int a = max(start, base) - base, e = min(start + nc, base + 32) - base;
+        if (a < e) {
+            const uint32_t seg = (e - a == 32) ? m : ((m >> a) & ((1u << (e - a)) - 1u));
+            bits |= seg << (base + a - start);
+        }
+    }
+    return bits;
+}
+
 // Persistent warps over batches of 32 Gaussians (pipeline above).
 template <bool LAZY_SH>
 __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, const float *__restrict__ params,
@@ -114,7 +170,11 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
         __syncwarp();
         const PPGeom &G = W.geom[slot];
         const int64_t i = batch * 32 + lane;
-        bool touched = false, big = false, need = false;
+        bool touched = false, big = false, need = false, front = false, small = false;
+        Projected pr;
+        float op = 0.0f, qcut = 0.0f, radius = -1.0f, logit = 0.0f;
+        int4 rect = make_int4(0, -1, 0, -1);
+        // 1) per lane: near-plane test and FP64 projection, radius and tile rectangle
         if (i < n) {
             float pk[11];
             {
@@ -123,25 +183,25 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
                 pk[4] = c1.x; pk[5] = c1.y; pk[6] = c1.z; pk[7] = c1.w;
                 pk[8] = c2.x; pk[9] = c2.y; pk[10] = c2.z;
             }
-            float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-            float4 *cv = reinterpret_cast<float4 *>(f.cov2d) + i;
-            int4 *rc = reinterpret_cast<int4 *>(f.rect) + i;
+            logit = pk[10];
             // near-plane test (R/gaussians.py:188-191)
             const float zf = (pk[0] * cam.rot_cw[6] + pk[1] * cam.rot_cw[7] + pk[2] * cam.rot_cw[8]) + cam.trans_cw[2];
             if (!(zf > GS_NEAR_CLIP)) {
+                float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
                 s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                 s2[1] = make_float4(0.f, 0.f, zf, 0.f);
                 s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-                *cv = make_float4(0.f, 0.f, 0.f, -1.f);
-                *rc = make_int4(0, -1, 0, -1);
+                reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(0.f, 0.f, 0.f, -1.f);
+                reinterpret_cast<int4 *>(f.rect)[i] = make_int4(0, -1, 0, -1);
                 f.valid[i] = 0;
                 f.kept[i] = 0;
+                f.touched[i] = 0;
             } else {
+                front = true;
                 // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians
                 // near the 0.01 m clip plane, and fp32 would shift their whole footprint
                 ProjectedT<double> pd;
                 project_full<double>(pk, cam, pd);
-                Projected pr;
                 pr.mu[2] = (float)pd.mu[2];
                 pr.mx = (float)pd.mx;
                 pr.my = (float)pd.my;
@@ -152,37 +212,39 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
                 pr.cb = (float)pd.cb;
                 pr.cc = (float)pd.cc;
                 pr.valid = pd.valid;
-                const float op = 1.0f / (1.0f + expf(-pk[10]));
-                int4 rect = make_int4(0, -1, 0, -1);
-                float qcut = 0.0f, radius = -1.0f;
+                op = 1.0f / (1.0f + expf(-pk[10]));
                 const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width,
                                                           f.height, f.tiles_x, f.tiles_y, rect, qcut, radius);
                 if (!active) rect = make_int4(0, -1, 0, -1);
-                // exact per-tile cull of the rectangle (R/rasterizer.py:150-166), fused here for
-                // small footprints; large ones by the big_* kernels (band / tile bounds, exact rows)
                 const int ncand = (rect.y - rect.x + 1) * (rect.w - rect.z + 1);
                 big = active && ncand > GS_SMALL_CAND;
-                uint64_t bits = 0ull;
-                const int kept = (active && !big) ? cull_rect(pr.mx, pr.my, pr.ca, pr.cb, pr.cc, qcut, rect, f.width,
-                                                              f.height, bits)
-                                                  : 0;
-                touched = kept > 0;
-                need = LAZY_SH ? (touched || big) : true;
-                s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
-                s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-                // the colour (s2[2].xyz) follows one iteration later; 1 - opacity = sigmoid(-logit),
-                // kept exact for the blend's 1 - alpha
-                if (!need) s2[2] = make_float4(0.f, 0.f, 0.f, 1.0f / (1.0f + expf(pk[10])));
-                *cv = make_float4(pr.c00, pr.c01, pr.c11, radius);
-                *rc = rect;
-                f.valid[i] = pr.valid ? 1 : 0;
-                f.kept[i] = kept;
-                f.keep_bits[i] = bits;
-                if (kept > 0)  // binning buckets
-                    count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
-                                     ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
-                                     f.tiles_x);
+                small = active && !big;
             }
+        }
+        // 2) the warp together: exact per-tile cull of the small rectangles (R/rasterizer.py:150-166),
+        //    one (Gaussian, candidate tile) pair per lane and round -- large footprints go to the
+        //    big_* kernels
+        const uint32_t bits = warp_cull_small(small, pr.mx, pr.my, pr.ca, pr.cb, pr.cc, qcut, rect, f.width, f.height);
+        // 3) per lane: outputs
+        if (front) {
+            const int kept = __popc(bits);
+            touched = kept > 0;
+            need = LAZY_SH ? (touched || big) : true;
+            float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+            s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
+            s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
+            // the colour (s2[2].xyz) follows one iteration later; 1 - opacity = sigmoid(-logit),
+            // kept exact for the blend's 1 - alpha
+            if (!need) s2[2] = make_float4(0.f, 0.f, 0.f, 1.0f / (1.0f + expf(logit)));
+            reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(pr.c00, pr.c01, pr.c11, radius);
+            reinterpret_cast<int4 *>(f.rect)[i] = rect;
+            f.valid[i] = pr.valid ? 1 : 0;
+            f.kept[i] = kept;
+            f.keep_bits[i] = bits;
+            if (kept > 0)  // binning buckets
+                count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
+                                 ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
+                                 f.tiles_x);
             f.touched[i] = touched ? 1 : 0;
         }
         warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
