@@ -25,8 +25,8 @@ constexpr int CA_BATCH = 4;  // float4 per lane and array in flight in the fused
 template <typename T>
 __device__ __forceinline__ void quat_grad(const float q0[4], const T gR[9], float out[4]) {
     const T a = q0[0], b = q0[1], c = q0[2], d = q0[3];
-    const T nrm = gs_sqrt(a * a + b * b + c * c + d * d);
-    const T w = a / nrm, x = b / nrm, y = c / nrm, z = d / nrm;
+    const T rn = (T)1 / gs_sqrt(a * a + b * b + c * c + d * d);
+    const T w = a * rn, x = b * rn, y = c * rn, z = d * rn;
     const T zero = 0, two = 2;
     const T dw[9] = {zero, -z, y, z, zero, -x, -y, x, zero};
     const T dx[9] = {zero, y, z, y, -two * x, -w, z, w, -two * x};
@@ -44,7 +44,7 @@ __device__ __forceinline__ void quat_grad(const float q0[4], const T gR[9], floa
     const T qh[4] = {w, x, y, z};
     const T dot = gq[0] * qh[0] + gq[1] * qh[1] + gq[2] * qh[2] + gq[3] * qh[3];
 #pragma unroll
-    for (int k = 0; k < 4; k++) out[k] = (float)((gq[k] - qh[k] * dot) / nrm);
+    for (int k = 0; k < 4; k++) out[k] = (float)((gq[k] - qh[k] * dot) * rn);
 }
 
 // gradient of the scalar loss w.r.t. one parameter row (59 columns written to G; every write
@@ -130,7 +130,8 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
     const float u0 = p[0] - cam.center[0], u1 = p[1] - cam.center[1], u2 = p[2] - cam.center[2];
     float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
     if (un < 1e-12f) un = 1.0f;
-    const float d0 = u0 / un, d1 = u1 / un, d2 = u2 / un;
+    const float run = 1.0f / un;
+    const float d0 = u0 * run, d1 = u1 * run, d2 = u2 * run;
     float bs[16];
     sh_basis(d0, d1, d2, bs);
     float gcol[3];
@@ -149,7 +150,7 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
     float gd[3];
     sh_basis_vjp(d0, d1, d2, sk, gd);
     const float dot = gd[0] * d0 + gd[1] * d1 + gd[2] * d2;
-    const float gu[3] = {(gd[0] - d0 * dot) / un, (gd[1] - d1 * dot) / un, (gd[2] - d2 * dot) / un};
+    const float gu[3] = {(gd[0] - d0 * dot) * run, (gd[1] - d1 * dot) * run, (gd[2] - d2 * dot) * run};
     if (POSE) {
         // translation: g_mu_cam + R_cw gu (the camera centre moves with rho, :656); rotation:
         // mu_cam x g_mu_cam + the covariance path through M = J R_cw: X = (J^T gM) R_cw^T,
@@ -195,21 +196,11 @@ __device__ __forceinline__ void chain_row(const float *p, const double *g, const
 // ~1 ulp; the denominator is >= 1e-15, never subnormal): with IEEE sqrtf and __frcp_rn
 // (Newton steps + fix-up paths) the 59 updates per row were a third of the fused chain+Adam
 // kernel's instructions.
-__device__ __forceinline__ float mufu_sqrt(float x) {
-    float y;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float mufu_rcp(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 __device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float rbc1, float rbc2) {
     m = 0.9f * m + 0.1f * g;
     v = 0.999f * v + 0.001f * g * g;
-    const float den = mufu_sqrt(v * rbc2) + 1e-15f;
-    return p - (lr * (m * rbc1)) * mufu_rcp(den);
+    const float den = fast_sqrt(v * rbc2) + 1e-15f;
+    return p - (lr * (m * rbc1)) * fast_rcp(den);
 }
 
 // mode 0: fused Adam on params/m/v/t.  mode 1: grads[row] += G, touched_accum[row] = 1.

@@ -29,6 +29,25 @@ constexpr int HSTAGE = HKEYS + 2 * GS_HUGE_CAP;  // unsorted keys staged by big_
 void set_error(const char *fmt, ...);
 int check_launch(const char *what);
 
+// Single MUFU instructions without the IEEE rounding / range fix-up sequences (~1-2 ulp,
+// subnormal inputs and results flush to zero).  Used where the operands are known to be normal
+// and an ulp is far below the path's tolerance (blend alpha, SSIM map, Adam denominator).
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float fast_sqrt(float x) {
+    float y;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // Programmatic dependent launch: every kernel of the library is launched with programmatic
 // stream serialisation and waits for its predecessor's completion (and memory flush) as its
 // first action, so its launch and block scheduling overlap the predecessor's tail instead of
@@ -152,8 +171,8 @@ __device__ __forceinline__ double gs_exp(double x) { return exp(x); }
 template <typename T>
 __device__ __forceinline__ void quat_rot(const float q[4], T R[9]) {
     const T q0 = q[0], q1 = q[1], q2 = q[2], q3 = q[3];
-    const T nrm = gs_sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-    const T w = q0 / nrm, x = q1 / nrm, y = q2 / nrm, z = q3 / nrm;
+    const T rn = (T)1 / gs_sqrt(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);  // one divide, four products
+    const T w = q0 * rn, x = q1 * rn, y = q2 * rn, z = q3 * rn;
     const T one = 1, two = 2;
     R[0] = one - two * (y * y + z * z); R[1] = two * (x * y - w * z); R[2] = two * (x * z + w * y);
     R[3] = two * (x * y + w * z); R[4] = one - two * (x * x + z * z); R[5] = two * (y * z - w * x);
@@ -179,7 +198,8 @@ __device__ __forceinline__ void project_full(const float *p, const gs_camera &ca
         for (int c = 0; c < 3; c++)
             o.M[3 * r + c] = o.J[3 * r] * (T)Rc[c] + o.J[3 * r + 1] * (T)Rc[3 + c] + o.J[3 * r + 2] * (T)Rc[6 + c];
     quat_rot<T>(p + 6, o.R);
-    o.s[0] = gs_exp((T)p[3]); o.s[1] = gs_exp((T)p[4]); o.s[2] = gs_exp((T)p[5]);
+    // scales from the fp32 exponential (~2 ulp): no cancellation downstream, unlike mu_cam
+    o.s[0] = (T)expf(p[3]); o.s[1] = (T)expf(p[4]); o.s[2] = (T)expf(p[5]);
     const T s2[3] = {o.s[0] * o.s[0], o.s[1] * o.s[1], o.s[2] * o.s[2]};
     for (int a = 0; a < 3; a++)
         for (int b = a; b < 3; b++) {
@@ -197,10 +217,10 @@ __device__ __forceinline__ void project_full(const float *p, const gs_camera &ca
     o.det = o.c00 * o.c11 - o.c01 * o.c01;
     v = v && (o.det > (T)1e-12f) && isfinite(o.det);
     o.valid = v;
-    const T dets = v ? o.det : (T)1;
-    o.ca = o.c11 / dets;
-    o.cb = -o.c01 / dets;
-    o.cc = o.c00 / dets;
+    const T idet = (T)1 / (v ? o.det : (T)1);
+    o.ca = o.c11 * idet;
+    o.cb = -o.c01 * idet;
+    o.cc = o.c00 * idet;
 }
 
 // ---------------------------------------------------------------------------

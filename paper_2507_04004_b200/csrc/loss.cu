@@ -230,11 +230,12 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                     const float va = u[2][k] - ua * ua, vb = u[3][k] - ub * ub, vab = u[4][k] - ua * ub;
                     const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
                     const float b1 = ua * ua + ub * ub + C1, b2 = va + vb + C2;
-                    const float rden = 1.0f / (b1 * b2);
+                    // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
+                    const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
                     const float S = (a1 * a2) * rden;
-                    g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua / b1) + S * (2.0f * ua / b2)) *
+                    g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) *
                          inv_n;
-                    g1 = (-S / b2) * inv_n;
+                    g1 = (-S * rb2) * inv_n;
                     g2 = (2.0f * a1 * rden) * inv_n;
                     if (gy >= 5 && gy < 5 + TH && gx >= 5 && gx < 5 + TW) s_acc += S;
                 }

@@ -27,18 +27,9 @@ __device__ __forceinline__ float quad(float ca, float cb, float cc, float dx, fl
 // with one rounding (FMA) and is exactly 0.01 on the clamp, so the transmittance product does
 // not pick up the cancellation of 1 - 0.99f.  (omo = 1 - o is carried in the splat record for
 // the higher-accuracy variant 1 - o e = (1 - e) + (1 - o) e.)
-// MUFU ex2 / rcp without the IEEE range and rounding fix-ups (relative error ~2^-22; results
-// below 2^-126 flush to 0, i.e. alpha < 1e-38): the blend and its adjoint use the same alpha.
-__device__ __forceinline__ float fast_ex2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-__device__ __forceinline__ float fast_rcp(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
+// fast_ex2 / fast_rcp (common.cuh): MUFU without the IEEE range and rounding fix-ups (relative
+// error ~2^-22; results below 2^-126 flush to 0, i.e. alpha < 1e-38): the blend and its adjoint
+// use the same alpha.
 
 __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &araw, float &alpha, float &oma) {
     (void)omo;
