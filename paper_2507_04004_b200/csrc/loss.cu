@@ -127,12 +127,14 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, c = blockIdx.z;
     const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
     const int tid = threadIdx.x;
-    // strip lengths: border tiles (per-position table weights) use shorter strips so that the
-    // table loads do not push the register budget
-    constexpr int HB = INTERIOR ? 6 : 3;
+    // The forward blurs of every tile are plain 11-tap convolutions (compile-time weights): a
+    // border tile loads its halo mirror-padded (R/losses.py:31-42, triangle wave), which is what
+    // the reflection of the blur amounts to.  Only the adjoint passes of border tiles need the
+    // per-position tables (the reflection folds several taps onto one pixel).
+    constexpr int HB = 6;
     constexpr int VS = 5, NVS = (GR + VS - 1) / VS;
     constexpr int AS = 4, NAS = TH / AS;
-    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, zero outside the image
+    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, mirror-padded
     {
         constexpr int NEL = NIR * NIC, PER = (NEL + L_THREADS - 1) / L_THREADS;
         float va[PER], vb[PER];
@@ -140,9 +142,13 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
         for (int q = 0; q < PER; q++) {  // all loads in flight before the stores
             const int k = tid + q * L_THREADS;
             const int iy = k / NIC, ix = k % NIC;
-            const int y = y0 - 10 + iy, x = x0 - 10 + ix;
+            int y = y0 - 10 + iy, x = x0 - 10 + ix;
+            if (!INTERIOR) {
+                y = reflect_idx(y, H);
+                x = reflect_idx(x, W);
+            }
             va[q] = vb[q] = 0.0f;
-            if (k < NEL && ix < TW + 20 && (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H))) {
+            if (k < NEL && ix < TW + 20) {
                 const int64_t p = (int64_t)y * W + x;
                 va[q] = __ldg(color + 3 * p + c);
                 vb[q] = __ldg(target + 3 * p + c);
@@ -176,8 +182,7 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
             for (int k = 0; k < HB; k++) {
                 const int d = t - k;
                 if (d >= 0 && d < 11) {
-                    const int xp = min(max(x0 - 5 + c0 + k, 0), W - 1);
-                    const float w = wtab<INTERIOR>(tab_x, xp, d);
+                    const float w = kw(d);
                     m[0][k] += w * at;
                     m[1][k] += w * bt;
                     m[2][k] += w * aa;
@@ -212,8 +217,7 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                 for (int k = 0; k < VS; k++) {
                     const int d = r - k;
                     if (d >= 0 && d < 11) {
-                        const int yp = min(max(y0 - 5 + gy0 + k, 0), H - 1);
-                        const float w = wtab<INTERIOR>(tab_y, yp, d);
+                        const float w = kw(d);
 #pragma unroll
                         for (int q = 0; q < 5; q++) u[q][k] += w * h[q];
                     }
