@@ -187,15 +187,17 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             // near-plane test (R/gaussians.py:188-191)
             const float zf = (pk[0] * cam.rot_cw[6] + pk[1] * cam.rot_cw[7] + pk[2] * cam.rot_cw[8]) + cam.trans_cw[2];
             if (!(zf > GS_NEAR_CLIP)) {
-                float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-                s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
-                s2[1] = make_float4(0.f, 0.f, zf, 0.f);
-                s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
-                reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(0.f, 0.f, 0.f, -1.f);
-                reinterpret_cast<int4 *>(f.rect)[i] = make_int4(0, -1, 0, -1);
-                f.valid[i] = 0;
-                f.kept[i] = 0;
-                f.touched[i] = 0;
+                if (!LAZY_SH) {  // the engine never reads the records of Gaussians it cannot draw
+                    float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+                    s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    s2[1] = make_float4(0.f, 0.f, zf, 0.f);
+                    s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(0.f, 0.f, 0.f, -1.f);
+                    reinterpret_cast<int4 *>(f.rect)[i] = make_int4(0, -1, 0, -1);
+                    f.valid[i] = 0;
+                    f.kept[i] = 0;
+                    f.touched[i] = 0;
+                }
             } else {
                 front = true;
                 // FP64 projection, rounded once to fp32: mu_cam = R p + t cancels for Gaussians
@@ -230,22 +232,28 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
             const int kept = __popc(bits);
             touched = kept > 0;
             need = LAZY_SH ? (touched || big) : true;
-            float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-            s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
-            s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
-            // the colour (s2[2].xyz) follows one iteration later; 1 - opacity = sigmoid(-logit),
-            // kept exact for the blend's 1 - alpha
-            if (!need) s2[2] = make_float4(0.f, 0.f, 0.f, 1.0f / (1.0f + expf(logit)));
-            reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(pr.c00, pr.c01, pr.c11, radius);
-            reinterpret_cast<int4 *>(f.rect)[i] = rect;
-            f.valid[i] = pr.valid ? 1 : 0;
-            f.kept[i] = kept;
-            f.keep_bits[i] = bits;
+            // the engine (LAZY_SH) writes only what the binning and the blend read: the records of
+            // the Gaussians that can be drawn (kept in a tile, or large footprints still to be
+            // culled); the reference-shaped API writes every record (out.ctx["proj"], R/gaussians.py:180-215)
+            if (need) {
+                float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+                s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
+                s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
+                reinterpret_cast<int4 *>(f.rect)[i] = rect;
+                f.kept[i] = kept;
+                f.keep_bits[i] = bits;
+            }
+            if (!LAZY_SH) {
+                // (the colour, s2[2].xyz, follows one iteration later; 1 - opacity = sigmoid(-logit)
+                // is kept exact for the blend's 1 - alpha)
+                reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(pr.c00, pr.c01, pr.c11, radius);
+                f.valid[i] = pr.valid ? 1 : 0;
+                f.touched[i] = touched ? 1 : 0;
+            }
             if (kept > 0)  // binning buckets
                 count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
                                  ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
                                  f.tiles_x);
-            f.touched[i] = touched ? 1 : 0;
         }
         warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
         warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
