@@ -143,6 +143,12 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     PPWarp &W = ws_all[warp];
+    {  // clear the screen-covering Gaussians' per-slot tile bitmaps (big_* kernels OR into them)
+        const int64_t n4 = ((int64_t)GS_HUGE_CAP * (((int64_t)f.tiles_x * f.tiles_y + 31) >> 5)) >> 2;
+        uint4 *hm = reinterpret_cast<uint4 *>(f.huge_mask_t);
+        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += (int64_t)gridDim.x * blockDim.x)
+            hm[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
     const int64_t n = f.n;
     const int64_t nbatch = (n + 31) / 32;
     const int64_t stride = (int64_t)gridDim.x * PP_WARPS;
@@ -435,7 +441,8 @@ __device__ __forceinline__ int big_bit(const BigCtx &c, int tiles_x, int tx, int
     return c.slot >= 0 ? ty * tiles_x + tx : (ty - c.r.z) * (c.r.y - c.r.x + 1) + (tx - c.r.x);
 }
 
-constexpr int CB_BSTRIDE = 64;  // threads per Gaussian in big_bands_kernel (bands beyond: strided)
+constexpr int CB_BSTRIDE = 64;  // threads per Gaussian in big_bands_kernel (bands beyond: strided); a
+                                // multiple of 32 so that a warp serves one Gaussian (warp-wide reservations)
 
 // K0: thread per large-footprint Gaussian: huge slot or bitmap base (warp-aggregated
 // reservations: one atomic per warp and counter)
@@ -479,12 +486,11 @@ __global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_hu
             f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
             f.kept[g] = 0;
         }
-        // zero the output bitmap rows (the band / tile kernels OR into them), one row at a time
-        // with the whole warp (coalesced)
-        const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
-        uint32_t *bits = (b < nb) ? (slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : (base >= 0 ? f.big_bits + base : nullptr))
-                                  : nullptr;
-        const int nwords = slot >= 0 ? tw : words;
+        // zero the cull bitmap rows of the non-screen-covering ones (the band / tile kernels OR
+        // into them), one row at a time with the whole warp (coalesced); the huge-slot rows were
+        // cleared wholesale by preprocess_kernel
+        uint32_t *bits = (b < nb && slot < 0 && base >= 0) ? f.big_bits + base : nullptr;
+        const int nwords = words;
         for (int k = 0; k < 32; k++) {
             uint32_t *row = reinterpret_cast<uint32_t *>(__shfl_sync(0xffffffffu, (unsigned long long)bits, k));
             const int nw = __shfl_sync(0xffffffffu, nwords, k);
