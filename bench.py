@@ -283,7 +283,7 @@ def run_ours(args) -> dict:
         "e2e": {"value": round(1000.0 / e2e_ms, 2), "unit": "it/s", "h2d_bytes_per_step": int(eng.h2d_bytes),
                 "d2h_bytes_per_step": int(eng.d2h_bytes), "wall_ms_per_step": round(wall_ms, 4),
                 "path": "MapOptimizer.run_host: pinned host keyframe (target image + LiDAR K-list) -> H2D on a "
-                        "copy stream, double-buffered behind the previous iteration -> iteration -> D2H loss"},
+                        "copy stream, multi-buffered ahead of the iterations -> iteration -> D2H loss"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",

@@ -76,9 +76,12 @@ class Keyframe:
 
 class HostKeyframes:
     """Keyframes in pinned host memory -- the target image and the LiDAR returns as a K-list
-    (pixel index, depth; compacted once here, as the device path caches it) -- streamed into two
-    device slots: the upload of keyframe j+1 (copy stream) overlaps iteration j.  `cur` is the
+    (pixel index, depth; compacted once here, as the device path caches it) -- streamed into
+    NSLOT device slots: the upload of keyframe j+1 (copy stream) starts as soon as iteration
+    j + 1 - NSLOT has released its slot, so it has NSLOT - 1 iterations to land.  `cur` is the
     engine's device gs_view that the captured iteration reads."""
+
+    NSLOT = 3
 
     def __init__(self, keyframes, width: int, height: int, cur: torch.Tensor, device):
         h, w = int(height), int(width)
@@ -94,7 +97,8 @@ class HostKeyframes:
         kmax = max(1, max(len(i) for i in self.idx))
         self.slots = [{"img": torch.empty((h, w, 3), device=device),
                        "idx": torch.empty(kmax, dtype=torch.int32, device=device),
-                       "z": torch.empty(kmax, device=device), "view": torch.empty_like(cur)} for _ in range(2)]
+                       "z": torch.empty(kmax, device=device), "view": torch.empty_like(cur)}
+                      for _ in range(self.NSLOT)]
         self.views = []  # per keyframe, per slot: the gs_view pointing at that slot's buffers
         for k, kf in enumerate(keyframes):
             per = []
@@ -106,15 +110,15 @@ class HostKeyframes:
                 per.append(torch.frombuffer(bytearray(bytes(memoryview(v).cast("B"))), dtype=torch.uint8).pin_memory())
             self.views.append(per)
         self.copy_stream = torch.cuda.Stream(device=device)
-        self.slot_free = [None, None]
+        self.slot_free = [None] * self.NSLOT
         nbytes = [self.img[k].numel() * 4 + self.idx[k].numel() * 8 + self.views[k][0].numel()
                   for k in range(len(keyframes))]
         self.h2d_bytes = int(round(float(np.mean(nbytes))))
 
     def upload(self, j: int, k: int) -> torch.cuda.Event:
-        """H2D of keyframe k into slot j % 2 on the copy stream, once the iteration that last read
-        that slot has finished; returns the event marking the slot ready."""
-        s = j % 2
+        """H2D of keyframe k into slot j % NSLOT on the copy stream, once the iteration that last
+        read that slot has finished; returns the event marking the slot ready."""
+        s = j % self.NSLOT
         sl, cs = self.slots[s], self.copy_stream
         with torch.cuda.stream(cs):
             if self.slot_free[s] is not None:
@@ -137,16 +141,19 @@ class HostKeyframes:
         if not order:
             return
         self.copy_stream.wait_stream(main)  # uploads start after the work queued so far
-        ready = self.upload(0, order[0])
+        ahead = self.NSLOT - 1  # uploads in flight ahead of the iteration that runs
+        ready = {}
+        for j in range(min(ahead, len(order))):
+            ready[j] = self.upload(j, order[j])
         for j, k in enumerate(order):
-            nxt = self.upload(j + 1, order[j + 1]) if j + 1 < len(order) else None
-            main.wait_event(ready)
-            self.cur.copy_(self.slots[j % 2]["view"])
+            if j + ahead < len(order):
+                ready[j + ahead] = self.upload(j + ahead, order[j + ahead])
+            main.wait_event(ready.pop(j))
+            self.cur.copy_(self.slots[j % self.NSLOT]["view"])
             body(j, k)
             free = torch.cuda.Event()
             free.record(main)
-            self.slot_free[j % 2] = free
-            ready = nxt
+            self.slot_free[j % self.NSLOT] = free
 
 
 class MapOptimizer:
@@ -302,7 +309,13 @@ class MapOptimizer:
                 self.graph.replay()
             else:
                 self._launch()
-            self._h_loss[self._host_steps % 1024].copy_(self.ws.loss[0], non_blocking=True)
+            # the loss read-back rides on the copy stream: the next iteration does not queue behind it
+            done = torch.cuda.Event()
+            done.record()
+            cs = self.host.copy_stream
+            cs.wait_event(done)
+            with torch.cuda.stream(cs):
+                self._h_loss[self._host_steps % 1024].copy_(self.ws.loss[0], non_blocking=True)
             self._host_steps += 1
             s = self._steps % 4
             self._ring[s].copy_(self.ws.counters[:8], non_blocking=True)
