@@ -618,3 +618,42 @@ def test_photometric_refine_matches_reference(name):
         assert abs(loss - lref) < 2e-3 * lref + 1e-5, (n, loss, lref)
     # the refinement converges toward the true pose (the image is the rendering at it)
     assert np.linalg.norm(trans - z["trans_cw"]) < np.linalg.norm(t[f"{name}_t0"] - z["trans_cw"])
+
+
+def test_engine_edge_cases():
+    """The graph-captured engine on degenerate inputs: no Gaussian in view (every one behind the
+    camera), no LiDAR return (K = 0), and an empty map (R/mapper.py:240-241 DataError)."""
+    import torch
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.errors import DataError
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(4096, 128, 72, lidar=16, render_views=(0,))
+    cam = R.camera_from(sc.cams[0])
+    # 1) looking away: rotate the camera by pi about its y axis (every Gaussian behind it)
+    flip = np.diag([-1.0, 1.0, -1.0])
+    away = cam.with_pose(flip @ np.asarray(cam.rot_cw), flip @ np.asarray(cam.trans_cw) - np.array([0, 0, 50.0]))
+    g = GaussianMap.from_rows(sc.rows)
+    eng = M.MapOptimizer(g, [M.Keyframe(away, sc.targets[0], sc.sparse_depths[0])], R.default_lrs(3.0))
+    eng.capture()
+    before = g.rows().clone()
+    eng.step(0)
+    eng.step(0)
+    torch.cuda.synchronize()
+    assert eng.counters()["touched"] == 0 and eng.counters()["entries"] == 0
+    assert torch.equal(before, g.rows())  # untouched rows are bit-identical (R/rasterizer.py:716)
+    assert not eng.adam.t.any()
+    assert np.isfinite(eng.loss_sum())
+    # 2) no LiDAR return: the depth term is 0 and the engine still steps
+    g2 = GaussianMap.from_rows(sc.rows)
+    eng2 = M.MapOptimizer(g2, [M.Keyframe(cam, sc.targets[0], np.zeros_like(sc.sparse_depths[0]))],
+                          R.default_lrs(3.0))
+    eng2.step(0)
+    torch.cuda.synchronize()
+    assert float(eng2.ws.loss[2].item()) == 0.0 and not eng2.ws.g_depth.any()
+    assert int(eng2.adam.t.sum().item()) == eng2.counters()["touched"] > 0
+    # 3) empty map
+    with pytest.raises(DataError):
+        M.MapOptimizer(GaussianMap.from_rows(np.zeros((0, 59))), [M.Keyframe(cam, sc.targets[0], None)],
+                       R.default_lrs(3.0))
