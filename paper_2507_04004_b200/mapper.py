@@ -532,7 +532,9 @@ class Mapper:
     def submit(self, kf: Keyframe) -> int:
         if len(self.gmap) == 0:
             added = init_map(self.gmap, kf)
-            pts = np.asarray(kf.points, dtype=np.float64)
+            pts = kf.points.detach().double().cpu().numpy() if isinstance(kf.points, torch.Tensor) else \
+                np.asarray(kf.points, dtype=np.float64)
+            pts = pts.reshape(-1, 3)
             extent = float(np.linalg.norm(pts - pts.mean(axis=0), axis=1).max()) if len(pts) else 1.0
             self.lrs = default_lrs(max(extent, 1e-6))
         else:
@@ -555,3 +557,19 @@ class Mapper:
     def snapshot(self) -> GaussianMap:
         with self._lock:
             return self._published
+
+
+def mapping_loop(keyframe_queue, mapper: Mapper) -> None:
+    """R/mapper.py:319-334: drain a queue of keyframes; None closes it and triggers refinement
+    (max(cfg.refine_rounds, 1) rounds).  Calls task_done after each item when the queue supports
+    it, so a producer can rendezvous on queue.join()."""
+    done = getattr(keyframe_queue, "task_done", lambda: None)
+    while True:
+        kf = keyframe_queue.get()
+        if kf is None:
+            done()
+            break
+        mapper.submit(kf)
+        done()
+    if mapper.keyframes:
+        mapper.refine(max(mapper.cfg.refine_rounds, 1))

@@ -657,3 +657,64 @@ def test_engine_edge_cases():
     with pytest.raises(DataError):
         M.MapOptimizer(GaussianMap.from_rows(np.zeros((0, 59))), [M.Keyframe(cam, sc.targets[0], None)],
                        R.default_lrs(3.0))
+
+
+def _mapper_keyframes():
+    """Same construction as tests/golden/make_golden.py mapper_keyframes (three room keyframes,
+    seed points back-projected from the LiDAR pixels)."""
+    from paper_2507_04004_b200 import scenes
+    sc = scenes.scene_room(2048, 128, 72, lidar=16, render_views=(0, 10, 20))
+    out = []
+    for c, tgt, sd in zip(sc.cams, sc.targets, sc.sparse_depths):
+        sd = sd.astype(np.float32).astype(np.float64)
+        tgt = tgt.astype(np.float32).astype(np.float64)
+        rot = np.asarray(c["rot_cw"]).astype(np.float32).astype(np.float64)
+        trans = np.asarray(c["trans_cw"]).astype(np.float32).astype(np.float64)
+        ys, xs = np.nonzero(sd > 0)
+        dirs = np.stack([(xs - c["cx"]) / c["fx"], (ys - c["cy"]) / c["fy"], np.ones(len(xs))], axis=1)
+        pts = ((dirs * sd[ys, xs][:, None] - trans) @ rot).astype(np.float32).astype(np.float64)
+        out.append(dict(width=c["width"], height=c["height"], fx=float(np.float32(c["fx"])),
+                        fy=float(np.float32(c["fy"])), cx=float(np.float32(c["cx"])), cy=float(np.float32(c["cy"])),
+                        rot_cw=rot, trans_cw=trans, image=tgt, sparse=sd, points=pts, colors=tgt[ys, xs]))
+    return out
+
+
+def test_mapper_schedule_matches_reference():
+    """mapper.Mapper (R/mapper.py:267-316): init_map, expand_map
+    (opacity gate on the device), optimize_map rounds with the reference's per-keyframe RNG
+    streams, then one refine round -- same Gaussians added, same losses, same map."""
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    z = np.load(os.path.join(GOLD, "mapper.npz"))
+    m = M.Mapper(M.MappingConfig(), seed=0)
+    added = []
+    for d in _mapper_keyframes():
+        cam = R.Camera(d["width"], d["height"], d["fx"], d["fy"], d["cx"], d["cy"], d["rot_cw"], d["trans_cw"])
+        kf = M.Keyframe(cam=cam, image=d["image"], sparse_depth=d["sparse"], points=d["points"], colors=d["colors"])
+        n0 = len(m.gmap)
+        added.append(m.submit(kf))
+        assert len(m.gmap) == n0 + added[-1]
+    m.refine(1)
+    assert added == [int(a) for a in z["added"]]
+    ref = z["losses"]
+    assert abs(m.losses[0] - ref[0]) < REL_TOL * ref[0]
+    assert np.max(np.abs(np.array(m.losses) - ref) / ref) < 1e-2
+    assert np.array_equal(_np(m.adam.t)[:len(m.gmap)].astype(np.int64), z["adam_t"])
+    assert normwise(_np(m.gmap.rows())[:, :59], z["rows"]) < 5e-2
+    snap = m.snapshot()
+    assert snap is not m.gmap and len(snap) == len(m.gmap)
+
+
+def test_mapping_loop_drains_queue_and_refines():
+    import queue
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    q = queue.Queue()
+    for d in _mapper_keyframes()[:2]:
+        cam = R.Camera(d["width"], d["height"], d["fx"], d["fy"], d["cx"], d["cy"], d["rot_cw"], d["trans_cw"])
+        q.put(M.Keyframe(cam=cam, image=d["image"], sparse_depth=d["sparse"], points=d["points"], colors=d["colors"]))
+    q.put(None)
+    m = M.Mapper(M.MappingConfig(), seed=0)
+    M.mapping_loop(q, m)
+    assert len(m.keyframes) == 2 and len(m.losses) == 3  # two submits + max(refine_rounds, 1) round
+    q.join()
