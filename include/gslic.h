@@ -147,7 +147,7 @@ typedef struct gs_frame {
     float *g_depth;          /* H x W      xi dLd/ddepth */
     float *g_opac;           /* H x W      xi dLd/dopacity */
     double *loss_parts;      /* per-block partial sums */
-    double *loss;            /* 4: total, photometric, depth, dssim */
+    double *loss;            /* 8: total, photometric, depth, dssim, running sum (GS_LOSS_ACCUMULATE) */
     int64_t loss_blocks;
 } gs_frame;
 
@@ -189,9 +189,19 @@ int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream);
 /* R/losses.py:157-161 with the depth term on the view's LiDAR K-list; writes g_color,
  * g_depth, g_opac and loss[0..3]. */
 int gs_loss(const gs_frame *f, const gs_view *view, float lam, float xi, void *stream);
+/* flags: GS_LOSS_TABLES_READY -- the per-axis reflection tables of this image size are already in
+ * the workspace (a previous gs_loss built them): skip rebuilding; GS_LOSS_ACCUMULATE -- also add
+ * the total to loss[4] (a running sum the caller resets). gs_loss(...) = gs_loss_ex(..., 0). */
+#define GS_LOSS_TABLES_READY 1
+#define GS_LOSS_ACCUMULATE 2
+int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int32_t flags, void *stream);
 
 /* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
 int gs_render_bwd(const gs_frame *f, void *stream);
+/* flags = GS_BWD_ROWS_ZERO: the caller guarantees the touched Gaussians' g2d rows are zero (the
+ * engine: the chain rule clears every row it consumes), so they are not cleared first. */
+#define GS_BWD_ROWS_ZERO 1
+int gs_render_bwd_ex(const gs_frame *f, int32_t flags, void *stream);
 
 /* R/rasterizer.py:559-644 + :707-725 fused.  lr_cols: device (GS_ROW) per-column rates.
  * adam_t: per-Gaussian step counter (int32). */

@@ -22,6 +22,8 @@ CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3
 GS_CNT_SLOTS = 16
 GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists materialised on demand)
 GS_PP_LAZY_SH = 1  # gs_preprocess_ex flag of the iteration engine (colours only where blended)
+GS_LOSS_TABLES_READY, GS_LOSS_ACCUMULATE = 1, 2  # gs_loss_ex flags
+GS_BWD_ROWS_ZERO = 1  # gs_render_bwd_ex flag
 
 P = ctypes.c_void_p
 i32 = ctypes.c_int32
@@ -77,6 +79,8 @@ def lib():
         "gs_bin": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_render_fwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_loss": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, P]),
+        "gs_loss_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, i32, P]),
+        "gs_render_bwd_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_render_bwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), P]),
         "gs_chain_adam": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P]),
         "gs_chain_adam_part": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, i32, i32, i32, P]),
@@ -103,7 +107,7 @@ def lib():
 
 
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
-            "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_render_bwd", "gs_chain_adam",
+            "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
             "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
             "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_track_mask", "gs_track_grad", "gs_pose_adam"]
 

@@ -399,7 +399,7 @@ constexpr int LF_THREADS = 1024;
 static_assert(LF_THREADS % 3 == 1, "component bookkeeping of loss_finalize_kernel");
 
 __global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
-                                     float xi, float *tab_stamp) {
+                                     float xi, float *tab_stamp, int accumulate) {
     pdl_wait();
     // 1024 threads, coalesced over the flat (nparts x 3) array with 4 loads in flight each, then
     // a fixed-order shuffle tree: deterministic, and latency-bound only ~2 round trips deep
@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, c
         f.loss[1] = lc;
         f.loss[2] = ld;
         f.loss[3] = dssim;
+        if (accumulate) f.loss[4] += lc + (double)xi * ld;  // running sum of the engine's losses
         int *stamp = reinterpret_cast<int *>(tab_stamp);
         stamp[0] = (f.width << 16) + f.height;
         stamp[1] = ~((f.width << 16) + f.height);
@@ -461,7 +462,15 @@ int64_t loss_parts_needed(int32_t width, int32_t height) {
 }  // namespace gs
 
 extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float xi, void *stream) {
+    return gs_loss_ex(f, view, lam, xi, 0, stream);
+}
+
+extern "C" int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int32_t flags, void *stream) {
     using namespace gs;
+    if (flags & ~(GS_LOSS_TABLES_READY | GS_LOSS_ACCUMULATE)) {
+        set_error("gs_loss_ex: unknown flags");
+        return GS_ERR_ARG;
+    }
     cudaStream_t st = (cudaStream_t)stream;
     if (f->width <= 0 || f->height <= 0) {
         set_error("gs_loss: empty image");
@@ -474,15 +483,19 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
     }
     float *tab_x = reinterpret_cast<float *>(f->loss_parts + 3 * f->loss_blocks);
     float *tab_y = tab_x + 22 * f->width;
-    launch_pdl(loss_tables_kernel, (f->width + f->height + 127) / 128, 128, 0, st, tab_x, f->width, tab_y, f->height);
-    int rc = check_launch("loss_tables_kernel");
-    if (rc) return rc;
+    int rc;
+    if (!(flags & GS_LOSS_TABLES_READY)) {
+        launch_pdl(loss_tables_kernel, (f->width + f->height + 127) / 128, 128, 0, st, tab_x, f->width, tab_y,
+                   f->height);
+        if ((rc = check_launch("loss_tables_kernel"))) return rc;
+    }
     dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
     launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, xi, ssim_blocks);
     if ((rc = check_launch("depth_loss_kernel"))) return rc;
-    launch_pdl(loss_finalize_kernel, 1, LF_THREADS, 0, st, *f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi, tab_y + 22 * f->height);
+    launch_pdl(loss_finalize_kernel, 1, LF_THREADS, 0, st, *f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi,
+               tab_y + 22 * f->height, (flags & GS_LOSS_ACCUMULATE) ? 1 : 0);
     return check_launch("loss_finalize_kernel");
 }
 

@@ -468,10 +468,16 @@ extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream
     return check_launch("tile_finish_kernel");
 }
 
-extern "C" int gs_render_bwd(const gs_frame *f, void *stream) {
+extern "C" int gs_render_bwd(const gs_frame *f, void *stream) { return gs_render_bwd_ex(f, 0, stream); }
+
+extern "C" int gs_render_bwd_ex(const gs_frame *f, int32_t flags, void *stream) {
+    if (flags & ~GS_BWD_ROWS_ZERO) {
+        set_error("gs_render_bwd_ex: unknown flags");
+        return GS_ERR_ARG;
+    }
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
-    if (f->n > 0) {  // each backward starts from zero gradients (backward_2d is a pure function)
+    if (f->n > 0 && !(flags & GS_BWD_ROWS_ZERO)) {  // each backward starts from zero gradients (backward_2d is a pure function)
         // grid-stride over a small fixed grid: in the engine (lazy lists) every CTA exits at once
         launch_pdl(zero_g2d_kernel, 2 * 148, 256, 0, (cudaStream_t)stream, *f);
         int rc = check_launch("zero_g2d_kernel");

@@ -29,13 +29,14 @@ def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     """Our kernels per map-optimisation iteration:
     preprocess 5 (projection + small-footprint cull, large-footprint setup / bands / tiles /
     finish), bin 3 (lazy lists: huge sort, huge transpose, tile scan), forward 3 (blend, bucket
-    fill + sorted continuation for the tiles that need them), loss 4 (tables, SSIM+L1, depth,
-    finalize), backward 2 (zero + tiles), chain rule fused with Adam 1 (2 with
-    GSLIC_SPLIT_ADAM=1: chain + adam_list)."""
+    fill + sorted continuation for the tiles that need them), loss 3 (SSIM+L1, depth, finalize;
+    the reflection tables are built once per workspace), backward 1 (the g2d rows are kept
+    zero by the chain rule), chain rule fused with Adam 1 (2 with GSLIC_SPLIT_ADAM=1: chain +
+    adam_list)."""
     del tiles
     import os
     split = os.environ.get("GSLIC_SPLIT_ADAM", "0") == "1"
-    return 5 + 3 + 3 + 4 + 2 + (1 if chain_only or not split else 2)
+    return 5 + 3 + 3 + 3 + 1 + (1 if chain_only or not split else 2)
 
 
 @dataclass
@@ -182,8 +183,7 @@ class MapOptimizer:
             _, cnt = _bin_frame(self.g, v, True)
             emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
         self.headroom = headroom
-        self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
-        self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.ws = self._workspace(int(emax * headroom) + 4096)
         self.graph = None
         self._ring = [torch.zeros(8, dtype=torch.int32).pin_memory() for _ in range(4)]
         self._events = [None] * 4
@@ -193,16 +193,22 @@ class MapOptimizer:
         self.overlap_parts = int(os.environ.get("GSLIC_OVERLAP_PARTS", "0"))
         self._side = torch.cuda.Stream(device=self.dev)
 
+    def _workspace(self, capacity: int) -> Workspace:
+        """A zero-filled workspace whose loss reflection tables are built (one gs_loss on the
+        blank images), so the captured iteration can skip that launch (GS_LOSS_TABLES_READY)."""
+        ws = Workspace(len(self.g), self.W, self.H, capacity, self.dev)
+        call("gs_loss", ws.fptr, self.views[0].ptr, self.lam, self.xi, stream_ptr())
+        return ws
+
     # -- one iteration: R/mapper.py:249-256 --------------------------------------------
     def _launch(self) -> None:
         f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss", f, cur, self.lam, self.xi, s)
-        call("gs_render_bwd", f, s)
+        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_ACCUMULATE, s)
+        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the fused chain clears the rows it consumes
         self._chain_adam()
-        self.loss_acc += self.ws.loss[0:1]
 
     def _chain_adam(self) -> None:
         """Chain rule + sparse Adam.  overlap_parts > 1: the touched list is cut into chunks; the
@@ -259,7 +265,9 @@ class MapOptimizer:
                             "raise MapOptimizer headroom")
         if int(cnt[_lib.CNT_ENTRIES]) > 0.9 * self.ws.capacity:
             torch.cuda.current_stream().synchronize()
-            self.ws = Workspace(len(self.g), self.W, self.H, int(int(cnt[_lib.CNT_ENTRIES]) * self.headroom), self.dev)
+            old = self.ws
+            self.ws = self._workspace(int(int(cnt[_lib.CNT_ENTRIES]) * self.headroom))
+            self.ws.loss[4:5].copy_(old.loss[4:5])  # the running loss sum moves along
             if self.graph is not None:
                 self.capture()
 
@@ -281,9 +289,9 @@ class MapOptimizer:
         ev[2].record()
         call("gs_render_fwd", f, 1, s)
         ev[3].record()
-        call("gs_loss", f, cur, self.lam, self.xi, s)
+        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_ACCUMULATE, s)
         ev[4].record()
-        call("gs_render_bwd", f, s)
+        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)
         ev[5].record()
         self._chain_adam()
         ev[6].record()
@@ -341,9 +349,11 @@ class MapOptimizer:
             dst.copy_(src)
 
     def loss_sum(self, reset: bool = True) -> float:
-        v = float(self.loss_acc.item())
+        """Sum of the losses of the iterations since the last reset (ws.loss[4], accumulated on
+        the device by the loss kernel)."""
+        v = float(self.ws.loss[4].item())
         if reset:
-            self.loss_acc.zero_()
+            self.ws.loss[4:5].zero_()
         return v
 
     def counters(self) -> dict:

@@ -39,6 +39,7 @@ class PoseRefiner:
         self.lr, self.opac_gate = float(lr), float(opac_gate)
         _, cnt = _bin_frame(self.g, self.view, True)
         self.ws = Workspace(len(self.g), w, h, int(int(cnt[_lib.CNT_ENTRIES]) * headroom) + 4096, self.dev)
+        call("gs_loss", self.ws.fptr, self.view.ptr, 0.5, 0.0, stream_ptr())  # builds the reflection tables
         self.mask = torch.empty(h * w, dtype=torch.uint8, device=self.dev)
         call("gs_track_mask", self.view.target.data_ptr(), w, h, float(grad_gate), self.mask.data_ptr(), stream_ptr())
         self.pose_grad = torch.zeros(6, dtype=torch.float64, device=self.dev)
@@ -64,9 +65,9 @@ class PoseRefiner:
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), v, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss", f, v, 0.5, 0.0, s)  # R/odometry.py:323: photometric_loss(lam=0.5)
+        call("gs_loss_ex", f, v, 0.5, 0.0, _lib.GS_LOSS_TABLES_READY, s)  # R/odometry.py:323: photometric_loss(lam=0.5)
         call("gs_track_grad", f, self.mask.data_ptr(), self.opac_gate, s)
-        call("gs_render_bwd", f, s)
+        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the pose chain clears the rows it consumes
         call("gs_chain_pose", f, self.g.data.data_ptr(), None, None, v, self.pose_grad.data_ptr(), s)
         call("gs_pose_adam", v, self.state.data_ptr(), self.pose_grad.data_ptr(), self.lr, s)
 

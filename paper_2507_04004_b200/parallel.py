@@ -58,6 +58,7 @@ class BatchMapOptimizer:
             _, cnt = _bin_frame(self.g, v, True)
             emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
         self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
+        call("gs_loss", self.ws.fptr, self.views[0].ptr, self.lam, self.xi, stream_ptr())  # reflection tables
         n = len(self.g)
         self.grads = torch.zeros((n, GS_ROW), dtype=torch.float32, device=self.dev)
         self.touched = torch.zeros(n, dtype=torch.uint8, device=self.dev)
@@ -79,8 +80,8 @@ class BatchMapOptimizer:
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss", f, cur, self.lam, self.xi, s)
-        call("gs_render_bwd", f, s)
+        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY, s)
+        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # gs_chain clears the rows it consumes
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
         self.loss_acc += self.ws.loss[0:1]
 
