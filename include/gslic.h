@@ -64,7 +64,7 @@ enum {
     GS_CNT_OVERFLOW = 3, /* nonzero when E exceeded entry_capacity (downstream kernels no-op) */
     GS_CNT_ENTRIES_EFF = 4, /* E, or 0 after an overflow (what the downstream kernels use) */
     GS_CNT_BIG = 5,      /* Gaussians culled warp-cooperatively (many candidate tiles) */
-    GS_CNT_RESERVED6 = 6,
+    GS_CNT_LOSS_TICKET = 6, /* blocks of the loss kernel done (the last one finalises; self-resetting) */
     GS_CNT_BIG_BITS = 7, /* words of big_bits in use */
     GS_CNT_SLOTS = 16,
     /* slots 8-15: look-back tickets; second half of the counters array: */

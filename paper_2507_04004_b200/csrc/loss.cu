@@ -46,7 +46,7 @@ __device__ __forceinline__ int reflect_idx(int j, int n) {  // R/losses.py:31-42
 // (adjoint, zero where p+d leaves the axis).  Layout: x axis (w positions) then y axis.
 __global__ void loss_tables_kernel(float *tab_x, int w, float *tab_y, int h) {
     pdl_wait();
-    // the tables depend only on (w, h): loss_finalize_kernel stamps them valid after first use
+    // the tables depend only on (w, h): the loss finalisation stamps them valid after first use
     const int *stamp = reinterpret_cast<const int *>(tab_y + 22 * h);
     if (stamp[0] == (w << 16) + h && stamp[1] == ~((w << 16) + h)) return;
     double K[11], s = 0.0;
@@ -364,10 +364,18 @@ __global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const
 }
 
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
-__global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_view *__restrict__ view, float xi,
-                                                         int64_t part0) {
+// (defined below)
+template <int NT>
+__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t nparts,
+                                              float lam, float xi, float *tab_stamp, int accumulate);
+
+// depth_ratio_loss on the LiDAR K-list, then -- in the last block to finish, found by a ticket
+// (threadfence reduction) -- the mapping loss from all block partials: no separate finalize launch
+__global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_view *__restrict__ view, float lam,
+                                                         float xi, int64_t part0, float *tab_stamp, int accumulate) {
     pdl_wait();
     __shared__ float red[8];
+    __shared__ int s_last;
     const int32_t K = view->lidar_k;
     const int32_t *idx = view->lidar_idx;
     const float *zl = view->lidar_z;
@@ -392,30 +400,35 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
         f.loss_parts[3 * (part0 + blockIdx.x) + 2] = s;
         f.loss_parts[3 * (part0 + blockIdx.x)] = 0.0;
         f.loss_parts[3 * (part0 + blockIdx.x) + 1] = 0.0;
+        __threadfence();
+        s_last = atomicAdd(&f.counters[GS_CNT_LOSS_TICKET], 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last) {
+        __threadfence();
+        finalize_body<256>(f, view, part0 + gridDim.x, lam, xi, tab_stamp, accumulate);
+        if (threadIdx.x == 0) f.counters[GS_CNT_LOSS_TICKET] = 0;
     }
 }
 
-constexpr int LF_THREADS = 1024;
-static_assert(LF_THREADS % 3 == 1, "component bookkeeping of loss_finalize_kernel");
 
-__global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, const gs_view *__restrict__ view, int64_t nparts, float lam,
-                                     float xi, float *tab_stamp, int accumulate) {
-    pdl_wait();
-    // 1024 threads, coalesced over the flat (nparts x 3) array with 4 loads in flight each, then
-    // a fixed-order shuffle tree: deterministic, and latency-bound only ~2 round trips deep
-    __shared__ double r[3][32];
+// mapping_loss from the block partials (R/losses.py:157-161), by NT threads: coalesced over the
+// flat (nparts x 3) array, then a fixed-order shuffle tree -- deterministic
+template <int NT>
+__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t nparts,
+                                              float lam, float xi, float *tab_stamp, int accumulate) {
+    static_assert(NT % 3 == 1, "component bookkeeping: thread t keeps component (t + j) % 3 in acc[j]");
+    __shared__ double r[3][NT / 32];
     const int64_t total = 3 * nparts;
     double acc[3] = {0.0, 0.0, 0.0};
-    const int64_t stride = LF_THREADS * 3;  // every thread keeps one component
+    const int64_t stride = NT * 3;  // element e is component e % 3, and 3 NT % 3 == 0
     const int comp0 = threadIdx.x % 3;
-    // thread t reads elements t, t + 3072, ...: element e is component e % 3, and 3072 % 3 == 0
 #pragma unroll 4
     for (int64_t e = threadIdx.x; e < total; e += stride) {
         acc[0] += f.loss_parts[e];
-        if (e + LF_THREADS < total) acc[1] += f.loss_parts[e + LF_THREADS];
-        if (e + 2 * LF_THREADS < total) acc[2] += f.loss_parts[e + 2 * LF_THREADS];
+        if (e + NT < total) acc[1] += f.loss_parts[e + NT];
+        if (e + 2 * NT < total) acc[2] += f.loss_parts[e + 2 * NT];
     }
-    // acc[j] holds component (comp0 + j * (LF_THREADS % 3)) % 3 -- LF_THREADS % 3 == 1
     double comp[3];
 #pragma unroll
     for (int j = 0; j < 3; j++) comp[(comp0 + j) % 3] = acc[j];
@@ -430,7 +443,7 @@ __global__ void __launch_bounds__(LF_THREADS) loss_finalize_kernel(gs_frame f, c
     __syncthreads();
     if (threadIdx.x == 0) {
         double l1 = 0.0, ss = 0.0, dd = 0.0;
-        for (int k = 0; k < LF_THREADS / 32; k++) {
+        for (int k = 0; k < NT / 32; k++) {
             l1 += r[0][k];
             ss += r[1][k];
             dd += r[2][k];
@@ -492,11 +505,9 @@ extern "C" int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, flo
     dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
     launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
-    launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, xi, ssim_blocks);
-    if ((rc = check_launch("depth_loss_kernel"))) return rc;
-    launch_pdl(loss_finalize_kernel, 1, LF_THREADS, 0, st, *f, view, ssim_blocks + DEPTH_BLOCKS, lam, xi,
-               tab_y + 22 * f->height, (flags & GS_LOSS_ACCUMULATE) ? 1 : 0);
-    return check_launch("loss_finalize_kernel");
+    launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, lam, xi, ssim_blocks, tab_y + 22 * f->height,
+               (flags & GS_LOSS_ACCUMULATE) ? 1 : 0);
+    return check_launch("depth_loss_kernel");
 }
 
 namespace gs {
