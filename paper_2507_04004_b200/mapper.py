@@ -135,9 +135,10 @@ class HostKeyframes:
             ev.record(cs)
         return ev
 
-    def stream(self, order, body) -> None:
-        """For j, k in enumerate(order): keyframe k lands in `cur`'s slot, then body(j, k) runs the
-        iteration on the current stream; keyframe j+1 uploads meanwhile."""
+    def stream(self, order, body, use_cur: bool = True) -> None:
+        """For j, k in enumerate(order): keyframe k lands in a slot, then body(j, k, view_ptr) runs
+        the iteration on the current stream (view_ptr: the slot's device gs_view; copied into
+        `cur` first when use_cur); keyframe j+1 .. uploads meanwhile."""
         main = torch.cuda.current_stream()
         order = [int(k) for k in order]
         if not order:
@@ -150,9 +151,13 @@ class HostKeyframes:
         for j, k in enumerate(order):
             if j + ahead < len(order):
                 ready[j + ahead] = self.upload(j + ahead, order[j + ahead])
-            main.wait_event(ready.pop(j))
-            self.cur.copy_(self.slots[j % self.NSLOT]["view"])
-            body(j, k)
+            ev = ready.pop(j)
+            if not ev.query():  # uploads run ahead: usually landed already, no device-side wait
+                main.wait_event(ev)
+            view = self.slots[j % self.NSLOT]["view"]
+            if use_cur:
+                self.cur.copy_(view)
+            body(j, k, view.data_ptr())
             free = torch.cuda.Event()
             free.record(main)
             self.slot_free[j % self.NSLOT] = free
@@ -186,6 +191,7 @@ class MapOptimizer:
         self.headroom = headroom
         self.ws = self._workspace(int(emax * headroom) + 4096)
         self.graph = None
+        self.graphs: dict = {}
         self._ring = [torch.zeros(8, dtype=torch.int32).pin_memory() for _ in range(4)]
         self._events = [None] * 4
         self._steps = 0
@@ -202,20 +208,22 @@ class MapOptimizer:
         return ws
 
     # -- one iteration: R/mapper.py:249-256 --------------------------------------------
-    def _launch(self) -> None:
-        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+    def _launch(self, view_ptr: int | None = None) -> None:
+        f, s = self.ws.fptr, stream_ptr()
+        cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_ACCUMULATE, s)
         call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the fused chain clears the rows it consumes
-        self._chain_adam()
+        self._chain_adam(cur)
 
-    def _chain_adam(self) -> None:
+    def _chain_adam(self, view_ptr: int | None = None) -> None:
         """Chain rule + sparse Adam.  overlap_parts > 1: the touched list is cut into chunks; the
         FP64 chain of chunk i+1 runs on this stream while the HBM-bound Adam stream of chunk i runs
         on a side stream (gs_chain_adam_part), so latency-bound math and bandwidth overlap."""
-        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+        f, s = self.ws.fptr, stream_ptr()
+        cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         args = (self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
                 self.adam.t.data_ptr(), cur, self.lr.data_ptr())
         P = self.overlap_parts
@@ -233,19 +241,31 @@ class MapOptimizer:
         main.wait_stream(self._side)
 
     def capture(self) -> None:
-        """Capture the launch sequence into a CUDA graph (replayed by step())."""
+        """Capture the launch sequence into CUDA graphs: one per device view (keyframes, host
+        slots), each reading its own gs_view, so a step is a single replay with no view copy."""
         torch.cuda.current_stream().synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):  # capture records the launches; it executes nothing
             self._launch()
         self.graph = g
+        self.graphs = {}
+
+    def _graph_for(self, view_ptr: int):
+        gr = self.graphs.get(view_ptr)
+        if gr is None:
+            torch.cuda.current_stream().synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self._launch(view_ptr)
+            self.graphs[view_ptr] = gr
+        return gr
 
     def step(self, k: int) -> None:
         self._check()
-        self.cur.copy_(self.views[k].buf)
         if self.graph is not None:
-            self.graph.replay()
+            self._graph_for(self.views[k].ptr).replay()
         else:
+            self.cur.copy_(self.views[k].buf)
             self._launch()
         slot = self._steps % 4
         self._ring[slot].copy_(self.ws.counters[:8], non_blocking=True)
@@ -270,7 +290,7 @@ class MapOptimizer:
             self.ws = self._workspace(int(int(cnt[_lib.CNT_ENTRIES]) * self.headroom))
             self.ws.loss[4:5].copy_(old.loss[4:5])  # the running loss sum moves along
             if self.graph is not None:
-                self.capture()
+                self.capture()  # (the per-view graphs are re-captured on first use)
 
     PHASES = ("preprocess", "bin", "render_fwd", "loss", "render_bwd", "chain_adam")
 
@@ -312,12 +332,12 @@ class MapOptimizer:
         """Map-optimisation iterations over host keyframes `order` (R/mapper.py:242-256 samples
         the keyframe order up front): keyframe j+1 is uploaded on a copy stream while iteration j
         runs; each iteration's loss is read back into pinned host memory (D2H)."""
-        def body(j, k):
+        def body(j, k, view_ptr):
             self._check()
             if self.graph is not None:
-                self.graph.replay()
+                self._graph_for(view_ptr).replay()
             else:
-                self._launch()
+                self._launch(view_ptr)
             # the loss read-back rides on the copy stream: the next iteration does not queue behind it
             done = torch.cuda.Event()
             done.record()
@@ -333,7 +353,7 @@ class MapOptimizer:
             self._events[s] = ev
             self._steps += 1
 
-        self.host.stream(order, body)
+        self.host.stream(order, body, use_cur=False)
 
     def step_host(self, k: int, slot: int = 0) -> None:
         """One iteration on host keyframe k (no prefetch): run_host([k])."""

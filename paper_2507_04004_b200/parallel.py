@@ -97,7 +97,7 @@ class BatchMapOptimizer:
         view runs, then the allreduce and the Adam step; the batch loss is read back (D2H)."""
         self.grads.zero_()
         self.touched.zero_()
-        self.host.stream(view_ids, lambda j, k: self._accumulate_cur())
+        self.host.stream(view_ids, lambda j, k, view_ptr: self._accumulate_cur())
         self._finish()
         self._h_loss.copy_(self.loss_acc, non_blocking=True)
 
