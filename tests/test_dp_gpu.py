@@ -1,0 +1,79 @@
+"""The multi-GPU keyframe-batch path end to end on the GPU with two ranks: two
+processes share the one B200 of the test box (gloo carries the collective; NCCL refuses two ranks
+on one device), each runs parallel.BatchMapOptimizer on its half of the batch through the sm_100a
+kernels, the gradient rows + touched flags are allreduced in one collective and each rank applies
+the same sparse Adam.  The replicas must end bit-identical, and equal (to the atomic-order noise
+of the backward) the single-process batch over all views."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+VIEWS = (0, 8, 16, 24)
+
+
+def _scene():
+    from paper_2507_04004_b200 import scenes
+    return scenes.scene_room(8192, 128, 72, lidar=16, render_views=VIEWS)
+
+
+def _engine(sc, ids):
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import parallel as PAR
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    kfs = [M.Keyframe(R.camera_from(sc.cams[k]), sc.targets[k], sc.sparse_depths[k]) for k in ids]
+    return PAR.BatchMapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sc = _scene()
+    mine = list(range(rank, len(VIEWS), world))
+    eng = _engine(sc, mine)
+    eng.step(range(len(mine)))
+    torch.cuda.synchronize()
+    np.save(out.format(f"g{rank}"), eng.grads.cpu().numpy())  # allreduced gradient rows
+    np.save(out.format(f"m{rank}"), eng.touched.cpu().numpy())
+    eng.step(range(len(mine)))
+    torch.cuda.synchronize()
+    np.save(out.format(rank), eng.g.rows().cpu().numpy())
+    np.save(out.format(f"t{rank}"), eng.adam.t.cpu().numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(900)
+def test_two_ranks_on_device_match_single_process_batch(tmp_path):
+    out = str(tmp_path / "r_{}.npy")
+    mp.spawn(_worker, args=(2, _port(), out), nprocs=2, join=True)
+    r0, r1 = np.load(out.format(0)), np.load(out.format(1))
+    assert np.array_equal(r0, r1)  # replicas bit-identical after two batch steps
+    assert np.array_equal(np.load(out.format("t0")), np.load(out.format("t1")))
+    assert np.array_equal(np.load(out.format("g0")), np.load(out.format("g1")))
+    sc = _scene()
+    eng = _engine(sc, list(range(len(VIEWS))))
+    eng.step(range(len(VIEWS)))
+    torch.cuda.synchronize()
+    # the batch gradient of the single process (same views, other summation order)
+    gref, g0 = eng.grads.cpu().numpy()[:, :59], np.load(out.format("g0"))[:, :59]
+    assert np.array_equal(eng.touched.cpu().numpy(), np.load(out.format("m0")))
+    assert np.max(np.abs(g0 - gref)) / np.max(np.abs(gref)) < 1e-3
+    eng.step(range(len(VIEWS)))
+    assert np.array_equal(eng.adam.t.cpu().numpy(), np.load(out.format("t0")))
