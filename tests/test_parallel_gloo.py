@@ -34,7 +34,7 @@ def _view_grads(sc, rows, k):
     return O.grads_to_rows(grads), touched
 
 
-def _worker(rank, world, port, result_path):
+def _worker(rank, world, port, result_path, sparse=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2507_04004_b200 import parallel as PAR
@@ -47,7 +47,10 @@ def _worker(rank, world, port, result_path):
         gr, t = _view_grads(sc, rows, k)
         acc[:, :59] += torch.as_tensor(gr, dtype=torch.float32)
         touched |= torch.as_tensor(t.astype(np.uint8))
-    PAR.allreduce_grads(acc, touched)
+    if sparse:
+        PAR.allreduce_grads_sparse(acc, touched)
+    else:
+        PAR.allreduce_grads(acc, touched)
     st = O.AdamState()
     O.adam_rows(rows, acc[:, :59].double().numpy(), touched.numpy().astype(bool), st, O.default_lrs(3.0))
     np.save(result_path.format(rank), rows)
@@ -65,9 +68,11 @@ def _free_port():
 
 
 @pytest.mark.timeout(600)
-def test_batch_dp_two_ranks_matches_batch_oracle(tmp_path):
+@pytest.mark.parametrize("sparse", [False, True])
+def test_batch_dp_two_ranks_matches_batch_oracle(tmp_path, sparse):
+    """Dense (one collective, flag in the padding column) and two-phase sparse allreduce."""
     path = str(tmp_path / "rows_{}.npy")
-    mp.spawn(_worker, args=(2, _free_port(), path), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), path, sparse), nprocs=2, join=True)
     r0 = np.load(path.format(0))
     r1 = np.load(path.format(1))
     assert np.array_equal(r0, r1), "replicas diverged"
