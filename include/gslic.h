@@ -268,6 +268,10 @@ int gs_zbuffer(const float *points, int64_t m, const gs_camera *cam, int32_t wid
 int gs_init_rows(const float *points, const float *colors, const float *depths, int64_t m, float focal,
                  float *rows, void *stream);
 
+/* 8-bit frame (n bytes, e.g. an RGB camera image) -> float32 k / 255 (computed in FP64, rounded
+ * once: bit-identical to the fp32 rounding of a float64 image loaded from PNG, R/io_formats.py:52-57) */
+int gs_decode_u8(const uint8_t *src, float *dst, int64_t n, void *stream);
+
 /* ---- photometric pose refinement (SURVEY.md 8f row 2, R/odometry.py:305-336) ------------- */
 /* img_mask[p] = |np.gradient(mean over channels of image)| > grad_gate (R/odometry.py:314-316) */
 int gs_track_mask(const float *image, int32_t width, int32_t height, float grad_gate, uint8_t *mask, void *stream);

@@ -89,6 +89,7 @@ def lib():
         "gs_project_points": (ctypes.c_int, [P, i64, P, P, P, f32, P, P, P, P, P, P, P, P]),
         "gs_zbuffer": (ctypes.c_int, [P, i64, P, i32, i32, P, P, P]),
         "gs_init_rows": (ctypes.c_int, [P, P, P, i64, f32, P, P]),
+        "gs_decode_u8": (ctypes.c_int, [P, P, i64, P]),
         "gs_track_mask": (ctypes.c_int, [P, i32, i32, f32, P, P]),
         "gs_track_grad": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, P]),
         "gs_pose_adam": (ctypes.c_int, [P, P, P, f32, P]),
@@ -109,7 +110,7 @@ def lib():
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
             "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
             "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
-            "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_track_mask", "gs_track_grad", "gs_pose_adam"]
+            "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_decode_u8", "gs_track_mask", "gs_track_grad", "gs_pose_adam"]
 
 
 def check(rc: int, what: str) -> None:

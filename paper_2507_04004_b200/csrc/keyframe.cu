@@ -131,6 +131,14 @@ __global__ void init_rows_kernel(const float *__restrict__ points, const float *
     }
 }
 
+// 8-bit camera frame -> the fp32 target: v = k / 255 in FP64, rounded once -- bit-identical to
+// the fp32 rounding of the reference's float64 image k / 255 (R/io_formats.py:52-57)
+__global__ void u8_to_f32_kernel(const uint8_t *__restrict__ src, float *__restrict__ dst, int64_t n) {
+    pdl_wait();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = (float)((double)src[i] / 255.0);
+}
+
 }  // namespace gs
 
 using namespace gs;
@@ -181,4 +189,14 @@ extern "C" int gs_init_rows(const float *points, const float *colors, const floa
     if (m == 0) return GS_OK;
     launch_pdl(init_rows_kernel, grid_for(m * 16), 256, 0, (cudaStream_t)stream, points, colors, depths, m, focal, rows);
     return check_launch("init_rows_kernel");
+}
+
+extern "C" int gs_decode_u8(const uint8_t *src, float *dst, int64_t n, void *stream) {
+    if (n < 0 || (n > 0 && (!src || !dst))) {
+        set_error("gs_decode_u8: bad arguments");
+        return GS_ERR_ARG;
+    }
+    if (n == 0) return GS_OK;
+    launch_pdl(u8_to_f32_kernel, grid_for(n), 256, 0, (cudaStream_t)stream, src, dst, n);
+    return check_launch("u8_to_f32_kernel");
 }

@@ -76,6 +76,19 @@ class Keyframe:
     stamp: float = 0.0
 
 
+def _host_frame(image, h: int, w: int) -> torch.Tensor:
+    """A keyframe image in pinned host memory: as 8 bits when every value is exactly k / 255 (a
+    camera frame, R/io_formats.py:52-57 -- decoded on the device by gs_decode_u8 to the same fp32
+    values), else as float32."""
+    img = image.detach().double().cpu().numpy() if isinstance(image, torch.Tensor) else \
+        np.asarray(image, dtype=np.float64)
+    img = img.reshape(h, w, 3)
+    q = np.round(img * 255.0)
+    if np.all((q >= 0) & (q <= 255)) and np.array_equal(q / 255.0, img):
+        return torch.as_tensor(q.astype(np.uint8)).pin_memory()
+    return torch.as_tensor(img.astype(np.float32)).pin_memory()
+
+
 class HostKeyframes:
     """Keyframes in pinned host memory -- the target image and the LiDAR returns as a K-list
     (pixel index, depth; compacted once here, as the device path caches it) -- streamed into
@@ -90,7 +103,7 @@ class HostKeyframes:
         self.cur, self.dev = cur, device
         self.img, self.idx, self.z = [], [], []
         for kf in keyframes:
-            self.img.append(torch.as_tensor(np.asarray(kf.image, dtype=np.float32)).reshape(h, w, 3).pin_memory())
+            self.img.append(_host_frame(kf.image, h, w))
             sd = np.asarray(kf.sparse_depth, dtype=np.float32).reshape(-1) if kf.sparse_depth is not None else \
                 np.zeros(h * w, np.float32)
             idx = np.flatnonzero(sd > 0).astype(np.int32)  # pixel order, as gs_lidar_compact
@@ -98,6 +111,7 @@ class HostKeyframes:
             self.z.append(torch.as_tensor(sd[idx]).pin_memory())
         kmax = max(1, max(len(i) for i in self.idx))
         self.slots = [{"img": torch.empty((h, w, 3), device=device),
+                       "u8": torch.empty((h, w, 3), dtype=torch.uint8, device=device),
                        "idx": torch.empty(kmax, dtype=torch.int32, device=device),
                        "z": torch.empty(kmax, device=device), "view": torch.empty_like(cur)}
                       for _ in range(self.NSLOT)]
@@ -113,8 +127,8 @@ class HostKeyframes:
             self.views.append(per)
         self.copy_stream = torch.cuda.Stream(device=device)
         self.slot_free = [None] * self.NSLOT
-        nbytes = [self.img[k].numel() * 4 + self.idx[k].numel() * 8 + self.views[k][0].numel()
-                  for k in range(len(keyframes))]
+        nbytes = [self.img[k].numel() * self.img[k].element_size() + self.idx[k].numel() * 8 +
+                  self.views[k][0].numel() for k in range(len(keyframes))]
         self.h2d_bytes = int(round(float(np.mean(nbytes))))
 
     def upload(self, j: int, k: int) -> torch.cuda.Event:
@@ -126,7 +140,11 @@ class HostKeyframes:
             if self.slot_free[s] is not None:
                 cs.wait_event(self.slot_free[s])
             kk = self.idx[k].numel()
-            sl["img"].copy_(self.img[k], non_blocking=True)
+            if self.img[k].dtype == torch.uint8:  # 8-bit frame: a quarter of the bytes, exact decode
+                sl["u8"].copy_(self.img[k], non_blocking=True)
+                call("gs_decode_u8", sl["u8"].data_ptr(), sl["img"].data_ptr(), sl["img"].numel(), stream_ptr())
+            else:
+                sl["img"].copy_(self.img[k], non_blocking=True)
             if kk:
                 sl["idx"][:kk].copy_(self.idx[k], non_blocking=True)
                 sl["z"][:kk].copy_(self.z[k], non_blocking=True)

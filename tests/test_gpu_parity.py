@@ -453,15 +453,19 @@ def test_pose_gradient_fd_scenes(seed):
     assert normwise(_np(grads["_rows"])[:, :59], p[f"{key}_grads"]) < REL_TOL
 
 
-def test_host_streaming_matches_device_keyframes():
-    """MapOptimizer.run_host (pinned host keyframes, K-list compacted on the host, H2D double-
-    buffered on a copy stream) runs the same iterations as device-resident keyframes."""
+@pytest.mark.parametrize("frames", ["float", "8bit"])
+def test_host_streaming_matches_device_keyframes(frames):
+    """MapOptimizer.run_host (pinned host keyframes, K-list compacted on the host, H2D multi-
+    buffered on a copy stream; 8-bit frames decoded on the device) runs the same iterations as
+    device-resident keyframes."""
     import torch
     from paper_2507_04004_b200 import mapper as M
     from paper_2507_04004_b200 import rasterizer as R
     from paper_2507_04004_b200 import scenes
     from paper_2507_04004_b200.gaussians import GaussianMap
     sc = scenes.scene_room(8192, 160, 96, lidar=16, render_views=(0, 1, 2))
+    if frames == "8bit":
+        sc.targets = [np.round(np.clip(t, 0, 1) * 255.0) / 255.0 for t in sc.targets]
     kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
     order = [0, 2, 1, 1, 0, 2, 2]
     a = M.MapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
@@ -473,6 +477,7 @@ def test_host_streaming_matches_device_keyframes():
     b = M.MapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
     b.capture()
     b.attach_host_keyframes(kfs)
+    assert (b.host.img[0].dtype == torch.uint8) == (frames == "8bit")
     b.run_host(order)
     torch.cuda.synchronize()
     lb = b._h_loss[:len(order)].numpy()
