@@ -338,7 +338,8 @@ __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const flo
 
 // 128 threads per 16x16 tile, two pixels per thread (rows y and y + 8): the two pixels'
 // contributions are summed in registers before the warp reduction.
-constexpr int BT = 128;
+constexpr int BPX = 2;              // pixels per backward thread (one column, rows 16 / BPX apart; 4 measured no faster)
+constexpr int BT = RT / BPX;        // backward threads per tile
 
 __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
     pdl_wait();
@@ -370,13 +371,14 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
         // lazy, unflagged: the blend ended within the leading screen-covering Gaussians
         return lazy ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : f.entry_splat[start + p];
     };
-    BwdPixel px[2];
+    BwdPixel px[BPX];
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
+    int mc = 0;
 #pragma unroll
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < BPX; k++) {
         BwdPixel &p = px[k];
-        const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + 8 * k;
+        const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / BPX) * k;
         p.fx = (float)x;
         p.fy = (float)y;
         p.T = 1.0f;
@@ -394,7 +396,9 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
             p.go = f.g_opac[q];
         }
     }
-    atomicMax(&s_max, max(px[0].cnt, px[1].cnt));
+#pragma unroll
+    for (int k = 0; k < BPX; k++) mc = max(mc, px[k].cnt);
+    atomicMax(&s_max, mc);
     __syncthreads();
     const int max_cnt = s_max;
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
@@ -414,14 +418,17 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
         __syncthreads();
         for (int j = nb - 1; j >= 0; j--) {
             const int le = b0 + j - start;
-            const bool c0 = le < px[0].cnt, c1 = le < px[1].cnt;
-            if (!__any_sync(0xffffffffu, c0 || c1)) continue;
+            bool any = false;
+#pragma unroll
+            for (int k = 0; k < BPX; k++) any |= le < px[k].cnt;
+            if (!__any_sync(0xffffffffu, any)) continue;
             const float4 A = s_a[j], B = s_b[j], C = s_c[j];
             float v[10];
 #pragma unroll
             for (int k = 0; k < 10; k++) v[k] = 0.0f;
-            if (c0) bwd_step(px[0], A, B, C, v);
-            if (c1) bwd_step(px[1], A, B, C, v);
+#pragma unroll
+            for (int k = 0; k < BPX; k++)
+                if (le < px[k].cnt) bwd_step(px[k], A, B, C, v);
             const float sum = reduce10(v);
             if (fld >= 0 && sum != 0.0f) atomicAdd(&s_acc[j][fld], sum);
         }
