@@ -277,7 +277,7 @@ def run_ours(args) -> dict:
         "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: S2r room scene (seed 7), Gaussians seeded on ray-cast surfaces from 32 views, "
-                "targets and LiDAR ray-traced; random-free deterministic generator",
+                "targets (8-bit, like camera frames) and LiDAR ray-traced; random-free deterministic generator",
         "config": {"workload": name, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
                    "keyframes": nv, "semantics": "per-keyframe sparse Adam (R/mapper.py:246-257)",
                    "l2": "inputs larger than L2 (params + Adam moments = 768 MB per step)",
