@@ -224,7 +224,8 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
     // touched-list chunk `part` of `nparts` (warp-aligned bounds)
-    const int64_t kb = (ntt * part / nparts) & ~(int64_t)31;
+    // (no 64-bit divide -- a long subroutine -- on the common single-chunk path)
+    const int64_t kb = nparts == 1 ? 0 : (ntt * part / nparts) & ~(int64_t)31;
     const int64_t nt = part == nparts - 1 ? ntt : ((ntt * (part + 1) / nparts) & ~(int64_t)31);
     const int64_t k0 = kb + ((int64_t)blockIdx.x * CA_WARPS + warp) * 32;
     if (k0 >= nt) return;
@@ -358,7 +359,7 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
                                                         const float *__restrict__ lr_cols, int part, int nparts) {
     pdl_wait();
     const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
-    const int64_t kb = (ntt * part / nparts) & ~(int64_t)31;
+    const int64_t kb = nparts == 1 ? 0 : (ntt * part / nparts) & ~(int64_t)31;
     const int64_t nt = part == nparts - 1 ? ntt : ((ntt * (part + 1) / nparts) & ~(int64_t)31);
     for (int64_t idx = kb * 16 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < nt * 16;
          idx += (int64_t)gridDim.x * blockDim.x) {
