@@ -342,18 +342,6 @@ __device__ __forceinline__ bool tile_keep(float mx, float my, float ca, float cb
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
-// Whether entry words fit 32 bits as (tile << rank_bits | depth rank).  Only then are the
-// screen-covering Gaussians binned per tile (the merge compares depth ranks).
-inline bool compact_words(int64_t n, int32_t tiles, int *tile_bits, int *rank_bits) {
-    int tb = 0, rb = 0;
-    while ((1 << tb) < tiles) tb++;
-    while ((int64_t(1) << rb) < n) rb++;
-    if (rb == 0) rb = 1;
-    *tile_bits = tb;
-    *rank_bits = rb;
-    return tb + rb <= 32;
-}
-
 // Exact cull of every candidate tile of a Gaussian's rectangle (ty-major, then tx, as
 // R/rasterizer.py:113-122 enumerates them).  Returns the kept count; bit c of `bits` is the
 // result for candidate c < 64 (the emit pass recomputes candidates >= 64).
