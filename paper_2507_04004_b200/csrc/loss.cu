@@ -134,32 +134,41 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     constexpr int HB = 6;
     constexpr int VS = 5, NVS = (GR + VS - 1) / VS;
     constexpr int AS = 4, NAS = TH / AS;
-    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, mirror-padded
+    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, mirror-padded: warp w
+    //    stages rows w, w + 8, ... (the TW + 20 = 52 columns in two lane passes), every load in
+    //    flight before the first store, no index division (columns >= TW + 20 are never read)
     {
-        constexpr int NEL = NIR * NIC, PER = (NEL + L_THREADS - 1) / L_THREADS;
-        float va[PER], vb[PER];
+        constexpr int NW = L_THREADS / 32, RPW = (NIR + NW - 1) / NW, CP = (TW + 20 + 31) / 32;
+        const int warp = tid >> 5, lane = tid & 31;
+        float va[RPW][CP], vb[RPW][CP];
 #pragma unroll
-        for (int q = 0; q < PER; q++) {  // all loads in flight before the stores
-            const int k = tid + q * L_THREADS;
-            const int iy = k / NIC, ix = k % NIC;
-            int y = y0 - 10 + iy, x = x0 - 10 + ix;
-            if (!INTERIOR) {
-                y = reflect_idx(y, H);
-                x = reflect_idx(x, W);
-            }
-            va[q] = vb[q] = 0.0f;
-            if (k < NEL && ix < TW + 20) {
-                const int64_t p = (int64_t)y * W + x;
-                va[q] = __ldg(color + 3 * p + c);
-                vb[q] = __ldg(target + 3 * p + c);
+        for (int j = 0; j < RPW; j++) {
+            const int iy = warp + NW * j;
+            int y = y0 - 10 + iy;
+            if (!INTERIOR) y = reflect_idx(min(y, y0 - 10 + NIR - 1), H);
+#pragma unroll
+            for (int h = 0; h < CP; h++) {
+                const int ix = lane + 32 * h;
+                int x = x0 - 10 + ix;
+                if (!INTERIOR) x = reflect_idx(x, W);
+                va[j][h] = vb[j][h] = 0.0f;
+                if (iy < NIR && ix < TW + 20) {
+                    const int64_t p = (int64_t)y * W + x;
+                    va[j][h] = __ldg(color + 3 * p + c);
+                    vb[j][h] = __ldg(target + 3 * p + c);
+                }
             }
         }
 #pragma unroll
-        for (int q = 0; q < PER; q++) {
-            const int k = tid + q * L_THREADS;
-            if (k < NEL) {
-                (&sm.in[0][0][0])[k] = va[q];
-                (&sm.in[1][0][0])[k] = vb[q];
+        for (int j = 0; j < RPW; j++) {
+            const int iy = warp + NW * j;
+#pragma unroll
+            for (int h = 0; h < CP; h++) {
+                const int ix = lane + 32 * h;
+                if (iy < NIR && ix < TW + 20) {
+                    sm.in[0][iy][ix] = va[j][h];
+                    sm.in[1][iy][ix] = vb[j][h];
+                }
             }
         }
     }
