@@ -375,15 +375,15 @@ __global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
 // (defined below)
 template <int NT>
-__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t nparts,
-                                              float lam, float xi, float *tab_stamp, int accumulate);
+__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t first,
+                                              int64_t nparts, float lam, float xi, float *tab_stamp, int accumulate);
 
 // depth_ratio_loss on the LiDAR K-list, then -- in the last block to finish, found by a ticket
 // (threadfence reduction) -- the mapping loss from all block partials: no separate finalize launch
 __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_view *__restrict__ view, float lam,
                                                          float xi, int64_t part0, float *tab_stamp, int accumulate) {
     pdl_wait();
-    __shared__ float red[8];
+    __shared__ double red[3][8];
     __shared__ int s_last;
     const int32_t K = view->lidar_k;
     const int32_t *idx = view->lidar_idx;
@@ -400,22 +400,43 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
         f.g_depth[p] = xi * (s / so);
         f.g_opac[p] = O >= 1e-6f ? xi * (-s * D / (so * so)) : 0.0f;
     }
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    // this block's share of the SSIM-kernel partials (part0 triples), one per thread: the last
+    // block then sums gridDim.x triples instead of part0 + gridDim.x (one memory round trip)
+    double l1 = 0.0, ss = 0.0;
+    const int64_t per = (part0 + gridDim.x - 1) / gridDim.x;
+    for (int64_t i = blockIdx.x * per + threadIdx.x; i < min(part0, (int64_t)(blockIdx.x + 1) * per); i += blockDim.x) {
+        l1 += f.loss_parts[3 * i];
+        ss += f.loss_parts[3 * i + 1];
+    }
+    double dsum = acc;
+    for (int o = 16; o > 0; o >>= 1) {
+        dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = l1;
+        red[1][threadIdx.x >> 5] = ss;
+        red[2][threadIdx.x >> 5] = dsum;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0.0;
-        for (int w = 0; w < 8; w++) s += red[w];
-        f.loss_parts[3 * (part0 + blockIdx.x) + 2] = s;
-        f.loss_parts[3 * (part0 + blockIdx.x)] = 0.0;
-        f.loss_parts[3 * (part0 + blockIdx.x) + 1] = 0.0;
+        double a = 0.0, b = 0.0, d = 0.0;
+        for (int w = 0; w < 8; w++) {
+            a += red[0][w];
+            b += red[1][w];
+            d += red[2][w];
+        }
+        f.loss_parts[3 * (part0 + blockIdx.x)] = a;
+        f.loss_parts[3 * (part0 + blockIdx.x) + 1] = b;
+        f.loss_parts[3 * (part0 + blockIdx.x) + 2] = d;
         __threadfence();
         s_last = atomicAdd(&f.counters[GS_CNT_LOSS_TICKET], 1) == (int)gridDim.x - 1;
     }
     __syncthreads();
     if (s_last) {
         __threadfence();
-        finalize_body<256>(f, view, part0 + gridDim.x, lam, xi, tab_stamp, accumulate);
+        finalize_body<256>(f, view, part0, gridDim.x, lam, xi, tab_stamp, accumulate);
         if (threadIdx.x == 0) f.counters[GS_CNT_LOSS_TICKET] = 0;
     }
 }
@@ -424,8 +445,9 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
 // mapping_loss from the block partials (R/losses.py:157-161), by NT threads: coalesced over the
 // flat (nparts x 3) array, then a fixed-order shuffle tree -- deterministic
 template <int NT>
-__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t nparts,
-                                              float lam, float xi, float *tab_stamp, int accumulate) {
+__device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *__restrict__ view, int64_t first,
+                                              int64_t nparts, float lam, float xi, float *tab_stamp, int accumulate) {
+    const double *parts = f.loss_parts + 3 * first;
     static_assert(NT % 3 == 1, "component bookkeeping: thread t keeps component (t + j) % 3 in acc[j]");
     __shared__ double r[3][NT / 32];
     const int64_t total = 3 * nparts;
@@ -434,9 +456,9 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
     const int comp0 = threadIdx.x % 3;
 #pragma unroll 4
     for (int64_t e = threadIdx.x; e < total; e += stride) {
-        acc[0] += f.loss_parts[e];
-        if (e + NT < total) acc[1] += f.loss_parts[e + NT];
-        if (e + 2 * NT < total) acc[2] += f.loss_parts[e + 2 * NT];
+        acc[0] += parts[e];
+        if (e + NT < total) acc[1] += parts[e + NT];
+        if (e + 2 * NT < total) acc[2] += parts[e + 2 * NT];
     }
     double comp[3];
 #pragma unroll
