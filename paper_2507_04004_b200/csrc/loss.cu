@@ -5,7 +5,7 @@
 // dependent 11-tap correlations: blur(x)(q) = sum_d F[q][d] x(q+d) with
 // F[q][d] = sum_t K(t) [refl(q+t) == q+d], and adjoint(g)(p) = sum_d F[p+d][-d] g(p+d); the
 // per-axis tables absorb every reflection, so interior and border pixels share one code path.
-// One CTA computes a 32x16 output tile of one channel: halo-10 inputs -> 5 blurred moments
+// One CTA computes a 32x16 output tile of one channel: halo-10 inputs -> 4 blurred moments (a, b, aa + bb, ab)
 // (halo 5) -> SSIM map + partials -> two adjoint passes -> gradient, all in shared memory (one
 // HBM read of rendered+target, one write of the gradient).
 //
@@ -17,7 +17,7 @@ namespace gs {
 // One CTA per (32 x 16 output tile, colour channel).  Every pass is register-blocked along its
 // blur axis (a thread produces a strip of outputs from one sliding window of shared-memory
 // reads); row strides are odd so that a warp reading one column per lane (or one row per lane)
-// hits 32 distinct banks.  46 KB of shared memory and <= 64 registers give 4 CTAs (32 warps)
+// hits 32 distinct banks.  40 KB of shared memory and <= 64 registers give 4 CTAs (32 warps)
 // per SM: the passes are separated by barriers, so it is the other CTAs that keep the SM busy.
 constexpr int TW = 32, TH = 16;
 constexpr int NIR = TH + 20;          // input rows (halo 10)
@@ -105,10 +105,10 @@ __device__ __forceinline__ void split32(int it, int groups, int len, int &group,
 // weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
 struct SsimSmem {
     float in[2][NIR][NIC];  // rendered / target channel; later the SSIM partials g[3][GR][GC]
-    float hx[5][NIR][HXS];  // horizontal moments; later the vertical adjoint ry[3][TH][GC]
+    float hx[4][NIR][HXS];  // horizontal moments; later the vertical adjoint ry[3][TH][GC]
     float red[2][L_THREADS / 32];
 };
-static_assert(3 * GR * GC <= 2 * NIR * NIC && 3 * TH * GC <= 5 * NIR * HXS, "smem aliasing");
+static_assert(3 * GR * GC <= 2 * NIR * NIC && 3 * TH * GC <= 4 * NIR * HXS, "smem aliasing");
 
 template <bool INTERIOR>
 __device__ __forceinline__ float wtab(const float *__restrict__ tab, int pos, int d) {
@@ -173,20 +173,22 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
         }
     }
     __syncthreads();
-    // 2) horizontal blur of the 5 moments (a, b, aa, bb, ab); hx column j <-> x = x0-5+j
+    // 2) horizontal blur of the 4 moments (a, b, aa + bb, ab) -- SSIM uses the variances only as
+    //    the sum va + vb (R/losses.py:100-104), so blur(aa) + blur(bb) is one blur; hx column j
+    //    <-> x = x0-5+j
     for (int it = tid; it < NIR * (HXC / HB); it += L_THREADS) {
         // warp-aligned items: rows 0..31 of a strip per warp, then the last NIR - 32 rows of every
         // strip (odd row stride: a warp's 32 rows hit 32 banks)
         int iy, c0;
         split32(it, HXC / HB, NIR, c0, iy);
         c0 *= HB;
-        float m[5][HB];
+        float m[4][HB];
 #pragma unroll
-        for (int k = 0; k < HB; k++) m[0][k] = m[1][k] = m[2][k] = m[3][k] = m[4][k] = 0.0f;
+        for (int k = 0; k < HB; k++) m[0][k] = m[1][k] = m[2][k] = m[3][k] = 0.0f;
 #pragma unroll
         for (int t = 0; t < HB + 10; t++) {
             const float at = sm.in[0][iy][c0 + t], bt = sm.in[1][iy][c0 + t];
-            const float aa = at * at, bb = bt * bt, ab = at * bt;
+            const float ss = fmaf(at, at, bt * bt), ab = at * bt;
 #pragma unroll
             for (int k = 0; k < HB; k++) {
                 const int d = t - k;
@@ -194,14 +196,13 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                     const float w = kw(d);
                     m[0][k] += w * at;
                     m[1][k] += w * bt;
-                    m[2][k] += w * aa;
-                    m[3][k] += w * bb;
-                    m[4][k] += w * ab;
+                    m[2][k] += w * ss;
+                    m[3][k] += w * ab;
                 }
             }
         }
 #pragma unroll
-        for (int q = 0; q < 5; q++)
+        for (int q = 0; q < 4; q++)
 #pragma unroll
             for (int k = 0; k < HB; k++) sm.hx[q][iy][c0 + k] = m[q][k];
     }
@@ -213,22 +214,22 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
         split32(it, NVS, GW, gy0, gx);
         gy0 *= VS;
         const int x = x0 - 5 + gx;
-        float u[5][VS];
+        float u[4][VS];
 #pragma unroll
-        for (int k = 0; k < VS; k++) u[0][k] = u[1][k] = u[2][k] = u[3][k] = u[4][k] = 0.0f;
+        for (int k = 0; k < VS; k++) u[0][k] = u[1][k] = u[2][k] = u[3][k] = 0.0f;
 #pragma unroll
         for (int r = 0; r < VS + 10; r++) {
             if (gy0 + r < NIR) {
-                float h[5];
+                float h[4];
 #pragma unroll
-                for (int q = 0; q < 5; q++) h[q] = sm.hx[q][gy0 + r][gx];
+                for (int q = 0; q < 4; q++) h[q] = sm.hx[q][gy0 + r][gx];
 #pragma unroll
                 for (int k = 0; k < VS; k++) {
                     const int d = r - k;
                     if (d >= 0 && d < 11) {
                         const float w = kw(d);
 #pragma unroll
-                        for (int q = 0; q < 5; q++) u[q][k] += w * h[q];
+                        for (int q = 0; q < 4; q++) u[q][k] += w * h[q];
                     }
                 }
             }
@@ -240,9 +241,10 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                 float g0 = 0.f, g1 = 0.f, g2 = 0.f;
                 if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
                     const float ua = u[0][k], ub = u[1][k];
-                    const float va = u[2][k] - ua * ua, vb = u[3][k] - ub * ub, vab = u[4][k] - ua * ub;
+                    const float vab = u[3][k] - ua * ub;
                     const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
-                    const float b1 = ua * ua + ub * ub + C1, b2 = va + vb + C2;
+                    const float uu = ua * ua + ub * ub;
+                    const float b1 = uu + C1, b2 = (u[2][k] - uu) + C2;  // va + vb + C2
                     // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
                     const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
                     const float S = (a1 * a2) * rden;
