@@ -11,6 +11,7 @@ namespace gs {
 
 constexpr int PP_WARPS = 4;
 constexpr int PP_THREADS = PP_WARPS * 32;
+constexpr int PP_CTAS_PER_SM = 5;  // persistent grid: shared memory allows five
 
 __device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -19,7 +20,7 @@ __device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
 __device__ __forceinline__ void pp_cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void pp_cp_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
-// Per warp, batches of 32 Gaussians flow through a three-stage software pipeline:
+// Per warp, batches of 32 Gaussians flow through a software pipeline (two geometry slots):
 //   A  the geometry chunks (floats 0-15 of each row: pos, log_scale, quat, opacity logit,
 //      sh_low, sh_high[0]) of batch b+1 stream in (cp.async) while batch b is projected,
 //      its radius / rectangle computed and its small footprints culled;
@@ -36,8 +37,8 @@ struct PPGeom {  // chunk c of row r at c ^ ((r >> 1) & 3): 8 consecutive rows h
 struct PPSh {  // 11 chunks per row, 176-B row stride (conflict-free without a swizzle)
     float4 row[32][11];
 };
-struct PPWarp {
-    PPGeom geom[3];
+struct PPWarp {  // 9.6 KB: five 4-warp CTAs per SM
+    PPGeom geom[2];
     PPSh sh;
 };
 
@@ -46,8 +47,8 @@ __device__ __forceinline__ void pp_cp_wait_0() { asm volatile("cp.async.wait_gro
 
 // colour of one Gaussian (R/rasterizer.py:447-452, eval_sh R/gaussians.py:102-111) from its
 // geometry chunks and its staged sh_high chunks
-__device__ __forceinline__ float3 pp_colour(const PPGeom &g, const PPSh &sh, int r, const gs_camera &cam) {
-    const float4 c0 = pp_geom(g, r, 0), c2 = pp_geom(g, r, 2), c3 = pp_geom(g, r, 3);
+__device__ __forceinline__ float3 pp_colour(const float4 &c0, const float4 &c2, const float4 &c3, const PPSh &sh, int r,
+                                            const gs_camera &cam) {
     const float u0 = c0.x - cam.center[0], u1 = c0.y - cam.center[1], u2 = c0.z - cam.center[2];
     float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
     if (un < 1e-12f) un = 1.0f;
@@ -133,7 +134,7 @@ __device__ __forceinline__ uint32_t warp_cull_small(bool flag, float mx, float m
 
 // Persistent warps over batches of 32 Gaussians (pipeline above).
 template <bool LAZY_SH>
-__global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, const float *__restrict__ params,
+__global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(gs_frame f, const float *__restrict__ params,
                                                                 const gs_view *__restrict__ view) {
     pdl_wait();
     extern __shared__ float4 pp_raw[];
@@ -167,10 +168,12 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
     pp_cp_commit();  // (empty) SH group of the batch before the first
     bool prev_need = false;
     int64_t prev_i = -1;
+    // the previous batch's colour inputs (position, logit, sh_low, sh_high[0]) stay in registers,
+    // so its geometry slot can take the next batch: two slots instead of three
+    float4 pc0 = make_float4(0.f, 0.f, 0.f, 0.f), pc2 = pc0, pc3 = pc0;
     int slot = 0;
-    for (; batch < nbatch; batch += stride, slot = slot == 2 ? 0 : slot + 1) {
-        const int next_slot = slot == 2 ? 0 : slot + 1, prev_slot = slot == 0 ? 2 : slot - 1;
-        if (batch + stride < nbatch) issue_geom(batch + stride, W.geom[next_slot]);
+    for (; batch < nbatch; batch += stride, slot ^= 1) {
+        if (batch + stride < nbatch) issue_geom(batch + stride, W.geom[slot ^ 1]);
         else pp_cp_commit();
         pp_cp_wait_1();  // this batch's geometry and the previous batch's SH chunks have landed
         __syncwarp();
@@ -265,12 +268,16 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
         warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
         // colour of the previous batch (its SH chunks landed with this batch's geometry)
         if (prev_need) {
-            const float3 col = pp_colour(W.geom[prev_slot], W.sh, lane, cam);
-            const float lg = pp_geom(W.geom[prev_slot], lane, 2).z;
+            const float3 col = pp_colour(pc0, pc2, pc3, W.sh, lane, cam);
             reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] =
-                make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(lg)));
+                make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(pc2.z)));
         }
-        __syncwarp();  // the SH buffer and the previous geometry slot are free again
+        if (need) {
+            pc0 = pp_geom(G, lane, 0);
+            pc2 = pp_geom(G, lane, 2);
+            pc3 = pp_geom(G, lane, 3);
+        }
+        __syncwarp();  // the SH buffer and this geometry slot are free again
         if (need) {
             const float *src = params + i * GS_ROW + 16;
 #pragma unroll
@@ -282,10 +289,8 @@ __global__ void __launch_bounds__(PP_THREADS) preprocess_kernel(gs_frame f, cons
     }
     if (prev_need) {  // drain: the last batch's colour
         pp_cp_wait_0();
-        const int last = slot == 0 ? 2 : slot - 1;
-        const float3 col = pp_colour(W.geom[last], W.sh, lane, cam);
-        const float lg = pp_geom(W.geom[last], lane, 2).z;
-        reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] = make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(lg)));
+        const float3 col = pp_colour(pc0, pc2, pc3, W.sh, lane, cam);
+        reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] = make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(pc2.z)));
     }
 }
 
@@ -888,10 +893,10 @@ extern "C" int gs_preprocess_ex(const gs_frame *f, const float *params, const gs
     cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
     if (f->n == 0) return GS_OK;
     if (flags & GS_PP_LAZY_SH)
-        launch_pdl(preprocess_kernel<true>, 4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
+        launch_pdl(preprocess_kernel<true>, PP_CTAS_PER_SM * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
                                                                                                          view);
     else
-        launch_pdl(preprocess_kernel<false>, 4 * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
+        launch_pdl(preprocess_kernel<false>, PP_CTAS_PER_SM * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
                                                                                                           view);
     int rc = check_launch("preprocess_kernel");
     if (rc) return rc;
@@ -953,5 +958,7 @@ void init_preprocess_attrs() {
                          (int)(PP_WARPS * sizeof(PPWarp)));
     cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(PP_WARPS * sizeof(PPWarp)));
+    cudaFuncSetAttribute(preprocess_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 }  // namespace gs
