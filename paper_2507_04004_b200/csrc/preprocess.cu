@@ -656,23 +656,38 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
     const int64_t nb = f.counters[GS_CNT_BIG];
     for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = b0 + threadIdx.x;  // uniform trip count: warp_append is warp-wide
-        int g = -1;
+        int g = -1, kept = 0, slot = -1;
         bool t = false;
         if (b < nb) {
             g = f.big_list[b];
-            const int kept = f.kept[g], slot = f.big_slot[b];
+            kept = f.kept[g];
+            slot = f.big_slot[b];
             t = kept > 0;
-            if (slot >= 0 && t) {  // kept < 0 encodes the huge slot
-                f.kept[g] = -(1 + slot);
-                atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
-                // stage the depth key for the binning's huge sort (binning.cu, HKEYS)
-                const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
+        }
+        // kept screen-covering Gaussians: entry count and a staging slot for the binning's huge
+        // sort (binning.cu, HKEYS; the sort is by key, so the staging order is free), reserved
+        // with one atomic per warp and counter
+        const bool hk = slot >= 0 && t;
+        const unsigned hm = __ballot_sync(0xffffffffu, hk);
+        if (hm) {
+            int e = hk ? kept : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            const int lane = threadIdx.x & 31;
+            int h0 = 0;
+            if (lane == 0) {
+                atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
+                h0 = atomicAdd(&f.counters[GS_CNT_HUGE_N], __popc(hm));
+            }
+            const int h = __shfl_sync(0xffffffffu, h0, 0) + __popc(hm & ((1u << lane) - 1u));
+            if (hk) {
+                f.kept[g] = -(1 + slot);  // kept < 0 encodes the huge slot
                 if (h < GS_HUGE_CAP)
                     reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] =
                         ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
             }
-            f.touched[g] = t;
         }
+        if (b < nb) f.touched[g] = t;
         // per-tile bucket counts of the binning (bitmap, or the exact re-test on bitmap overflow):
         // the warp walks the candidates of each of its non-huge kept Gaussians together
         const bool cnt = b < nb && t && f.big_slot[b] < 0;
