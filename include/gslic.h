@@ -194,6 +194,10 @@ int gs_loss(const gs_frame *f, const gs_view *view, float lam, float xi, void *s
  * the total to loss[4] (a running sum the caller resets). gs_loss(...) = gs_loss_ex(..., 0). */
 #define GS_LOSS_TABLES_READY 1
 #define GS_LOSS_ACCUMULATE 2
+/* GS_LOSS_DEPTH_GRADS_ZERO -- g_depth / g_opac are zero on entry (fresh workspace, or the previous
+ * gs_render_bwd_ex ran with GS_BWD_CLEAR_DEPTH_GRADS): only the LiDAR pixels are written, and the
+ * depth term runs alongside the photometric kernel's tail. */
+#define GS_LOSS_DEPTH_GRADS_ZERO 4
 int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int32_t flags, void *stream);
 
 /* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
@@ -201,6 +205,9 @@ int gs_render_bwd(const gs_frame *f, void *stream);
 /* flags = GS_BWD_ROWS_ZERO: the caller guarantees the touched Gaussians' g2d rows are zero (the
  * engine: the chain rule clears every row it consumes), so they are not cleared first. */
 #define GS_BWD_ROWS_ZERO 1
+/* GS_BWD_CLEAR_DEPTH_GRADS: the backward resets g_depth / g_opac to zero after reading them (the
+ * protocol of GS_LOSS_DEPTH_GRADS_ZERO) */
+#define GS_BWD_CLEAR_DEPTH_GRADS 2
 int gs_render_bwd_ex(const gs_frame *f, int32_t flags, void *stream);
 
 /* R/rasterizer.py:559-644 + :707-725 fused.  lr_cols: device (GS_ROW) per-column rates.

@@ -22,8 +22,8 @@ CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3
 GS_CNT_SLOTS = 16
 GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists materialised on demand)
 GS_PP_LAZY_SH = 1  # gs_preprocess_ex flag of the iteration engine (colours only where blended)
-GS_LOSS_TABLES_READY, GS_LOSS_ACCUMULATE = 1, 2  # gs_loss_ex flags
-GS_BWD_ROWS_ZERO = 1  # gs_render_bwd_ex flag
+GS_LOSS_TABLES_READY, GS_LOSS_ACCUMULATE, GS_LOSS_DEPTH_GRADS_ZERO = 1, 2, 4  # gs_loss_ex flags
+GS_BWD_ROWS_ZERO, GS_BWD_CLEAR_DEPTH_GRADS = 1, 2  # gs_render_bwd_ex flags
 
 P = ctypes.c_void_p
 i32 = ctypes.c_int32

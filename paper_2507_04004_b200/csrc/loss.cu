@@ -118,7 +118,7 @@ __device__ __forceinline__ float wtab(const float *__restrict__ tab, int pos, in
 template <bool INTERIOR>
 __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
                                           const float *__restrict__ tab_x, const float *__restrict__ tab_y,
-                                          float lam) {
+                                          float lam, int depth_grads_zero) {
     float(*g)[GR][GC] = reinterpret_cast<float(*)[GR][GC]>(&sm.in[0][0][0]);
     float(*ry)[TH][GC] = reinterpret_cast<float(*)[TH][GC]>(&sm.hx[0][0][0]);
     const float *__restrict__ target = view->target;
@@ -329,8 +329,9 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                 const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
                 f.g_color[3 * p + c] =
                     (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A[0][k] + 2.0f * a * A[1][k] + b * A[2][k]));
-                // the depth/opacity gradient images start at zero (the LiDAR kernel follows)
-                if (c == 0) {
+                // the depth/opacity gradient images start at zero (the LiDAR kernel follows; under
+                // GS_LOSS_DEPTH_GRADS_ZERO they already are, and the LiDAR kernel runs alongside)
+                if (c == 0 && !depth_grads_zero) {
                     f.g_depth[p] = 0.0f;
                     f.g_opac[p] = 0.0f;
                 }
@@ -364,14 +365,19 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
 // the compile-time-weight path, border tiles the reflection-table path
 __global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
                                                                const float *__restrict__ tab_x,
-                                                               const float *__restrict__ tab_y, float lam) {
+                                                               const float *__restrict__ tab_y, float lam,
+                                                               int depth_grads_zero) {
     pdl_wait();
+    // let the LiDAR kernel launch into the SMs this grid's last wave leaves idle (it waits for
+    // this grid's completion itself before it reads the partials, or before anything when the
+    // g_depth / g_opac clearing below is on)
+    asm volatile("griddepcontrol.launch_dependents;");
     __shared__ SsimSmem sm;
     const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
     if (x0 >= 10 && x0 + TW + 10 <= f.width && y0 >= 10 && y0 + TH + 10 <= f.height)
-        ssim_tile<true>(sm, f, view, tab_x, tab_y, lam);
+        ssim_tile<true>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
     else
-        ssim_tile<false>(sm, f, view, tab_x, tab_y, lam);
+        ssim_tile<false>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
 }
 
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
@@ -383,8 +389,11 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
 // depth_ratio_loss on the LiDAR K-list, then -- in the last block to finish, found by a ticket
 // (threadfence reduction) -- the mapping loss from all block partials: no separate finalize launch
 __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_view *__restrict__ view, float lam,
-                                                         float xi, int64_t part0, float *tab_stamp, int accumulate) {
-    pdl_wait();
+                                                         float xi, int64_t part0, float *tab_stamp, int accumulate,
+                                                         int overlap) {
+    // overlap (GS_LOSS_DEPTH_GRADS_ZERO): the depth term reads only the forward's images, which
+    // were complete before the SSIM grid started; it waits for that grid before the partials
+    if (!overlap) pdl_wait();
     __shared__ double red[3][8];
     __shared__ int s_last;
     const int32_t K = view->lidar_k;
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
         f.g_depth[p] = xi * (s / so);
         f.g_opac[p] = O >= 1e-6f ? xi * (-s * D / (so * so)) : 0.0f;
     }
+    if (overlap) pdl_wait();
     // this block's share of the SSIM-kernel partials (part0 triples), one per thread: the last
     // block then sums gridDim.x triples instead of part0 + gridDim.x (one memory round trip)
     double l1 = 0.0, ss = 0.0;
@@ -513,7 +523,7 @@ extern "C" int gs_loss(const gs_frame *f, const gs_view *view, float lam, float 
 
 extern "C" int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int32_t flags, void *stream) {
     using namespace gs;
-    if (flags & ~(GS_LOSS_TABLES_READY | GS_LOSS_ACCUMULATE)) {
+    if (flags & ~(GS_LOSS_TABLES_READY | GS_LOSS_ACCUMULATE | GS_LOSS_DEPTH_GRADS_ZERO)) {
         set_error("gs_loss_ex: unknown flags");
         return GS_ERR_ARG;
     }
@@ -536,10 +546,11 @@ extern "C" int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, flo
         if ((rc = check_launch("loss_tables_kernel"))) return rc;
     }
     dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
-    launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam);
+    const int dz = (flags & GS_LOSS_DEPTH_GRADS_ZERO) ? 1 : 0;
+    launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam, dz);
     if ((rc = check_launch("ssim_l1_kernel"))) return rc;
     launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, lam, xi, ssim_blocks, tab_y + 22 * f->height,
-               (flags & GS_LOSS_ACCUMULATE) ? 1 : 0);
+               (flags & GS_LOSS_ACCUMULATE) ? 1 : 0, dz);
     return check_launch("depth_loss_kernel");
 }
 

@@ -341,7 +341,7 @@ __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const flo
 constexpr int BPX = 2;              // pixels per backward thread (one column, rows 16 / BPX apart; 4 measured no faster)
 constexpr int BT = RT / BPX;        // backward threads per tile
 
-__global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
+__global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_depth_grads) {
     pdl_wait();
     __shared__ float4 s_a[RT];
     __shared__ float4 s_b[RT];
@@ -352,6 +352,17 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
     const int tile = blockIdx.x;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
+    if (clear_depth_grads && stop == start) {  // (GS_BWD_CLEAR_DEPTH_GRADS) an empty tile's pixels
+#pragma unroll
+        for (int k = 0; k < BPX; k++) {
+            const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / BPX) * k;
+            if (x < f.width && y < f.height) {
+                const int64_t q = (int64_t)y * f.width + x;
+                if (f.g_depth[q] != 0.0f) f.g_depth[q] = 0.0f;
+                if (f.g_opac[q] != 0.0f) f.g_opac[q] = 0.0f;
+            }
+        }
+    }
     if (stop == start) return;
     const unsigned lane = threadIdx.x & 31u;
     const int fld = reduce10_field(lane);
@@ -394,6 +405,10 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f) {
             p.gc2 = f.g_color[3 * q + 2];
             p.gd = f.g_depth[q];
             p.go = f.g_opac[q];
+            if (clear_depth_grads) {  // nonzero only at the view's LiDAR pixels
+                if (p.gd != 0.0f) f.g_depth[q] = 0.0f;
+                if (p.go != 0.0f) f.g_opac[q] = 0.0f;
+            }
         }
     }
 #pragma unroll
@@ -478,7 +493,7 @@ extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream
 extern "C" int gs_render_bwd(const gs_frame *f, void *stream) { return gs_render_bwd_ex(f, 0, stream); }
 
 extern "C" int gs_render_bwd_ex(const gs_frame *f, int32_t flags, void *stream) {
-    if (flags & ~GS_BWD_ROWS_ZERO) {
+    if (flags & ~(GS_BWD_ROWS_ZERO | GS_BWD_CLEAR_DEPTH_GRADS)) {
         set_error("gs_render_bwd_ex: unknown flags");
         return GS_ERR_ARG;
     }
@@ -490,7 +505,7 @@ extern "C" int gs_render_bwd_ex(const gs_frame *f, int32_t flags, void *stream) 
         int rc = check_launch("zero_g2d_kernel");
         if (rc) return rc;
     }
-    launch_pdl(render_bwd_kernel, T, BT, 0, (cudaStream_t)stream, *f);
+    launch_pdl(render_bwd_kernel, T, BT, 0, (cudaStream_t)stream, *f, (flags & GS_BWD_CLEAR_DEPTH_GRADS) ? 1 : 0);
     return check_launch("render_bwd_kernel");
 }
 

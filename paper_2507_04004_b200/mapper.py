@@ -19,7 +19,8 @@ from . import _lib
 from ._lib import call
 from .errors import DataError
 from .gaussians import GaussianMap, as_device_map, default_device, init_from_points, stream_ptr, struct_to_device
-from .rasterizer import (AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from, default_lrs, forward,
+from .rasterizer import (BWD_FLAGS, LOSS_FLAGS, AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from,
+                         default_lrs, forward, prime_workspace,
                          lr_columns)
 
 NEAR_CLIP = 0.01
@@ -220,9 +221,11 @@ class MapOptimizer:
 
     def _workspace(self, capacity: int) -> Workspace:
         """A zero-filled workspace whose loss reflection tables are built (one gs_loss on the
-        blank images), so the captured iteration can skip that launch (GS_LOSS_TABLES_READY)."""
+        blank images), so the captured iteration can skip that launch (GS_LOSS_TABLES_READY);
+        a backward over its empty tiles then clears the depth / opacity gradient images that
+        gs_loss wrote, the state the iteration keeps (GS_LOSS_DEPTH_GRADS_ZERO)."""
         ws = Workspace(len(self.g), self.W, self.H, capacity, self.dev)
-        call("gs_loss", ws.fptr, self.views[0].ptr, self.lam, self.xi, stream_ptr())
+        prime_workspace(ws, self.views[0].ptr, self.lam, self.xi)
         return ws
 
     # -- one iteration: R/mapper.py:249-256 --------------------------------------------
@@ -232,8 +235,8 @@ class MapOptimizer:
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_ACCUMULATE, s)
-        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the fused chain clears the rows it consumes
+        call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
+        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # the fused chain clears the rows it consumes
         self._chain_adam(cur)
 
     def _chain_adam(self, view_ptr: int | None = None) -> None:
@@ -328,9 +331,9 @@ class MapOptimizer:
         ev[2].record()
         call("gs_render_fwd", f, 1, s)
         ev[3].record()
-        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_ACCUMULATE, s)
+        call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
         ev[4].record()
-        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)
+        call("gs_render_bwd_ex", f, BWD_FLAGS, s)
         ev[5].record()
         self._chain_adam()
         ev[6].record()

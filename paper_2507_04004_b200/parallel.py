@@ -22,7 +22,8 @@ from . import _lib
 from ._lib import GS_ROW, call
 from .errors import DataError
 from .gaussians import as_device_map, stream_ptr
-from .rasterizer import AdamState, DeviceView, Workspace, _bin_frame, camera_from, lr_columns
+from .rasterizer import (BWD_FLAGS, LOSS_FLAGS, AdamState, DeviceView, Workspace, _bin_frame, camera_from, lr_columns,
+                         prime_workspace)
 
 TOUCH_COL = GS_ROW - 1  # padding column carrying the touched flag through the allreduce
 
@@ -75,7 +76,7 @@ class BatchMapOptimizer:
             _, cnt = _bin_frame(self.g, v, True)
             emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
         self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
-        call("gs_loss", self.ws.fptr, self.views[0].ptr, self.lam, self.xi, stream_ptr())  # reflection tables
+        prime_workspace(self.ws, self.views[0].ptr, self.lam, self.xi)  # reflection tables, cleared images
         n = len(self.g)
         self.grads = torch.zeros((n, GS_ROW), dtype=torch.float32, device=self.dev)
         self.sparse_allreduce = True  # two-phase allreduce of the touched rows only
@@ -98,8 +99,8 @@ class BatchMapOptimizer:
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss_ex", f, cur, self.lam, self.xi, _lib.GS_LOSS_TABLES_READY, s)
-        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # gs_chain clears the rows it consumes
+        call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS, s)
+        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_chain clears the rows it consumes
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
         self.loss_acc += self.ws.loss[0:1]
 

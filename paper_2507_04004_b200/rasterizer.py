@@ -186,6 +186,20 @@ def _remember_capacity(n, w, h, cull, entries):
         _CAP_HINT[(n, w, h, cull)] = max(int(entries * 1.25) + 1024, 1 << 16)
 
 
+# Flags of the iteration engines (MapOptimizer, BatchMapOptimizer): the loss reflection tables
+# are built once per workspace, and the depth / opacity gradient images stay zero between
+# iterations -- the loss writes only the LiDAR pixels and the backward clears them.
+LOSS_FLAGS = _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO
+BWD_FLAGS = _lib.GS_BWD_ROWS_ZERO | _lib.GS_BWD_CLEAR_DEPTH_GRADS
+
+
+def prime_workspace(ws: Workspace, view_ptr: int, lam: float, xi: float) -> None:
+    """Bring a fresh (zero-filled) workspace into the engines' state: one gs_loss builds the
+    reflection tables, a backward over its still-empty tiles clears the gradient images."""
+    call("gs_loss", ws.fptr, view_ptr, float(lam), float(xi), stream_ptr())
+    call("gs_render_bwd_ex", ws.fptr, BWD_FLAGS, stream_ptr())
+
+
 def _bin_frame(g: GaussianMap, view: DeviceView, cull: bool, ws: Workspace | None = None):
     """preprocess + bin with an exact-capacity retry (one host sync: E is data dependent)."""
     cam = view.cam

@@ -286,6 +286,9 @@ def test_mapping_iterations_match_oracle():
         gl = eng.loss_sum()
         ol = O.map_iteration(og, ocams[k], sc.targets[k], sc.sparse_depths[k], ost, lrs)
         assert abs(gl - ol) < REL_TOL * abs(ol), (it, gl, ol)
+        # the engine keeps the depth / opacity gradient images zero between iterations (the
+        # backward clears the LiDAR pixels the loss wrote: GS_BWD_CLEAR_DEPTH_GRADS)
+        assert not bool(eng.ws.g_depth.any()) and not bool(eng.ws.g_opac.any()), it
     delta_gpu = _np(g.rows())[:, :59] - sc.rows
     delta_ref = og.rows() - sc.rows
     assert normwise(delta_gpu, delta_ref) < 0.05
