@@ -65,7 +65,9 @@ class PoseRefiner:
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), v, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
-        call("gs_loss_ex", f, v, 0.5, 0.0, _lib.GS_LOSS_TABLES_READY, s)  # R/odometry.py:323: photometric_loss(lam=0.5)
+        # R/odometry.py:323: photometric_loss(lam=0.5).  No LiDAR term (lidar_k = 0): the depth /
+        # opacity gradient images stay as the table-building gs_loss left them, zero
+        call("gs_loss_ex", f, v, 0.5, 0.0, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO, s)
         call("gs_track_grad", f, self.mask.data_ptr(), self.opac_gate, s)
         call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the pose chain clears the rows it consumes
         call("gs_chain_pose", f, self.g.data.data_ptr(), None, None, v, self.pose_grad.data_ptr(), s)
