@@ -143,9 +143,10 @@ def algorithmic_bytes(eng, scene_cam) -> dict:
     import torch
     ws = eng.ws
     n = len(eng.g)
-    cnt = ws.counters[:8].cpu().numpy()
+    cnt = ws.counters[:20].cpu().numpy()
     n_t = int(cnt[2])
     E = int(cnt[1])
+    huge_n = min(int(cnt[19]), 4096)  # GS_CNT_HUGE_N (capped at GS_HUGE_CAP)
     P = eng.W * eng.H
     nc = ws.n_contrib
     tx, ty = ws.tiles_x, ws.tiles_y
@@ -173,7 +174,11 @@ def algorithmic_bytes(eng, scene_cam) -> dict:
         # screen-space gradients read (80 B) and zeroed (96 B), the step counter
         "chain_adam": n_t * (3 * 240 + 80 + 4 + 3 * 240 + 96 + 4),
         "loss": 36 * P + 8 * P,
-        "bin": 24 * E * 2 + 12 * E + 8 * E + 4 * E + 16 * valid * 4,
+        # lazy binning (the engine): per-tile counts read, offsets / flags written (20 B per
+        # tile), the screen-covering Gaussians' depth keys sorted (16 B each) and their per-tile
+        # bitmaps transposed (read + write).  The small Gaussians' entries are not materialised
+        # here: the forward fills the buckets of the tiles that outlive the screen-covering run.
+        "bin": 20 * tx * ty + 16 * huge_n + 2 * huge_n * ((tx * ty + 31) // 32) * 4,
         "_stats": {"n": n, "n_valid": valid, "n_touched": n_t, "entries": E, "blend_entries": proc, "pixels": P},
     }
 
