@@ -29,6 +29,10 @@ import time
 
 import numpy as np
 
+# NCCL's debug output (including its version banner, which some environments enable through
+# NCCL_DEBUG) goes to stderr: stdout carries exactly one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
