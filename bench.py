@@ -29,9 +29,6 @@ import time
 
 import numpy as np
 
-# NCCL's debug output (including its version banner, which some environments enable through
-# NCCL_DEBUG) goes to stderr: stdout carries exactly one JSON line
-os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -573,12 +570,18 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=150.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    # stdout carries exactly one JSON line: everything else the process (or a library -- NCCL
+    # prints its version banner to stdout on communicator set-up) writes to fd 1 goes to stderr
+    sys.stdout.flush()
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     if args.impl == "reference":
         out = run_reference(args)
     else:
         out = run_ours(args)
     if out is not None and int(os.environ.get("RANK", 0)) == 0:
-        print(json.dumps(out), flush=True)
+        json_out.write(json.dumps(out) + "\n")
+        json_out.flush()
     if (int(os.environ.get("WORLD_SIZE", 1)) > 1 or args.batch) and args.impl == "ours":
         import torch.distributed as dist
         if dist.is_initialized():
