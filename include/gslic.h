@@ -45,7 +45,13 @@ extern "C" {
 #define GS_NPARAM 59
 #define GS_TILE 16
 #define GS_SMALL_CAND 16 /* candidate tiles culled per thread; larger footprints go warp-wide */
-#define GS_G2D 12      /* floats per screen-space gradient row: mean2d 2, conic 3, opacity 1, color 3, depth 1, pad 2 */
+#define GS_G2D 20      /* int64 words per screen-space gradient row: 10 fields (mean2d 2, conic 3, opacity 1,
+                          color 3, depth 1), each a fixed-point pair (hi, lo), value = hi 2^-24 + lo 2^-64
+                          (integer atomics: sums are bit-identical run to run) */
+#define GS_G2D_FIELDS 10
+#define GS_SPLAT 16    /* floats per 2D splat record: (mx, my, a, beta) (gamma, opacity, depth, qcut)
+                          (r, g, b, 1 - opacity) (b, c, 0, 0); conic = (a, b, c), and the blend evaluates
+                          q = a (dx + beta dy)^2 + gamma dy^2 with beta = b / a, gamma = (a c - b^2) / a */
 
 enum {
     GS_OK = 0,
@@ -106,13 +112,13 @@ typedef struct gs_frame {
     int64_t entry_capacity;  /* max kept (splat, tile) pairs */
     int32_t width, height, tiles_x, tiles_y;
     /* per Gaussian */
-    float *splat2d;          /* n x 12: mx my ca cb | cc opacity depth qcut | r g b 1-opacity */
+    float *splat2d;          /* n x GS_SPLAT records (see GS_SPLAT) */
     float *cov2d;            /* n x 4: c00 c01 c11 radius */
     int32_t *rect;           /* n x 4: tx0 tx1 ty0 ty1 (empty: tx1 < tx0) */
     uint8_t *valid;          /* n: near-plane & det test (R/gaussians.py:190-208) */
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
-    double *g2d;             /* n x GS_G2D screen-space gradients, FP64 accumulators (touched rows) */
+    int64_t *g2d;            /* n x GS_G2D screen-space gradients, fixed-point accumulators (touched rows) */
     float *grad_rows;        /* n x GS_ROW parameter gradients in touched-list order */
     float *bias_corr;        /* n x 2 reciprocal Adam bias corrections 1/(1-b1^t), 1/(1-b2^t) (touched-list order) */
     uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
@@ -149,6 +155,7 @@ typedef struct gs_frame {
     double *loss_parts;      /* per-block partial sums */
     double *loss;            /* 8: total, photometric, depth, dssim, running sum (GS_LOSS_ACCUMULATE) */
     int64_t loss_blocks;
+    int64_t *pose_acc;       /* 12: fixed-point accumulators of the pose gradient (gs_chain_pose) */
 } gs_frame;
 
 /* ---- setup ---------------------------------------------------------------- */

@@ -12,12 +12,15 @@ import os
 from .errors import DataError, DomainError, NumericalError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libgslic.so")
+# GSLIC_LIB: a developer override for A/B builds (tools/build_variant.sh); default the in-tree build
+LIB_PATH = os.environ.get("GSLIC_LIB") or os.path.join(_HERE, "lib", "libgslic.so")
 
 GS_ROW = 64
 GS_NPARAM = 59
 GS_TILE = 16
-GS_G2D = 12
+GS_G2D = 20  # int64 words per screen-space gradient row (10 fixed-point (hi, lo) fields)
+GS_G2D_FIELDS = 10
+GS_SPLAT = 16  # floats per 2D splat record
 CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3, 4
 GS_CNT_SLOTS = 16
 GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists materialised on demand)
@@ -53,7 +56,7 @@ class GsFrame(ctypes.Structure):
                 ("entry_splat", P), ("tile_offsets", P), ("counters", P),
                 ("color", P), ("depth", P), ("opacity", P), ("trans", P), ("n_contrib", P),
                 ("g_color", P), ("g_depth", P), ("g_opac", P), ("loss_parts", P), ("loss", P),
-                ("loss_blocks", i64)]
+                ("loss_blocks", i64), ("pose_acc", P)]
 
 
 _lib = None

@@ -28,35 +28,42 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, "common.cuh"),
-                                                      os.path.join(ROOT, "include", "gslic.h")]
+    deps = [os.path.join(CSRC, s) for s in SOURCES] + [os.path.join(CSRC, h) for h in os.listdir(CSRC)
+                                                      if h.endswith(".cuh")] + [os.path.join(ROOT, "include", "gslic.h")]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile and link libgslic.so (or, with `defines` / `out`, an experiment variant elsewhere)."""
+    if not force and not defines and out is None and not _stale():
         return LIB
-    os.makedirs(os.path.join(LIBDIR, "obj"), exist_ok=True)
+    lib_out = out or LIB
+    objdir = os.path.join(LIBDIR, "obj") if out is None else os.path.join(os.path.dirname(out), "obj_" + os.path.basename(out))
+    os.makedirs(objdir, exist_ok=True)
     objs = []
     logs = []
     for src in SOURCES:
-        obj = os.path.join(LIBDIR, "obj", src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-I", os.path.join(ROOT, "include"), "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(objdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-c",
+               os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stderr)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{r.stderr}")
         objs.append(obj)
-    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart"]
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", lib_out, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")
-    with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
-        fh.write("\n".join(logs))
+    if out is None:
+        with open(os.path.join(LIBDIR, "ptxas.log"), "w") as fh:
+            fh.write("\n".join(logs))
     if verbose:
         print("\n".join(logs))
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

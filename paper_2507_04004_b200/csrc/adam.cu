@@ -248,11 +248,17 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     __syncwarp();
     double pose6[6] = {0, 0, 0, 0, 0, 0};
     if (g >= 0) {
-        double2 *g2 = reinterpret_cast<double2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
-        const double2 a = g2[0], b = g2[1], c = g2[2], d = g2[3], e = g2[4];
+        // the fixed-point screen-space gradient row (GS_G2D_FIELDS (hi, lo) pairs, render.cu)
+        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d) + (int64_t)g * (GS_G2D / 2);
+        double gv[GS_G2D_FIELDS];
+#pragma unroll
+        for (int q = 0; q < GS_G2D_FIELDS; q++) {
+            const longlong2 w = g2[q];
+            gv[q] = fx_value(w.x, w.y);
+        }
         if (mode != 2 && f.counters[GS_CNT_LAZY])  // keep the row zero for the next view
-            for (int q = 0; q < GS_G2D / 2; q++) g2[q] = make_double2(0.0, 0.0);
-        const double gv[10] = {a.x, a.y, b.x, b.y, c.x, c.y, d.x, d.y, e.x, e.y};
+#pragma unroll
+            for (int q = 0; q < GS_G2D_FIELDS; q++) g2[q] = make_longlong2(0, 0);
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {
@@ -269,13 +275,21 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
         }
     }
     if (POSE) {
-        // warp butterfly, then one FP64 atomic per component per warp
+        // per Gaussian to fixed point, integer warp sums, one pair of integer atomics per
+        // component and warp: the sum does not depend on the (atomic-built) touched-list order
 #pragma unroll
         for (int q = 0; q < 6; q++) {
-            double v = pose6[q];
+            long long hi, lo;
+            fx_split(pose6[q], hi, lo);
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) atomicAdd(pose_out + q, v);
+            for (int o = 16; o > 0; o >>= 1) {
+                hi += __shfl_xor_sync(0xffffffffu, hi, o);
+                lo += __shfl_xor_sync(0xffffffffu, lo, o);
+            }
+            if (lane == 0) {
+                atomicAdd(reinterpret_cast<unsigned long long *>(f.pose_acc) + 2 * q, (unsigned long long)hi);
+                atomicAdd(reinterpret_cast<unsigned long long *>(f.pose_acc) + 2 * q + 1, (unsigned long long)lo);
+            }
         }
         if (mode == 3) return;
     }
@@ -370,7 +384,7 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
         // the iteration engine keeps the screen-space gradient rows zero between backwards (the
         // chain has consumed this one)
         if (c4 < GS_G2D / 2 && f.counters[GS_CNT_LAZY])
-            reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + c4] = make_double2(0.0, 0.0);
+            reinterpret_cast<longlong2 *>(f.g2d)[g * (GS_G2D / 2) + c4] = make_longlong2(0, 0);
         const float2 bc = reinterpret_cast<const float2 *>(f.bias_corr)[k];
         const float4 G = reinterpret_cast<const float4 *>(f.grad_rows)[k * (GS_ROW / 4) + c4];
         const int64_t off = g * GS_ROW + 4 * c4;
@@ -417,6 +431,13 @@ __global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, 
     *reinterpret_cast<float4 *>(am + off) = m4;
     *reinterpret_cast<float4 *>(av + off) = v4;
     *reinterpret_cast<float4 *>(params + off) = p4;
+}
+
+// the pose gradient from its fixed-point accumulators (gs_chain_pose)
+__global__ void pose_finish_kernel(const int64_t *__restrict__ acc, double *pose) {
+    pdl_wait();
+    const int q = threadIdx.x;
+    if (q < 6) pose[q] = fx_value(acc[2 * q], acc[2 * q + 1]);
 }
 
 // step counters advance after the update kernel has read them (no intra-kernel race)
@@ -497,13 +518,16 @@ extern "C" int gs_chain_pose(const gs_frame *f, const float *params, float *grad
         set_error("gs_chain_pose: null argument (grads and touched_accum are both set or both NULL)");
         return GS_ERR_ARG;
     }
-    cudaError_t e = cudaMemsetAsync(pose, 0, 6 * sizeof(double), (cudaStream_t)stream);
+    cudaError_t e = cudaMemsetAsync(f->pose_acc, 0, 12 * sizeof(int64_t), (cudaStream_t)stream);
     if (e != cudaSuccess) {
         set_error("gs_chain_pose: %s", cudaGetErrorString(e));
         return GS_ERR_CUDA;
     }
-    return launch_chain(f, const_cast<float *>(params), nullptr, nullptr, nullptr, view, nullptr, grads ? 1 : 3, grads,
-                        touched_accum, stream, pose);
+    int rc = launch_chain(f, const_cast<float *>(params), nullptr, nullptr, nullptr, view, nullptr, grads ? 1 : 3,
+                          grads, touched_accum, stream, pose);
+    if (rc) return rc;
+    launch_pdl(pose_finish_kernel, 1, 32, 0, (cudaStream_t)stream, (const int64_t *)f->pose_acc, pose);
+    return check_launch("pose_finish_kernel");
 }
 
 extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,

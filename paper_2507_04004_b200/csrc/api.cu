@@ -70,13 +70,13 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.height = h;
     f.tiles_x = tx;
     f.tiles_y = ty;
-    f.splat2d = c.take<float>(12 * nn);
+    f.splat2d = c.take<float>((int64_t)GS_SPLAT * nn);
     f.cov2d = c.take<float>(4 * nn);
     f.rect = c.take<int32_t>(4 * nn);
     f.valid = c.take<uint8_t>(nn);
     f.touched = c.take<uint8_t>(nn);
     f.touched_list = c.take<int32_t>(nn);
-    f.g2d = c.take<double>(GS_G2D * nn);
+    f.g2d = c.take<int64_t>((int64_t)GS_G2D * nn);
     f.grad_rows = c.take<float>((int64_t)GS_ROW * nn);
     f.bias_corr = c.take<float>(2 * nn);
     f.keep_bits = c.take<uint64_t>(nn);
@@ -111,6 +111,7 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     // loss partials (3 doubles per block) followed by the two 11-tap reflection tables
     f.loss_parts = c.take<double>(3 * f.loss_blocks + (int64_t)11 * (w + h) + 1);
     f.loss = c.take<double>(8);  // total, photometric, depth, dssim, running sum (GS_LOSS_ACCUMULATE)
+    f.pose_acc = c.take<int64_t>(16);
 }
 
 }  // namespace gs

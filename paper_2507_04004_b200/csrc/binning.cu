@@ -37,8 +37,7 @@ __device__ __forceinline__ void for_kept_tiles(const gs_frame &f, int g, F fn) {
     }
     // large footprint: bitmap of the big_* cull kernels, or the exact test again on overflow
     const int64_t base = (int64_t)f.keep_bits[g];
-    const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-    const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+    const SplatCull s = splat_cull(f.splat2d, g);
     for (int c = 0; c < ncand; c++) {
         const int tx = r.x + c % nx, ty = r.z + c / nx;
         bool keep;
@@ -47,7 +46,7 @@ __device__ __forceinline__ void for_kept_tiles(const gs_frame &f, int g, F fn) {
         } else {
             const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
             const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-            keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+            keep = tile_keep(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, x0, x1, y0, y1);
         }
         if (keep) fn(ty * f.tiles_x + tx);
     }
@@ -236,18 +235,23 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
         }
         __syncthreads();
     }
+    const int64_t E = s_carry[0];
+    const bool over = E > f.entry_capacity;
     if (threadIdx.x == 0) {
-        const int64_t E = s_carry[0];
-        f.tile_offsets[T] = (int32_t)E;
+        f.tile_offsets[T] = over ? 0 : (int32_t)E;
         boff[T] = s_carry[1];
         f.counters[GS_CNT_ENTRIES] = (int32_t)E;
         f.counters[GS_CNT_SMALL_E] = s_carry[1];
-        const bool over = E > f.entry_capacity;
         if (over) f.counters[GS_CNT_OVERFLOW] = 1;
         f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
         f.counters[GS_CNT_LAZY] = lazy;
         f.counters[GS_CNT_ANYFLAG] = 0;
     }
+    // over capacity: every tile range is emptied, so no later kernel (lazy or materialised lists,
+    // forward, backward) can index entry_splat / keys past the capacity; the caller re-lays out
+    // the workspace and repeats the frame
+    if (over)
+        for (int t = threadIdx.x; t < T; t += TS_THREADS) f.tile_offsets[t] = 0;
 }
 
 // 5) every bucketed pair's key into its tile's bucket (keys_b), unordered

@@ -342,6 +342,72 @@ __device__ __forceinline__ bool tile_keep(float mx, float my, float ca, float cb
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
+// ---------------------------------------------------------------------------
+// 2D splat records (GS_SPLAT floats per Gaussian, gslic.h).  The blend evaluates the quadratic
+// in the factored form q = a (dx + beta dy)^2 + gamma dy^2 (beta = b / a, gamma = det / a =
+// 1 / c00'), whose three coefficients are rounded to fp32 from FP64 and stay well conditioned for
+// needle-shaped footprints: rounding (a, b, c) themselves perturbs det(conic) by
+// ~6e-8 * a c / det, up to 5e-3 for Gaussians just past the near plane, which moved their
+// position gradients by 2e-3.  The binning keeps the reference's
+// (a, b, c) in the strict-IEEE decision path of the fp32 oracle restatement.
+struct SplatCull {
+    float mx, my, ca, cb, cc, qcut;
+};
+
+__device__ __forceinline__ SplatCull splat_cull(const float *splat2d, int64_t g) {
+    const float4 A = reinterpret_cast<const float4 *>(splat2d)[GS_SPLAT / 4 * g];
+    const float4 B = reinterpret_cast<const float4 *>(splat2d)[GS_SPLAT / 4 * g + 1];
+    const float2 D = reinterpret_cast<const float2 *>(splat2d)[GS_SPLAT / 2 * g + 6];
+    return SplatCull{A.x, A.y, A.z, D.x, D.y, B.w};
+}
+
+__device__ __forceinline__ float splat_depth(const float *splat2d, int64_t g) { return splat2d[GS_SPLAT * g + 6]; }
+
+// stores a record: A = (mx, my, a, beta), B = (gamma, opacity, depth, qcut), C = (r, g, b,
+// 1 - opacity) (colour written separately when c == nullptr), D = (b, c, 0, 0)
+__device__ __forceinline__ void splat_store(float *splat2d, int64_t g, float mx, float my, double ca, double cb,
+                                            double cc, float op, float z, float qcut) {
+    float4 *s = reinterpret_cast<float4 *>(splat2d) + GS_SPLAT / 4 * g;
+    const bool ok = ca > 0.0;
+    const double beta = ok ? cb / ca : 0.0, gamma = ok ? (ca * cc - cb * cb) / ca : 0.0;
+    s[0] = make_float4(mx, my, (float)ca, (float)beta);
+    s[1] = make_float4((float)gamma, op, z, qcut);
+    s[3] = make_float4((float)cb, (float)cc, 0.0f, 0.0f);
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic accumulation.  Screen-space gradient rows (and the pose gradient) are sums of
+// per-tile (per-Gaussian) partials in an order the scheduler picks.  Each partial is split
+// exactly into two 64-bit fixed-point words, hi in units of 2^-24 and lo in units of 2^-64, and
+// added with integer atomics: integer addition is associative, so the sums -- and everything
+// computed from them -- are bit-identical run to run (the reference pins this,
+// T/test_rasterizer.py:153-162, T/test_mapper.py:399-410).  Range |x| < 2^38 per partial and
+// 2^39 per sum (hi); lo holds < 2^40 per partial, so 2^23 partials fit; bits below 2^-64 are
+// truncated (deterministically).
+constexpr double FX_HI_SCALE = 16777216.0;             // 2^24
+constexpr double FX_LO_SCALE = 1099511627776.0;        // 2^40
+constexpr double FX_HI_UNIT = 1.0 / 16777216.0;        // 2^-24
+constexpr double FX_LO_UNIT = 5.421010862427522e-20;   // 2^-64
+
+__device__ __forceinline__ void fx_split(double x, long long &hi, long long &lo) {
+    double d = x * FX_HI_SCALE;
+    d = fmin(fmax(d, -4.0e18), 4.0e18);  // saturate (never reached by a finite gradient of this path)
+    const double h = trunc(d);
+    hi = (long long)h;
+    lo = (long long)trunc((d - h) * FX_LO_SCALE);  // d - h is exact
+}
+
+__device__ __forceinline__ void fx_atomic_add(long long *dst, double x) {
+    long long hi, lo;
+    fx_split(x, hi, lo);
+    if (hi) atomicAdd(reinterpret_cast<unsigned long long *>(dst), (unsigned long long)hi);
+    if (lo) atomicAdd(reinterpret_cast<unsigned long long *>(dst) + 1, (unsigned long long)lo);
+}
+
+__device__ __forceinline__ double fx_value(long long hi, long long lo) {
+    return (double)hi * FX_HI_UNIT + (double)lo * FX_LO_UNIT;
+}
+
 // Exact cull of every candidate tile of a Gaussian's rectangle (ty-major, then tx, as
 // R/rasterizer.py:113-122 enumerates them).  Returns the kept count; bit c of `bits` is the
 // result for candidate c < 64 (the emit pass recomputes candidates >= 64).

@@ -501,7 +501,10 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
         f.loss[1] = lc;
         f.loss[2] = ld;
         f.loss[3] = dssim;
-        if (accumulate) f.loss[4] += lc + (double)xi * ld;  // running sum of the engine's losses
+        // running sum of the engine's losses; an iteration whose binning overflowed its entry
+        // capacity is a no-op (rendered nothing, no gradient, no Adam step) and is re-run by the
+        // engine after re-laying out the workspace, so it is not counted here
+        if (accumulate && !f.counters[GS_CNT_OVERFLOW]) f.loss[4] += lc + (double)xi * ld;
         int *stamp = reinterpret_cast<int *>(tab_stamp);
         stamp[0] = (f.width << 16) + f.height;
         stamp[1] = ~((f.width << 16) + f.height);

@@ -181,6 +181,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
         const int64_t i = batch * 32 + lane;
         bool touched = false, big = false, need = false, front = false, small = false;
         Projected pr;
+        double pca = 0.0, pcb = 0.0, pcc = 0.0;  // FP64 conic (the blend's factored record)
         float op = 0.0f, qcut = 0.0f, radius = -1.0f, logit = 0.0f;
         int4 rect = make_int4(0, -1, 0, -1);
         // 1) per lane: near-plane test and FP64 projection, radius and tile rectangle
@@ -197,10 +198,11 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
             const float zf = (pk[0] * cam.rot_cw[6] + pk[1] * cam.rot_cw[7] + pk[2] * cam.rot_cw[8]) + cam.trans_cw[2];
             if (!(zf > GS_NEAR_CLIP)) {
                 if (!LAZY_SH) {  // the engine never reads the records of Gaussians it cannot draw
-                    float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
+                    float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + GS_SPLAT / 4 * i;
                     s2[0] = make_float4(0.f, 0.f, 0.f, 0.f);
                     s2[1] = make_float4(0.f, 0.f, zf, 0.f);
                     s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    s2[3] = make_float4(0.f, 0.f, 0.f, 0.f);
                     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(0.f, 0.f, 0.f, -1.f);
                     reinterpret_cast<int4 *>(f.rect)[i] = make_int4(0, -1, 0, -1);
                     f.valid[i] = 0;
@@ -222,6 +224,9 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
                 pr.ca = (float)pd.ca;
                 pr.cb = (float)pd.cb;
                 pr.cc = (float)pd.cc;
+                pca = pd.ca;
+                pcb = pd.cb;
+                pcc = pd.cc;
                 pr.valid = pd.valid;
                 op = 1.0f / (1.0f + expf(-pk[10]));
                 const bool active = pr.valid && tile_rect(pr.c00, pr.c01, pr.c11, op, pr.mx, pr.my, f.width,
@@ -245,9 +250,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
             // the Gaussians that can be drawn (kept in a tile, or large footprints still to be
             // culled); the reference-shaped API writes every record (out.ctx["proj"], R/gaussians.py:180-215)
             if (need) {
-                float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-                s2[0] = make_float4(pr.mx, pr.my, pr.ca, pr.cb);
-                s2[1] = make_float4(pr.cc, op, pr.mu[2], qcut);
+                splat_store(f.splat2d, i, pr.mx, pr.my, pca, pcb, pcc, op, pr.mu[2], qcut);
                 reinterpret_cast<int4 *>(f.rect)[i] = rect;
                 f.kept[i] = kept;
                 f.keep_bits[i] = bits;
@@ -269,7 +272,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
         // colour of the previous batch (its SH chunks landed with this batch's geometry)
         if (prev_need) {
             const float3 col = pp_colour(pc0, pc2, pc3, W.sh, lane, cam);
-            reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] =
+            reinterpret_cast<float4 *>(f.splat2d)[GS_SPLAT / 4 * prev_i + 2] =
                 make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(pc2.z)));
         }
         if (need) {
@@ -290,7 +293,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
     if (prev_need) {  // drain: the last batch's colour
         pp_cp_wait_0();
         const float3 col = pp_colour(pc0, pc2, pc3, W.sh, lane, cam);
-        reinterpret_cast<float4 *>(f.splat2d)[3 * prev_i + 2] = make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(pc2.z)));
+        reinterpret_cast<float4 *>(f.splat2d)[GS_SPLAT / 4 * prev_i + 2] = make_float4(col.x, col.y, col.z, 1.0f / (1.0f + expf(pc2.z)));
     }
 }
 
@@ -424,7 +427,7 @@ __device__ __forceinline__ void set_bit_range(uint32_t *bits, int b0, int b1) {
 struct BigCtx {
     int g, slot;
     int64_t base;
-    float4 s0, s1;
+    SplatCull s;
     int4 r;
     uint32_t *bits;  // output bitmap row (nullptr: big_bits overflow, the emit re-culls)
 };
@@ -432,8 +435,7 @@ struct BigCtx {
 __device__ __forceinline__ BigCtx big_ctx(const gs_frame &f, int64_t b) {
     BigCtx c;
     c.g = f.big_list[b];
-    c.s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * c.g];
-    c.s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * c.g + 1];
+    c.s = splat_cull(f.splat2d, c.g);
     c.r = reinterpret_cast<const int4 *>(f.rect)[c.g];
     c.slot = f.big_slot[b];
     c.base = (int64_t)f.keep_bits[c.g];
@@ -528,12 +530,12 @@ __global__ void __launch_bounds__(256, 3) big_bands_kernel(gs_frame f) {
             nbands = r.w - r.z + 1;
             slot = c.slot;
             bits = c.bits;
-            mx = c.s0.x;
-            my = c.s0.y;
-            ca = c.s0.z;
-            cb = c.s0.w;
-            cc = c.s1.x;
-            qcut = c.s1.w;
+            mx = c.s.mx;
+            my = c.s.my;
+            ca = c.s.ca;
+            cb = c.s.cb;
+            cc = c.s.cc;
+            qcut = c.s.qcut;
         }
         const BandConst K = band_const(mx, my, ca, cb, cc, qcut, r);
         for (int bi0 = 0; bi0 < ((nbands + CB_BSTRIDE - 1) / CB_BSTRIDE) * CB_BSTRIDE || bi0 == 0; bi0 += CB_BSTRIDE) {
@@ -605,12 +607,12 @@ __global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
             y0 = ty * GS_TILE;
             x1 = min(x0 + GS_TILE - 1, f.width - 1);
             y1 = min(y0 + GS_TILE - 1, f.height - 1);
-            mx = c.s0.x;
-            my = c.s0.y;
-            ca = c.s0.z;
-            cb = c.s0.w;
-            cc = c.s1.x;
-            qcut = c.s1.w;
+            mx = c.s.mx;
+            my = c.s.my;
+            ca = c.s.ca;
+            cb = c.s.cb;
+            cc = c.s.cc;
+            qcut = c.s.qcut;
             cls = tile_class(mx, my, ca, cb, cc, qcut, __fdividef(-cb, ca), __fdividef(-cb, cc), x0, x1, y0, y1);
         }
         unsigned amb = __ballot_sync(0xffffffffu, cls < 0);
@@ -684,7 +686,7 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                 f.kept[g] = -(1 + slot);  // kept < 0 encodes the huge slot
                 if (h < GS_HUGE_CAP)
                     reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] =
-                        ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
+                        ((uint64_t)__float_as_uint(splat_depth(f.splat2d, g)) << 32) | (uint32_t)g;
             }
         }
         if (b < nb) f.touched[g] = t;
@@ -699,9 +701,8 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
             const int4 r = reinterpret_cast<const int4 *>(f.rect)[gj];
             const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
             const int64_t base = (int64_t)f.keep_bits[gj];
-            const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * gj];
-            const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * gj + 1];
-            const unsigned long long key = ((unsigned long long)__float_as_uint(s1.z) << 32) | (uint32_t)gj;
+            const SplatCull s = splat_cull(f.splat2d, gj);
+            const unsigned long long key = ((unsigned long long)__float_as_uint(splat_depth(f.splat2d, gj)) << 32) | (uint32_t)gj;
             for (int c = threadIdx.x & 31; c < ncand; c += 32) {
                 const int tx = r.x + c % nx, ty = r.z + c / nx;
                 bool keep;
@@ -710,7 +711,7 @@ __global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
                 } else {
                     const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
                     const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                    keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                    keep = tile_keep(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, x0, x1, y0, y1);
                 }
                 if (keep) {
                     atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
@@ -802,10 +803,8 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     if (kept > 0)  // binning buckets
         count_kept_tiles(f.tile_scratch, reinterpret_cast<unsigned long long *>(f.tile_minkey),
                          ((unsigned long long)__float_as_uint(depth[i]) << 32) | (uint32_t)i, rect, bits, f.tiles_x);
-    float4 *s2 = reinterpret_cast<float4 *>(f.splat2d) + 3 * i;
-    s2[0] = make_float4(mx, my, ca, cb);
-    s2[1] = make_float4(cc, o, depth[i], qcut);
-    s2[2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 1.0f - o)
+    splat_store(f.splat2d, i, mx, my, ca, cb, cc, o, depth[i], qcut);
+    reinterpret_cast<float4 *>(f.splat2d)[GS_SPLAT / 4 * i + 2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 1.0f - o)
                    : make_float4(0.f, 0.f, 0.f, 1.0f - o);
     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(c00, c01, c11, radius);
     reinterpret_cast<int4 *>(f.rect)[i] = rect;

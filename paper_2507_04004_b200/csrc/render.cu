@@ -19,8 +19,16 @@ namespace gs {
 constexpr int RT = 256;  // threads per tile CTA = pixels per tile
 constexpr float NEG_HALF_LOG2E = -0.5f * GS_LOG2E;
 
-__device__ __forceinline__ float quad(float ca, float cb, float cc, float dx, float dy) {
-    return ca * dx * dx + 2.0f * cb * dx * dy + cc * dy * dy;
+// q = a (dx + beta dy)^2 + gamma dy^2 (the factored conic of the splat record, common.cuh);
+// au = a (dx + beta dy) = a dx + b dy is returned for the mean gradient
+__device__ __forceinline__ float quad(float a, float beta, float gamma, float dx, float dy, float &au) {
+#ifdef GS_EXP_U64
+    const float u = (float)fma((double)beta, (double)dy, (double)dx);
+#else
+    const float u = fmaf(beta, dy, dx);
+#endif
+    au = a * u;
+    return fmaf(au, u, gamma * dy * dy);
 }
 
 // alpha = min(o e^{-q/2}, 0.99) (R/rasterizer.py:270-272) and 1 - alpha.  1 - alpha is formed
@@ -31,9 +39,18 @@ __device__ __forceinline__ float quad(float ca, float cb, float cc, float dx, fl
 // error ~2^-22; results below 2^-126 flush to 0, i.e. alpha < 1e-38): the blend and its adjoint
 // use the same alpha.
 
+// (GS_EXP_PRECISE / GS_EXP_BWD_F64: precision experiments of tools/build_variant.sh, not the product)
+__device__ __forceinline__ float blend_exp(float q) {
+#ifdef GS_EXP_PRECISE
+    return expf(-0.5f * q);
+#else
+    return fast_ex2(-0.5f * GS_LOG2E * q);
+#endif
+}
+
 __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &araw, float &alpha, float &oma) {
     (void)omo;
-    const float e = fast_ex2(-0.5f * GS_LOG2E * q);
+    const float e = blend_exp(q);
     araw = op * e;
     if (araw > GS_ALPHA_CLAMP) {
         alpha = GS_ALPHA_CLAMP;
@@ -54,9 +71,9 @@ struct FwdPixel {
 };
 
 struct FwdStage {
-    float4 a[RT];  // mx my ca cb
-    float4 b[RT];  // cc opacity depth 1-opacity
-    float4 c[RT];  // r g b -
+    float4 a[RT];  // mx my a beta
+    float4 b[RT];  // gamma opacity depth qcut
+    float4 c[RT];  // r g b 1-opacity
 };
 
 __device__ __forceinline__ FwdPixel fwd_pixel_init(const gs_frame &f, int tile) {
@@ -102,10 +119,10 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
         if (__syncthreads_count(px.done) == RT) return true;
         const int e = b + threadIdx.x;
         if ((int)threadIdx.x < step && e < p1) {
-            const int g = fetch(e);
-            st.a[threadIdx.x] = __ldg(sp + 3 * g);
-            st.b[threadIdx.x] = __ldg(sp + 3 * g + 1);
-            st.c[threadIdx.x] = __ldg(sp + 3 * g + 2);
+            const int64_t g = fetch(e);
+            st.a[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g);
+            st.b[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 1);
+            st.c[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 2);
         }
         __syncthreads();
         if (!px.done) {
@@ -113,8 +130,8 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
             for (int j = 0; j < nb; j++) {
                 const float4 A = st.a[j], B = st.b[j], C = st.c[j];
                 const float dx = px.fx - A.x, dy = px.fy - A.y;
-                float araw, alpha, oma;
-                alpha_oma(B.y, C.w, quad(A.z, A.w, B.x, dx, dy), araw, alpha, oma);
+                float araw, alpha, oma, au;
+                alpha_oma(B.y, C.w, quad(A.z, A.w, B.x, dx, dy, au), araw, alpha, oma);
                 const float w = alpha * px.T;
                 px.c0 += C.x * w;
                 px.c1 += C.y * w;
@@ -142,6 +159,10 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
     __shared__ int32_t s_tmp[RT / 32];
     const int tile = blockIdx.x;
     FwdPixel px = fwd_pixel_init(f, tile);
+    if (f.counters[GS_CNT_OVERFLOW]) {  // binning over capacity (tile ranges emptied): background
+        fwd_pixel_store(f, tile, px);
+        return;
+    }
     if (f.counters[GS_CNT_LAZY]) {
         // lazy lists: the leading screen-covering Gaussians (every one whose key is below the
         // tile's smallest bucketed key precedes the whole bucket); tiles whose blend outlives them
@@ -175,7 +196,7 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
 // Lazy lists, continuation 1: the bucket keys of the tiles that need them (ts_flag != 0)
 __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
     pdl_wait();
-    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
+    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG] || f.counters[GS_CNT_OVERFLOW]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     int32_t *cur = ts_cursor(f);
     const int32_t *flag = ts_flag(f);
@@ -186,8 +207,7 @@ __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
         const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
         const int64_t base = (int64_t)f.keep_bits[g];
-        const float4 s0 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g];
-        const float4 s1 = reinterpret_cast<const float4 *>(f.splat2d)[3 * g + 1];
+        const SplatCull s = splat_cull(f.splat2d, g);
         for (int c = 0; c < ncand; c++) {
             const int tx = r.x + c % nx, ty = r.z + c / nx, t = ty * f.tiles_x + tx;
             bool keep;
@@ -198,7 +218,7 @@ __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
             } else {
                 const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
                 const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                keep = tile_keep(s0.x, s0.y, s0.z, s0.w, s1.x, s1.w, x0, x1, y0, y1);
+                keep = tile_keep(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, x0, x1, y0, y1);
             }
             if (keep && flag[t]) f.keys_b[atomicAdd(&cur[t], 1)] = key;
         }
@@ -223,7 +243,7 @@ struct FinishSmem {
 
 __global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int early_stop) {
     pdl_wait();
-    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG]) return;
+    if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG] || f.counters[GS_CNT_OVERFLOW]) return;
     const int tile = blockIdx.x;
     if (ts_flag(f)[tile] != TL_LIST) return;
     extern __shared__ uint64_t fin_raw[];
@@ -252,81 +272,126 @@ __global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int
     fwd_pixel_store(f, tile, px);
 }
 
-// Transposed butterfly over 10 fields in 12 shuffles: on return, an even lane L holds the warp
-// sum of field reduce10_field(L) (or -1: nothing to store; field 2 is held by 4 lanes, only one
-// stores it).  Stages: xor 16 splits the fields 5/5, xor 8 splits 2/2 and sums the fifth
-// everywhere, xor 4 splits 1/1 (+ the fifth), xor 2 separates the fifth, xor 1 completes.
-__device__ __forceinline__ float reduce10(const float v[10]) {
+// Per-entry warp reductions (transposed butterflies: each stage halves the fields a lane carries).
+// The six geometric fields (mean2d 2, conic 3, opacity) are summed in FP64: for Gaussians just
+// past the near plane the chain rule cancels their mean and conic paths ~1e4-fold, and rounding
+// the per-pixel partial sums to fp32 alone moved position gradients by ~2e-3 of the reference
+// (tools/bwd_emulator.py); the colour / depth fields stay fp32.
+//
+// reduce_geo: on return lane L with (L & 3) == 0 holds the warp sum of field geo_field(L) >= 0.
+__device__ __forceinline__ double reduce_geo(const float v[6]) {
     const unsigned lane = threadIdx.x & 31u;
-    const bool h = lane & 16u, b3 = lane & 8u, b2 = lane & 4u, b1 = lane & 2u;
-    float u[5];
+    const bool h = lane & 16u, b3 = lane & 8u, b2 = lane & 4u;
+    double u[3];
 #pragma unroll
-    for (int k = 0; k < 5; k++) {
-        const float send = h ? v[k] : v[k + 5];
-        const float keep = h ? v[k + 5] : v[k];
+    for (int k = 0; k < 3; k++) {  // xor 16: fields {0,1,2} | {3,4,5}
+        const double send = h ? (double)v[k] : (double)v[k + 3];
+        const double keep = h ? (double)v[k + 3] : (double)v[k];
         u[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
     }
-    float w[3];
-#pragma unroll
-    for (int k = 0; k < 2; k++) {
-        const float send = b3 ? u[k] : u[k + 3];
-        const float keep = b3 ? u[k + 3] : u[k];
-        w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-    w[2] = u[2] + __shfl_xor_sync(0xffffffffu, u[2], 8);
-    float z0, z1;
-    {
-        const float send = b2 ? w[0] : w[1];
-        const float keep = b2 ? w[1] : w[0];
-        z0 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-        z1 = w[2] + __shfl_xor_sync(0xffffffffu, w[2], 4);
-    }
-    const float send = b1 ? z0 : z1;
-    const float keep = b1 ? z1 : z0;
-    const float y = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-    return y + __shfl_xor_sync(0xffffffffu, y, 1);
+    // xor 8: b3 = 0 keeps u0, u1; b3 = 1 keeps u2
+    const double r1 = __shfl_xor_sync(0xffffffffu, b3 ? u[0] : u[2], 8);
+    const double r2 = __shfl_xor_sync(0xffffffffu, u[1], 8);
+    const double w0 = b3 ? u[2] + r1 : u[0] + r1;
+    const double w1 = u[1] + r2;  // meaningful for b3 = 0 only
+    // xor 4: b3 = 0 splits (w0 | w1); b3 = 1 lanes both hold field 2 of their half
+    const double send = b3 ? w0 : (b2 ? w0 : w1);
+    const double keep = b3 ? w0 : (b2 ? w1 : w0);
+    double z = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    z += __shfl_xor_sync(0xffffffffu, z, 2);
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    return z;
 }
 
-__device__ __forceinline__ int reduce10_field(unsigned lane) {
-    if (lane & 1u) return -1;
-    const int h5 = (lane & 16u) ? 5 : 0;
-    if (!(lane & 2u)) return h5 + ((lane & 8u) ? 3 : 0) + ((lane & 4u) ? 1 : 0);
-    return (lane & 12u) ? -1 : h5 + 2;
+__device__ __forceinline__ int geo_field(unsigned lane) {
+    if (lane & 3u) return -1;
+    const int base = (lane & 16u) ? 3 : 0;
+    if (!(lane & 8u)) return base + ((lane & 4u) ? 1 : 0);
+    return (lane & 4u) ? -1 : base + 2;
+}
+
+// reduce_col: the four fp32 fields (colour 3, depth); lane L with (L & 7) == 0 holds field
+// col_field(L)
+__device__ __forceinline__ float reduce_col(const float v[4]) {
+    const unsigned lane = threadIdx.x & 31u;
+    const bool h = lane & 16u, b3 = lane & 8u;
+    float u[2];
+#pragma unroll
+    for (int k = 0; k < 2; k++) {  // xor 16: {0,1} | {2,3}
+        const float send = h ? v[k] : v[k + 2];
+        const float keep = h ? v[k + 2] : v[k];
+        u[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+    float z = (b3 ? u[1] : u[0]) + __shfl_xor_sync(0xffffffffu, b3 ? u[0] : u[1], 8);
+    z += __shfl_xor_sync(0xffffffffu, z, 4);
+    z += __shfl_xor_sync(0xffffffffu, z, 2);
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    return z;
+}
+
+__device__ __forceinline__ int col_field(unsigned lane) {
+    if (lane & 7u) return -1;
+    return ((lane & 16u) ? 2 : 0) + ((lane & 8u) ? 1 : 0);
 }
 
 // One pixel's contribution to the 10 screen-space gradient fields of an entry, back-to-front
 // replay step (R/rasterizer.py:365-410): undoes the entry's 1 - alpha on T, accumulates into v
-// and advances the suffix sums S.
+// and advances the suffix sums S.  The quadratic and the mean gradient use the factored conic
+// of the splat record: a dx + b dy = a u and b dx + c dy = beta a u + gamma dy (u = dx + beta dy).
+#if defined(GS_EXP_BWD_F64) || defined(GS_EXP_STATE64)
+using bwd_t = double;
+#else
+using bwd_t = float;
+#endif
+
 struct BwdPixel {
-    float fx, fy, T, gc0, gc1, gc2, gd, go, S0, S1, S2, Sd, So;
+    float fx, fy;
+    bwd_t T, gc0, gc1, gc2, gd, go, S0, S1, S2, Sd, So;
     int cnt;
 };
 
-__device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const float4 &B, const float4 &C, float v[10]) {
+__device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const float4 &B, const float4 &C, bwd_t v[10]) {
+#ifdef GS_EXP_BWD_F64
+    const double dx = p.fx - (double)A.x, dy = p.fy - (double)A.y;
+    const double a = A.z, beta = A.w, gamma = B.x, op = B.y, dep = B.z;
+    const double u = dx + beta * dy, au = a * u;
+    const double e = exp(-0.5 * (au * u + gamma * dy * dy));
+    const double araw = op * e;
+    const bool clamped = araw > (double)GS_ALPHA_CLAMP;
+    const double alpha = clamped ? (double)GS_ALPHA_CLAMP : araw;
+    const double om = clamped ? 1.0 - (double)GS_ALPHA_CLAMP : 1.0 - op * e;
+    const double rom = 1.0 / om;
+#else
     const float dx = p.fx - A.x, dy = p.fy - A.y;
-    const float ca = A.z, cb = A.w, cc = B.x, op = B.y, dep = B.z;
-    const float e = fast_ex2(NEG_HALF_LOG2E * quad(ca, cb, cc, dx, dy));
+    const float a = A.z, beta = A.w, gamma = B.x, op = B.y, dep = B.z;
+    float au;
+    const float e = blend_exp(quad(a, beta, gamma, dx, dy, au));
     const float araw = op * e;
     const bool clamped = araw > GS_ALPHA_CLAMP;
     const float alpha = clamped ? GS_ALPHA_CLAMP : araw;
     const float om = clamped ? 0.01f : fmaf(-op, e, 1.0f);
+#ifdef GS_EXP_PRECISE
+    const float rom = 1.0f / om;
+#else
     const float rom = fast_rcp(om);
-    const float Tb = p.T * rom;
-    const float w = alpha * Tb;
+#endif
+#endif
+    const bwd_t Tb = p.T * rom;
+    const bwd_t w = alpha * Tb;
     v[6] += w * p.gc0;
     v[7] += w * p.gc1;
     v[8] += w * p.gc2;
     v[9] += w * p.gd;
-    const float dl = Tb * (C.x * p.gc0 + C.y * p.gc1 + C.z * p.gc2 + dep * p.gd + p.go) -
+    const bwd_t dl = Tb * (C.x * p.gc0 + C.y * p.gc1 + C.z * p.gc2 + dep * p.gd + p.go) -
                      (p.S0 * p.gc0 + p.S1 * p.gc1 + p.S2 * p.gc2 + p.Sd * p.gd + p.So * p.go) * rom;
     if (!clamped) {  // no alpha-chain gradient on the 0.99 clamp (R/rasterizer.py:399-404)
-        const float gq = dl * (-0.5f * alpha);
+        const bwd_t gq = dl * (bwd_t)(-0.5f * alpha);
         v[5] += dl * e;  // d alpha / d opacity = e
         v[2] += gq * dx * dx;
-        v[3] += gq * 2.0f * dx * dy;
+        v[3] += gq * 2 * dx * dy;
         v[4] += gq * dy * dy;
-        v[0] += gq * (-2.0f * (ca * dx + cb * dy));
-        v[1] += gq * (-2.0f * (cb * dx + cc * dy));
+        v[0] += gq * (-2 * au);
+        v[1] += gq * (-2 * (beta * au + gamma * dy));
     }
     p.S0 += C.x * w;
     p.S1 += C.y * w;
@@ -337,17 +402,26 @@ __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const flo
 }
 
 // 128 threads per 16x16 tile, two pixels per thread (rows y and y + 8): the two pixels'
-// contributions are summed in registers before the warp reduction.
-constexpr int BPX = 2;              // pixels per backward thread (one column, rows 16 / BPX apart; 4 measured no faster)
+// contributions are summed in registers before the warp reduction.  Deterministic: per staged
+// entry every warp stores its butterfly sums in its own shared-memory slot, the four warp sums
+// are added in warp order, and the tile partial goes to the Gaussian's row through fixed-point
+// integer atomics (fx_atomic_add) -- no floating-point sum depends on scheduling order.
+#ifndef GS_BPX
+#define GS_BPX 2
+#endif
+constexpr int BPX = GS_BPX;         // pixels per backward thread (one column, rows 16 / BPX apart)
 constexpr int BT = RT / BPX;        // backward threads per tile
+constexpr int BW = BT / 32;         // warps per backward CTA
+constexpr int BST = BT / 2;         // entries staged per round
 
 __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_depth_grads) {
     pdl_wait();
-    __shared__ float4 s_a[RT];
-    __shared__ float4 s_b[RT];
-    __shared__ float4 s_c[RT];
-    __shared__ int s_g[RT];
-    __shared__ float s_acc[RT][10];
+    __shared__ float4 s_a[BST];
+    __shared__ float4 s_b[BST];
+    __shared__ float4 s_c[BST];
+    __shared__ int s_g[BST];
+    __shared__ double s_geo[BW][BST][6];
+    __shared__ float s_col[BW][BST][4];
     __shared__ int s_max;
     const int tile = blockIdx.x;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
@@ -365,7 +439,8 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
     }
     if (stop == start) return;
     const unsigned lane = threadIdx.x & 31u;
-    const int fld = reduce10_field(lane);
+    const int warp = threadIdx.x >> 5;
+    const int fgeo = geo_field(lane), fcol = col_field(lane);
     // entry source: materialised list, or (lazy lists) the screen-covering Gaussians then the
     // sorted bucket
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
@@ -417,18 +492,17 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
     __syncthreads();
     const int max_cnt = s_max;
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
-    for (int b_end = start + max_cnt; b_end > start; b_end -= RT) {
-        const int b0 = max(start, b_end - RT);
+    for (int b_end = start + max_cnt; b_end > start; b_end -= BST) {
+        const int b0 = max(start, b_end - BST);
         const int nb = b_end - b0;
         __syncthreads();
-        for (int i = threadIdx.x; i < nb; i += BT) {
-            const int g = fetch(b0 - start + i);
-            s_g[i] = g;
-            s_a[i] = __ldg(sp + 3 * g);
-            s_b[i] = __ldg(sp + 3 * g + 1);
-            s_c[i] = __ldg(sp + 3 * g + 2);
-#pragma unroll
-            for (int k = 0; k < 10; k++) s_acc[i][k] = 0.0f;
+        if ((int)threadIdx.x < nb) {  // (nb <= BST <= BT)
+            const int i = threadIdx.x;
+            const int64_t g = fetch(b0 - start + i);
+            s_g[i] = (int)g;
+            s_a[i] = __ldg(sp + GS_SPLAT / 4 * g);
+            s_b[i] = __ldg(sp + GS_SPLAT / 4 * g + 1);
+            s_c[i] = __ldg(sp + GS_SPLAT / 4 * g + 2);
         }
         __syncthreads();
         for (int j = nb - 1; j >= 0; j--) {
@@ -436,40 +510,55 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
             bool any = false;
 #pragma unroll
             for (int k = 0; k < BPX; k++) any |= le < px[k].cnt;
-            if (!__any_sync(0xffffffffu, any)) continue;
-            const float4 A = s_a[j], B = s_b[j], C = s_c[j];
-            float v[10];
+            double sg = 0.0;
+            float sc = 0.0f;
+            if (__any_sync(0xffffffffu, any)) {
+                const float4 A = s_a[j], B = s_b[j], C = s_c[j];
+                bwd_t v[10];
 #pragma unroll
-            for (int k = 0; k < 10; k++) v[k] = 0.0f;
+                for (int k = 0; k < 10; k++) v[k] = 0;
 #pragma unroll
-            for (int k = 0; k < BPX; k++)
-                if (le < px[k].cnt) bwd_step(px[k], A, B, C, v);
-            const float sum = reduce10(v);
-            if (fld >= 0 && sum != 0.0f) atomicAdd(&s_acc[j][fld], sum);
+                for (int k = 0; k < BPX; k++)
+                    if (le < px[k].cnt) bwd_step(px[k], A, B, C, v);
+                const float vg[6] = {(float)v[0], (float)v[1], (float)v[2], (float)v[3], (float)v[4], (float)v[5]};
+                const float vc[4] = {(float)v[6], (float)v[7], (float)v[8], (float)v[9]};
+                sg = reduce_geo(vg);
+                sc = reduce_col(vc);
+            }
+            if (fgeo >= 0) s_geo[warp][j][fgeo] = sg;
+            if (fcol >= 0) s_col[warp][j][fcol] = sc;
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < nb; i += BT) {
-            // cross-tile accumulation in FP64: a large Gaussian collects thousands of per-tile
-            // partial sums of mixed sign (near-plane splats cover every tile of the image)
-            const float *a = s_acc[i];
-            double *dst = f.g2d + (int64_t)s_g[i] * GS_G2D;
+        // the tile's partial of every staged entry: warp sums in warp order, then fixed point
+        for (int idx = threadIdx.x; idx < nb * GS_G2D_FIELDS; idx += BT) {
+            const int i = idx / GS_G2D_FIELDS, k = idx - i * GS_G2D_FIELDS;
+            double v;
+            if (k < 6) {
+                v = s_geo[0][i][k];
 #pragma unroll
-            for (int k = 0; k < 10; k++)
-                if (a[k] != 0.0f) atomicAdd(dst + k, (double)a[k]);
+                for (int w = 1; w < BW; w++) v += s_geo[w][i][k];
+            } else {
+                float c = s_col[0][i][k - 6];
+#pragma unroll
+                for (int w = 1; w < BW; w++) c += s_col[w][i][k - 6];
+                v = c;
+            }
+            if (v != 0.0) fx_atomic_add(reinterpret_cast<long long *>(f.g2d) + (int64_t)s_g[i] * GS_G2D + 2 * k, v);
         }
     }
 }
 
-// zero the g2d rows of the touched Gaussians (12 doubles = 6 double2 per row)
+// zero the g2d rows of the touched Gaussians (GS_G2D int64 = GS_G2D / 2 16-B words per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
     pdl_wait();
     // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
     // batches, the chain rule) clears every row it consumes, and the workspace starts zero-filled
     if (f.counters[GS_CNT_LAZY]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 6 * nt; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g = f.touched_list[i / 6];
-        reinterpret_cast<double2 *>(f.g2d)[g * (GS_G2D / 2) + i % 6] = make_double2(0.0, 0.0);
+    constexpr int W = GS_G2D / 2;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < W * nt; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = f.touched_list[i / W];
+        reinterpret_cast<longlong2 *>(f.g2d)[g * W + i % W] = make_longlong2(0, 0);
     }
 }
 

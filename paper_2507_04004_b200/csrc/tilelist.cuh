@@ -30,7 +30,7 @@ __device__ __forceinline__ const uint64_t *huge_keys(const gs_frame &f) {
 }
 
 __device__ __forceinline__ uint64_t depth_key(const gs_frame &f, int g) {
-    return ((uint64_t)__float_as_uint(f.splat2d[12 * (int64_t)g + 6]) << 32) | (uint32_t)g;
+    return ((uint64_t)__float_as_uint(splat_depth(f.splat2d, g)) << 32) | (uint32_t)g;
 }
 
 // ---------------------------------------------------------------------------------------------

@@ -17,7 +17,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import GS_G2D, GS_ROW, call
+from ._lib import GS_G2D, GS_ROW, GS_SPLAT, call
 from .errors import DataError
 from .gaussians import (GaussianMap, NAMES, SLICES, as_device_map, camera_struct, default_device,
                         stream_ptr, struct_to_device)
@@ -150,21 +150,32 @@ class Workspace:
         self.g_color = self.view("g_color", "f32", (h, w, 3))
         self.g_depth = self.view("g_depth", "f32", (h, w))
         self.g_opac = self.view("g_opac", "f32", (h, w))
-        self.splat2d = self.view("splat2d", "f32", (n, 12))
+        self.splat2d = self.view("splat2d", "f32", (n, GS_SPLAT))
         self.cov2d = self.view("cov2d", "f32", (n, 4))
         self.valid = self.view("valid", "u8", (n,))
         self.touched = self.view("touched", "u8", (n,))
-        self.g2d = self.view("g2d", "f64", (n, GS_G2D))
+        self.g2d_fixed = self.view("g2d", "u64", (n, GS_G2D))
         self.counters = self.view("counters", "i32", (2 * _lib.GS_CNT_SLOTS,))
         self.entry_splat = self.view("entry_splat", "i32", (max(self.capacity, 1),))
         self.tile_offsets = self.view("tile_offsets", "i32", (self.tiles_x * self.tiles_y + 1,))
         self.loss = self.view("loss", "f64", (8,))
+
+    @property
+    def g2d(self) -> torch.Tensor:
+        """(n, 10) float64 screen-space gradient rows (mean2d 2, conic 3, opacity, colour 3, depth)
+        decoded from the fixed-point accumulators: value = hi 2^-24 + lo 2^-64 (gslic.h GS_G2D)."""
+        return g2d_decode(self.g2d_fixed)
 
     def view(self, field: str, kind: str, shape) -> torch.Tensor:
         dtype, item = _DT[kind]
         off = getattr(self.frame, field) - self.base + (self.base - self.buf.data_ptr())
         nbytes = int(np.prod(shape)) * item
         return self.buf[off:off + nbytes].view(dtype).view(*shape)
+
+
+def g2d_decode(fixed: torch.Tensor) -> torch.Tensor:
+    """Fixed-point (hi, lo) int64 pairs -> float64 values (same arithmetic as the device's fx_value)."""
+    return fixed[:, 0::2].double() * 2.0 ** -24 + fixed[:, 1::2].double() * 2.0 ** -64
 
 
 _CAP_HINT: dict = {}
@@ -229,7 +240,7 @@ def forward(gmap, cam, cull: bool = True, early_stop: bool = True) -> RenderOutp
     E = int(cnt[_lib.CNT_ENTRIES])
     n = len(g)
     s2 = ws.splat2d
-    proj = {"mean2d": s2[:, 0:2], "conic": s2[:, 2:5], "depth": s2[:, 6], "valid": ws.valid.bool(),
+    proj = {"mean2d": s2[:, 0:2], "conic": s2[:, [2, 12, 13]], "depth": s2[:, 6], "valid": ws.valid.bool(),
             "cov2d": ws.cov2d[:, 0:3], "radius": ws.cov2d[:, 3]}
     ctx = {"proj": proj, "opac": s2[:, 5], "colors": s2[:, 8:11], "entry_splat": ws.entry_splat[:E],
            "tile_offsets": ws.tile_offsets, "tiles_x": ws.tiles_x, "tiles_y": ws.tiles_y, "cam": cam,

@@ -20,11 +20,11 @@ pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 SCENES = sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLD, "*.npz"))
                 if "entry_splat" in np.load(p).files)  # the forward/backward scenes
+GROUPS = {"pos": (0, 3), "log_scale": (3, 6), "quat": (6, 10), "opacity_logit": (10, 11), "sh_low": (11, 14),
+          "sh_high": (14, 59)}
 IMG_TOL = 1e-4
 REL_TOL = 1e-3
-# screen-space (intermediate) gradients: the mean2d term sums pixel contributions of opposite
-# sign, so its fp32 round-off is ~1e-3 of the largest row; the parameter gradients keep 1e-3
-G2D_TOL = 3e-3
+G2D_TOL = REL_TOL  # screen-space (intermediate) gradients: the same 1e-3 bar
 
 
 def _np(t):
@@ -79,11 +79,21 @@ def test_forward_matches_reference(name):
                    ("transmittance", z["transmittance"])):
         err = np.max(np.abs(_np(getattr(out, k)) - ref))
         assert err < IMG_TOL * max(1.0, float(np.abs(ref).max()) if k == "depth" else 1.0), (k, err)
-    assert np.mean(_np(out.n_contrib) != z["n_contrib"]) < 1e-3
+    assert np.array_equal(_np(out.n_contrib), z["n_contrib"])
     assert np.array_equal(_np(out.ctx["proj"]["valid"]).astype(bool), z["valid"])
-    vm = z["valid"] & (z["pdepth"] > 0.1)  # fp32 mu_cam cancels near the 0.01 m clip plane
-    mref = z["mean2d"][vm]
-    assert np.max(np.abs(_np(out.ctx["proj"]["mean2d"])[vm] - mref) / np.maximum(1.0, np.abs(mref))) < 1e-5
+    # mean2d of every valid Gaussian against the oracle projection of the same fp32 parameters
+    # and fp32 camera (the device's map and gs_camera are fp32; just past the 0.01 m clip plane
+    # fx / z ~ 1e5 turns their 6e-8 rounding into ~1e-5 relative, so the float64 golden is the
+    # bar beyond 0.1 m)
+    vm = z["valid"]
+    r32 = lambda a: np.asarray(a).astype(np.float32).astype(np.float64)  # noqa: E731
+    oproj = O.project(O.GaussianMap.from_rows(r32(z["rows"])), r32(z["rot_cw"]), r32(z["trans_cw"]),
+                      tuple(float(np.float32(z[k])) for k in ("fx", "fy", "cx", "cy")))
+    m32 = oproj["mean2d"][vm]
+    assert np.max(np.abs(_np(out.ctx["proj"]["mean2d"])[vm] - m32) / np.maximum(1.0, np.abs(m32))) < 1e-6
+    far = z["valid"] & (z["pdepth"] > 0.1)
+    mref = z["mean2d"][far]
+    assert np.max(np.abs(_np(out.ctx["proj"]["mean2d"])[far] - mref) / np.maximum(1.0, np.abs(mref))) < 1e-5
     nearv = z["pdepth"] > 0.01  # colours of Gaussians behind the camera are never used
     assert normwise(_np(out.ctx["colors"])[nearv], z["colors"][nearv]) < 1e-5
     full = R.forward(g, cam, cull=False)
@@ -117,19 +127,12 @@ def test_loss_and_gradients_match_reference(name):
     grads, touched, _ = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
     assert np.array_equal(_np(touched).astype(bool), z["touched"])
     gr = _np(grads["_rows"])[:, :59]
-    groups = {"pos": (0, 3), "log_scale": (3, 6), "quat": (6, 10), "opacity_logit": (10, 11),
-              "sh_low": (11, 14), "sh_high": (14, 59)}
-    # Gaussians within 5 cm of the camera (just past the 0.01 m clip plane) cover the whole
-    # image with near-constant alpha; their position/covariance gradients cancel ~100x between
-    # the mean and conic paths, amplifying the fp32 per-pixel rounding of the blend (DESIGN.md,
-    # "precision").  They are held to 2e-2; every other Gaussian to the 1e-3 bar.
-    near = z["pdepth"] < 0.05
-    for k, (a, b) in groups.items():
-        far_err = normwise(gr[~near, a:b], z["grads"][~near, a:b])
-        assert far_err < REL_TOL, (k, far_err)
-        if near.any():
-            near_err = normwise(gr[near, a:b], z["grads"][near, a:b])
-            assert near_err < 2e-2, (k, near_err)
+    # every Gaussian, including those just past the 0.01 m clip plane (room4096: 1,818 of 4,096
+    # within 5 cm, whose mean and conic paths cancel ~1e4-fold in the chain rule; the factored
+    # conic record and the FP64 geometric reduction keep them at ~1e-4)
+    for k, (a, b) in GROUPS.items():
+        err = normwise(gr[:, a:b], z["grads"][:, a:b])
+        assert err < REL_TOL, (k, err)
 
 
 def test_losses_match_reference_golden():
@@ -291,7 +294,7 @@ def test_mapping_iterations_match_oracle():
         assert not bool(eng.ws.g_depth.any()) and not bool(eng.ws.g_opac.any()), it
     delta_gpu = _np(g.rows())[:, :59] - sc.rows
     delta_ref = og.rows() - sc.rows
-    assert normwise(delta_gpu, delta_ref) < 0.05
+    assert normwise(delta_gpu, delta_ref) < REL_TOL
     # graph-captured replay runs the same iteration
     eng.capture()
     eng.step(0)
@@ -382,7 +385,7 @@ def test_lazy_lists_match_materialised(which):
     if which == "interleaved":
         assert cnt[16 + 3] > 0  # screen-covering Gaussians present
         assert (flags == 1).any()  # some tile's bucket interleaves with them: merged list
-    # the backward over the lazy lists matches the materialised lists' (up to atomic order)
+    # the backward over the lazy lists matches the materialised lists' bit for bit
     rng = np.random.default_rng(0)
     h, w = int(cam.height), int(cam.width)
     gc = torch.as_tensor(rng.standard_normal((h, w, 3)), dtype=torch.float32, device="cuda")
@@ -402,14 +405,15 @@ def test_lazy_lists_match_materialised(which):
         cols = {0: [0, 1], 1: [2, 3, 4], 2: [5], 3: [6, 7, 8], 4: [9]}[k]
         a = _np(ref).reshape(len(touched), -1)[touched]
         b = g2d[touched][:, cols].reshape(a.shape)
-        assert normwise(b, a) < 1e-5, k
+        assert np.array_equal(b, a), k
 
 
 @pytest.mark.parametrize("name", SCENES)
 def test_pose_gradient_matches_reference(name):
     """backward(with_pose=True) through gs_chain_pose: the 6-dof pose gradient of
     R/rasterizer.py:646-657 (golden from the reference), attribute gradients unchanged, and the
-    tracker's pose-only call (grads not materialised) agrees."""
+    tracker's pose-only call (grads not materialised) agrees bit for bit."""
+    import torch
     from paper_2507_04004_b200 import rasterizer as R
     p = np.load(os.path.join(GOLD, "pose.npz"))
     z, cam, g = load(name)
@@ -425,17 +429,18 @@ def test_pose_gradient_matches_reference(name):
                        with_pose=True)
     assert normwise(_np(pose), opose) < 1e-4, (_np(pose), opose)
     ref = p[f"{name}_pose"]
-    # the pose sums every touched Gaussian's term; Gaussians within 5 cm of the camera carry the
-    # fp32 blend rounding amplified ~100x (see test_loss_and_gradients_match_reference): 2e-2 there
-    tol = 2e-2 if (z["pdepth"][z["touched"]] < 0.05).any() else REL_TOL
-    assert normwise(_np(pose), ref) < tol, (_np(pose), ref)
+    assert normwise(_np(pose), ref) < REL_TOL, (_np(pose), ref)
     assert np.array_equal(_np(touched).astype(bool), z["touched"])
+    # bit-identical run to run (fixed-point accumulation; T/test_rasterizer.py:153-162)
+    g1, _, pose1 = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"], with_pose=True)
+    assert torch.equal(g1["_rows"], grads["_rows"]) and torch.equal(pose1, pose)
+    only = R.pose_backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
+    assert torch.equal(only, pose)
+    # without the pose: the same screen-space gradients through the non-pose chain instantiation
+    # (its FP64 chain is compiled separately, so rounding may differ in the last bits)
     g0, _, none = R.backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
     assert none is None
-    # (the backward's FP64 atomics are not bit-deterministic run to run)
-    assert normwise(_np(g0["_rows"]), _np(grads["_rows"])) < 2e-3  # near-camera rows amplify the atomic-order noise
-    only = R.pose_backward(g, out, z["g_color"], z["g_depth"], z["g_opac"])
-    assert normwise(_np(only), _np(pose)) < 1e-3  # separate backward: atomic order differs (near-camera terms)
+    assert normwise(_np(g0["_rows"]), _np(grads["_rows"])) < 1e-6
 
 
 @pytest.mark.parametrize("seed", [0, 1])
@@ -545,12 +550,8 @@ def test_batch_optimizer_matches_batch_oracle():
     assert np.array_equal(_np(eng.touched).astype(bool), tun)
     ggpu = _np(eng.grads)[:, :59]
     assert not ggpu[~tun].any()
-    assert normwise(ggpu, gsum) < 1e-2  # near-camera Gaussians included (see the 2e-2 bar above)
-    near = np.zeros(len(rows64), bool)
-    for c in sc.cams:
-        z = rows64[:, :3] @ np.asarray(c["rot_cw"])[2] + np.asarray(c["trans_cw"])[2]
-        near |= (z > 0.01) & (z < 0.05)
-    assert normwise(ggpu[~near & tun], gsum[~near & tun]) < REL_TOL
+    for k, (a, b) in GROUPS.items():  # near-camera Gaussians included
+        assert normwise(ggpu[:, a:b], gsum[:, a:b]) < REL_TOL, k
     # the Adam step on the GPU's own gradients
     exp = rows64.copy()
     st = O.AdamState()
@@ -620,10 +621,10 @@ def test_photometric_refine_matches_reference(name):
     for n in (1, 5, 15):
         rot, trans, loss = OD.photometric_refine(g, t[f"{name}_image"], start, n_iters=n)
         rref, tref = t[f"{name}_{n}_rot"], t[f"{name}_{n}_trans"]
-        assert np.max(np.abs(rot - rref)) < 2e-5 * n, (n, rot, rref)
-        assert np.max(np.abs(trans - tref)) < 2e-5 * n, (n, trans, tref)
+        assert np.max(np.abs(rot - rref)) < 1e-6 * n, (n, rot, rref)
+        assert np.max(np.abs(trans - tref)) < 1e-6 * n, (n, trans, tref)
         lref = float(t[f"{name}_{n}_loss"])
-        assert abs(loss - lref) < 2e-3 * lref + 1e-5, (n, loss, lref)
+        assert abs(loss - lref) < REL_TOL * lref, (n, loss, lref)
     # the refinement converges toward the true pose (the image is the rendering at it)
     assert np.linalg.norm(trans - z["trans_cw"]) < np.linalg.norm(t[f"{name}_t0"] - z["trans_cw"])
 
@@ -705,10 +706,22 @@ def test_mapper_schedule_matches_reference():
     m.refine(1)
     assert added == [int(a) for a in z["added"]]
     ref = z["losses"]
-    assert abs(m.losses[0] - ref[0]) < REL_TOL * ref[0]
-    assert np.max(np.abs(np.array(m.losses) - ref) / ref) < 1e-2
-    assert np.array_equal(_np(m.adam.t)[:len(m.gmap)].astype(np.int64), z["adam_t"])
-    assert normwise(_np(m.gmap.rows())[:, :59], z["rows"]) < 5e-2
+    assert np.max(np.abs(np.array(m.losses) - ref) / ref) < REL_TOL
+    t = _np(m.adam.t)[:len(m.gmap)].astype(np.int64)
+    assert np.array_equal(t, z["adam_t"])
+    # The map after up to 7 Adam steps per Gaussian.  Adam moves every touched parameter by up to
+    # lr per step whatever |g| (its first step is lr * sign(g)), so a parameter whose reference
+    # gradient is at fp32 resolution can step the other way: the elementwise deviation is bounded
+    # by 2 lr t; measured, its median is ~1e-5..1e-3 of lr t per group and the 99th percentile
+    # <= 0.2 lr t (tools/parity_probe.py mapper_detail).
+    rows = _np(m.gmap.rows())[:, :59]
+    lr = O.lr_columns(m.lrs)[:59]
+    dev = np.abs(rows - z["rows"])
+    assert np.all(dev <= 2.0 * lr[None, :] * t[:, None] + 1e-6)
+    ratio = dev / np.maximum(lr[None, :] * np.maximum(t[:, None], 1), 1e-30)
+    for k, (a, b) in GROUPS.items():
+        assert np.median(ratio[:, a:b]) < 1e-2, k
+        assert np.quantile(ratio[:, a:b], 0.99) < 0.5, k
     snap = m.snapshot()
     assert snap is not m.gmap and len(snap) == len(m.gmap)
 
@@ -726,3 +739,57 @@ def test_mapping_loop_drains_queue_and_refines():
     M.mapping_loop(q, m)
     assert len(m.keyframes) == 2 and len(m.losses) == 3  # two submits + max(refine_rounds, 1) round
     q.join()
+
+
+def test_backward_bit_deterministic_at_benchmark_scale():
+    """T/test_rasterizer.py:153-162 (forward, backward and pose gradient bit-identical across
+    runs) on the headline scene, S2r 1M Gaussians at 1280x720, where every (tile, entry) of the
+    backward belongs to a near-plane Gaussian covering the whole image."""
+    import torch
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(1 << 20, 1280, 720, lidar=32)
+    cam = R.camera_from(sc.cams[0])
+    g = GaussianMap.from_rows(sc.rows)
+    rng = np.random.default_rng(3)
+    gc = torch.as_tensor(rng.standard_normal((720, 1280, 3)) * 1e-6, dtype=torch.float32, device="cuda")
+    runs = []
+    for _ in range(2):
+        out = R.forward(g, cam)
+        grads, touched, pose = R.backward(g, out, gc, with_pose=True)
+        runs.append((out.color.clone(), grads["_rows"].clone(), touched.clone(), pose.clone()))
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
+
+
+def test_engine_bit_deterministic():
+    """T/test_mapper.py:399-410: the same keyframes in the same order give bit-identical maps
+    and Adam state (graph-captured engine, fused chain + Adam)."""
+    import torch
+    from paper_2507_04004_b200 import mapper as M
+    from paper_2507_04004_b200 import rasterizer as R
+    from paper_2507_04004_b200 import scenes
+    from paper_2507_04004_b200.gaussians import GaussianMap
+    sc = scenes.scene_room(1 << 18, 640, 360, lidar=16, render_views=(0, 8, 16))
+    kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
+    states = []
+    for _ in range(2):
+        eng = M.MapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
+        eng.capture()
+        for k in (0, 1, 2, 2, 0, 1, 0):
+            eng.step(k)
+        torch.cuda.synchronize()
+        states.append(eng.save_state() + (torch.tensor(eng.loss_sum()),))
+    for a, b in zip(*states):
+        assert torch.equal(a, b)
+    # and through the Mapper (R/mapper.py:267-316): submit the same keyframe twice, seed 7
+    maps = []
+    for _ in range(2):
+        m = M.Mapper(M.MappingConfig(), seed=7)
+        for d in _mapper_keyframes()[:1] * 2:
+            cam = R.Camera(d["width"], d["height"], d["fx"], d["fy"], d["cx"], d["cy"], d["rot_cw"], d["trans_cw"])
+            m.submit(M.Keyframe(cam=cam, image=d["image"], sparse_depth=d["sparse"], points=d["points"],
+                                colors=d["colors"]))
+        maps.append(m.gmap.rows().clone())
+    assert torch.equal(maps[0], maps[1])
