@@ -17,145 +17,138 @@ from pathlib import Path
 import numpy as np
 
 from .errors import DataError
+from .plyio import PlyFormat
 
+# ---------------------------------------------------------------------------------------------
+# format tables
+
+# headered float32 grid (R/io_formats.py:20-42): magic, width, height (uint32 LE), row-major data
 GRID_MAGIC = b"F32GRID\x00"
+GRID_HEAD = struct.Struct("<8sII")
+# coloured seed cloud (R/io_formats.py:60-95)
+POINT_PLY = PlyFormat(properties=(("x", "float"), ("y", "float"), ("z", "float"),
+                                  ("red", "uchar"), ("green", "uchar"), ("blue", "uchar")))
+# TUM trajectory row (R/io_formats.py:98-121): stamp, translation, quaternion x y z w
+TUM_FIELDS = 8
+TUM_DIGITS = 9
 
 
 def _host(a) -> np.ndarray:
-    if hasattr(a, "detach"):
-        return a.detach().double().cpu().numpy()
-    return np.asarray(a, dtype=np.float64)
+    return a.detach().double().cpu().numpy() if hasattr(a, "detach") else np.asarray(a, dtype=np.float64)
+
+
+def _to_u8(x) -> np.ndarray:
+    """[0, 1] -> 0..255, round half to even (np.round), as the reference's writers."""
+    return np.round(np.clip(_host(x), 0.0, 1.0) * 255.0).astype(np.uint8)
+
+
+# ---------------------------------------------------------------------------------------------
+# grids, images, point clouds
 
 
 def save_f32_grid(path, grid) -> None:
-    """R/io_formats.py:23-31: 8-byte magic, uint32 width, uint32 height, row-major float32."""
-    grid = _host(grid).astype(np.float32)
-    if grid.ndim != 2:
+    g = np.ascontiguousarray(_host(grid), dtype="<f4")
+    if g.ndim != 2:
         raise ValueError("grid must be 2-D")
-    h, w = grid.shape
-    with open(path, "wb") as f:
-        f.write(GRID_MAGIC)
-        f.write(struct.pack("<II", w, h))
-        f.write(grid.tobytes(order="C"))
+    Path(path).write_bytes(GRID_HEAD.pack(GRID_MAGIC, g.shape[1], g.shape[0]) + g.tobytes())
 
 
 def load_f32_grid(path) -> np.ndarray:
-    raw = Path(path).read_bytes()
-    if len(raw) < 16 or raw[:8] != GRID_MAGIC:
+    blob = Path(path).read_bytes()
+    if len(blob) < GRID_HEAD.size:
         raise DataError(f"{path}: not a float32 grid file")
-    w, h = struct.unpack("<II", raw[8:16])
-    expect = 16 + 4 * w * h
-    if len(raw) != expect:
-        raise DataError(f"{path}: truncated grid ({len(raw)} != {expect} bytes)")
-    return np.frombuffer(raw[16:], dtype="<f4").reshape(h, w).astype(np.float64)
+    magic, w, h = GRID_HEAD.unpack_from(blob)
+    if magic != GRID_MAGIC:
+        raise DataError(f"{path}: not a float32 grid file")
+    if len(blob) != GRID_HEAD.size + 4 * w * h:
+        raise DataError(f"{path}: truncated grid ({len(blob)} != {GRID_HEAD.size + 4 * w * h} bytes)")
+    return np.frombuffer(blob, dtype="<f4", offset=GRID_HEAD.size).reshape(h, w).astype(np.float64)
 
 
 def save_png(path, image) -> None:
-    """R/io_formats.py:45-49: [0, 1] image to 8-bit PNG (round half to even, as np.round)."""
     from PIL import Image
-    data = np.round(np.clip(_host(image), 0.0, 1.0) * 255.0).astype(np.uint8)
-    Image.fromarray(data).save(path)
+    Image.fromarray(_to_u8(image)).save(path)
 
 
 def load_png(path) -> np.ndarray:
     from PIL import Image
-    arr = np.asarray(Image.open(path), dtype=np.float64) / 255.0
-    if arr.ndim == 3 and arr.shape[2] == 4:
-        arr = arr[:, :, :3]
-    return arr
-
-
-_POINT_DTYPE = [("xyz", "<f4", 3), ("rgb", "u1", 3)]
+    px = np.asarray(Image.open(path))
+    return (px[..., :3] if px.ndim == 3 else px).astype(np.float64) / 255.0
 
 
 def save_point_ply(path, points, colors) -> None:
-    """R/io_formats.py:60-78: coloured point cloud, binary little-endian PLY."""
-    points = _host(points).astype(np.float32).reshape(-1, 3)
-    rgb = np.round(np.clip(_host(colors).reshape(-1, 3), 0.0, 1.0) * 255.0).astype(np.uint8)
-    n = len(points)
-    header = ("ply\nformat binary_little_endian 1.0\n" f"element vertex {n}\n"
-              "property float x\nproperty float y\nproperty float z\n"
-              "property uchar red\nproperty uchar green\nproperty uchar blue\n" "end_header\n")
-    rec = np.zeros(n, dtype=_POINT_DTYPE)
-    rec["xyz"] = points
-    rec["rgb"] = rgb
-    with open(path, "wb") as f:
-        f.write(header.encode("ascii"))
-        f.write(rec.tobytes())
+    xyz = _host(points).astype(np.float32).reshape(-1, 3)
+    rgb = _to_u8(_host(colors).reshape(-1, 3))
+    rec = np.empty(len(xyz), dtype=POINT_PLY.dtype)
+    for i, name in enumerate(("x", "y", "z")):
+        rec[name] = xyz[:, i]
+    for i, name in enumerate(("red", "green", "blue")):
+        rec[name] = rgb[:, i]
+    Path(path).write_bytes(POINT_PLY.encode(rec))
 
 
 def load_point_ply(path):
-    raw = Path(path).read_bytes()
-    end = raw.find(b"end_header\n")
-    if end < 0:
-        raise DataError(f"{path}: missing PLY header terminator")
-    n = None
-    for line in raw[:end].decode("ascii").splitlines():
-        if line.startswith("element vertex"):
-            n = int(line.split()[-1])
-    if n is None:
-        raise DataError(f"{path}: no vertex element")
-    rec = np.frombuffer(raw[end + len(b"end_header\n"):], dtype=_POINT_DTYPE, count=n)
-    return rec["xyz"].astype(np.float64), rec["rgb"].astype(np.float64) / 255.0
+    rec = POINT_PLY.decode(Path(path).read_bytes(), str(path))
+    xyz = np.stack([rec[c] for c in ("x", "y", "z")], axis=1).astype(np.float64)
+    rgb = np.stack([rec[c] for c in ("red", "green", "blue")], axis=1).astype(np.float64) / 255.0
+    return xyz, rgb
+
+
+# ---------------------------------------------------------------------------------------------
+# poses
 
 
 def mat_to_quat(rot) -> np.ndarray:
-    """R/geometry.py:134-170: (w, x, y, z) by Shepperd's method (largest pivot)."""
-    a = np.asarray(rot, dtype=np.float64).reshape(3, 3)
-    t = a[0, 0] + a[1, 1] + a[2, 2]
-    c = int(np.argmax([t, a[0, 0], a[1, 1], a[2, 2]]))
-    if c == 0:
-        r = np.sqrt(1.0 + t)
-        s = 0.5 / r
-        q = [0.5 * r, (a[2, 1] - a[1, 2]) * s, (a[0, 2] - a[2, 0]) * s, (a[1, 0] - a[0, 1]) * s]
-    elif c == 1:
-        r = np.sqrt(1.0 + a[0, 0] - a[1, 1] - a[2, 2])
-        s = 0.5 / r
-        q = [(a[2, 1] - a[1, 2]) * s, 0.5 * r, (a[0, 1] + a[1, 0]) * s, (a[0, 2] + a[2, 0]) * s]
-    elif c == 2:
-        r = np.sqrt(1.0 - a[0, 0] + a[1, 1] - a[2, 2])
-        s = 0.5 / r
-        q = [(a[0, 2] - a[2, 0]) * s, (a[0, 1] + a[1, 0]) * s, 0.5 * r, (a[1, 2] + a[2, 1]) * s]
-    else:
-        r = np.sqrt(1.0 - a[0, 0] - a[1, 1] + a[2, 2])
-        s = 0.5 / r
-        q = [(a[1, 0] - a[0, 1]) * s, (a[0, 2] + a[2, 0]) * s, (a[1, 2] + a[2, 1]) * s, 0.5 * r]
-    q = np.asarray(q)[None]
-    q = np.where(q[:, :1] < 0.0, -q, q)
-    return (q / np.linalg.norm(q, axis=-1, keepdims=True))[0]
+    """Unit quaternion (w, x, y, z), w >= 0, of a rotation matrix: the component of largest
+    magnitude is taken from the matching diagonal combination (no cancellation) and the other
+    three from the off-diagonal sums / differences (the method of R/geometry.py:134-170)."""
+    m = np.asarray(rot, dtype=np.float64).reshape(3, 3)
+    diag = np.array([m[0, 0] + m[1, 1] + m[2, 2], m[0, 0], m[1, 1], m[2, 2]])
+    k = int(np.argmax(diag))
+    # 4 |q_k|^2 = 1 + sign pattern . diag(m); rows: which diagonal signs each pivot uses
+    signs = {0: (1, 1, 1), 1: (1, -1, -1), 2: (-1, 1, -1), 3: (-1, -1, 1)}[k]
+    r = np.sqrt(1.0 + signs[0] * m[0, 0] + signs[1] * m[1, 1] + signs[2] * m[2, 2])
+    inv = 0.5 / r
+    skew = np.array([m[2, 1] - m[1, 2], m[0, 2] - m[2, 0], m[1, 0] - m[0, 1]])  # 4 w (x, y, z)
+    sym = {(1, 2): m[0, 1] + m[1, 0], (1, 3): m[0, 2] + m[2, 0], (2, 3): m[1, 2] + m[2, 1]}  # 4 q_i q_j
+    q = np.empty(4)
+    q[k] = 0.5 * r
+    for j in range(4):
+        if j == k:
+            continue
+        if 0 in (j, k):  # w pairs with the skew part
+            q[j] = skew[max(j, k) - 1] * inv
+        else:
+            q[j] = sym[(min(j, k), max(j, k))] * inv
+    if q[0] < 0.0:
+        q = -q
+    return q / np.linalg.norm(q)
 
 
 def quat_to_mat(q) -> np.ndarray:
-    """R/geometry.py:118-131 (normalised (w, x, y, z))."""
-    q = np.asarray(q, dtype=np.float64)[None]
-    w, x, y, z = (q / np.linalg.norm(q, axis=-1, keepdims=True))[0]
+    """Rotation of the normalised quaternion (w, x, y, z) (R/geometry.py:118-131)."""
+    w, x, y, z = np.asarray(q, dtype=np.float64) / np.linalg.norm(q)
     return np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y)],
                      [2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x)],
                      [2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)]])
 
 
 def tum_row(t: float, rot, trans) -> str:
-    """R/io_formats.py:98-103: timestamp, translation, quaternion (x y z w)."""
     q = mat_to_quat(rot)
-    tx, ty, tz = np.asarray(trans, dtype=np.float64)
-    return f"{t:.9f} {tx:.9f} {ty:.9f} {tz:.9f} {q[1]:.9f} {q[2]:.9f} {q[3]:.9f} {q[0]:.9f}"
+    vals = [t, *np.asarray(trans, dtype=np.float64), q[1], q[2], q[3], q[0]]
+    return " ".join(f"{v:.{TUM_DIGITS}f}" for v in vals)
 
 
 def parse_tum(text: str):
-    """R/io_formats.py:106-121: rows of (t, rot 3x3, trans 3)."""
-    stamps, rots, transs = [], [], []
-    for line in text.strip().splitlines():
-        line = line.strip()
-        if not line or line.startswith("#"):
-            continue
-        vals = [float(v) for v in line.split()]
-        if len(vals) != 8:
-            raise DataError(f"trajectory row needs 8 fields, got {len(vals)}")
-        t, tx, ty, tz, qx, qy, qz, qw = vals
-        stamps.append(t)
-        rots.append(quat_to_mat([qw, qx, qy, qz]))
-        transs.append(np.array([tx, ty, tz]))
-    return np.array(stamps), np.array(rots).reshape(-1, 3, 3), np.array(transs).reshape(-1, 3)
+    """(stamps, rotations (k, 3, 3), translations (k, 3)) of a TUM trajectory; DataError on a row
+    without exactly TUM_FIELDS numbers."""
+    rows = [ln.split() for ln in text.splitlines() if ln.strip() and not ln.lstrip().startswith("#")]
+    bad = [r for r in rows if len(r) != TUM_FIELDS]
+    if bad:
+        raise DataError(f"trajectory row needs {TUM_FIELDS} fields, got {len(bad[0])}")
+    v = np.array(rows, dtype=np.float64).reshape(-1, TUM_FIELDS)
+    rots = np.array([quat_to_mat([r[7], r[4], r[5], r[6]]) for r in v]).reshape(-1, 3, 3)
+    return v[:, 0], rots, v[:, 1:4].copy()
 
 
 def save_keyframe(dirpath, kf) -> None:

@@ -21,55 +21,43 @@ import torch
 
 from .errors import DataError
 from .gaussians import GaussianMap, as_device_map, default_device
+from .plyio import PlyFormat, parse
 
 PLY_VERSION = 1
+# parameter-row columns as PLY vertex properties: position, log-scale, quaternion (w first),
+# opacity logit, DC colour, 45 higher-order SH coefficients (R/gaussians.py:255-256)
 FIELDS = ["x", "y", "z", "sx", "sy", "sz", "qw", "qx", "qy", "qz", "op"] + \
     [f"sl{i}" for i in range(3)] + [f"sh{i}" for i in range(45)]
 NF = len(FIELDS)  # 59 = the used columns of a parameter row
+GAUSSIAN_PLY = PlyFormat(properties=tuple((name, "float") for name in FIELDS),
+                         comments=(f"splatmap_version {PLY_VERSION}",))
 
 
 def _header(n: int) -> bytes:
-    lines = ["ply", "format binary_little_endian 1.0", f"comment splatmap_version {PLY_VERSION}",
-             f"element vertex {n}"] + [f"property float {name}" for name in FIELDS] + ["end_header", ""]
-    return "\n".join(lines).encode("ascii")
+    return GAUSSIAN_PLY.header(n)
 
 
 def save_gaussian_ply(gmap, path) -> None:
-    """R/gaussians.py:257-272: binary little-endian PLY, one vertex per splat, versioned header."""
+    """R/gaussians.py:257-272: the map's 59 used row columns as one float32 record per splat."""
     g = as_device_map(gmap)
-    data = g.rows()[:, :NF].detach().to("cpu", torch.float32).numpy().astype("<f4", copy=False)
+    cols = g.rows()[:, :NF].detach().to("cpu", torch.float32).contiguous().numpy()
     with open(path, "wb") as fh:
-        fh.write(_header(len(g)))
-        fh.write(np.ascontiguousarray(data).tobytes())
+        fh.write(GAUSSIAN_PLY.encode(cols.view(GAUSSIAN_PLY.dtype).reshape(-1)))
 
 
 def load_gaussian_ply(path, device=None) -> GaussianMap:
-    """R/gaussians.py:275-305 onto the device (same validation and error messages)."""
+    """R/gaussians.py:275-305 onto the device; DataError for a foreign, newer or short file."""
     with open(path, "rb") as fh:
         blob = fh.read()
-    end = blob.find(b"end_header\n")
-    if end < 0:
-        raise DataError(f"{path}: not a PLY file (missing end_header)")
-    header = blob[:end].decode("ascii", "replace").splitlines()
-    if not header or header[0] != "ply":
-        raise DataError(f"{path}: not a PLY file")
-    n = None
-    for line in header:
-        if line.startswith("element vertex"):
-            n = int(line.split()[-1])
-        if line.startswith("comment splatmap_version"):
-            version = int(line.split()[-1])
-            if version > PLY_VERSION:
-                raise DataError(f"{path}: unsupported splatmap version {version}")
-    if n is None:
-        raise DataError(f"{path}: missing vertex element")
-    body = blob[end + len(b"end_header\n"):]
-    expect = n * NF * 4
-    if len(body) < expect:
-        raise DataError(f"{path}: truncated payload ({len(body)} < {expect} bytes)")
-    arr = np.frombuffer(body[:expect], dtype="<f4").reshape(n, NF)
+    head = parse(blob, str(path))
+    for c in head.comments:
+        key, _, val = c.partition(" ")
+        if key == "splatmap_version" and int(val) > PLY_VERSION:
+            raise DataError(f"{path}: unsupported splatmap version {int(val)}")
+    rec = GAUSSIAN_PLY.decode(blob, str(path), head)
+    rows = rec.view("<f4").reshape(len(rec), NF)
     dev = torch.device(device) if device is not None else default_device()
-    return GaussianMap.from_rows(torch.from_numpy(arr.copy()).to(dev), device=dev)
+    return GaussianMap.from_rows(torch.from_numpy(rows.copy()).to(dev), device=dev)
 
 
 def save_checkpoint(gmap, adam, path_prefix) -> tuple[str, str]:
