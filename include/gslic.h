@@ -49,6 +49,7 @@ extern "C" {
                           color 3, depth 1), each a fixed-point pair (hi, lo), value = hi 2^-24 + lo 2^-64
                           (integer atomics: sums are bit-identical run to run) */
 #define GS_G2D_FIELDS 10
+#define GS_LOSS_RING 64 /* per-iteration losses kept by an engine workspace (gs_frame.loss) */
 #define GS_SPLAT 16    /* floats per 2D splat record: (mx, my, a, beta) (gamma, opacity, depth, qcut)
                           (r, g, b, 1 - opacity) (b, c, 0, 0); conic = (a, b, c), and the blend evaluates
                           q = a (dx + beta dy)^2 + gamma dy^2 with beta = b / a, gamma = (a c - b^2) / a */
@@ -153,7 +154,10 @@ typedef struct gs_frame {
     float *g_depth;          /* H x W      xi dLd/ddepth */
     float *g_opac;           /* H x W      xi dLd/dopacity */
     double *loss_parts;      /* per-block partial sums */
-    double *loss;            /* 8: total, photometric, depth, dssim, running sum (GS_LOSS_ACCUMULATE) */
+    double *loss;            /* 8 + GS_LOSS_RING: total, photometric, depth, dssim, running sum
+                                (GS_LOSS_ACCUMULATE), -, ring position, -, then the per-iteration loss
+                                ring: with GS_LOSS_ACCUMULATE iteration i writes its total to
+                                loss[8 + i % GS_LOSS_RING] (i counted from the workspace's layout) */
     int64_t loss_blocks;
     int64_t *pose_acc;       /* 12: fixed-point accumulators of the pose gradient (gs_chain_pose) */
 } gs_frame;

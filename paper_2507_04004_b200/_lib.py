@@ -20,6 +20,7 @@ GS_NPARAM = 59
 GS_TILE = 16
 GS_G2D = 20  # int64 words per screen-space gradient row (10 fixed-point (hi, lo) fields)
 GS_G2D_FIELDS = 10
+GS_LOSS_RING = 64  # per-iteration loss ring of an engine workspace (gs_frame.loss[8:])
 GS_SPLAT = 16  # floats per 2D splat record
 CNT_ACTIVE, CNT_ENTRIES, CNT_TOUCHED, CNT_OVERFLOW, CNT_ENTRIES_EFF = 0, 1, 2, 3, 4
 GS_CNT_SLOTS = 16

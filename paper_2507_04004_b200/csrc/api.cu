@@ -110,7 +110,9 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.loss_blocks = loss_parts_needed(w, h);
     // loss partials (3 doubles per block) followed by the two 11-tap reflection tables
     f.loss_parts = c.take<double>(3 * f.loss_blocks + (int64_t)11 * (w + h) + 1);
-    f.loss = c.take<double>(8);  // total, photometric, depth, dssim, running sum (GS_LOSS_ACCUMULATE)
+    // total, photometric, depth, dssim, running sum, -, ring position, -, then the per-iteration
+    // loss ring (GS_LOSS_ACCUMULATE)
+    f.loss = c.take<double>(8 + GS_LOSS_RING);
     f.pose_acc = c.take<int64_t>(16);
 }
 

@@ -505,6 +505,11 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
         // capacity is a no-op (rendered nothing, no gradient, no Adam step) and is re-run by the
         // engine after re-laying out the workspace, so it is not counted here
         if (accumulate && !f.counters[GS_CNT_OVERFLOW]) f.loss[4] += lc + (double)xi * ld;
+        if (accumulate) {  // per-iteration ring: the host reads iteration i's loss at slot i % RING
+            const long long pos = (long long)f.loss[6];
+            f.loss[8 + pos % GS_LOSS_RING] = lc + (double)xi * ld;
+            f.loss[6] = (double)(pos + 1);
+        }
         int *stamp = reinterpret_cast<int *>(tab_stamp);
         stamp[0] = (f.width << 16) + f.height;
         stamp[1] = ~((f.width << 16) + f.height);

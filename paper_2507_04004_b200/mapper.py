@@ -154,6 +154,31 @@ class HostKeyframes:
             ev.record(cs)
         return ev
 
+    def replay_slot(self, k: int) -> int:
+        """Keyframe k uploaded synchronously into a slot of its own (the re-run of an iteration
+        whose streaming slot may have been refilled); returns the device gs_view pointer."""
+        if not hasattr(self, "_replay"):
+            sl = self.slots[0]
+            self._replay = {key: torch.empty_like(t) for key, t in sl.items()}
+            self._replay_views = []
+            for kk in range(len(self.img)):
+                v = _lib.GsView.from_buffer_copy(bytes(self.views[kk][0].numpy()))
+                v.target, v.lidar_idx, v.lidar_z = (self._replay["img"].data_ptr(), self._replay["idx"].data_ptr(),
+                                                    self._replay["z"].data_ptr())
+                self._replay_views.append(torch.frombuffer(bytearray(bytes(memoryview(v).cast("B"))),
+                                                           dtype=torch.uint8).pin_memory())
+        r, kk = self._replay, self.idx[k].numel()
+        if self.img[k].dtype == torch.uint8:
+            r["u8"].copy_(self.img[k])
+            call("gs_decode_u8", r["u8"].data_ptr(), r["img"].data_ptr(), r["img"].numel(), stream_ptr())
+        else:
+            r["img"].copy_(self.img[k])
+        if kk:
+            r["idx"][:kk].copy_(self.idx[k])
+            r["z"][:kk].copy_(self.z[k])
+        r["view"].copy_(self._replay_views[k])
+        return r["view"].data_ptr()
+
     def stream(self, order, body, use_cur: bool = True) -> None:
         """For j, k in enumerate(order): keyframe k lands in a slot, then body(j, k, view_ptr) runs
         the iteration on the current stream (view_ptr: the slot's device gs_view; copied into
@@ -211,10 +236,12 @@ class MapOptimizer:
         self.ws = self._workspace(int(emax * headroom) + 4096)
         self.graph = None
         self.graphs: dict = {}
-        self._ring = [torch.zeros(8, dtype=torch.int32).pin_memory() for _ in range(4)]
-        self._events = [None] * 4
+        # per-step counters read back asynchronously: (event, pinned counters, how to re-run it)
+        self._ring = [torch.zeros(8, dtype=torch.int32).pin_memory() for _ in range(self.RING)]
+        self._pending: list = []
         self._steps = 0
-        self._grow = False
+        self.replayed = 0  # iterations re-run after an entry-capacity overflow
+        self._dev_iter = 0  # GS_LOSS_ACCUMULATE iterations run on this workspace (its loss ring position)
         import os
         self.overlap_parts = int(os.environ.get("GSLIC_OVERLAP_PARTS", "0"))
         self._side = torch.cuda.Stream(device=self.dev)
@@ -281,37 +308,67 @@ class MapOptimizer:
             self.graphs[view_ptr] = gr
         return gr
 
-    def step(self, k: int) -> None:
-        self._check()
+    RING = 8  # counter snapshots in flight (>= LAG + 2)
+    LAG = 2  # steps between an iteration and the host's look at its counters (no per-step sync)
+
+    def _run_view(self, view_ptr: int) -> None:
         if self.graph is not None:
-            self._graph_for(self.views[k].ptr).replay()
+            self._graph_for(view_ptr).replay()
         else:
-            self.cur.copy_(self.views[k].buf)
-            self._launch()
-        slot = self._steps % 4
-        self._ring[slot].copy_(self.ws.counters[:8], non_blocking=True)
+            self._launch(view_ptr)
+
+    def step(self, k: int) -> None:
+        self._check(self.LAG)
+        vp = self.views[k].ptr
+        self._run_view(vp)
+        self._record(lambda: self._run_view(vp))
+
+    def _record(self, rerun, loss_slot: int | None = None) -> None:
+        """Snapshot this iteration's counters (async D2H) for the lagged capacity check; with
+        loss_slot, also read its loss back into pinned memory (run_host)."""
+        ring = self._ring[self._steps % self.RING]
+        ring.copy_(self.ws.counters[:8], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        self._events[slot] = ev
+        if loss_slot is not None:
+            self._read_loss(ev, loss_slot)
+        self._pending.append((ev, ring, rerun, loss_slot))
         self._steps += 1
+        self._dev_iter += 1
 
-    def _check(self) -> None:
-        """Look at the counters of the step before last (already finished in practice)."""
-        if self._steps < 2:
-            return
-        slot = (self._steps - 2) % 4
-        self._events[slot].synchronize()
-        cnt = self._ring[slot]
-        if int(cnt[_lib.CNT_OVERFLOW]):
-            raise DataError(f"entry capacity {self.ws.capacity} overflowed (E={int(cnt[_lib.CNT_ENTRIES])}); "
-                            "raise MapOptimizer headroom")
-        if int(cnt[_lib.CNT_ENTRIES]) > 0.9 * self.ws.capacity:
-            torch.cuda.current_stream().synchronize()
-            old = self.ws
-            self.ws = self._workspace(int(int(cnt[_lib.CNT_ENTRIES]) * self.headroom))
-            self.ws.loss[4:5].copy_(old.loss[4:5])  # the running loss sum moves along
-            if self.graph is not None:
-                self.capture()  # (the per-view graphs are re-captured on first use)
+    def _regrow(self, entries: int) -> None:
+        torch.cuda.synchronize(self.dev)  # no kernel or copy still reads the old workspace
+        old = self.ws
+        self.ws = self._workspace(int(entries * self.headroom) + 4096)
+        self.ws.loss[4:5].copy_(old.loss[4:5])  # the running loss sum moves along
+        self._dev_iter = 0  # the new workspace's loss ring starts over
+        if self.graph is not None:
+            self.capture()  # (the per-view graphs are re-captured on first use)
+
+    def _check(self, keep: int) -> None:
+        """Counters of the iterations older than the last `keep` (finished in practice, so the
+        event waits are free).  An iteration whose binning overflowed the entry capacity did
+        nothing (background render, no gradient, no Adam step, loss not accumulated: the device
+        kernels no-op on GS_CNT_OVERFLOW); the workspace is re-laid out and that iteration re-run
+        at once -- after the `keep` iterations queued behind it, so the map sees it that much
+        later (the only deviation from the reference's order, and only on overflow).  A step near
+        capacity grows the workspace before it overflows."""
+        while len(self._pending) > keep:
+            ev, ring, rerun, loss_slot = self._pending.pop(0)
+            ev.synchronize()
+            over, entries = int(ring[_lib.CNT_OVERFLOW]), int(ring[_lib.CNT_ENTRIES])
+            if over:
+                self._regrow(entries)
+                self.replayed += 1
+                rerun()
+                self._record(rerun, loss_slot)
+            elif entries > 0.9 * self.ws.capacity:
+                self._regrow(entries)
+
+    def finish(self) -> None:
+        """Check every queued iteration (re-running any that overflowed); returns when all of
+        them have completed."""
+        self._check(0)
 
     PHASES = ("preprocess", "bin", "render_fwd", "loss", "render_bwd", "chain_adam")
 
@@ -337,6 +394,7 @@ class MapOptimizer:
         ev[5].record()
         self._chain_adam()
         ev[6].record()
+        self._dev_iter += 1
         ev[6].synchronize()
         return {p: ev[i].elapsed_time(ev[i + 1]) for i, p in enumerate(self.PHASES)}
 
@@ -346,35 +404,43 @@ class MapOptimizer:
         on a copy stream while iteration j runs."""
         self.host = HostKeyframes(keyframes, self.W, self.H, self.cur, self.dev)
         self.h2d_bytes, self.d2h_bytes = self.host.h2d_bytes, 8
-        self._h_loss = torch.zeros(1024, dtype=torch.float64).pin_memory()
+        self._h_loss = torch.zeros(self.LOSS_RING, dtype=torch.float64).pin_memory()
         self._host_steps = 0
 
     def run_host(self, order) -> None:
         """Map-optimisation iterations over host keyframes `order` (R/mapper.py:242-256 samples
         the keyframe order up front): keyframe j+1 is uploaded on a copy stream while iteration j
         runs; each iteration's loss is read back into pinned host memory (D2H)."""
+        cs = self.host.copy_stream
+
         def body(j, k, view_ptr):
-            self._check()
-            if self.graph is not None:
-                self._graph_for(view_ptr).replay()
-            else:
-                self._launch(view_ptr)
-            # the loss read-back rides on the copy stream: the next iteration does not queue behind it
-            done = torch.cuda.Event()
-            done.record()
-            cs = self.host.copy_stream
-            cs.wait_event(done)
-            with torch.cuda.stream(cs):
-                self._h_loss[self._host_steps % 1024].copy_(self.ws.loss[0], non_blocking=True)
+            self._check(self.LAG)
+            self._run_view(view_ptr)
+            h = self._host_steps % self.LOSS_RING
             self._host_steps += 1
-            s = self._steps % 4
-            self._ring[s].copy_(self.ws.counters[:8], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record()
-            self._events[s] = ev
-            self._steps += 1
+            # an overflowed iteration is re-run from a dedicated slot (its streaming slot may have
+            # been refilled by then) and its loss read again
+            self._record(lambda: self._rerun_host(k, h), loss_slot=h)
 
         self.host.stream(order, body, use_cur=False)
+
+    LOSS_RING = 1024
+
+    def _read_loss(self, ev, h: int) -> None:
+        """D2H of the iteration's loss (device ring slot, written by the loss kernel itself) into
+        pinned slot h, on the copy stream once the iteration's event has fired: no kernel and no
+        main-stream work per iteration.  The device ring holds GS_LOSS_RING iterations, far more
+        than the copy stream ever lags (the host keyframe slots bound the run-ahead to
+        HostKeyframes.NSLOT iterations)."""
+        pos = self._dev_iter % _lib.GS_LOSS_RING
+        cs = self.host.copy_stream
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            self._h_loss[h].copy_(self.ws.loss[8 + pos], non_blocking=True)
+
+    def _rerun_host(self, k: int, h: int) -> None:
+        torch.cuda.synchronize(self.dev)
+        self._run_view(self.host.replay_slot(k))
 
     def step_host(self, k: int, slot: int = 0) -> None:
         """One iteration on host keyframe k (no prefetch): run_host([k])."""
@@ -409,7 +475,9 @@ _ENGINES_LOCK = threading.Lock()
 
 
 def _engine_for(gmap, keyframes, adam, lrs, cfg) -> MapOptimizer:
-    key = (id(gmap), id(keyframes), len(keyframes), len(gmap), id(adam))
+    # keyed on the identity of every keyframe (a keyframe replaced in place gets a new engine,
+    # whose device views hold its image and camera), the map, its size and the Adam state
+    key = (id(gmap), tuple(id(kf) for kf in keyframes), len(gmap), id(adam))
     with _ENGINES_LOCK:
         eng = _ENGINES.get(key)
     if eng is None or eng.g is not gmap:
@@ -420,6 +488,12 @@ def _engine_for(gmap, keyframes, adam, lrs, cfg) -> MapOptimizer:
     eng.lr = lr_columns(lrs, eng.dev)
     eng.lam, eng.xi = float(cfg.lam), float(cfg.xi)
     return eng
+
+
+def release_engines() -> None:
+    """Drop the cached optimize_map engine (its workspace and device keyframes)."""
+    with _ENGINES_LOCK:
+        _ENGINES.clear()
 
 
 def optimize_map(gmap, keyframes, cfg: MappingConfig, rng, adam: AdamState, lrs: dict,
@@ -438,6 +512,7 @@ def optimize_map(gmap, keyframes, cfg: MappingConfig, rng, adam: AdamState, lrs:
     start.record()
     for i in order:
         eng.step(int(i))
+    eng.finish()  # every iteration checked (and re-run on an entry-capacity overflow)
     end.record()
     total = eng.loss_sum()
     if timing is not None:
