@@ -29,6 +29,11 @@ GS_PP_LAZY_SH = 1  # gs_preprocess_ex flag of the iteration engine (colours only
 GS_LOSS_TABLES_READY, GS_LOSS_ACCUMULATE, GS_LOSS_DEPTH_GRADS_ZERO = 1, 2, 4  # gs_loss_ex flags
 GS_BWD_ROWS_ZERO, GS_BWD_CLEAR_DEPTH_GRADS = 1, 2  # gs_render_bwd_ex flags
 
+# Set by dropin.install: the reference-shaped entry points then return numpy arrays for every
+# map (the reference's callers do numpy arithmetic on them, R/cli.py:153-159, R/apps.py:208-223),
+# not only for reference-typed (numpy) maps
+HOST_ARRAYS = False
+
 P = ctypes.c_void_p
 i32 = ctypes.c_int32
 i64 = ctypes.c_int64

@@ -182,9 +182,20 @@ def struct_to_device(s, device) -> torch.Tensor:
     return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
 
 
+def _host_dict(d: dict) -> dict:
+    return {k: (v.double() if v.is_floating_point() else v).cpu().numpy() for k, v in d.items()}
+
+
 def project(gmap, rot_cw, trans_cw, intrinsics) -> dict:
-    """R/gaussians.py:180-215 on the device; returns the reference's record dict."""
-    g = as_device_map(gmap)
+    """R/gaussians.py:180-215 on the device; returns the reference's record dict (numpy arrays for
+    a reference-typed map, device tensors for a device map)."""
+    if not isinstance(gmap, GaussianMap) or _lib.HOST_ARRAYS:
+        host_mode, _lib.HOST_ARRAYS = _lib.HOST_ARRAYS, False
+        try:
+            return _host_dict(project(as_device_map(gmap), rot_cw, trans_cw, intrinsics))
+        finally:
+            _lib.HOST_ARRAYS = host_mode
+    g = gmap
     n = len(g)
     dev = g.device
     cam_buf = struct_to_device(camera_struct(rot_cw, trans_cw, intrinsics), dev)
@@ -201,7 +212,10 @@ def project(gmap, rot_cw, trans_cw, intrinsics) -> dict:
 
 
 def eval_sh(sh_low, sh_high, dirs):
-    """R/gaussians.py:102-111: returns (colors, preclamp) on the device."""
+    """R/gaussians.py:102-111: returns (colors, preclamp) -- numpy for numpy inputs."""
+    if not isinstance(dirs, torch.Tensor):
+        col, pre = eval_sh(sh_low, sh_high, _as_f32(dirs, default_device()))
+        return col.double().cpu().numpy(), pre.double().cpu().numpy()
     dev = default_device()
     sl = _as_f32(sh_low, dev).reshape(-1, 3).contiguous()
     sh = _as_f32(sh_high, dev).reshape(-1, 45).contiguous()

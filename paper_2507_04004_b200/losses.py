@@ -8,6 +8,9 @@ runs as one fused L1 + D-SSIM kernel with the exact mirror-padding adjoint; the 
 
 from __future__ import annotations
 
+import threading
+
+import numpy as np
 import torch
 
 from ._lib import call
@@ -21,16 +24,21 @@ C1 = 0.01 ** 2
 C2 = 0.03 ** 2
 GUARD = 1e-6
 
-_WS: dict = {}
+# one loss workspace per (thread, image size): the entry points are re-entrant across threads
+# (tracker and mapper, R/cli.py:298-344) and do not allocate after the first call of a size
+_TLS = threading.local()
 
 
-def _loss_workspace(h: int, w: int, device) -> Workspace:
-    key = (h, w, str(device))
-    ws = _WS.get(key)
-    if ws is None:
-        ws = Workspace(0, w, h, 0, device)
-        _WS[key] = ws
-    return ws
+def _workspace(h: int, w: int, dev) -> tuple:
+    cache = getattr(_TLS, "ws", None)
+    if cache is None:
+        cache = _TLS.ws = {}
+    key = (h, w, str(dev))
+    if key not in cache:
+        cam = Camera(w, h, 1.0, 1.0, 0.0, 0.0, np.eye(3), np.zeros(3))
+        cache[key] = (Workspace(0, w, h, 0, dev), DeviceView(cam, target=np.zeros((h, w, 3)),
+                                                                sparse_depth=np.zeros((h, w)), device=dev))
+    return cache[key]
 
 
 def frame_loss(ws: Workspace, view: DeviceView, lam: float, xi: float) -> None:
@@ -41,36 +49,47 @@ def frame_loss(ws: Workspace, view: DeviceView, lam: float, xi: float) -> None:
 def _run(color, depth, opac, target, sparse_depth, lam, xi):
     dev = default_device()
     c = _f32(color, dev)
-    h, w = int(c.shape[0]), int(c.shape[1])
     if c.ndim != 3 or c.shape[2] != 3:
         raise DomainError("colour images must be (H, W, 3)")
-    ws = Workspace(0, w, h, 0, dev)
+    h, w = int(c.shape[0]), int(c.shape[1])
+    ws, view = _workspace(h, w, dev)
     ws.color.copy_(c)
-    ws.depth.copy_(_f32(depth, dev).reshape(h, w) if depth is not None else torch.zeros((h, w), device=dev))
-    ws.opacity.copy_(_f32(opac, dev).reshape(h, w) if opac is not None else torch.zeros((h, w), device=dev))
-    cam = Camera(w, h, 1.0, 1.0, 0.0, 0.0, [[1, 0, 0], [0, 1, 0], [0, 0, 1]], [0, 0, 0])
-    sd = sparse_depth if sparse_depth is not None else torch.zeros((h, w), device=dev)
-    view = DeviceView(cam, target=target, sparse_depth=sd, device=dev)
+    if depth is None:
+        ws.depth.zero_()
+    else:
+        ws.depth.copy_(_f32(depth, dev).reshape(h, w))
+    if opac is None:
+        ws.opacity.zero_()
+    else:
+        ws.opacity.copy_(_f32(opac, dev).reshape(h, w))
+    view.set_supervision(target, sparse_depth)
     frame_loss(ws, view, lam, xi)
     return ws
+
+
+def _out(host: bool, *grads):
+    """Copies of the gradient images: numpy (float64) for numpy inputs, as the reference."""
+    if host:
+        return tuple(g.double().cpu().numpy() for g in grads)
+    return tuple(g.clone() for g in grads)
 
 
 def mapping_loss(color, depth, opac, target_color, sparse_depth, lam: float, xi: float):
     """R/losses.py:157-161: L = Lc + xi Ld; returns (L, gC, xi gD, xi gO)."""
     ws = _run(color, depth, opac, target_color, sparse_depth, lam, xi)
-    return float(ws.loss[0].item()), ws.g_color.clone(), ws.g_depth.clone(), ws.g_opac.clone()
+    return (float(ws.loss[0].item()),) + _out(not isinstance(color, torch.Tensor), ws.g_color, ws.g_depth, ws.g_opac)
 
 
 def photometric_loss(rendered, target, lam: float):
     """R/losses.py:122-130: (1-lam) L1 + lam D-SSIM and its gradient."""
     ws = _run(rendered, None, None, target, None, lam, 0.0)
-    return float(ws.loss[1].item()), ws.g_color.clone()
+    return (float(ws.loss[1].item()),) + _out(not isinstance(rendered, torch.Tensor), ws.g_color)
 
 
 def dssim_and_grad(rendered, target):
     """R/losses.py:89-119: (1 - SSIM)/2 and its exact gradient."""
     ws = _run(rendered, None, None, target, None, 1.0, 0.0)
-    return float(ws.loss[3].item()), ws.g_color.clone()
+    return (float(ws.loss[3].item()),) + _out(not isinstance(rendered, torch.Tensor), ws.g_color)
 
 
 def depth_ratio_loss(depth, opac, sparse_depth, guard: float = GUARD):
@@ -82,4 +101,4 @@ def depth_ratio_loss(depth, opac, sparse_depth, guard: float = GUARD):
     h, w = int(d.shape[0]), int(d.shape[1])
     zeros = torch.zeros((h, w, 3), device=dev)
     ws = _run(zeros, d, opac, zeros, sparse_depth, 0.0, 1.0)
-    return float(ws.loss[2].item()), ws.g_depth.clone(), ws.g_opac.clone()
+    return (float(ws.loss[2].item()),) + _out(not isinstance(depth, torch.Tensor), ws.g_depth, ws.g_opac)

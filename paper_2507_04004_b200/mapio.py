@@ -68,7 +68,7 @@ def save_checkpoint(gmap, adam, path_prefix) -> tuple[str, str]:
     adam.ensure(g)
     n = len(g)
     np.savez(st, version=PLY_VERSION, n=n, m=adam.m_rows[:n, :NF].cpu().numpy(),
-             v=adam.v_rows[:n, :NF].cpu().numpy(), t=adam.t[:n].cpu().numpy())
+             v=adam.v_rows[:n, :NF].cpu().numpy(), t=adam.t_dev[:n].cpu().numpy())
     return ply, st
 
 
@@ -87,5 +87,5 @@ def load_checkpoint(path_prefix, device=None):
     adam.ensure(g)
     adam.m_rows[:n, :NF] = torch.as_tensor(z["m"], device=g.device)
     adam.v_rows[:n, :NF] = torch.as_tensor(z["v"], device=g.device)
-    adam.t[:n] = torch.as_tensor(z["t"], device=g.device).to(adam.t.dtype)
+    adam.t_dev[:n] = torch.as_tensor(z["t"], device=g.device).to(adam.t_dev.dtype)
     return g, adam

@@ -273,7 +273,7 @@ class MapOptimizer:
         f, s = self.ws.fptr, stream_ptr()
         cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         args = (self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
-                self.adam.t.data_ptr(), cur, self.lr.data_ptr())
+                self.adam.t_dev.data_ptr(), cur, self.lr.data_ptr())
         P = self.overlap_parts
         if P <= 1:
             call("gs_chain_adam", f, *args, s)
@@ -449,11 +449,11 @@ class MapOptimizer:
     def save_state(self) -> tuple:
         """Device copies of the optimised state (parameter rows, Adam m, v, t)."""
         a = self.adam
-        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t))
+        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t_dev))
 
     def restore_state(self, state: tuple) -> None:
         a = self.adam
-        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t), state):
+        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t_dev), state):
             dst.copy_(src)
 
     def loss_sum(self, reset: bool = True) -> float:
@@ -496,12 +496,46 @@ def release_engines() -> None:
         _ENGINES.clear()
 
 
+def _write_back(ref_map, rows: torch.Tensor, base: torch.Tensor) -> None:
+    """Apply a device map's change since `base` to a reference-typed (numpy) map in place: the
+    float64 difference of two fp32 rows is exact, so untouched rows are left bit-identical and
+    touched ones move by exactly the device's step."""
+    delta = rows[:, :59].double() - base[:, :59].double()
+    idx = torch.nonzero(delta.abs().amax(dim=1) > 0, as_tuple=True)[0]
+    d = delta[idx].cpu().numpy()
+    ii = idx.cpu().numpy()
+    from .gaussians import NAMES, SLICES
+    for name in NAMES:
+        a, b = SLICES[name]
+        arr = getattr(ref_map, name)
+        arr[ii] += d[:, a:b].reshape((len(ii),) + arr.shape[1:])
+
+
+def _append(gmap, new: GaussianMap) -> None:
+    """gmap.append(new) for a device map, or the same rows as a map of the caller's own type."""
+    if isinstance(gmap, GaussianMap):
+        gmap.append(new)
+        return
+    r = new.rows()[:, :59].double().cpu().numpy()
+    n = len(r)
+    gmap.append(type(gmap)(pos=r[:, 0:3], log_scale=r[:, 3:6], quat=r[:, 6:10], opacity_logit=r[:, 10],
+                           sh_low=r[:, 11:14], sh_high=r[:, 14:59].reshape(n, 15, 3)))
+
+
 def optimize_map(gmap, keyframes, cfg: MappingConfig, rng, adam: AdamState, lrs: dict,
                  timing: dict | None = None) -> float:
     """R/mapper.py:233-264: sample min(K, #kf) keyframes without replacement, shuffle, and run
-    one descent step (fwd -> loss -> bwd -> sparse Adam) on each; returns the mean loss."""
+    one descent step (fwd -> loss -> bwd -> sparse Adam) on each; returns the mean loss.  A
+    reference-typed (numpy) map is optimised on a device copy and updated in place at the end."""
     if len(gmap) == 0:
         raise DataError("map not initialized")
+    if not isinstance(gmap, GaussianMap):
+        dev_map = as_device_map(gmap)
+        base = dev_map.rows().clone()
+        loss = optimize_map(dev_map, keyframes, cfg, rng, adam, lrs, timing)
+        _write_back(gmap, dev_map.rows(), base)
+        adam.host = True
+        return loss
     m = min(cfg.k_keyframes, len(keyframes))
     order = rng.choice(len(keyframes), size=m, replace=False)
     rng.shuffle(order)
@@ -621,7 +655,7 @@ def init_map(gmap: GaussianMap, kf: Keyframe) -> int:
     if len(gmap):
         raise DataError("map already initialized")
     _, _, _, _, z, _, _, pts = _project(kf.points, kf.cam)
-    gmap.append(_init_rows(pts, kf.colors, z, camera_from(kf.cam).fx, gmap.device))
+    _append(gmap, _init_rows(pts, kf.colors, z, camera_from(kf.cam).fx, pts.device))
     return len(pts)
 
 
@@ -636,8 +670,8 @@ def expand_map(gmap: GaussianMap, kf: Keyframe, tau: float) -> int:
     nf = int(fresh.sum())
     if nf == 0:
         return 0
-    cols = torch.as_tensor(kf.colors, dtype=torch.float32, device=gmap.device).reshape(-1, 3)
-    gmap.append(_init_rows(pts[fresh], cols[fresh], z[fresh], camera_from(kf.cam).fx, gmap.device))
+    cols = torch.as_tensor(kf.colors, dtype=torch.float32, device=pts.device).reshape(-1, 3)
+    _append(gmap, _init_rows(pts[fresh], cols[fresh], z[fresh], camera_from(kf.cam).fx, pts.device))
     return nf
 
 

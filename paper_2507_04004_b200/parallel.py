@@ -129,11 +129,11 @@ class BatchMapOptimizer:
 
     def save_state(self) -> tuple:
         a = self.adam
-        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t))
+        return tuple(t.clone() for t in (self.g.data, a.m_rows, a.v_rows, a.t_dev))
 
     def restore_state(self, state: tuple) -> None:
         a = self.adam
-        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t), state):
+        for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t_dev), state):
             dst.copy_(src)
 
     def _finish(self) -> None:
@@ -142,5 +142,5 @@ class BatchMapOptimizer:
         else:
             allreduce_grads(self.grads, self.touched, self.group)
         call("gs_adam", self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
-             self.adam.t.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), len(self.g),
+             self.adam.t_dev.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), len(self.g),
              self.lr.data_ptr(), stream_ptr())

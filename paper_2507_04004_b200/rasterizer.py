@@ -114,6 +114,22 @@ class DeviceView:
     def ptr(self) -> int:
         return self.buf.data_ptr()
 
+    def set_supervision(self, target, sparse_depth) -> None:
+        """Overwrite the view's target image and LiDAR returns in place (same image size; a
+        view built with both), recompacting the K-list on the device."""
+        h, w = int(self.cam.height), int(self.cam.width)
+        if target is None:
+            self.target.zero_()
+        else:
+            self.target.copy_(_f32(target, self.device).reshape(h, w, 3))
+        if sparse_depth is None:
+            self.sparse.zero_()
+        else:
+            self.sparse.copy_(_f32(sparse_depth, self.device).reshape(h, w))
+        k_ptr = self.buf.data_ptr() + _lib.GsView.lidar_k.offset
+        call("gs_lidar_compact", self.sparse.data_ptr(), w, h, self.lidar_idx.data_ptr(), self.lidar_z.data_ptr(),
+             k_ptr, stream_ptr())
+
 
 def _f32(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
@@ -230,8 +246,44 @@ def _bin_frame(g: GaussianMap, view: DeviceView, cull: bool, ws: Workspace | Non
     raise DataError("tile binning kept overflowing its entry capacity")
 
 
+def is_host_map(gmap) -> bool:
+    """A reference-typed map (numpy attribute arrays, R/gaussians.py:118-153) rather than a device
+    GaussianMap: the reference-shaped entry points then return numpy arrays, as the reference."""
+    return not isinstance(gmap, GaussianMap)
+
+
+def _to_host(x):
+    """Device tensor -> numpy (float64 for floating point), recursively through dicts."""
+    if isinstance(x, dict):
+        return {k: _to_host(v) for k, v in x.items()}
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.is_floating_point():
+            t = t.double()
+        return t.cpu().numpy()
+    return x
+
+
+def _view_dirs(g: GaussianMap, cam: Camera):
+    """R/rasterizer.py:447-452 preamble: camera->Gaussian directions, their norms (< 1e-12 -> 1)
+    and the pre-clamp SH colours."""
+    from .gaussians import eval_sh
+    c = torch.as_tensor(np.asarray(cam.center(), dtype=np.float32), device=g.device)
+    u = g.pos - c
+    nrm = torch.linalg.norm(u, dim=1, keepdim=True)
+    nrm = torch.where(nrm < 1e-12, torch.ones_like(nrm), nrm)
+    dirs = u / nrm
+    _, pre = eval_sh(g.sh_low, g.sh_high, dirs)
+    return dirs, nrm, pre
+
+
 def forward(gmap, cam, cull: bool = True, early_stop: bool = True) -> RenderOutput:
-    """R/rasterizer.py:442-484: render colour, depth (sum z w), opacity, transmittance, n_contrib."""
+    """R/rasterizer.py:442-484: render colour, depth (sum z w), opacity, transmittance, n_contrib.
+    The reference's ctx keys are all present (R/rasterizer.py:479-483).  A device GaussianMap gives
+    CUDA tensors; a reference-typed numpy map gives numpy arrays (float64 images, int64 entry
+    lists), so reference callers' numpy code (R/cli.py:153-159, R/mapper.py:218-230,
+    R/apps.py:208-223) runs unchanged."""
+    host = is_host_map(gmap) or _lib.HOST_ARRAYS
     g = as_device_map(gmap)
     cam = camera_from(cam)
     view = DeviceView(cam, device=g.device)
@@ -241,11 +293,19 @@ def forward(gmap, cam, cull: bool = True, early_stop: bool = True) -> RenderOutp
     n = len(g)
     s2 = ws.splat2d
     proj = {"mean2d": s2[:, 0:2], "conic": s2[:, [2, 12, 13]], "depth": s2[:, 6], "valid": ws.valid.bool(),
-            "cov2d": ws.cov2d[:, 0:3], "radius": ws.cov2d[:, 3]}
-    ctx = {"proj": proj, "opac": s2[:, 5], "colors": s2[:, 8:11], "entry_splat": ws.entry_splat[:E],
-           "tile_offsets": ws.tile_offsets, "tiles_x": ws.tiles_x, "tiles_y": ws.tiles_y, "cam": cam,
-           "workspace": ws, "view": view, "gmap": g, "n": n, "counters": cnt}
-    return RenderOutput(ws.color, ws.depth, ws.opacity, ws.trans, ws.n_contrib, ctx)
+            "cov2d": ws.cov2d[:, [0, 1, 1, 2]].reshape(n, 2, 2), "radius": ws.cov2d[:, 3]}
+    dirs, unorm, pre = _view_dirs(g, cam)
+    ctx = {"proj": proj, "opac": s2[:, 5], "colors": s2[:, 8:11], "preclamp": pre, "dirs": dirs, "u_norm": unorm,
+           "entry_splat": ws.entry_splat[:E], "tile_offsets": ws.tile_offsets, "tiles_x": ws.tiles_x,
+           "tiles_y": ws.tiles_y, "cam": cam}
+    images = (ws.color, ws.depth, ws.opacity, ws.trans, ws.n_contrib)
+    if host:
+        ctx = _to_host(ctx)
+        ctx["entry_splat"] = ctx["entry_splat"].astype(np.int64)
+        ctx["tile_offsets"] = ctx["tile_offsets"].astype(np.int64)
+        images = tuple(_to_host(a) for a in images)
+    ctx.update(workspace=ws, view=view, gmap=g, n=n, counters=cnt, host=host)
+    return RenderOutput(*images, ctx)
 
 
 def _load_image_grads(ws: Workspace, g_color_img, g_depth_img, g_opac_img):
@@ -266,7 +326,8 @@ def backward_2d(out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=Non
     call("gs_render_bwd", ws.fptr, stream_ptr())
     touched = ws.touched.bool()
     g2d = torch.where(touched[:, None], ws.g2d, torch.zeros((), device=ws.device))
-    return g2d[:, 0:2], g2d[:, 2:5], g2d[:, 5], g2d[:, 6:9], g2d[:, 9], touched
+    res = (g2d[:, 0:2], g2d[:, 2:5], g2d[:, 5], g2d[:, 6:9], g2d[:, 9], touched)
+    return tuple(_to_host(a) for a in res) if out.ctx.get("host") else res
 
 
 def rows_to_grads(rows: torch.Tensor) -> dict:
@@ -294,7 +355,14 @@ def backward(gmap, out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=
     """R/rasterizer.py:543-556 -> (grads dict mirroring parameters(), touched, pose_grad).
 
     pose_grad (with_pose=True) is the 6-vector (rho, theta) on the left tangent of T_cw
-    (R/rasterizer.py:646-657) as a float64 device tensor, else None."""
+    (R/rasterizer.py:646-657) as a float64 tensor, else None.  For a reference-typed map the
+    three come back as numpy arrays in the reference's shapes."""
+    if is_host_map(gmap) or out.ctx.get("host"):
+        out = RenderOutput(out.color, out.depth, out.opacity, out.transmittance, out.n_contrib,
+                           {**out.ctx, "host": False})
+        grads, touched, pose = backward(out.ctx["gmap"], out, g_color_img, g_depth_img, g_opac_img, with_pose)
+        grads.pop("_rows")
+        return _to_host(grads), _to_host(touched), _to_host(pose)
     g = as_device_map(gmap)
     ws: Workspace = out.ctx["workspace"]
     view: DeviceView = out.ctx["view"]
@@ -315,6 +383,8 @@ def backward(gmap, out: RenderOutput, g_color_img, g_depth_img=None, g_opac_img=
 def pose_backward(gmap, out, g_color_img, g_depth_img=None, g_opac_img=None):
     """The pose gradient alone (the tracker's need, R/odometry.py:324-328): the attribute
     gradients are not materialised."""
+    if is_host_map(gmap) or out.ctx.get("host"):
+        return _to_host(pose_backward(out.ctx["gmap"], out, g_color_img, g_depth_img, g_opac_img))
     g = as_device_map(gmap)
     ws: Workspace = out.ctx["workspace"]
     view: DeviceView = out.ctx["view"]
@@ -329,7 +399,12 @@ def cull_tiles(mean2d, conic, cov2d, opacity, depth, valid, width, height, cull=
     """R/rasterizer.py:169-219 on externally supplied 2D splats.
 
     cov2d may be (n, 2, 2), (n, 4) or (n, 3) = (c00, c01, c11).  Returns
-    (entry_splat, tile_offsets, tiles_x, tiles_y) as device tensors."""
+    (entry_splat, tile_offsets, tiles_x, tiles_y): device tensors for device inputs, int64
+    numpy arrays for numpy inputs (the reference's types)."""
+    if not isinstance(mean2d, torch.Tensor):
+        ent, offs, tx, ty = cull_tiles(_f32(mean2d, default_device()), conic, cov2d, opacity, depth, valid, width,
+                                       height, cull)
+        return ent.cpu().numpy().astype(np.int64), offs.cpu().numpy().astype(np.int64), tx, ty
     dev = default_device()
     m = _f32(mean2d, dev).reshape(-1, 2).contiguous()
     n = len(m)
@@ -375,56 +450,97 @@ def lr_columns(lrs: dict, device) -> torch.Tensor:
 
 
 class AdamState:
-    """First/second moments (parameter rows) plus a per-splat int32 step counter."""
+    """R/rasterizer.py:684-704: first/second moments (device parameter rows) plus a per-splat
+    int32 step counter (`t_dev`).  `t`, `m`, `v` read as device tensors -- or, once the state has
+    stepped a reference-typed (numpy) map, as numpy arrays, as the reference's AdamState."""
 
     def __init__(self, device=None) -> None:
         self.device = torch.device(device) if device is not None else None
         self.m_rows = None
         self.v_rows = None
-        self.t = None
+        self.t_dev = None
+        self.host = False  # numpy views (set by sparse_adam_step on a reference-typed map)
+
+    @property
+    def t(self):
+        if self.host and self.t_dev is not None:
+            return self.t_dev.cpu().numpy().astype(np.int64)
+        return self.t_dev
+
+    @t.setter
+    def t(self, value) -> None:
+        self.t_dev = value
 
     def ensure(self, gmap) -> None:
-        g = as_device_map(gmap)
-        dev = g.device
-        n = len(g)
-        if self.t is None:
+        n = len(gmap)
+        dev = gmap.device if isinstance(gmap, GaussianMap) else (self.device or default_device())
+        if self.t_dev is None:
             self.m_rows = torch.zeros((0, GS_ROW), device=dev)
             self.v_rows = torch.zeros((0, GS_ROW), device=dev)
-            self.t = torch.zeros(0, dtype=torch.int32, device=dev)
-        if self.t.numel() < n:
-            grow = n - self.t.numel()
-            cap = max(n, 2 * self.t.numel())
-            for name in ("m_rows", "v_rows"):
-                old = getattr(self, name)
-                new = torch.zeros((cap, GS_ROW), device=dev)
-                new[:old.shape[0]] = old
-                setattr(self, name, new)
+            self.t_dev = torch.zeros(0, dtype=torch.int32, device=dev)
+        have = self.t_dev.numel()
+        if have < n:
+            cap = max(n, 2 * have)
+            if self.m_rows.shape[0] < cap:
+                for name in ("m_rows", "v_rows"):
+                    old = getattr(self, name)
+                    new = torch.zeros((cap, GS_ROW), device=dev)
+                    new[:old.shape[0]] = old
+                    setattr(self, name, new)
             t = torch.zeros(cap, dtype=torch.int32, device=dev)
-            t[:self.t.numel()] = self.t
-            self.t = t[:n] if grow else t
-            self._cap_t = t
-        if self.t.numel() > n:
-            self.t = self.t[:n]
+            t[:have] = self.t_dev
+            self.t_dev = t[:n]
+        if self.t_dev.numel() > n:
+            self.t_dev = self.t_dev[:n]
+
+    def _view(self, rows) -> dict:
+        d = rows_to_grads(rows[:self.t_dev.numel()])
+        d.pop("_rows")
+        return {k: v.double().cpu().numpy() for k, v in d.items()} if self.host else d
 
     @property
     def m(self) -> dict:
-        return rows_to_grads(self.m_rows[:self.t.numel()])
+        return self._view(self.m_rows)
 
     @property
     def v(self) -> dict:
-        return rows_to_grads(self.v_rows[:self.t.numel()])
+        return self._view(self.v_rows)
 
 
 def sparse_adam_step(gmap, grads: dict, touched, state: AdamState, lrs: dict) -> None:
-    """R/rasterizer.py:707-725: Adam restricted to touched splats, per-splat bias correction."""
-    g = as_device_map(gmap)
-    state.ensure(g)
-    n = len(g)
+    """R/rasterizer.py:707-725: Adam restricted to touched splats, per-splat bias correction, in
+    place.  A device map is updated on the device.  A reference-typed map (numpy attribute
+    arrays) is updated in place on the host, at float64: the device computes the fp32 step of
+    the touched rows (gs_adam on zero rows yields -step exactly) and `param[idx] += -step` is
+    applied to the caller's arrays; untouched rows are not written at all."""
+    n = len(gmap)
+    host = not isinstance(gmap, GaussianMap)
+    dev = gmap.device if not host else default_device()
+    state.ensure(gmap if not host else _Sized(n, dev))
     if n == 0:
         return
-    rows = grads_to_rows(grads, n, g.device).contiguous()
+    rows = grads_to_rows(grads, n, dev).contiguous()
     tm = touched if isinstance(touched, torch.Tensor) else torch.as_tensor(np.asarray(touched))
-    tm = tm.to(device=g.device, dtype=torch.uint8).contiguous()
-    lr = lr_columns(lrs, g.device)
-    call("gs_adam", g.data.data_ptr(), state.m_rows.data_ptr(), state.v_rows.data_ptr(), state.t.data_ptr(),
+    tm = tm.to(device=dev, dtype=torch.uint8).contiguous()
+    lr = lr_columns(lrs, dev)
+    params = gmap.data if not host else torch.zeros((n, GS_ROW), dtype=torch.float32, device=dev)
+    call("gs_adam", params.data_ptr(), state.m_rows.data_ptr(), state.v_rows.data_ptr(), state.t_dev.data_ptr(),
          rows.data_ptr(), tm.data_ptr(), n, lr.data_ptr(), stream_ptr())
+    if host:
+        state.host = True
+        idx = np.flatnonzero(tm.cpu().numpy())
+        step = params[torch.as_tensor(idx, device=dev)].double().cpu().numpy()
+        for name in NAMES:
+            a, b = SLICES[name]
+            arr = getattr(gmap, name)
+            arr[idx] += step[:, a:b].reshape((len(idx),) + arr.shape[1:])
+
+
+class _Sized:
+    """len() + device of a host map, for AdamState.ensure."""
+
+    def __init__(self, n: int, device) -> None:
+        self.n, self.device = n, device
+
+    def __len__(self) -> int:
+        return self.n

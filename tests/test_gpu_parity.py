@@ -48,7 +48,7 @@ def load(name):
 def gpu_splats(out):
     p = out.ctx["proj"]
     return (_np(p["mean2d"]).astype(np.float32), _np(p["conic"]).astype(np.float32),
-            _np(p["cov2d"]).astype(np.float32), _np(out.ctx["opac"]).astype(np.float32),
+            _np(p["cov2d"]).reshape(-1, 4)[:, [0, 1, 3]].astype(np.float32), _np(out.ctx["opac"]).astype(np.float32),
             _np(p["depth"]).astype(np.float32), _np(p["valid"]).astype(bool))
 
 
