@@ -68,6 +68,16 @@ def peaks() -> tuple[dict, str]:
     return dict(PEAKS_FALLBACK), "fallback"
 
 
+def fp32_peak() -> tuple[float, str]:
+    """Measured FP32 issue peak (lane instructions / s) of the FFMA microbenchmark
+    (profiles/r02_fp32_peak.json, tools/micro/ffma2.cu); the theoretical figure otherwise."""
+    p = os.path.join(ROOT, "profiles", "r02_fp32_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["fp32_lane_instr_per_s"]), "profiles/r02_fp32_peak.json (FFMA microbenchmark)"
+    return 148 * 128 * 1.965e9, "theoretical 148 SM x 128 lanes x 1.965 GHz"
+
+
 def make_scene(name: str, rank: int = 0, world: int = 1, views_override=None):
     from paper_2507_04004_b200 import scenes
     kind, n, w, h, lidar, nkf, mode = CONFIGS[name]
@@ -82,57 +92,82 @@ def make_scene(name: str, rank: int = 0, world: int = 1, views_override=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region: NVML polled
+    every ~2 ms from a thread (so even a 10 ms region gets samples), nvidia-smi -lms 100 as the
+    fallback."""
 
-    FIELDS = ("clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
-              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
-              "clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
-        self.rows = []
-        self.proc = None
-        self.thread = None
+    def __init__(self, cuda_index: int):
+        self.idx = cuda_index
+        self.samples = []  # (sm MHz, reason bitmask)
+        self.max_mhz = None
+        self.source = None
+        self._stop = threading.Event()
+        self._go = threading.Event()
+        self.t0 = self.t1 = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.idx)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001 -- fall back to the CUDA index
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+
+    def _poll(self, nv, h):
+        while not self._stop.is_set():
+            if self._go.is_set():
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(sm), int(rs)))
+                except Exception:  # noqa: BLE001
+                    pass
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={','.join(self.FIELDS)}", "--format=csv,noheader,nounits",
-                 "-lms", "100", "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            nv, h = self._handle()
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._mask = {name: getattr(nv, attr) for name, attr in self.REASONS if hasattr(nv, attr)}
+            self.source = "nvml, 2 ms polling during the timed region"
+            self.thread = threading.Thread(target=self._poll, args=(nv, h), daemon=True)
             self.thread.start()
-            t0 = time.perf_counter()  # the sampler is live before the timed region starts
-            while not self.rows and time.perf_counter() - t0 < 3.0:
-                time.sleep(0.01)
-            self.rows.clear()
-        except (OSError, FileNotFoundError):
-            self.proc = None
+        except Exception:  # noqa: BLE001 -- no NVML: unsampled
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == len(self.FIELDS):
-                self.rows.append(parts)
+    def start(self) -> None:
+        """Mark the start of the timed region (call right before it)."""
+        self.t0 = time.perf_counter()
+        self._go.set()
+
+    def stop(self) -> None:
+        self._go.clear()
+        self.t1 = time.perf_counter()
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self._stop.set()
+        if self.thread is not None:
             self.thread.join(timeout=2)
 
     def summary(self) -> dict:
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        window = None if self.t0 is None or self.t1 is None else round((self.t1 - self.t0) * 1e3, 1)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0,
+                    "window_ms": window}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({name for _, r in self.samples for name, m in self._mask.items() if r & m})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples), "window_ms": window, "source": self.source}
 
 
 # ---------------------------------------------------------------------------
@@ -163,7 +198,15 @@ def algorithmic_bytes(eng, scene_cam) -> dict:
     valid = int(full.valid.sum().item())
     blend = int(full.touched.sum().item())
     K = int(eng.views[0].lidar_z.numel()) if eng.views[0].sparse is not None else 0
+    # FP32 work (lane instructions): blend ~17 + 1 MUFU per (entry, pixel) pair
+    # forward, ~50 + 2 MUFU backward; SSIM 4 moments x 11 taps x 2 passes + 3 adjoint images x 11
+    # x 2 + ~26 for the SSIM map per pixel-channel; preprocess ~300 per Gaussian in front of the
+    # camera; chain rule ~900 + Adam 10 per parameter per touched Gaussian
+    pairs = int(nc.sum().item())
+    fp32 = {"render_fwd": 18 * pairs, "render_bwd": 52 * pairs, "loss": 3 * P * (88 + 66 + 26),
+            "preprocess": 300 * near, "chain_adam": n_t * (900 + 10 * 59)}
     return {
+        "_fp32": fp32,
         # compulsory bytes of the preprocess: the position of every Gaussian (12 B), the rest of
         # the geometry of those in front of the camera (32 B), the SH tail of the drawable ones
         # (180 B) and their 76-B records (splat 48, rect 16, kept 4, cull bits 8).  (The kernel
@@ -171,16 +214,19 @@ def algorithmic_bytes(eng, scene_cam) -> dict:
         "preprocess": 12 * n + 32 * near + 180 * blend + 76 * blend,
         "render_fwd": 52 * proc + 28 * P + 8 * tx * ty,
         "render_bwd": 28 * P + (52 + 40) * proc + 48 * n_t + 8 * tx * ty,
-        # fused chain + Adam: params, m, v read and written (240 of 256 B per row), the FP64
-        # screen-space gradients read (80 B) and zeroed (96 B), the step counter
-        "chain_adam": n_t * (3 * 240 + 80 + 4 + 3 * 240 + 96 + 4),
+        # fused chain + Adam, SURVEY.md 8d's 1,465 B per touched Gaussian: params, m and v read
+        # and written (236 B each way), the screen-space gradients read (40 B), the step counter
+        # read and written (the fixed-point rows' 160-B read + 160-B clear are implementation
+        # overhead, in "traffic")
+        "chain_adam": 1465 * n_t,
         "loss": 36 * P + 8 * P,
         # lazy binning (the engine): per-tile counts read, offsets / flags written (20 B per
         # tile), the screen-covering Gaussians' depth keys sorted (16 B each) and their per-tile
         # bitmaps transposed (read + write).  The small Gaussians' entries are not materialised
         # here: the forward fills the buckets of the tiles that outlive the screen-covering run.
         "bin": 20 * tx * ty + 16 * huge_n + 2 * huge_n * ((tx * ty + 31) // 32) * 4,
-        "_stats": {"n": n, "n_valid": valid, "n_touched": n_t, "entries": E, "blend_entries": proc, "pixels": P},
+        "_stats": {"n": n, "n_valid": valid, "n_touched": n_t, "entries": E, "blend_entries": proc, "pixels": P,
+                   "blend_pairs": pairs},
     }
 
 
@@ -220,7 +266,7 @@ def run_ours(args) -> dict:
     nv = len(kfs)
     initial = eng.save_state()
 
-    def timed(block_fn):
+    def timed(block_fn, clk=None):
         """K steps timed with CUDA events in segments of <= SEGMENT iterations; between
         segments (untimed) the map and Adam state are restored to the scene's initial state, so
         the workload is the named scene + < SEGMENT iterations of optimisation whatever K is.
@@ -230,6 +276,8 @@ def run_ours(args) -> dict:
         eng.restore_state(initial)
         torch.cuda.synchronize()
         total_ms, wall_s, done = 0.0, 0.0, 0
+        if clk is not None:
+            clk.start()
         while done < args.steps:
             seg = min(SEGMENT, args.steps - done)
             s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -243,6 +291,8 @@ def run_ours(args) -> dict:
             total_ms += s_.elapsed_time(e_)
             done += seg
             eng.restore_state(initial)
+        if clk is not None:
+            clk.stop()
         return total_ms / args.steps, wall_s * 1e3 / args.steps
 
     def graph_block(first, count):
@@ -250,7 +300,7 @@ def run_ours(args) -> dict:
             eng.step(i % nv)
 
     with ClockSampler(local) as clk:
-        ms, _ = timed(graph_block)
+        ms, _ = timed(graph_block, clk)
     value = 1000.0 / ms
     loss = eng.loss_sum() / (args.steps + args.warmup)
     # e2e: host keyframes through the public streaming API (H2D inside the timed region)
@@ -269,10 +319,21 @@ def run_ours(args) -> dict:
     dom = max((p for p in phase_ms if p != "bin"), key=lambda p: phase_ms[p] * TOP_KERNEL_SHARE.get(p, 1.0))
     dom_all = max(phase_ms, key=lambda p: phase_ms[p])
     hbm = float(pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+    f32peak, f32src = fp32_peak()
     achieved = bytes_[dom] / (phase_ms[dom] * 1e-3) / 1e9
-    phases = {p: {"ms": round(phase_ms[p], 4), "share": round(phase_ms[p] / sum(phase_ms.values()), 4),
-                  "alg_bytes": int(bytes_[p]), "gbs": round(bytes_[p] / (phase_ms[p] * 1e-3) / 1e9, 1)}
-              for p in phase_ms}
+    # per phase: both rooflines -- HBM (algorithmic bytes / time vs the measured copy bandwidth)
+    # and FP32 issue (algorithmic FP32 lane instructions / time vs the measured FFMA rate)
+    phases = {}
+    for p in phase_ms:
+        sec = phase_ms[p] * 1e-3
+        e = {"ms": round(phase_ms[p], 4), "share": round(phase_ms[p] / sum(phase_ms.values()), 4),
+             "alg_bytes": int(bytes_[p]), "gbs": round(bytes_[p] / sec / 1e9, 1),
+             "hbm_frac": round(bytes_[p] / sec / 1e9 / hbm, 4)}
+        if p in bytes_["_fp32"]:
+            e["fp32_instr"] = int(bytes_["_fp32"][p])
+            e["fp32_frac"] = round(bytes_["_fp32"][p] / sec / f32peak, 4)
+        e["bound"] = "fp32" if e.get("fp32_frac", 0.0) > e["hbm_frac"] else "hbm"
+        phases[p] = e
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -284,12 +345,11 @@ def run_ours(args) -> dict:
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: S2r room scene (seed 7), Gaussians seeded on ray-cast surfaces from 32 views, "
                 "targets (8-bit, like camera frames) and LiDAR ray-traced; random-free deterministic generator",
-        "config": {"workload": name, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
-                   "keyframes": nv, "semantics": "per-keyframe sparse Adam (R/mapper.py:246-257)",
-                   "l2": "inputs larger than L2 (params + Adam moments = 768 MB per step)",
-                   "cuda_graph": True, "mean_loss": round(loss, 6),
-                   "timing": f"CUDA events over segments of {SEGMENT} iterations; map + Adam state restored "
-                             "to the initial scene between segments (untimed)"},
+        "config": bench_config(name, nv),
+        "notes": {"l2": "inputs larger than L2 (params + Adam moments = 768 MB per step)",
+                  "cuda_graph": True, "mean_loss": round(loss, 6),
+                  "timing": f"CUDA events over segments of {SEGMENT} iterations; map + Adam state restored "
+                            "to the initial scene between segments (untimed)"},
         "e2e": {"value": round(1000.0 / e2e_ms, 2), "unit": "it/s", "h2d_bytes_per_step": int(eng.h2d_bytes),
                 "d2h_bytes_per_step": int(eng.d2h_bytes), "wall_ms_per_step": round(wall_ms, 4),
                 "path": "MapOptimizer.run_host: pinned host keyframe (8-bit target frame + LiDAR K-list) -> H2D "
@@ -298,7 +358,9 @@ def run_ours(args) -> dict:
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": traffic,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({pk_kind})",
-                     "dominant_phase_overall": dom_all, "kernel_name": TOP_KERNEL.get(dom, dom)},
+                     "bytes": "SURVEY.md 8d: 1,465 B per touched Gaussian" if dom == "chain_adam" else "DESIGN.md 3",
+                     "dominant_phase_overall": dom_all, "kernel_name": TOP_KERNEL.get(dom, dom),
+                     "fp32_peak": f32peak, "fp32_peak_source": f32src},
         "phases": phases,
         "stats": bytes_["_stats"],
         "gpu_launches": int(eng.kernels_per_step() * args.steps),
@@ -307,6 +369,19 @@ def run_ours(args) -> dict:
     if not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(sc, args.cpu_budget)
     return out
+
+
+def bench_config(name: str, keyframes: int | None = None, batch: int | None = None, world: int = 1) -> dict:
+    """The workload description both arms print (ours and --impl reference)."""
+    kind, n_g, W, H, lidar, nkf, mode = CONFIGS[name]
+    cfg = {"workload": name, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
+           "keyframes": int(keyframes if keyframes is not None else nkf), "mode": mode}
+    if batch:
+        cfg["semantics"] = f"batch-{batch}: gradient sum + touched union + one sparse Adam per batch"
+        cfg["parallelism"] = f"dp{world}"
+    elif mode == "train":
+        cfg["semantics"] = "per-keyframe sparse Adam (R/mapper.py:246-257)"
+    return cfg
 
 
 def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
@@ -342,12 +417,14 @@ def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        clk.start()
         s.record()
         for i in range(args.steps):
             cur.copy_(views[i % len(views)].buf)
             graph.replay()
         e.record()
         e.synchronize()
+        clk.stop()
     ms = s.elapsed_time(e) / args.steps
     cnt = ws.counters.cpu().numpy()
     stats = {"entries": int(cnt[_lib.CNT_ENTRIES]), "touched": int(cnt[_lib.CNT_TOUCHED]),
@@ -355,7 +432,7 @@ def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
     return {"metric": METRIC, "value": round(1000.0 / ms, 2), "unit": "FPS", "stats": stats, "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene",
-            "config": {"workload": name, "gaussians": len(g), "mode": "forward-only render"},
+            "config": bench_config(name, len(kfs)),
             "clocks": clk.summary()}
 
 
@@ -384,26 +461,29 @@ def run_track(args, g, kfs, name) -> dict:
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
+        clk.start()
         s.record()
         for _ in range(args.steps):
             frame()
         e.record()
         e.synchronize()
+        clk.stop()
     ms = s.elapsed_time(e) / args.steps
     rot, trans, loss = ref.result()
     return {"metric": METRIC, "value": round(1000.0 / ms, 2), "unit": "frames/s (30 pose iterations)",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic S2r room scene", "config": {"workload": name, "gaussians": len(g),
-                                                           "mode": "photometric_refine, 30 iterations"},
+            "data": "synthetic S2r room scene", "config": bench_config(name, 1),
             "final_loss": round(loss, 6), "pose_error_m": float(np.linalg.norm(trans - np.asarray(cam.trans_cw))),
             "clocks": clk.summary()}
 
 
 def run_ours_dp(args, rank, world, local) -> dict:
-    """Keyframe-batch data parallelism: 32 views per step, 32/N per rank, one NCCL
-    allreduce of the parameter-row gradients (touched flags fused) and one sparse Adam per step.
-    Also the N=1 reference point of the same semantics (`--batch`)."""
+    """Keyframe-batch data parallelism: 32 views per step, 32/N per rank (each
+    rank's view loop one CUDA graph), the touched union compacted on the device, its gradient rows
+    allreduced with NCCL in chunks whose sparse Adam steps overlap the remaining chunks' transfer.
+    One step = one batch; `value` counts views (map-optimisation iterations) per second of the
+    whole job, so N = 1 (`--batch`) and N > 1 are the same unit and semantics."""
     import torch
     import torch.distributed as dist
 
@@ -421,7 +501,7 @@ def run_ours_dp(args, rank, world, local) -> dict:
     initial = eng.save_state()
     seg = max(1, SEGMENT // batch)  # batches per timed segment (~100 iterations), state restored between
 
-    def timed(step_fn):
+    def timed(step_fn, clk=None):
         eng.restore_state(initial)
         for _ in range(args.warmup):
             step_fn()
@@ -429,6 +509,8 @@ def run_ours_dp(args, rank, world, local) -> dict:
         torch.cuda.synchronize()
         dist.barrier()
         total, done = 0.0, 0
+        if clk is not None:
+            clk.start()
         while done < args.steps:
             n = min(seg, args.steps - done)
             s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -442,28 +524,70 @@ def run_ours_dp(args, rank, world, local) -> dict:
             total += s_.elapsed_time(e_)
             done += n
             eng.restore_state(initial)
+        if clk is not None:
+            clk.stop()
         ms = torch.tensor([total / args.steps], device="cuda")
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)  # the job's time is the slowest rank's
         return float(ms.item())
 
     with ClockSampler(local) as clk:
-        ms = timed(lambda: eng.step(ids))
+        ms = timed(lambda: eng.step(ids), clk)
     eng.attach_host_keyframes(kfs)
     e2e_ms = timed(lambda: eng.step_host(ids))
     value = batch * 1000.0 / ms
     out = {"metric": METRIC, "value": round(value, 2), "unit": "it/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene (seed 7)",
-           "config": {"workload": args.config, "gaussians": len(g), "batch_keyframes": batch,
-                      "semantics": "batch-32 gradient sum + touched union + one sparse Adam per batch",
-                      "parallelism": f"dp{world} (NCCL allreduce of parameter-row gradients)",
-                      "timing": f"segments of {seg} batches, map + Adam state restored between (untimed)"},
+           "config": bench_config(args.config, batch, batch=batch, world=world),
+           "notes": {"per_rank_views": len(mine), "union_rows_last_batch": eng.union,
+                     "reduction": "touched OR (n bytes) + device compaction + NCCL allreduce of the union's "
+                                  f"rows in {PAR.BatchMapOptimizer.CHUNKS} chunks, Adam per chunk",
+                     "timing": f"segments of {seg} batches, map + Adam state restored between (untimed); "
+                               "max over ranks"},
            "e2e": {"value": round(batch * 1000.0 / e2e_ms, 2), "unit": "it/s",
-                   "h2d_bytes_per_step": int(eng.h2d_bytes_per_view * len(ids)), "d2h_bytes_per_step": 8,
+                   "h2d_bytes_per_step": int(eng.h2d_bytes_per_view * len(ids) * world), "d2h_bytes_per_step": 8 * world,
                    "path": "BatchMapOptimizer.step_host: pinned host keyframes streamed per view (copy stream, "
-                           "double-buffered) -> accumulate -> allreduce -> Adam -> D2H batch loss"},
+                           "multi-buffered) -> accumulate -> allreduce -> Adam -> D2H batch loss"},
            "gpu_launches": int(eng.kernels_per_step() * args.steps), "clocks": clk.summary()}
     dist.barrier()
+    return out
+
+
+def run_plumbing(args) -> dict:
+    """GSLIC_BENCH_PLUMBING=1 (tests/test_bench_launch.py, CPU): the multi-rank launch path of
+    this script -- self-spawn through torchrun, rendezvous on 127.0.0.1, barrier-bracketed timing,
+    max over ranks, one JSON line from rank 0 -- with a gloo allreduce of gradient rows standing
+    in for the GPU step.  Never a benchmark number."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_04004_b200 import parallel as PAR
+    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+    dist.init_process_group("gloo")
+    n = 4096
+    gen = torch.Generator().manual_seed(rank)
+    base = torch.randn(n, 64, generator=gen)
+    flags = (torch.rand(n, generator=gen) < 0.3).to(torch.uint8)
+
+    def step():
+        PAR.allreduce_grads_sparse(base.clone(), flags.clone())
+
+    for _ in range(args.warmup):
+        step()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dist.barrier()
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3 / args.steps])
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    union = flags.clone()
+    dist.all_reduce(union, op=dist.ReduceOp.MAX)
+    out = {"metric": METRIC, "value": None, "unit": "it/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(float(ms.item()), 4), "plumbing": True,
+           "union_rows": int(union.sum().item()), "config": bench_config(args.config, 32, batch=32, world=world)}
+    dist.barrier()
+    dist.destroy_process_group()
     return out
 
 
@@ -544,12 +668,12 @@ def run_reference(args) -> dict | None:
             break
     ms = 1e3 * float(np.mean(times))
     value = 1000.0 / ms
-    return {"metric": METRIC, "value": round(value, 4), "unit": unit, "n_gpus": world, "steps": len(times),
+    return {"metric": METRIC, "value": round(value, 4), "unit": unit, "n_gpus": args.gpus, "steps": len(times),
             "warmup": warm, "ms_per_step": round(ms, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "impl": "reference",
             "data": "synthetic S2r room scene (seed 7), same generator as the GPU arm",
-            "config": {"workload": args.config, "gaussians": int(n_g), "width": W, "height": H, "lidar": lidar,
-                       "keyframes": nkf, "semantics": "per-keyframe sparse Adam (R/mapper.py:246-257)"},
+            "config": bench_config(args.config, 32 if args.gpus > 1 or args.batch else None,
+                                   batch=32 if args.gpus > 1 or args.batch else None, world=args.gpus),
             "cpu_baseline": {"value": round(value, 4), "unit": unit, "cores": threads, "kind": "port",
                              "sample": f"{len(times)} full steps (capped by a {budget:.0f} s budget) of the "
                                        f"workload; oracle/gs_oracle.c float64, {threads} OpenMP threads"},
@@ -570,19 +694,32 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=150.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # N GPUs requested without a launcher: become torchrun with one rank per GPU (rank 0
+        # prints the JSON line; rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     # stdout carries exactly one JSON line: everything else the process (or a library -- NCCL
     # prints its version banner to stdout on communicator set-up) writes to fd 1 goes to stderr
     sys.stdout.flush()
     json_out = os.fdopen(os.dup(1), "w")
     os.dup2(2, 1)
+    plumbing = os.environ.get("GSLIC_BENCH_PLUMBING") == "1"
     if args.impl == "reference":
         out = run_reference(args)
+    elif plumbing:
+        out = run_plumbing(args)
     else:
         out = run_ours(args)
     if out is not None and int(os.environ.get("RANK", 0)) == 0:
         json_out.write(json.dumps(out) + "\n")
         json_out.flush()
-    if (int(os.environ.get("WORLD_SIZE", 1)) > 1 or args.batch) and args.impl == "ours":
+    if (int(os.environ.get("WORLD_SIZE", 1)) > 1 or args.batch) and args.impl == "ours" and not plumbing:
         import torch.distributed as dist
         if dist.is_initialized():
             dist.destroy_process_group()

@@ -249,6 +249,22 @@ int gs_chain_pose(const gs_frame *f, const float *params, float *grads, uint8_t 
 int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *grads,
             const uint8_t *touched, int64_t n, const float *lr_cols, void *stream);
 
+/* ---- batch reduction (multi-view / multi-GPU) -------------------------------- */
+/* idx[0 .. *count) = the i with flags[i] != 0, ascending (device-side, no host sync; identical on
+ * every rank for identical flags).  scratch: ceil(n / 1024) ints. */
+int gs_compact_flags(const uint8_t *flags, int64_t n, int32_t *idx, int32_t *count, int32_t *scratch, void *stream);
+/* packed[i] = rows[idx[i]][0:60] for i < min(*count, cap) (the 59 parameters + 1 pad, 16-B aligned):
+ * the union's gradient rows, contiguous for the allreduce. */
+int gs_gather_rows(const float *rows, const int32_t *idx, const int32_t *count, int64_t cap, float *packed,
+                   void *stream);
+/* sparse_adam_step (R/rasterizer.py:707-725) over rows idx[first .. first + num) clipped to *count,
+ * gradient row i from packed[i] (60 floats) or, with packed == NULL, from grads[idx[i]]; the step
+ * counters advance; grads rows (when given) and touched flags (when given) of those rows are
+ * cleared for the next batch. */
+int gs_adam_packed(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *packed,
+                   const int32_t *idx, const int32_t *count, int64_t first, int64_t num, const float *lr_cols,
+                   float *grads, uint8_t *touched, void *stream);
+
 /* ---- helpers for the reference-shaped Python API ------------------------------------- */
 /* dense sparse_depth (H,W) -> K-list (idx, z) in pixel order; count written to *k_out (device
  * int32).  idx must hold H*W + ceil(H*W/1024) ints (the tail is scratch), z H*W floats. */

@@ -107,6 +107,9 @@ def lib():
         "gs_project": (ctypes.c_int, [P, i64, P, P, P, P, P, P, P, P, P, P, P]),
         "gs_eval_sh": (ctypes.c_int, [P, P, P, i64, P, P, P]),
         "gs_pack_splats": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P, P]),
+        "gs_compact_flags": (ctypes.c_int, [P, i64, P, P, P, P]),
+        "gs_gather_rows": (ctypes.c_int, [P, P, P, i64, P, P]),
+        "gs_adam_packed": (ctypes.c_int, [P, P, P, P, P, P, P, i64, i64, P, P, P, P]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -119,7 +122,8 @@ def lib():
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
             "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
             "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
-            "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_decode_u8", "gs_track_mask", "gs_track_grad", "gs_pose_adam"]
+            "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_decode_u8", "gs_track_mask", "gs_track_grad", "gs_pose_adam",
+            "gs_compact_flags", "gs_gather_rows", "gs_adam_packed"]
 
 
 def check(rc: int, what: str) -> None:

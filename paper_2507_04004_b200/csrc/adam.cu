@@ -7,6 +7,7 @@
 // computes its Gaussian's 59 gradients into shared memory, then the warp streams the Adam
 // update over the 32 rows (params, m, v) with coalesced float4 traffic.  Nothing but the
 // updated rows is written: the parameter-gradient rows never reach HBM on the 1-GPU path.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -433,6 +434,123 @@ __global__ void adam_kernel(float *__restrict__ params, float *__restrict__ am, 
     *reinterpret_cast<float4 *>(params + off) = p4;
 }
 
+// ---------------------------------------------------------------------------------------------
+// Batch reduction (multi-view / multi-GPU): the touched union compacted in id
+// order (identical on every rank, no host-side nonzero), the union's gradient rows gathered
+// into a packed buffer for the collective, and Adam applied straight from the packed rows.
+
+constexpr int CF_CHUNK = 1024;  // flags per compaction block
+
+__global__ void __launch_bounds__(CF_CHUNK) compact_count_kernel(const uint8_t *__restrict__ flags, int64_t n,
+                                                                 int32_t *chunk_cnt) {
+    pdl_wait();
+    __shared__ int s_w[CF_CHUNK / 32];
+    const int64_t i = (int64_t)blockIdx.x * CF_CHUNK + threadIdx.x;
+    const unsigned m = __ballot_sync(0xffffffffu, i < n && flags[i]);
+    if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int v = s_w[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) chunk_cnt[blockIdx.x] = v;
+    }
+}
+
+__global__ void __launch_bounds__(CF_CHUNK) compact_write_kernel(const uint8_t *__restrict__ flags, int64_t n,
+                                                                 const int32_t *__restrict__ chunk_cnt, int32_t *idx,
+                                                                 int32_t *count) {
+    pdl_wait();
+    __shared__ int s_w[CF_CHUNK / 32];
+    __shared__ int s_base;
+    // this block's offset: the counts of the blocks before it (summed by the whole block)
+    int acc = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += CF_CHUNK) acc += chunk_cnt[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) s_w[warp] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int b = 0;
+        for (int w = 0; w < CF_CHUNK / 32; w++) b += s_w[w];
+        s_base = b;
+    }
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * CF_CHUNK + threadIdx.x;
+    const bool hit = i < n && flags[i];
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) s_w[warp] = __popc(m);
+    __syncthreads();
+    int before = s_base;
+    for (int w = 0; w < warp; w++) before += s_w[w];
+    if (hit) idx[before + __popc(m & ((1u << lane) - 1u))] = (int32_t)i;
+    if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) {
+        int tot = s_base;
+        for (int w = 0; w < CF_CHUNK / 32; w++) tot += s_w[w];
+        *count = tot;
+    }
+}
+
+// packed[i, 0:60] = rows[idx[i], 0:60] for i < min(*count, cap): 15 float4 per row
+__global__ void gather_rows_kernel(const float *__restrict__ rows, const int32_t *__restrict__ idx,
+                                   const int32_t *__restrict__ count, int64_t cap, float *__restrict__ packed) {
+    pdl_wait();
+    const int64_t nr = min((int64_t)*count, cap);
+    for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nr * 15; q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q / 15;
+        const int c4 = (int)(q - i * 15);
+        reinterpret_cast<float4 *>(packed)[i * 15 + c4] =
+            reinterpret_cast<const float4 *>(rows)[(int64_t)idx[i] * (GS_ROW / 4) + c4];
+    }
+}
+
+// Sparse Adam over rows idx[first .. first + num) (clipped to *count): 16 threads per row; the
+// gradient row is packed[i] (60 floats) or, without a packed buffer, grads[idx[i]]; the
+// consumed gradient row and touched flag are cleared for the next batch.
+__global__ void adam_packed_kernel(float *__restrict__ params, float *__restrict__ am, float *__restrict__ av,
+                                   int32_t *__restrict__ at, const float *__restrict__ packed,
+                                   const int32_t *__restrict__ idx, const int32_t *__restrict__ count, int64_t first,
+                                   int64_t num, const float *__restrict__ lr_cols, float *__restrict__ grads,
+                                   uint8_t *__restrict__ touched) {
+    pdl_wait();
+    const int64_t end = min(first + num, (int64_t)*count);
+    for (int64_t q = first * 16 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < end * 16;
+         q += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = q >> 4;
+        const int c4 = (int)(q & 15);
+        const int64_t row = idx[i];
+        const int tn = at[row] + 1;  // read by the row's 16 lanes before its lane 15 writes it
+        __syncwarp(0xffffu << (threadIdx.x & 16u));  // (the 16 lanes of a row share every loop trip)
+        const float bc1 = (float)(1.0 / (1.0 - pow(0.9, (double)tn))), bc2 = (float)(1.0 / (1.0 - pow(0.999, (double)tn)));
+        if (c4 == 15) {  // columns 60-63: padding; this lane bumps the step and clears the flag
+            at[row] = tn;
+            if (touched) touched[row] = 0;
+            continue;
+        }
+        const int64_t off = row * GS_ROW + 4 * c4;
+        const float4 g4 = packed ? reinterpret_cast<const float4 *>(packed)[i * 15 + c4]
+                                 : *reinterpret_cast<const float4 *>(grads + off);
+        if (grads) *reinterpret_cast<float4 *>(grads + off) = make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 P = *reinterpret_cast<const float4 *>(params + off);
+        float4 m4 = *reinterpret_cast<const float4 *>(am + off);
+        float4 v4 = *reinterpret_cast<const float4 *>(av + off);
+        const float4 lr = __ldg(reinterpret_cast<const float4 *>(lr_cols) + c4);
+        float4 p4;
+        p4.x = adam_one(P.x, m4.x, v4.x, g4.x, lr.x, bc1, bc2);
+        p4.y = adam_one(P.y, m4.y, v4.y, g4.y, lr.y, bc1, bc2);
+        p4.z = adam_one(P.z, m4.z, v4.z, g4.z, lr.z, bc1, bc2);
+        if (c4 == 14) {  // column 59: padding
+            p4.w = P.w;
+        } else {
+            p4.w = adam_one(P.w, m4.w, v4.w, g4.w, lr.w, bc1, bc2);
+        }
+        *reinterpret_cast<float4 *>(am + off) = m4;
+        *reinterpret_cast<float4 *>(av + off) = v4;
+        *reinterpret_cast<float4 *>(params + off) = p4;
+    }
+}
+
 // the pose gradient from its fixed-point accumulators (gs_chain_pose)
 __global__ void pose_finish_kernel(const int64_t *__restrict__ acc, double *pose) {
     pdl_wait();
@@ -540,6 +658,52 @@ extern "C" int gs_adam(float *params, float *adam_m, float *adam_v, int32_t *ada
     if (rc) return rc;
     launch_pdl(adam_step_kernel, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, adam_t, touched, n);
     return check_launch("adam_step_kernel");
+}
+
+extern "C" int gs_compact_flags(const uint8_t *flags, int64_t n, int32_t *idx, int32_t *count, int32_t *scratch,
+                                void *stream) {
+    if (n < 0 || (n > 0 && (!flags || !idx || !count || !scratch))) {
+        set_error("gs_compact_flags: bad arguments");
+        return GS_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (n == 0) {
+        cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+        return check_launch("gs_compact_flags");
+    }
+    const unsigned chunks = (unsigned)((n + CF_CHUNK - 1) / CF_CHUNK);
+    launch_pdl(compact_count_kernel, chunks, CF_CHUNK, 0, st, flags, n, scratch);
+    int rc = check_launch("compact_count_kernel");
+    if (rc) return rc;
+    launch_pdl(compact_write_kernel, chunks, CF_CHUNK, 0, st, flags, n, (const int32_t *)scratch, idx, count);
+    return check_launch("compact_write_kernel");
+}
+
+extern "C" int gs_gather_rows(const float *rows, const int32_t *idx, const int32_t *count, int64_t cap, float *packed,
+                              void *stream) {
+    if (!rows || !idx || !count || !packed || cap < 0) {
+        set_error("gs_gather_rows: bad arguments");
+        return GS_ERR_ARG;
+    }
+    if (cap == 0) return GS_OK;
+    launch_pdl(gather_rows_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, rows, idx, count, cap, packed);
+    return check_launch("gather_rows_kernel");
+}
+
+extern "C" int gs_adam_packed(float *params, float *adam_m, float *adam_v, int32_t *adam_t, const float *packed,
+                              const int32_t *idx, const int32_t *count, int64_t first, int64_t num,
+                              const float *lr_cols, float *grads, uint8_t *touched, void *stream) {
+    if (!params || !adam_m || !adam_v || !adam_t || !idx || !count || !lr_cols || (!packed && !grads) || first < 0 ||
+        num < 0) {
+        set_error("gs_adam_packed: bad arguments");
+        return GS_ERR_ARG;
+    }
+    if (num == 0) return GS_OK;
+    const int64_t work = num * 16;
+    const unsigned blocks = (unsigned)std::min<int64_t>((work + 255) / 256, 16 * 148);
+    launch_pdl(adam_packed_kernel, blocks, 256, 0, (cudaStream_t)stream, params, adam_m, adam_v, adam_t, packed, idx,
+               count, first, num, lr_cols, grads, touched);
+    return check_launch("adam_packed_kernel");
 }
 
 namespace gs {

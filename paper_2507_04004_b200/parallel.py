@@ -7,6 +7,8 @@ views, accumulating parameter-row gradients and a touched mask.  The touched mas
 allreduce_grads is the dense single-collective form with the flag in padding column 63).  A
 touched Gaussian with zero gradient still steps: its moments decay (R/rasterizer.py:714-725).
 Every rank then applies the same sparse Adam step, so the replicas stay bitwise identical.
+`allreduce_grads` / `allreduce_grads_sparse` are the host-orchestrated (torch) forms of the
+reduction, kept for CPU / gloo use; `BatchMapOptimizer` reduces on the device.
 
 This is a deliberate, documented deviation from the reference's per-keyframe Adam
 (R/mapper.py:246-257): the batch oracle is sum of per-view gradients, union of touched,
@@ -57,7 +59,20 @@ def allreduce_grads_sparse(rows: torch.Tensor, touched: torch.Tensor, group=None
 
 
 class BatchMapOptimizer:
-    """Batched (optionally data-parallel) map optimisation over this rank's keyframes."""
+    """Batched (optionally data-parallel) map optimisation over this rank's keyframes.
+
+    A step: every view of the batch (this rank's share) runs forward -> loss -> backward ->
+    chain rule into (grads, touched) -- the view loop graph-captured once per batch; then the
+    touched masks are OR-ed across ranks (n bytes), the union is compacted in id order on the
+    device (gs_compact_flags), its rows gathered into one packed buffer (gs_gather_rows), summed
+    across ranks in CHUNKS collectives issued back to back, and each chunk's Adam step
+    (gs_adam_packed: straight from the packed rows, clearing the consumed gradient rows and
+    flags) runs as soon as its collective lands, overlapping the ones still on the wire.  The
+    union's size is the one host read per batch (it sizes the collective; the entry-overflow
+    flag of the batch's views rides along).  On one rank nothing is gathered: Adam reads the
+    gradient rows in place."""
+
+    CHUNKS = 4
 
     def __init__(self, gmap, keyframes, lrs: dict, lam: float = 0.2, xi: float = 0.005, group=None,
                  adam: AdamState | None = None, headroom: float = 1.3):
@@ -71,31 +86,51 @@ class BatchMapOptimizer:
         self.adam = adam if adam is not None else AdamState()
         self.adam.ensure(self.g)
         self.lr = lr_columns(lrs, self.dev)
+        self.headroom = headroom
         emax = 1
         for v in self.views:
             _, cnt = _bin_frame(self.g, v, True)
             emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
-        self.ws = Workspace(len(self.g), self.W, self.H, int(emax * headroom) + 4096, self.dev)
-        prime_workspace(self.ws, self.views[0].ptr, self.lam, self.xi)  # reflection tables, cleared images
+        self.ws = self._workspace(int(emax * headroom) + 4096)
         n = len(self.g)
         self.grads = torch.zeros((n, GS_ROW), dtype=torch.float32, device=self.dev)
-        self.sparse_allreduce = True  # two-phase allreduce of the touched rows only
         self.touched = torch.zeros(n, dtype=torch.uint8, device=self.dev)
+        self.idx = torch.zeros(max(n, 1), dtype=torch.int32, device=self.dev)
+        self.scratch = torch.zeros((n + 1023) // 1024 + 1, dtype=torch.int32, device=self.dev)
+        self.count = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self._h = torch.zeros(2, dtype=torch.int32).pin_memory()  # (union size, overflow) read back
+        self.packed = torch.zeros((0, 60), dtype=torch.float32, device=self.dev)
         self.cur = torch.empty_like(self.views[0].buf)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.graphs: dict = {}
+        self.union = 0
+        self.replayed = 0
+        self.keep_reduced = False  # tests: keep (union ids, reduced gradient rows) of the last batch
+        self.reduced = None
+
+    def _workspace(self, capacity: int) -> Workspace:
+        ws = Workspace(len(self.g), self.W, self.H, capacity, self.dev)
+        prime_workspace(ws, self.views[0].ptr, self.lam, self.xi)  # reflection tables, cleared images
+        return ws
+
+    def _world(self) -> int:
+        return dist.get_world_size(self.group) if dist.is_available() and dist.is_initialized() else 1
 
     def kernels_per_step(self, views: int | None = None) -> int:
         from .mapper import kernels_per_iteration
-        per_view = kernels_per_iteration(self.ws.tiles_x * self.ws.tiles_y)
-        return per_view * (views if views is not None else len(self.views)) + 2  # + adam, step counters
+        per_view = kernels_per_iteration(self.ws.tiles_x * self.ws.tiles_y, chain_only=True)
+        extra = 2 + (1 + self.CHUNKS if self._world() > 1 else 1)  # compaction 2, gather, Adam chunk(s)
+        return per_view * (views if views is not None else len(self.views)) + extra
 
     def accumulate(self, k: int) -> None:
         """forward -> loss -> backward -> chain rule of view k into (grads, touched)."""
         self.cur.copy_(self.views[k].buf)
         self._accumulate_cur()
 
-    def _accumulate_cur(self) -> None:
-        f, s, cur = self.ws.fptr, stream_ptr(), self.cur.data_ptr()
+    def _accumulate_cur(self, view_ptr: int | None = None) -> None:
+        f, s = self.ws.fptr, stream_ptr()
+        cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
@@ -103,6 +138,21 @@ class BatchMapOptimizer:
         call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_chain clears the rows it consumes
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
         self.loss_acc += self.ws.loss[0:1]
+        # an overflowed view contributed nothing: remember it for the batch's check
+        torch.maximum(self.overflow, self.ws.counters[_lib.CNT_OVERFLOW:_lib.CNT_OVERFLOW + 1], out=self.overflow)
+
+    def _views(self, view_ids) -> None:
+        """The batch's views, one CUDA graph replay per distinct view tuple."""
+        key = tuple(int(k) for k in view_ids)
+        gr = self.graphs.get(key)
+        if gr is None:
+            torch.cuda.current_stream().synchronize()
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                for k in key:
+                    self._accumulate_cur(self.views[k].ptr)
+            self.graphs[key] = gr
+        gr.replay()
 
     def attach_host_keyframes(self, keyframes) -> None:
         """Keyframes in pinned host memory, streamed per view (mapper.HostKeyframes)."""
@@ -113,19 +163,16 @@ class BatchMapOptimizer:
 
     def step_host(self, view_ids) -> None:
         """One batch over host keyframes: each view's image + K-list uploaded while the previous
-        view runs, then the allreduce and the Adam step; the batch loss is read back (D2H)."""
-        self.grads.zero_()
-        self.touched.zero_()
-        self.host.stream(view_ids, lambda j, k, view_ptr: self._accumulate_cur())
-        self._finish()
+        view runs, then the reduction and the Adam step; the batch loss is read back (D2H)."""
+        self.loss_acc.zero_()
+        self.host.stream(view_ids, lambda j, k, view_ptr: self._accumulate_cur(view_ptr), use_cur=False)
+        self._finish(lambda: self.host.stream(view_ids, lambda j, k, vp: self._accumulate_cur(vp), use_cur=False))
         self._h_loss.copy_(self.loss_acc, non_blocking=True)
 
     def step(self, view_ids) -> None:
-        self.grads.zero_()
-        self.touched.zero_()
-        for k in view_ids:
-            self.accumulate(int(k))
-        self._finish()
+        self.loss_acc.zero_()
+        self._views(view_ids)
+        self._finish(lambda: self._views(view_ids))
 
     def save_state(self) -> tuple:
         a = self.adam
@@ -136,11 +183,53 @@ class BatchMapOptimizer:
         for dst, src in zip((self.g.data, a.m_rows, a.v_rows, a.t_dev), state):
             dst.copy_(src)
 
-    def _finish(self) -> None:
-        if self.sparse_allreduce:
-            allreduce_grads_sparse(self.grads, self.touched, self.group)
-        else:
-            allreduce_grads(self.grads, self.touched, self.group)
-        call("gs_adam", self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
-             self.adam.t_dev.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), len(self.g),
-             self.lr.data_ptr(), stream_ptr())
+    def _finish(self, rerun) -> None:
+        s = stream_ptr()
+        world = self._world()
+        if world > 1:
+            dist.all_reduce(self.touched, op=dist.ReduceOp.MAX, group=self.group)
+        n = len(self.g)
+        call("gs_compact_flags", self.touched.data_ptr(), n, self.idx.data_ptr(), self.count.data_ptr(),
+             self.scratch.data_ptr(), s)
+        self._h[0:1].copy_(self.count, non_blocking=True)
+        self._h[1:2].copy_(self.overflow, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if int(self._h[1]):  # some view overflowed its entry capacity: redo the batch's views
+            torch.cuda.synchronize(self.dev)
+            self.grads.zero_()
+            self.touched.zero_()
+            self.overflow.zero_()
+            self.loss_acc.zero_()
+            self.ws = self._workspace(int(self.ws.capacity * 2))
+            self.graphs = {}
+            self.replayed += 1
+            rerun()
+            self._finish(rerun)
+            return
+        u = self.union = int(self._h[0])
+        adam_args = (self.g.data.data_ptr(), self.adam.m_rows.data_ptr(), self.adam.v_rows.data_ptr(),
+                     self.adam.t_dev.data_ptr())
+        if world == 1:
+            if self.keep_reduced:
+                ids = self.idx[:u].long()
+                self.reduced = (ids.clone(), self.grads[ids, :60].clone())
+            call("gs_adam_packed", *adam_args, None, self.idx.data_ptr(), self.count.data_ptr(), 0, u,
+                 self.lr.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), s)
+            return
+        if self.packed.shape[0] < u:
+            self.packed = torch.zeros((int(u * 1.25) + 1024, 60), dtype=torch.float32, device=self.dev)
+        call("gs_gather_rows", self.grads.data_ptr(), self.idx.data_ptr(), self.count.data_ptr(), u,
+             self.packed.data_ptr(), s)
+        bounds = [u * c // self.CHUNKS for c in range(self.CHUNKS + 1)]
+        works = [dist.all_reduce(self.packed[bounds[c]:bounds[c + 1]], op=dist.ReduceOp.SUM, group=self.group,
+                                 async_op=True) for c in range(self.CHUNKS)]
+        if self.keep_reduced:
+            for w in works:
+                w.wait()
+            self.reduced = (self.idx[:u].long().clone(), self.packed[:u].clone())
+        for c in range(self.CHUNKS):
+            works[c].wait()  # the compute stream waits for chunk c only
+            call("gs_adam_packed", *adam_args, self.packed.data_ptr(), self.idx.data_ptr(), self.count.data_ptr(),
+                 bounds[c], bounds[c + 1] - bounds[c], self.lr.data_ptr(), self.grads.data_ptr(),
+                 self.touched.data_ptr(), stream_ptr())
+        self.overflow.zero_()

@@ -535,6 +535,7 @@ def test_batch_optimizer_matches_batch_oracle():
     g = GaussianMap.from_rows(sc.rows)
     kfs = [M.Keyframe(R.camera_from(c), t, s) for c, t, s in zip(sc.cams, sc.targets, sc.sparse_depths)]
     eng = PAR.BatchMapOptimizer(g, kfs, R.default_lrs(3.0))
+    eng.keep_reduced = True
     eng.step(range(4))
     gsum = np.zeros((len(rows64), 59))
     tun = np.zeros(len(rows64), bool)
@@ -547,15 +548,19 @@ def test_batch_optimizer_matches_batch_oracle():
         gr, t, _ = O.backward(og, out, gc, gd, go)
         gsum += O.grads_to_rows(gr)
         tun |= t
-    assert np.array_equal(_np(eng.touched).astype(bool), tun)
-    ggpu = _np(eng.grads)[:, :59]
-    assert not ggpu[~tun].any()
+    ids, red = eng.reduced
+    tgpu = np.zeros(len(rows64), bool)
+    tgpu[_np(ids).astype(np.int64)] = True
+    assert np.array_equal(tgpu, tun)
+    ggpu = np.zeros((len(rows64), 59))
+    ggpu[_np(ids).astype(np.int64)] = _np(red)[:, :59]
+    assert not eng.grads.any() and not eng.touched.any()  # consumed by the packed Adam
     for k, (a, b) in GROUPS.items():  # near-camera Gaussians included
         assert normwise(ggpu[:, a:b], gsum[:, a:b]) < REL_TOL, k
     # the Adam step on the GPU's own gradients
     exp = rows64.copy()
     st = O.AdamState()
-    O.adam_rows(exp, ggpu.astype(np.float64), _np(eng.touched).astype(bool), st, O.default_lrs(3.0))
+    O.adam_rows(exp, ggpu.astype(np.float64), tgpu, st, O.default_lrs(3.0))
     assert np.max(np.abs(_np(g.rows())[:, :59] - exp)) < 1e-5
     assert np.array_equal(_np(eng.adam.t).astype(np.int64), st.t)
 

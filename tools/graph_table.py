@@ -22,13 +22,17 @@ for d in data:
 tot = sum(a["gpu__time_duration.sum"] for a in agg.values())
 lines = [f"Warm-cache graph replay (`ncu --cache-control none --clock-control none`), {iters} iterations; "
          f"per-iteration kernel time {tot / iters / 1e3:.1f} us (serialised by the profiler).", "",
-         "| kernel | launches/iter | us / launch | DRAM rd MB | DRAM wr MB | GB/s | share |", "|---|---|---|---|---|---|---|"]
+         "| kernel | launches/iter | us / launch | DRAM rd MB | DRAM wr MB | GB/s | warp instr (M) | issue active % | warps active % | share |",
+         "|---|---|---|---|---|---|---|---|---|---|"]
 for k, a in sorted(agg.items(), key=lambda x: -x[1]["gpu__time_duration.sum"]):
     n = a["n"]
     us = a["gpu__time_duration.sum"] / n / 1e3
     rd, wr = a["dram__bytes_read.sum"] / n / 1e6, a["dram__bytes_write.sum"] / n / 1e6
-    lines.append(f"| `{k}` | {n / iters:g} | {us:.1f} | {rd:.1f} | {wr:.1f} | {(rd + wr) / us * 1e3:.0f} | "
-                 f"{a['gpu__time_duration.sum'] / tot:.3f} |")
+    ins = a.get("smsp__inst_executed.sum", 0.0) / n / 1e6
+    iss = a.get("smsp__issue_active.avg.pct_of_peak_sustained_active", 0.0) / n
+    wa = a.get("sm__warps_active.avg.pct_of_peak_sustained_active", 0.0) / n
+    lines.append(f"| `{k}` | {n / iters:g} | {us:.1f} | {rd:.1f} | {wr:.1f} | {(rd + wr) / us * 1e3:.0f} | {ins:.1f} | "
+                 f"{iss:.0f} | {wa:.0f} | {a['gpu__time_duration.sum'] / tot:.3f} |")
 out = "\n".join(lines)
 print(out)
 if len(sys.argv) > 3:
