@@ -22,11 +22,7 @@ constexpr float NEG_HALF_LOG2E = -0.5f * GS_LOG2E;
 // q = a (dx + beta dy)^2 + gamma dy^2 (the factored conic of the splat record, common.cuh);
 // au = a (dx + beta dy) = a dx + b dy is returned for the mean gradient
 __device__ __forceinline__ float quad(float a, float beta, float gamma, float dx, float dy, float &au) {
-#ifdef GS_EXP_U64
-    const float u = (float)fma((double)beta, (double)dy, (double)dx);
-#else
     const float u = fmaf(beta, dy, dx);
-#endif
     au = a * u;
     return fmaf(au, u, gamma * dy * dy);
 }
@@ -39,14 +35,7 @@ __device__ __forceinline__ float quad(float a, float beta, float gamma, float dx
 // error ~2^-22; results below 2^-126 flush to 0, i.e. alpha < 1e-38): the blend and its adjoint
 // use the same alpha.
 
-// (GS_EXP_PRECISE / GS_EXP_BWD_F64: precision experiments of tools/build_variant.sh, not the product)
-__device__ __forceinline__ float blend_exp(float q) {
-#ifdef GS_EXP_PRECISE
-    return expf(-0.5f * q);
-#else
-    return fast_ex2(-0.5f * GS_LOG2E * q);
-#endif
-}
+__device__ __forceinline__ float blend_exp(float q) { return fast_ex2(NEG_HALF_LOG2E * q); }
 
 __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &araw, float &alpha, float &oma) {
     (void)omo;
@@ -334,71 +323,79 @@ __device__ __forceinline__ int col_field(unsigned lane) {
     return ((lane & 16u) ? 2 : 0) + ((lane & 8u) ? 1 : 0);
 }
 
-// One pixel's contribution to the 10 screen-space gradient fields of an entry, back-to-front
-// replay step (R/rasterizer.py:365-410): undoes the entry's 1 - alpha on T, accumulates into v
-// and advances the suffix sums S.  The quadratic and the mean gradient use the factored conic
-// of the splat record: a dx + b dy = a u and b dx + c dy = beta a u + gamma dy (u = dx + beta dy).
-#if defined(GS_EXP_BWD_F64) || defined(GS_EXP_STATE64)
-using bwd_t = double;
-#else
-using bwd_t = float;
-#endif
+// Paired fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: one instruction, two lanes): a backward
+// thread owns two pixels of one column (rows y and y + 8), whose replay steps are the same
+// instruction stream on different data.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
-struct BwdPixel {
-    float fx, fy;
-    bwd_t T, gc0, gc1, gc2, gd, go, S0, S1, S2, Sd, So;
-    int cnt;
+// The two pixels' replay state (R/rasterizer.py:365-410, run back to front from the final T).
+struct BwdPair {
+    float fx;                       // column (shared)
+    float2 fy;                      // rows
+    float2 T, gc0, gc1, gc2, gd, go, S0, S1, S2, Sd, So;
+    int cnt0, cnt1;
 };
 
-__device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const float4 &B, const float4 &C, bwd_t v[10]) {
-#ifdef GS_EXP_BWD_F64
-    const double dx = p.fx - (double)A.x, dy = p.fy - (double)A.y;
-    const double a = A.z, beta = A.w, gamma = B.x, op = B.y, dep = B.z;
-    const double u = dx + beta * dy, au = a * u;
-    const double e = exp(-0.5 * (au * u + gamma * dy * dy));
-    const double araw = op * e;
-    const bool clamped = araw > (double)GS_ALPHA_CLAMP;
-    const double alpha = clamped ? (double)GS_ALPHA_CLAMP : araw;
-    const double om = clamped ? 1.0 - (double)GS_ALPHA_CLAMP : 1.0 - op * e;
-    const double rom = 1.0 / om;
-#else
-    const float dx = p.fx - A.x, dy = p.fy - A.y;
+// One entry's contribution of both pixels to the 10 screen-space gradient fields (v[k] holds
+// the two pixels' terms in .x / .y): undoes the entry's 1 - alpha on T, accumulates, advances
+// the suffix sums.  alpha is computed exactly as the forward computes it (same operation order:
+// quad(), fast_ex2, fmaf(-op, e, 1)), so the replay divides out precisely what the blend
+// multiplied in.  The quadratic and the mean gradient use the factored conic of the splat
+// record: a dx + b dy = a u and b dx + c dy = beta a u + gamma dy (u = dx + beta dy).
+__device__ __forceinline__ void bwd_step2(BwdPair &p, bool act0, bool act1, const float4 &A, const float4 &B,
+                                          const float4 &C, float2 v[10]) {
+    const float dx = p.fx - A.x;
+    const float2 dy = add2(p.fy, f2(-A.y));
     const float a = A.z, beta = A.w, gamma = B.x, op = B.y, dep = B.z;
-    float au;
-    const float e = blend_exp(quad(a, beta, gamma, dx, dy, au));
-    const float araw = op * e;
-    const bool clamped = araw > GS_ALPHA_CLAMP;
-    const float alpha = clamped ? GS_ALPHA_CLAMP : araw;
-    const float om = clamped ? 0.01f : fmaf(-op, e, 1.0f);
-#ifdef GS_EXP_PRECISE
-    const float rom = 1.0f / om;
-#else
-    const float rom = fast_rcp(om);
-#endif
-#endif
-    const bwd_t Tb = p.T * rom;
-    const bwd_t w = alpha * Tb;
-    v[6] += w * p.gc0;
-    v[7] += w * p.gc1;
-    v[8] += w * p.gc2;
-    v[9] += w * p.gd;
-    const bwd_t dl = Tb * (C.x * p.gc0 + C.y * p.gc1 + C.z * p.gc2 + dep * p.gd + p.go) -
-                     (p.S0 * p.gc0 + p.S1 * p.gc1 + p.S2 * p.gc2 + p.Sd * p.gd + p.So * p.go) * rom;
-    if (!clamped) {  // no alpha-chain gradient on the 0.99 clamp (R/rasterizer.py:399-404)
-        const bwd_t gq = dl * (bwd_t)(-0.5f * alpha);
-        v[5] += dl * e;  // d alpha / d opacity = e
-        v[2] += gq * dx * dx;
-        v[3] += gq * 2 * dx * dy;
-        v[4] += gq * dy * dy;
-        v[0] += gq * (-2 * au);
-        v[1] += gq * (-2 * (beta * au + gamma * dy));
-    }
-    p.S0 += C.x * w;
-    p.S1 += C.y * w;
-    p.S2 += C.z * w;
-    p.Sd += dep * w;
-    p.So += w;
-    p.T = Tb;
+    const float2 u = fma2(f2(beta), dy, f2(dx));
+    const float2 au = mul2(f2(a), u);
+    const float2 q = fma2(au, u, mul2(mul2(f2(gamma), dy), dy));
+    const float2 hq = mul2(f2(NEG_HALF_LOG2E), q);
+    const float2 e = make_float2(fast_ex2(hq.x), fast_ex2(hq.y));
+    const float2 araw = mul2(f2(op), e);
+    const bool c0 = araw.x > GS_ALPHA_CLAMP, c1 = araw.y > GS_ALPHA_CLAMP;
+    const float2 alpha = make_float2(c0 ? GS_ALPHA_CLAMP : araw.x, c1 ? GS_ALPHA_CLAMP : araw.y);
+    float2 om = fma2(f2(-op), e, f2(1.0f));
+    om = make_float2(c0 ? 0.01f : om.x, c1 ? 0.01f : om.y);
+    const float2 rom = make_float2(fast_rcp(om.x), fast_rcp(om.y));
+    const float2 Tb = mul2(p.T, rom);
+    float2 w = mul2(alpha, Tb);
+    w = make_float2(act0 ? w.x : 0.0f, act1 ? w.y : 0.0f);  // a finished pixel takes no part
+    v[6] = fma2(w, p.gc0, v[6]);
+    v[7] = fma2(w, p.gc1, v[7]);
+    v[8] = fma2(w, p.gc2, v[8]);
+    v[9] = fma2(w, p.gd, v[9]);
+    float2 own = fma2(f2(C.x), p.gc0, p.go);
+    own = fma2(f2(C.y), p.gc1, own);
+    own = fma2(f2(C.z), p.gc2, own);
+    own = fma2(f2(dep), p.gd, own);
+    float2 suf = mul2(p.So, p.go);
+    suf = fma2(p.S0, p.gc0, suf);
+    suf = fma2(p.S1, p.gc1, suf);
+    suf = fma2(p.S2, p.gc2, suf);
+    suf = fma2(p.Sd, p.gd, suf);
+    const float2 dl = fma2(Tb, own, mul2(f2(-1.0f), mul2(suf, rom)));
+    // no alpha-chain gradient on the 0.99 clamp (R/rasterizer.py:399-404), none from a finished pixel
+    const bool g0 = act0 && !c0, g1 = act1 && !c1;
+    float2 gq = mul2(dl, mul2(f2(-0.5f), alpha));
+    gq = make_float2(g0 ? gq.x : 0.0f, g1 ? gq.y : 0.0f);
+    float2 de = mul2(dl, e);  // d alpha / d opacity = e
+    de = make_float2(g0 ? de.x : 0.0f, g1 ? de.y : 0.0f);
+    v[5] = add2(v[5], de);
+    v[2] = fma2(gq, f2(dx * dx), v[2]);
+    v[3] = fma2(gq, mul2(f2(2.0f * dx), dy), v[3]);
+    v[4] = fma2(mul2(gq, dy), dy, v[4]);
+    v[0] = fma2(gq, mul2(f2(-2.0f), au), v[0]);
+    v[1] = fma2(gq, mul2(f2(-2.0f), fma2(f2(beta), au, mul2(f2(gamma), dy))), v[1]);
+    p.S0 = fma2(f2(C.x), w, p.S0);
+    p.S1 = fma2(f2(C.y), w, p.S1);
+    p.S2 = fma2(f2(C.z), w, p.S2);
+    p.Sd = fma2(f2(dep), w, p.Sd);
+    p.So = add2(p.So, w);
+    p.T = make_float2(act0 ? Tb.x : p.T.x, act1 ? Tb.y : p.T.y);
 }
 
 // 128 threads per 16x16 tile, two pixels per thread (rows y and y + 8): the two pixels'
@@ -406,11 +403,7 @@ __device__ __forceinline__ void bwd_step(BwdPixel &p, const float4 &A, const flo
 // entry every warp stores its butterfly sums in its own shared-memory slot, the four warp sums
 // are added in warp order, and the tile partial goes to the Gaussian's row through fixed-point
 // integer atomics (fx_atomic_add) -- no floating-point sum depends on scheduling order.
-#ifndef GS_BPX
-#define GS_BPX 2
-#endif
-constexpr int BPX = GS_BPX;         // pixels per backward thread (one column, rows 16 / BPX apart)
-constexpr int BT = RT / BPX;        // backward threads per tile
+constexpr int BT = RT / 2;          // backward threads per tile (two pixels each)
 constexpr int BW = BT / 32;         // warps per backward CTA
 constexpr int BST = BT / 2;         // entries staged per round
 
@@ -428,8 +421,8 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
     const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
     if (clear_depth_grads && stop == start) {  // (GS_BWD_CLEAR_DEPTH_GRADS) an empty tile's pixels
 #pragma unroll
-        for (int k = 0; k < BPX; k++) {
-            const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / BPX) * k;
+        for (int k = 0; k < 2; k++) {
+            const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / 2) * k;
             if (x < f.width && y < f.height) {
                 const int64_t q = (int64_t)y * f.width + x;
                 if (f.g_depth[q] != 0.0f) f.g_depth[q] = 0.0f;
@@ -457,38 +450,44 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         // lazy, unflagged: the blend ended within the leading screen-covering Gaussians
         return lazy ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : f.entry_splat[start + p];
     };
-    BwdPixel px[BPX];
+    BwdPair px;
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
-    int mc = 0;
+    {
+        const int x = tx * GS_TILE + (threadIdx.x & 15), y0 = ty * GS_TILE + (threadIdx.x >> 4);
+        px.fx = (float)x;
+        px.fy = make_float2((float)y0, (float)(y0 + GS_TILE / 2));
+        float T[2] = {1.0f, 1.0f}, gc[2][3] = {}, gd[2] = {}, go[2] = {};
+        int cnt[2] = {0, 0};
 #pragma unroll
-    for (int k = 0; k < BPX; k++) {
-        BwdPixel &p = px[k];
-        const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / BPX) * k;
-        p.fx = (float)x;
-        p.fy = (float)y;
-        p.T = 1.0f;
-        p.gc0 = p.gc1 = p.gc2 = p.gd = p.go = 0.0f;
-        p.S0 = p.S1 = p.S2 = p.Sd = p.So = 0.0f;
-        p.cnt = 0;
-        if (x < f.width && y < f.height) {
-            const int64_t q = (int64_t)y * f.width + x;
-            p.T = f.trans[q];
-            p.cnt = f.n_contrib[q];
-            p.gc0 = f.g_color[3 * q];
-            p.gc1 = f.g_color[3 * q + 1];
-            p.gc2 = f.g_color[3 * q + 2];
-            p.gd = f.g_depth[q];
-            p.go = f.g_opac[q];
-            if (clear_depth_grads) {  // nonzero only at the view's LiDAR pixels
-                if (p.gd != 0.0f) f.g_depth[q] = 0.0f;
-                if (p.go != 0.0f) f.g_opac[q] = 0.0f;
+        for (int k = 0; k < 2; k++) {
+            const int y = y0 + (GS_TILE / 2) * k;
+            if (x < f.width && y < f.height) {
+                const int64_t q = (int64_t)y * f.width + x;
+                T[k] = f.trans[q];
+                cnt[k] = f.n_contrib[q];
+                gc[k][0] = f.g_color[3 * q];
+                gc[k][1] = f.g_color[3 * q + 1];
+                gc[k][2] = f.g_color[3 * q + 2];
+                gd[k] = f.g_depth[q];
+                go[k] = f.g_opac[q];
+                if (clear_depth_grads) {  // nonzero only at the view's LiDAR pixels
+                    if (gd[k] != 0.0f) f.g_depth[q] = 0.0f;
+                    if (go[k] != 0.0f) f.g_opac[q] = 0.0f;
+                }
             }
         }
+        px.T = make_float2(T[0], T[1]);
+        px.gc0 = make_float2(gc[0][0], gc[1][0]);
+        px.gc1 = make_float2(gc[0][1], gc[1][1]);
+        px.gc2 = make_float2(gc[0][2], gc[1][2]);
+        px.gd = make_float2(gd[0], gd[1]);
+        px.go = make_float2(go[0], go[1]);
+        px.S0 = px.S1 = px.S2 = px.Sd = px.So = f2(0.0f);
+        px.cnt0 = cnt[0];
+        px.cnt1 = cnt[1];
+        atomicMax(&s_max, max(cnt[0], cnt[1]));
     }
-#pragma unroll
-    for (int k = 0; k < BPX; k++) mc = max(mc, px[k].cnt);
-    atomicMax(&s_max, mc);
     __syncthreads();
     const int max_cnt = s_max;
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
@@ -507,21 +506,20 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         __syncthreads();
         for (int j = nb - 1; j >= 0; j--) {
             const int le = b0 + j - start;
-            bool any = false;
-#pragma unroll
-            for (int k = 0; k < BPX; k++) any |= le < px[k].cnt;
+            const bool a0 = le < px.cnt0, a1 = le < px.cnt1;
             double sg = 0.0;
             float sc = 0.0f;
-            if (__any_sync(0xffffffffu, any)) {
+            if (__any_sync(0xffffffffu, a0 || a1)) {
                 const float4 A = s_a[j], B = s_b[j], C = s_c[j];
-                bwd_t v[10];
+                float2 v[10];
 #pragma unroll
-                for (int k = 0; k < 10; k++) v[k] = 0;
+                for (int k = 0; k < 10; k++) v[k] = f2(0.0f);
+                bwd_step2(px, a0, a1, A, B, C, v);
+                float vg[6], vc[4];
 #pragma unroll
-                for (int k = 0; k < BPX; k++)
-                    if (le < px[k].cnt) bwd_step(px[k], A, B, C, v);
-                const float vg[6] = {(float)v[0], (float)v[1], (float)v[2], (float)v[3], (float)v[4], (float)v[5]};
-                const float vc[4] = {(float)v[6], (float)v[7], (float)v[8], (float)v[9]};
+                for (int k = 0; k < 6; k++) vg[k] = v[k].x + v[k].y;
+#pragma unroll
+                for (int k = 0; k < 4; k++) vc[k] = v[6 + k].x + v[6 + k].y;
                 sg = reduce_geo(vg);
                 sc = reduce_col(vc);
             }
