@@ -23,7 +23,8 @@ constexpr int TW = 32, TH = 16;
 constexpr int NIR = TH + 20;          // input rows (halo 10)
 constexpr int HXC = TW + 10;          // horizontal-moment columns (strips of 6 / 3)
 constexpr int HXS = HXC + 1;          // their row stride (odd)
-constexpr int NIC = HXC + 11;         // input row stride (odd, >= HXC + 10); columns >= TW + 20 are 0
+constexpr int NIC = HXC + 12;         // input row stride in float2 (even: 16-B aligned rows for pairwise
+                                      // LDS.128; >= HXC + 10); columns >= TW + 20 are never read
 constexpr int GR = TH + 10;           // SSIM-map rows (halo 5)
 constexpr int GW = TW + 10;           // SSIM-map columns
 constexpr int GC = GW + 1;            // SSIM-map / vertical-adjoint row stride (odd)
@@ -103,12 +104,21 @@ __device__ __forceinline__ void split32(int it, int groups, int len, int &group,
 
 // INTERIOR: the CTA's whole halo lies >= 10 px inside the image, so every blur / adjoint
 // weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
+// The moments travel in pairs -- (a, b) and (a^2 + b^2, ab) through the blurs, (dS/dua, dS/dsig)
+// through the adjoint -- so every tap of every pass is one paired FMA (sm_100 FFMA2) per pair.
 struct SsimSmem {
-    float in[2][NIR][NIC];  // rendered / target channel; later the SSIM partials g[3][GR][GC]
-    float hx[4][NIR][HXS];  // horizontal moments; later the vertical adjoint ry[3][TH][GC]
+    union {
+        float2 in[NIR][NIC];  // (rendered, target) of the channel
+        float4 g[GR][GC];     // SSIM partials (d/d mu_a, d/d (var sum), d/d sigma_ab, -)
+    } u1;
+    union {
+        float4 hx[NIR][HXS];  // horizontal moments (a, b, aa + bb, ab)
+        float4 ry[TH][GC];    // vertical adjoint of the three partial images
+    } u2;
     float red[2][L_THREADS / 32];
 };
-static_assert(3 * GR * GC <= 2 * NIR * NIC && 3 * TH * GC <= 4 * NIR * HXS, "smem aliasing");
+
+__device__ __forceinline__ float2 pfma(float w, float2 x, float2 acc) { return __ffma2_rn(make_float2(w, w), x, acc); }
 
 template <bool INTERIOR>
 __device__ __forceinline__ float wtab(const float *__restrict__ tab, int pos, int d) {
@@ -119,8 +129,6 @@ template <bool INTERIOR>
 __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
                                           const float *__restrict__ tab_x, const float *__restrict__ tab_y,
                                           float lam, int depth_grads_zero) {
-    float(*g)[GR][GC] = reinterpret_cast<float(*)[GR][GC]>(&sm.in[0][0][0]);
-    float(*ry)[TH][GC] = reinterpret_cast<float(*)[TH][GC]>(&sm.hx[0][0][0]);
     const float *__restrict__ target = view->target;
     const float *__restrict__ color = f.color;
     const int W = f.width, H = f.height;
@@ -165,10 +173,7 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
 #pragma unroll
             for (int h = 0; h < CP; h++) {
                 const int ix = lane + 32 * h;
-                if (iy < NIR && ix < TW + 20) {
-                    sm.in[0][iy][ix] = va[j][h];
-                    sm.in[1][iy][ix] = vb[j][h];
-                }
+                if (iy < NIR && ix < TW + 20) sm.u1.in[iy][ix] = make_float2(va[j][h], vb[j][h]);
             }
         }
     }
@@ -178,58 +183,58 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     //    <-> x = x0-5+j
     for (int it = tid; it < NIR * (HXC / HB); it += L_THREADS) {
         // warp-aligned items: rows 0..31 of a strip per warp, then the last NIR - 32 rows of every
-        // strip (odd row stride: a warp's 32 rows hit 32 banks)
+        // strip (odd row stride: a warp's 32 rows hit distinct banks)
         int iy, c0;
         split32(it, HXC / HB, NIR, c0, iy);
         c0 *= HB;
-        float m[4][HB];
+        float2 m01[HB], m23[HB];
 #pragma unroll
-        for (int k = 0; k < HB; k++) m[0][k] = m[1][k] = m[2][k] = m[3][k] = 0.0f;
+        for (int k = 0; k < HB; k++) m01[k] = m23[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
-        for (int t = 0; t < HB + 10; t++) {
-            const float at = sm.in[0][iy][c0 + t], bt = sm.in[1][iy][c0 + t];
-            const float ss = fmaf(at, at, bt * bt), ab = at * bt;
+        for (int t2 = 0; t2 < (HB + 10) / 2; t2++) {  // two input columns per 16-B load
+            const float4 in2 = *reinterpret_cast<const float4 *>(&sm.u1.in[iy][c0 + 2 * t2]);
 #pragma unroll
-            for (int k = 0; k < HB; k++) {
-                const int d = t - k;
-                if (d >= 0 && d < 11) {
-                    const float w = kw(d);
-                    m[0][k] += w * at;
-                    m[1][k] += w * bt;
-                    m[2][k] += w * ss;
-                    m[3][k] += w * ab;
+            for (int h = 0; h < 2; h++) {
+                const int t = 2 * t2 + h;
+                const float2 ab = h ? make_float2(in2.z, in2.w) : make_float2(in2.x, in2.y);
+                const float2 q = make_float2(fmaf(ab.x, ab.x, ab.y * ab.y), ab.x * ab.y);
+#pragma unroll
+                for (int k = 0; k < HB; k++) {
+                    const int d = t - k;
+                    if (d >= 0 && d < 11) {
+                        m01[k] = pfma(kw(d), ab, m01[k]);
+                        m23[k] = pfma(kw(d), q, m23[k]);
+                    }
                 }
             }
         }
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-#pragma unroll
-            for (int k = 0; k < HB; k++) sm.hx[q][iy][c0 + k] = m[q][k];
+        for (int k = 0; k < HB; k++) sm.u2.hx[iy][c0 + k] = make_float4(m01[k].x, m01[k].y, m23[k].x, m23[k].y);
     }
     __syncthreads();
     // 3) vertical blur -> SSIM map and its partials (R/losses.py:96-113); g row gy <-> y0-5+gy
     float s_acc = 0.0f;
+    float2 g01v[VS];
+    float g2v[VS];
     for (int it = tid; it < GW * NVS; it += L_THREADS) {
         int gx, gy0;  // warp-aligned items: 32 consecutive columns of one strip per warp
         split32(it, NVS, GW, gy0, gx);
         gy0 *= VS;
         const int x = x0 - 5 + gx;
-        float u[4][VS];
+        float2 u01[VS], u23[VS];
 #pragma unroll
-        for (int k = 0; k < VS; k++) u[0][k] = u[1][k] = u[2][k] = u[3][k] = 0.0f;
+        for (int k = 0; k < VS; k++) u01[k] = u23[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
         for (int r = 0; r < VS + 10; r++) {
             if (gy0 + r < NIR) {
-                float h[4];
-#pragma unroll
-                for (int q = 0; q < 4; q++) h[q] = sm.hx[q][gy0 + r][gx];
+                const float4 h = sm.u2.hx[gy0 + r][gx];
+                const float2 h01 = make_float2(h.x, h.y), h23 = make_float2(h.z, h.w);
 #pragma unroll
                 for (int k = 0; k < VS; k++) {
                     const int d = r - k;
                     if (d >= 0 && d < 11) {
-                        const float w = kw(d);
-#pragma unroll
-                        for (int q = 0; q < 4; q++) u[q][k] += w * h[q];
+                        u01[k] = pfma(kw(d), h01, u01[k]);
+                        u23[k] = pfma(kw(d), h23, u23[k]);
                     }
                 }
             }
@@ -237,28 +242,27 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
 #pragma unroll
         for (int k = 0; k < VS; k++) {
             const int gy = gy0 + k, y = y0 - 5 + gy;
-            if (gy < GR) {
-                float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-                if (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H)) {
-                    const float ua = u[0][k], ub = u[1][k];
-                    const float vab = u[3][k] - ua * ub;
-                    const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
-                    const float uu = ua * ua + ub * ub;
-                    const float b1 = uu + C1, b2 = (u[2][k] - uu) + C2;  // va + vb + C2
-                    // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
-                    const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
-                    const float S = (a1 * a2) * rden;
-                    g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) *
-                         inv_n;
-                    g1 = (-S * rb2) * inv_n;
-                    g2 = (2.0f * a1 * rden) * inv_n;
-                    if (gy >= 5 && gy < 5 + TH && gx >= 5 && gx < 5 + TW) s_acc += S;
-                }
-                g[0][gy][gx] = g0;
-                g[1][gy][gx] = g1;
-                g[2][gy][gx] = g2;
+            float g0 = 0.f, g1 = 0.f, g2 = 0.f;
+            if (gy < GR && (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H))) {
+                const float ua = u01[k].x, ub = u01[k].y;
+                const float vab = u23[k].y - ua * ub;
+                const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
+                const float uu = ua * ua + ub * ub;
+                const float b1 = uu + C1, b2 = (u23[k].x - uu) + C2;  // va + vb + C2
+                // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
+                const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
+                const float S = (a1 * a2) * rden;
+                g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) * inv_n;
+                g1 = (-S * rb2) * inv_n;
+                g2 = (2.0f * a1 * rden) * inv_n;
+                if (gy >= 5 && gy < 5 + TH && gx >= 5 && gx < 5 + TW) s_acc += S;
             }
+            g01v[k] = make_float2(g0, g1);
+            g2v[k] = g2;
         }
+#pragma unroll
+        for (int k = 0; k < VS; k++)
+            if (gy0 + k < GR) sm.u1.g[gy0 + k][gx] = make_float4(g01v[k].x, g01v[k].y, g2v[k], 0.0f);
     }
     __syncthreads();
     // 4) vertical adjoint at rows [y0, y0+TH): r(p) = sum_d A[p][d] g(p+d) (zero weights where
@@ -267,30 +271,33 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
         int gx, oy0;
         split32(it, NAS, GW, oy0, gx);
         oy0 *= AS;
-        float r3[3][AS];
+        float2 r01[AS];
+        float r2[AS];
 #pragma unroll
-        for (int k = 0; k < AS; k++) r3[0][k] = r3[1][k] = r3[2][k] = 0.0f;
+        for (int k = 0; k < AS; k++) {
+            r01[k] = make_float2(0.0f, 0.0f);
+            r2[k] = 0.0f;
+        }
 #pragma unroll
         for (int r = 0; r < AS + 10; r++) {
-            const float h0 = g[0][oy0 + r][gx], h1 = g[1][oy0 + r][gx], h2 = g[2][oy0 + r][gx];
+            const float4 hg = sm.u1.g[oy0 + r][gx];
+            const float2 h01 = make_float2(hg.x, hg.y);
+            const float h2 = hg.z;
 #pragma unroll
             for (int k = 0; k < AS; k++) {
                 const int d = r - k;
                 if (d >= 0 && d < 11) {
                     const int yp = min(y0 + oy0 + k, H - 1);
                     const float w = wtab<INTERIOR>(tab_y + 11, yp, d);
-                    r3[0][k] += w * h0;
-                    r3[1][k] += w * h1;
-                    r3[2][k] += w * h2;
+                    r01[k] = pfma(w, h01, r01[k]);
+                    r2[k] = fmaf(w, h2, r2[k]);
                 }
             }
         }
 #pragma unroll
         for (int k = 0; k < AS; k++) {
             const bool ok = INTERIOR || y0 + oy0 + k < H;
-            ry[0][oy0 + k][gx] = ok ? r3[0][k] : 0.0f;
-            ry[1][oy0 + k][gx] = ok ? r3[1][k] : 0.0f;
-            ry[2][oy0 + k][gx] = ok ? r3[2][k] : 0.0f;
+            sm.u2.ry[oy0 + k][gx] = ok ? make_float4(r01[k].x, r01[k].y, r2[k], 0.0f) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
     }
     __syncthreads();
@@ -298,25 +305,31 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
     //    covers 16 rows x 2 strips
     float l1_acc = 0.0f;
     {
-        // lanes 0-15: strip w, lanes 16-31: strip w + 8 (16 banks apart: conflict-free rows)
+        // lanes 0-15: strip w, lanes 16-31: strip w + 8
         const int oy = tid & 15, ox0 = HS * ((tid >> 5) + 8 * ((tid >> 4) & 1));
-        float A[3][HS];
+        float2 A01[HS];
+        float A2[HS];
 #pragma unroll
-        for (int k = 0; k < HS; k++) A[0][k] = A[1][k] = A[2][k] = 0.0f;
+        for (int k = 0; k < HS; k++) {
+            A01[k] = make_float2(0.0f, 0.0f);
+            A2[k] = 0.0f;
+        }
 #pragma unroll
-        for (int q = 0; q < 3; q++)
+        for (int t = 0; t < HS + 10; t++) {
+            const float4 rv = sm.u2.ry[oy][ox0 + t];
+            const float2 v01 = make_float2(rv.x, rv.y);
+            const float v2 = rv.z;
 #pragma unroll
-            for (int t = 0; t < HS + 10; t++) {
-                const float v = ry[q][oy][ox0 + t];
-#pragma unroll
-                for (int k = 0; k < HS; k++) {
-                    const int d = t - k;
-                    if (d >= 0 && d < 11) {
-                        const int xp = min(x0 + ox0 + k, W - 1);
-                        A[q][k] += wtab<INTERIOR>(tab_x + 11, xp, d) * v;
-                    }
+            for (int k = 0; k < HS; k++) {
+                const int d = t - k;
+                if (d >= 0 && d < 11) {
+                    const int xp = min(x0 + ox0 + k, W - 1);
+                    const float w = wtab<INTERIOR>(tab_x + 11, xp, d);
+                    A01[k] = pfma(w, v01, A01[k]);
+                    A2[k] = fmaf(w, v2, A2[k]);
                 }
             }
+        }
         const int y = y0 + oy;
 #pragma unroll
         for (int k = 0; k < HS; k++) {
@@ -328,7 +341,7 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                 l1_acc += fabsf(diff);
                 const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
                 f.g_color[3 * p + c] =
-                    (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A[0][k] + 2.0f * a * A[1][k] + b * A[2][k]));
+                    (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A01[k].x + 2.0f * a * A01[k].y + b * A2[k]));
                 // the depth/opacity gradient images start at zero (the LiDAR kernel follows; under
                 // GS_LOSS_DEPTH_GRADS_ZERO they already are, and the LiDAR kernel runs alongside)
                 if (c == 0 && !depth_grads_zero) {
