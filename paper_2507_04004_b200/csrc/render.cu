@@ -50,6 +50,33 @@ __device__ __forceinline__ void alpha_oma(float op, float omo, float q, float &a
     }
 }
 
+// Paired fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: one instruction, two lanes): the forward
+// and backward threads own two pixels of one column (rows y and y + 8), whose blend / replay
+// steps are the same instruction stream on different data.
+__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+
+// alpha, 1 - alpha and the exponential of an entry for two pixels of one column, with exactly
+// the operations of the scalar quad() / blend_exp() / alpha_oma() (IEEE per lane, same order), so
+// every kernel sees bit-identical alphas
+__device__ __forceinline__ void alpha2(const float4 &A, const float4 &B, float dx, float2 dy, float2 &au, float2 &e,
+                                       float2 &alpha, float2 &om, bool &c0, bool &c1) {
+    const float a = A.z, beta = A.w, gamma = B.x, op = B.y;
+    const float2 u = fma2(f2(beta), dy, f2(dx));
+    au = mul2(f2(a), u);
+    const float2 q = fma2(au, u, mul2(mul2(f2(gamma), dy), dy));
+    const float2 hq = mul2(f2(NEG_HALF_LOG2E), q);
+    e = make_float2(fast_ex2(hq.x), fast_ex2(hq.y));
+    const float2 araw = mul2(f2(op), e);
+    c0 = araw.x > GS_ALPHA_CLAMP;
+    c1 = araw.y > GS_ALPHA_CLAMP;
+    alpha = make_float2(c0 ? GS_ALPHA_CLAMP : araw.x, c1 ? GS_ALPHA_CLAMP : araw.y);
+    om = fma2(f2(-op), e, f2(1.0f));
+    om = make_float2(c0 ? 0.01f : om.x, c1 ? 0.01f : om.y);
+}
+
 // One pixel's blend state (R/rasterizer.py:256-291).  Opacity is accumulated as sum(w) (== 1 - T
 // exactly in real arithmetic): 1 - T in fp32 cancels for nearly transparent pixels, and the
 // depth loss divides by it.
@@ -57,6 +84,14 @@ struct FwdPixel {
     float fx, fy, T, c0, c1, c2, dsum, osum;
     int cnt;
     bool inside, done;
+};
+
+// Two pixels of one column (rows y and y + 8): the paired forward thread.
+struct FwdPair {
+    float fx;
+    float2 fy, T, c0, c1, c2, dsum, osum;
+    int cnt0, cnt1;
+    bool in0, in1, done0, done1;
 };
 
 struct FwdStage {
@@ -94,6 +129,94 @@ __device__ __forceinline__ void fwd_pixel_store(const gs_frame &f, int tile, con
     f.opacity[q] = p.osum;
     f.trans[q] = p.T;
     f.n_contrib[q] = p.cnt;
+}
+
+__device__ __forceinline__ FwdPair fwd_pair_init(const gs_frame &f, int tile) {
+    FwdPair p;
+    const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
+    const int px = tx * GS_TILE + (threadIdx.x & 15), py = ty * GS_TILE + (threadIdx.x >> 4);
+    p.in0 = px < f.width && py < f.height;
+    p.in1 = px < f.width && py + GS_TILE / 2 < f.height;
+    p.fx = (float)px;
+    p.fy = make_float2((float)py, (float)(py + GS_TILE / 2));
+    p.T = f2(1.0f);
+    p.c0 = p.c1 = p.c2 = p.dsum = p.osum = f2(0.0f);
+    p.cnt0 = p.cnt1 = 0;
+    p.done0 = !p.in0;
+    p.done1 = !p.in1;
+    return p;
+}
+
+__device__ __forceinline__ void fwd_pair_store(const gs_frame &f, int tile, const FwdPair &p) {
+    const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
+    const int64_t q0 = (int64_t)(ty * GS_TILE + (threadIdx.x >> 4)) * f.width + tx * GS_TILE + (threadIdx.x & 15);
+#pragma unroll
+    for (int h = 0; h < 2; h++) {
+        if (!(h ? p.in1 : p.in0)) continue;
+        const int64_t q = q0 + (int64_t)h * (GS_TILE / 2) * f.width;
+        f.color[3 * q] = h ? p.c0.y : p.c0.x;
+        f.color[3 * q + 1] = h ? p.c1.y : p.c1.x;
+        f.color[3 * q + 2] = h ? p.c2.y : p.c2.x;
+        f.depth[q] = h ? p.dsum.y : p.dsum.x;
+        f.opacity[q] = h ? p.osum.y : p.osum.x;
+        f.trans[q] = h ? p.T.y : p.T.x;
+        f.n_contrib[q] = h ? p.cnt1 : p.cnt0;
+    }
+}
+
+// The paired form of blend_range (FT = 128 threads, two pixels each): same staging, same
+// per-pixel termination, alphas bit-identical to the scalar path.
+constexpr int FT = RT / 2;
+
+template <typename Fetch>
+__device__ __forceinline__ bool blend_range2(const gs_frame &f, FwdPair &px, FwdStage &st, int p0, int p1,
+                                             int early_stop, Fetch fetch) {
+    const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
+    for (int b = p0, step = FT / 2; b < p1; b += step, step = FT) {
+        if (__syncthreads_count(px.done0 && px.done1) == FT) return true;
+        const int e = b + threadIdx.x;
+        if ((int)threadIdx.x < step && e < p1) {
+            const int64_t g = fetch(e);
+            st.a[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g);
+            st.b[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 1);
+            st.c[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 2);
+        }
+        __syncthreads();
+        const int nb = min(step, p1 - b);
+        for (int j = 0; j < nb && !(px.done0 && px.done1); j++) {
+            const float4 A = st.a[j], B = st.b[j], C = st.c[j];
+            const float dx = px.fx - A.x;
+            const float2 dy = add2(px.fy, f2(-A.y));
+            float2 au, ev, alpha, om;
+            bool c0, c1;
+            alpha2(A, B, dx, dy, au, ev, alpha, om, c0, c1);
+            float2 w = mul2(alpha, px.T);
+            w = make_float2(px.done0 ? 0.0f : w.x, px.done1 ? 0.0f : w.y);
+            px.c0 = fma2(f2(C.x), w, px.c0);
+            px.c1 = fma2(f2(C.y), w, px.c1);
+            px.c2 = fma2(f2(C.z), w, px.c2);
+            px.dsum = fma2(f2(B.z), w, px.dsum);
+            px.osum = add2(px.osum, w);
+            const float2 Tn = mul2(px.T, om);
+            if (!px.done0) {
+                px.T.x = Tn.x;
+                if (early_stop && Tn.x < GS_EARLY_STOP_T) {
+                    px.done0 = true;
+                    px.cnt0 = b + j + 1;
+                }
+            }
+            if (!px.done1) {
+                px.T.y = Tn.y;
+                if (early_stop && Tn.y < GS_EARLY_STOP_T) {
+                    px.done1 = true;
+                    px.cnt1 = b + j + 1;
+                }
+            }
+        }
+        if (!px.done0) px.cnt0 = b + nb;
+        if (!px.done1) px.cnt1 = b + nb;
+    }
+    return __syncthreads_count(px.done0 && px.done1) == FT;
 }
 
 // Blends list positions [p0, p1) of the tile front to back; fetch(p) -> Gaussian id.  The
@@ -140,16 +263,16 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
     return __syncthreads_count(px.done) == RT;
 }
 
-__global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_stop) {
+__global__ void __launch_bounds__(FT) render_fwd_kernel(gs_frame f, int early_stop) {
     pdl_wait();
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
-    __shared__ int32_t s_tmp[RT / 32];
+    __shared__ int32_t s_tmp[FT / 32];
     const int tile = blockIdx.x;
-    FwdPixel px = fwd_pixel_init(f, tile);
+    FwdPair px = fwd_pair_init(f, tile);
     if (f.counters[GS_CNT_OVERFLOW]) {  // binning over capacity (tile ranges emptied): background
-        fwd_pixel_store(f, tile, px);
+        fwd_pair_store(f, tile, px);
         return;
     }
     if (f.counters[GS_CNT_LAZY]) {
@@ -166,8 +289,8 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
         __syncthreads();
         const int lead = s_lead;
         const int32_t *hid = f.huge + HIDS;
-        const bool all = blend_range(f, px, st, 0, lead, early_stop,
-                                     [&](int p) { return hid[tile_huge_select(p, s_words, s_wpre, nw)]; });
+        const bool all = blend_range2(f, px, st, 0, lead, early_stop,
+                                      [&](int p) { return hid[tile_huge_select(p, s_words, s_wpre, nw)]; });
         const int total = f.tile_offsets[tile + 1] - f.tile_offsets[tile];
         if (!all && total > lead && threadIdx.x == 0) {
             ts_flag(f)[tile] = TL_LIST;
@@ -177,9 +300,9 @@ __global__ void __launch_bounds__(RT) render_fwd_kernel(gs_frame f, int early_st
     } else {
         const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
         const int32_t *list = f.entry_splat + start;
-        blend_range(f, px, st, 0, stop - start, early_stop, [&](int p) { return list[p]; });
+        blend_range2(f, px, st, 0, stop - start, early_stop, [&](int p) { return list[p]; });
     }
-    fwd_pixel_store(f, tile, px);
+    fwd_pair_store(f, tile, px);
 }
 
 // Lazy lists, continuation 1: the bucket keys of the tiles that need them (ts_flag != 0)
@@ -323,13 +446,6 @@ __device__ __forceinline__ int col_field(unsigned lane) {
     return ((lane & 16u) ? 2 : 0) + ((lane & 8u) ? 1 : 0);
 }
 
-// Paired fp32 arithmetic (sm_100 FFMA2 / FADD2 / FMUL2: one instruction, two lanes): a backward
-// thread owns two pixels of one column (rows y and y + 8), whose replay steps are the same
-// instruction stream on different data.
-__device__ __forceinline__ float2 f2(float v) { return make_float2(v, v); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
-__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
 
 // The two pixels' replay state (R/rasterizer.py:365-410, run back to front from the final T).
 struct BwdPair {
@@ -349,17 +465,10 @@ __device__ __forceinline__ void bwd_step2(BwdPair &p, bool act0, bool act1, cons
                                           const float4 &C, float2 v[10]) {
     const float dx = p.fx - A.x;
     const float2 dy = add2(p.fy, f2(-A.y));
-    const float a = A.z, beta = A.w, gamma = B.x, op = B.y, dep = B.z;
-    const float2 u = fma2(f2(beta), dy, f2(dx));
-    const float2 au = mul2(f2(a), u);
-    const float2 q = fma2(au, u, mul2(mul2(f2(gamma), dy), dy));
-    const float2 hq = mul2(f2(NEG_HALF_LOG2E), q);
-    const float2 e = make_float2(fast_ex2(hq.x), fast_ex2(hq.y));
-    const float2 araw = mul2(f2(op), e);
-    const bool c0 = araw.x > GS_ALPHA_CLAMP, c1 = araw.y > GS_ALPHA_CLAMP;
-    const float2 alpha = make_float2(c0 ? GS_ALPHA_CLAMP : araw.x, c1 ? GS_ALPHA_CLAMP : araw.y);
-    float2 om = fma2(f2(-op), e, f2(1.0f));
-    om = make_float2(c0 ? 0.01f : om.x, c1 ? 0.01f : om.y);
+    const float beta = A.w, gamma = B.x, dep = B.z;
+    float2 au, e, alpha, om;
+    bool c0, c1;
+    alpha2(A, B, dx, dy, au, e, alpha, om, c0, c1);
     const float2 rom = make_float2(fast_rcp(om.x), fast_rcp(om.y));
     const float2 Tb = mul2(p.T, rom);
     float2 w = mul2(alpha, Tb);
@@ -567,7 +676,7 @@ using namespace gs;
 extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream) {
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
-    launch_pdl(render_fwd_kernel, T, RT, 0, (cudaStream_t)stream, *f, early_stop);
+    launch_pdl(render_fwd_kernel, T, FT, 0, (cudaStream_t)stream, *f, early_stop);
     int rc = check_launch("render_fwd_kernel");
     if (rc) return rc;
     // lazy lists: bucket fill + sorted continuation of the tiles that need them (no-ops otherwise)
