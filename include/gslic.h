@@ -75,7 +75,7 @@ enum {
     GS_CNT_BIG_BITS = 7, /* words of big_bits in use */
     GS_CNT_SLOTS = 16,
     /* slots 8-15: look-back tickets; second half of the counters array: */
-    GS_CNT_HUGE = 16,    /* screen-covering Gaussians binned per tile by bitmap (not sorted) */
+    GS_CNT_HUGE = 16,    /* reserved (0): huge slots are big-list indices below GS_HUGE_CAP */
     GS_CNT_HUGE_E = 17,  /* their kept pairs */
     GS_CNT_SMALL_E = 18, /* entries binned through the per-tile buckets */
     GS_CNT_HUGE_N = 19,  /* huge Gaussians with >= 1 kept tile (records in depth order) */

@@ -6,7 +6,7 @@
 // preprocess.cu (kept counts, cull bitmaps, huge-slot masks); here, with the 64-bit key
 // (depth_f32_bits << 32 | id) -- a total order equal to lexsort((id, depth)) inside a tile:
 //   1. per-tile counts of the kept pairs of the non-screen-covering Gaussians, taken where the
-//      cull decides them (preprocess_kernel, big_finish_kernel; bucket_count for cull=False);
+//      cull decides them (preprocess_kernel, big_cull_kernel; bucket_count for cull=False);
 //   2. huge_sort: the screen-covering ("huge") Gaussians, already binned per tile by bitmap,
 //      are rank-sorted by key (records in depth order);
 //   3. huge_transpose: their per-tile masks in that order, per-tile counts;
@@ -66,7 +66,7 @@ __global__ void nocull_kernel(gs_frame f) {
 }
 
 // 1) per-tile bucket counts for cull=False (every tile holds every valid Gaussian); with the
-// cull they are counted where the cull decides (preprocess_kernel, big_finish_kernel)
+// cull they are counted where the cull decides (preprocess_kernel, big_cull_kernel)
 __global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f) {
     pdl_wait();
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
 }
 
 // 3) per-tile masks in depth order: bit j of huge_mask[t][w] <-> huge record 32w + j keeps tile
-// t (a 32 x 32 bit transpose per warp of huge_mask_t rows, which the big_* cull kernels wrote
+// t (a 32 x 32 bit transpose per warp of huge_mask_t rows, which big_cull_kernel wrote
 // by slot), plus the per-tile huge counts (tile_scratch[T+1 ..))
 __global__ void __launch_bounds__(256) huge_transpose_kernel(gs_frame f) {
     pdl_wait();
@@ -363,7 +363,7 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
         launch_pdl(bucket_count_kernel, 4 * 148, 256, 0, st, *f);
         if ((rc = check_launch("bucket_count_kernel"))) return rc;
     }
-    if (cull) {  // the bucket counts come from the cull (preprocess, big_finish)
+    if (cull) {  // the bucket counts come from the cull (preprocess, big_cull)
         launch_pdl(huge_sort_kernel, GS_HUGE_CAP / HS_KEYS, HS_THREADS, 0, st, *f);
         if ((rc = check_launch("huge_sort_kernel"))) return rc;
         launch_pdl(huge_transpose_kernel, dim3((unsigned)((T + 31) / 32), GS_HUGE_CAP / 256), 256, 0, st, *f);

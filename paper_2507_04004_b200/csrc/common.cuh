@@ -22,7 +22,7 @@ namespace gs {
 constexpr int HREC = 8;
 constexpr int HIDS = HREC * GS_HUGE_CAP;
 constexpr int HKEYS = HIDS + GS_HUGE_CAP;  // int offset of the uint64 key array (8-B aligned)
-constexpr int HSTAGE = HKEYS + 2 * GS_HUGE_CAP;  // unsorted keys staged by big_finish_kernel
+constexpr int HSTAGE = HKEYS + 2 * GS_HUGE_CAP;  // unsorted keys staged by big_cull_kernel
 
 // ---------------------------------------------------------------------------
 // error plumbing (thread-local, no global mutable state shared across threads)

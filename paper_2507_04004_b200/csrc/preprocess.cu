@@ -144,12 +144,6 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     PPWarp &W = ws_all[warp];
-    {  // clear the screen-covering Gaussians' per-slot tile bitmaps (big_* kernels OR into them)
-        const int64_t n4 = ((int64_t)GS_HUGE_CAP * (((int64_t)f.tiles_x * f.tiles_y + 31) >> 5)) >> 2;
-        uint4 *hm = reinterpret_cast<uint4 *>(f.huge_mask_t);
-        for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < n4; k += (int64_t)gridDim.x * blockDim.x)
-            hm[k] = make_uint4(0u, 0u, 0u, 0u);
-    }
     const int64_t n = f.n;
     const int64_t nbatch = (n + 31) / 32;
     const int64_t stride = (int64_t)gridDim.x * PP_WARPS;
@@ -298,48 +292,44 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
 }
 
 // Exact cull of the large-footprint Gaussians (> GS_SMALL_CAND candidate tiles), same decision
-// as cull_rect, spread over the whole GPU in four launches (a few screen-covering Gaussians
-// carry thousands of candidate tiles, so per-Gaussian work units would serialise on them):
-//   K0 big_setup_kernel  huge slot / bitmap base per Gaussian, zeroed output rows;
-//   K1 big_bands_kernel  thread per (Gaussian, tile row = "band"): bounds of the footprint
-//                        ellipse give a run of surely-kept tiles (set as bit ranges) between
-//                        runs of surely-culled ones; the tiles in between are queued;
-//   K2 big_tiles_kernel  thread per queued tile: per-tile corner / lower bounds; the tiles the
-//                        boundary actually crosses get the exact test, 8 lanes per tile and
-//                        two pixel rows each (row_hits);
-//   K3 big_finish_kernel touched / key / huge encoding / touched list.
-// Output bitmaps: big_bits by candidate index (for the emit) or, for screen-covering Gaussians
-// with a huge slot, by tile index (huge_mask_t row of the slot, transposed into depth order by
-// huge_transpose_kernel).
+// as cull_rect, one warp per Gaussian (big_bands_kernel / big_exact_kernel below).  Output bitmaps: big_bits by
+// candidate index (for the emit) or, for screen-covering Gaussians with a huge slot, by tile
+// index (huge_mask_t row of the slot, transposed into depth order by huge_transpose_kernel).
 
 // Per-tile bounds: 1 if every pixel of the tile has q <= qcut (its four corners, q convex),
-// 0 if none has (continuous lower bound over the rectangle, as tile_keep), -1: decide exactly.
-// kx = -cb/ca, ky = -cb/cc: the bounds carry a margin, so their minimisers need not be exact.
+// 0 if none has (lower bound over the rectangle, as tile_keep), -1: decide exactly.  Evaluated in
+// FP64 on the fp32 inputs, so the bounds are (to ~1e-16) those of the exact quadratic; the margin
+// only has to cover the fp32 evaluation error of the exact test: quad_q rounds each of its three
+// terms <= 4 times (dx, dy included) and sums twice, |q_fp32 - q| <= 6u (|T1| + |T2| + |T3|) <=
+// 12u (a dx^2 + c dy^2) = 7.2e-7 scale (u = 2^-24, |2b dx dy| <= a dx^2 + c dy^2).  A 2e-6 scale
+// margin keeps 2.8x of that in hand.  kx ~ -cb/ca, ky ~ -cb/cc locate the edge minima: an error
+// there raises the bound by a (dx err)^2 ~ 1e-14 scale, far inside the margin.
+constexpr double CULL_MARGIN = 2e-6;
+
 __device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb, float cc, float qcut, float kx,
                                           float ky, int x0, int x1, int y0, int y1) {
-    const float ax0 = (float)x0 - mx, ax1 = (float)x1 - mx, ay0 = (float)y0 - my, ay1 = (float)y1 - my;
-    const float scale = ca * fmaxf(ax0 * ax0, ax1 * ax1) + cc * fmaxf(ay0 * ay0, ay1 * ay1);
-    const float margin = 1e-5f * scale + 1e-6f;
-    const float tb = 2.0f * cb;
-    const float xx0 = ca * ax0 * ax0, xx1 = ca * ax1 * ax1, yy0 = cc * ay0 * ay0, yy1 = cc * ay1 * ay1;
-    float qmax = xx0 + tb * ax0 * ay0 + yy0;
-    qmax = fmaxf(qmax, xx1 + tb * ax1 * ay0 + yy0);
-    qmax = fmaxf(qmax, xx0 + tb * ax0 * ay1 + yy1);
-    qmax = fmaxf(qmax, xx1 + tb * ax1 * ay1 + yy1);
-    if (qmax + margin < qcut) return 1;
-    if (!(ax0 <= 0.0f && ax1 >= 0.0f && ay0 <= 0.0f && ay1 >= 0.0f)) {
-        float qc = 3.0e38f;
-        const float ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
+    const double a = ca, c = cc, tb = 2.0 * (double)cb;
+    const double ax0 = (double)x0 - mx, ax1 = (double)x1 - mx, ay0 = (double)y0 - my, ay1 = (double)y1 - my;
+    const double xx0 = a * ax0 * ax0, xx1 = a * ax1 * ax1, yy0 = c * ay0 * ay0, yy1 = c * ay1 * ay1;
+    const double margin = CULL_MARGIN * (fmax(xx0, xx1) + fmax(yy0, yy1)) + 1e-6;
+    double qmax = xx0 + tb * ax0 * ay0 + yy0;
+    qmax = fmax(qmax, xx1 + tb * ax1 * ay0 + yy0);
+    qmax = fmax(qmax, xx0 + tb * ax0 * ay1 + yy1);
+    qmax = fmax(qmax, xx1 + tb * ax1 * ay1 + yy1);
+    if (qmax + margin < (double)qcut) return 1;
+    if (!(ax0 <= 0.0 && ax1 >= 0.0 && ay0 <= 0.0 && ay1 >= 0.0)) {
+        double qc = 1e300;
+        const double ys[2] = {ay0, ay1}, xs[2] = {ax0, ax1};
 #pragma unroll
         for (int k = 0; k < 2; k++) {
-            const float y = ys[k];
-            const float dx = fminf(fmaxf(kx * y, ax0), ax1);
-            qc = fminf(qc, ca * dx * dx + tb * dx * y + cc * y * y);
-            const float x = xs[k];
-            const float dy = fminf(fmaxf(ky * x, ay0), ay1);
-            qc = fminf(qc, ca * x * x + tb * x * dy + cc * dy * dy);
+            const double y = ys[k];
+            const double dx = fmin(fmax((double)kx * y, ax0), ax1);
+            qc = fmin(qc, a * dx * dx + tb * dx * y + c * y * y);
+            const double x = xs[k];
+            const double dy = fmin(fmax((double)ky * x, ay0), ay1);
+            qc = fmin(qc, a * x * x + tb * x * dy + c * dy * dy);
         }
-        if (qc - margin > qcut) return 0;
+        if (qc - margin > (double)qcut) return 0;
     }
     return -1;
 }
@@ -347,8 +337,10 @@ __device__ __forceinline__ int tile_class(float mx, float my, float ca, float cb
 // Per-Gaussian constants of the band bounds.  E(k) = {q <= k} is an ellipse: its x-extent over
 // a band's rows bounds the possibly-kept tiles (k = qp = qcut + margin), and a tile whose four
 // corner pixels lie in E(qm), qm = qcut - margin, has every pixel inside (q is convex).  The
-// discriminants are formed in FP64 (no cancellation), the square roots in fp32: their 1e-7
-// relative error is far below the margin's 5e-6 relative widening of the ellipse.
+// discriminants are formed in FP64 (no cancellation), the square roots in fp32: their ~1e-7
+// relative error moves the extents by <= 1e-7 of the half-width, which the eps widening in x
+// (1e-3 + 1e-6 (|mx| + half-width) px) covers ten times over.  The margin (CULL_MARGIN of the
+// rectangle's scale) covers the fp32 evaluation error of the exact test, as in tile_class.
 struct BandConst {
     double mx, my, a, b, det, inv_a, qm, qp, dymax, dyr, eps;
     bool ok;
@@ -364,7 +356,7 @@ __device__ __forceinline__ BandConst band_const(float mx, float my, float ca, fl
     k.det = k.a * c - k.b * k.b;
     const double ax = fmax(fabs((double)(r.x * GS_TILE) - k.mx), fabs((double)(r.y * GS_TILE + GS_TILE) - k.mx));
     const double ay = fmax(fabs((double)(r.z * GS_TILE) - k.my), fabs((double)(r.w * GS_TILE + GS_TILE) - k.my));
-    const double margin = 1e-5 * (k.a * ax * ax + c * ay * ay) + 1e-6;
+    const double margin = CULL_MARGIN * (k.a * ax * ax + c * ay * ay) + 1e-6;
     k.qm = (double)qcut - margin;
     k.qp = (double)qcut + margin;
     k.ok = k.a > 0.0 && c > 0.0 && k.det > 0.0 && k.qp > 0.0 && isfinite(k.det) && isfinite(margin);
@@ -413,9 +405,7 @@ __device__ __forceinline__ int4 band_ranges(const BandConst &k, int ty, int4 r, 
     return out;
 }
 
-// K1: thread per (large-footprint Gaussian, band): sets the surely-kept run of the band and
-// queues its ambiguous tiles (overflowing the queue: exact test in place); kept[g] accumulates
-// the surely-kept counts.
+// Sets bits [b0, b1] of a warp's shared-memory bitmap (bands of one Gaussian share words).
 __device__ __forceinline__ void set_bit_range(uint32_t *bits, int b0, int b1) {
     for (int w = b0 >> 5; w <= (b1 >> 5); w++) {
         const int lo_b = max(b0, w << 5) - (w << 5), hi_b = min(b1, (w << 5) + 31) - (w << 5);
@@ -424,302 +414,312 @@ __device__ __forceinline__ void set_bit_range(uint32_t *bits, int b0, int b1) {
     }
 }
 
-struct BigCtx {
-    int g, slot;
-    int64_t base;
-    SplatCull s;
-    int4 r;
-    uint32_t *bits;  // output bitmap row (nullptr: big_bits overflow, the emit re-culls)
-};
-
-__device__ __forceinline__ BigCtx big_ctx(const gs_frame &f, int64_t b) {
-    BigCtx c;
-    c.g = f.big_list[b];
-    c.s = splat_cull(f.splat2d, c.g);
-    c.r = reinterpret_cast<const int4 *>(f.rect)[c.g];
-    c.slot = f.big_slot[b];
-    c.base = (int64_t)f.keep_bits[c.g];
-    const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
-    c.bits = c.slot >= 0 ? f.huge_mask_t + (int64_t)c.slot * tw : (c.base >= 0 ? f.big_bits + c.base : nullptr);
-    return c;
-}
-
-__device__ __forceinline__ int big_bit(const BigCtx &c, int tiles_x, int tx, int ty) {
-    return c.slot >= 0 ? ty * tiles_x + tx : (ty - c.r.z) * (c.r.y - c.r.x + 1) + (tx - c.r.x);
-}
-
-constexpr int CB_BSTRIDE = 64;  // threads per Gaussian in big_bands_kernel (bands beyond: strided); a
-                                // multiple of 32 so that a warp serves one Gaussian (warp-wide reservations)
-
-// K0: thread per large-footprint Gaussian: huge slot or bitmap base (warp-aggregated
-// reservations: one atomic per warp and counter)
-__global__ void __launch_bounds__(256) big_setup_kernel(gs_frame f, int allow_huge) {
-    pdl_wait();
-    const int64_t nb = f.counters[GS_CNT_BIG];
-    const int lane = threadIdx.x & 31;
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = b0 + threadIdx.x;  // uniform trip count: the reservations are warp-wide
-        int g = 0, words = 0;
-        bool huge = false;
-        if (b < nb) {
-            g = f.big_list[b];
-            const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
-            const int ncand = (r.y - r.x + 1) * (r.w - r.z + 1);
-            words = (ncand + 31) >> 5;
-            huge = allow_huge && ncand > GS_HUGE_CAND;
-        }
-        // screen-covering Gaussians take a huge slot: their kept tiles are recorded per tile
-        // and they skip the emit + sort; the others keep a cull bitmap for the emit
-        const unsigned hm = __ballot_sync(0xffffffffu, huge);
-        int s0 = 0;
-        if (lane == 0 && hm) s0 = atomicAdd(&f.counters[GS_CNT_HUGE], __popc(hm));
-        const int sbase = __shfl_sync(0xffffffffu, s0, 0);  // all lanes: full-mask shuffle
-        int slot = huge ? sbase + __popc(hm & ((1u << lane) - 1u)) : -1;
-        if (slot >= GS_HUGE_CAP) slot = -1;
-        const int w = (b < nb && slot < 0) ? words : 0;
-        int x = w;
+// Exact resolution of up to 32 (tile, Gaussian) pairs held one per lane: cls = tile_class on
+// entry (1 kept, 0 culled, -1 open); the open tiles are decided four per round, 8 lanes per tile
+// and two pixel rows per lane (row_hits), with the owner's parameters fetched by shuffles.
+__device__ __forceinline__ int resolve_open(int cls, const SplatCull &s, int x0, int x1, int y0, int y1) {
+    const int lane = threadIdx.x & 31, grp = lane >> 3, sub = lane & 7;
+    unsigned amb = __ballot_sync(0xffffffffu, cls < 0);
+    while (amb) {
+        int mine = -1;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
+        for (int k = 0; k < 4; k++) {
+            const int l = amb ? __ffs(amb) - 1 : -1;
+            if (l >= 0) amb &= amb - 1u;
+            if (k == grp) mine = l;
         }
-        const int tot = __shfl_sync(0xffffffffu, x, 31);
-        long long bb = 0;
-        if (lane == 0 && tot) bb = atomicAdd(&f.counters[GS_CNT_BIG_BITS], tot);
-        long long base = __shfl_sync(0xffffffffu, bb, 0) + (x - w);
-        if (b < nb) {
-            if (slot >= 0 || base + w > f.big_bits_words) base = -1;  // overflow: the emit re-culls
-            f.big_slot[b] = slot;
-            f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
-            f.kept[g] = 0;
+        const int src = mine >= 0 ? mine : 0;
+        const float smx = __shfl_sync(0xffffffffu, s.mx, src), smy = __shfl_sync(0xffffffffu, s.my, src);
+        const float sca = __shfl_sync(0xffffffffu, s.ca, src), scb = __shfl_sync(0xffffffffu, s.cb, src);
+        const float scc = __shfl_sync(0xffffffffu, s.cc, src), sq = __shfl_sync(0xffffffffu, s.qcut, src);
+        const int sx0 = __shfl_sync(0xffffffffu, x0, src), sx1 = __shfl_sync(0xffffffffu, x1, src);
+        const int sy0 = __shfl_sync(0xffffffffu, y0, src), sy1 = __shfl_sync(0xffffffffu, y1, src);
+        bool hit = false;
+        if (mine >= 0) {
+            const int ya = sy0 + sub, yb = sy0 + sub + 8;
+            hit = (ya <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, ya)) ||
+                  (yb <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, yb));
         }
-        // zero the cull bitmap rows of the non-screen-covering ones (the band / tile kernels OR
-        // into them), one row at a time with the whole warp (coalesced); the huge-slot rows were
-        // cleared wholesale by preprocess_kernel
-        uint32_t *bits = (b < nb && slot < 0 && base >= 0) ? f.big_bits + base : nullptr;
-        const int nwords = words;
-        for (int k = 0; k < 32; k++) {
-            uint32_t *row = reinterpret_cast<uint32_t *>(__shfl_sync(0xffffffffu, (unsigned long long)bits, k));
-            const int nw = __shfl_sync(0xffffffffu, nwords, k);
-            if (row)
-                for (int w = lane; w < nw; w += 32) row[w] = 0u;
+        const unsigned bal = __ballot_sync(0xffffffffu, hit);
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int owner = __shfl_sync(0xffffffffu, mine, 8 * k);
+            if (lane == owner && owner >= 0) cls = ((bal >> (8 * k)) & 0xffu) ? 1 : 0;
         }
     }
+    return cls;
 }
 
-__global__ void __launch_bounds__(256, 3) big_bands_kernel(gs_frame f) {
-    pdl_wait();
+__device__ __forceinline__ uint64_t big_key(const gs_frame &f, int g) {
+    return ((uint64_t)__float_as_uint(splat_depth(f.splat2d, g)) << 32) | (uint32_t)g;
+}
+
+// Publishes one large-footprint Gaussian once its bitmap is complete (the whole warp calls it
+// with the same arguments; `bits` = its bitmap, shared or global): kept count, touched, the
+// non-huge kept tiles into the binning's bucket counts and, with `lists`, the huge key staging
+// and the touched-list entry (big_bands_kernel aggregates those per CTA instead).  Returns the
+// kept count.
+template <bool GLOBAL>
+__device__ __forceinline__ int big_publish(const gs_frame &f, int g, int slot, const uint32_t *bits, int nwords,
+                                           int4 r, bool lists) {
     const int lane = threadIdx.x & 31;
+    // rows in global memory were completed by other SMs' atomics: read them at L2
+    auto word = [&](int w) -> uint32_t { return GLOBAL ? __ldcg(bits + w) : bits[w]; };
+    int kept = 0;
+    for (int w = lane; w < nwords; w += 32) kept += __popc(word(w));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+    const bool t = kept > 0;
+    const uint64_t key = big_key(f, g);
+    if (lane == 0) {
+        f.kept[g] = (slot >= 0 && t) ? -(1 + slot) : kept;  // kept < 0 encodes the huge slot
+        f.touched[g] = t;
+        if (t && lists) {
+            // kept screen-covering Gaussians: entry count and a staging slot for the binning's
+            // huge sort (binning.cu, HKEYS; the sort is by key, so the staging order is free)
+            if (slot >= 0) {
+                atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
+                const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
+                if (h < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] = key;
+            }
+            f.touched_list[atomicAdd(&f.counters[GS_CNT_TOUCHED], 1)] = g;
+        }
+    }
+    if (t && slot < 0) {  // per-tile bucket counts (bitmap by candidate index)
+        const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
+        for (int c = lane; c < ncand; c += 32) {
+            if ((word(c >> 5) >> (c & 31)) & 1u) {
+                const int tile = (r.z + c / nx) * f.tiles_x + r.x + c % nx;
+                atomicAdd(&f.tile_scratch[tile], 1);
+                atomicMin(reinterpret_cast<unsigned long long *>(f.tile_minkey) + tile, (unsigned long long)key);
+            }
+        }
+    }
+    return kept;
+}
+
+// Exact cull of the large-footprint Gaussians in two launches:
+//   big_bands_kernel  one warp per Gaussian: lane 0 reserves the output (a huge slot: kept tiles
+//                     by tile index in huge_mask_t; or a big_bits row by candidate index); lane j
+//                     takes bands j, j + 32, ...: the band bounds give a run of surely-kept tiles
+//                     (set in the warp's shared-memory bitmap) between runs of surely-culled
+//                     ones; the ambiguous tiles of the 32 bands are laid end to end (warp prefix
+//                     sum) and queued for big_exact_kernel (the long tail -- needle-shaped
+//                     near-plane footprints leave thousands of tiles within the bounds' margin --
+//                     would serialise a warp on one Gaussian; measured: resolving up to 64 tiles
+//                     in the warp made this kernel 2.3x slower than queueing them all).  Only a
+//                     Gaussian without an output row (big_bits overflow) or a full queue is
+//                     resolved here.  The bitmap goes out as full rows (coalesced, no clearing
+//                     pass); a Gaussian without queued tiles is published at once (touched-list
+//                     and huge-list reservations aggregated per CTA), the others keep their
+//                     queued count in kept[g];
+//   big_exact_kernel  thread per queued tile: tile_class, the open tiles decided 8 lanes per
+//                     tile; kept bits OR-ed into the Gaussian's row; the thread that retires a
+//                     Gaussian's last queued tile publishes it (with its warp).
+// Same decisions as tile_keep (bit-exact against the fp32 oracle restatement).
+constexpr int BC_WARPS = 8;
+
+__global__ void __launch_bounds__(BC_WARPS * 32, 2) big_bands_kernel(gs_frame f, int allow_huge) {
+    pdl_wait();
+    extern __shared__ uint32_t bc_raw[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int T = f.tiles_x * f.tiles_y, tw = (T + 31) >> 5;
+    uint32_t *bm = bc_raw + warp * tw;
     const int64_t nb = f.counters[GS_CNT_BIG];
     const int64_t cap = f.cull_queue_cap;
-    int2 *q1 = reinterpret_cast<int2 *>(f.cull_queue);
-    // thread per (Gaussian, band): CB_BSTRIDE threads per Gaussian, striding its bands
-    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x; t0 < nb * CB_BSTRIDE; t0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = t0 + threadIdx.x;  // uniform trip count: the queue slots are reserved warp-wide
-        const int64_t b = t / CB_BSTRIDE;
-        const int j = (int)(t % CB_BSTRIDE);
-        int nbands = 0, g = 0, nx = 1, slot = -1;
-        int4 r = make_int4(0, -1, 0, -1);
-        float mx = 0.f, my = 0.f, ca = 1.f, cb = 0.f, cc = 1.f, qcut = 0.f;
-        uint32_t *bits = nullptr;
+    int2 *queue = reinterpret_cast<int2 *>(f.cull_queue);
+    __shared__ int s_g[BC_WARPS], s_kept[BC_WARPS], s_slot[BC_WARPS];
+    // CTA-uniform trip count: the touched-list / huge-list reservations are made once per CTA
+    // and round (same-address atomics from every warp serialise in L2)
+    for (int64_t b0 = (int64_t)blockIdx.x * BC_WARPS; b0 < nb; b0 += (int64_t)gridDim.x * BC_WARPS) {
+        const int64_t b = b0 + warp;
+        if (lane == 0) s_kept[warp] = 0;
         if (b < nb) {
-            const BigCtx c = big_ctx(f, b);
-            g = c.g;
-            r = c.r;
-            nx = r.y - r.x + 1;
-            nbands = r.w - r.z + 1;
-            slot = c.slot;
-            bits = c.bits;
-            mx = c.s.mx;
-            my = c.s.my;
-            ca = c.s.ca;
-            cb = c.s.cb;
-            cc = c.s.cc;
-            qcut = c.s.qcut;
-        }
-        const BandConst K = band_const(mx, my, ca, cb, cc, qcut, r);
-        for (int bi0 = 0; bi0 < ((nbands + CB_BSTRIDE - 1) / CB_BSTRIDE) * CB_BSTRIDE || bi0 == 0; bi0 += CB_BSTRIDE) {
-            const int bi = bi0 + j;
-            const int ty = r.z + bi;
-            int4 br = make_int4(0, 1, 0, -1);  // nothing
-            if (bi < nbands) br = band_ranges(K, ty, r, f.width, f.height, f.tiles_x);
-            const int base_bit = slot >= 0 ? ty * f.tiles_x : bi * nx - r.x;  // bit of tile tx: base_bit + tx
-            const bool has_keep = br.y <= br.z;
-            int kept = 0;
-            if (has_keep) {
-                kept = br.z - br.y + 1;
-                if (bits) set_bit_range(bits, base_bit + br.y, base_bit + br.z);
+            const int g = f.big_list[b];
+            const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+            const SplatCull s = splat_cull(f.splat2d, g);
+            const int nx = r.y - r.x + 1, nbands = r.w - r.z + 1, ncand = nx * nbands;
+            // huge slot = the Gaussian's big-list index (no reservation atomic; slots of the others
+            // stay unused)
+            const int slot = (allow_huge && ncand > GS_HUGE_CAND && b < GS_HUGE_CAP) ? (int)b : -1;
+            long long base = -1;
+            if (lane == 0) {
+                if (slot < 0) {  // bitmap by candidate index for the emit (overflow: the emit re-culls)
+                    const int words = (ncand + 31) >> 5;
+                    const long long bb = atomicAdd(&f.counters[GS_CNT_BIG_BITS], words);
+                    base = bb + words > f.big_bits_words ? -1 : bb;
+                }
             }
-            // ambiguous: [pl, kl) and (kr, pr] (all of [pl, pr] when nothing is surely kept)
-            const int namb = has_keep ? (br.y - br.x) + (br.w - br.z) : max(0, br.w - br.x + 1);
-            // warp-wide reservation (every lane gets here: the band loop is warp-uniform)
-            int x = namb;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            const int tot = __shfl_sync(0xffffffffu, x, 31);
-            long long qb = 0;
-            if (lane == 0 && tot) qb = atomicAdd(&f.counters[GS_CNT_CULLQ1], tot);
-            int64_t q = (int64_t)__shfl_sync(0xffffffffu, qb, 0) + (x - namb);
-            for (int tx = br.x; tx <= br.w && namb > 0; tx++, q++) {
-                if (has_keep && tx == br.y) tx = br.z + 1;
-                if (tx > br.w) break;
-                if (q < cap) {
-                    q1[q] = make_int2((int)b, (int)(((uint32_t)tx << 16) | (uint32_t)ty));
-                } else {
-                    const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
+            base = __shfl_sync(0xffffffffu, base, 0);
+            uint32_t *row = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : (base >= 0 ? f.big_bits + base : nullptr);
+            const int nwords = slot >= 0 ? tw : (ncand + 31) >> 5;
+            for (int w = lane; w < nwords; w += 32) bm[w] = 0u;
+            __syncwarp();
+            const BandConst K = band_const(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, r);
+            const float kx = __fdividef(-s.cb, s.ca), ky = __fdividef(-s.cb, s.cc);
+            int queued = 0;
+            for (int bi0 = 0; bi0 < nbands; bi0 += 32) {
+                const int bi = bi0 + lane, ty = r.z + bi;
+                int4 br = make_int4(0, 1, 0, -1);  // nothing
+                if (bi < nbands) br = band_ranges(K, ty, r, f.width, f.height, f.tiles_x);
+                const int bit0 = slot >= 0 ? ty * f.tiles_x : bi * nx - r.x;  // bit of tile tx: bit0 + tx
+                const bool has_keep = br.y <= br.z;
+                if (has_keep) set_bit_range(bm, bit0 + br.y, bit0 + br.z);
+                // ambiguous: [pl, kl) and (kr, pr] (all of [pl, pr] when nothing is surely kept)
+                const int left = has_keep ? br.y - br.x : max(0, br.w - br.x + 1);
+                const int namb = has_keep ? left + (br.w - br.z) : left;
+                int pre = namb;  // inclusive prefix over the warp's bands
+    #pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, pre, o);
+                    if (lane >= o) pre += y;
+                }
+                const int total = __shfl_sync(0xffffffffu, pre, 31);
+                const int start = pre - namb;
+                // many: queue them (a row must exist for the exact kernel to OR into)
+                long long q0 = 0;
+                const bool to_queue = total > 0 && row != nullptr;
+                if (to_queue) {
+                    if (lane == 0) q0 = atomicAdd(&f.counters[GS_CNT_CULLQ1], total);
+                    q0 = __shfl_sync(0xffffffffu, q0, 0);
+                    if (q0 + total > cap) q0 = -1;  // queue full: resolve here
+                }
+                if (to_queue && q0 >= 0) {
+                    for (int c = 0; c < namb; c++) {
+                        const int tx = c < left ? br.x + c : br.z + 1 + (c - left);
+                        queue[q0 + start + c] = make_int2((int)b, (int)(((uint32_t)tx << 16) | (uint32_t)ty));
+                    }
+                    queued += total;
+                    continue;
+                }
+                for (int p0 = 0; p0 < total; p0 += 32) {
+                    const int idx = p0 + lane;
+                    int lo = 0, hi = 31;  // owner band = the first lane with pre > idx
+    #pragma unroll
+                    for (int it = 0; it < 5; it++) {
+                        const int mid = (lo + hi) >> 1;
+                        if (__shfl_sync(0xffffffffu, pre, mid) > idx) hi = mid;
+                        else lo = mid + 1;
+                    }
+                    const int own = lo;
+                    const int c = idx - __shfl_sync(0xffffffffu, start, own);
+                    const int oleft = __shfl_sync(0xffffffffu, left, own), obx = __shfl_sync(0xffffffffu, br.x, own);
+                    const int obz = __shfl_sync(0xffffffffu, br.z, own), obit = __shfl_sync(0xffffffffu, bit0, own);
+                    const int tx = c < oleft ? obx + c : obz + 1 + (c - oleft);
+                    const int oty = r.z + bi0 + own;
+                    const int x0 = tx * GS_TILE, y0 = oty * GS_TILE;
                     const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                    if (tile_keep(mx, my, ca, cb, cc, qcut, x0, x1, y0, y1)) {
-                        kept++;
-                        if (bits) atomicOr(&bits[(base_bit + tx) >> 5], 1u << ((base_bit + tx) & 31));
+                    int cls = 0;
+                    if (idx < total) cls = tile_class(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, kx, ky, x0, x1, y0, y1);
+                    cls = resolve_open(cls, s, x0, x1, y0, y1);
+                    if (cls > 0) {
+                        const int bit = obit + tx;
+                        atomicOr(&bm[bit >> 5], 1u << (bit & 31));
                     }
                 }
             }
-            if (kept) atomicAdd(&f.kept[g], kept);
+            __syncwarp();
+            if (row)
+                for (int w = lane; w < nwords; w += 32) row[w] = bm[w];
+            if (lane == 0) {
+                f.big_slot[b] = slot;
+                f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+                if (queued) f.kept[g] = queued;  // countdown of big_exact_kernel
+            }
+            if (!queued) {
+                const int kept = big_publish<false>(f, g, slot, bm, nwords, r, false);
+                if (lane == 0) {
+                    s_g[warp] = g;
+                    s_kept[warp] = kept;
+                    s_slot[warp] = slot;
+                }
+            }
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int nt = 0, nh = 0, e = 0;
+            for (int w = 0; w < BC_WARPS; w++)
+                if (s_kept[w] > 0) {
+                    nt++;
+                    if (s_slot[w] >= 0) {
+                        nh++;
+                        e += s_kept[w];
+                    }
+                }
+            if (nt) {
+                int tb = atomicAdd(&f.counters[GS_CNT_TOUCHED], nt);
+                int hb = nh ? atomicAdd(&f.counters[GS_CNT_HUGE_N], nh) : 0;
+                if (e) atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
+                for (int w = 0; w < BC_WARPS; w++)
+                    if (s_kept[w] > 0) {
+                        f.touched_list[tb++] = s_g[w];
+                        if (s_slot[w] >= 0) {
+                            if (hb < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[hb] = big_key(f, s_g[w]);
+                            hb++;
+                        }
+                    }
+            }
+        }
+        __syncthreads();  // the warps' bitmaps and the CTA's records are free for the next round
     }
 }
 
-// K2: thread per band-ambiguous tile: per-tile bounds; the tiles the qcut boundary actually
-// crosses get the exact per-row test cooperatively, 8 lanes per tile (two pixel rows each)
-__global__ void __launch_bounds__(256) big_tiles_kernel(gs_frame f) {
+__global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
     pdl_wait();
     const int64_t cap = f.cull_queue_cap;
-    const int64_t n1 = min((int64_t)f.counters[GS_CNT_CULLQ1], cap);
-    const int2 *q1 = reinterpret_cast<const int2 *>(f.cull_queue);
-    const int lane = threadIdx.x & 31, row = lane & 15;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n1; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t nq = min((int64_t)f.counters[GS_CNT_CULLQ1], cap);
+    const int2 *queue = reinterpret_cast<const int2 *>(f.cull_queue);
+    const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nq; i0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = i0 + threadIdx.x;  // uniform trip count: the exact test is warp-wide
-        int cls = 0, g = 0, bit = 0;
-        uint32_t *bits = nullptr;
-        float mx = 0.f, my = 0.f, ca = 1.f, cb = 0.f, cc = 1.f, qcut = 0.f;
-        int x0 = 0, x1 = 0, y0 = 0, y1 = -1;
-        if (i < n1) {
-            const int2 e = q1[i];
-            const BigCtx c = big_ctx(f, e.x);
-            g = c.g;
-            bits = c.bits;
+        int cls = 0, g = 0, b = 0, slot = -1;
+        uint32_t *row = nullptr;
+        SplatCull s{0.f, 0.f, 1.f, 0.f, 1.f, 0.f};
+        int4 r = make_int4(0, -1, 0, -1);
+        int x0 = 0, x1 = 0, y0 = 0, y1 = -1, bit = 0;
+        if (i < nq) {
+            const int2 e = queue[i];
+            b = e.x;
+            g = f.big_list[b];
+            slot = f.big_slot[b];
+            r = reinterpret_cast<const int4 *>(f.rect)[g];
+            s = splat_cull(f.splat2d, g);
             const int tx = (int)((uint32_t)e.y >> 16), ty = e.y & 0xffff;
-            bit = big_bit(c, f.tiles_x, tx, ty);
+            row = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : f.big_bits + (int64_t)f.keep_bits[g];
+            bit = slot >= 0 ? ty * f.tiles_x + tx : (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
             x0 = tx * GS_TILE;
             y0 = ty * GS_TILE;
             x1 = min(x0 + GS_TILE - 1, f.width - 1);
             y1 = min(y0 + GS_TILE - 1, f.height - 1);
-            mx = c.s.mx;
-            my = c.s.my;
-            ca = c.s.ca;
-            cb = c.s.cb;
-            cc = c.s.cc;
-            qcut = c.s.qcut;
-            cls = tile_class(mx, my, ca, cb, cc, qcut, __fdividef(-cb, ca), __fdividef(-cb, cc), x0, x1, y0, y1);
+            cls = tile_class(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, __fdividef(-s.cb, s.ca), __fdividef(-s.cb, s.cc), x0,
+                             x1, y0, y1);
         }
-        unsigned amb = __ballot_sync(0xffffffffu, cls < 0);
-        const int grp = lane >> 3, sub = lane & 7;
-        while (amb) {  // four open tiles per round: 8 lanes per tile, two pixel rows per lane
-            int mine = -1;  // the open tile of this lane's group
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int l = amb ? __ffs(amb) - 1 : -1;
-                if (l >= 0) amb &= amb - 1u;
-                if (k == grp) mine = l;
-            }
-            const int src = mine >= 0 ? mine : 0;
-            const float smx = __shfl_sync(0xffffffffu, mx, src), smy = __shfl_sync(0xffffffffu, my, src);
-            const float sca = __shfl_sync(0xffffffffu, ca, src), scb = __shfl_sync(0xffffffffu, cb, src);
-            const float scc = __shfl_sync(0xffffffffu, cc, src), sq = __shfl_sync(0xffffffffu, qcut, src);
-            const int sx0 = __shfl_sync(0xffffffffu, x0, src), sx1 = __shfl_sync(0xffffffffu, x1, src);
-            const int sy0 = __shfl_sync(0xffffffffu, y0, src), sy1 = __shfl_sync(0xffffffffu, y1, src);
-            bool hit = false;
-            if (mine >= 0) {
-                const int ya = sy0 + sub, yb = sy0 + sub + 8;
-                hit = (ya <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, ya)) ||
-                      (yb <= sy1 && row_hits(smx, smy, sca, scb, scc, sq, sx0, sx1, yb));
-            }
-            const unsigned bal = __ballot_sync(0xffffffffu, hit);
-            // hand each group's verdict to the tile's owner lane
-#pragma unroll
-            for (int k = 0; k < 4; k++) {
-                const int owner = __shfl_sync(0xffffffffu, mine, 8 * k);
-                if (lane == owner && owner >= 0) cls = ((bal >> (8 * k)) & 0xffu) ? 1 : 0;
-            }
+        cls = resolve_open(cls, s, x0, x1, y0, y1);
+        // kept bits: one atomicOr per distinct bitmap word of the warp (queue entries of one
+        // Gaussian are contiguous, so a warp's tiles share few words)
+        uint32_t *wp = row + (bit >> 5);
+        const unsigned same_word = __match_any_sync(0xffffffffu, (unsigned long long)wp);
+        const uint32_t m = __reduce_or_sync(same_word, (i < nq && cls > 0) ? 1u << (bit & 31) : 0u);
+        if (i < nq && m && lane == __ffs(same_word) - 1) atomicOr(wp, m);
+        __threadfence();  // the bits are visible before the countdown that may retire the Gaussian
+        // countdown: one atomicSub per distinct Gaussian of the warp; the lane that retires a
+        // Gaussian's last queued tile publishes it (with its warp)
+        const unsigned same_g = __match_any_sync(0xffffffffu, i < nq ? g : -1);
+        bool last = false;
+        if (i < nq && lane == __ffs(same_g) - 1) last = atomicSub(&f.kept[g], __popc(same_g)) == __popc(same_g);
+        unsigned fin = __ballot_sync(0xffffffffu, last);
+        if (fin) __threadfence();
+        while (fin) {  // the warp publishes each Gaussian whose last queued tile one of its lanes retired
+            const int l = __ffs(fin) - 1;
+            fin &= fin - 1u;
+            const int gl = __shfl_sync(0xffffffffu, g, l), sl = __shfl_sync(0xffffffffu, slot, l);
+            const int4 rl = make_int4(__shfl_sync(0xffffffffu, r.x, l), __shfl_sync(0xffffffffu, r.y, l),
+                                      __shfl_sync(0xffffffffu, r.z, l), __shfl_sync(0xffffffffu, r.w, l));
+            const uint32_t *rowl = reinterpret_cast<const uint32_t *>(__shfl_sync(0xffffffffu, (unsigned long long)row, l));
+            const int nwords = sl >= 0 ? tw : ((rl.y - rl.x + 1) * (rl.w - rl.z + 1) + 31) >> 5;
+            big_publish<true>(f, gl, sl, rowl, nwords, rl, true);
         }
-        if (cls > 0) {
-            atomicAdd(&f.kept[g], 1);
-            if (bits) atomicOr(&bits[bit >> 5], 1u << (bit & 31));
-        }
-    }
-}
-
-// K3: per large-footprint Gaussian: touched, depth key, huge encoding, touched list
-__global__ void __launch_bounds__(256) big_finish_kernel(gs_frame f) {
-    pdl_wait();
-    const int64_t nb = f.counters[GS_CNT_BIG];
-    for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < nb; b0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = b0 + threadIdx.x;  // uniform trip count: warp_append is warp-wide
-        int g = -1, kept = 0, slot = -1;
-        bool t = false;
-        if (b < nb) {
-            g = f.big_list[b];
-            kept = f.kept[g];
-            slot = f.big_slot[b];
-            t = kept > 0;
-        }
-        // kept screen-covering Gaussians: entry count and a staging slot for the binning's huge
-        // sort (binning.cu, HKEYS; the sort is by key, so the staging order is free), reserved
-        // with one atomic per warp and counter
-        const bool hk = slot >= 0 && t;
-        const unsigned hm = __ballot_sync(0xffffffffu, hk);
-        if (hm) {
-            int e = hk ? kept : 0;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-            const int lane = threadIdx.x & 31;
-            int h0 = 0;
-            if (lane == 0) {
-                atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
-                h0 = atomicAdd(&f.counters[GS_CNT_HUGE_N], __popc(hm));
-            }
-            const int h = __shfl_sync(0xffffffffu, h0, 0) + __popc(hm & ((1u << lane) - 1u));
-            if (hk) {
-                f.kept[g] = -(1 + slot);  // kept < 0 encodes the huge slot
-                if (h < GS_HUGE_CAP)
-                    reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] =
-                        ((uint64_t)__float_as_uint(splat_depth(f.splat2d, g)) << 32) | (uint32_t)g;
-            }
-        }
-        if (b < nb) f.touched[g] = t;
-        // per-tile bucket counts of the binning (bitmap, or the exact re-test on bitmap overflow):
-        // the warp walks the candidates of each of its non-huge kept Gaussians together
-        const bool cnt = b < nb && t && f.big_slot[b] < 0;
-        unsigned pend = __ballot_sync(0xffffffffu, cnt);
-        while (pend) {
-            const int j = __ffs(pend) - 1;
-            pend &= pend - 1;
-            const int gj = __shfl_sync(0xffffffffu, g, j);
-            const int4 r = reinterpret_cast<const int4 *>(f.rect)[gj];
-            const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
-            const int64_t base = (int64_t)f.keep_bits[gj];
-            const SplatCull s = splat_cull(f.splat2d, gj);
-            const unsigned long long key = ((unsigned long long)__float_as_uint(splat_depth(f.splat2d, gj)) << 32) | (uint32_t)gj;
-            for (int c = threadIdx.x & 31; c < ncand; c += 32) {
-                const int tx = r.x + c % nx, ty = r.z + c / nx;
-                bool keep;
-                if (base >= 0) {
-                    keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
-                } else {
-                    const int x0 = tx * GS_TILE, y0 = ty * GS_TILE;
-                    const int x1 = min(x0 + GS_TILE - 1, f.width - 1), y1 = min(y0 + GS_TILE - 1, f.height - 1);
-                    keep = tile_keep(s.mx, s.my, s.ca, s.cb, s.cc, s.qcut, x0, x1, y0, y1);
-                }
-                if (keep) {
-                    atomicAdd(&f.tile_scratch[ty * f.tiles_x + tx], 1);
-                    atomicMin(reinterpret_cast<unsigned long long *>(f.tile_minkey) + ty * f.tiles_x + tx, key);
-                }
-            }
-        }
-        warp_append(t, g, &f.counters[GS_CNT_TOUCHED], f.touched_list);
     }
 }
 
@@ -879,16 +879,12 @@ __global__ void lidar_write_kernel(const float *__restrict__ sparse, int64_t npx
 using namespace gs;
 
 static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
-    launch_pdl(big_setup_kernel, 148, 256, 0, st, *f, allow_huge);
-    int rc = check_launch("big_setup_kernel");
+    const int tw = (f->tiles_x * f->tiles_y + 31) >> 5;
+    launch_pdl(big_bands_kernel, 2 * 148, BC_WARPS * 32, (size_t)BC_WARPS * tw * sizeof(uint32_t), st, *f, allow_huge);
+    int rc = check_launch("big_bands_kernel");
     if (rc) return rc;
-    launch_pdl(big_bands_kernel, 8 * 148, 256, 0, st, *f);
-    if ((rc = check_launch("big_bands_kernel"))) return rc;
-    if (rc) return rc;
-    launch_pdl(big_tiles_kernel, 8 * 148, 256, 0, st, *f);
-    if ((rc = check_launch("big_tiles_kernel"))) return rc;
-    launch_pdl(big_finish_kernel, 148, 256, 0, st, *f);
-    return check_launch("big_finish_kernel");
+    launch_pdl(big_exact_kernel, 8 * 148, 256, 0, st, *f);
+    return check_launch("big_exact_kernel");
 }
 
 extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream) {
@@ -972,6 +968,8 @@ void init_preprocess_attrs() {
                          (int)(PP_WARPS * sizeof(PPWarp)));
     cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(PP_WARPS * sizeof(PPWarp)));
+    cudaFuncSetAttribute(big_bands_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(BC_WARPS * ((GS_MAX_TILES + 31) / 32) * sizeof(uint32_t)));
     cudaFuncSetAttribute(preprocess_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaFuncSetAttribute(preprocess_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }

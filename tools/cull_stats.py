@@ -18,6 +18,6 @@ for k in range(len(sc.cams)):
     rect = ws.view("rect", "i32", (len(g), 4))[nb]
     ncand = ((rect[:, 1] - rect[:, 0] + 1) * (rect[:, 3] - rect[:, 2] + 1)).cpu().numpy()
     nbands = (rect[:, 3] - rect[:, 2] + 1).cpu().numpy()
-    print(f"view {k}: touched {c[2]} big {big} huge(slots) {c[16]} huge_n {c[19]} cullq1 {c[20]} big_bits_words {c[7]} "
-          f"ncand sum {ncand.sum()} (>256: {(ncand > 256).sum()}, 17-256: {((ncand > 16) & (ncand <= 256)).sum()}) bands sum {nbands.sum()} "
-          f"huge_E {c[17]}")
+    print(f"view {k}: touched {c[2]} big {big} huge_n {c[19]} queued tiles {c[20]} big_bits_words {c[7]} "
+          f"ncand sum {ncand.sum()} (>256: {(ncand > 256).sum()}, 17-256: {((ncand > 16) & (ncand <= 256)).sum()}) "
+          f"bands sum {nbands.sum()} huge_E {c[17]}")
