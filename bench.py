@@ -56,7 +56,7 @@ DEFAULT = "S2r-1M-1280x720-32line"
 SEGMENT = 100  # iterations per timed segment (the map is restored between segments, untimed)
 # share of each phase's time taken by its largest kernel (warm graph-replay ncu list, r01d)
 TOP_KERNEL_SHARE = {"preprocess": 0.60, "render_fwd": 0.85, "loss": 0.88, "render_bwd": 0.96, "chain_adam": 1.0}
-TOP_KERNEL = {"preprocess": "preprocess_kernel", "render_fwd": "render_fwd_kernel", "loss": "ssim_l1_kernel",
+TOP_KERNEL = {"preprocess": "preprocess_kernel", "render_fwd": "render_fwd_kernel", "loss": "ssim_fwd_kernel + ssim_bwd_kernel",
               "render_bwd": "render_bwd_kernel", "chain_adam": "chain_kernel (fused chain rule + sparse Adam)"}
 
 

@@ -160,6 +160,8 @@ typedef struct gs_frame {
                                 loss[8 + i % GS_LOSS_RING] (i counted from the workspace's layout) */
     int64_t loss_blocks;
     int64_t *pose_acc;       /* 12: fixed-point accumulators of the pose gradient (gs_chain_pose) */
+    float *ssim_g;           /* 3 x H x W x 4: SSIM-map partials per channel (d/d mu_a, d/d var sum,
+                                d/d sigma_ab, -), written and read by gs_loss */
 } gs_frame;
 
 /* ---- setup ---------------------------------------------------------------- */

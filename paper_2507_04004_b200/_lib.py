@@ -62,7 +62,7 @@ class GsFrame(ctypes.Structure):
                 ("entry_splat", P), ("tile_offsets", P), ("counters", P),
                 ("color", P), ("depth", P), ("opacity", P), ("trans", P), ("n_contrib", P),
                 ("g_color", P), ("g_depth", P), ("g_opac", P), ("loss_parts", P), ("loss", P),
-                ("loss_blocks", i64), ("pose_acc", P)]
+                ("loss_blocks", i64), ("pose_acc", P), ("ssim_g", P)]
 
 
 _lib = None

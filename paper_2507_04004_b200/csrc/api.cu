@@ -114,6 +114,7 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     // loss ring (GS_LOSS_ACCUMULATE)
     f.loss = c.take<double>(8 + GS_LOSS_RING);
     f.pose_acc = c.take<int64_t>(16);
+    f.ssim_g = c.take<float>(12 * P);
 }
 
 }  // namespace gs

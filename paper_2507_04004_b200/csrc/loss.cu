@@ -5,33 +5,42 @@
 // dependent 11-tap correlations: blur(x)(q) = sum_d F[q][d] x(q+d) with
 // F[q][d] = sum_t K(t) [refl(q+t) == q+d], and adjoint(g)(p) = sum_d F[p+d][-d] g(p+d); the
 // per-axis tables absorb every reflection, so interior and border pixels share one code path.
-// One CTA computes a 32x16 output tile of one channel: halo-10 inputs -> 4 blurred moments (a, b, aa + bb, ab)
-// (halo 5) -> SSIM map + partials -> two adjoint passes -> gradient, all in shared memory (one
-// HBM read of rendered+target, one write of the gradient).
+// Two kernels per view (below): the SSIM map and its partials, then their adjoint.
 //
 // Depth term (R/losses.py:133-154) is evaluated only at the view's LiDAR pixels (K-list).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gs {
 
-// One CTA per (32 x 16 output tile, colour channel).  Every pass is register-blocked along its
-// blur axis (a thread produces a strip of outputs from one sliding window of shared-memory
-// reads); row strides are odd so that a warp reading one column per lane (or one row per lane)
-// hits 32 distinct banks.  40 KB of shared memory and <= 64 registers give 4 CTAs (32 warps)
-// per SM: the passes are separated by barriers, so it is the other CTAs that keep the SM busy.
-constexpr int TW = 32, TH = 16;
-constexpr int NIR = TH + 20;          // input rows (halo 10)
-constexpr int HXC = TW + 10;          // horizontal-moment columns (strips of 6 / 3)
-constexpr int HXS = HXC + 1;          // their row stride (odd)
-constexpr int NIC = HXC + 12;         // input row stride in float2 (even: 16-B aligned rows for pairwise
-                                      // LDS.128; >= HXC + 10); columns >= TW + 20 are never read
-constexpr int GR = TH + 10;           // SSIM-map rows (halo 5)
-constexpr int GW = TW + 10;           // SSIM-map columns
-constexpr int GC = GW + 1;            // SSIM-map / vertical-adjoint row stride (odd)
-constexpr int HS = 2;                 // horizontal adjoint: strips of 2 columns, one per thread
-constexpr int L_THREADS = 256;
-static_assert(TH * (TW / HS) == L_THREADS, "one horizontal-adjoint strip per thread");
-static_assert(HXC % 6 == 0 && HXC % 3 == 0, "horizontal strips");
+// Two launches per view, CTA per (64 x 16 output tile, colour channel), 256 threads:
+//   ssim_fwd_kernel  inputs on the tile + halo 5 (mirror-padded at the border) -> the four
+//                    moments (a, b, aa + bb, ab) blurred vertically over the 74 tile columns,
+//                    then horizontally -> SSIM map on the tile only -> its three partial images
+//                    (d/d mu_a, d/d (var sum), d/d sigma_ab) to HBM (ssim_g, L2-resident), block
+//                    sums of SSIM and |a - b|;
+//   ssim_bwd_kernel  the partials on the tile + halo 5 -> vertical, then horizontal adjoint
+//                    blur -> gradient of the photometric term.
+// Splitting at the SSIM map removes the halo recompute of the fused form (SSIM map and first
+// adjoint pass on a (TW+10) x (TH+10) region, forward moments on (TW+20) x (TH+20)): ~125
+// instead of ~230 FP32 operations per pixel and channel.  Each pass is register-blocked along
+// its blur axis (a thread produces a strip of 4 outputs from one sliding window of
+// shared-memory reads), blur-axis-first passes run over columns so that a warp's lanes read
+// consecutive words, and the second passes map lanes to rows with an odd float4 row stride
+// (conflict-free LDS.128).
+constexpr int TW = 64, TH = 16;
+constexpr int NR = TH + 10;           // staged rows (halo 5)
+constexpr int NC = TW + 10;           // staged columns (halo 5)
+constexpr int VS = 4;                 // outputs per vertical strip
+constexpr int HS = 4;                 // outputs per horizontal strip
+constexpr int RS = NC + 1;            // row stride (float4) of the vertical-pass output (odd)
+constexpr int H_THREADS = TH * (TW / HS);    // second-pass strips: one per thread
+constexpr int L_THREADS = 320;               // >= the first pass's NC * TH / VS = 296 strips, so
+                                             // that neither pass takes a second round (the idle
+                                             // warps of a pass wait at its barrier without issuing)
+static_assert(H_THREADS == 256 && TH == 16, "second pass: warps 0-7, lanes 0-15 = rows");
+static_assert(NC * (TH / VS) <= L_THREADS, "first pass: one strip per thread");
 constexpr float C1 = 0.01f * 0.01f, C2 = 0.03f * 0.03f;
 
 
@@ -89,34 +98,19 @@ __device__ __forceinline__ float kw(int d) {
     return K[d];
 }
 
-// Item it of `groups` groups of `len` (>= 32) elements, in warp-aligned order: the first 32
-// elements of every group (one warp each), then the remaining len - 32 of every group.
-__device__ __forceinline__ void split32(int it, int groups, int len, int &group, int &elem) {
-    if (it < 32 * groups) {
-        group = it >> 5;
-        elem = it & 31;
-    } else {
-        const int j = it - 32 * groups, rest = len - 32;
-        group = j / rest;
-        elem = 32 + j % rest;
-    }
+// INTERIOR: the CTA's halo lies inside the image, so every blur / adjoint weight is the plain
+// kernel (compile-time immediates); border CTAs read their halo mirror-padded (forward) or the
+// reflection tables (adjoint).
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem));
 }
-
-// INTERIOR: the CTA's whole halo lies >= 10 px inside the image, so every blur / adjoint
-// weight is the plain kernel (compile-time immediates); border CTAs read the reflection tables.
-// The moments travel in pairs -- (a, b) and (a^2 + b^2, ab) through the blurs, (dS/dua, dS/dsig)
-// through the adjoint -- so every tap of every pass is one paired FMA (sm_100 FFMA2) per pair.
-struct SsimSmem {
-    union {
-        float2 in[NIR][NIC];  // (rendered, target) of the channel
-        float4 g[GR][GC];     // SSIM partials (d/d mu_a, d/d (var sum), d/d sigma_ab, -)
-    } u1;
-    union {
-        float4 hx[NIR][HXS];  // horizontal moments (a, b, aa + bb, ab)
-        float4 ry[TH][GC];    // vertical adjoint of the three partial images
-    } u2;
-    float red[2][L_THREADS / 32];
-};
+__device__ __forceinline__ void cp_async16_zfill(void *smem, const void *gmem, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+                 "l"(gmem), "r"(valid ? 16 : 0));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 __device__ __forceinline__ float2 pfma(float w, float2 x, float2 acc) { return __ffma2_rn(make_float2(w, w), x, acc); }
 
@@ -125,125 +119,109 @@ __device__ __forceinline__ float wtab(const float *__restrict__ tab, int pos, in
     return INTERIOR ? kw(d) : __ldg(tab + 22 * pos + d);
 }
 
+struct SsimFwdSmem {
+    float2 in[2][NR][NC];  // (rendered, target) of the channel, halo 5: the tile and the next one
+    float4 v[TH][RS];    // vertically blurred moments (a, b, aa + bb, ab)
+    float red[2][L_THREADS / 32];
+};
+
+struct SsimBwdSmem {
+    float4 g[NR][NC];    // SSIM partials (d/d mu_a, d/d (var sum), d/d sigma_ab, -), halo 5
+    float4 v[TH][RS];    // their vertical adjoint
+};
+
+__device__ __forceinline__ bool ssim_interior(int x0, int y0, int W, int H) {
+    return x0 >= 5 && x0 + TW + 5 <= W && y0 >= 5 && y0 + TH + 5 <= H;
+}
+
+// ssim_fwd inputs of one tile on [y0-5, y0+TH+5) x [x0-5, x0+TW+5) of channel c, mirror-padded
+// (R/losses.py:31-42), issued as cp.async (the caller commits): warp w stages rows w, w + 10, ...,
+// lane l columns l, l + 32, l + 64 (their reflected offsets computed once)
 template <bool INTERIOR>
-__device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
-                                          const float *__restrict__ tab_x, const float *__restrict__ tab_y,
-                                          float lam, int depth_grads_zero) {
-    const float *__restrict__ target = view->target;
-    const float *__restrict__ color = f.color;
+__device__ __forceinline__ void ssim_fwd_stage(float2 (*in)[NC], const float *__restrict__ color,
+                                               const float *__restrict__ target, int W, int H, int x0, int y0,
+                                               int c) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int CP = (NC + 31) / 32;
+    int xo[CP];
+#pragma unroll
+    for (int h = 0; h < CP; h++) {
+        int x = x0 - 5 + lane + 32 * h;
+        if (!INTERIOR) x = reflect_idx(min(x, x0 - 5 + NC - 1), W);
+        xo[h] = 3 * x + c;
+    }
+    for (int iy = warp; iy < NR; iy += L_THREADS / 32) {
+        int y = y0 - 5 + iy;
+        if (!INTERIOR) y = reflect_idx(y, H);
+        const float *crow = color + (int64_t)y * W * 3, *trow = target + (int64_t)y * W * 3;
+#pragma unroll
+        for (int h = 0; h < CP; h++) {
+            const int ix = lane + 32 * h;
+            if (ix < NC) {
+                cp_async4(&in[iy][ix].x, crow + xo[h]);
+                cp_async4(&in[iy][ix].y, trow + xo[h]);
+            }
+        }
+    }
+}
+
+// SSIM map and partials of one staged tile; adds the tile's SSIM and |a - b| sums to s_acc, l1_acc
+template <bool INTERIOR>
+__device__ __forceinline__ void ssim_fwd_tile(SsimFwdSmem &sm, const float2 (*in)[NC], const gs_frame &f, int x0,
+                                              int y0, int c, float &s_acc, float &l1_acc) {
     const int W = f.width, H = f.height;
-    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, c = blockIdx.z;
-    const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
-    const int tid = threadIdx.x;
-    // The forward blurs of every tile are plain 11-tap convolutions (compile-time weights): a
-    // border tile loads its halo mirror-padded (R/losses.py:31-42, triangle wave), which is what
-    // the reflection of the blur amounts to.  Only the adjoint passes of border tiles need the
-    // per-position tables (the reflection folds several taps onto one pixel).
-    constexpr int HB = 6;
-    constexpr int VS = 5, NVS = (GR + VS - 1) / VS;
-    constexpr int AS = 4, NAS = TH / AS;
-    // 1) inputs on [y0-10, y0+TH+10) x [x0-10, x0+TW+10) of channel c, mirror-padded: warp w
-    //    stages rows w, w + 8, ... (the TW + 20 = 52 columns in two lane passes), every load in
-    //    flight before the first store, no index division (columns >= TW + 20 are never read)
-    {
-        constexpr int NW = L_THREADS / 32, RPW = (NIR + NW - 1) / NW, CP = (TW + 20 + 31) / 32;
-        const int warp = tid >> 5, lane = tid & 31;
-        float va[RPW][CP], vb[RPW][CP];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // 2) vertical blur of the moment pairs (a, b) and (a^2 + b^2, ab) -- the SSIM uses the
+    //    variances only as the sum va + vb (R/losses.py:100-104) -- over all NC columns
+    for (int it = tid; it < NC * (TH / VS); it += L_THREADS) {
+        const int s = it / NC, col = it - s * NC, r0 = s * VS;
+        float2 m01[VS], m23[VS];
 #pragma unroll
-        for (int j = 0; j < RPW; j++) {
-            const int iy = warp + NW * j;
-            int y = y0 - 10 + iy;
-            if (!INTERIOR) y = reflect_idx(min(y, y0 - 10 + NIR - 1), H);
+        for (int k = 0; k < VS; k++) m01[k] = m23[k] = make_float2(0.0f, 0.0f);
 #pragma unroll
-            for (int h = 0; h < CP; h++) {
-                const int ix = lane + 32 * h;
-                int x = x0 - 10 + ix;
-                if (!INTERIOR) x = reflect_idx(x, W);
-                va[j][h] = vb[j][h] = 0.0f;
-                if (iy < NIR && ix < TW + 20) {
-                    const int64_t p = (int64_t)y * W + x;
-                    va[j][h] = __ldg(color + 3 * p + c);
-                    vb[j][h] = __ldg(target + 3 * p + c);
+        for (int t = 0; t < VS + 10; t++) {
+            const float2 ab = in[r0 + t][col];
+            const float2 q = make_float2(fmaf(ab.x, ab.x, ab.y * ab.y), ab.x * ab.y);
+#pragma unroll
+            for (int k = 0; k < VS; k++) {
+                const int d = t - k;
+                if (d >= 0 && d < 11) {
+                    m01[k] = pfma(kw(d), ab, m01[k]);
+                    m23[k] = pfma(kw(d), q, m23[k]);
                 }
             }
         }
 #pragma unroll
-        for (int j = 0; j < RPW; j++) {
-            const int iy = warp + NW * j;
-#pragma unroll
-            for (int h = 0; h < CP; h++) {
-                const int ix = lane + 32 * h;
-                if (iy < NIR && ix < TW + 20) sm.u1.in[iy][ix] = make_float2(va[j][h], vb[j][h]);
-            }
-        }
+        for (int k = 0; k < VS; k++) sm.v[r0 + k][col] = make_float4(m01[k].x, m01[k].y, m23[k].x, m23[k].y);
     }
     __syncthreads();
-    // 2) horizontal blur of the 4 moments (a, b, aa + bb, ab) -- SSIM uses the variances only as
-    //    the sum va + vb (R/losses.py:100-104), so blur(aa) + blur(bb) is one blur; hx column j
-    //    <-> x = x0-5+j
-    for (int it = tid; it < NIR * (HXC / HB); it += L_THREADS) {
-        // warp-aligned items: rows 0..31 of a strip per warp, then the last NIR - 32 rows of every
-        // strip (odd row stride: a warp's 32 rows hit distinct banks)
-        int iy, c0;
-        split32(it, HXC / HB, NIR, c0, iy);
-        c0 *= HB;
-        float2 m01[HB], m23[HB];
-#pragma unroll
-        for (int k = 0; k < HB; k++) m01[k] = m23[k] = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int t2 = 0; t2 < (HB + 10) / 2; t2++) {  // two input columns per 16-B load
-            const float4 in2 = *reinterpret_cast<const float4 *>(&sm.u1.in[iy][c0 + 2 * t2]);
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-                const int t = 2 * t2 + h;
-                const float2 ab = h ? make_float2(in2.z, in2.w) : make_float2(in2.x, in2.y);
-                const float2 q = make_float2(fmaf(ab.x, ab.x, ab.y * ab.y), ab.x * ab.y);
-#pragma unroll
-                for (int k = 0; k < HB; k++) {
-                    const int d = t - k;
-                    if (d >= 0 && d < 11) {
-                        m01[k] = pfma(kw(d), ab, m01[k]);
-                        m23[k] = pfma(kw(d), q, m23[k]);
-                    }
+    // 3) horizontal blur -> SSIM map and its partials (R/losses.py:96-113), warps 0-7; lanes
+    //    0-15: rows of strip 2w, lanes 16-31: rows of strip 2w + 1
+    if (tid < H_THREADS) {
+        const int oy = lane & 15, xs = HS * (2 * warp + (lane >> 4));
+        float2 u01[HS], u23[HS];
+    #pragma unroll
+        for (int k = 0; k < HS; k++) u01[k] = u23[k] = make_float2(0.0f, 0.0f);
+    #pragma unroll
+        for (int t = 0; t < HS + 10; t++) {
+            const float4 h = sm.v[oy][xs + t];
+            const float2 h01 = make_float2(h.x, h.y), h23 = make_float2(h.z, h.w);
+    #pragma unroll
+            for (int k = 0; k < HS; k++) {
+                const int d = t - k;
+                if (d >= 0 && d < 11) {
+                    u01[k] = pfma(kw(d), h01, u01[k]);
+                    u23[k] = pfma(kw(d), h23, u23[k]);
                 }
             }
         }
-#pragma unroll
-        for (int k = 0; k < HB; k++) sm.u2.hx[iy][c0 + k] = make_float4(m01[k].x, m01[k].y, m23[k].x, m23[k].y);
-    }
-    __syncthreads();
-    // 3) vertical blur -> SSIM map and its partials (R/losses.py:96-113); g row gy <-> y0-5+gy
-    float s_acc = 0.0f;
-    float2 g01v[VS];
-    float g2v[VS];
-    for (int it = tid; it < GW * NVS; it += L_THREADS) {
-        int gx, gy0;  // warp-aligned items: 32 consecutive columns of one strip per warp
-        split32(it, NVS, GW, gy0, gx);
-        gy0 *= VS;
-        const int x = x0 - 5 + gx;
-        float2 u01[VS], u23[VS];
-#pragma unroll
-        for (int k = 0; k < VS; k++) u01[k] = u23[k] = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int r = 0; r < VS + 10; r++) {
-            if (gy0 + r < NIR) {
-                const float4 h = sm.u2.hx[gy0 + r][gx];
-                const float2 h01 = make_float2(h.x, h.y), h23 = make_float2(h.z, h.w);
-#pragma unroll
-                for (int k = 0; k < VS; k++) {
-                    const int d = r - k;
-                    if (d >= 0 && d < 11) {
-                        u01[k] = pfma(kw(d), h01, u01[k]);
-                        u23[k] = pfma(kw(d), h23, u23[k]);
-                    }
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < VS; k++) {
-            const int gy = gy0 + k, y = y0 - 5 + gy;
-            float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-            if (gy < GR && (INTERIOR || (x >= 0 && x < W && y >= 0 && y < H))) {
+        const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
+        const int y = y0 + oy;
+        float4 *gout = reinterpret_cast<float4 *>(f.ssim_g) + ((int64_t)c * H + y) * W + x0 + xs;
+    #pragma unroll
+        for (int k = 0; k < HS; k++) {
+            const int x = x0 + xs + k;
+            if (INTERIOR || (x < W && y < H)) {
                 const float ua = u01[k].x, ub = u01[k].y;
                 const float vab = u23[k].y - ua * ub;
                 const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
@@ -252,145 +230,208 @@ __device__ __forceinline__ void ssim_tile(SsimSmem &sm, const gs_frame &f, const
                 // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
                 const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
                 const float S = (a1 * a2) * rden;
-                g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) * inv_n;
-                g1 = (-S * rb2) * inv_n;
-                g2 = (2.0f * a1 * rden) * inv_n;
-                if (gy >= 5 && gy < 5 + TH && gx >= 5 && gx < 5 + TW) s_acc += S;
+                const float g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) * inv_n;
+                const float g1 = (-S * rb2) * inv_n;
+                const float g2 = (2.0f * a1 * rden) * inv_n;
+                s_acc += S;
+                const float2 ab = in[oy + 5][xs + k + 5];
+                l1_acc += fabsf(ab.x - ab.y);
+                gout[k] = make_float4(g0, g1, g2, 0.0f);
             }
-            g01v[k] = make_float2(g0, g1);
-            g2v[k] = g2;
         }
-#pragma unroll
-        for (int k = 0; k < VS; k++)
-            if (gy0 + k < GR) sm.u1.g[gy0 + k][gx] = make_float4(g01v[k].x, g01v[k].y, g2v[k], 0.0f);
     }
-    __syncthreads();
-    // 4) vertical adjoint at rows [y0, y0+TH): r(p) = sum_d A[p][d] g(p+d) (zero weights where
-    //    p+d leaves the image)
-    for (int it = tid; it < GW * NAS; it += L_THREADS) {
-        int gx, oy0;
-        split32(it, NAS, GW, oy0, gx);
-        oy0 *= AS;
-        float2 r01[AS];
-        float r2[AS];
+}
+
+template <bool INTERIOR>
+__device__ __forceinline__ void ssim_bwd_tile(SsimBwdSmem &sm, const gs_frame &f, const gs_view *__restrict__ view,
+                                              const float *__restrict__ tab_x, const float *__restrict__ tab_y,
+                                              float lam, int depth_grads_zero) {
+    const float *__restrict__ target = view->target;
+    const float *__restrict__ color = f.color;
+    const int W = f.width, H = f.height;
+    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH, c = blockIdx.z;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float4 *__restrict__ gin = reinterpret_cast<const float4 *>(f.ssim_g) + (int64_t)c * H * W;
+    // 1) partials on [y0-5, y0+TH+5) x [x0-5, x0+TW+5); zero outside the image (the adjoint
+    //    weights of those positions are zero)
+    for (int iy = warp; iy < NR; iy += L_THREADS / 32) {  // warp per row, lanes along it
+        const int y = y0 - 5 + iy;
+        const bool yin = INTERIOR || (y >= 0 && y < H);
+        const float4 *grow = gin + (int64_t)(yin ? y : 0) * W;
 #pragma unroll
-        for (int k = 0; k < AS; k++) {
+        for (int h = 0; h < (NC + 31) / 32; h++) {
+            const int ix = lane + 32 * h, x = x0 - 5 + ix;
+            const bool in = yin && (INTERIOR || (x >= 0 && x < W));
+            if (ix < NC) cp_async16_zfill(&sm.g[iy][ix], grow + (in ? x : 0), in);
+        }
+    }
+    // this thread's rendered / target values for the gradient assembly, fetched under the staging
+    const bool second = tid < H_THREADS;
+    const int oy = lane & 15, xs = HS * (2 * warp + (lane >> 4));
+    const int y = y0 + oy;
+    float av[HS], bv[HS];
+#pragma unroll
+    for (int k = 0; k < HS; k++) {
+        const int x = x0 + xs + k;
+        av[k] = bv[k] = 0.0f;
+        if (second && (INTERIOR || (x < W && y < H))) {
+            const int64_t p = (int64_t)y * W + x;
+            av[k] = __ldg(color + 3 * p + c);
+            bv[k] = __ldg(target + 3 * p + c);
+        }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // 2) vertical adjoint at rows [y0, y0+TH): r(p) = sum_d A[p][d] g(p+d)
+    for (int it = tid; it < NC * (TH / VS); it += L_THREADS) {
+        const int s = it / NC, col = it - s * NC, r0 = s * VS;
+        float2 r01[VS];
+        float r2[VS];
+#pragma unroll
+        for (int k = 0; k < VS; k++) {
             r01[k] = make_float2(0.0f, 0.0f);
             r2[k] = 0.0f;
         }
 #pragma unroll
-        for (int r = 0; r < AS + 10; r++) {
-            const float4 hg = sm.u1.g[oy0 + r][gx];
-            const float2 h01 = make_float2(hg.x, hg.y);
-            const float h2 = hg.z;
+        for (int t = 0; t < VS + 10; t++) {
+            const float4 g = sm.g[r0 + t][col];
+            const float2 g01 = make_float2(g.x, g.y);
 #pragma unroll
-            for (int k = 0; k < AS; k++) {
-                const int d = r - k;
-                if (d >= 0 && d < 11) {
-                    const int yp = min(y0 + oy0 + k, H - 1);
-                    const float w = wtab<INTERIOR>(tab_y + 11, yp, d);
-                    r01[k] = pfma(w, h01, r01[k]);
-                    r2[k] = fmaf(w, h2, r2[k]);
-                }
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < AS; k++) {
-            const bool ok = INTERIOR || y0 + oy0 + k < H;
-            sm.u2.ry[oy0 + k][gx] = ok ? make_float4(r01[k].x, r01[k].y, r2[k], 0.0f) : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-    }
-    __syncthreads();
-    // 5) horizontal adjoint + gradient assembly (R/losses.py:115-117 and :126-130); a warp
-    //    covers 16 rows x 2 strips
-    float l1_acc = 0.0f;
-    {
-        // lanes 0-15: strip w, lanes 16-31: strip w + 8
-        const int oy = tid & 15, ox0 = HS * ((tid >> 5) + 8 * ((tid >> 4) & 1));
-        float2 A01[HS];
-        float A2[HS];
-#pragma unroll
-        for (int k = 0; k < HS; k++) {
-            A01[k] = make_float2(0.0f, 0.0f);
-            A2[k] = 0.0f;
-        }
-#pragma unroll
-        for (int t = 0; t < HS + 10; t++) {
-            const float4 rv = sm.u2.ry[oy][ox0 + t];
-            const float2 v01 = make_float2(rv.x, rv.y);
-            const float v2 = rv.z;
-#pragma unroll
-            for (int k = 0; k < HS; k++) {
+            for (int k = 0; k < VS; k++) {
                 const int d = t - k;
                 if (d >= 0 && d < 11) {
-                    const int xp = min(x0 + ox0 + k, W - 1);
-                    const float w = wtab<INTERIOR>(tab_x + 11, xp, d);
-                    A01[k] = pfma(w, v01, A01[k]);
-                    A2[k] = fmaf(w, v2, A2[k]);
+                    const int yp = min(y0 + r0 + k, H - 1);
+                    const float w = wtab<INTERIOR>(tab_y + 11, yp, d);
+                    r01[k] = pfma(w, g01, r01[k]);
+                    r2[k] = fmaf(w, g.z, r2[k]);
                 }
             }
         }
-        const int y = y0 + oy;
+#pragma unroll
+        for (int k = 0; k < VS; k++) sm.v[r0 + k][col] = make_float4(r01[k].x, r01[k].y, r2[k], 0.0f);
+    }
+    __syncthreads();
+    // 3) horizontal adjoint + gradient assembly (R/losses.py:115-117 and :126-130), warps 0-7
+    if (!second) return;
+    float2 A01[HS];
+    float A2[HS];
+#pragma unroll
+    for (int k = 0; k < HS; k++) {
+        A01[k] = make_float2(0.0f, 0.0f);
+        A2[k] = 0.0f;
+    }
+#pragma unroll
+    for (int t = 0; t < HS + 10; t++) {
+        const float4 rv = sm.v[oy][xs + t];
+        const float2 v01 = make_float2(rv.x, rv.y);
 #pragma unroll
         for (int k = 0; k < HS; k++) {
-            const int x = x0 + ox0 + k;
-            if (INTERIOR || (x < W && y < H)) {
-                const int64_t p = (int64_t)y * W + x;
-                const float a = __ldg(color + 3 * p + c), b = __ldg(target + 3 * p + c);
-                const float diff = a - b;
-                l1_acc += fabsf(diff);
-                const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
-                f.g_color[3 * p + c] =
-                    (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A01[k].x + 2.0f * a * A01[k].y + b * A2[k]));
-                // the depth/opacity gradient images start at zero (the LiDAR kernel follows; under
-                // GS_LOSS_DEPTH_GRADS_ZERO they already are, and the LiDAR kernel runs alongside)
-                if (c == 0 && !depth_grads_zero) {
-                    f.g_depth[p] = 0.0f;
-                    f.g_opac[p] = 0.0f;
-                }
+            const int d = t - k;
+            if (d >= 0 && d < 11) {
+                const int xp = min(x0 + xs + k, W - 1);
+                const float w = wtab<INTERIOR>(tab_x + 11, xp, d);
+                A01[k] = pfma(w, v01, A01[k]);
+                A2[k] = fmaf(w, rv.z, A2[k]);
             }
         }
     }
-    // block partial sums (deterministic order: warp butterfly, then fixed warp order)
+    const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
+#pragma unroll
+    for (int k = 0; k < HS; k++) {
+        const int x = x0 + xs + k;
+        if (INTERIOR || (x < W && y < H)) {
+            const int64_t p = (int64_t)y * W + x;
+            const float a = av[k], b = bv[k];
+            const float diff = a - b;
+            const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
+            f.g_color[3 * p + c] =
+                (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A01[k].x + 2.0f * a * A01[k].y + b * A2[k]));
+            // the depth/opacity gradient images start at zero (the LiDAR kernel follows; under
+            // GS_LOSS_DEPTH_GRADS_ZERO they already are, and the LiDAR kernel runs alongside)
+            if (c == 0 && !depth_grads_zero) {
+                f.g_depth[p] = 0.0f;
+                f.g_opac[p] = 0.0f;
+            }
+        }
+    }
+}
+
+// persistent: CTA k takes tiles k, k + grid, ... (tile = channel-major, then row, then column),
+// the next tile's inputs streaming in (cp.async, double buffer) while this one is computed; one
+// (|a - b|, SSIM) partial per CTA, summed in a fixed order (deterministic)
+__global__ void __launch_bounds__(L_THREADS, 4) ssim_fwd_kernel(gs_frame f, const gs_view *__restrict__ view) {
+    pdl_wait();
+    extern __shared__ float4 sf_raw[];
+    SsimFwdSmem &sm = *reinterpret_cast<SsimFwdSmem *>(sf_raw);
+    const int W = f.width, H = f.height;
+    const int ntx = (W + TW - 1) / TW, nty = (H + TH - 1) / TH, T = 3 * ntx * nty;
+    const float *__restrict__ target = view->target;
+    const float *__restrict__ color = f.color;
+    auto tile_xy = [&](int t, int &x0, int &y0, int &c) {
+        c = t / (ntx * nty);
+        const int r = t - c * ntx * nty;
+        y0 = (r / ntx) * TH;
+        x0 = (r - (r / ntx) * ntx) * TW;
+    };
+    auto stage = [&](int t, int buf) {
+        int x0, y0, c;
+        tile_xy(t, x0, y0, c);
+        if (ssim_interior(x0, y0, W, H)) ssim_fwd_stage<true>(sm.in[buf], color, target, W, H, x0, y0, c);
+        else ssim_fwd_stage<false>(sm.in[buf], color, target, W, H, x0, y0, c);
+    };
+    float s_acc = 0.0f, l1_acc = 0.0f;
+    int t = blockIdx.x, buf = 0;
+    if (t < T) stage(t, 0);
+    cp_async_commit();
+    for (; t < T; t += gridDim.x, buf ^= 1) {
+        if (t + (int)gridDim.x < T) stage(t + gridDim.x, buf ^ 1);
+        cp_async_commit();
+        cp_async_wait_1();  // this tile's inputs have landed (the next tile's stay in flight)
+        __syncthreads();
+        int x0, y0, c;
+        tile_xy(t, x0, y0, c);
+        if (ssim_interior(x0, y0, W, H)) ssim_fwd_tile<true>(sm, sm.in[buf], f, x0, y0, c, s_acc, l1_acc);
+        else ssim_fwd_tile<false>(sm, sm.in[buf], f, x0, y0, c, s_acc, l1_acc);
+        __syncthreads();  // the input buffer and the moments are free for the tile after next
+    }
+    // CTA partial sums (deterministic order: warp butterfly, then fixed warp order)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int o = 16; o > 0; o >>= 1) {
         l1_acc += __shfl_xor_sync(0xffffffffu, l1_acc, o);
         s_acc += __shfl_xor_sync(0xffffffffu, s_acc, o);
     }
-    if ((tid & 31) == 0) {
-        sm.red[0][tid >> 5] = l1_acc;
-        sm.red[1][tid >> 5] = s_acc;
+    if (lane == 0) {
+        sm.red[0][warp] = l1_acc;
+        sm.red[1][warp] = s_acc;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
         double l1 = 0.0, ss = 0.0;
         for (int w = 0; w < L_THREADS / 32; w++) {
             l1 += sm.red[0][w];
             ss += sm.red[1][w];
         }
-        const int64_t blk = ((int64_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-        f.loss_parts[3 * blk] = l1;
-        f.loss_parts[3 * blk + 1] = ss;
-        f.loss_parts[3 * blk + 2] = 0.0;
+        f.loss_parts[3 * blockIdx.x] = l1;
+        f.loss_parts[3 * blockIdx.x + 1] = ss;
+        f.loss_parts[3 * blockIdx.x + 2] = 0.0;
     }
 }
 
-// one launch for every (tile, channel): interior tiles (halo >= 10 px inside the image) take
-// the compile-time-weight path, border tiles the reflection-table path
-__global__ void __launch_bounds__(L_THREADS, 4) ssim_l1_kernel(gs_frame f, const gs_view *__restrict__ view,
-                                                               const float *__restrict__ tab_x,
-                                                               const float *__restrict__ tab_y, float lam,
-                                                               int depth_grads_zero) {
+__global__ void __launch_bounds__(L_THREADS, 3) ssim_bwd_kernel(gs_frame f, const gs_view *__restrict__ view,
+                                                                const float *__restrict__ tab_x,
+                                                                const float *__restrict__ tab_y, float lam,
+                                                                int depth_grads_zero) {
     pdl_wait();
     // let the LiDAR kernel launch into the SMs this grid's last wave leaves idle (it waits for
     // this grid's completion itself before it reads the partials, or before anything when the
     // g_depth / g_opac clearing below is on)
     asm volatile("griddepcontrol.launch_dependents;");
-    __shared__ SsimSmem sm;
-    const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
-    if (x0 >= 10 && x0 + TW + 10 <= f.width && y0 >= 10 && y0 + TH + 10 <= f.height)
-        ssim_tile<true>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
+    extern __shared__ float4 sb_raw[];
+    SsimBwdSmem &sm = *reinterpret_cast<SsimBwdSmem *>(sb_raw);
+    if (ssim_interior(blockIdx.x * TW, blockIdx.y * TH, f.width, f.height))
+        ssim_bwd_tile<true>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
     else
-        ssim_tile<false>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
+        ssim_bwd_tile<false>(sm, f, view, tab_x, tab_y, lam, depth_grads_zero);
 }
 
 // depth_ratio_loss on the LiDAR K-list (R/losses.py:133-154), scaled by xi (R/losses.py:161)
@@ -568,15 +609,21 @@ extern "C" int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, flo
     }
     dim3 grid((f->width + TW - 1) / TW, (f->height + TH - 1) / TH, 3);
     const int dz = (flags & GS_LOSS_DEPTH_GRADS_ZERO) ? 1 : 0;
-    launch_pdl(ssim_l1_kernel, grid, L_THREADS, 0, st, *f, view, tab_x, tab_y, lam, dz);
-    if ((rc = check_launch("ssim_l1_kernel"))) return rc;
-    launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, lam, xi, ssim_blocks, tab_y + 22 * f->height,
+    const int fwd_ctas = (int)std::min<int64_t>(ssim_blocks, 4 * 148);
+    launch_pdl(ssim_fwd_kernel, fwd_ctas, L_THREADS, sizeof(SsimFwdSmem), st, *f, view);
+    if ((rc = check_launch("ssim_fwd_kernel"))) return rc;
+    launch_pdl(ssim_bwd_kernel, grid, L_THREADS, sizeof(SsimBwdSmem), st, *f, view, tab_x, tab_y, lam, dz);
+    if ((rc = check_launch("ssim_bwd_kernel"))) return rc;
+    launch_pdl(depth_loss_kernel, DEPTH_BLOCKS, 256, 0, st, *f, view, lam, xi, (int64_t)fwd_ctas, tab_y + 22 * f->height,
                (flags & GS_LOSS_ACCUMULATE) ? 1 : 0, dz);
     return check_launch("depth_loss_kernel");
 }
 
 namespace gs {
 void init_loss_attrs() {
-    cudaFuncSetAttribute(ssim_l1_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ssim_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimFwdSmem));
+    cudaFuncSetAttribute(ssim_fwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(ssim_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimBwdSmem));
+    cudaFuncSetAttribute(ssim_bwd_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 }  // namespace gs

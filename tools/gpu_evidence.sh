@@ -2,7 +2,7 @@
 # One gpurun call producing the round's evidence: GPU parity tests, smoke, bench (N=1, with CPU
 # baseline), reference arm, ncu launch list, and --set full captures of the top kernels.
 #   gpurun --timeout 2400 -- bash tools/gpu_evidence.sh <tag> [kernel-regex] [count]
-TAG=${1:-ev}; K=${2:-render_bwd_kernel|preprocess_kernel|ssim_l1_kernel|chain_kernel|render_fwd_kernel|big_cull|huge_sort|tile_scan}; C=${3:-10}
+TAG=${1:-ev}; K=${2:-render_bwd_kernel|preprocess_kernel|ssim_fwd_kernel|ssim_bwd_kernel|chain_kernel|render_fwd_kernel|big_cull|huge_sort|tile_scan}; C=${3:-10}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
 nvidia-smi > gpurun_out/nvidia-smi_$TAG.txt 2>&1

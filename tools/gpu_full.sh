@@ -1,7 +1,7 @@
 #!/bin/bash
 # gpurun --timeout 1500 -- bash tools/gpu_full.sh <tag> <kernel-regex> [count] [pytest-args]
 # --set full captures (warm, graph replay) of the kernels matching the regex, after the GPU tests.
-TAG=${1:-f}; K=${2:-ssim_l1_kernel}; C=${3:-6}; shift 3; PT=${@:-tests -m gpu -x -q}
+TAG=${1:-f}; K=${2:-ssim_fwd_kernel}; C=${3:-6}; shift 3; PT=${@:-tests -m gpu -x -q}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
 timeout 900 python -m pytest $PT > gpurun_out/pt_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pt_$TAG.log

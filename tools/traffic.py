@@ -9,7 +9,7 @@ import sys
 PHASE = {"preprocess": ("preprocess_kernel", "big_cull"),
          "bin": ("huge_sort", "huge_transpose", "tile_scan", "bucket_fill", "tile_sort_merge"),
          "render_fwd": ("render_fwd", "lazy_fill", "tile_finish"),
-         "loss": ("loss_tables", "ssim_l1", "depth_loss", "loss_finalize"),
+         "loss": ("loss_tables", "ssim_fwd", "ssim_bwd", "depth_loss", "loss_finalize"),
          "render_bwd": ("zero_g2d", "render_bwd"),
          "chain_adam": ("chain_kernel", "adam_list")}
 rows = list(csv.reader(open(sys.argv[1])))
