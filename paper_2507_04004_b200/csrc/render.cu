@@ -507,14 +507,16 @@ __device__ __forceinline__ void bwd_step2(BwdPair &p, bool act0, bool act1, cons
     p.T = make_float2(act0 ? Tb.x : p.T.x, act1 ? Tb.y : p.T.y);
 }
 
-// 128 threads per 16x16 tile, two pixels per thread (rows y and y + 8): the two pixels'
-// contributions are summed in registers before the warp reduction.  Deterministic: per staged
-// entry every warp stores its butterfly sums in its own shared-memory slot, the four warp sums
-// are added in warp order, and the tile partial goes to the Gaussian's row through fixed-point
-// integer atomics (fx_atomic_add) -- no floating-point sum depends on scheduling order.
-constexpr int BT = RT / 2;          // backward threads per tile (two pixels each)
+// 64 threads per 16x16 tile, four pixels per thread (column x, rows r, r + 4, r + 8, r + 12 as
+// two row pairs): the four pixels' contributions are summed in registers before the warp
+// reduction, so each staged entry costs the tile two warp reductions instead of eight (one per
+// 32 pixels).  Deterministic: per staged entry every warp stores its butterfly sums in its own
+// shared-memory slot, the warp sums are added in warp order, and the tile partial goes to the
+// Gaussian's row through fixed-point integer atomics (fx_atomic_add) -- no floating-point sum
+// depends on scheduling order.
+constexpr int BT = RT / 4;          // backward threads per tile (four pixels each)
 constexpr int BW = BT / 32;         // warps per backward CTA
-constexpr int BST = BT / 2;         // entries staged per round
+constexpr int BST = BT;             // entries staged per round (one per thread)
 
 __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_depth_grads) {
     pdl_wait();
@@ -528,10 +530,11 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
     const int tile = blockIdx.x;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
+    const int col = threadIdx.x & 15, row = threadIdx.x >> 4;  // rows row + 4 k, k < 4
     if (clear_depth_grads && stop == start) {  // (GS_BWD_CLEAR_DEPTH_GRADS) an empty tile's pixels
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
-            const int x = tx * GS_TILE + (threadIdx.x & 15), y = ty * GS_TILE + (threadIdx.x >> 4) + (GS_TILE / 2) * k;
+        for (int k = 0; k < 4; k++) {
+            const int x = tx * GS_TILE + col, y = ty * GS_TILE + row + 4 * k;
             if (x < f.width && y < f.height) {
                 const int64_t q = (int64_t)y * f.width + x;
                 if (f.g_depth[q] != 0.0f) f.g_depth[q] = 0.0f;
@@ -559,43 +562,49 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         // lazy, unflagged: the blend ended within the leading screen-covering Gaussians
         return lazy ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : f.entry_splat[start + p];
     };
-    BwdPair px;
+    BwdPair px[2];  // pair h: rows row + 4 h and row + 4 h + 8
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
     {
-        const int x = tx * GS_TILE + (threadIdx.x & 15), y0 = ty * GS_TILE + (threadIdx.x >> 4);
-        px.fx = (float)x;
-        px.fy = make_float2((float)y0, (float)(y0 + GS_TILE / 2));
-        float T[2] = {1.0f, 1.0f}, gc[2][3] = {}, gd[2] = {}, go[2] = {};
-        int cnt[2] = {0, 0};
+        const int x = tx * GS_TILE + col;
+        int mx = 0;
 #pragma unroll
-        for (int k = 0; k < 2; k++) {
-            const int y = y0 + (GS_TILE / 2) * k;
-            if (x < f.width && y < f.height) {
-                const int64_t q = (int64_t)y * f.width + x;
-                T[k] = f.trans[q];
-                cnt[k] = f.n_contrib[q];
-                gc[k][0] = f.g_color[3 * q];
-                gc[k][1] = f.g_color[3 * q + 1];
-                gc[k][2] = f.g_color[3 * q + 2];
-                gd[k] = f.g_depth[q];
-                go[k] = f.g_opac[q];
-                if (clear_depth_grads) {  // nonzero only at the view's LiDAR pixels
-                    if (gd[k] != 0.0f) f.g_depth[q] = 0.0f;
-                    if (go[k] != 0.0f) f.g_opac[q] = 0.0f;
+        for (int h = 0; h < 2; h++) {
+            const int y0 = ty * GS_TILE + row + 4 * h;
+            px[h].fx = (float)x;
+            px[h].fy = make_float2((float)y0, (float)(y0 + GS_TILE / 2));
+            float T[2] = {1.0f, 1.0f}, gc[2][3] = {}, gd[2] = {}, go[2] = {};
+            int cnt[2] = {0, 0};
+#pragma unroll
+            for (int k = 0; k < 2; k++) {
+                const int y = y0 + (GS_TILE / 2) * k;
+                if (x < f.width && y < f.height) {
+                    const int64_t q = (int64_t)y * f.width + x;
+                    T[k] = f.trans[q];
+                    cnt[k] = f.n_contrib[q];
+                    gc[k][0] = f.g_color[3 * q];
+                    gc[k][1] = f.g_color[3 * q + 1];
+                    gc[k][2] = f.g_color[3 * q + 2];
+                    gd[k] = f.g_depth[q];
+                    go[k] = f.g_opac[q];
+                    if (clear_depth_grads) {  // nonzero only at the view's LiDAR pixels
+                        if (gd[k] != 0.0f) f.g_depth[q] = 0.0f;
+                        if (go[k] != 0.0f) f.g_opac[q] = 0.0f;
+                    }
                 }
             }
+            px[h].T = make_float2(T[0], T[1]);
+            px[h].gc0 = make_float2(gc[0][0], gc[1][0]);
+            px[h].gc1 = make_float2(gc[0][1], gc[1][1]);
+            px[h].gc2 = make_float2(gc[0][2], gc[1][2]);
+            px[h].gd = make_float2(gd[0], gd[1]);
+            px[h].go = make_float2(go[0], go[1]);
+            px[h].S0 = px[h].S1 = px[h].S2 = px[h].Sd = px[h].So = f2(0.0f);
+            px[h].cnt0 = cnt[0];
+            px[h].cnt1 = cnt[1];
+            mx = max(mx, max(cnt[0], cnt[1]));
         }
-        px.T = make_float2(T[0], T[1]);
-        px.gc0 = make_float2(gc[0][0], gc[1][0]);
-        px.gc1 = make_float2(gc[0][1], gc[1][1]);
-        px.gc2 = make_float2(gc[0][2], gc[1][2]);
-        px.gd = make_float2(gd[0], gd[1]);
-        px.go = make_float2(go[0], go[1]);
-        px.S0 = px.S1 = px.S2 = px.Sd = px.So = f2(0.0f);
-        px.cnt0 = cnt[0];
-        px.cnt1 = cnt[1];
-        atomicMax(&s_max, max(cnt[0], cnt[1]));
+        atomicMax(&s_max, mx);
     }
     __syncthreads();
     const int max_cnt = s_max;
@@ -604,7 +613,7 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         const int b0 = max(start, b_end - BST);
         const int nb = b_end - b0;
         __syncthreads();
-        if ((int)threadIdx.x < nb) {  // (nb <= BST <= BT)
+        if ((int)threadIdx.x < nb) {  // (nb <= BST == BT)
             const int i = threadIdx.x;
             const int64_t g = fetch(b0 - start + i);
             s_g[i] = (int)g;
@@ -615,15 +624,16 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         __syncthreads();
         for (int j = nb - 1; j >= 0; j--) {
             const int le = b0 + j - start;
-            const bool a0 = le < px.cnt0, a1 = le < px.cnt1;
+            const bool a00 = le < px[0].cnt0, a01 = le < px[0].cnt1, a10 = le < px[1].cnt0, a11 = le < px[1].cnt1;
             double sg = 0.0;
             float sc = 0.0f;
-            if (__any_sync(0xffffffffu, a0 || a1)) {
+            if (__any_sync(0xffffffffu, a00 || a01 || a10 || a11)) {
                 const float4 A = s_a[j], B = s_b[j], C = s_c[j];
                 float2 v[10];
 #pragma unroll
                 for (int k = 0; k < 10; k++) v[k] = f2(0.0f);
-                bwd_step2(px, a0, a1, A, B, C, v);
+                bwd_step2(px[0], a00, a01, A, B, C, v);
+                bwd_step2(px[1], a10, a11, A, B, C, v);
                 float vg[6], vc[4];
 #pragma unroll
                 for (int k = 0; k < 6; k++) vg[k] = v[k].x + v[k].y;
