@@ -428,15 +428,21 @@ __device__ __forceinline__ int cull_rect(float mx, float my, float ca, float cb,
     return count;
 }
 
+// c / n for 0 <= c < 2^16 and 1 <= n <= 2^16 from rn = 1/n (fp32): (c + 0.5) / n lies >= 0.5 / n
+// from every integer, far beyond the ~1e-7 relative error of the product, so the floor is exact
+// (an integer divide by a runtime value is a ~20-instruction subroutine)
+__device__ __forceinline__ int small_div(int c, float rn) { return (int)(((float)c + 0.5f) * rn); }
+
 // Per-tile bucket counts (tile_scratch[0..T)) and smallest keys of one Gaussian's kept
 // candidates (cull bits of cull_rect, ncand <= GS_SMALL_CAND); fire-and-forget reductions.
 __device__ __forceinline__ void count_kept_tiles(int32_t *cnt, unsigned long long *minkey, unsigned long long key, int4 r,
                                                  uint64_t bits, int tiles_x) {
     const int nx = r.y - r.x + 1;
+    const float rnx = __frcp_rn((float)nx);
     while (bits) {
         const int c = __ffsll((long long)bits) - 1;
         bits &= bits - 1ull;
-        const int t = (r.z + c / nx) * tiles_x + r.x + c % nx;
+        const int dy = small_div(c, rnx), t = (r.z + dy) * tiles_x + r.x + c - dy * nx;
         atomicAdd(&cnt[t], 1);
         atomicMin(&minkey[t], key);  // smallest bucketed key of the tile (lazy lists)
     }

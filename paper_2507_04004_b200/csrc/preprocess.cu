@@ -53,7 +53,8 @@ __device__ __forceinline__ float3 pp_colour(const float4 &c0, const float4 &c2, 
     float un = sqrtf(u0 * u0 + u1 * u1 + u2 * u2);
     if (un < 1e-12f) un = 1.0f;
     float b[16];
-    sh_basis(u0 / un, u1 / un, u2 / un, b);
+    const float run = 1.0f / un;
+    sh_basis(u0 * run, u1 * run, u2 * run, b);
     // floats 11-15: sh_low 0-2 (c2.w, c3.x, c3.y), sh_high[0] (c3.z, c3.w)
     float acc[3] = {b[1] * c3.z, b[1] * c3.w, 0.0f};
 #pragma unroll
@@ -116,7 +117,8 @@ __device__ __forceinline__ uint32_t warp_cull_small(bool flag, float mx, float m
         const int onx = __shfl_sync(0xffffffffu, nx, own);
         bool keep = false;
         if (idx < total) {
-            const int tx = orx + c % onx, ty = orz + c / onx;
+            const int dy = small_div(c, __frcp_rn((float)onx));
+            const int tx = orx + c - dy * onx, ty = orz + dy;
             const int x0 = tx * GS_TILE, x1 = min(x0 + GS_TILE - 1, width - 1);
             const int y0 = ty * GS_TILE, y1 = min(y0 + GS_TILE - 1, height - 1);
             keep = tile_keep(omx, omy, oca, ocb, occ, oq, x0, x1, y0, y1);
