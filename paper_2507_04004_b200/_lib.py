@@ -12,7 +12,7 @@ import os
 from .errors import DataError, DomainError, NumericalError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# GSLIC_LIB: a developer override for A/B builds (tools/build_variant.sh); default the in-tree build
+# GSLIC_LIB: a developer override for A/B builds (tools/gpu_ab.sh); default the in-tree build
 LIB_PATH = os.environ.get("GSLIC_LIB") or os.path.join(_HERE, "lib", "libgslic.so")
 
 GS_ROW = 64
