@@ -112,6 +112,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// barrier over the first n threads of the CTA (the warps that run the second pass)
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 __device__ __forceinline__ float2 pfma(float w, float2 x, float2 acc) { return __ffma2_rn(make_float2(w, w), x, acc); }
 
 template <bool INTERIOR>
@@ -217,27 +220,40 @@ __device__ __forceinline__ void ssim_fwd_tile(SsimFwdSmem &sm, const float2 (*in
         }
         const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
         const int y = y0 + oy;
-        float4 *gout = reinterpret_cast<float4 *>(f.ssim_g) + ((int64_t)c * H + y) * W + x0 + xs;
+        float4 gk[HS];
     #pragma unroll
         for (int k = 0; k < HS; k++) {
             const int x = x0 + xs + k;
+            const float ua = u01[k].x, ub = u01[k].y;
+            const float vab = u23[k].y - ua * ub;
+            const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
+            const float uu = ua * ua + ub * ub;
+            const float b1 = uu + C1, b2 = (u23[k].x - uu) + C2;  // va + vb + C2
+            // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
+            const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
+            const float S = (a1 * a2) * rden;
+            const float g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) * inv_n;
+            const float g1 = (-S * rb2) * inv_n;
+            const float g2 = (2.0f * a1 * rden) * inv_n;
+            gk[k] = make_float4(g0, g1, g2, 0.0f);
             if (INTERIOR || (x < W && y < H)) {
-                const float ua = u01[k].x, ub = u01[k].y;
-                const float vab = u23[k].y - ua * ub;
-                const float a1 = 2.0f * ua * ub + C1, a2 = 2.0f * vab + C2;
-                const float uu = ua * ua + ub * ub;
-                const float b1 = uu + C1, b2 = (u23[k].x - uu) + C2;  // va + vb + C2
-                // b1 >= C1, b2 ~ va + vb + C2 > 0: MUFU reciprocals (no IEEE divide sequences)
-                const float rb1 = fast_rcp(b1), rb2 = fast_rcp(b2), rden = rb1 * rb2;
-                const float S = (a1 * a2) * rden;
-                const float g0 = ((2.0f * ub * a2 - 2.0f * a1 * ub) * rden - S * (2.0f * ua) * rb1 + S * (2.0f * ua) * rb2) * inv_n;
-                const float g1 = (-S * rb2) * inv_n;
-                const float g2 = (2.0f * a1 * rden) * inv_n;
                 s_acc += S;
                 const float2 ab = in[oy + 5][xs + k + 5];
                 l1_acc += fabsf(ab.x - ab.y);
-                gout[k] = make_float4(g0, g1, g2, 0.0f);
             }
+        }
+        // the partials leave through shared memory: this thread's lanes run down the rows (the
+        // conflict-free layout of the blur), the stores run along them (coalesced 16-B rows)
+        named_sync(1, H_THREADS);  // every horizontal window of sm.v has been read
+    #pragma unroll
+        for (int k = 0; k < HS; k++) sm.v[oy][xs + k] = gk[k];
+        named_sync(1, H_THREADS);
+        float4 *gout = reinterpret_cast<float4 *>(f.ssim_g) + (int64_t)c * H * W;
+    #pragma unroll
+        for (int k = 0; k < TH * TW / H_THREADS; k++) {
+            const int q = tid + H_THREADS * k, ry = q / TW, rx = q - ry * TW;
+            const int gy = y0 + ry, gx = x0 + rx;
+            if (INTERIOR || (gx < W && gy < H)) gout[(int64_t)gy * W + gx] = sm.v[ry][rx];
         }
     }
 }
@@ -268,11 +284,14 @@ __device__ __forceinline__ void ssim_bwd_tile(SsimBwdSmem &sm, const gs_frame &f
     // this thread's rendered / target values for the gradient assembly, fetched under the staging
     const bool second = tid < H_THREADS;
     const int oy = lane & 15, xs = HS * (2 * warp + (lane >> 4));
-    const int y = y0 + oy;
-    float av[HS], bv[HS];
+    // the gradient assembly runs along the rows (coalesced): thread tid takes pixels
+    // q = tid + H_THREADS k of the tile; their rendered / target values load under the staging
+    constexpr int AQ = TH * TW / H_THREADS;
+    float av[AQ], bv[AQ];
 #pragma unroll
-    for (int k = 0; k < HS; k++) {
-        const int x = x0 + xs + k;
+    for (int k = 0; k < AQ; k++) {
+        const int q = tid + H_THREADS * k, ry = q / TW, rx = q - ry * TW;
+        const int x = x0 + rx, y = y0 + ry;
         av[k] = bv[k] = 0.0f;
         if (second && (INTERIOR || (x < W && y < H))) {
             const int64_t p = (int64_t)y * W + x;
@@ -335,17 +354,24 @@ __device__ __forceinline__ void ssim_bwd_tile(SsimBwdSmem &sm, const gs_frame &f
             }
         }
     }
+    // transpose through shared memory: every window of sm.v has been read, then each thread
+    // leaves its four pixels' adjoints and the assembly picks them up along the rows
+    named_sync(1, H_THREADS);
+#pragma unroll
+    for (int k = 0; k < HS; k++) sm.v[oy][xs + k] = make_float4(A01[k].x, A01[k].y, A2[k], 0.0f);
+    named_sync(1, H_THREADS);
     const float inv_n = 1.0f / (3.0f * (float)W * (float)H);
 #pragma unroll
-    for (int k = 0; k < HS; k++) {
-        const int x = x0 + xs + k;
+    for (int k = 0; k < AQ; k++) {
+        const int q = tid + H_THREADS * k, ry = q / TW, rx = q - ry * TW;
+        const int x = x0 + rx, y = y0 + ry;
         if (INTERIOR || (x < W && y < H)) {
             const int64_t p = (int64_t)y * W + x;
+            const float4 A = sm.v[ry][rx];
             const float a = av[k], b = bv[k];
             const float diff = a - b;
             const float sg = (float)((diff > 0.0f) - (diff < 0.0f));
-            f.g_color[3 * p + c] =
-                (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A01[k].x + 2.0f * a * A01[k].y + b * A2[k]));
+            f.g_color[3 * p + c] = (1.0f - lam) * (sg * inv_n) + lam * (-0.5f * (A.x + 2.0f * a * A.y + b * A.z));
             // the depth/opacity gradient images start at zero (the LiDAR kernel follows; under
             // GS_LOSS_DEPTH_GRADS_ZERO they already are, and the LiDAR kernel runs alongside)
             if (c == 0 && !depth_grads_zero) {

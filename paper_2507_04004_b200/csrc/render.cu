@@ -168,6 +168,44 @@ __device__ __forceinline__ void fwd_pair_store(const gs_frame &f, int tile, cons
 // per-pixel termination, alphas bit-identical to the scalar path.
 constexpr int FT = RT / 2;
 
+// Blends the nb staged entries (list positions b, b + 1, ...) into the thread's two pixels.
+// Branch-free per-pixel bookkeeping: a pixel that is still blending takes the entry (T and its
+// count advance) and, with EARLY, stops after the entry that drives T below 1e-4 -- the
+// reference's semantics (R/rasterizer.py:270-291) with selects instead of divergent branches.
+template <bool EARLY>
+__device__ __forceinline__ void blend_chunk2(FwdPair &px, const FwdStage &st, int b, int nb) {
+    unsigned act = (px.done0 ? 0u : 1u) | (px.done1 ? 0u : 2u);
+    int n0 = px.cnt0, n1 = px.cnt1;
+    float2 T = px.T;
+    for (int j = 0; j < nb && act; j++) {
+        const float4 A = st.a[j], B = st.b[j], C = st.c[j];
+        const float dx = px.fx - A.x;
+        const float2 dy = add2(px.fy, f2(-A.y));
+        float2 au, ev, alpha, om;
+        bool c0, c1;
+        alpha2(A, B, dx, dy, au, ev, alpha, om, c0, c1);
+        const bool a0 = act & 1u, a1 = act & 2u;
+        float2 w = mul2(alpha, T);
+        w = make_float2(a0 ? w.x : 0.0f, a1 ? w.y : 0.0f);
+        px.c0 = fma2(f2(C.x), w, px.c0);
+        px.c1 = fma2(f2(C.y), w, px.c1);
+        px.c2 = fma2(f2(C.z), w, px.c2);
+        px.dsum = fma2(f2(B.z), w, px.dsum);
+        px.osum = add2(px.osum, w);
+        const float2 Tn = mul2(T, om);
+        const int e1 = b + j + 1;
+        T = make_float2(a0 ? Tn.x : T.x, a1 ? Tn.y : T.y);
+        n0 = a0 ? e1 : n0;
+        n1 = a1 ? e1 : n1;
+        if (EARLY) act &= (Tn.x < GS_EARLY_STOP_T ? 0u : 1u) | (Tn.y < GS_EARLY_STOP_T ? 0u : 2u);
+    }
+    px.T = T;
+    px.done0 = !(act & 1u);
+    px.done1 = !(act & 2u);
+    px.cnt0 = n0;
+    px.cnt1 = n1;
+}
+
 template <typename Fetch>
 __device__ __forceinline__ bool blend_range2(const gs_frame &f, FwdPair &px, FwdStage &st, int p0, int p1,
                                              int early_stop, Fetch fetch) {
@@ -183,38 +221,11 @@ __device__ __forceinline__ bool blend_range2(const gs_frame &f, FwdPair &px, Fwd
         }
         __syncthreads();
         const int nb = min(step, p1 - b);
-        for (int j = 0; j < nb && !(px.done0 && px.done1); j++) {
-            const float4 A = st.a[j], B = st.b[j], C = st.c[j];
-            const float dx = px.fx - A.x;
-            const float2 dy = add2(px.fy, f2(-A.y));
-            float2 au, ev, alpha, om;
-            bool c0, c1;
-            alpha2(A, B, dx, dy, au, ev, alpha, om, c0, c1);
-            float2 w = mul2(alpha, px.T);
-            w = make_float2(px.done0 ? 0.0f : w.x, px.done1 ? 0.0f : w.y);
-            px.c0 = fma2(f2(C.x), w, px.c0);
-            px.c1 = fma2(f2(C.y), w, px.c1);
-            px.c2 = fma2(f2(C.z), w, px.c2);
-            px.dsum = fma2(f2(B.z), w, px.dsum);
-            px.osum = add2(px.osum, w);
-            const float2 Tn = mul2(px.T, om);
-            if (!px.done0) {
-                px.T.x = Tn.x;
-                if (early_stop && Tn.x < GS_EARLY_STOP_T) {
-                    px.done0 = true;
-                    px.cnt0 = b + j + 1;
-                }
-            }
-            if (!px.done1) {
-                px.T.y = Tn.y;
-                if (early_stop && Tn.y < GS_EARLY_STOP_T) {
-                    px.done1 = true;
-                    px.cnt1 = b + j + 1;
-                }
-            }
-        }
-        if (!px.done0) px.cnt0 = b + nb;
-        if (!px.done1) px.cnt1 = b + nb;
+        // branch-free per-pixel bookkeeping: a pixel that is still blending takes the entry
+        // (T and its count advance), and stops after the entry that drives T below 1e-4 --
+        // the reference's semantics with selects instead of divergent branches
+        if (early_stop) blend_chunk2<true>(px, st, b, nb);
+        else blend_chunk2<false>(px, st, b, nb);
     }
     return __syncthreads_count(px.done0 && px.done1) == FT;
 }
