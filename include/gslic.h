@@ -115,15 +115,17 @@ typedef struct gs_frame {
     /* per Gaussian */
     float *splat2d;          /* n x GS_SPLAT records (see GS_SPLAT) */
     float *cov2d;            /* n x 4: c00 c01 c11 radius */
-    int32_t *rect;           /* n x 4: tx0 tx1 ty0 ty1 (empty: tx1 < tx0) */
+    int32_t *rect;           /* n x 8: per-Gaussian 32-B binning record: tile rect tx0 tx1 ty0 ty1 (empty:
+                                tx1 < tx0), keep bits (uint64, first 64 candidate tiles) or the large
+                                footprint's bitmap base, kept (Gaussian, tile) pairs, pad */
     uint8_t *valid;          /* n: near-plane & det test (R/gaussians.py:190-208) */
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
     int64_t *g2d;            /* n x GS_G2D screen-space gradients, fixed-point accumulators (touched rows) */
     float *grad_rows;        /* n x GS_ROW parameter gradients in touched-list order */
     float *bias_corr;        /* n x 2 reciprocal Adam bias corrections 1/(1-b1^t), 1/(1-b2^t) (touched-list order) */
-    uint64_t *keep_bits;     /* n: exact-cull result for the first 64 candidate tiles (by id) */
-    int32_t *kept;           /* n: kept (Gaussian, tile) pairs per Gaussian (by id) */
+    uint64_t *keep_bits;     /* unused (in the rect records) */
+    int32_t *kept;           /* unused (in the rect records) */
     int32_t *big_list;       /* n: Gaussians with > GS_SMALL_CAND candidate tiles (warp-culled) */
     int32_t *big_slot;       /* n: huge slot (or -1) per big_list entry */
     int32_t *cull_queue;     /* cull_queue_cap x 2: (big index, tx << 16 | ty) left open by the band bounds */

@@ -72,15 +72,15 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.tiles_y = ty;
     f.splat2d = c.take<float>((int64_t)GS_SPLAT * nn);
     f.cov2d = c.take<float>(4 * nn);
-    f.rect = c.take<int32_t>(4 * nn);
+    f.rect = c.take<int32_t>(8 * nn);  // BinRec (common.cuh): rect, keep bits, kept
     f.valid = c.take<uint8_t>(nn);
     f.touched = c.take<uint8_t>(nn);
     f.touched_list = c.take<int32_t>(nn);
     f.g2d = c.take<int64_t>((int64_t)GS_G2D * nn);
     f.grad_rows = c.take<float>((int64_t)GS_ROW * nn);
     f.bias_corr = c.take<float>(2 * nn);
-    f.keep_bits = c.take<uint64_t>(nn);
-    f.kept = c.take<int32_t>(nn);
+    f.keep_bits = nullptr;  // in the BinRec records
+    f.kept = nullptr;
     f.big_list = c.take<int32_t>(nn);
     f.big_slot = c.take<int32_t>(nn);
     f.cull_queue_cap = nn > (1 << 20) ? nn : (1 << 20);

@@ -26,17 +26,17 @@ namespace gs {
 // (ty-major, then tx, R/rasterizer.py:113-122).
 template <typename F>
 __device__ __forceinline__ void for_kept_tiles(const gs_frame &f, int g, F fn) {
-    const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+    const int4 r = bin_rec(f)[g].rect;
     const int nx = r.y - r.x + 1;
     const int ncand = nx > 0 ? nx * (r.w - r.z + 1) : 0;
     if (ncand <= GS_SMALL_CAND) {  // cull bits from preprocess_kernel
-        const uint64_t bits = f.keep_bits[g];
+        const uint64_t bits = bin_rec(f)[g].bits;
         for (int c = 0; c < ncand; c++)
             if ((bits >> c) & 1ull) fn((r.z + c / nx) * f.tiles_x + r.x + c % nx);
         return;
     }
     // large footprint: bitmap of the big_* cull kernels, or the exact test again on overflow
-    const int64_t base = (int64_t)f.keep_bits[g];
+    const int64_t base = (int64_t)bin_rec(f)[g].bits;
     const SplatCull s = splat_cull(f.splat2d, g);
     for (int c = 0; c < ncand; c++) {
         const int tx = r.x + c % nx, ty = r.z + c / nx;
@@ -59,7 +59,7 @@ __global__ void nocull_kernel(gs_frame f) {
     bool v = false;
     if (i < f.n) {
         v = f.valid[i] != 0;
-        f.kept[i] = v ? f.tiles_x * f.tiles_y : 0;
+        bin_rec(f)[i].kept = v ? f.tiles_x * f.tiles_y : 0;
         f.touched[i] = v;
     }
     warp_append(v, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
 #pragma unroll
         for (int q = 0; q < HS_GROUPS; q++) rank += s_part[q][k];
         const int g = (int)(uint32_t)mine;
-        reinterpret_cast<int4 *>(f.huge + HREC * rank)[0] = make_int4(g, (int)(mine >> 32), -f.kept[g] - 1, 0);
+        reinterpret_cast<int4 *>(f.huge + HREC * rank)[0] = make_int4(g, (int)(mine >> 32), -bin_rec(f)[g].kept - 1, 0);
         f.huge[HIDS + rank] = g;
         reinterpret_cast<uint64_t *>(f.huge + HKEYS)[rank] = mine;
     }
@@ -271,13 +271,13 @@ __global__ void __launch_bounds__(256) bucket_fill_kernel(gs_frame f, int cull) 
     }
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += (int64_t)gridDim.x * blockDim.x) {
         const int g = f.touched_list[k];
-        if (f.kept[g] <= 0) continue;
+        if (bin_rec(f)[g].kept <= 0) continue;
         const uint64_t key = depth_key(f, g);
-        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int4 r = bin_rec(f)[g].rect;
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
         if (ncand <= GS_SMALL_CAND) {
             // all slot reservations in flight before the first store
-            const uint64_t bits = f.keep_bits[g];
+            const uint64_t bits = bin_rec(f)[g].bits;
             int pos[GS_SMALL_CAND];
 #pragma unroll
             for (int c = 0; c < GS_SMALL_CAND; c++)

@@ -365,6 +365,24 @@ __device__ __forceinline__ float splat_depth(const float *splat2d, int64_t g) { 
 
 // stores a record: A = (mx, my, a, beta), B = (gamma, opacity, depth, qcut), C = (r, g, b,
 // 1 - opacity) (colour written separately when c == nullptr), D = (b, c, 0, 0)
+// Per-Gaussian binning record: one aligned 32-B sector (the preprocess writes it whole, so no
+// partial-sector write reaches HBM): tile rectangle (x0, x1, y0, y1), the keep bits of a small
+// rectangle (candidate order) or the bitmap base of a large one, and the kept-tile count (< 0:
+// -(1 + huge slot); the large-footprint cull's countdown while it runs).  gs_frame.rect points
+// at the array (gs_frame.keep_bits / kept are unused).
+struct __align__(32) BinRec {
+    int4 rect;
+    unsigned long long bits;
+    int kept;
+    int pad_;
+};
+__device__ __forceinline__ BinRec *bin_rec(const gs_frame &f) { return reinterpret_cast<BinRec *>(f.rect); }
+__device__ __forceinline__ void bin_store(const gs_frame &f, int64_t i, int4 rect, unsigned long long bits, int kept) {
+    int4 *p = reinterpret_cast<int4 *>(bin_rec(f) + i);
+    p[0] = rect;
+    p[1] = make_int4((int)(uint32_t)bits, (int)(uint32_t)(bits >> 32), kept, 0);
+}
+
 __device__ __forceinline__ void splat_store(float *splat2d, int64_t g, float mx, float my, double ca, double cb,
                                             double cc, float op, float z, float qcut) {
     float4 *s = reinterpret_cast<float4 *>(splat2d) + GS_SPLAT / 4 * g;

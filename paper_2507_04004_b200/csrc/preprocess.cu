@@ -200,9 +200,8 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
                     s2[2] = make_float4(0.f, 0.f, 0.f, 0.f);
                     s2[3] = make_float4(0.f, 0.f, 0.f, 0.f);
                     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(0.f, 0.f, 0.f, -1.f);
-                    reinterpret_cast<int4 *>(f.rect)[i] = make_int4(0, -1, 0, -1);
+                    bin_store(f, i, make_int4(0, -1, 0, -1), 0ull, 0);
                     f.valid[i] = 0;
-                    f.kept[i] = 0;
                     f.touched[i] = 0;
                 }
             } else {
@@ -247,9 +246,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
             // culled); the reference-shaped API writes every record (out.ctx["proj"], R/gaussians.py:180-215)
             if (need) {
                 splat_store(f.splat2d, i, pr.mx, pr.my, pca, pcb, pcc, op, pr.mu[2], qcut);
-                reinterpret_cast<int4 *>(f.rect)[i] = rect;
-                f.kept[i] = kept;
-                f.keep_bits[i] = bits;
+                bin_store(f, i, rect, bits, kept);
             }
             if (!LAZY_SH) {
                 // (the colour, s2[2].xyz, follows one iteration later; 1 - opacity = sigmoid(-logit)
@@ -474,7 +471,7 @@ __device__ __forceinline__ int big_publish(const gs_frame &f, int g, int slot, c
     const bool t = kept > 0;
     const uint64_t key = big_key(f, g);
     if (lane == 0) {
-        f.kept[g] = (slot >= 0 && t) ? -(1 + slot) : kept;  // kept < 0 encodes the huge slot
+        bin_rec(f)[g].kept = (slot >= 0 && t) ? -(1 + slot) : kept;  // kept < 0 encodes the huge slot
         f.touched[g] = t;
         if (t && lists) {
             // kept screen-covering Gaussians: entry count and a staging slot for the binning's
@@ -538,7 +535,7 @@ __global__ void __launch_bounds__(BC_WARPS * 32, 2) big_bands_kernel(gs_frame f,
         if (lane == 0) s_kept[warp] = 0;
         if (b < nb) {
             const int g = f.big_list[b];
-            const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+            const int4 r = bin_rec(f)[g].rect;
             const SplatCull s = splat_cull(f.splat2d, g);
             const int nx = r.y - r.x + 1, nbands = r.w - r.z + 1, ncand = nx * nbands;
             // huge slot = the Gaussian's big-list index (no reservation atomic; slots of the others
@@ -625,8 +622,8 @@ __global__ void __launch_bounds__(BC_WARPS * 32, 2) big_bands_kernel(gs_frame f,
                 for (int w = lane; w < nwords; w += 32) row[w] = bm[w];
             if (lane == 0) {
                 f.big_slot[b] = slot;
-                f.keep_bits[g] = (uint64_t)base;  // bitmap base for large footprints (-1: none)
-                if (queued) f.kept[g] = queued;  // countdown of big_exact_kernel
+                bin_rec(f)[g].bits = (uint64_t)base;  // bitmap base for large footprints (-1: none)
+                if (queued) bin_rec(f)[g].kept = queued;  // countdown of big_exact_kernel
             }
             if (!queued) {
                 const int kept = big_publish<false>(f, g, slot, bm, nwords, r, false);
@@ -685,10 +682,10 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
             b = e.x;
             g = f.big_list[b];
             slot = f.big_slot[b];
-            r = reinterpret_cast<const int4 *>(f.rect)[g];
+            r = bin_rec(f)[g].rect;
             s = splat_cull(f.splat2d, g);
             const int tx = (int)((uint32_t)e.y >> 16), ty = e.y & 0xffff;
-            row = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : f.big_bits + (int64_t)f.keep_bits[g];
+            row = slot >= 0 ? f.huge_mask_t + (int64_t)slot * tw : f.big_bits + (int64_t)bin_rec(f)[g].bits;
             bit = slot >= 0 ? ty * f.tiles_x + tx : (ty - r.z) * (r.y - r.x + 1) + (tx - r.x);
             x0 = tx * GS_TILE;
             y0 = ty * GS_TILE;
@@ -709,7 +706,7 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
         // Gaussian's last queued tile publishes it (with its warp)
         const unsigned same_g = __match_any_sync(0xffffffffu, i < nq ? g : -1);
         bool last = false;
-        if (i < nq && lane == __ffs(same_g) - 1) last = atomicSub(&f.kept[g], __popc(same_g)) == __popc(same_g);
+        if (i < nq && lane == __ffs(same_g) - 1) last = atomicSub(&bin_rec(f)[g].kept, __popc(same_g)) == __popc(same_g);
         unsigned fin = __ballot_sync(0xffffffffu, last);
         if (fin) __threadfence();
         while (fin) {  // the warp publishes each Gaussian whose last queued tile one of its lanes retired
@@ -809,10 +806,8 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
     reinterpret_cast<float4 *>(f.splat2d)[GS_SPLAT / 4 * i + 2] = colors ? make_float4(colors[3 * i], colors[3 * i + 1], colors[3 * i + 2], 1.0f - o)
                    : make_float4(0.f, 0.f, 0.f, 1.0f - o);
     reinterpret_cast<float4 *>(f.cov2d)[i] = make_float4(c00, c01, c11, radius);
-    reinterpret_cast<int4 *>(f.rect)[i] = rect;
+    bin_store(f, i, rect, bits, kept);
     f.valid[i] = v;
-    f.kept[i] = kept;
-    f.keep_bits[i] = bits;
     f.touched[i] = kept > 0;
 }
 
@@ -821,8 +816,8 @@ __global__ void pack_kernel(gs_frame f, const float *__restrict__ mean2d, const 
 __global__ void touched_list_kernel(gs_frame f) {
     pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = i < f.n ? f.kept[i] : 0;
-    if (k < 0) f.kept[i] = 0;
+    const int k = i < f.n ? bin_rec(f)[i].kept : 0;
+    if (k < 0) bin_rec(f)[i].kept = 0;
     warp_append(k > 0, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
     warp_append(k < 0, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
 }

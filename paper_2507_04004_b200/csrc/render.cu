@@ -325,17 +325,17 @@ __global__ void __launch_bounds__(256) lazy_fill_kernel(gs_frame f) {
     const int32_t *flag = ts_flag(f);
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nt; k += (int64_t)gridDim.x * blockDim.x) {
         const int g = f.touched_list[k];
-        if (f.kept[g] <= 0) continue;
+        if (bin_rec(f)[g].kept <= 0) continue;
         const uint64_t key = depth_key(f, g);
-        const int4 r = reinterpret_cast<const int4 *>(f.rect)[g];
+        const int4 r = bin_rec(f)[g].rect;
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
-        const int64_t base = (int64_t)f.keep_bits[g];
+        const int64_t base = (int64_t)bin_rec(f)[g].bits;
         const SplatCull s = splat_cull(f.splat2d, g);
         for (int c = 0; c < ncand; c++) {
             const int tx = r.x + c % nx, ty = r.z + c / nx, t = ty * f.tiles_x + tx;
             bool keep;
             if (ncand <= GS_SMALL_CAND) {
-                keep = (f.keep_bits[g] >> c) & 1ull;
+                keep = (bin_rec(f)[g].bits >> c) & 1ull;
             } else if (base >= 0) {
                 keep = (f.big_bits[base + (c >> 5)] >> (c & 31)) & 1u;
             } else {
