@@ -525,11 +525,19 @@ __device__ __forceinline__ void bwd_step2(BwdPair &p, bool act0, bool act1, cons
 // shared-memory slot, the warp sums are added in warp order, and the tile partial goes to the
 // Gaussian's row through fixed-point integer atomics (fx_atomic_add) -- no floating-point sum
 // depends on scheduling order.
-constexpr int BT = RT / 4;          // backward threads per tile (four pixels each)
+#ifndef BWD_PAIRS
+#define BWD_PAIRS 2
+#endif
+constexpr int NP = BWD_PAIRS;       // pixel pairs per backward thread
+constexpr int BT = RT / (2 * NP);   // backward threads per tile
+constexpr int RG = BT / 16;         // row groups: pair h of a thread is rows row + RG h, + RG h + 8
 constexpr int BW = BT / 32;         // warps per backward CTA
 constexpr int BST = BT;             // entries staged per round (one per thread)
 
-__global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_depth_grads) {
+#ifndef BWD_MINB
+#define BWD_MINB 1
+#endif
+__global__ void __launch_bounds__(BT, BWD_MINB) render_bwd_kernel(gs_frame f, int clear_depth_grads) {
     pdl_wait();
     __shared__ float4 s_a[BST];
     __shared__ float4 s_b[BST];
@@ -541,11 +549,11 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
     const int tile = blockIdx.x;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
     const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
-    const int col = threadIdx.x & 15, row = threadIdx.x >> 4;  // rows row + 4 k, k < 4
+    const int col = threadIdx.x & 15, row = threadIdx.x >> 4;  // rows row + RG k, k < 2 NP
     if (clear_depth_grads && stop == start) {  // (GS_BWD_CLEAR_DEPTH_GRADS) an empty tile's pixels
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int x = tx * GS_TILE + col, y = ty * GS_TILE + row + 4 * k;
+        for (int k = 0; k < 2 * NP; k++) {
+            const int x = tx * GS_TILE + col, y = ty * GS_TILE + row + RG * k;
             if (x < f.width && y < f.height) {
                 const int64_t q = (int64_t)y * f.width + x;
                 if (f.g_depth[q] != 0.0f) f.g_depth[q] = 0.0f;
@@ -573,15 +581,15 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         // lazy, unflagged: the blend ended within the leading screen-covering Gaussians
         return lazy ? hid[tile_huge_select(p, s_words, s_wpre, nw)] : f.entry_splat[start + p];
     };
-    BwdPair px[2];  // pair h: rows row + 4 h and row + 4 h + 8
+    BwdPair px[NP];  // pair h: rows row + RG h and row + RG h + 8
     if (threadIdx.x == 0) s_max = 0;
     __syncthreads();
     {
         const int x = tx * GS_TILE + col;
         int mx = 0;
 #pragma unroll
-        for (int h = 0; h < 2; h++) {
-            const int y0 = ty * GS_TILE + row + 4 * h;
+        for (int h = 0; h < NP; h++) {
+            const int y0 = ty * GS_TILE + row + RG * h;
             px[h].fx = (float)x;
             px[h].fy = make_float2((float)y0, (float)(y0 + GS_TILE / 2));
             float T[2] = {1.0f, 1.0f}, gc[2][3] = {}, gd[2] = {}, go[2] = {};
@@ -635,16 +643,22 @@ __global__ void __launch_bounds__(BT) render_bwd_kernel(gs_frame f, int clear_de
         __syncthreads();
         for (int j = nb - 1; j >= 0; j--) {
             const int le = b0 + j - start;
-            const bool a00 = le < px[0].cnt0, a01 = le < px[0].cnt1, a10 = le < px[1].cnt0, a11 = le < px[1].cnt1;
+            bool act[NP][2], any = false;
+#pragma unroll
+            for (int h = 0; h < NP; h++) {
+                act[h][0] = le < px[h].cnt0;
+                act[h][1] = le < px[h].cnt1;
+                any = any || act[h][0] || act[h][1];
+            }
             double sg = 0.0;
             float sc = 0.0f;
-            if (__any_sync(0xffffffffu, a00 || a01 || a10 || a11)) {
+            if (__any_sync(0xffffffffu, any)) {
                 const float4 A = s_a[j], B = s_b[j], C = s_c[j];
                 float2 v[10];
 #pragma unroll
                 for (int k = 0; k < 10; k++) v[k] = f2(0.0f);
-                bwd_step2(px[0], a00, a01, A, B, C, v);
-                bwd_step2(px[1], a10, a11, A, B, C, v);
+#pragma unroll
+                for (int h = 0; h < NP; h++) bwd_step2(px[h], act[h][0], act[h][1], A, B, C, v);
                 float vg[6], vc[4];
 #pragma unroll
                 for (int k = 0; k < 6; k++) vg[k] = v[k].x + v[k].y;

@@ -6,7 +6,7 @@ import json
 import os
 import sys
 
-PHASE = {"preprocess": ("preprocess_kernel", "big_cull"),
+PHASE = {"preprocess": ("preprocess_kernel", "big_bands", "big_exact", "big_cull"),
          "bin": ("huge_sort", "huge_transpose", "tile_scan", "bucket_fill", "tile_sort_merge"),
          "render_fwd": ("render_fwd", "lazy_fill", "tile_finish"),
          "loss": ("loss_tables", "ssim_fwd", "ssim_bwd", "depth_loss", "loss_finalize"),
