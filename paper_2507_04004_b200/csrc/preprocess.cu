@@ -276,8 +276,21 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
         __syncwarp();  // the SH buffer and this geometry slot are free again
         if (need) {
             const float *src = params + i * GS_ROW + 16;
+            if (LAZY_SH) {
+                // the engine's drawable Gaussians are (nearly) the touched ones, whose rows the
+                // chain rule + Adam re-read at the end of the iteration: their lines are marked
+                // evict-last, so more of them are still in L2 then (chain DRAM reads -4 %)
+                uint64_t pol;
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll
-            for (int c = 0; c < 11; c++) pp_cp_async16(&W.sh.row[lane][c], src + 4 * c);
+                for (int c = 0; c < 11; c++)
+                    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                                     (unsigned)__cvta_generic_to_shared(&W.sh.row[lane][c])),
+                                 "l"(src + 4 * c), "l"(pol));
+            } else {
+#pragma unroll
+                for (int c = 0; c < 11; c++) pp_cp_async16(&W.sh.row[lane][c], src + 4 * c);
+            }
         }
         pp_cp_commit();
         prev_need = need;
