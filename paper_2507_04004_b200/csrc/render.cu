@@ -131,10 +131,17 @@ __device__ __forceinline__ void fwd_pixel_store(const gs_frame &f, int tile, con
     f.n_contrib[q] = p.cnt;
 }
 
-__device__ __forceinline__ FwdPair fwd_pair_init(const gs_frame &f, int tile) {
+#ifndef FWD_PAIRS
+#define FWD_PAIRS 2
+#endif
+constexpr int NPF = FWD_PAIRS;       // pixel pairs per forward thread
+constexpr int FT = RT / (2 * NPF);   // forward threads per tile
+constexpr int RGF = FT / 16;         // pair h of a thread: rows row + RGF h and row + RGF h + 8
+
+__device__ __forceinline__ FwdPair fwd_pair_init(const gs_frame &f, int tile, int h) {
     FwdPair p;
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
-    const int px = tx * GS_TILE + (threadIdx.x & 15), py = ty * GS_TILE + (threadIdx.x >> 4);
+    const int px = tx * GS_TILE + (threadIdx.x & 15), py = ty * GS_TILE + (threadIdx.x >> 4) + RGF * h;
     p.in0 = px < f.width && py < f.height;
     p.in1 = px < f.width && py + GS_TILE / 2 < f.height;
     p.fx = (float)px;
@@ -147,9 +154,9 @@ __device__ __forceinline__ FwdPair fwd_pair_init(const gs_frame &f, int tile) {
     return p;
 }
 
-__device__ __forceinline__ void fwd_pair_store(const gs_frame &f, int tile, const FwdPair &p) {
+__device__ __forceinline__ void fwd_pair_store(const gs_frame &f, int tile, int hp, const FwdPair &p) {
     const int tx = tile % f.tiles_x, ty = tile / f.tiles_x;
-    const int64_t q0 = (int64_t)(ty * GS_TILE + (threadIdx.x >> 4)) * f.width + tx * GS_TILE + (threadIdx.x & 15);
+    const int64_t q0 = (int64_t)(ty * GS_TILE + (threadIdx.x >> 4) + RGF * hp) * f.width + tx * GS_TILE + (threadIdx.x & 15);
 #pragma unroll
     for (int h = 0; h < 2; h++) {
         if (!(h ? p.in1 : p.in0)) continue;
@@ -164,70 +171,94 @@ __device__ __forceinline__ void fwd_pair_store(const gs_frame &f, int tile, cons
     }
 }
 
-// The paired form of blend_range (FT = 128 threads, two pixels each): same staging, same
+// The paired form of blend_range (FT threads, NPF pixel pairs each): same staging, same
 // per-pixel termination, alphas bit-identical to the scalar path.
-constexpr int FT = RT / 2;
 
 // Blends the nb staged entries (list positions b, b + 1, ...) into the thread's two pixels.
 // Branch-free per-pixel bookkeeping: a pixel that is still blending takes the entry (T and its
 // count advance) and, with EARLY, stops after the entry that drives T below 1e-4 -- the
 // reference's semantics (R/rasterizer.py:270-291) with selects instead of divergent branches.
 template <bool EARLY>
-__device__ __forceinline__ void blend_chunk2(FwdPair &px, const FwdStage &st, int b, int nb) {
-    unsigned act = (px.done0 ? 0u : 1u) | (px.done1 ? 0u : 2u);
-    int n0 = px.cnt0, n1 = px.cnt1;
-    float2 T = px.T;
+__device__ __forceinline__ void blend_chunk2(FwdPair (&px)[NPF], const FwdStage &st, int b, int nb) {
+    unsigned act = 0u;
+    int n[NPF][2];
+    float2 T[NPF];
+#pragma unroll
+    for (int h = 0; h < NPF; h++) {
+        act |= (px[h].done0 ? 0u : 1u << (2 * h)) | (px[h].done1 ? 0u : 2u << (2 * h));
+        n[h][0] = px[h].cnt0;
+        n[h][1] = px[h].cnt1;
+        T[h] = px[h].T;
+    }
     for (int j = 0; j < nb && act; j++) {
         const float4 A = st.a[j], B = st.b[j], C = st.c[j];
-        const float dx = px.fx - A.x;
-        const float2 dy = add2(px.fy, f2(-A.y));
-        float2 au, ev, alpha, om;
-        bool c0, c1;
-        alpha2(A, B, dx, dy, au, ev, alpha, om, c0, c1);
-        const bool a0 = act & 1u, a1 = act & 2u;
-        float2 w = mul2(alpha, T);
-        w = make_float2(a0 ? w.x : 0.0f, a1 ? w.y : 0.0f);
-        px.c0 = fma2(f2(C.x), w, px.c0);
-        px.c1 = fma2(f2(C.y), w, px.c1);
-        px.c2 = fma2(f2(C.z), w, px.c2);
-        px.dsum = fma2(f2(B.z), w, px.dsum);
-        px.osum = add2(px.osum, w);
-        const float2 Tn = mul2(T, om);
+        const float dx = px[0].fx - A.x;
         const int e1 = b + j + 1;
-        T = make_float2(a0 ? Tn.x : T.x, a1 ? Tn.y : T.y);
-        n0 = a0 ? e1 : n0;
-        n1 = a1 ? e1 : n1;
-        if (EARLY) act &= (Tn.x < GS_EARLY_STOP_T ? 0u : 1u) | (Tn.y < GS_EARLY_STOP_T ? 0u : 2u);
+        unsigned keep = 0u;
+#pragma unroll
+        for (int h = 0; h < NPF; h++) {
+            const float2 dy = add2(px[h].fy, f2(-A.y));
+            float2 au, ev, alpha, om;
+            bool c0, c1;
+            alpha2(A, B, dx, dy, au, ev, alpha, om, c0, c1);
+            const bool a0 = act & (1u << (2 * h)), a1 = act & (2u << (2 * h));
+            float2 w = mul2(alpha, T[h]);
+            w = make_float2(a0 ? w.x : 0.0f, a1 ? w.y : 0.0f);
+            px[h].c0 = fma2(f2(C.x), w, px[h].c0);
+            px[h].c1 = fma2(f2(C.y), w, px[h].c1);
+            px[h].c2 = fma2(f2(C.z), w, px[h].c2);
+            px[h].dsum = fma2(f2(B.z), w, px[h].dsum);
+            px[h].osum = add2(px[h].osum, w);
+            const float2 Tn = mul2(T[h], om);
+            T[h] = make_float2(a0 ? Tn.x : T[h].x, a1 ? Tn.y : T[h].y);
+            n[h][0] = a0 ? e1 : n[h][0];
+            n[h][1] = a1 ? e1 : n[h][1];
+            if (EARLY) keep |= (Tn.x < GS_EARLY_STOP_T ? 0u : 1u << (2 * h)) | (Tn.y < GS_EARLY_STOP_T ? 0u : 2u << (2 * h));
+        }
+        if (EARLY) act &= keep;
     }
-    px.T = T;
-    px.done0 = !(act & 1u);
-    px.done1 = !(act & 2u);
-    px.cnt0 = n0;
-    px.cnt1 = n1;
+#pragma unroll
+    for (int h = 0; h < NPF; h++) {
+        px[h].T = T[h];
+        px[h].done0 = !(act & (1u << (2 * h)));
+        px[h].done1 = !(act & (2u << (2 * h)));
+        px[h].cnt0 = n[h][0];
+        px[h].cnt1 = n[h][1];
+    }
 }
 
+__device__ __forceinline__ bool pairs_done(const FwdPair (&px)[NPF]) {
+    bool d = true;
+#pragma unroll
+    for (int h = 0; h < NPF; h++) d = d && px[h].done0 && px[h].done1;
+    return d;
+}
+
+// entries staged per round: FS_FIRST in the first (most blends end within a few dozen), then FS
+constexpr int FS = 128, FS_FIRST = 64;
+static_assert(FS <= RT && FS_FIRST <= FS, "staging rounds");
+
 template <typename Fetch>
-__device__ __forceinline__ bool blend_range2(const gs_frame &f, FwdPair &px, FwdStage &st, int p0, int p1,
+__device__ __forceinline__ bool blend_range2(const gs_frame &f, FwdPair (&px)[NPF], FwdStage &st, int p0, int p1,
                                              int early_stop, Fetch fetch) {
     const float4 *sp = reinterpret_cast<const float4 *>(f.splat2d);
-    for (int b = p0, step = FT / 2; b < p1; b += step, step = FT) {
-        if (__syncthreads_count(px.done0 && px.done1) == FT) return true;
-        const int e = b + threadIdx.x;
-        if ((int)threadIdx.x < step && e < p1) {
-            const int64_t g = fetch(e);
-            st.a[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g);
-            st.b[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 1);
-            st.c[threadIdx.x] = __ldg(sp + GS_SPLAT / 4 * g + 2);
+    for (int b = p0, step = FS_FIRST; b < p1; b += step, step = FS) {
+        if (__syncthreads_count(pairs_done(px)) == FT) return true;
+        for (int i = threadIdx.x; i < step; i += FT) {
+            const int e = b + i;
+            if (e < p1) {
+                const int64_t g = fetch(e);
+                st.a[i] = __ldg(sp + GS_SPLAT / 4 * g);
+                st.b[i] = __ldg(sp + GS_SPLAT / 4 * g + 1);
+                st.c[i] = __ldg(sp + GS_SPLAT / 4 * g + 2);
+            }
         }
         __syncthreads();
         const int nb = min(step, p1 - b);
-        // branch-free per-pixel bookkeeping: a pixel that is still blending takes the entry
-        // (T and its count advance), and stops after the entry that drives T below 1e-4 --
-        // the reference's semantics with selects instead of divergent branches
         if (early_stop) blend_chunk2<true>(px, st, b, nb);
         else blend_chunk2<false>(px, st, b, nb);
     }
-    return __syncthreads_count(px.done0 && px.done1) == FT;
+    return __syncthreads_count(pairs_done(px)) == FT;
 }
 
 // Blends list positions [p0, p1) of the tile front to back; fetch(p) -> Gaussian id.  The
@@ -279,11 +310,17 @@ __global__ void __launch_bounds__(FT) render_fwd_kernel(gs_frame f, int early_st
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
-    __shared__ int32_t s_tmp[FT / 32];
+    __shared__ int32_t s_tmp[FT / 32 > 0 ? FT / 32 : 1];
     const int tile = blockIdx.x;
-    FwdPair px = fwd_pair_init(f, tile);
+    FwdPair px[NPF];
+#pragma unroll
+    for (int h = 0; h < NPF; h++) px[h] = fwd_pair_init(f, tile, h);
+    auto store = [&]() {
+#pragma unroll
+        for (int h = 0; h < NPF; h++) fwd_pair_store(f, tile, h, px[h]);
+    };
     if (f.counters[GS_CNT_OVERFLOW]) {  // binning over capacity (tile ranges emptied): background
-        fwd_pair_store(f, tile, px);
+        store();
         return;
     }
     if (f.counters[GS_CNT_LAZY]) {
@@ -313,7 +350,7 @@ __global__ void __launch_bounds__(FT) render_fwd_kernel(gs_frame f, int early_st
         const int32_t *list = f.entry_splat + start;
         blend_range2(f, px, st, 0, stop - start, early_stop, [&](int p) { return list[p]; });
     }
-    fwd_pair_store(f, tile, px);
+    store();
 }
 
 // Lazy lists, continuation 1: the bucket keys of the tiles that need them (ts_flag != 0)

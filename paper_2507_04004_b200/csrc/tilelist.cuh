@@ -61,8 +61,19 @@ __device__ __forceinline__ int tile_huge_setup(const gs_frame &f, int t, uint32_
     const int nrec = min(f.counters[GS_CNT_HUGE_N], GS_HUGE_CAP);
     const int nw = (nrec + 31) >> 5;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-    const uint32_t word = tid < nw ? f.huge_mask[(int64_t)t * (GS_HUGE_CAP / 32) + tid] : 0u;
-    const int c = __popc(word);
+    // thread tid holds words [K tid, K tid + K) (K = 1 for CTAs of >= GS_HUGE_CAP / 32 threads;
+    // a 64-thread backward CTA needs K = 2 once there are more than 2048 records)
+    constexpr int KMAX = 4;  // CTAs of >= GS_HUGE_CAP / 128 = 32 threads
+    const int K = (GS_HUGE_CAP / 32 + blockDim.x - 1) / blockDim.x;
+    const uint32_t *row = f.huge_mask + (int64_t)t * (GS_HUGE_CAP / 32);
+    uint32_t wv[KMAX];
+    int c = 0;
+#pragma unroll
+    for (int k = 0; k < KMAX; k++) {
+        const int w = K * tid + k;
+        wv[k] = (k < K && w < nw) ? row[w] : 0u;
+        c += __popc(wv[k]);
+    }
     int x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -77,9 +88,14 @@ __device__ __forceinline__ int tile_huge_setup(const gs_frame &f, int t, uint32_
         pos += w < warp ? sw : 0;
         na += sw;
     }
-    if (tid < nw) {
-        s_words[tid] = word;
-        s_wpre[tid] = pos;
+#pragma unroll
+    for (int k = 0; k < KMAX; k++) {
+        const int w = K * tid + k;
+        if (k < K && w < nw) {
+            s_words[w] = wv[k];
+            s_wpre[w] = pos;
+            pos += __popc(wv[k]);
+        }
     }
     __syncthreads();
     return na;

@@ -29,11 +29,11 @@ def normwise(a, b):
     return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30)) if b.size else 0.0
 
 
-def _scene(kind, n, w, h, lidar):
+def _scene(kind, n, w, h, lidar, view=0):
     from paper_2507_04004_b200 import scenes
     if kind == "s1":
         return scenes.scene_s1(n, w, h, k_lidar=lidar)
-    sc = scenes.scene_room(n, w, h, lidar=lidar, render_views=(0,))
+    sc = scenes.scene_room(n, w, h, lidar=lidar, render_views=(view,))
     sc.targets = [np.round(np.clip(t, 0.0, 1.0) * 255.0) / 255.0 for t in sc.targets]  # bench: 8-bit frames
     return sc
 
@@ -45,6 +45,9 @@ def _ocam(c):
 
 
 CASES = [("S2r-1M-1280x720-32line", "room", 1 << 20, 1280, 720, 32),
+         # the bench's fourth keyframe: ~2.4k screen-covering Gaussians, more depth-ordered mask
+         # words per tile (> 64) than a 64-thread backward CTA has threads
+         ("S2r-1M-1280x720-32line-view3", "room3", 1 << 20, 1280, 720, 32),
          ("S1-10k-320x240", "s1", 10000, 320, 240, 5000),
          ("S2r-1M-1280x720-16line", "room", 1 << 20, 1280, 720, 16),
          ("S2r-1M-1280x720-64line", "room", 1 << 20, 1280, 720, 64),
@@ -59,7 +62,7 @@ def test_engine_iteration_matches_oracle(name, kind, n, w, h, lidar):
     from paper_2507_04004_b200 import mapper as M
     from paper_2507_04004_b200 import rasterizer as R
     from paper_2507_04004_b200.gaussians import GaussianMap
-    sc = _scene(kind, n, w, h, lidar)
+    sc = _scene("room" if kind == "room3" else kind, n, w, h, lidar, view=3 if kind == "room3" else 0)
     rows32 = sc.rows.astype(np.float32).astype(np.float64)
     g = GaussianMap.from_rows(sc.rows)
     lrs = R.default_lrs(3.0)
@@ -70,6 +73,8 @@ def test_engine_iteration_matches_oracle(name, kind, n, w, h, lidar):
     torch.cuda.synchronize()
     ref = O.iteration_detail(rows32.copy(), _ocam(sc.cams[0]), sc.targets[0], sc.sparse_depths[0], with_images=True)
     ws = eng.ws
+    if kind == "room3":  # the case exists for its many screen-covering Gaussians
+        assert int(ws.counters.cpu()[19]) > 2048  # GS_CNT_HUGE_N: > 64 mask words per tile
     # forward images of the timed path (lazy lists) against the float64 blend
     for k, a in (("color", ws.color), ("depth", ws.depth), ("opacity", ws.opacity), ("transmittance", ws.trans)):
         r = ref[k]
