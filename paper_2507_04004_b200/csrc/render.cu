@@ -534,19 +534,22 @@ __device__ __forceinline__ void bwd_step2(BwdPair &p, bool act0, bool act1, cons
     suf = fma2(p.S1, p.gc1, suf);
     suf = fma2(p.S2, p.gc2, suf);
     suf = fma2(p.Sd, p.gd, suf);
-    const float2 dl = fma2(Tb, own, mul2(f2(-1.0f), mul2(suf, rom)));
+    const float2 sr = mul2(suf, rom);
+    const float2 dl = fma2(Tb, own, make_float2(-sr.x, -sr.y));
     // no alpha-chain gradient on the 0.99 clamp (R/rasterizer.py:399-404), none from a finished pixel
     const bool g0 = act0 && !c0, g1 = act1 && !c1;
-    float2 gq = mul2(dl, mul2(f2(-0.5f), alpha));
-    gq = make_float2(g0 ? gq.x : 0.0f, g1 ? gq.y : 0.0f);
-    float2 de = mul2(dl, e);  // d alpha / d opacity = e
-    de = make_float2(g0 ? de.x : 0.0f, g1 ? de.y : 0.0f);
+    // ga = dl alpha; the reference's gq = -dl alpha / 2 (R/rasterizer.py:405-410) is ga / -2, and
+    // gq (-2 a u) = ga a u: the power-of-two scalings are exact, so every sum is bit-identical
+    const float2 dlm = make_float2(g0 ? dl.x : 0.0f, g1 ? dl.y : 0.0f);
+    const float2 ga = mul2(dlm, alpha);
+    const float2 gq = mul2(ga, f2(-0.5f));
+    const float2 de = mul2(dlm, e);  // d alpha / d opacity = e
     v[5] = add2(v[5], de);
     v[2] = fma2(gq, f2(dx * dx), v[2]);
     v[3] = fma2(gq, mul2(f2(2.0f * dx), dy), v[3]);
     v[4] = fma2(mul2(gq, dy), dy, v[4]);
-    v[0] = fma2(gq, mul2(f2(-2.0f), au), v[0]);
-    v[1] = fma2(gq, mul2(f2(-2.0f), fma2(f2(beta), au, mul2(f2(gamma), dy))), v[1]);
+    v[0] = fma2(ga, au, v[0]);
+    v[1] = fma2(ga, fma2(f2(beta), au, mul2(f2(gamma), dy)), v[1]);
     p.S0 = fma2(f2(C.x), w, p.S0);
     p.S1 = fma2(f2(C.y), w, p.S1);
     p.S2 = fma2(f2(C.z), w, p.S2);
