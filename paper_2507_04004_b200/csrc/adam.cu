@@ -204,6 +204,28 @@ __device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, 
     return p - (lr * (m * rbc1)) * fast_rcp(den);
 }
 
+// Two Adam elements with paired fp32 instructions (FFMA2 / FMUL2 / FADD2): the operations and
+// their order of adam_one as compiled (m = fma(0.9, m, 0.1 g), v = fma(0.999, v, (0.001 g) g),
+// p - (lr (m rbc1)) rcp(den) as one fused multiply-add), so the results are the same bits.
+__device__ __forceinline__ void adam_two(float p0, float p1, float &m0, float &m1, float &v0, float &v1, float g0,
+                                         float g1, float lr0, float lr1, float rbc1, float rbc2, float &o0,
+                                         float &o1) {
+    const float2 g = make_float2(g0, g1);
+    const float2 m = __ffma2_rn(make_float2(0.9f, 0.9f), make_float2(m0, m1), __fmul2_rn(g, make_float2(0.1f, 0.1f)));
+    const float2 gg = __fmul2_rn(__fmul2_rn(g, make_float2(0.001f, 0.001f)), g);
+    const float2 v = __ffma2_rn(make_float2(0.999f, 0.999f), make_float2(v0, v1), gg);
+    const float2 vr = __fmul2_rn(v, make_float2(rbc2, rbc2));
+    const float2 den = __fadd2_rn(make_float2(fast_sqrt(vr.x), fast_sqrt(vr.y)), make_float2(1e-15f, 1e-15f));
+    const float2 nstep = __fmul2_rn(make_float2(-lr0, -lr1), __fmul2_rn(m, make_float2(rbc1, rbc1)));
+    const float2 o = __ffma2_rn(nstep, make_float2(fast_rcp(den.x), fast_rcp(den.y)), make_float2(p0, p1));
+    m0 = m.x;
+    m1 = m.y;
+    v0 = v.x;
+    v1 = v.y;
+    o0 = o.x;
+    o1 = o.y;
+}
+
 // mode 0: fused Adam on params/m/v/t.  mode 1: grads[row] += G, touched_accum[row] = 1.
 // mode 2: compact gradient rows + bias corrections for adam_list_kernel.  mode 3: nothing but the
 // pose gradient (tracking).  POSE: pose6 (FP64, 6) += the pose gradient of the touched Gaussians.
@@ -334,10 +356,16 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
                 const float bc1 = sbc[warp][r][0], bc2 = sbc[warp][r][1];
                 const float4 lr = __ldg(reinterpret_cast<const float4 *>(lr_cols) + c4);
                 float4 m4 = M4[q], v4 = V4[q], p4;
+#ifdef CA_SCALAR_ADAM
                 p4.x = adam_one(P[q].x, m4.x, v4.x, G[0], lr.x, bc1, bc2);
                 p4.y = adam_one(P[q].y, m4.y, v4.y, G[1], lr.y, bc1, bc2);
                 p4.z = adam_one(P[q].z, m4.z, v4.z, G[2], lr.z, bc1, bc2);
                 p4.w = c4 == 14 ? P[q].w : adam_one(P[q].w, m4.w, v4.w, G[3], lr.w, bc1, bc2);  // col 59: padding
+#else
+                adam_two(P[q].x, P[q].y, m4.x, m4.y, v4.x, v4.y, G[0], G[1], lr.x, lr.y, bc1, bc2, p4.x, p4.y);
+                adam_two(P[q].z, P[q].w, m4.z, m4.w, v4.z, v4.w, G[2], G[3], lr.z, lr.w, bc1, bc2, p4.z, p4.w);
+                if (c4 == 14) p4.w = P[q].w;  // col 59: padding
+#endif
                 if (c4 == 14) {
                     m4.w = M4[q].w;
                     v4.w = V4[q].w;
