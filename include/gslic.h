@@ -237,6 +237,27 @@ int gs_chain_adam_part(const gs_frame *f, float *params, float *adam_m, float *a
                        const gs_view *view, const float *lr_cols, int32_t stage, int32_t part, int32_t nparts,
                        void *stream);
 
+/* Multi-GPU batch step over peer memory: the ranks' gradient-row allreduce fused
+ * with the sparse Adam update (R/rasterizer.py:707-725) in one persistent kernel per rank.
+ * grads / packed / gready / rdone: world device pointers each (this rank's own and its peers',
+ * opened with gs_ipc_import), packed >= u x 60 floats, the flags zero-initialised u64 words;
+ * idx[0..u): the union of touched ids (id order, identical on every rank); epoch: 1, 2, ... per
+ * step.  Rank r sums its shard [u r / world, u (r+1) / world) over the ranks in rank order into
+ * packed[r], then every rank applies the update for every shard from its owner's packed rows,
+ * clearing my_grads rows and touched flags (as gs_adam_packed).  keep (optional, u x 60): the
+ * reduced rows.  *err = 1 if a peer never arrived (bounded waits). */
+int gs_p2p_reduce_adam(int32_t world, int32_t rank, const float *const *grads, const float *const *packed,
+                       uint64_t *const *gready, uint64_t *const *rdone, uint64_t epoch, int64_t u,
+                       const int32_t *idx, float *params, float *adam_m, float *adam_v, int32_t *adam_t,
+                       const float *lr_cols, float *my_grads, uint8_t *touched, uint32_t *ticket, float *keep,
+                       int32_t *err, void *stream);
+
+/* CUDA IPC for gs_p2p_reduce_adam: the 64-byte handle of the allocation holding ptr and ptr's
+ * offset in it; a peer's pointer from (handle, offset) (base: for gs_ipc_close). */
+int gs_ipc_export(const void *ptr, uint8_t *handle, int64_t *offset);
+int gs_ipc_import(const uint8_t *handle, int64_t offset, void **ptr, void **base);
+int gs_ipc_close(void *base);
+
 /* R/rasterizer.py:559-644 only: grads[row] += d loss / d params (rows of GS_ROW floats);
  * touched_accum[i] |= touched[i]. */
 int gs_chain(const gs_frame *f, const float *params, float *grads, uint8_t *touched_accum, const gs_view *view,

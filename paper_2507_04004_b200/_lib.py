@@ -93,6 +93,11 @@ def lib():
         "gs_render_bwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), P]),
         "gs_chain_adam": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, P]),
         "gs_chain_adam_part": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P, i32, i32, i32, P]),
+        "gs_p2p_reduce_adam": (ctypes.c_int, [i32, i32, P, P, P, P, ctypes.c_uint64, i64, P, P, P, P, P, P, P, P, P, P,
+                                              P, P]),
+        "gs_ipc_export": (ctypes.c_int, [P, P, ctypes.POINTER(i64)]),
+        "gs_ipc_import": (ctypes.c_int, [P, i64, ctypes.POINTER(P), ctypes.POINTER(P)]),
+        "gs_ipc_close": (ctypes.c_int, [P]),
         "gs_chain": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P]),
         "gs_chain_pose": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, P, P, P, P]),
         "gs_project_points": (ctypes.c_int, [P, i64, P, P, P, f32, P, P, P, P, P, P, P, P]),
@@ -123,7 +128,8 @@ EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_e
             "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
             "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
             "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_decode_u8", "gs_track_mask", "gs_track_grad", "gs_pose_adam",
-            "gs_compact_flags", "gs_gather_rows", "gs_adam_packed"]
+            "gs_compact_flags", "gs_gather_rows", "gs_adam_packed", "gs_p2p_reduce_adam", "gs_ipc_export",
+            "gs_ipc_import", "gs_ipc_close"]
 
 
 def check(rc: int, what: str) -> None:

@@ -18,7 +18,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libgslic.so")
-SOURCES = ["api.cu", "preprocess.cu", "binning.cu", "render.cu", "loss.cu", "adam.cu", "keyframe.cu", "track.cu"]
+SOURCES = ["api.cu", "preprocess.cu", "binning.cu", "render.cu", "loss.cu", "adam.cu", "keyframe.cu", "track.cu",
+           "p2p.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

@@ -394,6 +394,44 @@ __device__ __forceinline__ void splat_store(float *splat2d, int64_t g, float mx,
 }
 
 // ---------------------------------------------------------------------------
+// Sparse Adam (R/rasterizer.py:707-725), shared by the fused chain + Adam and the packed updates
+
+// One Adam element (R/rasterizer.py:715-725): m, v moments, bias-corrected step
+// lr * (m / bc1) / (sqrt(v / bc2) + 1e-15).  rbc1 = 1/bc1, rbc2 = 1/bc2 are per-row constants.
+// The square root and the reciprocal are single MUFU instructions (sqrt.approx / rcp.approx,
+// ~1 ulp; the denominator is >= 1e-15, never subnormal): with IEEE sqrtf and __frcp_rn
+// (Newton steps + fix-up paths) the 59 updates per row were a third of the fused chain+Adam
+// kernel's instructions.
+__device__ __forceinline__ float adam_one(float p, float &m, float &v, float g, float lr, float rbc1, float rbc2) {
+    m = 0.9f * m + 0.1f * g;
+    v = 0.999f * v + 0.001f * g * g;
+    const float den = fast_sqrt(v * rbc2) + 1e-15f;
+    return p - (lr * (m * rbc1)) * fast_rcp(den);
+}
+
+// Two Adam elements with paired fp32 instructions (FFMA2 / FMUL2 / FADD2): the operations and
+// their order of adam_one as compiled (m = fma(0.9, m, 0.1 g), v = fma(0.999, v, (0.001 g) g),
+// p - (lr (m rbc1)) rcp(den) as one fused multiply-add), so the results are the same bits.
+__device__ __forceinline__ void adam_two(float p0, float p1, float &m0, float &m1, float &v0, float &v1, float g0,
+                                         float g1, float lr0, float lr1, float rbc1, float rbc2, float &o0,
+                                         float &o1) {
+    const float2 g = make_float2(g0, g1);
+    const float2 m = __ffma2_rn(make_float2(0.9f, 0.9f), make_float2(m0, m1), __fmul2_rn(g, make_float2(0.1f, 0.1f)));
+    const float2 gg = __fmul2_rn(__fmul2_rn(g, make_float2(0.001f, 0.001f)), g);
+    const float2 v = __ffma2_rn(make_float2(0.999f, 0.999f), make_float2(v0, v1), gg);
+    const float2 vr = __fmul2_rn(v, make_float2(rbc2, rbc2));
+    const float2 den = __fadd2_rn(make_float2(fast_sqrt(vr.x), fast_sqrt(vr.y)), make_float2(1e-15f, 1e-15f));
+    const float2 nstep = __fmul2_rn(make_float2(-lr0, -lr1), __fmul2_rn(m, make_float2(rbc1, rbc1)));
+    const float2 o = __ffma2_rn(nstep, make_float2(fast_rcp(den.x), fast_rcp(den.y)), make_float2(p0, p1));
+    m0 = m.x;
+    m1 = m.y;
+    v0 = v.x;
+    v1 = v.y;
+    o0 = o.x;
+    o1 = o.y;
+}
+
+// ---------------------------------------------------------------------------
 // Deterministic accumulation.  Screen-space gradient rows (and the pose gradient) are sums of
 // per-tile (per-Gaussian) partials in an order the scheduler picks.  Each partial is split
 // exactly into two 64-bit fixed-point words, hi in units of 2^-24 and lo in units of 2^-64, and

@@ -58,6 +58,47 @@ def allreduce_grads_sparse(rows: torch.Tensor, touched: torch.Tensor, group=None
     return int(idx.numel())
 
 
+class PeerExchange:
+    """Every rank's gradient rows, reduced-shard buffer and two epoch flags, opened in every other
+    rank's address space through CUDA IPC (one exchange at set-up), for gs_p2p_reduce_adam: the
+    allreduce of the batch step reads peer memory directly (NVLink / NVSwitch on one node; the
+    same device when ranks share a GPU) instead of going through NCCL."""
+
+    def __init__(self, grads: torch.Tensor, packed: torch.Tensor, flags: torch.Tensor, group=None):
+        import ctypes
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        mine = []
+        for t in (grads, packed, flags):
+            h = (ctypes.c_uint8 * 64)()
+            off = ctypes.c_int64(0)
+            call("gs_ipc_export", t.data_ptr(), ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off))
+            mine.append((bytes(h), int(off.value)))
+        allx = [None] * self.world
+        dist.all_gather_object(allx, mine, group=group)
+        self.bases = []
+        ptrs = [[0] * self.world for _ in range(3)]
+        for k in range(self.world):
+            for j, t in enumerate((grads, packed, flags)):
+                if k == self.rank:
+                    ptrs[j][k] = t.data_ptr()
+                    continue
+                hb, off = allx[k][j]
+                p, b = ctypes.c_void_p(), ctypes.c_void_p()
+                hbuf = (ctypes.c_uint8 * 64).from_buffer_copy(hb)
+                call("gs_ipc_import", ctypes.cast(hbuf, ctypes.c_void_p), off, ctypes.byref(p), ctypes.byref(b))
+                ptrs[j][k] = p.value
+                self.bases.append(b.value)
+        arr = ctypes.c_void_p * self.world
+        # host arrays of device pointers (the C ABI copies them into the kernel's parameters)
+        self._arrays = [arr(*ptrs[0]), arr(*ptrs[1]), arr(*ptrs[2]), arr(*[p + 8 for p in ptrs[2]])]
+        self.grads, self.packed, self.gready, self.rdone = (ctypes.cast(a, ctypes.c_void_p) for a in self._arrays)
+
+    def close(self) -> None:
+        for b in self.bases:
+            call("gs_ipc_close", b)
+        self.bases = []
+
+
 class BatchMapOptimizer:
     """Batched (optionally data-parallel) map optimisation over this rank's keyframes.
 
@@ -108,6 +149,17 @@ class BatchMapOptimizer:
         self.replayed = 0
         self.keep_reduced = False  # tests: keep (union ids, reduced gradient rows) of the last batch
         self.reduced = None
+        # world > 1: the allreduce + Adam over peer memory (gs_p2p_reduce_adam) unless
+        # GSLIC_P2P=0 selects the NCCL collectives + gs_adam_packed
+        import os
+        self.p2p = None
+        self.epoch = 0
+        if self._world() > 1 and os.environ.get("GSLIC_P2P", "1") != "0":
+            self.packed = torch.zeros((max(n, 1), 60), dtype=torch.float32, device=self.dev)
+            self._flags = torch.zeros(2, dtype=torch.int64, device=self.dev)  # (gready, rdone) epochs
+            self._ticket = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self.p2p_err = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self.p2p = PeerExchange(self.grads, self.packed, self._flags, group)
 
     def _workspace(self, capacity: int) -> Workspace:
         ws = Workspace(len(self.g), self.W, self.H, capacity, self.dev)
@@ -120,7 +172,10 @@ class BatchMapOptimizer:
     def kernels_per_step(self, views: int | None = None) -> int:
         from .mapper import kernels_per_iteration
         per_view = kernels_per_iteration(self.ws.tiles_x * self.ws.tiles_y, chain_only=True)
-        extra = 2 + (1 + self.CHUNKS if self._world() > 1 else 1)  # compaction 2, gather, Adam chunk(s)
+        if self._world() > 1:  # compaction 2, then the fused P2P kernel or gather + Adam chunks
+            extra = 2 + (1 if self.p2p is not None else 1 + self.CHUNKS)
+        else:
+            extra = 2 + 1
         return per_view * (views if views is not None else len(self.views)) + extra
 
     def accumulate(self, k: int) -> None:
@@ -187,6 +242,9 @@ class BatchMapOptimizer:
         s = stream_ptr()
         world = self._world()
         if world > 1:
+            # every rank re-runs the batch if any view of any rank overflowed (the collectives
+            # below must pair up), then the touched union
+            dist.all_reduce(self.overflow, op=dist.ReduceOp.MAX, group=self.group)
             dist.all_reduce(self.touched, op=dist.ReduceOp.MAX, group=self.group)
         n = len(self.g)
         call("gs_compact_flags", self.touched.data_ptr(), n, self.idx.data_ptr(), self.count.data_ptr(),
@@ -215,6 +273,17 @@ class BatchMapOptimizer:
                 self.reduced = (ids.clone(), self.grads[ids, :60].clone())
             call("gs_adam_packed", *adam_args, None, self.idx.data_ptr(), self.count.data_ptr(), 0, u,
                  self.lr.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), s)
+            return
+        if self.p2p is not None:  # allreduce fused with Adam over peer memory
+            self.epoch += 1
+            keep = torch.empty((u, 60), dtype=torch.float32, device=self.dev) if self.keep_reduced else None
+            x = self.p2p
+            call("gs_p2p_reduce_adam", world, x.rank, x.grads, x.packed, x.gready, x.rdone, self.epoch, u,
+                 self.idx.data_ptr(), *adam_args, self.lr.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(),
+                 self._ticket.data_ptr(), keep.data_ptr() if keep is not None else None, self.p2p_err.data_ptr(), s)
+            if keep is not None:
+                self.reduced = (self.idx[:u].long().clone(), keep)
+            self.overflow.zero_()
             return
         if self.packed.shape[0] < u:
             self.packed = torch.zeros((int(u * 1.25) + 1024, 60), dtype=torch.float32, device=self.dev)

@@ -32,13 +32,14 @@ def _engine(sc, ids):
     return PAR.BatchMapOptimizer(GaussianMap.from_rows(sc.rows), kfs, R.default_lrs(3.0))
 
 
-def _worker(rank, world, port, out):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, port, out, p2p):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), GSLIC_P2P="1" if p2p else "0")
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     sc = _scene()
     mine = list(range(rank, len(VIEWS), world))
     eng = _engine(sc, mine)
+    assert (eng.p2p is not None) == p2p
     eng.keep_reduced = True
     eng.step(range(len(mine)))
     torch.cuda.synchronize()
@@ -50,7 +51,11 @@ def _worker(rank, world, port, out):
     torch.cuda.synchronize()
     np.save(out.format(rank), eng.g.rows().cpu().numpy())
     np.save(out.format(f"t{rank}"), eng.adam.t.cpu().numpy())
+    if p2p:
+        assert int(eng.p2p_err.item()) == 0  # no bounded peer wait ran out
     dist.barrier()
+    if p2p:
+        eng.p2p.close()
     dist.destroy_process_group()
 
 
@@ -63,9 +68,12 @@ def _port():
 
 
 @pytest.mark.timeout(900)
-def test_two_ranks_on_device_match_single_process_batch(tmp_path):
+@pytest.mark.parametrize("p2p", [True, False], ids=["p2p-fused", "collective"])
+def test_two_ranks_on_device_match_single_process_batch(tmp_path, p2p):
+    """p2p-fused: the gradient allreduce + Adam as one kernel per rank reading the peer's memory
+    through CUDA IPC (gs_p2p_reduce_adam); collective: gloo allreduce chunks + gs_adam_packed."""
     out = str(tmp_path / "r_{}.npy")
-    mp.spawn(_worker, args=(2, _port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _port(), out, p2p), nprocs=2, join=True)
     r0, r1 = np.load(out.format(0)), np.load(out.format(1))
     assert np.array_equal(r0, r1)  # replicas bit-identical after two batch steps
     assert np.array_equal(np.load(out.format("t0")), np.load(out.format("t1")))
