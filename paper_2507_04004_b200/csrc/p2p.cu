@@ -232,11 +232,11 @@ extern "C" int gs_p2p_reduce_adam(int32_t world, int32_t rank, const float *cons
         a.rdone[k] = reinterpret_cast<unsigned long long *>(rdone[k]);
     }
     // persistent and fully resident: phase B waits on this grid's own phase A
-    static int per_sm = 0;
-    if (!per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, p2p_reduce_adam_kernel, P2P_THREADS, 0);
-        if (per_sm < 1) per_sm = 1;
-    }
+    static const int per_sm = [] {  // (thread-safe static initialisation)
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, p2p_reduce_adam_kernel, P2P_THREADS, 0);
+        return b < 1 ? 1 : b;
+    }();
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

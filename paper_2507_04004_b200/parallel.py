@@ -140,7 +140,8 @@ class BatchMapOptimizer:
         self.scratch = torch.zeros((n + 1023) // 1024 + 1, dtype=torch.int32, device=self.dev)
         self.count = torch.zeros(1, dtype=torch.int32, device=self.dev)
         self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
-        self._h = torch.zeros(2, dtype=torch.int32).pin_memory()  # (union size, overflow) read back
+        # (union size, overflow, the previous batch's peer-wait error) read back once per batch
+        self._h = torch.zeros(3, dtype=torch.int32).pin_memory()
         self.packed = torch.zeros((0, 60), dtype=torch.float32, device=self.dev)
         self.cur = torch.empty_like(self.views[0].buf)
         self.loss_acc = torch.zeros(1, dtype=torch.float64, device=self.dev)
@@ -251,7 +252,11 @@ class BatchMapOptimizer:
              self.scratch.data_ptr(), s)
         self._h[0:1].copy_(self.count, non_blocking=True)
         self._h[1:2].copy_(self.overflow, non_blocking=True)
+        if self.p2p is not None:
+            self._h[2:3].copy_(self.p2p_err, non_blocking=True)
         torch.cuda.current_stream().synchronize()
+        if int(self._h[2]):
+            raise DataError("gs_p2p_reduce_adam: a peer rank never reached the batch (bounded wait expired)")
         if int(self._h[1]):  # some view overflowed its entry capacity: redo the batch's views
             torch.cuda.synchronize(self.dev)
             self.grads.zero_()
