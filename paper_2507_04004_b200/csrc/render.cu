@@ -305,7 +305,10 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
     return __syncthreads_count(px.done) == RT;
 }
 
-__global__ void __launch_bounds__(FT) render_fwd_kernel(gs_frame f, int early_stop) {
+#ifndef FWD_MINB
+#define FWD_MINB 16  // 64 registers: 16 CTAs (32 warps) per SM
+#endif
+__global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, int early_stop) {
     pdl_wait();
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
