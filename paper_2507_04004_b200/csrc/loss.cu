@@ -443,7 +443,10 @@ __global__ void __launch_bounds__(L_THREADS, 4) ssim_fwd_kernel(gs_frame f, cons
     }
 }
 
-__global__ void __launch_bounds__(L_THREADS, 3) ssim_bwd_kernel(gs_frame f, const gs_view *__restrict__ view,
+#ifndef SB_MINB
+#define SB_MINB 3
+#endif
+__global__ void __launch_bounds__(L_THREADS, SB_MINB) ssim_bwd_kernel(gs_frame f, const gs_view *__restrict__ view,
                                                                 const float *__restrict__ tab_x,
                                                                 const float *__restrict__ tab_y, float lam,
                                                                 int depth_grads_zero) {
