@@ -17,7 +17,10 @@ namespace gs {
 constexpr int CA_WARPS = 4;
 constexpr int CA_THREADS = CA_WARPS * 32;
 constexpr int RP = 65;  // padded smem row
-constexpr int CA_BATCH = 4;  // float4 per lane and array in flight in the fused Adam stream
+#ifndef CA_BATCH
+#define CA_BATCH 4  // float4 per lane and array in flight in the fused Adam stream
+#endif
+static_assert(16 % CA_BATCH == 0, "the Adam stream's rounds tile the warp's 16 float4 per lane");
 #ifndef CA_MINB
 #define CA_MINB 4  // CTAs per SM the register budget is fitted to (16 warps)
 #endif

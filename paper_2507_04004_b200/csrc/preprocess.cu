@@ -11,7 +11,10 @@ namespace gs {
 
 constexpr int PP_WARPS = 4;
 constexpr int PP_THREADS = PP_WARPS * 32;
-constexpr int PP_CTAS_PER_SM = 5;  // persistent grid: shared memory allows five
+#ifndef PP_CTAS
+#define PP_CTAS 5
+#endif
+constexpr int PP_CTAS_PER_SM = PP_CTAS;  // persistent grid: shared memory allows five
 
 __device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
