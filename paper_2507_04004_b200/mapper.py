@@ -127,6 +127,9 @@ class HostKeyframes:
                 per.append(torch.frombuffer(bytearray(bytes(memoryview(v).cast("B"))), dtype=torch.uint8).pin_memory())
             self.views.append(per)
         self.copy_stream = torch.cuda.Stream(device=device)
+        # loss read-backs go on a stream of their own: on the upload stream each one would wait
+        # for its iteration and hold the next keyframe's upload behind it
+        self.d2h_stream = torch.cuda.Stream(device=device)
         self.slot_free = [None] * self.NSLOT
         nbytes = [self.img[k].numel() * self.img[k].element_size() + self.idx[k].numel() * 8 +
                   self.views[k][0].numel() for k in range(len(keyframes))]
@@ -411,7 +414,6 @@ class MapOptimizer:
         """Map-optimisation iterations over host keyframes `order` (R/mapper.py:242-256 samples
         the keyframe order up front): keyframe j+1 is uploaded on a copy stream while iteration j
         runs; each iteration's loss is read back into pinned host memory (D2H)."""
-        cs = self.host.copy_stream
 
         def body(j, k, view_ptr):
             self._check(self.LAG)
@@ -423,17 +425,19 @@ class MapOptimizer:
             self._record(lambda: self._rerun_host(k, h), loss_slot=h)
 
         self.host.stream(order, body, use_cur=False)
+        # the read-backs are part of the call: later work on this stream follows them
+        torch.cuda.current_stream().wait_stream(self.host.d2h_stream)
 
     LOSS_RING = 1024
 
     def _read_loss(self, ev, h: int) -> None:
         """D2H of the iteration's loss (device ring slot, written by the loss kernel itself) into
-        pinned slot h, on the copy stream once the iteration's event has fired: no kernel and no
+        pinned slot h, on the read-back stream once the iteration's event has fired: no kernel and no
         main-stream work per iteration.  The device ring holds GS_LOSS_RING iterations, far more
         than the copy stream ever lags (the host keyframe slots bound the run-ahead to
         HostKeyframes.NSLOT iterations)."""
         pos = self._dev_iter % _lib.GS_LOSS_RING
-        cs = self.host.copy_stream
+        cs = self.host.d2h_stream
         cs.wait_event(ev)
         with torch.cuda.stream(cs):
             self._h_loss[h].copy_(self.ws.loss[8 + pos], non_blocking=True)
