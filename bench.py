@@ -540,7 +540,9 @@ def run_ours_dp(args, rank, world, local) -> dict:
            "vs_baseline": None, "dtype": "f32", "data": "synthetic S2r room scene (seed 7)",
            "config": bench_config(args.config, batch, batch=batch, world=world),
            "notes": {"per_rank_views": len(mine), "union_rows_last_batch": eng.union,
-                     "reduction": ("touched OR (n bytes) + device compaction + one kernel per rank: reduce-scatter "
+                     "reduction": "single rank: device compaction of the touched union, one sparse Adam straight "
+                                  "from the accumulated gradient rows" if world == 1 else
+                                  ("touched OR (n bytes) + device compaction + one kernel per rank: reduce-scatter "
                                    "of the union's rows over peer memory (CUDA IPC, NVLink) fused with the all-gather "
                                    "and the sparse Adam (gs_p2p_reduce_adam)") if eng.p2p is not None else
                                   ("touched OR (n bytes) + device compaction + NCCL allreduce of the union's "
