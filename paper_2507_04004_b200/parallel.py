@@ -68,14 +68,19 @@ class PeerExchange:
         import ctypes
         self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
         mine = []
-        for t in (grads, packed, flags):
-            h = (ctypes.c_uint8 * 64)()
-            off = ctypes.c_int64(0)
-            call("gs_ipc_export", t.data_ptr(), ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off))
-            mine.append((bytes(h), int(off.value)))
+        try:
+            for t in (grads, packed, flags):
+                h = (ctypes.c_uint8 * 64)()
+                off = ctypes.c_int64(0)
+                call("gs_ipc_export", t.data_ptr(), ctypes.cast(h, ctypes.c_void_p), ctypes.byref(off))
+                mine.append((bytes(h), int(off.value)))
+        except Exception:  # noqa: BLE001 -- every rank still joins the exchange below
+            mine = None
         allx = [None] * self.world
         dist.all_gather_object(allx, mine, group=group)
         self.bases = []
+        if any(x is None for x in allx):
+            raise RuntimeError("a rank could not export its buffers through CUDA IPC")
         ptrs = [[0] * self.world for _ in range(3)]
         for k in range(self.world):
             for j, t in enumerate((grads, packed, flags)):
@@ -160,7 +165,22 @@ class BatchMapOptimizer:
             self._flags = torch.zeros(2, dtype=torch.int64, device=self.dev)  # (gready, rdone) epochs
             self._ticket = torch.zeros(1, dtype=torch.int32, device=self.dev)
             self.p2p_err = torch.zeros(1, dtype=torch.int32, device=self.dev)
-            self.p2p = PeerExchange(self.grads, self.packed, self._flags, group)
+            # every rank must take the same path: the peer-memory form only if every rank could
+            # open every peer's buffers (CUDA IPC), else the NCCL collectives for all
+            ex, ok = None, 1
+            try:
+                ex = PeerExchange(self.grads, self.packed, self._flags, group)
+            except Exception as e:  # noqa: BLE001 -- recorded, and the ranks agree below
+                self.p2p_reason = f"CUDA IPC unavailable: {e}"
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device=self.dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if int(flag.item()):
+                self.p2p = ex
+            else:
+                if ex is not None:
+                    ex.close()
+                self.p2p_reason = getattr(self, "p2p_reason", "a peer rank could not open CUDA IPC handles")
 
     def _workspace(self, capacity: int) -> Workspace:
         ws = Workspace(len(self.g), self.W, self.H, capacity, self.dev)
