@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
         boff[T] = s_carry[1];
         f.counters[GS_CNT_ENTRIES] = (int32_t)E;
         f.counters[GS_CNT_SMALL_E] = s_carry[1];
-        if (over) f.counters[GS_CNT_OVERFLOW] = 1;
+        f.counters[GS_CNT_OVERFLOW] = over ? 1 : 0;
         f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
         f.counters[GS_CNT_LAZY] = lazy;
         f.counters[GS_CNT_ANYFLAG] = 0;
@@ -346,10 +346,12 @@ extern "C" int gs_bin(const gs_frame *f, int32_t cull, void *stream) {
     }
     // reset the binning counters (touched, big and huge belong to preprocess) and the per-tile
     // counts
-    cudaMemsetAsync(f->counters + GS_CNT_ENTRIES, 0, sizeof(int32_t), st);
-    cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * 2, st);  // OVERFLOW, ENTRIES_EFF
-    cudaMemsetAsync(f->counters + GS_CNT_SMALL_E, 0, sizeof(int32_t), st);
+    // (tile_scan_kernel assigns the binning counters -- entries, small entries, overflow -- so a
+    // repeated binning of one preprocess starts from its own values)
     if (n == 0) {
+        cudaMemsetAsync(f->counters + GS_CNT_ENTRIES, 0, sizeof(int32_t), st);
+        cudaMemsetAsync(f->counters + GS_CNT_OVERFLOW, 0, sizeof(int32_t) * 2, st);  // OVERFLOW, ENTRIES_EFF
+        cudaMemsetAsync(f->counters + GS_CNT_SMALL_E, 0, sizeof(int32_t), st);
         cudaMemsetAsync(f->tile_offsets, 0, sizeof(int32_t) * (T + 1), st);
         return check_launch("gs_bin");
     }

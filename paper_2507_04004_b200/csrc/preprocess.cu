@@ -5,6 +5,8 @@
 // radius and tile rectangle).  One thread per Gaussian; each warp stages the geometry of its 32
 // parameter rows through shared memory with coalesced cp.async, and the SH columns only of the
 // Gaussians that need a colour.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace gs {
@@ -900,6 +902,27 @@ static int launch_big_cull(const gs_frame *f, int allow_huge, cudaStream_t st) {
     return check_launch("big_exact_kernel");
 }
 
+namespace gs {
+// a frame's per-view accumulators back to their initial state: counters 0, per-tile bucket and
+// huge counts 0, per-tile smallest bucketed keys ~0
+__global__ void __launch_bounds__(256) frame_reset_kernel(gs_frame f) {
+    pdl_wait();
+    const int T1 = f.tiles_x * f.tiles_y + 1;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < max(2 * T1, GS_CNT_SLOTS * 2); i += gridDim.x * blockDim.x) {
+        if (i < 2 * T1) f.tile_scratch[i] = 0;
+        if (i < T1) reinterpret_cast<unsigned long long *>(f.tile_minkey)[i] = ~0ull;
+        if (i < GS_CNT_SLOTS * 2) f.counters[i] = 0;
+    }
+}
+}  // namespace gs
+
+static int launch_frame_reset(const gs_frame *f, cudaStream_t st) {
+    const int T1 = f->tiles_x * f->tiles_y + 1;
+    const unsigned blocks = (unsigned)std::min(148, (2 * T1 + 255) / 256);
+    launch_pdl(frame_reset_kernel, blocks, 256, 0, st, *f);
+    return check_launch("frame_reset_kernel");
+}
+
 extern "C" int gs_preprocess(const gs_frame *f, const float *params, const gs_view *view, void *stream) {
     return gs_preprocess_ex(f, params, view, 0, stream);
 }
@@ -910,10 +933,10 @@ extern "C" int gs_preprocess_ex(const gs_frame *f, const float *params, const gs
         set_error("gs_preprocess: null argument or unknown flags");
         return GS_ERR_ARG;
     }
-    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
-    // per-tile bucket counts and huge counts of the binning (gs_bin reads them)
-    cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
-    cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
+    // counters, per-tile bucket / huge counts (gs_bin reads them) and smallest keys: one kernel
+    // (a graph node that keeps the launch chain programmatic, unlike three memsets)
+    int rc0 = launch_frame_reset(f, (cudaStream_t)stream);
+    if (rc0) return rc0;
     if (f->n == 0) return GS_OK;
     if (flags & GS_PP_LAZY_SH)
         launch_pdl(preprocess_kernel<true>, PP_CTAS_PER_SM * 148, PP_THREADS, PP_WARPS * sizeof(PPWarp), (cudaStream_t)stream, *f, params,
@@ -947,9 +970,8 @@ extern "C" int gs_eval_sh(const float *sh_low, const float *sh_high, const float
 extern "C" int gs_pack_splats(const gs_frame *f, const float *mean2d, const float *conic, const float *cov2d3,
                               const float *opacity, const float *depth, const uint8_t *valid, const float *colors,
                               void *stream) {
-    cudaMemsetAsync(f->counters, 0, sizeof(int32_t) * GS_CNT_SLOTS * 2, (cudaStream_t)stream);
-    cudaMemsetAsync(f->tile_scratch, 0, sizeof(int32_t) * 2 * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
-    cudaMemsetAsync(f->tile_minkey, 0xff, sizeof(uint64_t) * ((size_t)f->tiles_x * f->tiles_y + 1), (cudaStream_t)stream);
+    int rc0 = launch_frame_reset(f, (cudaStream_t)stream);
+    if (rc0) return rc0;
     if (f->n == 0) return GS_OK;
     launch_pdl(pack_kernel, (unsigned)((f->n + 127) / 128), 128, 0, (cudaStream_t)stream, *f, mean2d, conic, cov2d3, opacity,
                                                                                    depth, valid, colors);

@@ -27,18 +27,17 @@ NEAR_CLIP = 0.01
 
 
 def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
-    """Our kernels per map-optimisation iteration:
-    preprocess 5 (projection + small-footprint cull, large-footprint setup / bands / tiles /
-    finish), bin 3 (lazy lists: huge sort, huge transpose, tile scan), forward 3 (blend, bucket
-    fill + sorted continuation for the tiles that need them), loss 2 (SSIM+L1; depth with the
-    finalisation in its last block; the reflection tables are built once per workspace),
-    backward 1 (the g2d rows are kept
-    zero by the chain rule), chain rule fused with Adam 1 (2 with GSLIC_SPLIT_ADAM=1: chain +
-    adam_list)."""
+    """Our kernels per map-optimisation iteration: preprocess 4 (frame reset, projection +
+    small-footprint cull, large-footprint bands, exact tiles), bin 3 (lazy lists: huge sort, huge
+    transpose, tile scan), forward 3 (blend, bucket fill + sorted continuation for the tiles that
+    need them), loss 3 (SSIM map + partials, SSIM adjoint + gradient assembly, LiDAR depth with
+    the finalisation in its last block; the reflection tables are built once per workspace),
+    backward 1 (the g2d rows are kept zero by the chain rule), chain rule fused with Adam 1 (2
+    with GSLIC_SPLIT_ADAM=1: chain + adam_list)."""
     del tiles
     import os
     split = os.environ.get("GSLIC_SPLIT_ADAM", "0") == "1"
-    return 5 + 3 + 3 + 2 + 1 + (1 if chain_only or not split else 2)
+    return 4 + 3 + 3 + 3 + 1 + (1 if chain_only or not split else 2)
 
 
 @dataclass
