@@ -156,10 +156,12 @@ typedef struct gs_frame {
     float *g_depth;          /* H x W      xi dLd/ddepth */
     float *g_opac;           /* H x W      xi dLd/dopacity */
     double *loss_parts;      /* per-block partial sums */
-    double *loss;            /* 8 + GS_LOSS_RING: total, photometric, depth, dssim, running sum
+    double *loss;            /* 8 + 5 GS_LOSS_RING: total, photometric, depth, dssim, running sum
                                 (GS_LOSS_ACCUMULATE), -, ring position, -, then the per-iteration loss
                                 ring: with GS_LOSS_ACCUMULATE iteration i writes its total to
-                                loss[8 + i % GS_LOSS_RING] (i counted from the workspace's layout) */
+                                loss[8 + i % GS_LOSS_RING] (i counted from the workspace's layout)
+                                and a snapshot of counters[0..8) to the int32 words
+                                8 (i % GS_LOSS_RING) .. + 8 after loss[8 + GS_LOSS_RING] */
     int64_t loss_blocks;
     int64_t *pose_acc;       /* 12: fixed-point accumulators of the pose gradient (gs_chain_pose) */
     float *ssim_g;           /* 3 x H x W x 4: SSIM-map partials per channel (d/d mu_a, d/d var sum,

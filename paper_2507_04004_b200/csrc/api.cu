@@ -112,7 +112,7 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.loss_parts = c.take<double>(3 * f.loss_blocks + (int64_t)11 * (w + h) + 1);
     // total, photometric, depth, dssim, running sum, -, ring position, -, then the per-iteration
     // loss ring (GS_LOSS_ACCUMULATE)
-    f.loss = c.take<double>(8 + GS_LOSS_RING);
+    f.loss = c.take<double>(8 + 5 * GS_LOSS_RING);  // + the counter snapshot ring (gslic.h)
     f.pose_acc = c.take<int64_t>(16);
     f.ssim_g = c.take<float>(12 * P);
 }

@@ -591,6 +591,10 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
         if (accumulate) {  // per-iteration ring: the host reads iteration i's loss at slot i % RING
             const long long pos = (long long)f.loss[6];
             f.loss[8 + pos % GS_LOSS_RING] = lc + (double)xi * ld;
+            // the binning counters of this iteration (final here) for the host's lagged capacity
+            // check, read back off the compute stream
+            int32_t *snap = reinterpret_cast<int32_t *>(f.loss + 8 + GS_LOSS_RING) + 8 * (pos % GS_LOSS_RING);
+            for (int q = 0; q < 8; q++) snap[q] = f.counters[q];
             f.loss[6] = (double)(pos + 1);
         }
         int *stamp = reinterpret_cast<int *>(tab_stamp);

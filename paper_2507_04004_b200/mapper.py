@@ -126,9 +126,6 @@ class HostKeyframes:
                 per.append(torch.frombuffer(bytearray(bytes(memoryview(v).cast("B"))), dtype=torch.uint8).pin_memory())
             self.views.append(per)
         self.copy_stream = torch.cuda.Stream(device=device)
-        # loss read-backs go on a stream of their own: on the upload stream each one would wait
-        # for its iteration and hold the next keyframe's upload behind it
-        self.d2h_stream = torch.cuda.Stream(device=device)
         self.slot_free = [None] * self.NSLOT
         nbytes = [self.img[k].numel() * self.img[k].element_size() + self.idx[k].numel() * 8 +
                   self.views[k][0].numel() for k in range(len(keyframes))]
@@ -247,6 +244,7 @@ class MapOptimizer:
         import os
         self.overlap_parts = int(os.environ.get("GSLIC_OVERLAP_PARTS", "0"))
         self._side = torch.cuda.Stream(device=self.dev)
+        self._d2h = torch.cuda.Stream(device=self.dev)  # per-step read-backs (counters, losses)
 
     def _workspace(self, capacity: int) -> Workspace:
         """A zero-filled workspace whose loss reflection tables are built (one gs_loss on the
@@ -326,17 +324,31 @@ class MapOptimizer:
         self._record(lambda: self._run_view(vp))
 
     def _record(self, rerun, loss_slot: int | None = None) -> None:
-        """Snapshot this iteration's counters (async D2H) for the lagged capacity check; with
-        loss_slot, also read its loss back into pinned memory (run_host)."""
+        """After this iteration, read back (on the read-back stream, so the compute stream carries
+        nothing but the graph replays) its counter snapshot -- written by the loss kernel into the
+        workspace's device ring -- for the lagged capacity check, and with loss_slot its loss
+        into pinned slot loss_slot (run_host)."""
         ring = self._ring[self._steps % self.RING]
-        ring.copy_(self.ws.counters[:8], non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-        if loss_slot is not None:
-            self._read_loss(ev, loss_slot)
-        self._pending.append((ev, ring, rerun, loss_slot))
+        pos = self._dev_iter % _lib.GS_LOSS_RING
+        d = self._d2h
+        d.wait_event(ev)
+        with torch.cuda.stream(d):
+            ring.copy_(self._snap[pos], non_blocking=True)
+            if loss_slot is not None:
+                self._h_loss[loss_slot].copy_(self.ws.loss[8 + pos], non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(d)
+        self._pending.append((done, ring, rerun, loss_slot))
         self._steps += 1
         self._dev_iter += 1
+
+    @property
+    def _snap(self) -> torch.Tensor:
+        """The workspace's counter snapshots (GS_LOSS_RING x 8 int32, gs_frame.loss)."""
+        r = _lib.GS_LOSS_RING
+        return self.ws.loss[8 + r:8 + 5 * r].view(torch.int32).view(r, 8)
 
     def _regrow(self, entries: int) -> None:
         torch.cuda.synchronize(self.dev)  # no kernel or copy still reads the old workspace
@@ -425,21 +437,9 @@ class MapOptimizer:
 
         self.host.stream(order, body, use_cur=False)
         # the read-backs are part of the call: later work on this stream follows them
-        torch.cuda.current_stream().wait_stream(self.host.d2h_stream)
+        torch.cuda.current_stream().wait_stream(self._d2h)
 
     LOSS_RING = 1024
-
-    def _read_loss(self, ev, h: int) -> None:
-        """D2H of the iteration's loss (device ring slot, written by the loss kernel itself) into
-        pinned slot h, on the read-back stream once the iteration's event has fired: no kernel and no
-        main-stream work per iteration.  The device ring holds GS_LOSS_RING iterations, far more
-        than the copy stream ever lags (the host keyframe slots bound the run-ahead to
-        HostKeyframes.NSLOT iterations)."""
-        pos = self._dev_iter % _lib.GS_LOSS_RING
-        cs = self.host.d2h_stream
-        cs.wait_event(ev)
-        with torch.cuda.stream(cs):
-            self._h_loss[h].copy_(self.ws.loss[8 + pos], non_blocking=True)
 
     def _rerun_host(self, k: int, h: int) -> None:
         torch.cuda.synchronize(self.dev)

@@ -174,7 +174,7 @@ class Workspace:
         self.counters = self.view("counters", "i32", (2 * _lib.GS_CNT_SLOTS,))
         self.entry_splat = self.view("entry_splat", "i32", (max(self.capacity, 1),))
         self.tile_offsets = self.view("tile_offsets", "i32", (self.tiles_x * self.tiles_y + 1,))
-        self.loss = self.view("loss", "f64", (8 + _lib.GS_LOSS_RING,))
+        self.loss = self.view("loss", "f64", (8 + 5 * _lib.GS_LOSS_RING,))
 
     @property
     def g2d(self) -> torch.Tensor:
