@@ -81,7 +81,8 @@ enum {
     GS_CNT_HUGE_N = 19,  /* huge Gaussians with >= 1 kept tile (records in depth order) */
     GS_CNT_CULLQ1 = 20,  /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
     GS_CNT_LAZY = 21,    /* 1: gs_bin(GS_BIN_LAZY) left the tile lists unmaterialised */
-    GS_CNT_ANYFLAG = 22  /* lazy lists: some tile needs its bucket (blend continuation) */
+    GS_CNT_ANYFLAG = 22, /* lazy lists: some tile needs its bucket (blend continuation) */
+    GS_CNT_FLAGGED = 23  /* lazy lists: how many (their ids in a tile_scratch segment) */
 };
 
 #define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */

@@ -90,7 +90,7 @@ static void carve(Carver &c, int64_t n, int32_t w, int32_t h, int64_t cap, gs_fr
     f.huge = c.take<int32_t>(13 * GS_HUGE_CAP);
     f.huge_mask = c.take<uint32_t>(((int64_t)tx * ty) * (GS_HUGE_CAP / 32));
     f.huge_mask_t = c.take<uint32_t>((int64_t)GS_HUGE_CAP * (((int64_t)tx * ty + 31) / 32));
-    f.tile_scratch = c.take<int32_t>(5 * ((int64_t)tx * ty + 1));
+    f.tile_scratch = c.take<int32_t>(6 * ((int64_t)tx * ty + 1));  // segments: tilelist.cuh
     f.tile_minkey = c.take<uint64_t>((int64_t)tx * ty + 1);
     f.big_bits_words = 4 * nn > (1 << 20) ? 4 * nn : (1 << 20);
     f.big_bits = c.take<uint32_t>(f.big_bits_words);

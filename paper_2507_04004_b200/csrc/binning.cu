@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(TS_THREADS) tile_scan_kernel(gs_frame f, int l
         f.counters[GS_CNT_ENTRIES_EFF] = over ? 0 : (int32_t)E;
         f.counters[GS_CNT_LAZY] = lazy;
         f.counters[GS_CNT_ANYFLAG] = 0;
+        f.counters[GS_CNT_FLAGGED] = 0;
     }
     // over capacity: every tile range is emptied, so no later kernel (lazy or materialised lists,
     // forward, backward) can index entry_splat / keys past the capacity; the caller re-lays out

@@ -12,6 +12,8 @@
 // contributions are summed in registers, reduced across the warp with a transposed butterfly
 // (10 fields in 12 shuffles), merged across the 4 warps with shared-memory atomics, and added
 // to the per-Gaussian FP64 gradient rows once per tile.
+#include <algorithm>
+
 #include "tilelist.cuh"
 
 namespace gs {
@@ -347,6 +349,7 @@ __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, in
             ts_flag(f)[tile] = TL_LIST;
             ts_resume(f)[tile] = lead;
             f.counters[GS_CNT_ANYFLAG] = 1;
+            ts_flagged(f)[atomicAdd(&f.counters[GS_CNT_FLAGGED], 1)] = tile;
         }
     } else {
         const int start = f.tile_offsets[tile], stop = f.tile_offsets[tile + 1];
@@ -404,13 +407,23 @@ struct FinishSmem {
     FwdStage st;
 };
 
+__device__ __forceinline__ void tile_finish_one(const gs_frame &f, FinishSmem &sm, int tile, int early_stop);
+
+// persistent over the tiles the forward flagged (a compact list; most tiles need no
+// continuation, and a grid over all tiles would mostly launch CTAs that exit at once)
 __global__ void __launch_bounds__(TF_THREADS) tile_finish_kernel(gs_frame f, int early_stop) {
     pdl_wait();
     if (!f.counters[GS_CNT_LAZY] || !f.counters[GS_CNT_ANYFLAG] || f.counters[GS_CNT_OVERFLOW]) return;
-    const int tile = blockIdx.x;
-    if (ts_flag(f)[tile] != TL_LIST) return;
     extern __shared__ uint64_t fin_raw[];
     FinishSmem &sm = *reinterpret_cast<FinishSmem *>(fin_raw);
+    const int nflag = f.counters[GS_CNT_FLAGGED];
+    for (int it = blockIdx.x; it < nflag; it += gridDim.x) {
+        if (it != (int)blockIdx.x) __syncthreads();  // the previous tile's shared state is consumed
+        tile_finish_one(f, sm, ts_flagged(f)[it], early_stop);
+    }
+}
+
+__device__ __forceinline__ void tile_finish_one(const gs_frame &f, FinishSmem &sm, int tile, int early_stop) {
     const int sb = ts_boff(f)[tile], nb = ts_boff(f)[tile + 1] - sb;
     const uint64_t *B = sort_bucket<TF_THREADS>(sm.key, f.keys_b + sb, f.keys_a + sb, nb, false);
     const int na = tile_huge_setup(f, tile, sm.words, sm.wpre_a, sm.tmp);
@@ -760,7 +773,8 @@ extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream
     // lazy lists: bucket fill + sorted continuation of the tiles that need them (no-ops otherwise)
     launch_pdl(lazy_fill_kernel, 4 * 148, 256, 0, (cudaStream_t)stream, *f);
     if ((rc = check_launch("lazy_fill_kernel"))) return rc;
-    launch_pdl(tile_finish_kernel, T, TF_THREADS, sizeof(FinishSmem), (cudaStream_t)stream, *f, early_stop);
+    launch_pdl(tile_finish_kernel, (unsigned)std::min(T, 3 * 148), TF_THREADS, sizeof(FinishSmem), (cudaStream_t)stream, *f,
+               early_stop);
     return check_launch("tile_finish_kernel");
 }
 

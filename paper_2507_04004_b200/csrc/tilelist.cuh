@@ -19,6 +19,8 @@ __device__ __forceinline__ int32_t *ts_huge(const gs_frame &f) { return f.tile_s
 __device__ __forceinline__ int32_t *ts_boff(const gs_frame &f) { return f.tile_scratch + 2 * (f.tiles_x * f.tiles_y + 1); }
 __device__ __forceinline__ int32_t *ts_flag(const gs_frame &f) { return f.tile_scratch + 3 * (f.tiles_x * f.tiles_y + 1); }
 __device__ __forceinline__ int32_t *ts_resume(const gs_frame &f) { return f.tile_scratch + 4 * (f.tiles_x * f.tiles_y + 1); }
+// lazy lists: the ids of the tiles flagged for the continuation (GS_CNT_FLAGGED of them)
+__device__ __forceinline__ int32_t *ts_flagged(const gs_frame &f) { return f.tile_scratch + 5 * (f.tiles_x * f.tiles_y + 1); }
 
 // per-tile list state of lazy binning (ts_flag): the forward blends the leading run of
 // screen-covering Gaussians (those ahead of every bucketed key); a tile whose blend outlives
