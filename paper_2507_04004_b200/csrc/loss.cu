@@ -494,9 +494,10 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
         f.g_depth[p] = xi * (s / so);
         f.g_opac[p] = O >= 1e-6f ? xi * (-s * D / (so * so)) : 0.0f;
     }
-    if (overlap) pdl_wait();
     // this block's share of the SSIM-kernel partials (part0 triples), one per thread: the last
-    // block then sums gridDim.x triples instead of part0 + gridDim.x (one memory round trip)
+    // block then sums gridDim.x triples instead of part0 + gridDim.x (one memory round trip).
+    // They come from ssim_fwd, complete before the SSIM adjoint released this grid, so the
+    // pre-reduction runs before the wait for the adjoint below.
     double l1 = 0.0, ss = 0.0;
     const int64_t per = (part0 + gridDim.x - 1) / gridDim.x;
     for (int64_t i = blockIdx.x * per + threadIdx.x; i < min(part0, (int64_t)(blockIdx.x + 1) * per); i += blockDim.x) {
@@ -515,6 +516,7 @@ __global__ void __launch_bounds__(256) depth_loss_kernel(gs_frame f, const gs_vi
         red[2][threadIdx.x >> 5] = dsum;
     }
     __syncthreads();
+    if (overlap) pdl_wait();  // the adjoint grid is done before this grid completes (render_bwd follows)
     if (threadIdx.x == 0) {
         double a = 0.0, b = 0.0, d = 0.0;
         for (int w = 0; w < 8; w++) {
