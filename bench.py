@@ -398,30 +398,28 @@ def run_render(args, g, kfs, pk, pk_kind, name) -> dict:
         _, cnt = R._bin_frame(g, v, True)
         emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
     ws = R.Workspace(len(g), kfs[0].cam.width, kfs[0].cam.height, int(emax * 1.3) + 4096, g.device)
-    cur = torch.empty_like(views[0].buf)
-
-    def launch():
-        _lib.call("gs_preprocess_ex", ws.fptr, g.data.data_ptr(), cur.data_ptr(), _lib.GS_PP_LAZY_SH, stream_ptr())
+    def launch(view_ptr):
+        _lib.call("gs_preprocess_ex", ws.fptr, g.data.data_ptr(), view_ptr, _lib.GS_PP_LAZY_SH, stream_ptr())
         _lib.call("gs_bin", ws.fptr, _lib.GS_BIN_LAZY, stream_ptr())
         _lib.call("gs_render_fwd", ws.fptr, 1, stream_ptr())
 
-    cur.copy_(views[0].buf)
-    launch()
+    launch(views[0].ptr)
     torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        launch()
+    graphs = []  # one graph per view (each reads its own device gs_view: no per-frame copy)
+    for v in views:
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr):
+            launch(v.ptr)
+        graphs.append(gr)
     for i in range(args.warmup):
-        cur.copy_(views[i % len(views)].buf)
-        graph.replay()
+        graphs[i % len(views)].replay()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(torch.cuda.current_device()) as clk:
         clk.start()
         s.record()
         for i in range(args.steps):
-            cur.copy_(views[i % len(views)].buf)
-            graph.replay()
+            graphs[i % len(views)].replay()
         e.record()
         e.synchronize()
         clk.stop()
