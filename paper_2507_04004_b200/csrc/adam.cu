@@ -548,10 +548,17 @@ __global__ void adam_packed_kernel(float *__restrict__ params, float *__restrict
 }
 
 // the pose gradient from its fixed-point accumulators (gs_chain_pose)
-__global__ void pose_finish_kernel(const int64_t *__restrict__ acc, double *pose) {
+// the pose gradient from its fixed-point accumulators, which are then cleared for the next
+// gs_chain_pose (self-resetting: no memset node in a captured tracking iteration; workspaces
+// start zero-filled)
+__global__ void pose_finish_kernel(int64_t *__restrict__ acc, double *pose) {
     pdl_wait();
     const int q = threadIdx.x;
-    if (q < 6) pose[q] = fx_value(acc[2 * q], acc[2 * q + 1]);
+    if (q < 6) {
+        pose[q] = fx_value(acc[2 * q], acc[2 * q + 1]);
+        acc[2 * q] = 0;
+        acc[2 * q + 1] = 0;
+    }
 }
 
 // step counters advance after the update kernel has read them (no intra-kernel race)
@@ -632,15 +639,11 @@ extern "C" int gs_chain_pose(const gs_frame *f, const float *params, float *grad
         set_error("gs_chain_pose: null argument (grads and touched_accum are both set or both NULL)");
         return GS_ERR_ARG;
     }
-    cudaError_t e = cudaMemsetAsync(f->pose_acc, 0, 12 * sizeof(int64_t), (cudaStream_t)stream);
-    if (e != cudaSuccess) {
-        set_error("gs_chain_pose: %s", cudaGetErrorString(e));
-        return GS_ERR_CUDA;
-    }
+    // (pose_acc is zero here: pose_finish_kernel clears it after every use)
     int rc = launch_chain(f, const_cast<float *>(params), nullptr, nullptr, nullptr, view, nullptr, grads ? 1 : 3,
                           grads, touched_accum, stream, pose);
     if (rc) return rc;
-    launch_pdl(pose_finish_kernel, 1, 32, 0, (cudaStream_t)stream, (const int64_t *)f->pose_acc, pose);
+    launch_pdl(pose_finish_kernel, 1, 32, 0, (cudaStream_t)stream, f->pose_acc, pose);
     return check_launch("pose_finish_kernel");
 }
 
