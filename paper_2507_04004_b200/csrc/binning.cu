@@ -80,8 +80,14 @@ __global__ void __launch_bounds__(256) bucket_count_kernel(gs_frame f) {
 // slot.  CTA c ranks keys [HS_KEYS c, HS_KEYS (c+1)): its HS_GROUPS thread groups each count
 // over one slice of all keys (staged in shared memory), the partial counts are summed in shared
 // memory and every record is written straight to its slot.  No atomics, no global sync.
-constexpr int HS_KEYS = 64;
-constexpr int HS_GROUPS = 16;
+#ifndef HS_KEYS_N
+#define HS_KEYS_N 16
+#endif
+constexpr int HS_KEYS = HS_KEYS_N;
+#ifndef HS_GROUPS_N
+#define HS_GROUPS_N 64
+#endif
+constexpr int HS_GROUPS = HS_GROUPS_N;
 constexpr int HS_THREADS = HS_KEYS * HS_GROUPS;
 
 __global__ void __launch_bounds__(HS_THREADS) huge_sort_kernel(gs_frame f) {
