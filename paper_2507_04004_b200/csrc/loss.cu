@@ -605,7 +605,10 @@ __device__ __forceinline__ void finalize_body(const gs_frame &f, const gs_view *
     }
 }
 
-constexpr int DEPTH_BLOCKS = 64;
+#ifndef DEPTH_BLOCKS_N
+#define DEPTH_BLOCKS_N 148  // one per SM: short gather chains per thread
+#endif
+constexpr int DEPTH_BLOCKS = DEPTH_BLOCKS_N;
 
 // loss_parts holds ssim blocks followed by DEPTH_BLOCKS depth partials; the F tables follow.
 int64_t loss_parts_needed(int32_t width, int32_t height) {
