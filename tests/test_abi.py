@@ -93,3 +93,26 @@ def test_sass_is_sm100a():
     lib = build.build()
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib], capture_output=True, text=True)
     assert "sm_100a" in out.stdout
+
+
+def test_p2p_reduce_rejects_bad_arguments_without_a_device():
+    """gs_p2p_reduce_adam validates its arguments before touching the device (CPU-checkable):
+    world outside 1..8, a rank outside the world, epoch 0 and missing peer pointers are errors."""
+    from paper_2507_04004_b200 import _lib
+    L = _lib.lib()
+    P = ctypes.c_void_p
+    arr = (P * 2)(P(1), P(2))
+    a = ctypes.cast(arr, P)
+    none = (P * 2)(P(1), None)
+    n = ctypes.cast(none, P)
+    x = P(16)  # any non-null stand-in: these calls must fail before using it
+
+    def call(world, rank, epoch, grads=a):
+        return L.gs_p2p_reduce_adam(world, rank, grads, a, a, a, ctypes.c_uint64(epoch), ctypes.c_int64(10), x, x, x,
+                                    x, x, x, x, x, x, None, x, None)
+    assert call(0, 0, 1) == 1        # GS_ERR_ARG: empty world
+    assert call(9, 0, 1) == 1        # more ranks than peers supported
+    assert call(2, 2, 1) == 1        # rank outside the world
+    assert call(2, 0, 0) == 1        # epochs start at 1 (flags start at 0)
+    assert call(2, 0, 1, n) == 1     # a missing peer pointer
+    assert b"gs_p2p_reduce_adam" in L.gs_last_error()
