@@ -51,7 +51,7 @@ extern "C" {
 #define GS_G2D_FIELDS 10
 #define GS_LOSS_RING 64 /* per-iteration losses kept by an engine workspace (gs_frame.loss) */
 #define GS_SPLAT 16    /* floats per 2D splat record: (mx, my, a, beta) (gamma, opacity, depth, qcut)
-                          (r, g, b, 1 - opacity) (b, c, 0, 0); conic = (a, b, c), and the blend evaluates
+                          (r, g, b, 1 - opacity) (b, c, touched slot as int bits, 0); conic = (a, b, c), and the blend evaluates
                           q = a (dx + beta dy)^2 + gamma dy^2 with beta = b / a, gamma = (a c - b^2) / a */
 
 enum {
@@ -122,7 +122,8 @@ typedef struct gs_frame {
     uint8_t *valid;          /* n: near-plane & det test (R/gaussians.py:190-208) */
     uint8_t *touched;        /* n: >= 1 kept pair (R/rasterizer.py:424) */
     int32_t *touched_list;   /* n: compacted touched ids (unordered) */
-    int64_t *g2d;            /* n x GS_G2D screen-space gradients, fixed-point accumulators (touched rows) */
+    int64_t *g2d;            /* n x GS_G2D screen-space gradients, fixed-point accumulators; row k belongs to
+                                touched_list[k] (its slot is also float 14 of its splat record) */
     float *grad_rows;        /* n x GS_ROW parameter gradients in touched-list order */
     float *bias_corr;        /* n x 2 reciprocal Adam bias corrections 1/(1-b1^t), 1/(1-b2^t) (touched-list order) */
     uint64_t *keep_bits;     /* unused (in the rect records) */

@@ -62,7 +62,7 @@ __global__ void nocull_kernel(gs_frame f) {
         bin_rec(f)[i].kept = v ? f.tiles_x * f.tiles_y : 0;
         f.touched[i] = v;
     }
-    warp_append(v, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+    touched_append(f, v, (int32_t)i);
 }
 
 // 1) per-tile bucket counts for cull=False (every tile holds every valid Gaussian); with the

@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
                                  ((unsigned long long)__float_as_uint(pr.mu[2]) << 32) | (uint32_t)i, rect, bits,
                                  f.tiles_x);
         }
-        warp_append(touched, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+        touched_append(f, touched, (int32_t)i);
         warp_append(big, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
         // colour of the previous batch (its SH chunks landed with this batch's geometry)
         if (prev_need) {
@@ -499,7 +499,9 @@ __device__ __forceinline__ int big_publish(const gs_frame &f, int g, int slot, c
                 const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
                 if (h < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] = key;
             }
-            f.touched_list[atomicAdd(&f.counters[GS_CNT_TOUCHED], 1)] = g;
+            const int ts = atomicAdd(&f.counters[GS_CNT_TOUCHED], 1);
+            f.touched_list[ts] = g;
+            splat_set_slot(f.splat2d, g, ts);
         }
     }
     if (t && slot < 0) {  // per-tile bucket counts (bitmap by candidate index)
@@ -669,7 +671,8 @@ __global__ void __launch_bounds__(BC_WARPS * 32, 2) big_bands_kernel(gs_frame f,
                 if (e) atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
                 for (int w = 0; w < BC_WARPS; w++)
                     if (s_kept[w] > 0) {
-                        f.touched_list[tb++] = s_g[w];
+                        f.touched_list[tb] = s_g[w];
+                        splat_set_slot(f.splat2d, s_g[w], tb++);
                         if (s_slot[w] >= 0) {
                             if (hb < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[hb] = big_key(f, s_g[w]);
                             hb++;
@@ -836,7 +839,7 @@ __global__ void touched_list_kernel(gs_frame f) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int k = i < f.n ? bin_rec(f)[i].kept : 0;
     if (k < 0) bin_rec(f)[i].kept = 0;
-    warp_append(k > 0, (int32_t)i, &f.counters[GS_CNT_TOUCHED], f.touched_list);
+    touched_append(f, k > 0, (int32_t)i);
     warp_append(k < 0, (int32_t)i, &f.counters[GS_CNT_BIG], f.big_list);
 }
 

@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(BT, BWD_MINB) render_bwd_kernel(gs_frame f, in
         if ((int)threadIdx.x < nb) {  // (nb <= BST == BT)
             const int i = threadIdx.x;
             const int64_t g = fetch(b0 - start + i);
-            s_g[i] = (int)g;
+            s_g[i] = splat_slot(f.splat2d, g);  // its g2d row
             s_a[i] = __ldg(sp + GS_SPLAT / 4 * g);
             s_b[i] = __ldg(sp + GS_SPLAT / 4 * g + 1);
             s_c[i] = __ldg(sp + GS_SPLAT / 4 * g + 2);
@@ -746,7 +746,7 @@ __global__ void __launch_bounds__(BT, BWD_MINB) render_bwd_kernel(gs_frame f, in
     }
 }
 
-// zero the g2d rows of the touched Gaussians (GS_G2D int64 = GS_G2D / 2 16-B words per row)
+// zero the g2d rows of the touched slots 0..nt-1 (GS_G2D int64 = GS_G2D / 2 16-B words per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
     pdl_wait();
     // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
@@ -755,8 +755,7 @@ __global__ void zero_g2d_kernel(gs_frame f) {
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     constexpr int W = GS_G2D / 2;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < W * nt; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t g = f.touched_list[i / W];
-        reinterpret_cast<longlong2 *>(f.g2d)[g * W + i % W] = make_longlong2(0, 0);
+        reinterpret_cast<longlong2 *>(f.g2d)[i] = make_longlong2(0, 0);  // rows by touched slot
     }
 }
 

@@ -179,8 +179,15 @@ class Workspace:
     @property
     def g2d(self) -> torch.Tensor:
         """(n, 10) float64 screen-space gradient rows (mean2d 2, conic 3, opacity, colour 3, depth)
-        decoded from the fixed-point accumulators: value = hi 2^-24 + lo 2^-64 (gslic.h GS_G2D)."""
-        return g2d_decode(self.g2d_fixed)
+        by Gaussian, decoded from the fixed-point accumulators: value = hi 2^-24 + lo 2^-64
+        (gslic.h GS_G2D).  The device keeps one accumulator row per touched-list slot (the slot is
+        float 14 of the Gaussian's splat record); rows of untouched Gaussians read zero."""
+        n = self.g2d_fixed.shape[0]
+        if n == 0:
+            return g2d_decode(self.g2d_fixed)
+        slot = self.splat2d[:, 14].contiguous().view(torch.int32).long().clamp_(0, n - 1)
+        rows = g2d_decode(self.g2d_fixed.index_select(0, slot))
+        return torch.where(self.touched.bool()[:, None], rows, torch.zeros((), dtype=rows.dtype, device=rows.device))
 
     def view(self, field: str, kind: str, shape) -> torch.Tensor:
         dtype, item = _DT[kind]
