@@ -328,6 +328,20 @@ def test_full_size_properties(n, w, h):
     tiles_x = (cam.width + 15) // 16
     ty, tx = np.mgrid[0:cam.height, 0:cam.width] // 16
     assert np.all(nc <= counts[ty * tiles_x + tx])
+    # g2d rows are indexed by touched slot: slot(touched_list[k]) == k for every k < nt, both for
+    # the reference-shaped path and the engine's (lazy lists, large-footprint publishes)
+    for ws in (out.ctx["workspace"], _lazy_forward(g, cam)):
+        _check_touched_slots(ws)
+
+
+def _check_touched_slots(ws):
+    import torch
+    from paper_2507_04004_b200 import _lib
+    nt = int(ws.counters[_lib.CNT_TOUCHED].item())
+    tl = ws.view("touched_list", "i32", (max(ws.n, 1),))[:nt].long()
+    assert nt > 0 and len(torch.unique(tl)) == nt
+    slot = ws.splat2d[:, 14].contiguous().view(torch.int32).long()
+    assert torch.equal(slot[tl], torch.arange(nt, device=tl.device))
 
 
 def _lazy_forward(g, cam):
