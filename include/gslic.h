@@ -222,7 +222,7 @@ int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int3
 /* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
 int gs_render_bwd(const gs_frame *f, void *stream);
 /* flags = GS_BWD_ROWS_ZERO: the caller guarantees the touched Gaussians' g2d rows are zero (the
- * engine: the chain rule clears every row it consumes), so they are not cleared first. */
+ * engine: with lazy lists gs_render_fwd clears rows 0..nt-1), so they are not cleared first. */
 #define GS_BWD_ROWS_ZERO 1
 /* GS_BWD_CLEAR_DEPTH_GRADS: the backward resets g_depth / g_opac to zero after reading them (the
  * protocol of GS_LOSS_DEPTH_GRADS_ZERO) */

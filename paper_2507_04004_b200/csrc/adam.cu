@@ -240,16 +240,13 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     double pose6[6] = {0, 0, 0, 0, 0, 0};
     if (g >= 0) {
         // the fixed-point screen-space gradient row (GS_G2D_FIELDS (hi, lo) pairs, render.cu)
-        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
+        const longlong2 *g2 = reinterpret_cast<const longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
         double gv[GS_G2D_FIELDS];
 #pragma unroll
         for (int q = 0; q < GS_G2D_FIELDS; q++) {
             const longlong2 w = g2[q];
             gv[q] = fx_value(w.x, w.y);
         }
-        if (mode != 2 && f.counters[GS_CNT_LAZY])  // keep the row zero for the next view
-#pragma unroll
-            for (int q = 0; q < GS_G2D_FIELDS; q++) g2[q] = make_longlong2(0, 0);
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {
@@ -378,10 +375,6 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
         const int c4 = (int)(idx & 15);
         if (c4 == 15) continue;  // columns 60-63: padding
         const int64_t g = f.touched_list[k];
-        // the iteration engine keeps the screen-space gradient rows zero between backwards (the
-        // chain has consumed this one)
-        if (c4 < GS_G2D / 2 && f.counters[GS_CNT_LAZY])
-            reinterpret_cast<longlong2 *>(f.g2d)[k * (GS_G2D / 2) + c4] = make_longlong2(0, 0);
         const float2 bc = reinterpret_cast<const float2 *>(f.bias_corr)[k];
         const float4 G = reinterpret_cast<const float4 *>(f.grad_rows)[k * (GS_ROW / 4) + c4];
         const int64_t off = g * GS_ROW + 4 * c4;

@@ -312,6 +312,15 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
 #endif
 __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, int early_stop) {
     pdl_wait();
+    if (f.counters[GS_CNT_LAZY]) {
+        // the engine's screen-space gradient rows (touched slots 0..nt-1) start each backward at
+        // zero: cleared here, in the slack of an issue-bound kernel, as whole lines that stay in
+        // L2 for the backward's atomics (the chain rule only reads them)
+        const int64_t words = (int64_t)(GS_G2D / 2) * f.counters[GS_CNT_TOUCHED];
+        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d);
+        for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < words; i += (int64_t)gridDim.x * FT)
+            g2[i] = make_longlong2(0, 0);
+    }
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
@@ -749,8 +758,8 @@ __global__ void __launch_bounds__(BT, BWD_MINB) render_bwd_kernel(gs_frame f, in
 // zero the g2d rows of the touched slots 0..nt-1 (GS_G2D int64 = GS_G2D / 2 16-B words per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
     pdl_wait();
-    // the iteration engine (lazy lists) keeps the rows zero instead: the Adam pass (or, for
-    // batches, the chain rule) clears every row it consumes, and the workspace starts zero-filled
+    // with lazy lists the forward has cleared the rows (render_fwd_kernel), and a zero-filled
+    // workspace starts with them zero
     if (f.counters[GS_CNT_LAZY]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     constexpr int W = GS_G2D / 2;

@@ -32,7 +32,7 @@ def kernels_per_iteration(tiles: int, chain_only: bool = False) -> int:
     transpose, tile scan), forward 3 (blend, bucket fill + sorted continuation for the tiles that
     need them), loss 3 (SSIM map + partials, SSIM adjoint + gradient assembly, LiDAR depth with
     the finalisation in its last block; the reflection tables are built once per workspace),
-    backward 1 (the g2d rows are kept zero by the chain rule), chain rule fused with Adam 1 (2
+    backward 1 (the lazy forward clears the g2d rows), chain rule fused with Adam 1 (2
     with GSLIC_SPLIT_ADAM=1: chain + adam_list)."""
     del tiles
     import os
@@ -263,7 +263,7 @@ class MapOptimizer:
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
-        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # the fused chain clears the rows it consumes
+        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_render_fwd cleared the rows (lazy lists)
         self._chain_adam(cur)
 
     def _chain_adam(self, view_ptr: int | None = None) -> None:

@@ -69,7 +69,7 @@ class PoseRefiner:
         # opacity gradient images stay as the table-building gs_loss left them, zero
         call("gs_loss_ex", f, v, 0.5, 0.0, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO, s)
         call("gs_track_grad", f, self.mask.data_ptr(), self.opac_gate, s)
-        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # the pose chain clears the rows it consumes
+        call("gs_render_bwd_ex", f, _lib.GS_BWD_ROWS_ZERO, s)  # gs_render_fwd cleared the rows (lazy lists)
         call("gs_chain_pose", f, self.g.data.data_ptr(), None, None, v, self.pose_grad.data_ptr(), s)
         call("gs_pose_adam", v, self.state.data_ptr(), self.pose_grad.data_ptr(), self.lr, s)
 

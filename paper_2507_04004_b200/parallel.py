@@ -211,7 +211,7 @@ class BatchMapOptimizer:
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         call("gs_render_fwd", f, 1, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS, s)
-        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_chain clears the rows it consumes
+        call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_render_fwd cleared the rows (lazy lists)
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)
         self.loss_acc += self.ws.loss[0:1]
         # an overflowed view contributed nothing: remember it for the batch's check
