@@ -312,15 +312,6 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
 #endif
 __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, int early_stop) {
     pdl_wait();
-    if (f.counters[GS_CNT_LAZY]) {
-        // the engine's screen-space gradient rows (touched slots 0..nt-1) start each backward at
-        // zero: cleared here, in the slack of an issue-bound kernel, as whole lines that stay in
-        // L2 for the backward's atomics (the chain rule only reads them)
-        const int64_t words = (int64_t)(GS_G2D / 2) * f.counters[GS_CNT_TOUCHED];
-        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d);
-        for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < words; i += (int64_t)gridDim.x * FT)
-            g2[i] = make_longlong2(0, 0);
-    }
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
@@ -330,6 +321,16 @@ __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, in
 #pragma unroll
     for (int h = 0; h < NPF; h++) px[h] = fwd_pair_init(f, tile, h);
     auto store = [&]() {
+        if (f.counters[GS_CNT_LAZY]) {
+            // the engine's screen-space gradient rows (touched slots 0..nt-1) start each backward
+            // at zero: cleared here as whole lines once the tile is blended, so the stores overlap
+            // the other CTAs' blending, and the lines stay in L2 for the backward's atomics (the
+            // chain rule only reads them)
+            const int64_t words = (int64_t)(GS_G2D / 2) * f.counters[GS_CNT_TOUCHED];
+            longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d);
+            for (int64_t i = (int64_t)blockIdx.x * FT + threadIdx.x; i < words; i += (int64_t)gridDim.x * FT)
+                g2[i] = make_longlong2(0, 0);
+        }
 #pragma unroll
         for (int h = 0; h < NPF; h++) fwd_pair_store(f, tile, h, px[h]);
     };
