@@ -472,13 +472,12 @@ __device__ __forceinline__ uint64_t big_key(const gs_frame &f, int g) {
 }
 
 // Publishes one large-footprint Gaussian once its bitmap is complete (the whole warp calls it
-// with the same arguments; `bits` = its bitmap, shared or global): kept count, touched, the
-// non-huge kept tiles into the binning's bucket counts and, with `lists`, the huge key staging
-// and the touched-list entry (big_bands_kernel aggregates those per CTA instead).  Returns the
-// kept count.
+// with the same arguments; `bits` = its bitmap, shared or global): kept count, touched and the
+// non-huge kept tiles into the binning's bucket counts.  The touched-list entry and the huge key
+// staging are reserved per CTA by the callers.  Returns the kept count.
 template <bool GLOBAL>
 __device__ __forceinline__ int big_publish(const gs_frame &f, int g, int slot, const uint32_t *bits, int nwords,
-                                           int4 r, bool lists) {
+                                           int4 r) {
     const int lane = threadIdx.x & 31;
     // rows in global memory were completed by other SMs' atomics: read them at L2
     auto word = [&](int w) -> uint32_t { return GLOBAL ? __ldcg(bits + w) : bits[w]; };
@@ -491,18 +490,6 @@ __device__ __forceinline__ int big_publish(const gs_frame &f, int g, int slot, c
     if (lane == 0) {
         bin_rec(f)[g].kept = (slot >= 0 && t) ? -(1 + slot) : kept;  // kept < 0 encodes the huge slot
         f.touched[g] = t;
-        if (t && lists) {
-            // kept screen-covering Gaussians: entry count and a staging slot for the binning's
-            // huge sort (binning.cu, HKEYS; the sort is by key, so the staging order is free)
-            if (slot >= 0) {
-                atomicAdd(&f.counters[GS_CNT_HUGE_E], kept);
-                const int h = atomicAdd(&f.counters[GS_CNT_HUGE_N], 1);
-                if (h < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] = key;
-            }
-            const int ts = atomicAdd(&f.counters[GS_CNT_TOUCHED], 1);
-            f.touched_list[ts] = g;
-            splat_set_slot(f.splat2d, g, ts);
-        }
     }
     if (t && slot < 0) {  // per-tile bucket counts (bitmap by candidate index)
         const int nx = r.y - r.x + 1, ncand = nx * (r.w - r.z + 1);
@@ -646,7 +633,7 @@ __global__ void __launch_bounds__(BC_WARPS * 32, 2) big_bands_kernel(gs_frame f,
                 if (queued) bin_rec(f)[g].kept = queued;  // countdown of big_exact_kernel
             }
             if (!queued) {
-                const int kept = big_publish<false>(f, g, slot, bm, nwords, r, false);
+                const int kept = big_publish<false>(f, g, slot, bm, nwords, r);
                 if (lane == 0) {
                     s_g[warp] = g;
                     s_kept[warp] = kept;
@@ -691,7 +678,13 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
     const int2 *queue = reinterpret_cast<const int2 *>(f.cull_queue);
     const int tw = (f.tiles_x * f.tiles_y + 31) >> 5;
     const int lane = threadIdx.x & 31;
+    // the Gaussians this CTA publishes in a round: their touched-list / huge-list reservations are
+    // made once per CTA (same-address counter atomics from every publishing warp serialise in L2)
+    __shared__ int s_np, s_tb, s_hb;
+    __shared__ int s_pg[256], s_pk[256], s_ps[256];
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nq; i0 += (int64_t)gridDim.x * blockDim.x) {
+        if (threadIdx.x == 0) s_np = 0;
+        __syncthreads();
         const int64_t i = i0 + threadIdx.x;  // uniform trip count: the exact test is warp-wide
         int cls = 0, g = 0, b = 0, slot = -1;
         uint32_t *row = nullptr;
@@ -738,8 +731,43 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
                                       __shfl_sync(0xffffffffu, r.z, l), __shfl_sync(0xffffffffu, r.w, l));
             const uint32_t *rowl = reinterpret_cast<const uint32_t *>(__shfl_sync(0xffffffffu, (unsigned long long)row, l));
             const int nwords = sl >= 0 ? tw : ((rl.y - rl.x + 1) * (rl.w - rl.z + 1) + 31) >> 5;
-            big_publish<true>(f, gl, sl, rowl, nwords, rl, true);
+            const int kept = big_publish<true>(f, gl, sl, rowl, nwords, rl);
+            if (lane == 0 && kept > 0) {
+                const int p = atomicAdd(&s_np, 1);  // (<= 256: one per retired queue entry)
+                s_pg[p] = gl;
+                s_pk[p] = kept;
+                s_ps[p] = sl;
+            }
         }
+        __syncthreads();
+        const int np = s_np;
+        if (np > 0) {
+            if (threadIdx.x == 0) {
+                int nh = 0, e = 0;
+                for (int p = 0; p < np; p++)
+                    if (s_ps[p] >= 0) {
+                        nh++;
+                        e += s_pk[p];
+                    }
+                s_tb = atomicAdd(&f.counters[GS_CNT_TOUCHED], np);
+                int hb = nh ? atomicAdd(&f.counters[GS_CNT_HUGE_N], nh) : 0;
+                if (e) atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
+                // kept screen-covering Gaussians: a staging slot each for the binning's huge sort
+                // (binning.cu, HKEYS; the sort is by key, so the staging order is free)
+                for (int p = 0; p < np; p++)
+                    if (s_ps[p] >= 0) {
+                        if (hb < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[hb] = big_key(f, s_pg[p]);
+                        hb++;
+                    }
+            }
+            __syncthreads();
+            if ((int)threadIdx.x < np) {
+                const int g = s_pg[threadIdx.x], ts = s_tb + (int)threadIdx.x;
+                f.touched_list[ts] = g;
+                splat_set_slot(f.splat2d, g, ts);
+            }
+        }
+        __syncthreads();  // s_np and the records are free for the next round
     }
 }
 
