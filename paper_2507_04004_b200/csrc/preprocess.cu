@@ -17,6 +17,11 @@ constexpr int PP_THREADS = PP_WARPS * 32;
 #define PP_CTAS 5
 #endif
 constexpr int PP_CTAS_PER_SM = PP_CTAS;  // persistent grid: shared memory allows five
+#ifndef PP_EVICT_FRAC
+#define PP_EVICT_FRAC 1.0  // fraction of the drawable rows' SH lines marked evict-last
+#endif
+#define PP_STR2(x) #x
+#define PP_STR(x) PP_STR2(x)
 
 __device__ __forceinline__ void pp_cp_async16(void *smem, const void *gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -286,7 +291,7 @@ __global__ void __launch_bounds__(PP_THREADS, PP_CTAS_PER_SM) preprocess_kernel(
                 // chain rule + Adam re-read at the end of the iteration: their lines are marked
                 // evict-last, so more of them are still in L2 then (chain DRAM reads -4 %)
                 uint64_t pol;
-                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+                asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, " PP_STR(PP_EVICT_FRAC) ";" : "=l"(pol));
 #pragma unroll
                 for (int c = 0; c < 11; c++)
                     asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
