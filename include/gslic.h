@@ -204,6 +204,13 @@ int gs_bin(const gs_frame *f, int32_t cull, void *stream);
 
 /* R/rasterizer.py:226-293 */
 int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream);
+/* flags: GS_FWD_EARLY_STOP (the reference's early termination, as gs_render_fwd's early_stop);
+ * GS_FWD_CLEAR_G2D: the forward also clears the g2d rows of the touched slots 0..nt-1 (in its
+ * epilogue, as whole lines that stay in L2), so a following gs_render_bwd_ex(.., GS_BWD_ROWS_ZERO)
+ * starts from zero -- the iteration engines' form (a render-only caller leaves it off). */
+#define GS_FWD_EARLY_STOP 1
+#define GS_FWD_CLEAR_G2D 2
+int gs_render_fwd_ex(const gs_frame *f, int32_t flags, void *stream);
 
 /* R/losses.py:157-161 with the depth term on the view's LiDAR K-list; writes g_color,
  * g_depth, g_opac and loss[0..3]. */
@@ -222,7 +229,8 @@ int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int3
 /* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
 int gs_render_bwd(const gs_frame *f, void *stream);
 /* flags = GS_BWD_ROWS_ZERO: the caller guarantees the touched Gaussians' g2d rows are zero (the
- * engine: with lazy lists gs_render_fwd clears rows 0..nt-1), so they are not cleared first. */
+ * engines: gs_render_fwd_ex(.., GS_FWD_CLEAR_G2D) cleared rows 0..nt-1), so they are not cleared
+ * first. */
 #define GS_BWD_ROWS_ZERO 1
 /* GS_BWD_CLEAR_DEPTH_GRADS: the backward resets g_depth / g_opac to zero after reading them (the
  * protocol of GS_LOSS_DEPTH_GRADS_ZERO) */

@@ -28,6 +28,7 @@ GS_BIN_LAZY = 2  # gs_bin cull mode of the iteration engine (tile lists material
 GS_PP_LAZY_SH = 1  # gs_preprocess_ex flag of the iteration engine (colours only where blended)
 GS_LOSS_TABLES_READY, GS_LOSS_ACCUMULATE, GS_LOSS_DEPTH_GRADS_ZERO = 1, 2, 4  # gs_loss_ex flags
 GS_BWD_ROWS_ZERO, GS_BWD_CLEAR_DEPTH_GRADS = 1, 2  # gs_render_bwd_ex flags
+GS_FWD_EARLY_STOP, GS_FWD_CLEAR_G2D = 1, 2  # gs_render_fwd_ex flags
 
 # Set by dropin.install: the reference-shaped entry points then return numpy arrays for every
 # map (the reference's callers do numpy arithmetic on them, R/cli.py:153-159, R/apps.py:208-223),
@@ -87,6 +88,7 @@ def lib():
         "gs_preprocess_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, P, i32, P]),
         "gs_bin": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_render_fwd": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
+        "gs_render_fwd_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
         "gs_loss": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, P]),
         "gs_loss_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), P, f32, f32, i32, P]),
         "gs_render_bwd_ex": (ctypes.c_int, [ctypes.POINTER(GsFrame), i32, P]),
@@ -125,7 +127,7 @@ def lib():
 
 
 EXPORTED = ["gs_workspace_size", "gs_frame_layout", "gs_camera_init", "gs_last_error", "gs_version",
-            "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
+            "gs_preprocess", "gs_preprocess_ex", "gs_bin", "gs_render_fwd", "gs_render_fwd_ex", "gs_loss", "gs_loss_ex", "gs_render_bwd", "gs_render_bwd_ex", "gs_chain_adam",
             "gs_chain_adam_part", "gs_chain", "gs_chain_pose", "gs_adam", "gs_lidar_compact", "gs_project", "gs_eval_sh", "gs_pack_splats",
             "gs_project_points", "gs_zbuffer", "gs_init_rows", "gs_decode_u8", "gs_track_mask", "gs_track_grad", "gs_pose_adam",
             "gs_compact_flags", "gs_gather_rows", "gs_adam_packed", "gs_p2p_reduce_adam", "gs_ipc_export",

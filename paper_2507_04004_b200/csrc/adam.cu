@@ -240,13 +240,18 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     double pose6[6] = {0, 0, 0, 0, 0, 0};
     if (g >= 0) {
         // the fixed-point screen-space gradient row (GS_G2D_FIELDS (hi, lo) pairs, render.cu)
-        const longlong2 *g2 = reinterpret_cast<const longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
+        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
         double gv[GS_G2D_FIELDS];
 #pragma unroll
         for (int q = 0; q < GS_G2D_FIELDS; q++) {
             const longlong2 w = g2[q];
             gv[q] = fx_value(w.x, w.y);
         }
+#ifdef GS_CHAIN_CLEARS_G2D  // (A/B build: the round-2 scheme before the forward took the clear over)
+        if (mode != 2 && f.counters[GS_CNT_LAZY])
+#pragma unroll
+            for (int q = 0; q < GS_G2D_FIELDS; q++) g2[q] = make_longlong2(0, 0);
+#endif
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {

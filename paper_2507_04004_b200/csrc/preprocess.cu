@@ -685,7 +685,7 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
     const int lane = threadIdx.x & 31;
     // the Gaussians this CTA publishes in a round: their touched-list / huge-list reservations are
     // made once per CTA (same-address counter atomics from every publishing warp serialise in L2)
-    __shared__ int s_np, s_tb, s_hb;
+    __shared__ int s_np, s_tb, s_hb, s_wh[8], s_we[8];
     __shared__ int s_pg[256], s_pk[256], s_ps[256];
     for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < nq; i0 += (int64_t)gridDim.x * blockDim.x) {
         if (threadIdx.x == 0) s_np = 0;
@@ -746,30 +746,41 @@ __global__ void __launch_bounds__(256) big_exact_kernel(gs_frame f) {
         }
         __syncthreads();
         const int np = s_np;
-        if (np > 0) {
-            if (threadIdx.x == 0) {
-                int nh = 0, e = 0;
-                for (int p = 0; p < np; p++)
-                    if (s_ps[p] >= 0) {
-                        nh++;
-                        e += s_pk[p];
-                    }
-                s_tb = atomicAdd(&f.counters[GS_CNT_TOUCHED], np);
-                int hb = nh ? atomicAdd(&f.counters[GS_CNT_HUGE_N], nh) : 0;
-                if (e) atomicAdd(&f.counters[GS_CNT_HUGE_E], e);
-                // kept screen-covering Gaussians: a staging slot each for the binning's huge sort
-                // (binning.cu, HKEYS; the sort is by key, so the staging order is free)
-                for (int p = 0; p < np; p++)
-                    if (s_ps[p] >= 0) {
-                        if (hb < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[hb] = big_key(f, s_pg[p]);
-                        hb++;
-                    }
+        if (np > 0) {  // (CTA-uniform) record p is thread p's
+            const int p = threadIdx.x, warp = threadIdx.x >> 5;
+            const bool hug = p < np && s_ps[p] >= 0;
+            const unsigned hm = __ballot_sync(0xffffffffu, hug);
+            int e = hug ? s_pk[p] : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+            if (lane == 0) {
+                s_wh[warp] = __popc(hm);
+                s_we[warp] = e;
             }
             __syncthreads();
-            if ((int)threadIdx.x < np) {
-                const int g = s_pg[threadIdx.x], ts = s_tb + (int)threadIdx.x;
+            if (threadIdx.x == 0) {
+                int nh = 0, et = 0;
+                for (int w = 0; w < 8; w++) {  // exclusive prefix of the warps' huge counts, in place
+                    const int c = s_wh[w];
+                    s_wh[w] = nh;
+                    nh += c;
+                    et += s_we[w];
+                }
+                s_tb = atomicAdd(&f.counters[GS_CNT_TOUCHED], np);
+                s_hb = nh ? atomicAdd(&f.counters[GS_CNT_HUGE_N], nh) : 0;
+                if (et) atomicAdd(&f.counters[GS_CNT_HUGE_E], et);
+            }
+            __syncthreads();
+            if (p < np) {
+                const int g = s_pg[p], ts = s_tb + p;
                 f.touched_list[ts] = g;
                 splat_set_slot(f.splat2d, g, ts);
+                // kept screen-covering Gaussians: a staging slot each for the binning's huge sort
+                // (binning.cu, HKEYS; the sort is by key, so the staging order is free)
+                if (hug) {
+                    const int h = s_hb + s_wh[warp] + __popc(hm & ((1u << lane) - 1u));
+                    if (h < GS_HUGE_CAP) reinterpret_cast<uint64_t *>(f.huge + HSTAGE)[h] = big_key(f, g);
+                }
             }
         }
         __syncthreads();  // s_np and the records are free for the next round

@@ -310,8 +310,9 @@ __device__ __forceinline__ bool blend_range(const gs_frame &f, FwdPixel &px, Fwd
 #ifndef FWD_MINB
 #define FWD_MINB 16  // 64 registers: 16 CTAs (32 warps) per SM
 #endif
-__global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, int early_stop) {
+__global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, int flags) {
     pdl_wait();
+    const int early_stop = flags & GS_FWD_EARLY_STOP;
     __shared__ FwdStage st;
     __shared__ uint32_t s_words[GS_HUGE_CAP / 32];
     __shared__ int32_t s_wpre[GS_HUGE_CAP / 32];
@@ -321,8 +322,12 @@ __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, in
 #pragma unroll
     for (int h = 0; h < NPF; h++) px[h] = fwd_pair_init(f, tile, h);
     auto store = [&]() {
-        if (f.counters[GS_CNT_LAZY]) {
-            // the engine's screen-space gradient rows (touched slots 0..nt-1) start each backward
+#ifndef GS_CHAIN_CLEARS_G2D
+        if (flags & GS_FWD_CLEAR_G2D) {
+#else
+        if (false) {
+#endif
+            // the engines' screen-space gradient rows (touched slots 0..nt-1) start each backward
             // at zero: cleared here as whole lines once the tile is blended, so the stores overlap
             // the other CTAs' blending, and the lines stay in L2 for the backward's atomics (the
             // chain rule only reads them)
@@ -759,9 +764,6 @@ __global__ void __launch_bounds__(BT, BWD_MINB) render_bwd_kernel(gs_frame f, in
 // zero the g2d rows of the touched slots 0..nt-1 (GS_G2D int64 = GS_G2D / 2 16-B words per row)
 __global__ void zero_g2d_kernel(gs_frame f) {
     pdl_wait();
-    // with lazy lists the forward has cleared the rows (render_fwd_kernel), and a zero-filled
-    // workspace starts with them zero
-    if (f.counters[GS_CNT_LAZY]) return;
     const int64_t nt = f.counters[GS_CNT_TOUCHED];
     constexpr int W = GS_G2D / 2;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < W * nt; i += (int64_t)gridDim.x * blockDim.x) {
@@ -774,9 +776,18 @@ __global__ void zero_g2d_kernel(gs_frame f) {
 using namespace gs;
 
 extern "C" int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream) {
+    return gs_render_fwd_ex(f, early_stop ? GS_FWD_EARLY_STOP : 0, stream);
+}
+
+extern "C" int gs_render_fwd_ex(const gs_frame *f, int32_t flags, void *stream) {
+    if (flags & ~(GS_FWD_EARLY_STOP | GS_FWD_CLEAR_G2D)) {
+        set_error("gs_render_fwd_ex: unknown flags");
+        return GS_ERR_ARG;
+    }
+    const int early_stop = flags & GS_FWD_EARLY_STOP;
     const int T = f->tiles_x * f->tiles_y;
     if (T == 0) return GS_OK;
-    launch_pdl(render_fwd_kernel, T, FT, 0, (cudaStream_t)stream, *f, early_stop);
+    launch_pdl(render_fwd_kernel, T, FT, 0, (cudaStream_t)stream, *f, (int)flags);
     int rc = check_launch("render_fwd_kernel");
     if (rc) return rc;
     // lazy lists: bucket fill + sorted continuation of the tiles that need them (no-ops otherwise)

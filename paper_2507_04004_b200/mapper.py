@@ -19,7 +19,7 @@ from . import _lib
 from ._lib import call
 from .errors import DataError
 from .gaussians import GaussianMap, as_device_map, default_device, init_from_points, stream_ptr, struct_to_device
-from .rasterizer import (BWD_FLAGS, LOSS_FLAGS, AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from,
+from .rasterizer import (BWD_FLAGS, FWD_FLAGS, LOSS_FLAGS, AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from,
                          default_lrs, forward, prime_workspace,
                          lr_columns)
 
@@ -261,7 +261,7 @@ class MapOptimizer:
         cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
-        call("gs_render_fwd", f, 1, s)
+        call("gs_render_fwd_ex", f, FWD_FLAGS, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
         call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_render_fwd cleared the rows (lazy lists)
         self._chain_adam(cur)
@@ -400,7 +400,7 @@ class MapOptimizer:
         ev[1].record()
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         ev[2].record()
-        call("gs_render_fwd", f, 1, s)
+        call("gs_render_fwd_ex", f, FWD_FLAGS, s)
         ev[3].record()
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
         ev[4].record()

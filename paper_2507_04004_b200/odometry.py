@@ -64,7 +64,7 @@ class PoseRefiner:
         f, s, v = self.ws.fptr, stream_ptr(), self.view.ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), v, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
-        call("gs_render_fwd", f, 1, s)
+        call("gs_render_fwd_ex", f, _lib.GS_FWD_EARLY_STOP | _lib.GS_FWD_CLEAR_G2D, s)
         # R/odometry.py:323: photometric_loss(lam=0.5).  No LiDAR term (lidar_k = 0): the depth /
         # opacity gradient images stay as the table-building gs_loss left them, zero
         call("gs_loss_ex", f, v, 0.5, 0.0, _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO, s)

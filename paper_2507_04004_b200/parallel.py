@@ -24,7 +24,7 @@ from . import _lib
 from ._lib import GS_ROW, call
 from .errors import DataError
 from .gaussians import as_device_map, stream_ptr
-from .rasterizer import (BWD_FLAGS, LOSS_FLAGS, AdamState, DeviceView, Workspace, _bin_frame, camera_from, lr_columns,
+from .rasterizer import (BWD_FLAGS, FWD_FLAGS, LOSS_FLAGS, AdamState, DeviceView, Workspace, _bin_frame, camera_from, lr_columns,
                          prime_workspace)
 
 TOUCH_COL = GS_ROW - 1  # padding column carrying the touched flag through the allreduce
@@ -209,7 +209,7 @@ class BatchMapOptimizer:
         cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
-        call("gs_render_fwd", f, 1, s)
+        call("gs_render_fwd_ex", f, FWD_FLAGS, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS, s)
         call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_render_fwd cleared the rows (lazy lists)
         call("gs_chain", f, self.g.data.data_ptr(), self.grads.data_ptr(), self.touched.data_ptr(), cur, s)

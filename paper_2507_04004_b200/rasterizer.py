@@ -225,6 +225,8 @@ def _remember_capacity(n, w, h, cull, entries):
 # iterations -- the loss writes only the LiDAR pixels and the backward clears them.
 LOSS_FLAGS = _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO
 BWD_FLAGS = _lib.GS_BWD_ROWS_ZERO | _lib.GS_BWD_CLEAR_DEPTH_GRADS
+# the engines' forward: early termination, and the g2d rows cleared for the ROWS_ZERO backward
+FWD_FLAGS = _lib.GS_FWD_EARLY_STOP | _lib.GS_FWD_CLEAR_G2D
 
 
 def prime_workspace(ws: Workspace, view_ptr: int, lam: float, xi: float) -> None:
