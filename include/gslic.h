@@ -82,7 +82,9 @@ enum {
     GS_CNT_CULLQ1 = 20,  /* tiles left ambiguous by the band bounds of large footprints (cull_queue) */
     GS_CNT_LAZY = 21,    /* 1: gs_bin(GS_BIN_LAZY) left the tile lists unmaterialised */
     GS_CNT_ANYFLAG = 22, /* lazy lists: some tile needs its bucket (blend continuation) */
-    GS_CNT_FLAGGED = 23  /* lazy lists: how many (their ids in a tile_scratch segment) */
+    GS_CNT_FLAGGED = 23, /* lazy lists: how many (their ids in a tile_scratch segment) */
+    GS_CNT_FWD_CLEARED = 24 /* 1: the frame's forward cleared the g2d rows (GS_FWD_CLEAR_G2D); 0: with
+                               lazy lists the chain rule clears each row after reading it */
 };
 
 #define GS_HUGE_CAND 256 /* candidate tiles above which a Gaussian is binned per tile */
@@ -207,7 +209,9 @@ int gs_render_fwd(const gs_frame *f, int32_t early_stop, void *stream);
 /* flags: GS_FWD_EARLY_STOP (the reference's early termination, as gs_render_fwd's early_stop);
  * GS_FWD_CLEAR_G2D: the forward also clears the g2d rows of the touched slots 0..nt-1 (in its
  * epilogue, as whole lines that stay in L2), so a following gs_render_bwd_ex(.., GS_BWD_ROWS_ZERO)
- * starts from zero -- the iteration engines' form (a render-only caller leaves it off). */
+ * starts from zero, and the chain rule only reads them.  Without it (and with lazy lists) the
+ * chain rule clears each row after reading it instead.  An engine keeps one choice for all its
+ * iterations: the forward's clear pays at ~100k+ touched Gaussians, the chain's below. */
 #define GS_FWD_EARLY_STOP 1
 #define GS_FWD_CLEAR_G2D 2
 int gs_render_fwd_ex(const gs_frame *f, int32_t flags, void *stream);
@@ -229,8 +233,8 @@ int gs_loss_ex(const gs_frame *f, const gs_view *view, float lam, float xi, int3
 /* R/rasterizer.py:296-435: accumulates g2d rows of touched Gaussians. */
 int gs_render_bwd(const gs_frame *f, void *stream);
 /* flags = GS_BWD_ROWS_ZERO: the caller guarantees the touched Gaussians' g2d rows are zero (the
- * engines: gs_render_fwd_ex(.., GS_FWD_CLEAR_G2D) cleared rows 0..nt-1), so they are not cleared
- * first. */
+ * engines: gs_render_fwd_ex(.., GS_FWD_CLEAR_G2D) cleared rows 0..nt-1, or the previous chain rule
+ * cleared the rows it read), so they are not cleared first. */
 #define GS_BWD_ROWS_ZERO 1
 /* GS_BWD_CLEAR_DEPTH_GRADS: the backward resets g_depth / g_opac to zero after reading them (the
  * protocol of GS_LOSS_DEPTH_GRADS_ZERO) */

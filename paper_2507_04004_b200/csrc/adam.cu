@@ -247,11 +247,11 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
             const longlong2 w = g2[q];
             gv[q] = fx_value(w.x, w.y);
         }
-#ifdef GS_CHAIN_CLEARS_G2D  // (A/B build: the round-2 scheme before the forward took the clear over)
-        if (mode != 2 && f.counters[GS_CNT_LAZY])
+        // without the forward's clear (GS_FWD_CLEAR_G2D) the engine keeps the row zero for the
+        // next view by clearing it here
+        if (mode != 2 && f.counters[GS_CNT_LAZY] && !f.counters[GS_CNT_FWD_CLEARED])
 #pragma unroll
             for (int q = 0; q < GS_G2D_FIELDS; q++) g2[q] = make_longlong2(0, 0);
-#endif
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {
@@ -380,6 +380,8 @@ __global__ void __launch_bounds__(256) adam_list_kernel(gs_frame f, float *__res
         const int c4 = (int)(idx & 15);
         if (c4 == 15) continue;  // columns 60-63: padding
         const int64_t g = f.touched_list[k];
+        if (c4 < GS_G2D / 2 && f.counters[GS_CNT_LAZY] && !f.counters[GS_CNT_FWD_CLEARED])
+            reinterpret_cast<longlong2 *>(f.g2d)[k * (GS_G2D / 2) + c4] = make_longlong2(0, 0);
         const float2 bc = reinterpret_cast<const float2 *>(f.bias_corr)[k];
         const float4 G = reinterpret_cast<const float4 *>(f.grad_rows)[k * (GS_ROW / 4) + c4];
         const int64_t off = g * GS_ROW + 4 * c4;

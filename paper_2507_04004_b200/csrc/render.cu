@@ -321,12 +321,9 @@ __global__ void __launch_bounds__(FT, FWD_MINB) render_fwd_kernel(gs_frame f, in
     FwdPair px[NPF];
 #pragma unroll
     for (int h = 0; h < NPF; h++) px[h] = fwd_pair_init(f, tile, h);
+    if (blockIdx.x == 0 && threadIdx.x == 0) f.counters[GS_CNT_FWD_CLEARED] = (flags & GS_FWD_CLEAR_G2D) ? 1 : 0;
     auto store = [&]() {
-#ifndef GS_CHAIN_CLEARS_G2D
         if (flags & GS_FWD_CLEAR_G2D) {
-#else
-        if (false) {
-#endif
             // the engines' screen-space gradient rows (touched slots 0..nt-1) start each backward
             // at zero: cleared here as whole lines once the tile is blended, so the stores overlap
             // the other CTAs' blending, and the lines stay in L2 for the backward's atomics (the

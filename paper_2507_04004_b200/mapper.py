@@ -19,8 +19,8 @@ from . import _lib
 from ._lib import call
 from .errors import DataError
 from .gaussians import GaussianMap, as_device_map, default_device, init_from_points, stream_ptr, struct_to_device
-from .rasterizer import (BWD_FLAGS, FWD_FLAGS, LOSS_FLAGS, AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from,
-                         default_lrs, forward, prime_workspace,
+from .rasterizer import (BWD_FLAGS, LOSS_FLAGS, AdamState, Camera, DeviceView, Workspace, _bin_frame, camera_from,
+                         default_lrs, engine_fwd_flags, forward, prime_workspace,
                          lr_columns)
 
 NEAR_CLIP = 0.01
@@ -227,10 +227,12 @@ class MapOptimizer:
         self.lr = lr_columns(lrs, self.dev)
         self.cur = torch.empty_like(self.views[0].buf)
         # entry capacity from a dry binning pass over every keyframe
-        emax = 1
+        emax, tmax = 1, 1
         for v in self.views:
             _, cnt = _bin_frame(self.g, v, True)
             emax = max(emax, int(cnt[_lib.CNT_ENTRIES]))
+            tmax = max(tmax, int(cnt[_lib.CNT_TOUCHED]))
+        self.fwd_flags = engine_fwd_flags(tmax)
         self.headroom = headroom
         self.ws = self._workspace(int(emax * headroom) + 4096)
         self.graph = None
@@ -261,7 +263,7 @@ class MapOptimizer:
         cur = self.cur.data_ptr() if view_ptr is None else view_ptr
         call("gs_preprocess_ex", f, self.g.data.data_ptr(), cur, _lib.GS_PP_LAZY_SH, s)
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
-        call("gs_render_fwd_ex", f, FWD_FLAGS, s)
+        call("gs_render_fwd_ex", f, self.fwd_flags, s)
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
         call("gs_render_bwd_ex", f, BWD_FLAGS, s)  # gs_render_fwd cleared the rows (lazy lists)
         self._chain_adam(cur)
@@ -400,7 +402,7 @@ class MapOptimizer:
         ev[1].record()
         call("gs_bin", f, _lib.GS_BIN_LAZY, s)
         ev[2].record()
-        call("gs_render_fwd_ex", f, FWD_FLAGS, s)
+        call("gs_render_fwd_ex", f, self.fwd_flags, s)
         ev[3].record()
         call("gs_loss_ex", f, cur, self.lam, self.xi, LOSS_FLAGS | _lib.GS_LOSS_ACCUMULATE, s)
         ev[4].record()

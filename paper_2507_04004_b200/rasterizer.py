@@ -226,7 +226,14 @@ def _remember_capacity(n, w, h, cull, entries):
 LOSS_FLAGS = _lib.GS_LOSS_TABLES_READY | _lib.GS_LOSS_DEPTH_GRADS_ZERO
 BWD_FLAGS = _lib.GS_BWD_ROWS_ZERO | _lib.GS_BWD_CLEAR_DEPTH_GRADS
 # the engines' forward: early termination, and the g2d rows cleared for the ROWS_ZERO backward
+# (from this many touched Gaussians on; below it the chain rule clears the rows it reads)
 FWD_FLAGS = _lib.GS_FWD_EARLY_STOP | _lib.GS_FWD_CLEAR_G2D
+FWD_CLEAR_MIN_TOUCHED = 65536
+
+
+def engine_fwd_flags(max_touched: int) -> int:
+    """The forward flags an iteration engine keeps for all its iterations (gslic.h GS_FWD_CLEAR_G2D)."""
+    return FWD_FLAGS if max_touched >= FWD_CLEAR_MIN_TOUCHED else _lib.GS_FWD_EARLY_STOP
 
 
 def prime_workspace(ws: Workspace, view_ptr: int, lam: float, xi: float) -> None:
