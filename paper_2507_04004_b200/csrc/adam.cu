@@ -214,6 +214,9 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     __syncthreads();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t ntt = f.counters[GS_CNT_OVERFLOW] ? 0 : f.counters[GS_CNT_TOUCHED];
+    // without the forward's clear (GS_FWD_CLEAR_G2D) the engine keeps each row zero for the next
+    // view by clearing it once read
+    const bool clear_rows = mode != 2 && f.counters[GS_CNT_LAZY] && !f.counters[GS_CNT_FWD_CLEARED];
     // touched-list chunk `part` of `nparts` (warp-aligned bounds)
     // (no 64-bit divide -- a long subroutine -- on the common single-chunk path)
     const int64_t kb = nparts == 1 ? 0 : (ntt * part / nparts) & ~(int64_t)31;
@@ -240,18 +243,16 @@ __global__ void __launch_bounds__(CA_THREADS, CA_MINB) chain_kernel(gs_frame f, 
     double pose6[6] = {0, 0, 0, 0, 0, 0};
     if (g >= 0) {
         // the fixed-point screen-space gradient row (GS_G2D_FIELDS (hi, lo) pairs, render.cu)
-        longlong2 *g2 = reinterpret_cast<longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
+        const longlong2 *g2 = reinterpret_cast<const longlong2 *>(f.g2d) + k * (GS_G2D / 2);  // row = touched slot
         double gv[GS_G2D_FIELDS];
 #pragma unroll
         for (int q = 0; q < GS_G2D_FIELDS; q++) {
             const longlong2 w = g2[q];
             gv[q] = fx_value(w.x, w.y);
         }
-        // without the forward's clear (GS_FWD_CLEAR_G2D) the engine keeps the row zero for the
-        // next view by clearing it here
-        if (mode != 2 && f.counters[GS_CNT_LAZY] && !f.counters[GS_CNT_FWD_CLEARED])
+        if (clear_rows)
 #pragma unroll
-            for (int q = 0; q < GS_G2D_FIELDS; q++) g2[q] = make_longlong2(0, 0);
+            for (int q = 0; q < GS_G2D_FIELDS; q++) const_cast<longlong2 *>(g2)[q] = make_longlong2(0, 0);
         chain_row<POSE>(srow[warp][lane], gv, scam, sgr[warp][lane], pose6);
         for (int q = GS_NPARAM; q < RP; q++) sgr[warp][lane][q] = 0.0f;
         if (mode == 0 || mode == 2) {
